@@ -1,0 +1,126 @@
+/* spamm_b200.h -- C ABI of the B200-native SpAMM / SP2 hot path.
+ *
+ * Drop-in boundary.  The reference (Python package `spamm` 0.1.0,
+ * /root/reference/pkg/src/spamm) has no FFI; its hot path sits behind the
+ * public Python API and one compiled seam (the numba `_gemm_batch`).  Every
+ * entry point below replaces one of those call sites (file:line cited); the
+ * Python host layer `paper_1403_7458_b200` binds them with ctypes and keeps
+ * the reference's names, signatures and error behaviour (ValueError ->
+ * status SPAMM_EINVAL).  INTEGRATION.md shows the binding.
+ *
+ * Conventions
+ *  - int status return: 0 ok, SPAMM_EINVAL bad argument, SPAMM_ECUDA CUDA
+ *    failure; spamm_last_error() gives the message (thread-local).
+ *  - `stream` is a cudaStream_t passed as void* (0 = legacy default stream).
+ *    Calls are stream-ordered; those returning host scalars synchronise.
+ *  - Matrices are opaque device-resident handles (spamm_mat) owning their
+ *    memory (stream-ordered cudaMallocAsync pool); free with spamm_mat_free.
+ *  - Device arrays passed in are plain device pointers; no torch types.
+ */
+#ifndef SPAMM_B200_H
+#define SPAMM_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SPAMM_ABI_VERSION 1
+#define SPAMM_OK 0
+#define SPAMM_EINVAL 1
+#define SPAMM_ECUDA 2
+#define SPAMM_MAX_TIERS 64
+
+/* Leaf-product kernels (spamm_multiply / spamm_gemm_batch `kernel`). */
+#define SPAMM_LEAF_AUTO 0  /* DMMA for Nb in {8,16,32,64}, else exact        */
+#define SPAMM_LEAF_DMMA 1  /* FP64 tensor cores (mma.sync f64 -> DMMA)       */
+#define SPAMM_LEAF_EXACT 2 /* CUDA-core, reference order: bitwise identical  */
+
+typedef struct spamm_mat spamm_mat;
+
+/* Geometry + device pointers of a matrix (fields of QuadTreeMatrix,
+ * quadtree.py:85-113).  Pointers stay valid until spamm_mat_free. */
+typedef struct {
+  int64_t n_native;
+  int32_t block_size;  /* Nb */
+  int32_t depth;       /* tiers - 1 */
+  int64_t chunk_size;
+  int64_t n_blocks;    /* leaf grid side G = 2^depth */
+  int64_t stored;      /* non-null leaf blocks S */
+  double* data;        /* (S, Nb, Nb) f64, Morton order of (bi, bj) */
+  int64_t* keys;       /* (S,) bi * G + bj per stored block */
+  int32_t* slot;       /* (G*G,) storage slot per key, -1 = null */
+  double* norms;       /* pyramid, tier t (2^t x 2^t row-major) at (4^t-1)/3 */
+  double* norms2;      /* same, squared */
+} spamm_mat_info;
+
+/* ProductStats (kernel.py:38-61) plus device timings. */
+typedef struct {
+  double tau;
+  int32_t n_tiers;
+  int64_t visited[SPAMM_MAX_TIERS];
+  int64_t culled[SPAMM_MAX_TIERS];
+  int64_t leaf_products;
+  int64_t flop_estimate; /* leaf_products * 2 * Nb^3 (kernel.py:248) */
+  int64_t c_blocks;      /* C blocks produced before zero pruning */
+  float ms_cull;         /* CUDA-event times on `stream` (0 if not timed) */
+  float ms_leaf;
+  float ms_finalize;
+} spamm_stats;
+
+int spamm_abi_version(void);
+const char* spamm_last_error(void);
+
+/* build_from_dense (quadtree.py:208-242).  dense: device, n x n row-major
+ * with leading dimension ld.  Pads to Nb * 2^d, keeps non-zero blocks. */
+int spamm_mat_from_dense(const double* dense, int64_t n, int64_t ld, int32_t block_size,
+                         int64_t chunk_size, void* stream, spamm_mat** out);
+/* QuadTreeMatrix._from_blocks (quadtree.py:170-194).  keys/data: device,
+ * any key order; exact-zero blocks are pruned; the norm pyramid is rebuilt. */
+int spamm_mat_from_blocks(int64_t n_native, int32_t block_size, int64_t chunk_size,
+                          int32_t depth, const int64_t* keys, const double* data, int64_t m,
+                          void* stream, spamm_mat** out);
+/* identity (quadtree.py:308-323). */
+int spamm_mat_identity(int64_t n, int32_t block_size, int64_t chunk_size, void* stream,
+                       spamm_mat** out);
+int spamm_mat_info_get(const spamm_mat* m, spamm_mat_info* info);
+int spamm_mat_free(spamm_mat* m);
+/* to_dense (quadtree.py:245-252): dense n_native x n_native, leading dim ld. */
+int spamm_mat_to_dense(const spamm_mat* m, double* dense, int64_t ld, void* stream);
+
+/* multiply (kernel.py:157-223): C = A*B culled at tau (strict >). */
+int spamm_multiply(const spamm_mat* a, const spamm_mat* b, double tau, int32_t kernel,
+                   int32_t timed, void* stream, spamm_mat** c, spamm_stats* stats);
+/* convolution_census (kernel.py:226-239): counts only. */
+int spamm_census(const spamm_mat* a, const spamm_mat* b, double tau, void* stream,
+                 spamm_stats* stats);
+/* _sweep task list (kernel.py:96-122 + sort kernel.py:189-196): copies the
+ * surviving leaf triples, grouped by C block (Morton order) with k ascending,
+ * into caller device arrays of capacity `cap` (int32 i, k, j).  *n_out gets
+ * the count (also when it exceeds cap; nothing is written then). */
+int spamm_tasks(const spamm_mat* a, const spamm_mat* b, double tau, int32_t* ti, int32_t* tk,
+                int32_t* tj, int64_t cap, int64_t* n_out, void* stream);
+
+/* The compiled seam _gemm_batch(a_pos, b_pos, c_pos, a_data, b_data, c_data)
+ * (kernel.py:74-77): c_data[c_pos[t]] += a_data[a_pos[t]] @ b_data[b_pos[t]]
+ * for t in order.  Tasks of one C block must be contiguous (sorted by C);
+ * all arrays are device pointers; int64 positions as in the reference. */
+int spamm_gemm_batch(const int64_t* a_pos, const int64_t* b_pos, const int64_t* c_pos,
+                     int64_t n_tasks, const double* a_data, const double* b_data, double* c_data,
+                     int32_t block_size, int32_t kernel, void* stream);
+
+/* add_scaled (quadtree.py:281-293). */
+int spamm_add_scaled(double alpha, const spamm_mat* a, double beta, const spamm_mat* b,
+                     void* stream, spamm_mat** out);
+/* trace (quadtree.py:296-305). */
+int spamm_trace(const spamm_mat* m, void* stream, double* out);
+/* gershgorin_bounds (sp2.py:68-76): eps_min, eps_max and max|F-F^T|
+ * (caller raises when asym > sym_tol, as the reference does). */
+int spamm_gershgorin(const spamm_mat* f, void* stream, double* eps_min, double* eps_max,
+                     double* asym);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPAMM_B200_H */

@@ -1,0 +1,398 @@
+// C ABI (include/spamm_b200.h): argument checks, handle management and the
+// multiply driver (cull -> leaf products -> C finalisation).
+#include <cstring>
+#include <string>
+
+#include "../../include/spamm_b200.h"
+#include "internal.h"
+
+struct spamm_mat {
+  spamm::Mat m;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define SPAMM_API_BEGIN try {
+#define SPAMM_API_END                                              \
+  }                                                                \
+  catch (const spamm::CudaError& e) {                              \
+    return fail(SPAMM_ECUDA, e.what());                            \
+  }                                                                \
+  catch (const std::exception& e) {                                \
+    return fail(SPAMM_ECUDA, e.what());                            \
+  }                                                                \
+  return SPAMM_OK;
+
+inline cudaStream_t S(void* p) { return reinterpret_cast<cudaStream_t>(p); }
+
+bool is_pow2(int64_t x) { return x >= 1 && (x & (x - 1)) == 0; }
+
+int padded_depth(int64_t n, int64_t nb) {
+  int d = 0;
+  while ((nb << d) < n) ++d;
+  return d;
+}
+
+int check_conformable(const spamm_mat* a, const spamm_mat* b) {
+  if (!a || !b) return fail(SPAMM_EINVAL, "null matrix handle");
+  if (a->m.n_native != b->m.n_native || a->m.depth != b->m.depth || a->m.nb != b->m.nb)
+    return fail(SPAMM_EINVAL, "shape/blocking mismatch: (" + std::to_string(a->m.n_native) + ", " +
+                                  std::to_string(a->m.nb << a->m.depth) + ", " +
+                                  std::to_string(a->m.nb) + ") vs (" +
+                                  std::to_string(b->m.n_native) + ", " +
+                                  std::to_string(b->m.nb << b->m.depth) + ", " +
+                                  std::to_string(b->m.nb) + ")");
+  return SPAMM_OK;
+}
+
+struct EventTimer {
+  cudaEvent_t e[4] = {nullptr, nullptr, nullptr, nullptr};
+  bool on;
+  cudaStream_t s;
+  EventTimer(bool on_, cudaStream_t s_) : on(on_), s(s_) {
+    if (on)
+      for (auto& x : e) SPAMM_CK(cudaEventCreate(&x));
+  }
+  void mark(int i) {
+    if (on) SPAMM_CK(cudaEventRecord(e[i], s));
+  }
+  float ms(int i, int j) {
+    if (!on) return 0.f;
+    float v = 0.f;
+    SPAMM_CK(cudaEventSynchronize(e[j]));
+    SPAMM_CK(cudaEventElapsedTime(&v, e[i], e[j]));
+    return v;
+  }
+  ~EventTimer() {
+    if (on)
+      for (auto& x : e) cudaEventDestroy(x);
+  }
+};
+
+__global__ void k_keys_from_nodes(const int32_t* ci, const int32_t* cj, int64_t n, int64_t G,
+                                  int64_t* keys) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    keys[i] = (int64_t)ci[i] * G + cj[i];
+}
+
+__global__ void k_expand_tasks(const int32_t* ci, const int32_t* cj, const int64_t* seg,
+                               const int32_t* k, int64_t n_c, int32_t* ti, int32_t* tk,
+                               int32_t* tj) {
+  for (int64_t c = blockIdx.x; c < n_c; c += gridDim.x)
+    for (int64_t t = seg[c] + threadIdx.x; t < seg[c + 1]; t += blockDim.x) {
+      ti[t] = ci[c];
+      tj[t] = cj[c];
+      tk[t] = k[t];
+    }
+}
+
+__global__ void k_seg_flags(const int64_t* c_pos, int64_t n, uint8_t* flags) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n;
+       t += (int64_t)gridDim.x * blockDim.x)
+    flags[t] = (t == 0 || c_pos[t] != c_pos[t - 1]) ? 1 : 0;
+}
+
+__global__ void k_seg_build(const int64_t* c_pos, const uint8_t* flags, const int64_t* off,
+                            int64_t n, int64_t* seg, int64_t* c_out, int64_t nseg) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n;
+       t += (int64_t)gridDim.x * blockDim.x)
+    if (flags[t]) {
+      seg[off[t]] = t;
+      c_out[off[t]] = c_pos[t];
+    }
+  if (blockIdx.x == 0 && threadIdx.x == 0) seg[nseg] = n;
+}
+
+void fill_stats(spamm_stats* st, double tau, const spamm::CullResult& r, int nb) {
+  if (!st) return;
+  std::memset(st, 0, sizeof(*st));
+  st->tau = tau;
+  st->n_tiers = (int32_t)r.visited.size();
+  for (size_t t = 0; t < r.visited.size() && t < SPAMM_MAX_TIERS; ++t) {
+    st->visited[t] = r.visited[t];
+    st->culled[t] = r.culled[t];
+  }
+  st->leaf_products = r.visited.empty() ? 0 : r.visited.back();
+  st->flop_estimate = st->leaf_products * 2 * (int64_t)nb * nb * nb;
+}
+
+}  // namespace
+
+extern "C" {
+
+int spamm_abi_version(void) { return SPAMM_ABI_VERSION; }
+const char* spamm_last_error(void) { return g_err.c_str(); }
+
+int spamm_mat_from_dense(const double* dense, int64_t n, int64_t ld, int32_t block_size,
+                         int64_t chunk_size, void* stream, spamm_mat** out) {
+  if (!out) return fail(SPAMM_EINVAL, "null output handle");
+  if (n < 1) return fail(SPAMM_EINVAL, "matrix must have at least one row");
+  if (!is_pow2(block_size))
+    return fail(SPAMM_EINVAL, "block size must be a power of two, got " + std::to_string(block_size));
+  if (ld < n) return fail(SPAMM_EINVAL, "leading dimension smaller than n");
+  SPAMM_API_BEGIN
+  auto* h = new spamm_mat();
+  h->m.n_native = n;
+  h->m.nb = block_size;
+  h->m.depth = padded_depth(n, block_size);
+  h->m.G = int64_t(1) << h->m.depth;
+  h->m.chunk_size = chunk_size;
+  h->m.stream = S(stream);
+  try {
+    spamm::from_dense(dense, n, ld, h->m, S(stream));
+  } catch (...) {
+    h->m.release();
+    delete h;
+    throw;
+  }
+  *out = h;
+  SPAMM_API_END
+}
+
+int spamm_mat_from_blocks(int64_t n_native, int32_t block_size, int64_t chunk_size, int32_t depth,
+                          const int64_t* keys, const double* data, int64_t m, void* stream,
+                          spamm_mat** out) {
+  if (!out) return fail(SPAMM_EINVAL, "null output handle");
+  if (!is_pow2(block_size)) return fail(SPAMM_EINVAL, "block size must be a power of two");
+  if (depth < 0 || depth > 24) return fail(SPAMM_EINVAL, "depth out of range");
+  if (m < 0) return fail(SPAMM_EINVAL, "negative block count");
+  SPAMM_API_BEGIN
+  cudaStream_t s = S(stream);
+  auto* h = new spamm_mat();
+  spamm::Mat& M = h->m;
+  M.n_native = n_native;
+  M.nb = block_size;
+  M.chunk_size = chunk_size;
+  M.depth = depth;
+  M.G = int64_t(1) << depth;
+  M.stream = s;
+  // Re-order the given blocks along the Morton curve: 1.0 * blocks + (empty)
+  // through add_scaled, which walks the curve and is exact for alpha = 1.
+  spamm::Mat tmp;
+  tmp.n_native = n_native;
+  tmp.nb = block_size;
+  tmp.chunk_size = chunk_size;
+  tmp.depth = depth;
+  tmp.G = M.G;
+  tmp.stream = s;
+  tmp.nblocks = m;
+  tmp.data = const_cast<double*>(data);
+  tmp.keys = const_cast<int64_t*>(keys);
+  tmp.slot = spamm::dmalloc<int32_t>(M.G * M.G, s);
+  SPAMM_CK(cudaMemsetAsync(tmp.slot, 0xFF, M.G * M.G * sizeof(int32_t), s));
+  spamm::Mat empty;
+  empty.depth = depth;
+  empty.nb = block_size;
+  empty.G = M.G;
+  empty.slot = spamm::dmalloc<int32_t>(M.G * M.G, s);
+  SPAMM_CK(cudaMemsetAsync(empty.slot, 0xFF, M.G * M.G * sizeof(int32_t), s));
+  spamm::scatter_slots(keys, m, tmp.slot, s);
+  spamm::add_scaled(1.0, tmp, 0.0, empty, M, s);
+  spamm::dfree(tmp.slot, s);
+  spamm::dfree(empty.slot, s);
+  *out = h;
+  SPAMM_API_END
+}
+
+int spamm_mat_identity(int64_t n, int32_t block_size, int64_t chunk_size, void* stream,
+                       spamm_mat** out) {
+  if (!out) return fail(SPAMM_EINVAL, "null output handle");
+  if (n < 1) return fail(SPAMM_EINVAL, "identity needs n >= 1");
+  if (!is_pow2(block_size)) return fail(SPAMM_EINVAL, "block size must be a power of two");
+  SPAMM_API_BEGIN
+  auto* h = new spamm_mat();
+  h->m.n_native = n;
+  h->m.nb = block_size;
+  h->m.depth = padded_depth(n, block_size);
+  h->m.G = int64_t(1) << h->m.depth;
+  h->m.chunk_size = chunk_size;
+  h->m.stream = S(stream);
+  spamm::identity(h->m, S(stream));
+  *out = h;
+  SPAMM_API_END
+}
+
+int spamm_mat_info_get(const spamm_mat* h, spamm_mat_info* info) {
+  if (!h || !info) return fail(SPAMM_EINVAL, "null argument");
+  info->n_native = h->m.n_native;
+  info->block_size = h->m.nb;
+  info->depth = h->m.depth;
+  info->chunk_size = h->m.chunk_size;
+  info->n_blocks = h->m.G;
+  info->stored = h->m.nblocks;
+  info->data = h->m.data;
+  info->keys = h->m.keys;
+  info->slot = h->m.slot;
+  info->norms = h->m.norms;
+  info->norms2 = h->m.norms2;
+  return SPAMM_OK;
+}
+
+int spamm_mat_free(spamm_mat* h) {
+  if (!h) return SPAMM_OK;
+  h->m.release();
+  delete h;
+  return SPAMM_OK;
+}
+
+int spamm_mat_to_dense(const spamm_mat* h, double* dense, int64_t ld, void* stream) {
+  if (!h || !dense) return fail(SPAMM_EINVAL, "null argument");
+  if (ld < h->m.n_native) return fail(SPAMM_EINVAL, "leading dimension smaller than n");
+  SPAMM_API_BEGIN
+  spamm::to_dense(h->m, dense, ld, S(stream));
+  SPAMM_API_END
+}
+
+int spamm_multiply(const spamm_mat* a, const spamm_mat* b, double tau, int32_t kernel,
+                   int32_t timed, void* stream, spamm_mat** c, spamm_stats* stats) {
+  if (int rc = check_conformable(a, b)) return rc;
+  if (!(tau >= 0.0) || tau == __builtin_inf())
+    return fail(SPAMM_EINVAL, "tau must be finite and >= 0, got " + std::to_string(tau));
+  if (kernel < 0 || kernel > 2) return fail(SPAMM_EINVAL, "unknown leaf kernel");
+  if (kernel == SPAMM_LEAF_DMMA && !spamm::dmma_supported(a->m.nb))
+    return fail(SPAMM_EINVAL, "DMMA leaf kernel needs block size 8, 16, 32 or 64");
+  if (!c) return fail(SPAMM_EINVAL, "null output handle");
+  SPAMM_API_BEGIN
+  cudaStream_t s = S(stream);
+  EventTimer tm(timed != 0, s);
+  tm.mark(0);
+  spamm::CullResult r;
+  spamm::cull(a->m, b->m, tau, true, r, s);
+  tm.mark(1);
+  auto* h = new spamm_mat();
+  spamm::Mat& C = h->m;
+  C.n_native = a->m.n_native;
+  C.nb = a->m.nb;
+  C.chunk_size = a->m.chunk_size;
+  C.depth = a->m.depth;
+  C.G = a->m.G;
+  C.stream = s;
+  C.nblocks = r.n_c;
+  const int64_t nb2 = (int64_t)C.nb * C.nb;
+  C.data = spamm::dmalloc<double>((size_t)r.n_c * nb2, s);
+  C.keys = spamm::dmalloc<int64_t>(r.n_c, s);
+  if (r.n_c > 0) {
+    spamm::leaf_products<int32_t>(r.n_c, r.seg, r.a_idx, r.b_idx, nullptr, false, a->m.data,
+                                  b->m.data, C.data, C.nb, kernel, s);
+  }
+  tm.mark(2);
+  if (r.n_c > 0) {
+    k_keys_from_nodes<<<spamm::grid_for(r.n_c, 256), 256, 0, s>>>(r.ci, r.cj, r.n_c, C.G, C.keys);
+    SPAMM_LAUNCH_CK();
+  }
+  spamm::finalize(C, s);
+  tm.mark(3);
+  fill_stats(stats, tau, r, C.nb);
+  if (stats) {
+    stats->c_blocks = r.n_c;
+    stats->ms_cull = tm.ms(0, 1);
+    stats->ms_leaf = tm.ms(1, 2);
+    stats->ms_finalize = tm.ms(2, 3);
+  }
+  r.release(s);
+  *c = h;
+  SPAMM_API_END
+}
+
+int spamm_census(const spamm_mat* a, const spamm_mat* b, double tau, void* stream,
+                 spamm_stats* stats) {
+  if (int rc = check_conformable(a, b)) return rc;
+  if (!(tau >= 0.0) || tau == __builtin_inf())
+    return fail(SPAMM_EINVAL, "tau must be finite and >= 0, got " + std::to_string(tau));
+  SPAMM_API_BEGIN
+  cudaStream_t s = S(stream);
+  spamm::CullResult r;
+  spamm::cull(a->m, b->m, tau, false, r, s);
+  fill_stats(stats, tau, r, a->m.nb);
+  r.release(s);
+  SPAMM_API_END
+}
+
+int spamm_tasks(const spamm_mat* a, const spamm_mat* b, double tau, int32_t* ti, int32_t* tk,
+                int32_t* tj, int64_t cap, int64_t* n_out, void* stream) {
+  if (int rc = check_conformable(a, b)) return rc;
+  if (!(tau >= 0.0) || tau == __builtin_inf()) return fail(SPAMM_EINVAL, "tau must be finite and >= 0");
+  if (!n_out) return fail(SPAMM_EINVAL, "null n_out");
+  SPAMM_API_BEGIN
+  cudaStream_t s = S(stream);
+  spamm::CullResult r;
+  spamm::cull(a->m, b->m, tau, true, r, s);
+  *n_out = r.n_tasks;
+  if (r.n_tasks > 0 && r.n_tasks <= cap) {
+    k_expand_tasks<<<spamm::grid_for(r.n_c, 1, 148LL * 32), 128, 0, s>>>(r.ci, r.cj, r.seg, r.k,
+                                                                          r.n_c, ti, tk, tj);
+    SPAMM_LAUNCH_CK();
+  }
+  r.release(s);
+  SPAMM_API_END
+}
+
+int spamm_gemm_batch(const int64_t* a_pos, const int64_t* b_pos, const int64_t* c_pos,
+                     int64_t n_tasks, const double* a_data, const double* b_data, double* c_data,
+                     int32_t block_size, int32_t kernel, void* stream) {
+  if (n_tasks < 0) return fail(SPAMM_EINVAL, "negative task count");
+  if (block_size < 1) return fail(SPAMM_EINVAL, "block size must be >= 1");
+  if (kernel < 0 || kernel > 2) return fail(SPAMM_EINVAL, "unknown leaf kernel");
+  if (kernel == SPAMM_LEAF_DMMA && !spamm::dmma_supported(block_size))
+    return fail(SPAMM_EINVAL, "DMMA leaf kernel needs block size 8, 16, 32 or 64");
+  if (n_tasks == 0) return SPAMM_OK;
+  SPAMM_API_BEGIN
+  cudaStream_t s = S(stream);
+  uint8_t* flags = spamm::dmalloc<uint8_t>(n_tasks, s);
+  int64_t* off = spamm::dmalloc<int64_t>(n_tasks + 1, s);
+  k_seg_flags<<<spamm::grid_for(n_tasks, 256), 256, 0, s>>>(c_pos, n_tasks, flags);
+  SPAMM_LAUNCH_CK();
+  spamm::scan_exclusive_u8(flags, n_tasks, off, s);
+  int64_t nseg = 0;
+  spamm::d2h_sync(&nseg, off + n_tasks, 1, s);
+  int64_t* seg = spamm::dmalloc<int64_t>(nseg + 1, s);
+  int64_t* c_out = spamm::dmalloc<int64_t>(nseg, s);
+  k_seg_build<<<spamm::grid_for(n_tasks, 256), 256, 0, s>>>(c_pos, flags, off, n_tasks, seg, c_out,
+                                                             nseg);
+  SPAMM_LAUNCH_CK();
+  spamm::leaf_products<int64_t>(nseg, seg, a_pos, b_pos, c_out, true, a_data, b_data, c_data,
+                                block_size, kernel, s);
+  spamm::dfree(flags, s);
+  spamm::dfree(off, s);
+  spamm::dfree(seg, s);
+  spamm::dfree(c_out, s);
+  SPAMM_API_END
+}
+
+int spamm_add_scaled(double alpha, const spamm_mat* a, double beta, const spamm_mat* b,
+                     void* stream, spamm_mat** out) {
+  if (int rc = check_conformable(a, b)) return rc;
+  if (!out) return fail(SPAMM_EINVAL, "null output handle");
+  SPAMM_API_BEGIN
+  auto* h = new spamm_mat();
+  h->m.stream = S(stream);
+  spamm::add_scaled(alpha, a->m, beta, b->m, h->m, S(stream));
+  h->m.G = a->m.G;
+  *out = h;
+  SPAMM_API_END
+}
+
+int spamm_trace(const spamm_mat* m, void* stream, double* out) {
+  if (!m || !out) return fail(SPAMM_EINVAL, "null argument");
+  SPAMM_API_BEGIN
+  *out = spamm::trace(m->m, S(stream));
+  SPAMM_API_END
+}
+
+int spamm_gershgorin(const spamm_mat* f, void* stream, double* eps_min, double* eps_max,
+                     double* asym) {
+  if (!f || !eps_min || !eps_max || !asym) return fail(SPAMM_EINVAL, "null argument");
+  SPAMM_API_BEGIN
+  spamm::gershgorin(f->m, eps_min, eps_max, asym, S(stream));
+  SPAMM_API_END
+}
+
+}  // extern "C"

@@ -1,0 +1,245 @@
+// K2 + K3: tiered culling with in-order compaction.
+//
+// Reference: kernel._sweep (kernel.py:96-122) + the task sort / searchsorted
+// block of multiply (kernel.py:189-204).
+//
+// The reference expands every surviving triple (i,k,j) of tier t into its 8
+// children, keeps those with nA[t+1][i,k] * nB[t+1][k,j] > tau (strict), and
+// finally sorts the leaf triples by C block then k.  Here the survivors are
+// kept grouped by their C node (I,J) with K ascending, so no sort is needed:
+// a C node with K-list L has 4 children (di,dj) whose candidate lists are
+// [2K+dk for K in L for dk in (0,1)] -- already ascending.  Per tier:
+//   pass 1 (count): one warp per parent node counts survivors per child
+//                   with __ballot_sync/__popc, packing (node>0, count) into
+//                   one int64 so a single scan yields both offsets;
+//   pass 2 (scan):  device-wide exclusive scan (scan.cu);
+//   pass 3 (write): same predicate, ballot + popc(lanemask_lt) compaction
+//                   into the child node's segment (deterministic order).
+// Candidates per tier are 8 x survivors of the previous tier, exactly the
+// reference's expansion, so visited/culled per tier are identical.  The
+// surviving C nodes come out in Morton (Z) order of (i, j).
+#include "internal.h"
+
+namespace spamm {
+
+namespace {
+
+constexpr int NODE_SHIFT = 40;
+constexpr int64_t TASK_MASK = (int64_t(1) << NODE_SHIFT) - 1;
+constexpr int CULL_THREADS = 256;
+
+__device__ __forceinline__ bool keep_pair(double na, double nb, double tau) {
+  return __dmul_rn(na, nb) > tau;
+}
+
+__global__ void k_cull_root(const double* __restrict__ nA, const double* __restrict__ nB,
+                            double tau, int32_t* ci, int32_t* cj, int64_t* seg, int32_t* K,
+                            int64_t* count, const int32_t* slotA, const int32_t* slotB,
+                            int32_t* aidx, int32_t* bidx) {
+  const bool keep = keep_pair(nA[0], nB[0], tau);
+  ci[0] = 0;
+  cj[0] = 0;
+  seg[0] = 0;
+  seg[1] = keep ? 1 : 0;
+  K[0] = 0;
+  count[0] = keep ? 1 : 0;
+  if (aidx && keep) {
+    aidx[0] = slotA[0];
+    bidx[0] = slotB[0];
+  }
+}
+
+// WRITE=false: count pass.  WRITE=true: compaction pass (LEAF: also A/B slots).
+template <bool WRITE, bool LEAF>
+__global__ void __launch_bounds__(CULL_THREADS)
+    k_cull_expand(int t1, const double* __restrict__ nA, const double* __restrict__ nB, double tau,
+                  int64_t M, const int32_t* __restrict__ ci, const int32_t* __restrict__ cj,
+                  const int64_t* __restrict__ seg, const int32_t* __restrict__ K,
+                  int64_t* __restrict__ cnt4, const int64_t* __restrict__ off4,
+                  int32_t* __restrict__ ci_o, int32_t* __restrict__ cj_o,
+                  int64_t* __restrict__ seg_o, int32_t* __restrict__ K_o,
+                  const int32_t* __restrict__ slotA, const int32_t* __restrict__ slotB,
+                  int32_t* __restrict__ aidx, int32_t* __restrict__ bidx, int64_t Mn, int64_t Vn) {
+  const int64_t W = int64_t(1) << t1;
+  const double* A = nA + tier_offset(t1);
+  const double* B = nB + tier_offset(t1);
+  const int lane = threadIdx.x & 31;
+  const unsigned lt_mask = (1u << lane) - 1u;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  if (WRITE && gw == 0 && lane == 0) seg_o[Mn] = Vn;
+  for (int64_t p = gw; p < M; p += nw) {
+    const int64_t I = ci[p], J = cj[p];
+    const int64_t s = seg[p], e = seg[p + 1];
+#pragma unroll 1
+    for (int c = 0; c < 4; ++c) {
+      const int64_t row = 2 * I + (c >> 1), col = 2 * J + (c & 1);
+      const double* Arow = A + row * W;
+      int64_t toff = 0;
+      if (WRITE) {
+        const int64_t v = off4[4 * p + c], vn = off4[4 * p + c + 1];
+        if (((vn - v) & TASK_MASK) == 0) continue;
+        const int64_t node = v >> NODE_SHIFT;
+        toff = v & TASK_MASK;
+        if (lane == 0) {
+          ci_o[node] = (int32_t)row;
+          cj_o[node] = (int32_t)col;
+          seg_o[node] = toff;
+        }
+      }
+      int64_t cnt = 0;
+      for (int64_t q0 = s; q0 < e; q0 += 16) {
+        const int64_t q = q0 + (lane >> 1);
+        const bool valid = q < e;
+        const int64_t kk = valid ? 2 * (int64_t)K[q] + (lane & 1) : 0;
+        const bool keep = valid && keep_pair(Arow[kk], B[kk * W + col], tau);
+        const unsigned mask = __ballot_sync(0xffffffffu, keep);
+        if (WRITE) {
+          if (keep) {
+            const int64_t pos = toff + __popc(mask & lt_mask);
+            K_o[pos] = (int32_t)kk;
+            if (LEAF) {
+              aidx[pos] = slotA[row * W + kk];
+              bidx[pos] = slotB[kk * W + col];
+            }
+          }
+          toff += __popc(mask);
+        } else {
+          cnt += __popc(mask);
+        }
+      }
+      if (!WRITE && lane == 0)
+        cnt4[4 * p + c] = cnt + (cnt > 0 ? (int64_t(1) << NODE_SHIFT) : 0);
+    }
+  }
+}
+
+int cull_grid(int64_t M) { return grid_for(M * 32, CULL_THREADS, 148LL * 64); }
+
+}  // namespace
+
+void CullResult::release(cudaStream_t s) {
+  dfree(ci, s);
+  dfree(cj, s);
+  dfree(seg, s);
+  dfree(k, s);
+  dfree(a_idx, s);
+  dfree(b_idx, s);
+  ci = cj = nullptr;
+  seg = nullptr;
+  k = a_idx = b_idx = nullptr;
+  n_c = n_tasks = 0;
+}
+
+void cull(const Mat& a, const Mat& b, double tau, bool want_tasks, CullResult& r,
+          cudaStream_t s) {
+  const int depth = a.depth;
+  r.visited.assign(depth + 1, 0);
+  r.culled.assign(depth + 1, 0);
+  r.n_c = r.n_tasks = 0;
+
+  int32_t* ci = dmalloc<int32_t>(1, s);
+  int32_t* cj = dmalloc<int32_t>(1, s);
+  int64_t* seg = dmalloc<int64_t>(2, s);
+  int32_t* K = dmalloc<int32_t>(1, s);
+  int64_t* cnt = dmalloc<int64_t>(1, s);
+  int32_t* aidx = nullptr;
+  int32_t* bidx = nullptr;
+  if (depth == 0 && want_tasks) {
+    aidx = dmalloc<int32_t>(1, s);
+    bidx = dmalloc<int32_t>(1, s);
+  }
+  k_cull_root<<<1, 1, 0, s>>>(a.norms, b.norms, tau, ci, cj, seg, K, cnt, a.slot, b.slot, aidx,
+                              bidx);
+  SPAMM_LAUNCH_CK();
+  int64_t V = 0;
+  d2h_sync(&V, cnt, 1, s);
+  dfree(cnt, s);
+  r.visited[0] = V;
+  r.culled[0] = 1 - V;
+  int64_t M = V;
+
+  auto free_level = [&]() {
+    dfree(ci, s);
+    dfree(cj, s);
+    dfree(seg, s);
+    dfree(K, s);
+    dfree(aidx, s);
+    dfree(bidx, s);
+    ci = cj = nullptr;
+    seg = nullptr;
+    K = aidx = bidx = nullptr;
+  };
+
+  int t = 0;
+  for (; V > 0 && t < depth; ++t) {
+    const int t1 = t + 1;
+    const bool leaf = t1 == depth;
+    int64_t* cnt4 = dmalloc<int64_t>(4 * M, s);
+    int64_t* off4 = dmalloc<int64_t>(4 * M + 1, s);
+    k_cull_expand<false, false><<<cull_grid(M), CULL_THREADS, 0, s>>>(
+        t1, a.norms, b.norms, tau, M, ci, cj, seg, K, cnt4, nullptr, nullptr, nullptr, nullptr,
+        nullptr, nullptr, nullptr, nullptr, nullptr, 0, 0);
+    SPAMM_LAUNCH_CK();
+    scan_exclusive_i64(cnt4, 4 * M, off4, s);
+    int64_t packed = 0;
+    d2h_sync(&packed, off4 + 4 * M, 1, s);
+    const int64_t Vn = packed & TASK_MASK, Mn = packed >> NODE_SHIFT;
+    r.visited[t1] = Vn;
+    r.culled[t1] = 8 * V - Vn;
+    if (Vn == 0 || (leaf && !want_tasks)) {
+      dfree(cnt4, s);
+      dfree(off4, s);
+      free_level();
+      V = Vn;
+      M = Mn;
+      t = t1;
+      break;
+    }
+    int32_t* ci_o = dmalloc<int32_t>(Mn, s);
+    int32_t* cj_o = dmalloc<int32_t>(Mn, s);
+    int64_t* seg_o = dmalloc<int64_t>(Mn + 1, s);
+    int32_t* K_o = dmalloc<int32_t>(Vn, s);
+    int32_t* ai = nullptr;
+    int32_t* bi = nullptr;
+    if (leaf) {
+      ai = dmalloc<int32_t>(Vn, s);
+      bi = dmalloc<int32_t>(Vn, s);
+      k_cull_expand<true, true><<<cull_grid(M), CULL_THREADS, 0, s>>>(
+          t1, a.norms, b.norms, tau, M, ci, cj, seg, K, nullptr, off4, ci_o, cj_o, seg_o, K_o,
+          a.slot, b.slot, ai, bi, Mn, Vn);
+    } else {
+      k_cull_expand<true, false><<<cull_grid(M), CULL_THREADS, 0, s>>>(
+          t1, a.norms, b.norms, tau, M, ci, cj, seg, K, nullptr, off4, ci_o, cj_o, seg_o, K_o,
+          nullptr, nullptr, nullptr, nullptr, Mn, Vn);
+    }
+    SPAMM_LAUNCH_CK();
+    dfree(cnt4, s);
+    dfree(off4, s);
+    free_level();
+    ci = ci_o;
+    cj = cj_o;
+    seg = seg_o;
+    K = K_o;
+    aidx = ai;
+    bidx = bi;
+    V = Vn;
+    M = Mn;
+  }
+  // Tiers after an early exit keep zero counts (kernel.py:114-117).
+  if (V > 0 && want_tasks && ci != nullptr) {
+    r.n_c = M;
+    r.n_tasks = V;
+    r.ci = ci;
+    r.cj = cj;
+    r.seg = seg;
+    r.k = K;
+    r.a_idx = aidx;
+    r.b_idx = bidx;
+  } else {
+    free_level();
+    if (!want_tasks) r.n_tasks = r.visited[depth];
+  }
+}
+
+}  // namespace spamm

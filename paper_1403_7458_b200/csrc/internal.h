@@ -1,0 +1,94 @@
+// Internal (non-exported) host interfaces shared by the library's translation units.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <vector>
+
+#include "common.cuh"
+
+namespace spamm {
+
+// ---- stream-ordered device memory (cudaMallocAsync on the default pool) ----
+void* dmalloc_bytes(size_t bytes, cudaStream_t s);
+void dfree(void* p, cudaStream_t s);
+template <class T>
+T* dmalloc(size_t n, cudaStream_t s) {
+  return static_cast<T*>(dmalloc_bytes(n * sizeof(T), s));
+}
+
+// Copy a few int64 from device to host and wait (the only host syncs on the path).
+void d2h_sync(int64_t* host, const int64_t* dev, int n, cudaStream_t s);
+
+// ---- quadtree matrix (device resident) ----
+struct Mat {
+  int64_t n_native = 0;
+  int nb = 0;
+  int64_t chunk_size = 0;
+  int depth = 0;
+  int64_t G = 1;
+  int64_t nblocks = 0;
+  double* data = nullptr;    // nblocks * nb * nb, Morton order of (bi, bj)
+  int64_t* keys = nullptr;   // nblocks, bi * G + bj
+  int32_t* slot = nullptr;   // G * G, storage slot or -1
+  double* norms = nullptr;   // pyramid_size(depth)
+  double* norms2 = nullptr;  // pyramid_size(depth)
+  cudaStream_t stream = nullptr;
+  void release();
+};
+
+// Finalise a matrix whose data/keys (nblocks, Morton order) are set: prune
+// exact-zero blocks, build slot map and the bit-exact norm pyramid
+// (quadtree.py:170-194).  Takes ownership of data/keys.
+void finalize(Mat& m, cudaStream_t s);
+
+void scatter_slots(const int64_t* keys, int64_t m, int32_t* slot, cudaStream_t s);
+// Leaf norm^2 (einsum recipe) and nonzero flags for m blocks of nb x nb.
+void leaf_norms2(const double* data, int64_t m, int nb, double* norms2, uint8_t* nonzero,
+                 cudaStream_t s);
+// Fill the pyramid from per-block leaf norms^2 (keys given); zero elsewhere.
+void build_pyramid(const int64_t* keys, const double* blk_norms2, int64_t m, int depth,
+                   double* norms, double* norms2, cudaStream_t s);
+
+// ---- scan ----
+// out[0..n]: exclusive prefix sums, out[n] = total.
+void scan_exclusive_u8(const uint8_t* in, int64_t n, int64_t* out, cudaStream_t s);
+void scan_exclusive_i64(const int64_t* in, int64_t n, int64_t* out, cudaStream_t s);
+
+// ---- culling ----
+struct CullResult {
+  int64_t n_c = 0;            // C blocks (leaf-tier nodes with >= 1 survivor)
+  int64_t n_tasks = 0;        // surviving leaf products
+  int32_t* ci = nullptr;      // n_c
+  int32_t* cj = nullptr;      // n_c
+  int64_t* seg = nullptr;     // n_c + 1
+  int32_t* k = nullptr;       // n_tasks
+  int32_t* a_idx = nullptr;   // n_tasks (storage slot of A_ik)
+  int32_t* b_idx = nullptr;   // n_tasks (storage slot of B_kj)
+  std::vector<int64_t> visited, culled;
+  void release(cudaStream_t s);
+};
+// Tiered culling (kernel.py:96-122).  want_tasks=false: census only
+// (kernel.py:226-239) -- counts for every tier, no leaf task list.
+void cull(const Mat& a, const Mat& b, double tau, bool want_tasks, CullResult& r,
+          cudaStream_t s);
+
+// ---- leaf products ----
+enum LeafKernel { LEAF_AUTO = 0, LEAF_DMMA = 1, LEAF_EXACT = 2 };
+// For each segment m: C[c_out ? c_out[m] : m] (+)= sum_{t in seg m} A[a_idx[t]] * B[b_idx[t]]
+template <class Idx>
+void leaf_products(int64_t n_seg, const int64_t* seg, const Idx* a_idx, const Idx* b_idx,
+                   const int64_t* c_out, bool accumulate, const double* A, const double* B,
+                   double* C, int nb, int kernel, cudaStream_t s);
+bool dmma_supported(int nb);
+
+// ---- element-wise / reductions ----
+void from_dense(const double* dense, int64_t n, int64_t ld, Mat& m, cudaStream_t s);
+void to_dense(const Mat& m, double* dense, int64_t ld, cudaStream_t s);
+void identity(Mat& m, cudaStream_t s);
+void add_scaled(double alpha, const Mat& a, double beta, const Mat& b, Mat& out,
+                cudaStream_t s);
+double trace(const Mat& m, cudaStream_t s);
+void gershgorin(const Mat& f, double* eps_min, double* eps_max, double* asym, cudaStream_t s);
+
+}  // namespace spamm

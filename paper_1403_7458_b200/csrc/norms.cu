@@ -1,0 +1,279 @@
+// K1: bit-exact Frobenius-norm pyramid + storage finalisation.
+//
+// Reference: QuadTreeMatrix._from_blocks, quadtree.py:170-194.
+//  * leaf norm^2 = np.einsum("tij,tij->t") (quadtree.py:186-187).  numpy (SSE2
+//    build baseline) evaluates it as two lanes (even / odd element), each an
+//    unfused acc += x*x walking 8-element chunks in pair order
+//    (6,7),(4,5),(2,3),(0,1), then lane0 + lane1.  Restated here with explicit
+//    __dmul_rn/__dadd_rn so nvcc cannot contract to FMA.
+//  * parents: reshape(h,2,h,2).sum(axis=(1,3)) == (c00 + c01) + (c10 + c11)
+//    in the squared domain (quadtree.py:191), sqrt per tier (quadtree.py:188,192).
+//  * blocks whose entries are all exactly zero are pruned (quadtree.py:177-180).
+// HBM roofline: S*Nb^2*8 bytes read per pass; K1.
+#include <mutex>
+
+#include "internal.h"
+
+namespace spamm {
+
+// ------------------------------------------------------------------ memory
+namespace {
+std::once_flag g_pool_once;
+void init_pool() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+}
+}  // namespace
+
+void* dmalloc_bytes(size_t bytes, cudaStream_t s) {
+  std::call_once(g_pool_once, init_pool);
+  if (bytes == 0) return nullptr;
+  void* p = nullptr;
+  SPAMM_CK(cudaMallocAsync(&p, bytes, s));
+  return p;
+}
+
+void dfree(void* p, cudaStream_t s) {
+  if (p) cudaFreeAsync(p, s);
+}
+
+void d2h_sync(int64_t* host, const int64_t* dev, int n, cudaStream_t s) {
+  static thread_local int64_t* pinned = nullptr;
+  if (!pinned) SPAMM_CK(cudaMallocHost(&pinned, 64 * sizeof(int64_t)));
+  SPAMM_CK(cudaMemcpyAsync(pinned, dev, n * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  SPAMM_CK(cudaStreamSynchronize(s));
+  for (int i = 0; i < n; ++i) host[i] = pinned[i];
+}
+
+void Mat::release() {
+  cudaStream_t s = stream;
+  dfree(data, s);
+  dfree(keys, s);
+  dfree(slot, s);
+  dfree(norms, s);
+  dfree(norms2, s);
+  data = nullptr;
+  keys = nullptr;
+  slot = nullptr;
+  norms = nullptr;
+  norms2 = nullptr;
+  nblocks = 0;
+}
+
+// ------------------------------------------------------------------ kernels
+namespace {
+
+__device__ __forceinline__ void sq_acc(double& l, double x) { l = __dadd_rn(l, __dmul_rn(x, x)); }
+
+// One thread per block; the two einsum lanes are independent chains (ILP 2).
+template <int NB2>
+__global__ void __launch_bounds__(128)
+    k_leaf_norms2(const double* __restrict__ data, int64_t m, int nb2_rt, double* __restrict__ out,
+                  uint8_t* __restrict__ nz) {
+  const int nb2 = NB2 ? NB2 : nb2_rt;
+  for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < m;
+       b += (int64_t)gridDim.x * blockDim.x) {
+    const double* x = data + b * nb2;
+    double l0 = 0.0, l1 = 0.0;
+    bool any = false;
+    int i = 0;
+    if (nb2 >= 8) {
+      const double2* x2 = reinterpret_cast<const double2*>(x);
+#pragma unroll 4
+      for (; nb2 - i >= 8; i += 8) {
+        const double2 v0 = __ldg(x2 + i / 2), v1 = __ldg(x2 + i / 2 + 1);
+        const double2 v2 = __ldg(x2 + i / 2 + 2), v3 = __ldg(x2 + i / 2 + 3);
+        sq_acc(l0, v3.x);
+        sq_acc(l1, v3.y);
+        sq_acc(l0, v2.x);
+        sq_acc(l1, v2.y);
+        sq_acc(l0, v1.x);
+        sq_acc(l1, v1.y);
+        sq_acc(l0, v0.x);
+        sq_acc(l1, v0.y);
+        any |= (v0.x != 0.0) | (v0.y != 0.0) | (v1.x != 0.0) | (v1.y != 0.0) | (v2.x != 0.0) |
+               (v2.y != 0.0) | (v3.x != 0.0) | (v3.y != 0.0);
+      }
+    }
+    for (; i < nb2; i += 2) {
+      const double a = x[i];
+      sq_acc(l0, a);
+      any |= a != 0.0;
+      if (i + 1 < nb2) {
+        const double c = x[i + 1];
+        sq_acc(l1, c);
+        any |= c != 0.0;
+      }
+    }
+    out[b] = __dadd_rn(l0, l1);
+    if (nz) nz[b] = any ? 1 : 0;
+  }
+}
+
+__global__ void k_scatter_leaf(const int64_t* __restrict__ keys, const double* __restrict__ n2,
+                               int64_t m, double* __restrict__ leaf2, double* __restrict__ leafn) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t k = keys[i];
+    const double v = n2[i];
+    leaf2[k] = v;
+    leafn[k] = __dsqrt_rn(v);
+  }
+}
+
+// Tier t from tier t+1 (both row-major), squared domain, then sqrt.
+__global__ void k_tier_up(const double* __restrict__ c2, double* __restrict__ p2,
+                          double* __restrict__ pn, int t) {
+  const int64_t w = int64_t(1) << t, W = 2 * w, n = w * w;
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < n;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = idx / w, j = idx % w;
+    const double* r0 = c2 + (2 * i) * W + 2 * j;
+    const double* r1 = r0 + W;
+    const double s = __dadd_rn(__dadd_rn(r0[0], r0[1]), __dadd_rn(r1[0], r1[1]));
+    p2[idx] = s;
+    pn[idx] = __dsqrt_rn(s);
+  }
+}
+
+// Tiers t_top..0 in one CTA (small tiers: <= 1024 parents).
+__global__ void k_tiers_small(double* __restrict__ norms2, double* __restrict__ norms, int t_top) {
+  for (int t = t_top; t >= 0; --t) {
+    const int64_t w = int64_t(1) << t, W = 2 * w, n = w * w;
+    const double* c2 = norms2 + tier_offset(t + 1);
+    double* p2 = norms2 + tier_offset(t);
+    double* pn = norms + tier_offset(t);
+    for (int64_t idx = threadIdx.x; idx < n; idx += blockDim.x) {
+      const int64_t i = idx / w, j = idx % w;
+      const double* r0 = c2 + (2 * i) * W + 2 * j;
+      const double* r1 = r0 + W;
+      const double s = __dadd_rn(__dadd_rn(r0[0], r0[1]), __dadd_rn(r1[0], r1[1]));
+      p2[idx] = s;
+      pn[idx] = __dsqrt_rn(s);
+    }
+    __syncthreads();
+  }
+}
+
+// Gather the kept blocks (nz[b] = 1) to their compacted positions.
+__global__ void k_compact_blocks(const double* __restrict__ din, const int64_t* __restrict__ kin,
+                                 const double* __restrict__ nin, const uint8_t* __restrict__ nz,
+                                 const int64_t* __restrict__ off, int64_t m, int nb2,
+                                 double* __restrict__ dout, int64_t* __restrict__ kout,
+                                 double* __restrict__ nout) {
+  for (int64_t b = blockIdx.x; b < m; b += gridDim.x) {
+    if (!nz[b]) continue;
+    const int64_t d = off[b];
+    for (int e = threadIdx.x; e < nb2; e += blockDim.x) dout[d * nb2 + e] = din[b * nb2 + e];
+    if (threadIdx.x == 0) {
+      kout[d] = kin[b];
+      nout[d] = nin[b];
+    }
+  }
+}
+
+__global__ void k_scatter_slots(const int64_t* __restrict__ keys, int64_t m, int32_t* __restrict__ slot) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m;
+       i += (int64_t)gridDim.x * blockDim.x)
+    slot[keys[i]] = (int32_t)i;
+}
+
+}  // namespace
+
+void leaf_norms2(const double* data, int64_t m, int nb, double* norms2, uint8_t* nonzero,
+                 cudaStream_t s) {
+  if (m <= 0) return;
+  const int nb2 = nb * nb;
+  const int threads = 128;
+  const int grid = grid_for(m, threads, 1LL << 20);
+  if (nb2 == 1024)
+    k_leaf_norms2<1024><<<grid, threads, 0, s>>>(data, m, nb2, norms2, nonzero);
+  else if (nb2 == 4096)
+    k_leaf_norms2<4096><<<grid, threads, 0, s>>>(data, m, nb2, norms2, nonzero);
+  else
+    k_leaf_norms2<0><<<grid, threads, 0, s>>>(data, m, nb2, norms2, nonzero);
+  SPAMM_LAUNCH_CK();
+}
+
+void build_pyramid(const int64_t* keys, const double* blk_norms2, int64_t m, int depth,
+                   double* norms, double* norms2, cudaStream_t s) {
+  const int64_t G = int64_t(1) << depth;
+  double* leaf2 = norms2 + tier_offset(depth);
+  double* leafn = norms + tier_offset(depth);
+  SPAMM_CK(cudaMemsetAsync(leaf2, 0, G * G * sizeof(double), s));
+  SPAMM_CK(cudaMemsetAsync(leafn, 0, G * G * sizeof(double), s));
+  if (m > 0) {
+    k_scatter_leaf<<<grid_for(m, 256), 256, 0, s>>>(keys, blk_norms2, m, leaf2, leafn);
+    SPAMM_LAUNCH_CK();
+  }
+  int t = depth - 1;
+  for (; t >= 0 && (int64_t(1) << (2 * t)) > 4096; --t) {
+    const int64_t n = int64_t(1) << (2 * t);
+    k_tier_up<<<grid_for(n, 256), 256, 0, s>>>(norms2 + tier_offset(t + 1), norms2 + tier_offset(t),
+                                                norms + tier_offset(t), t);
+    SPAMM_LAUNCH_CK();
+  }
+  if (t >= 0) {
+    k_tiers_small<<<1, 1024, 0, s>>>(norms2, norms, t);
+    SPAMM_LAUNCH_CK();
+  }
+}
+
+void scatter_slots(const int64_t* keys, int64_t m, int32_t* slot, cudaStream_t s) {
+  if (m <= 0) return;
+  k_scatter_slots<<<grid_for(m, 256), 256, 0, s>>>(keys, m, slot);
+  SPAMM_LAUNCH_CK();
+}
+
+void finalize(Mat& m, cudaStream_t s) {
+  m.stream = s;
+  const int nb2 = m.nb * m.nb;
+  double* n2 = nullptr;
+  if (m.nblocks > 0) {
+    n2 = dmalloc<double>(m.nblocks, s);
+    uint8_t* nz = dmalloc<uint8_t>(m.nblocks, s);
+    leaf_norms2(m.data, m.nblocks, m.nb, n2, nz, s);
+    int64_t* off = dmalloc<int64_t>(m.nblocks + 1, s);
+    scan_exclusive_u8(nz, m.nblocks, off, s);
+    int64_t kept = 0;
+    d2h_sync(&kept, off + m.nblocks, 1, s);
+    if (kept < m.nblocks) {
+      double* d2 = dmalloc<double>((size_t)kept * nb2, s);
+      int64_t* k2 = dmalloc<int64_t>(kept, s);
+      double* nn = dmalloc<double>(kept, s);
+      if (kept > 0) {
+        k_compact_blocks<<<grid_for(m.nblocks, 1, 148LL * 32), 128, 0, s>>>(
+            m.data, m.keys, n2, nz, off, m.nblocks, nb2, d2, k2, nn);
+        SPAMM_LAUNCH_CK();
+      }
+      dfree(m.data, s);
+      dfree(m.keys, s);
+      dfree(n2, s);
+      m.data = d2;
+      m.keys = k2;
+      n2 = nn;
+      m.nblocks = kept;
+    }
+    dfree(nz, s);
+    dfree(off, s);
+  }
+  m.G = int64_t(1) << m.depth;
+  m.slot = dmalloc<int32_t>(m.G * m.G, s);
+  SPAMM_CK(cudaMemsetAsync(m.slot, 0xFF, m.G * m.G * sizeof(int32_t), s));
+  if (m.nblocks > 0) {
+    k_scatter_slots<<<grid_for(m.nblocks, 256), 256, 0, s>>>(m.keys, m.nblocks, m.slot);
+    SPAMM_LAUNCH_CK();
+  }
+  const int64_t ps = pyramid_size(m.depth);
+  m.norms = dmalloc<double>(ps, s);
+  m.norms2 = dmalloc<double>(ps, s);
+  build_pyramid(m.keys, n2, m.nblocks, m.depth, m.norms, m.norms2, s);
+  dfree(n2, s);
+}
+
+}  // namespace spamm

@@ -1,0 +1,132 @@
+"""Seeded synthetic inputs for BASELINE.json's five configurations.
+
+The paper's FreeON water clusters are not available; BASELINE.json restates
+each workload as a generator, fixed here:
+
+* cfg1: A_ij = exp(-0.1 |i-j|) u_ij, u ~ U[-1, 1) symmetrised as
+  triu(u) + triu(u, 1).T (the reference's own recipe, matgen.py:481-482),
+  A from seed 0, B from seed 1, N = 1024, Nb = 32, tau = 1e-8.
+* cfg2-5 ("water-cluster-like"): n_mol molecule centres uniform in a cube
+  of edge (n_mol / 0.0334)^(1/3) Angstrom; 25 sites per molecule = centre +
+  N(0, 0.5^2) per axis; H_ij = 0.3 exp(-r_ij / 1.5) s_ij with s symmetric
+  U[-1, 1); diagonal N(-1, 0.2^2) for the first 5 sites of each molecule,
+  N(+1, 0.2^2) for the other 20; n_occ = 5 n_mol.  Molecules are ordered
+  along a 3-D Hilbert curve (order 10, Skilling's transpose construction --
+  the published algorithm the reference's ordering.py:66-105 also uses)
+  and rows move as 25-row runs.  One numpy PCG64 stream per seed, draws in
+  the order centres, jitter, s, diagonal.
+
+Host-side numpy; this is input preparation, not the hot path.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+__all__ = ["decay_pair", "water_cluster", "hilbert_keys_3d", "ConfigSpec", "CONFIGS"]
+
+
+def decay_pair(n: int = 1024, lam: float = 0.1, seeds=(0, 1)):
+    """cfg1 operands: exp(-lam |i-j|) * symmetrised U[-1, 1)."""
+    idx = np.arange(n)
+    env = np.exp(-lam * np.abs(idx[:, None] - idx[None, :]))
+    out = []
+    for s in seeds:
+        u = np.random.default_rng(s).uniform(-1.0, 1.0, size=(n, n))
+        u = np.triu(u) + np.triu(u, 1).T
+        out.append(env * u)
+    return out
+
+
+def hilbert_keys_3d(cells: np.ndarray, order: int) -> np.ndarray:
+    """Hilbert keys of integer lattice cells (n, 3) in [0, 2^order).
+
+    Skilling (2004) "Programming the Hilbert curve": axes -> transposed
+    Hilbert index (inverse undo of the reflect/exchange pass from the top bit,
+    then Gray encoding), then bit interleave axis 0 first.  Vectorised.
+    """
+    x = np.array(cells, dtype=np.int64, copy=True).reshape(-1, 3)
+    m = np.int64(1) << (order - 1)
+    q = m
+    while q > 1:
+        p = q - 1
+        for a in range(3):
+            hit = (x[:, a] & q) != 0
+            x[hit, 0] ^= p
+            miss = ~hit
+            t = (x[miss, 0] ^ x[miss, a]) & p
+            x[miss, 0] ^= t
+            x[miss, a] ^= t
+        q >>= 1
+    for a in (1, 2):
+        x[:, a] ^= x[:, a - 1]
+    t = np.zeros(len(x), dtype=np.int64)
+    q = m
+    while q > 1:
+        t[(x[:, 2] & q) != 0] ^= q - 1
+        q >>= 1
+    x ^= t[:, None]
+    key = np.zeros(len(x), dtype=np.int64)
+    for bit in range(order - 1, -1, -1):
+        for a in range(3):
+            key = (key << 1) | ((x[:, a] >> bit) & 1)
+    return key
+
+
+def _hilbert_molecule_order(centres: np.ndarray, order: int = 10) -> np.ndarray:
+    side = 1 << order
+    lo = centres.min(axis=0)
+    span = centres.max(axis=0) - lo
+    cells = np.zeros(centres.shape, dtype=np.int64)
+    for a in range(3):
+        if span[a] > 0:
+            cells[:, a] = np.clip(((centres[:, a] - lo[a]) / span[a] * side).astype(np.int64),
+                                  0, side - 1)
+    return np.argsort(hilbert_keys_3d(cells, order), kind="stable")
+
+
+def water_cluster(n_mol: int, seed: int = 0, density: float = 0.0334, sites: int = 25,
+                  occupied: int = 5, jitter: float = 0.5, amp: float = 0.3,
+                  decay: float = 1.5, diag_sigma: float = 0.2, hilbert: bool = True):
+    """cfg2-5 Hamiltonian.  Returns (H dense (n, n) float64, n_occ)."""
+    rng = np.random.default_rng(seed)
+    n = n_mol * sites
+    edge = (n_mol / density) ** (1.0 / 3.0)
+    centres = rng.uniform(0.0, edge, size=(n_mol, 3))
+    pos = np.repeat(centres, sites, axis=0) + rng.normal(0.0, jitter, size=(n, 3))
+    sq = np.einsum("ij,ij->i", pos, pos)
+    r2 = np.maximum(sq[:, None] + sq[None, :] - 2.0 * (pos @ pos.T), 0.0)
+    s = rng.uniform(-1.0, 1.0, size=(n, n))
+    s = np.triu(s) + np.triu(s, 1).T
+    h = amp * np.exp(-np.sqrt(r2) / decay) * s
+    h = np.triu(h) + np.triu(h, 1).T          # exact symmetry after the matmul-based r2
+    occ = np.tile(np.arange(sites) < occupied, n_mol)
+    d = np.where(occ, -1.0, 1.0) + rng.normal(0.0, diag_sigma, size=n)
+    np.fill_diagonal(h, d)
+    if hilbert:
+        perm = _hilbert_molecule_order(centres)
+        rows = (perm[:, None] * sites + np.arange(sites)[None, :]).reshape(-1)
+        h = h[np.ix_(rows, rows)]
+    return np.ascontiguousarray(h), n_mol * occupied
+
+
+@dataclass(frozen=True)
+class ConfigSpec:
+    index: int
+    name: str
+    n_mol: int            # 0 for cfg1
+    n: int
+    block_size: int
+    tau: float
+    workload: str         # "multiply" | "sp2"
+
+
+CONFIGS = {
+    1: ConfigSpec(1, "cfg1-decay-N1024-Nb32", 0, 1024, 32, 1e-8, "multiply"),
+    2: ConfigSpec(2, "cfg2-water30-N750-Nb32", 30, 750, 32, 1e-8, "multiply"),
+    3: ConfigSpec(3, "cfg3-water90-N2250-Nb32-sp2", 90, 2250, 32, 1e-7, "sp2"),
+    4: ConfigSpec(4, "cfg4-water150-N3750-Nb64-sp2", 150, 3750, 64, 1e-7, "sp2"),
+    5: ConfigSpec(5, "cfg5-water4096-N102400-Nb64", 4096, 102400, 64, 1e-8, "multiply"),
+}
