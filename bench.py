@@ -1,0 +1,342 @@
+#!/usr/bin/env python
+"""SpAMM / SP2 hot-path benchmark (one JSON line on rank 0).
+
+Workload (BASELINE.json configs[3], "cfg4"): SP2 purification of the
+150-molecule water-cluster-like Hamiltonian (N=3750 -> 4096, Nb=64, FP64,
+tau=1e-7, stop when ||X^2-X||_F < 1e-6).  One *step* = one complete SP2
+solve H -> P through the public API (Gershgorin bounds, X0, every SpAMM X^2,
+traces, EXPAND updates, idempotency tests), inputs resident in HBM.
+``value`` = surviving-leaf flops of all multiplies (ProductStats.flop_estimate,
+kernel.py:248) / device time, in GFLOP/s.  ``sp2_ms_per_iter`` is the
+second half of BASELINE's metric.
+
+``--impl reference`` times the reference algorithm's CPU implementation on
+the host cores: the oracle port (oracle/spamm_oracle.py + oracle/leafgemm.c,
+numba-equivalent i-k-j leaf kernel, all host threads), one SP2 iteration of
+the same workload per step (bounded sample).
+
+Multi-GPU (torchrun): every rank solves its own replica of the workload
+(weak scaling, no data-path collective); time is the max over ranks.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "SpAMM surviving-leaf GFLOP/s & SP2 time/iter at 1/2/4/8 B200; % FP64 roofline"
+UNIT = "GFLOP/s"
+L2_FLUSH_BYTES = 512 << 20
+
+
+def fp64_peak():
+    """Measured DMMA peak (tools/fp64_peak.cu -> profiles/fp64_peak_r01.json);
+    MEASURED_PEAKS.json has no FP64 entry."""
+    path = os.path.join(ROOT, "profiles", "fp64_peak_r01.json")
+    try:
+        with open(path) as f:
+            res = json.load(f)["results"]
+        best = max(r["tflops"] for r in res if r.get("op", "").startswith("dmma"))
+        return best, "measured DMMA peak, tools/fp64_peak.cu (profiles/fp64_peak_r01.json)"
+    except (OSError, KeyError, ValueError):
+        return 37.2, "nominal 148 SM x 128 flop/clk x 1.965 GHz (fallback)"
+
+
+def ncu_traffic():
+    """dram bytes per K4 launch from the committed ncu --set full summary, if any."""
+    path = os.path.join(ROOT, "profiles", "ncu_leaf_r01.json")
+    try:
+        with open(path) as f:
+            return json.load(f).get("dram_bytes_per_launch")
+    except (OSError, ValueError):
+        return None
+
+
+class ClockSampler:
+    """NVML SM clock + throttle reasons sampled during the timed region."""
+
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+               0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+               0x100: "display_clock_setting"}
+
+    def __init__(self, index: int):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+        except Exception:  # noqa: BLE001 - clocks are best-effort evidence
+            self._nv = None
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self._nv.nvmlDeviceGetClockInfo(self._h, self._nv.NVML_CLOCK_SM))
+                r = self._nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and bit != 0x1:
+                        self.reasons.add(name)
+            except Exception:  # noqa: BLE001
+                pass
+            self._stop.wait(0.02)
+
+    def __enter__(self):
+        if self._nv:
+            self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self._nv:
+            self._t.join()
+
+    def summary(self):
+        busy = [s for s in self.samples if s > 300] or self.samples
+        return {"sm_mhz": float(np.median(busy)) if busy else None, "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def workload(cfg_index: int):
+    from paper_1403_7458_b200.synth import CONFIGS, water_cluster
+    cfg = CONFIGS[cfg_index]
+    if cfg.workload != "sp2":
+        raise SystemExit(f"bench workload must be an SP2 config, got {cfg.name}")
+    h, n_occ = water_cluster(cfg.n_mol, seed=0)
+    return cfg, h, n_occ
+
+
+def config_dict(cfg, n_occ, args, extra=None):
+    d = {"workload": cfg.name, "N": cfg.n, "n_padded": 64 << 6 if cfg.block_size == 64 else None,
+         "block_size": cfg.block_size, "tau": cfg.tau, "n_occ": n_occ,
+         "criterion": "||X^2-X||_F<1e-6", "step": "one full SP2 solve H->P",
+         "l2": f"flushed between steps ({L2_FLUSH_BYTES >> 20} MiB write)",
+         "parallelism": f"replicas x{args.gpus}", "inputs": "synthetic, seed 0 (synth.py)"}
+    from paper_1403_7458_b200.quadtree import _padded_geometry
+    d["n_padded"] = _padded_geometry(cfg.n, cfg.block_size)[0]
+    if extra:
+        d.update(extra)
+    return d
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1403_7458_b200 as sp
+    from paper_1403_7458_b200 import _native as nat
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    lib = nat.load()
+    cfg, h, n_occ = workload(args.config)
+    crit = dict(criterion="fro", fro_tol=1e-6)
+
+    h_dev = torch.from_numpy(h).cuda()
+    f = sp.build_from_dense(h_dev, cfg.block_size)
+    flush = torch.empty(L2_FLUSH_BYTES // 8, dtype=torch.float64, device="cuda")
+    stream = torch.cuda.current_stream()
+
+    def step():
+        p, st = sp.sp2_solve(f, n_occ, cfg.tau, timed=True, **crit)
+        return p, st
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    flops = 0
+    leaf_ms = 0.0
+    leaf_launches = 0
+    n_mult = 0
+    iters = []
+    dev_ms = 0.0
+    l0 = lib.spamm_launch_count()
+    with ClockSampler(local) as clocks:
+        for _ in range(args.steps):
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            p, st = step()
+            e1.record(stream)
+            e1.synchronize()
+            dev_ms += e0.elapsed_time(e1)
+            print(f"[bench] rank {rank} step {e0.elapsed_time(e1):.2f} ms "
+                  f"leaf {st.ms_leaf:.2f} ms iters {st.iteration}", file=sys.stderr, flush=True)
+            flops += st.flops
+            leaf_ms += st.ms_leaf
+            n_mult += len(st.product_stats)
+            leaf_launches += sum(1 for s in st.product_stats if s.leaf_products > 0)
+            iters.append(st.iteration)
+    launches = lib.spamm_launch_count() - l0
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+
+    # end to end: pinned host H -> device -> public API -> P back to pinned host
+    h_pin = torch.from_numpy(h).pin_memory()
+    p_pin = torch.empty((cfg.n, cfg.n), dtype=torch.float64).pin_memory()
+
+    def e2e_step():
+        hd = h_pin.to("cuda", non_blocking=True)
+        ff = sp.build_from_dense(hd, cfg.block_size)
+        pp, st = sp.sp2_solve(ff, n_occ, cfg.tau, **crit)
+        p_pin.copy_(sp.to_dense_device(pp), non_blocking=True)
+        return st
+
+    e2e_step()
+    torch.cuda.synchronize()
+    e2e_ms = 0.0
+    e2e_flops = 0
+    for _ in range(args.steps):
+        flush.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        st = e2e_step()
+        e1.record(stream)
+        e1.synchronize()
+        e2e_ms += e0.elapsed_time(e1)
+        e2e_flops += st.flops
+
+    tmax = dev_ms
+    e2e_max = e2e_ms
+    if ws > 1:
+        t = torch.tensor([dev_ms, e2e_ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tmax, e2e_max = float(t[0]), float(t[1])
+        fl = torch.tensor([flops, e2e_flops], dtype=torch.float64, device="cuda")
+        dist.all_reduce(fl, op=dist.ReduceOp.SUM)
+        flops_all, e2e_flops_all = float(fl[0]), float(fl[1])
+    else:
+        flops_all, e2e_flops_all = float(flops), float(e2e_flops)
+
+    if rank == 0:
+        peak, peak_src = fp64_peak()
+        achieved = flops / (leaf_ms * 1e-3) / 1e12 if leaf_ms > 0 else 0.0
+        out = {
+            "metric": METRIC, "value": flops_all / (tmax * 1e-3) / 1e9, "unit": UNIT,
+            "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": tmax / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": config_dict(cfg, n_occ, args),
+            "sp2_ms_per_iter": tmax / max(n_mult, 1),
+            "sp2_iterations": iters[0] if iters else None,
+            "multiplies_per_step": n_mult // max(args.steps, 1),
+            "leaf_flops_per_step": flops // max(args.steps, 1),
+            "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                         "frac": achieved / peak, "traffic": ncu_traffic(),
+                         "kernel": "k_leaf_dmma<64,2,2,3> (K4 leaf products)",
+                         "peak_source": peak_src,
+                         "algorithmic": "leaf_products*2*Nb^3 flops per launch"},
+            "e2e": {"value": e2e_flops_all / (e2e_max * 1e-3) / 1e9, "unit": UNIT,
+                    "h2d_bytes_per_step": int(h.nbytes), "d2h_bytes_per_step": int(h.nbytes)},
+            "gpu_launches": int(launches),
+            "clocks": clocks.summary(),
+        }
+        if ws == 1 and not args.no_cpu_baseline:
+            out["cpu_baseline"] = cpu_baseline(cfg, h, n_occ, sample_multiplies=1)
+        print(json.dumps(out), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+
+
+def _oracle_x0(cfg, h):
+    from oracle import spamm_oracle as O
+    O.self_check_numpy()
+    f = O.from_dense(h, cfg.block_size)
+    return O, O.sp2_init(f, O.gershgorin_bounds(f))
+
+
+def cpu_baseline(cfg, h, n_occ, sample_multiplies=1):
+    """Oracle port on the host cores: SP2 iterations from X0 (bounded sample)."""
+    threads = os.cpu_count() or 1
+    O, x0 = _oracle_x0(cfg, h)
+    O.multiply(x0, x0, cfg.tau, threads)  # warm the C library / page cache
+    flops = 0
+    t0 = time.perf_counter()
+    x = x0
+    for _ in range(sample_multiplies):
+        x, _, _, _, stats, _ = O.sp2_step(x, n_occ, cfg.tau, threads)
+        flops += stats["flop_estimate"]
+    dt = time.perf_counter() - t0
+    return {"value": flops / dt / 1e9, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"{sample_multiplies} SP2 iteration(s) of {cfg.name} from X0 "
+                      f"({flops:.3e} leaf flops, {dt:.2f} s), oracle/leafgemm.c i-k-j unfused, "
+                      f"{threads} threads"}
+
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    cfg, h, n_occ = workload(args.config)
+    threads = os.cpu_count() or 1
+    O, x0 = _oracle_x0(cfg, h)
+    for _ in range(args.warmup):
+        O.sp2_step(x0, n_occ, cfg.tau, threads)
+    flops = 0
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        _, _, _, _, stats, _ = O.sp2_step(x0, n_occ, cfg.tau, threads)
+        flops += stats["flop_estimate"]
+    dt = time.perf_counter() - t0
+    value = flops / dt / 1e9
+    sample = (f"one SP2 iteration (X0^2 SpAMM + traces + update) of {cfg.name} per step, "
+              f"oracle port on {threads} host threads")
+    out = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": dt * 1e3 / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config_dict(cfg, n_occ, args, {"step": "one SP2 iteration from X0"}),
+        "sp2_ms_per_iter": dt * 1e3 / args.steps, "impl": "reference",
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--config", type=int, default=4)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -71,6 +71,8 @@ typedef struct {
 
 int spamm_abi_version(void);
 const char* spamm_last_error(void);
+/* Number of kernels this library has launched in the process (evidence counter). */
+int64_t spamm_launch_count(void);
 
 /* build_from_dense (quadtree.py:208-242).  dense: device, n x n row-major
  * with leading dimension ld.  Pads to Nb * 2^d, keeps non-zero blocks. */

@@ -46,6 +46,7 @@ class Stats(ctypes.Structure):
 _SIGS = {
     "spamm_abi_version": (c_i32, []),
     "spamm_last_error": (ctypes.c_char_p, []),
+    "spamm_launch_count": (c_i64, []),
     "spamm_mat_from_dense": (c_i32, [c_vp, c_i64, c_i64, c_i32, c_i64, c_vp, ctypes.POINTER(c_vp)]),
     "spamm_mat_from_blocks": (c_i32, [c_i64, c_i32, c_i64, c_i32, c_vp, c_vp, c_i64, c_vp,
                                       ctypes.POINTER(c_vp)]),

@@ -16,6 +16,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
 #include <cstdio>
 #include <stdexcept>
 #include <string>
@@ -34,7 +35,14 @@ struct CudaError : std::runtime_error {
                                " at " + __FILE__ + ":" + std::to_string(__LINE__));      \
   } while (0)
 
-#define SPAMM_LAUNCH_CK() SPAMM_CK(cudaGetLastError())
+// Every kernel launch of the library goes through this check, which also
+// counts launches (spamm_launch_count(): evidence for bench.py's gpu_launches).
+extern std::atomic<long long> g_launch_count;
+#define SPAMM_LAUNCH_CK()                                          \
+  do {                                                             \
+    SPAMM_CK(cudaGetLastError());                                  \
+    ::spamm::g_launch_count.fetch_add(1, std::memory_order_relaxed); \
+  } while (0)
 
 __host__ __device__ inline int64_t tier_offset(int t) { return ((int64_t(1) << (2 * t)) - 1) / 3; }
 __host__ __device__ inline int64_t pyramid_size(int depth) { return tier_offset(depth + 1); }
