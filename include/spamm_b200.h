@@ -36,6 +36,7 @@ extern "C" {
 #define SPAMM_LEAF_AUTO 0  /* DMMA for Nb in {8,16,32,64}, else exact        */
 #define SPAMM_LEAF_DMMA 1  /* FP64 tensor cores (mma.sync f64 -> DMMA)       */
 #define SPAMM_LEAF_EXACT 2 /* CUDA-core, reference order: bitwise identical  */
+#define SPAMM_LEAF_DMMA_CPASYNC 3 /* first-generation DMMA kernel (A/B tests)  */
 
 typedef struct spamm_mat spamm_mat;
 
@@ -107,10 +108,12 @@ int spamm_tasks(const spamm_mat* a, const spamm_mat* b, double tau, int32_t* ti,
 /* The compiled seam _gemm_batch(a_pos, b_pos, c_pos, a_data, b_data, c_data)
  * (kernel.py:74-77): c_data[c_pos[t]] += a_data[a_pos[t]] @ b_data[b_pos[t]]
  * for t in order.  Tasks of one C block must be contiguous (sorted by C);
- * all arrays are device pointers; int64 positions as in the reference. */
+ * all arrays are device pointers; int64 positions as in the reference;
+ * a_blocks / b_blocks = leading extents of a_data / b_data (array shapes). */
 int spamm_gemm_batch(const int64_t* a_pos, const int64_t* b_pos, const int64_t* c_pos,
-                     int64_t n_tasks, const double* a_data, const double* b_data, double* c_data,
-                     int32_t block_size, int32_t kernel, void* stream);
+                     int64_t n_tasks, const double* a_data, int64_t a_blocks, const double* b_data,
+                     int64_t b_blocks, double* c_data, int32_t block_size, int32_t kernel,
+                     void* stream);
 
 /* add_scaled (quadtree.py:281-293). */
 int spamm_add_scaled(double alpha, const spamm_mat* a, double beta, const spamm_mat* b,

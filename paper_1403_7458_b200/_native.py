@@ -18,7 +18,7 @@ SPAMM_EINVAL = 1
 SPAMM_ECUDA = 2
 MAX_TIERS = 64
 
-LEAF_KERNELS = {"auto": 0, "dmma": 1, "exact": 2}
+LEAF_KERNELS = {"auto": 0, "dmma": 1, "exact": 2, "dmma_cpasync": 3}
 
 c_i32 = ctypes.c_int32
 c_i64 = ctypes.c_int64
@@ -58,7 +58,8 @@ _SIGS = {
                                ctypes.POINTER(Stats)]),
     "spamm_census": (c_i32, [c_vp, c_vp, c_f64, c_vp, ctypes.POINTER(Stats)]),
     "spamm_tasks": (c_i32, [c_vp, c_vp, c_f64, c_vp, c_vp, c_vp, c_i64, ctypes.POINTER(c_i64), c_vp]),
-    "spamm_gemm_batch": (c_i32, [c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_i32, c_i32, c_vp]),
+    "spamm_gemm_batch": (c_i32, [c_vp, c_vp, c_vp, c_i64, c_vp, c_i64, c_vp, c_i64, c_vp, c_i32, c_i32,
+                                 c_vp]),
     "spamm_add_scaled": (c_i32, [c_f64, c_vp, c_f64, c_vp, c_vp, ctypes.POINTER(c_vp)]),
     "spamm_trace": (c_i32, [c_vp, c_vp, ctypes.POINTER(c_f64)]),
     "spamm_gershgorin": (c_i32, [c_vp, c_vp, ctypes.POINTER(c_f64), ctypes.POINTER(c_f64),

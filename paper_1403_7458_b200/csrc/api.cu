@@ -261,8 +261,8 @@ int spamm_multiply(const spamm_mat* a, const spamm_mat* b, double tau, int32_t k
   if (int rc = check_conformable(a, b)) return rc;
   if (!(tau >= 0.0) || tau == __builtin_inf())
     return fail(SPAMM_EINVAL, "tau must be finite and >= 0, got " + std::to_string(tau));
-  if (kernel < 0 || kernel > 2) return fail(SPAMM_EINVAL, "unknown leaf kernel");
-  if (kernel == SPAMM_LEAF_DMMA && !spamm::dmma_supported(a->m.nb))
+  if (kernel < 0 || kernel > 3) return fail(SPAMM_EINVAL, "unknown leaf kernel");
+  if ((kernel == SPAMM_LEAF_DMMA || kernel == 3) && !spamm::dmma_supported(a->m.nb))
     return fail(SPAMM_EINVAL, "DMMA leaf kernel needs block size 8, 16, 32 or 64");
   if (!c) return fail(SPAMM_EINVAL, "null output handle");
   SPAMM_API_BEGIN
@@ -286,7 +286,7 @@ int spamm_multiply(const spamm_mat* a, const spamm_mat* b, double tau, int32_t k
   tm.mark(1);  // leaf window = the K4 launch only (allocation stays outside)
   if (r.n_c > 0) {
     spamm::leaf_products<int32_t>(r.n_c, r.seg, r.a_idx, r.b_idx, nullptr, false, a->m.data,
-                                  b->m.data, C.data, C.nb, kernel, s);
+                                  a->m.nblocks, b->m.data, b->m.nblocks, C.data, C.nb, kernel, s);
   }
   tm.mark(2);
   if (r.n_c > 0) {
@@ -341,12 +341,13 @@ int spamm_tasks(const spamm_mat* a, const spamm_mat* b, double tau, int32_t* ti,
 }
 
 int spamm_gemm_batch(const int64_t* a_pos, const int64_t* b_pos, const int64_t* c_pos,
-                     int64_t n_tasks, const double* a_data, const double* b_data, double* c_data,
-                     int32_t block_size, int32_t kernel, void* stream) {
+                     int64_t n_tasks, const double* a_data, int64_t a_blocks, const double* b_data,
+                     int64_t b_blocks, double* c_data, int32_t block_size, int32_t kernel,
+                     void* stream) {
   if (n_tasks < 0) return fail(SPAMM_EINVAL, "negative task count");
   if (block_size < 1) return fail(SPAMM_EINVAL, "block size must be >= 1");
-  if (kernel < 0 || kernel > 2) return fail(SPAMM_EINVAL, "unknown leaf kernel");
-  if (kernel == SPAMM_LEAF_DMMA && !spamm::dmma_supported(block_size))
+  if (kernel < 0 || kernel > 3) return fail(SPAMM_EINVAL, "unknown leaf kernel");
+  if ((kernel == SPAMM_LEAF_DMMA || kernel == 3) && !spamm::dmma_supported(block_size))
     return fail(SPAMM_EINVAL, "DMMA leaf kernel needs block size 8, 16, 32 or 64");
   if (n_tasks == 0) return SPAMM_OK;
   SPAMM_API_BEGIN
@@ -363,8 +364,8 @@ int spamm_gemm_batch(const int64_t* a_pos, const int64_t* b_pos, const int64_t* 
   k_seg_build<<<spamm::grid_for(n_tasks, 256), 256, 0, s>>>(c_pos, flags, off, n_tasks, seg, c_out,
                                                              nseg);
   SPAMM_LAUNCH_CK();
-  spamm::leaf_products<int64_t>(nseg, seg, a_pos, b_pos, c_out, true, a_data, b_data, c_data,
-                                block_size, kernel, s);
+  spamm::leaf_products<int64_t>(nseg, seg, a_pos, b_pos, c_out, true, a_data, a_blocks, b_data,
+                                b_blocks, c_data, block_size, kernel, s);
   spamm::dfree(flags, s);
   spamm::dfree(off, s);
   spamm::dfree(seg, s);

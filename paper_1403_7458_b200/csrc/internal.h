@@ -74,13 +74,23 @@ void cull(const Mat& a, const Mat& b, double tau, bool want_tasks, CullResult& r
           cudaStream_t s);
 
 // ---- leaf products ----
-enum LeafKernel { LEAF_AUTO = 0, LEAF_DMMA = 1, LEAF_EXACT = 2 };
+// LEAF_DMMA_CPASYNC: the first-generation DMMA kernel (cp.async ring, one CTA
+// per C block), kept for A/B measurements; AUTO/DMMA use the TMA kernel for
+// Nb in {32, 64}.
+enum LeafKernel { LEAF_AUTO = 0, LEAF_DMMA = 1, LEAF_EXACT = 2, LEAF_DMMA_CPASYNC = 3 };
 // For each segment m: C[c_out ? c_out[m] : m] (+)= sum_{t in seg m} A[a_idx[t]] * B[b_idx[t]]
+// a_blocks / b_blocks: number of blocks addressable in A / B (TMA bounds).
 template <class Idx>
 void leaf_products(int64_t n_seg, const int64_t* seg, const Idx* a_idx, const Idx* b_idx,
-                   const int64_t* c_out, bool accumulate, const double* A, const double* B,
-                   double* C, int nb, int kernel, cudaStream_t s);
+                   const int64_t* c_out, bool accumulate, const double* A, int64_t a_blocks,
+                   const double* B, int64_t b_blocks, double* C, int nb, int kernel,
+                   cudaStream_t s);
 bool dmma_supported(int nb);
+bool tma_leaf_supported(int nb);
+template <class Idx>
+void leaf_products_tma(int64_t n_seg, const int64_t* seg, const Idx* a_idx, const Idx* b_idx,
+                       const int64_t* c_out, bool accumulate, const double* A, int64_t a_blocks,
+                       const double* B, int64_t b_blocks, double* C, int nb, cudaStream_t s);
 
 // ---- element-wise / reductions ----
 void from_dense(const double* dense, int64_t n, int64_t ld, Mat& m, cudaStream_t s);

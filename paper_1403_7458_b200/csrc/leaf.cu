@@ -222,12 +222,18 @@ bool dmma_supported(int nb) { return nb == 8 || nb == 16 || nb == 32 || nb == 64
 
 template <class Idx>
 void leaf_products(int64_t n_seg, const int64_t* seg, const Idx* a_idx, const Idx* b_idx,
-                   const int64_t* c_out, bool accumulate, const double* A, const double* B,
-                   double* C, int nb, int kernel, cudaStream_t s) {
+                   const int64_t* c_out, bool accumulate, const double* A, int64_t a_blocks,
+                   const double* B, int64_t b_blocks, double* C, int nb, int kernel,
+                   cudaStream_t s) {
   if (n_seg <= 0) return;
   if (n_seg > 0x7fffffffLL) throw CudaError("too many C blocks for one launch");
+  if ((kernel == LEAF_AUTO || kernel == LEAF_DMMA) && tma_leaf_supported(nb)) {
+    leaf_products_tma<Idx>(n_seg, seg, a_idx, b_idx, c_out, accumulate, A, a_blocks, B, b_blocks,
+                           C, nb, s);
+    return;
+  }
   const bool dmma = kernel != LEAF_EXACT && dmma_supported(nb);
-  if (kernel == LEAF_DMMA && !dmma_supported(nb))
+  if ((kernel == LEAF_DMMA || kernel == LEAF_DMMA_CPASYNC) && !dmma_supported(nb))
     throw CudaError("DMMA leaf kernel needs block size 8, 16, 32 or 64");
   if (dmma) {
     switch (nb) {
@@ -264,10 +270,10 @@ void leaf_products(int64_t n_seg, const int64_t* seg, const Idx* a_idx, const Id
 }
 
 template void leaf_products<int32_t>(int64_t, const int64_t*, const int32_t*, const int32_t*,
-                                     const int64_t*, bool, const double*, const double*, double*,
-                                     int, int, cudaStream_t);
+                                     const int64_t*, bool, const double*, int64_t, const double*,
+                                     int64_t, double*, int, int, cudaStream_t);
 template void leaf_products<int64_t>(int64_t, const int64_t*, const int64_t*, const int64_t*,
-                                     const int64_t*, bool, const double*, const double*, double*,
-                                     int, int, cudaStream_t);
+                                     const int64_t*, bool, const double*, int64_t, const double*,
+                                     int64_t, double*, int, int, cudaStream_t);
 
 }  // namespace spamm

@@ -1,0 +1,302 @@
+// K4 (Nb = 32 / 64): persistent, warp-specialised FP64-DMMA leaf products.
+//
+// Reference: _gemm_acc / _gemm_batch (kernel.py:64-77).  Same contract as
+// leaf.cu: segment m (tasks of one C block, k ascending) is reduced by ONE
+// CTA in registers, in task order -> deterministic, no atomics.
+//
+// B200 mapping
+//  * one producer warp: a single lane issues TMA tiled loads
+//    (cp.async.bulk.tensor.2d, SWIZZLE_128B, box 16 x Nb doubles) of the
+//    A_ik / B_kj leaf blocks into a STAGES-deep smem ring, completion through
+//    mbarrier transaction counts (full[]), slot reuse through empty[];
+//  * CONSUMERS warps: FP64 tensor cores via mma.sync.m8n8k4.f64 (DMMA; sm_100a
+//    has no f64 tcgen05 kind), fragments read from the swizzled tiles,
+//    accumulators in registers; the epilogue of C block m overlaps the TMA
+//    loads of block m + grid;
+//  * persistent grid (min(#segments, SMs x CTAs/SM)), static round-robin over
+//    the Morton-ordered C blocks.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <mutex>
+
+#include "internal.h"
+
+namespace spamm {
+
+namespace {
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  uint32_t ok = 0;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity)
+        : "memory");
+  } while (!ok);
+}
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, uint32_t bar,
+                                            int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];\n" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void dmma884(double (&c)[2], double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(c[0]), "+d"(c[1])
+      : "d"(a), "d"(b));
+}
+__device__ __forceinline__ double lds64(uint32_t addr) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];\n" : "=d"(v) : "r"(addr));
+  return v;
+}
+
+template <int NB, int WARPS_M, int WARPS_N, int STAGES>
+struct TmaCfg {
+  static constexpr int CONSUMERS = WARPS_M * WARPS_N;
+  static constexpr int THREADS = 32 * (CONSUMERS + 1);
+  static constexpr int SLAB = NB * 128;              // bytes of one 16-column slab
+  static constexpr int TILE = NB * NB * 8;           // bytes of one leaf block
+  static constexpr int STAGE = 2 * TILE;             // A + B
+  static constexpr size_t SMEM = (size_t)STAGES * STAGE + 1024 + 2 * STAGES * 8 + 64;
+};
+
+// Byte offset of element (r, c) inside a swizzled tile: 16-column slabs of
+// NB rows x 128 B, 16-byte chunk index XOR (r mod 8) (TMA SWIZZLE_128B).
+template <int NB>
+__host__ __device__ constexpr int swz(int r, int c) {
+  return (c >> 4) * (NB * 128) + r * 128 + ((((c & 15) >> 1) ^ (r & 7)) << 4) + ((c & 1) << 3);
+}
+
+template <int NB, int WARPS_M, int WARPS_N, int STAGES, class Idx>
+__global__ void __launch_bounds__(32 * (WARPS_M * WARPS_N + 1), 1)
+    k_leaf_dmma_tma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                    int64_t n_seg, const int64_t* __restrict__ seg, const Idx* __restrict__ a_idx,
+                    const Idx* __restrict__ b_idx, const int64_t* __restrict__ c_out,
+                    int accumulate, double* __restrict__ C) {
+  using Cfg = TmaCfg<NB, WARPS_M, WARPS_N, STAGES>;
+  constexpr int WTM = NB / WARPS_M, WTN = NB / WARPS_N, MT = WTM / 8, NT = WTN / 8;
+  static_assert(WTN % 8 == 0 && WTM % 8 == 0, "warp tile must be a multiple of 8");
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = smem_u32(smem_raw);
+  const uint32_t base = (raw + 1023u) & ~1023u;  // SWIZZLE_128B needs 1024-B alignment
+  const uint32_t bars = base + STAGES * Cfg::STAGE;
+  auto full = [&](int s) { return bars + 8u * s; };
+  auto empty = [&](int s) { return bars + 8u * (STAGES + s); };
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(full(s), 1);
+      mbar_init(empty(s), Cfg::CONSUMERS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == Cfg::CONSUMERS) {
+    // ---------------- producer warp ----------------
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+      asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int64_t m = blockIdx.x; m < n_seg; m += gridDim.x) {
+        const int64_t t1 = seg[m + 1];
+        for (int64_t t = seg[m]; t < t1; ++t) {
+          mbar_wait(empty(stage), phase ^ 1u);
+          mbar_expect_tx(full(stage), Cfg::STAGE);
+          const int ra = (int)a_idx[t] * NB, rb = (int)b_idx[t] * NB;
+          const uint32_t sa = base + stage * Cfg::STAGE, sb = sa + Cfg::TILE;
+#pragma unroll
+          for (int sl = 0; sl < NB / 16; ++sl) {
+            tma_load_2d(sa + sl * Cfg::SLAB, &tmA, full(stage), sl * 16, ra);
+            tma_load_2d(sb + sl * Cfg::SLAB, &tmB, full(stage), sl * 16, rb);
+          }
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1u;
+          }
+        }
+      }
+    }
+    return;
+  }
+
+  // ---------------- consumer warps ----------------
+  const int wm = warp / WARPS_N, wn = warp % WARPS_N;
+  const int r8 = lane >> 2, c4 = lane & 3;
+  const int row0 = wm * WTM, col0 = wn * WTN;
+  // Lane-constant swizzle offsets (see swz): A by (kk & 15) >> 2, B by (half, kk & 4).
+  uint32_t offA[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+    offA[q] = (uint32_t)((((2 * q + (c4 >> 1)) ^ r8) << 4) + ((c4 & 1) << 3) + r8 * 128);
+  uint32_t offB[2][2];
+#pragma unroll
+  for (int h = 0; h < 2; ++h)
+#pragma unroll
+    for (int g = 0; g < 2; ++g)
+      offB[h][g] = (uint32_t)((((h * 4 + (r8 >> 1)) ^ (g * 4 + c4)) << 4) + ((r8 & 1) << 3) + c4 * 128);
+
+  int stage = 0;
+  uint32_t phase = 0;
+  for (int64_t m = blockIdx.x; m < n_seg; m += gridDim.x) {
+    double* Cb = C + (c_out ? c_out[m] : m) * (int64_t)(NB * NB);
+    double acc[MT][NT][2];
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        if (accumulate) {
+          const double2 v = *reinterpret_cast<const double2*>(
+              Cb + (row0 + mt * 8 + r8) * NB + col0 + nt * 8 + 2 * c4);
+          acc[mt][nt][0] = v.x;
+          acc[mt][nt][1] = v.y;
+        } else {
+          acc[mt][nt][0] = 0.0;
+          acc[mt][nt][1] = 0.0;
+        }
+      }
+    const int64_t t1 = seg[m + 1];
+    for (int64_t t = seg[m]; t < t1; ++t) {
+      mbar_wait(full(stage), phase);
+      const uint32_t sa = base + stage * Cfg::STAGE, sb = sa + Cfg::TILE;
+#pragma unroll
+      for (int kk = 0; kk < NB; kk += 4) {
+        double af[MT], bf[NT];
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt)
+          af[mt] = lds64(sa + (kk >> 4) * Cfg::SLAB + (row0 + mt * 8) * 128 + offA[(kk >> 2) & 3]);
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          const int cb = col0 + nt * 8;
+          bf[nt] = lds64(sb + (cb >> 4) * Cfg::SLAB + kk * 128 + offB[(cb >> 3) & 1][(kk >> 2) & 1]);
+        }
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) dmma884(acc[mt][nt], af[mt], bf[nt]);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty(stage));
+      if (++stage == STAGES) {
+        stage = 0;
+        phase ^= 1u;
+      }
+    }
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        double2 v;
+        v.x = acc[mt][nt][0];
+        v.y = acc[mt][nt][1];
+        *reinterpret_cast<double2*>(Cb + (row0 + mt * 8 + r8) * NB + col0 + nt * 8 + 2 * c4) = v;
+      }
+  }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  if (!fn) throw CudaError("cuTensorMapEncodeTiled unavailable");
+  return fn;
+}
+
+CUtensorMap make_map(const double* data, int64_t nblocks, int nb) {
+  CUtensorMap m;
+  const int64_t rows = nblocks > 0 ? nblocks * nb : nb;
+  cuuint64_t dims[2] = {(cuuint64_t)nb, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)nb * sizeof(double)};
+  cuuint32_t box[2] = {16, (cuuint32_t)nb};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(data), dims,
+                           strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+  return m;
+}
+
+int sm_count() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    SPAMM_CK(cudaGetDevice(&dev));
+    SPAMM_CK(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
+  }
+  return n;
+}
+
+template <int NB, int WM, int WN, int ST, int CTAS_PER_SM, class Idx>
+void launch_tma(int64_t n_seg, const int64_t* seg, const Idx* a_idx, const Idx* b_idx,
+                const int64_t* c_out, bool acc, const double* A, int64_t a_blocks, const double* B,
+                int64_t b_blocks, double* C, cudaStream_t s) {
+  using Cfg = TmaCfg<NB, WM, WN, ST>;
+  auto kern = k_leaf_dmma_tma<NB, WM, WN, ST, Idx>;
+  static std::once_flag once;
+  std::call_once(once, [&] {
+    SPAMM_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM));
+  });
+  const CUtensorMap ta = make_map(A, a_blocks, NB), tb = make_map(B, b_blocks, NB);
+  int64_t grid = (int64_t)sm_count() * CTAS_PER_SM;
+  if (grid > n_seg) grid = n_seg;
+  kern<<<(unsigned)grid, Cfg::THREADS, Cfg::SMEM, s>>>(ta, tb, n_seg, seg, a_idx, b_idx, c_out,
+                                                       acc ? 1 : 0, C);
+  SPAMM_LAUNCH_CK();
+}
+
+}  // namespace
+
+bool tma_leaf_supported(int nb) { return nb == 32 || nb == 64; }
+
+template <class Idx>
+void leaf_products_tma(int64_t n_seg, const int64_t* seg, const Idx* a_idx, const Idx* b_idx,
+                       const int64_t* c_out, bool accumulate, const double* A, int64_t a_blocks,
+                       const double* B, int64_t b_blocks, double* C, int nb, cudaStream_t s) {
+  if (n_seg <= 0) return;
+  if (nb == 64)
+    launch_tma<64, 2, 4, 3, 1, Idx>(n_seg, seg, a_idx, b_idx, c_out, accumulate, A, a_blocks, B,
+                                    b_blocks, C, s);
+  else if (nb == 32)
+    launch_tma<32, 2, 2, 6, 2, Idx>(n_seg, seg, a_idx, b_idx, c_out, accumulate, A, a_blocks, B,
+                                    b_blocks, C, s);
+  else
+    throw CudaError("TMA leaf kernel needs block size 32 or 64");
+}
+
+template void leaf_products_tma<int32_t>(int64_t, const int64_t*, const int32_t*, const int32_t*,
+                                         const int64_t*, bool, const double*, int64_t,
+                                         const double*, int64_t, double*, int, cudaStream_t);
+template void leaf_products_tma<int64_t>(int64_t, const int64_t*, const int64_t*, const int64_t*,
+                                         const int64_t*, bool, const double*, int64_t,
+                                         const double*, int64_t, double*, int, cudaStream_t);
+
+}  // namespace spamm

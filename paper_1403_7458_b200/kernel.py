@@ -181,7 +181,8 @@ def gemm_batch(a_pos, b_pos, c_pos, a_data, b_data, c_data, kernel: str = "auto"
     if not (b_pos.numel() == c_pos.numel() == n):
         raise ValueError("position arrays must have equal length")
     nat.check(nat.load().spamm_gemm_batch(a_pos.data_ptr(), b_pos.data_ptr(), c_pos.data_ptr(),
-                                          n, a_data.data_ptr(), b_data.data_ptr(),
+                                          n, a_data.data_ptr(), int(a_data.shape[0]),
+                                          b_data.data_ptr(), int(b_data.shape[0]),
                                           c_data.data_ptr(), nb, _leaf_kernel(kernel),
                                           nat.current_stream()))
 
