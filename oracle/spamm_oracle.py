@@ -96,6 +96,27 @@ def self_check_numpy() -> None:
                                "on this numpy build")
 
 
+def contig_sum_recipe(x: np.ndarray) -> float:
+    """einsum's sum_of_arr for a contiguous run (used by trace when Nb = 1: the
+    (t,1,1) diagonal coalesces to one contiguous vector): two lanes, per
+    8-element chunk ((x0+x2)+(x4+x6)) added to lane 0 (odd elements to lane 1),
+    tail two at a time, then lane0 + lane1."""
+    x = np.asarray(x, dtype=np.float64)
+    n = len(x)
+    l0 = l1 = 0.0
+    i = 0
+    while n - i >= 8:
+        l0 = ((float(x[i]) + float(x[i + 2])) + (float(x[i + 4]) + float(x[i + 6]))) + l0
+        l1 = ((float(x[i + 1]) + float(x[i + 3])) + (float(x[i + 5]) + float(x[i + 7]))) + l1
+        i += 8
+    while i < n:
+        l0 = float(x[i]) + l0
+        if i + 1 < n:
+            l1 = float(x[i + 1]) + l1
+        i += 2
+    return l0 + l1
+
+
 def pairwise_sum(a: np.ndarray) -> float:
     """numpy's pairwise summation (PW_BLOCKSIZE=128, 8 accumulators), scalar."""
     n = len(a)
@@ -166,12 +187,18 @@ def default_chunk_size(n_padded: int, block_size: int) -> int:
 
 
 def pyramid_from_leaf_norms2(norms2: np.ndarray) -> list:
-    """quadtree.py:188-192: sqrt per tier, tier sums (c00+c01)+(c10+c11)."""
+    """quadtree.py:188-192: sqrt per tier; reshape(h,2,h,2).sum(axis=(1,3)) is
+    (c00+c01)+(c10+c11) for h >= 2, but for the root (h = 1) numpy coalesces
+    the two reduced axes into one contiguous run of 4 and sums it
+    sequentially: ((c00+c01)+c10)+c11."""
     tiers = [np.sqrt(norms2)]
     while norms2.shape[0] > 1:
         h = norms2.shape[0] // 2
         q = norms2.reshape(h, 2, h, 2)
-        norms2 = (q[:, 0, :, 0] + q[:, 0, :, 1]) + (q[:, 1, :, 0] + q[:, 1, :, 1])
+        if h == 1:
+            norms2 = ((q[:, 0, :, 0] + q[:, 0, :, 1]) + q[:, 1, :, 0]) + q[:, 1, :, 1]
+        else:
+            norms2 = (q[:, 0, :, 0] + q[:, 0, :, 1]) + (q[:, 1, :, 0] + q[:, 1, :, 1])
         tiers.insert(0, np.sqrt(norms2))
     return tiers
 
@@ -248,6 +275,8 @@ def trace(m: OMatrix) -> float:
     g = m.n_blocks
     diag = np.arange(g, dtype=np.int64) * (g + 1)
     hit = np.flatnonzero(np.isin(m.keys, diag))
+    if m.block_size == 1:
+        return contig_sum_recipe(m.data[hit].reshape(-1))
     total = 0.0
     for p in hit:                       # keys are sorted -> diagonal blocks in key order
         d = np.diagonal(m.data[p])

@@ -7,7 +7,9 @@
 //    (6,7),(4,5),(2,3),(0,1), then lane0 + lane1.  Restated here with explicit
 //    __dmul_rn/__dadd_rn so nvcc cannot contract to FMA.
 //  * parents: reshape(h,2,h,2).sum(axis=(1,3)) == (c00 + c01) + (c10 + c11)
-//    in the squared domain (quadtree.py:191), sqrt per tier (quadtree.py:188,192).
+//    in the squared domain (quadtree.py:191) for h >= 2; for the root (h = 1)
+//    numpy coalesces the 2x2 into one contiguous run and sums sequentially,
+//    ((c00 + c01) + c10) + c11; sqrt per tier (quadtree.py:188,192).
 //  * blocks whose entries are all exactly zero are pruned (quadtree.py:177-180).
 // HBM roofline: S*Nb^2*8 bytes read per pass; K1.
 #include <mutex>
@@ -152,7 +154,9 @@ __global__ void k_tiers_small(double* __restrict__ norms2, double* __restrict__ 
       const int64_t i = idx / w, j = idx % w;
       const double* r0 = c2 + (2 * i) * W + 2 * j;
       const double* r1 = r0 + W;
-      const double s = __dadd_rn(__dadd_rn(r0[0], r0[1]), __dadd_rn(r1[0], r1[1]));
+      // root (t = 0): numpy coalesces the 2x2 into one run of 4 -> sequential
+      const double s = t == 0 ? __dadd_rn(__dadd_rn(__dadd_rn(r0[0], r0[1]), r1[0]), r1[1])
+                              : __dadd_rn(__dadd_rn(r0[0], r0[1]), __dadd_rn(r1[0], r1[1]));
       p2[idx] = s;
       pn[idx] = __dsqrt_rn(s);
     }

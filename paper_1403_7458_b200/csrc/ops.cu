@@ -141,12 +141,33 @@ __global__ void k_trace(const int32_t* __restrict__ slot, const double* __restri
     }
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    double tot = 0.0;
-    for (int64_t b = 0; b < G; ++b)
-      if (present[b]) tot = __dadd_rn(tot, partial[b]);
-    out[0] = tot;
+  if (threadIdx.x != 0) return;
+  if (nb == 1) {
+    // Nb = 1: einsum sees one contiguous run of diagonal values and uses its
+    // two-lane sum_of_arr: per 8 values ((x0+x2)+(x4+x6)) into lane 0, odd
+    // ones into lane 1, tail two at a time, then lane0 + lane1.
+    double l0 = 0.0, l1 = 0.0, v[8];
+    int nv = 0;
+    for (int64_t b = 0; b < G; ++b) {
+      if (!present[b]) continue;
+      v[nv++] = partial[b];
+      if (nv == 8) {
+        l0 = __dadd_rn(__dadd_rn(__dadd_rn(v[0], v[2]), __dadd_rn(v[4], v[6])), l0);
+        l1 = __dadd_rn(__dadd_rn(__dadd_rn(v[1], v[3]), __dadd_rn(v[5], v[7])), l1);
+        nv = 0;
+      }
+    }
+    for (int i = 0; i < nv; i += 2) {
+      l0 = __dadd_rn(v[i], l0);
+      if (i + 1 < nv) l1 = __dadd_rn(v[i + 1], l1);
+    }
+    out[0] = __dadd_rn(l0, l1);
+    return;
   }
+  double tot = 0.0;
+  for (int64_t b = 0; b < G; ++b)
+    if (present[b]) tot = __dadd_rn(tot, partial[b]);
+  out[0] = tot;
 }
 
 // max |F - F^T| over native entries; non-negative doubles order like their bits.

@@ -16,22 +16,58 @@ each workload as a generator, fixed here:
   and rows move as 25-row runs.  One numpy PCG64 stream per seed, draws in
   the order centres, jitter, s, diagonal.
 
-Host-side numpy; this is input preparation, not the hot path.
+Host-side numpy; this is input preparation, not the hot path.  The inputs
+are bit-identical on every host: only correctly rounded IEEE operations are
+used (no BLAS, whose kernels are chosen per CPU, and no ``np.exp``, whose
+SIMD implementation is chosen per CPU) -- a last-ulp difference in H is
+enough to move an SP2 run off the reference's trajectory after ~20
+iterations.  ``input_digest`` pins that in the tests.
 """
 
 from __future__ import annotations
 
+import hashlib
 from dataclasses import dataclass
 
 import numpy as np
 
-__all__ = ["decay_pair", "water_cluster", "hilbert_keys_3d", "ConfigSpec", "CONFIGS"]
+__all__ = ["decay_pair", "water_cluster", "hilbert_keys_3d", "det_exp", "input_digest",
+           "ConfigSpec", "CONFIGS"]
+
+_LN2_HI = 6.93147180369123816490e-01   # 32 trailing zero bits: k * LN2_HI exact
+_LN2_LO = 1.90821492927058770002e-10
+_INV_LN2 = 1.44269504088896338700e+00
+
+
+def det_exp(x) -> np.ndarray:
+    """exp(x) from +, *, rint and ldexp only (host independent, < 2 ulp).
+
+    Cody-Waite reduction x = k ln2 + r, |r| <= ln2/2, degree-13 Taylor
+    polynomial by Horner (numpy never fuses the multiply-add).
+    """
+    x = np.asarray(x, dtype=np.float64)
+    k = np.rint(x * _INV_LN2)
+    r = (x - k * _LN2_HI) - k * _LN2_LO
+    p = np.full_like(r, 1.0 / 6227020800.0)          # 1/13!
+    fact = 6227020800.0
+    for n in range(12, -1, -1):
+        fact /= (n + 1)
+        p = p * r + 1.0 / fact
+    return np.ldexp(p, k.astype(np.int64))
+
+
+def input_digest(*arrays) -> str:
+    """sha256 of the raw bytes of generated inputs (host-independence pin)."""
+    h = hashlib.sha256()
+    for a in arrays:
+        h.update(np.ascontiguousarray(a, dtype=np.float64).tobytes())
+    return h.hexdigest()
 
 
 def decay_pair(n: int = 1024, lam: float = 0.1, seeds=(0, 1)):
     """cfg1 operands: exp(-lam |i-j|) * symmetrised U[-1, 1)."""
     idx = np.arange(n)
-    env = np.exp(-lam * np.abs(idx[:, None] - idx[None, :]))
+    env = det_exp(-lam * np.abs(idx[:, None] - idx[None, :]))
     out = []
     for s in seeds:
         u = np.random.default_rng(s).uniform(-1.0, 1.0, size=(n, n))
@@ -96,12 +132,13 @@ def water_cluster(n_mol: int, seed: int = 0, density: float = 0.0334, sites: int
     edge = (n_mol / density) ** (1.0 / 3.0)
     centres = rng.uniform(0.0, edge, size=(n_mol, 3))
     pos = np.repeat(centres, sites, axis=0) + rng.normal(0.0, jitter, size=(n, 3))
-    sq = np.einsum("ij,ij->i", pos, pos)
-    r2 = np.maximum(sq[:, None] + sq[None, :] - 2.0 * (pos @ pos.T), 0.0)
+    r2 = np.zeros((n, n))
+    for a in range(3):                         # fixed order, elementwise: host independent
+        d = pos[:, a, None] - pos[None, :, a]
+        r2 += d * d
     s = rng.uniform(-1.0, 1.0, size=(n, n))
     s = np.triu(s) + np.triu(s, 1).T
-    h = amp * np.exp(-np.sqrt(r2) / decay) * s
-    h = np.triu(h) + np.triu(h, 1).T          # exact symmetry after the matmul-based r2
+    h = amp * det_exp(-np.sqrt(r2) / decay) * s   # symmetric: r2 and s are exactly symmetric
     occ = np.tile(np.arange(sites) < occupied, n_mol)
     d = np.where(occ, -1.0, 1.0) + rng.normal(0.0, diag_sigma, size=n)
     np.fill_diagonal(h, d)

@@ -1,0 +1,115 @@
+"""SP2 on the GPU vs the reference (sp2.py) and its golden runs.
+
+Contract (BASELINE north_star): identical iteration count and branch
+sequence; density matrix within relative Frobenius 1e-12; with the exact leaf
+kernel the whole run is bitwise identical to the reference."""
+
+import numpy as np
+import pytest
+
+from conftest import golden, pyramid_flat
+from oracle import spamm_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+import paper_1403_7458_b200 as sp  # noqa: E402
+from paper_1403_7458_b200.synth import CONFIGS, water_cluster  # noqa: E402
+
+REL_FRO_TOL = 1e-12
+
+
+def rel(a, b):
+    return np.linalg.norm(a - b) / np.linalg.norm(b)
+
+
+def test_gershgorin_bitwise_cfg2():
+    gb = golden("cfg2_bounds")
+    h, _ = water_cluster(CONFIGS[2].n_mol, seed=0)
+    b = sp.gershgorin_bounds(sp.build_from_dense(h, 32))
+    assert (b.eps_min, b.eps_max) == (float(gb["eps_min"]), float(gb["eps_max"]))
+
+
+def test_gershgorin_rejects_asymmetric(rng):
+    d = rng.standard_normal((20, 20))
+    with pytest.raises(ValueError, match="not symmetric"):
+        sp.gershgorin_bounds(sp.build_from_dense(d, 4))
+
+
+def test_sp2_validation():
+    f = sp.build_from_dense(np.diag(np.arange(1.0, 9.0)), 4)
+    for bad in (0, 8, -1):
+        with pytest.raises(ValueError):
+            sp.sp2_solve(f, bad, 1e-8)
+    with pytest.raises(ValueError):
+        sp.sp2_init(f, sp.SpectralBounds(1.0, 1.0))
+
+
+@pytest.mark.parametrize("nb,kernel", [(16, "exact"), (16, "auto"), (8, "auto"), (4, "exact")])
+def test_sp2_trace_criterion_vs_oracle(nb, kernel):
+    h, n_occ = water_cluster(12, seed=3)
+    p, st = sp.sp2_solve(sp.build_from_dense(h, nb), n_occ, 1e-9, kernel=kernel)
+    r = O.sp2_solve(O.from_dense(h, nb), n_occ, 1e-9, threads=4)
+    assert st.iteration == r.iterations and st.converged == r.converged
+    assert st.branch_history == r.branches
+    ref = O.to_dense(r.x)
+    if kernel == "exact":
+        assert st.trace_history == r.trace_history
+        assert np.array_equal(sp.to_dense(p), ref)
+    else:
+        assert rel(sp.to_dense(p), ref) <= REL_FRO_TOL
+
+
+def test_sp2_step_branches():
+    h, n_occ = water_cluster(8, seed=1)
+    x = sp.sp2_init(sp.build_from_dense(h, 8), sp.gershgorin_bounds(sp.build_from_dense(h, 8)))
+    ox = O.sp2_init(O.from_dense(h, 8), O.gershgorin_bounds(O.from_dense(h, 8)))
+    for _ in range(4):
+        x, br = sp.sp2_step(x, n_occ, 1e-10, kernel="exact")
+        ox, obr, *_ = O.sp2_step(ox, n_occ, 1e-10)
+        assert br == obr
+        assert np.array_equal(sp.to_dense(x), O.to_dense(ox))
+
+
+@pytest.mark.parametrize("name,cfg_index", [("cfg3_sp2", 3), ("cfg4_sp2", 4)])
+def test_sp2_baseline_configs(name, cfg_index):
+    """BASELINE cfg3 / cfg4: ||X^2-X||_F < 1e-6 with SpAMM tau on every X^2."""
+    from paper_1403_7458_b200.synth import input_digest
+    gd = golden(name)
+    cfg = CONFIGS[cfg_index]
+    h, n_occ = water_cluster(cfg.n_mol, seed=0)
+    assert input_digest(h) == str(gd["input_sha256"]), "generator not host independent"
+    f = sp.build_from_dense(h, cfg.block_size)
+    assert np.array_equal(pyramid_flat(f._tier_norms), gd["f_pyramid"])
+    b = sp.gershgorin_bounds(f)
+    assert (b.eps_min, b.eps_max) == (float(gd["eps_min"]), float(gd["eps_max"]))
+    p, st = sp.sp2_solve(f, n_occ, cfg.tau, criterion="fro", fro_tol=1e-6)
+    assert st.converged and st.iteration == int(gd["iterations"])
+    assert [br == sp.SQUARE for br in st.branch_history] == list(gd["branches"])
+    assert list(st.leaf_products) == list(gd["leaf_products"])   # task sets: exact counts
+    assert np.allclose(st.trace_history, gd["traces"], rtol=1e-12, atol=0)
+    leaf = p._tier_norms[-1]
+    ref_leaf = gd["p_pyramid"][-leaf.size:].reshape(leaf.shape)
+    assert rel(leaf, ref_leaf) <= REL_FRO_TOL
+    assert abs(sp.trace(p) - float(gd["p_trace"])) <= 1e-12 * float(gd["p_trace"])
+    assert abs(sp.trace(p) - n_occ) < 1e-3
+    # exact leaf kernel: the whole SP2 trajectory is bitwise the reference's
+    pe, ste = sp.sp2_solve(f, n_occ, cfg.tau, criterion="fro", fro_tol=1e-6, kernel="exact")
+    assert ste.iteration == int(gd["iterations"])
+    assert np.array_equal(np.array(ste.trace_history), gd["traces"])
+    assert np.array_equal(np.array(ste.idempotency_history), gd["idem"])
+    assert np.array_equal(pyramid_flat(pe._tier_norms), gd["p_pyramid"])
+    assert np.array_equal(pe._block_keys, gd["p_keys"])
+
+
+def test_idempotency_and_energy_error():
+    h, n_occ = water_cluster(10, seed=4)
+    f = sp.build_from_dense(h, 16)
+    p, st = sp.sp2_solve(f, n_occ, 0.0)
+    assert st.converged
+    assert sp.idempotency_error(p) < 1e-6
+    of = O.from_dense(h, 16)
+    assert abs(sp.energy_error(f, p, p)) == 0.0
+    w, v = np.linalg.eigh(h)
+    proj = v[:, :n_occ] @ v[:, :n_occ].T
+    assert np.linalg.norm(sp.to_dense(p) - proj) < 1e-6
+    assert of.n_native == h.shape[0]
