@@ -120,6 +120,13 @@ int spamm_add_scaled(double alpha, const spamm_mat* a, double beta, const spamm_
                      void* stream, spamm_mat** out);
 /* trace (quadtree.py:296-305). */
 int spamm_trace(const spamm_mat* m, void* stream, double* out);
+/* Fused SP2 update (sp2.py:92-101 EXPAND branch + BASELINE cfg3's idempotency
+ * test): one pass over the key union of X and X2 = X*X.
+ *   want_idem: *idem_norm = add_scaled(1.0, X2, -1.0, X).norm() (bit-exact),
+ *              without materialising X2 - X;
+ *   expand:    *e_out = add_scaled(2.0, X, -1.0, X2) (quadtree.py:281-293). */
+int spamm_sp2_update(const spamm_mat* x, const spamm_mat* x2, int32_t want_idem, int32_t expand,
+                     void* stream, double* idem_norm, spamm_mat** e_out);
 /* gershgorin_bounds (sp2.py:68-76): eps_min, eps_max and max|F-F^T|
  * (caller raises when asym > sym_tol, as the reference does). */
 int spamm_gershgorin(const spamm_mat* f, void* stream, double* eps_min, double* eps_max,

@@ -62,6 +62,8 @@ _SIGS = {
                                  c_vp]),
     "spamm_add_scaled": (c_i32, [c_f64, c_vp, c_f64, c_vp, c_vp, ctypes.POINTER(c_vp)]),
     "spamm_trace": (c_i32, [c_vp, c_vp, ctypes.POINTER(c_f64)]),
+    "spamm_sp2_update": (c_i32, [c_vp, c_vp, c_i32, c_i32, c_vp, ctypes.POINTER(c_f64),
+                                 ctypes.POINTER(c_vp)]),
     "spamm_gershgorin": (c_i32, [c_vp, c_vp, ctypes.POINTER(c_f64), ctypes.POINTER(c_f64),
                                  ctypes.POINTER(c_f64)]),
 }

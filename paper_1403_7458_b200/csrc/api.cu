@@ -393,6 +393,23 @@ int spamm_trace(const spamm_mat* m, void* stream, double* out) {
   SPAMM_API_END
 }
 
+int spamm_sp2_update(const spamm_mat* x, const spamm_mat* x2, int32_t want_idem, int32_t expand,
+                     void* stream, double* idem_norm, spamm_mat** e_out) {
+  if (int rc = check_conformable(x, x2)) return rc;
+  if (want_idem && !idem_norm) return fail(SPAMM_EINVAL, "null idem_norm");
+  if (expand && !e_out) return fail(SPAMM_EINVAL, "null output handle");
+  SPAMM_API_BEGIN
+  cudaStream_t s = S(stream);
+  spamm_mat* h = expand ? new spamm_mat() : nullptr;
+  spamm::Mat dummy;
+  spamm::sp2_update(x->m, x2->m, want_idem != 0, expand != 0, idem_norm, h ? h->m : dummy, s);
+  if (h) {
+    h->m.stream = s;
+    *e_out = h;
+  }
+  SPAMM_API_END
+}
+
 int spamm_gershgorin(const spamm_mat* f, void* stream, double* eps_min, double* eps_max,
                      double* asym) {
   if (!f || !eps_min || !eps_max || !asym) return fail(SPAMM_EINVAL, "null argument");

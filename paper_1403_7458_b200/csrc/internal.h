@@ -39,8 +39,15 @@ struct Mat {
 
 // Finalise a matrix whose data/keys (nblocks, Morton order) are set: prune
 // exact-zero blocks, build slot map and the bit-exact norm pyramid
-// (quadtree.py:170-194).  Takes ownership of data/keys.
-void finalize(Mat& m, cudaStream_t s);
+// (quadtree.py:170-194).  Takes ownership of data/keys, and of pre_n2 / pre_nz
+// when given (per-block leaf norm^2 and nonzero flags already computed by a
+// fused producer kernel; K1 is then skipped).
+void finalize(Mat& m, cudaStream_t s, double* pre_n2 = nullptr, uint8_t* pre_nz = nullptr);
+// Fused SP2 update over the key union of X and X^2 (sp2.cu):
+//   idem2_root <- pyramid root of ||X^2 - X||^2 (add_scaled(1,X2,-1,X).norm()^2)
+//   expand     -> E = add_scaled(2, X, -1, X2) finalised into `e`.
+void sp2_update(const Mat& x, const Mat& x2, bool want_idem, bool expand, double* idem_norm,
+                Mat& e, cudaStream_t s);
 
 void scatter_slots(const int64_t* keys, int64_t m, int32_t* slot, cudaStream_t s);
 // Leaf norm^2 (einsum recipe) and nonzero flags for m blocks of nb x nb.

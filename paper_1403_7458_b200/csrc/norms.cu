@@ -189,18 +189,79 @@ __global__ void k_scatter_slots(const int64_t* __restrict__ keys, int64_t m, int
 
 }  // namespace
 
+// Warp-per-block variant for Nb^2 a multiple of 256: the warp streams the block
+// through shared memory in 256-element chunks with fully coalesced loads
+// (next chunk in flight while the current one is reduced), squares are formed
+// by all 32 lanes, and lanes 0 / 1 run the two einsum lanes' add chains (the
+// only inherently serial part).  Same recipe, same result bits as k_leaf_norms2.
+template <int NB2>
+__global__ void __launch_bounds__(256)
+    k_leaf_norms2_warp(const double* __restrict__ data, int64_t m, double* __restrict__ out,
+                       uint8_t* __restrict__ nz) {
+  constexpr int CH = 256, NCH = NB2 / CH;
+  __shared__ __align__(16) double sq[8][CH];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* buf = sq[warp];
+  const int64_t nw = (int64_t)gridDim.x * 8;
+  for (int64_t b = (int64_t)blockIdx.x * 8 + warp; b < m; b += nw) {
+    const double2* x = reinterpret_cast<const double2*>(data + b * NB2);
+    double2 r[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) r[k] = __ldg(x + k * 32 + lane);
+    double acc = 0.0;
+    bool any = false;
+    for (int c = 0; c < NCH; ++c) {
+      __syncwarp();
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        double2 p;
+        p.x = __dmul_rn(r[k].x, r[k].x);
+        p.y = __dmul_rn(r[k].y, r[k].y);
+        any |= (r[k].x != 0.0) | (r[k].y != 0.0);
+        *reinterpret_cast<double2*>(buf + k * 64 + 2 * lane) = p;
+      }
+      __syncwarp();
+      if (c + 1 < NCH) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) r[k] = __ldg(x + (c + 1) * (CH / 2) + k * 32 + lane);
+      }
+      if (lane < 2) {
+        const double* p = buf + lane;
+        double l = acc;
+#pragma unroll 8
+        for (int g = 0; g < CH / 8; ++g) {
+          l = __dadd_rn(l, p[g * 8 + 6]);
+          l = __dadd_rn(l, p[g * 8 + 4]);
+          l = __dadd_rn(l, p[g * 8 + 2]);
+          l = __dadd_rn(l, p[g * 8 + 0]);
+        }
+        acc = l;
+      }
+    }
+    const double l1 = __shfl_sync(0xffffffffu, acc, 1);
+    any = __any_sync(0xffffffffu, any);
+    if (lane == 0) {
+      out[b] = __dadd_rn(acc, l1);
+      if (nz) nz[b] = any ? 1 : 0;
+    }
+  }
+}
+
 void leaf_norms2(const double* data, int64_t m, int nb, double* norms2, uint8_t* nonzero,
                  cudaStream_t s) {
   if (m <= 0) return;
   const int nb2 = nb * nb;
-  const int threads = 128;
-  const int grid = grid_for(m, threads, 1LL << 20);
-  if (nb2 == 1024)
-    k_leaf_norms2<1024><<<grid, threads, 0, s>>>(data, m, nb2, norms2, nonzero);
-  else if (nb2 == 4096)
-    k_leaf_norms2<4096><<<grid, threads, 0, s>>>(data, m, nb2, norms2, nonzero);
-  else
-    k_leaf_norms2<0><<<grid, threads, 0, s>>>(data, m, nb2, norms2, nonzero);
+  if (nb2 == 1024 || nb2 == 4096) {
+    const int grid = grid_for(m * 32, 256, 1LL << 20);
+    if (nb2 == 1024)
+      k_leaf_norms2_warp<1024><<<grid, 256, 0, s>>>(data, m, norms2, nonzero);
+    else
+      k_leaf_norms2_warp<4096><<<grid, 256, 0, s>>>(data, m, norms2, nonzero);
+  } else {
+    const int threads = 128;
+    k_leaf_norms2<0><<<grid_for(m, threads, 1LL << 20), threads, 0, s>>>(data, m, nb2, norms2,
+                                                                        nonzero);
+  }
   SPAMM_LAUNCH_CK();
 }
 
@@ -234,14 +295,17 @@ void scatter_slots(const int64_t* keys, int64_t m, int32_t* slot, cudaStream_t s
   SPAMM_LAUNCH_CK();
 }
 
-void finalize(Mat& m, cudaStream_t s) {
+void finalize(Mat& m, cudaStream_t s, double* pre_n2, uint8_t* pre_nz) {
   m.stream = s;
   const int nb2 = m.nb * m.nb;
-  double* n2 = nullptr;
+  double* n2 = pre_n2;
   if (m.nblocks > 0) {
-    n2 = dmalloc<double>(m.nblocks, s);
-    uint8_t* nz = dmalloc<uint8_t>(m.nblocks, s);
-    leaf_norms2(m.data, m.nblocks, m.nb, n2, nz, s);
+    uint8_t* nz = pre_nz;
+    if (!n2) {
+      n2 = dmalloc<double>(m.nblocks, s);
+      nz = dmalloc<uint8_t>(m.nblocks, s);
+      leaf_norms2(m.data, m.nblocks, m.nb, n2, nz, s);
+    }
     int64_t* off = dmalloc<int64_t>(m.nblocks + 1, s);
     scan_exclusive_u8(nz, m.nblocks, off, s);
     int64_t kept = 0;

@@ -126,21 +126,35 @@ __global__ void k_add_scaled(double alpha, const double* __restrict__ A, const i
   }
 }
 
+// Per diagonal block: warp-parallel loads of the diagonal, then a sequential
+// sum (lane 0 pulls element d from lane d % 32) -- einsum's inner loop order.
+__global__ void k_trace_blocks(const int32_t* __restrict__ slot, const double* __restrict__ data,
+                               int64_t G, int nb, double* __restrict__ partial,
+                               uint8_t* __restrict__ present) {
+  const int64_t nb2 = (int64_t)nb * nb;
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t b = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; b < G; b += nw) {
+    const int32_t s = slot[b * G + b];
+    if (lane == 0) present[b] = s >= 0;
+    if (s < 0) continue;
+    const double* x = data + (int64_t)s * nb2;
+    double acc = 0.0;
+    for (int d0 = 0; d0 < nb; d0 += 32) {
+      const int d = d0 + lane;
+      const double v = d < nb ? x[(int64_t)d * nb + d] : 0.0;
+      const int cnt = min(32, nb - d0);
+      for (int i = 0; i < cnt; ++i) acc = __dadd_rn(acc, __shfl_sync(0xffffffffu, v, i));
+    }
+    if (lane == 0) partial[b] = acc;
+  }
+}
+
 __global__ void k_trace(const int32_t* __restrict__ slot, const double* __restrict__ data, int64_t G,
                         int nb, double* __restrict__ partial, uint8_t* __restrict__ present,
                         double* __restrict__ out) {
-  const int64_t nb2 = (int64_t)nb * nb;
-  for (int64_t b = threadIdx.x; b < G; b += blockDim.x) {
-    const int32_t s = slot[b * G + b];
-    present[b] = s >= 0;
-    if (s >= 0) {
-      const double* x = data + (int64_t)s * nb2;
-      double acc = 0.0;
-      for (int d = 0; d < nb; ++d) acc = __dadd_rn(acc, x[(int64_t)d * nb + d]);
-      partial[b] = acc;
-    }
-  }
-  __syncthreads();
+  (void)slot;
+  (void)data;
   if (threadIdx.x != 0) return;
   if (nb == 1) {
     // Nb = 1: einsum sees one contiguous run of diagonal values and uses its
@@ -380,7 +394,10 @@ void add_scaled(double alpha, const Mat& a, double beta, const Mat& b, Mat& out,
 double trace(const Mat& m, cudaStream_t s) {
   double* partial = dmalloc<double>(m.G + 1, s);
   uint8_t* present = dmalloc<uint8_t>(m.G, s);
-  k_trace<<<1, 1024, 0, s>>>(m.slot, m.data, m.G, m.nb, partial, present, partial + m.G);
+  k_trace_blocks<<<grid_for(m.G * 32, 256), 256, 0, s>>>(m.slot, m.data, m.G, m.nb, partial,
+                                                          present);
+  SPAMM_LAUNCH_CK();
+  k_trace<<<1, 32, 0, s>>>(m.slot, m.data, m.G, m.nb, partial, present, partial + m.G);
   SPAMM_LAUNCH_CK();
   int64_t bits = 0;
   d2h_sync(&bits, reinterpret_cast<const int64_t*>(partial + m.G), 1, s);

@@ -101,6 +101,29 @@ def test_sp2_baseline_configs(name, cfg_index):
     assert np.array_equal(pe._block_keys, gd["p_keys"])
 
 
+@pytest.mark.parametrize("nb", [8, 32, 64])
+def test_fused_update_bitwise_equals_add_scaled(rng, nb):
+    """K6 fused pass == add_scaled(2,X,-1,X2) and add_scaled(1,X2,-1,X).norm()."""
+    from paper_1403_7458_b200.sp2 import _update
+    n = 5 * nb + 3
+    d = rng.standard_normal((n, n))
+    d[np.abs(d) < 1.0] = 0.0
+    d[: nb, nb: 2 * nb] = 0.0             # a block present in X only after squaring
+    x = sp.build_from_dense(d, nb)
+    x2, _ = sp.multiply(x, x, 0.5)
+    e, idem = _update(x, x2, True, True)
+    ref_e = sp.add_scaled(2.0, x, -1.0, x2)
+    assert np.array_equal(sp.to_dense(e), sp.to_dense(ref_e))
+    assert np.array_equal(pyramid_flat(e._tier_norms), pyramid_flat(ref_e._tier_norms))
+    assert np.array_equal(e._block_keys, ref_e._block_keys)
+    assert idem == sp.add_scaled(1.0, x2, -1.0, x).norm()
+    oe = O.add_scaled(2.0, O.from_dense(d, nb), -1.0, O.from_dense(sp.to_dense(x2), nb))
+    assert np.array_equal(sp.to_dense(e), O.to_dense(oe))
+    # X == X2: the expansion cancels to X exactly, the idempotency error is 0
+    z, idem0 = _update(x, x, True, True)
+    assert idem0 == 0.0 and np.array_equal(sp.to_dense(z), d)
+
+
 def test_idempotency_and_energy_error():
     h, n_occ = water_cluster(10, seed=4)
     f = sp.build_from_dense(h, 16)
