@@ -54,6 +54,7 @@ typedef struct {
   int32_t* slot;       /* (G*G,) storage slot per key, -1 = null */
   double* norms;       /* pyramid, tier t (2^t x 2^t row-major) at (4^t-1)/3 */
   double* norms2;      /* same, squared */
+  int32_t symmetric;   /* 1: X == X^T bitwise (enables symmetric products) */
 } spamm_mat_info;
 
 /* ProductStats (kernel.py:38-61) plus device timings. */
@@ -68,6 +69,8 @@ typedef struct {
   float ms_cull;         /* CUDA-event times on `stream` (0 if not timed) */
   float ms_leaf;
   float ms_finalize;
+  int64_t executed_products; /* leaf products actually run (half when symmetric) */
+  int32_t symmetric;         /* 1: symmetric SpAMM path (C_ji = C_ij^T mirrored) */
 } spamm_stats;
 
 int spamm_abi_version(void);
@@ -95,6 +98,13 @@ int spamm_mat_to_dense(const spamm_mat* m, double* dense, int64_t ld, void* stre
 /* multiply (kernel.py:157-223): C = A*B culled at tau (strict >). */
 int spamm_multiply(const spamm_mat* a, const spamm_mat* b, double tau, int32_t kernel,
                    int32_t timed, void* stream, spamm_mat** c, spamm_stats* stats);
+/* Symmetric products (default on): when a == b and the matrix is exactly
+ * symmetric, multiply computes only C blocks with i <= j and mirrors the rest;
+ * counters stay the full reference counts.  0 disables (A/B testing). */
+int spamm_set_symmetric_products(int32_t enabled);
+/* Pre-grow the library's stream-ordered memory pool by `bytes` (kept mapped),
+ * so steady-state allocations never wait on a new device mapping. */
+int spamm_reserve_pool(int64_t bytes, void* stream);
 /* convolution_census (kernel.py:226-239): counts only. */
 int spamm_census(const spamm_mat* a, const spamm_mat* b, double tau, void* stream,
                  spamm_stats* stats);
@@ -127,6 +137,14 @@ int spamm_trace(const spamm_mat* m, void* stream, double* out);
  *   expand:    *e_out = add_scaled(2.0, X, -1.0, X2) (quadtree.py:281-293). */
 int spamm_sp2_update(const spamm_mat* x, const spamm_mat* x2, int32_t want_idem, int32_t expand,
                      void* stream, double* idem_norm, spamm_mat** e_out);
+/* One SP2 iteration, native driver (sp2.py:92-101 + the idempotency test):
+ * X2 = X*X (SpAMM at tau), t_x = tr X (cached per matrix), t_sq = tr X2, branch
+ * SQUARE (0) if |t_sq - n_occ| <= |2 t_x - t_sq - n_occ| else EXPAND (1),
+ * x_next = X2 or 2X - X2, and with want_idem *idem = ||X2 - X||_F -- with one
+ * host sync for the traces (+ union size) and one for idem. */
+int spamm_sp2_step(const spamm_mat* x, double n_occ, double tau, int32_t kernel, int32_t want_idem,
+                   int32_t timed, void* stream, spamm_mat** x_next, int32_t* branch, double* t_x,
+                   double* t_sq, double* idem, spamm_stats* stats);
 /* gershgorin_bounds (sp2.py:68-76): eps_min, eps_max and max|F-F^T|
  * (caller raises when asym > sym_tol, as the reference does). */
 int spamm_gershgorin(const spamm_mat* f, void* stream, double* eps_min, double* eps_max,

@@ -31,6 +31,7 @@ class MatInfo(ctypes.Structure):
         ("n_native", c_i64), ("block_size", c_i32), ("depth", c_i32),
         ("chunk_size", c_i64), ("n_blocks", c_i64), ("stored", c_i64),
         ("data", c_vp), ("keys", c_vp), ("slot", c_vp), ("norms", c_vp), ("norms2", c_vp),
+        ("symmetric", c_i32),
     ]
 
 
@@ -40,6 +41,7 @@ class Stats(ctypes.Structure):
         ("visited", c_i64 * MAX_TIERS), ("culled", c_i64 * MAX_TIERS),
         ("leaf_products", c_i64), ("flop_estimate", c_i64), ("c_blocks", c_i64),
         ("ms_cull", ctypes.c_float), ("ms_leaf", ctypes.c_float), ("ms_finalize", ctypes.c_float),
+        ("executed_products", c_i64), ("symmetric", c_i32),
     ]
 
 
@@ -57,6 +59,8 @@ _SIGS = {
     "spamm_multiply": (c_i32, [c_vp, c_vp, c_f64, c_i32, c_i32, c_vp, ctypes.POINTER(c_vp),
                                ctypes.POINTER(Stats)]),
     "spamm_census": (c_i32, [c_vp, c_vp, c_f64, c_vp, ctypes.POINTER(Stats)]),
+    "spamm_set_symmetric_products": (c_i32, [c_i32]),
+    "spamm_reserve_pool": (c_i32, [c_i64, c_vp]),
     "spamm_tasks": (c_i32, [c_vp, c_vp, c_f64, c_vp, c_vp, c_vp, c_i64, ctypes.POINTER(c_i64), c_vp]),
     "spamm_gemm_batch": (c_i32, [c_vp, c_vp, c_vp, c_i64, c_vp, c_i64, c_vp, c_i64, c_vp, c_i32, c_i32,
                                  c_vp]),
@@ -64,6 +68,10 @@ _SIGS = {
     "spamm_trace": (c_i32, [c_vp, c_vp, ctypes.POINTER(c_f64)]),
     "spamm_sp2_update": (c_i32, [c_vp, c_vp, c_i32, c_i32, c_vp, ctypes.POINTER(c_f64),
                                  ctypes.POINTER(c_vp)]),
+    "spamm_sp2_step": (c_i32, [c_vp, c_f64, c_f64, c_i32, c_i32, c_i32, c_vp, ctypes.POINTER(c_vp),
+                               ctypes.POINTER(c_i32), ctypes.POINTER(c_f64),
+                               ctypes.POINTER(c_f64), ctypes.POINTER(c_f64),
+                               ctypes.POINTER(Stats)]),
     "spamm_gershgorin": (c_i32, [c_vp, c_vp, ctypes.POINTER(c_f64), ctypes.POINTER(c_f64),
                                  ctypes.POINTER(c_f64)]),
 }

@@ -1,5 +1,6 @@
 // C ABI (include/spamm_b200.h): argument checks, handle management and the
 // multiply driver (cull -> leaf products -> C finalisation).
+#include <cmath>
 #include <cstring>
 #include <string>
 
@@ -115,6 +116,36 @@ __global__ void k_seg_build(const int64_t* c_pos, const uint8_t* flags, const in
   if (blockIdx.x == 0 && threadIdx.x == 0) seg[nseg] = n;
 }
 
+bool g_sym_enabled = true;
+
+__global__ void k_sym_flags(const int32_t* ci, const int32_t* cj, int64_t n, uint8_t* flags) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    flags[spamm::morton_encode(ci[i], cj[i])] = 1;
+    flags[spamm::morton_encode(cj[i], ci[i])] = 1;
+  }
+}
+
+__global__ void k_sym_layout(const int32_t* ci, const int32_t* cj, int64_t n, const int64_t* off,
+                             int64_t* c_out, int64_t* c_mirror) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    c_out[i] = off[spamm::morton_encode(ci[i], cj[i])];
+    c_mirror[i] = ci[i] != cj[i] ? off[spamm::morton_encode(cj[i], ci[i])] : -1;
+  }
+}
+
+__global__ void k_flag_keys(const uint8_t* flags, const int64_t* off, int depth, int64_t* keys) {
+  const int64_t G = int64_t(1) << depth, npos = G * G;
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < npos;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    if (!flags[p]) continue;
+    uint32_t bi, bj;
+    spamm::morton_decode((uint64_t)p, bi, bj);
+    keys[off[p]] = (int64_t)bi * G + bj;
+  }
+}
+
 void fill_stats(spamm_stats* st, double tau, const spamm::CullResult& r, int nb) {
   if (!st) return;
   std::memset(st, 0, sizeof(*st));
@@ -125,8 +156,13 @@ void fill_stats(spamm_stats* st, double tau, const spamm::CullResult& r, int nb)
     st->culled[t] = r.culled[t];
   }
   st->leaf_products = r.visited.empty() ? 0 : r.visited.back();
+  st->executed_products = r.sym ? r.n_tasks : st->leaf_products;
+  st->symmetric = r.sym ? 1 : 0;
   st->flop_estimate = st->leaf_products * 2 * (int64_t)nb * nb * nb;
 }
+
+void multiply_impl(const spamm_mat* a, const spamm_mat* b, double tau, int32_t kernel, bool timed,
+                   cudaStream_t s, spamm::Mat& C, spamm_stats* stats);
 
 }  // namespace
 
@@ -203,6 +239,7 @@ int spamm_mat_from_blocks(int64_t n_native, int32_t block_size, int64_t chunk_si
   spamm::add_scaled(1.0, tmp, 0.0, empty, M, s);
   spamm::dfree(tmp.slot, s);
   spamm::dfree(empty.slot, s);
+  M.sym = spamm::is_symmetric(M, s);
   *out = h;
   SPAMM_API_END
 }
@@ -238,6 +275,7 @@ int spamm_mat_info_get(const spamm_mat* h, spamm_mat_info* info) {
   info->slot = h->m.slot;
   info->norms = h->m.norms;
   info->norms2 = h->m.norms2;
+  info->symmetric = h->m.sym ? 1 : 0;
   return SPAMM_OK;
 }
 
@@ -266,45 +304,165 @@ int spamm_multiply(const spamm_mat* a, const spamm_mat* b, double tau, int32_t k
     return fail(SPAMM_EINVAL, "DMMA leaf kernel needs block size 8, 16, 32 or 64");
   if (!c) return fail(SPAMM_EINVAL, "null output handle");
   SPAMM_API_BEGIN
-  cudaStream_t s = S(stream);
-  EventTimer tm(timed != 0, s);
+  auto* h = new spamm_mat();
+  try {
+    multiply_impl(a, b, tau, kernel, timed != 0, S(stream), h->m, stats);
+  } catch (...) {
+    h->m.release();
+    delete h;
+    throw;
+  }
+  *c = h;
+  SPAMM_API_END
+}
+
+}  // extern "C"
+
+namespace {
+
+void multiply_impl(const spamm_mat* a, const spamm_mat* b, double tau, int32_t kernel, bool timed,
+                   cudaStream_t s, spamm::Mat& C, spamm_stats* stats) {
+  EventTimer tm(timed, s);
   tm.mark(0);
   spamm::CullResult r;
-  spamm::cull(a->m, b->m, tau, true, r, s);
-  auto* h = new spamm_mat();
-  spamm::Mat& C = h->m;
+  // Symmetric SpAMM: X*X with X == X^T bitwise -> compute C_ij for i <= j only
+  // and store C_ji = C_ij^T (bitwise what the full product yields).
+  bool sym = g_sym_enabled && a == b && a->m.sym;
+  if (sym && !spamm::cull(a->m, b->m, tau, true, r, s, true)) sym = false;  // ulp tie: full path
+  if (!sym) spamm::cull(a->m, b->m, tau, true, r, s, false);
   C.n_native = a->m.n_native;
   C.nb = a->m.nb;
   C.chunk_size = a->m.chunk_size;
   C.depth = a->m.depth;
   C.G = a->m.G;
   C.stream = s;
-  C.nblocks = r.n_c;
   const int64_t nb2 = (int64_t)C.nb * C.nb;
-  C.data = spamm::dmalloc<double>((size_t)r.n_c * nb2, s);
-  C.keys = spamm::dmalloc<int64_t>(r.n_c, s);
+  int64_t* c_out = nullptr;
+  int64_t* c_mirror = nullptr;
+  if (sym && r.n_c > 0) {
+    const int64_t npos = C.G * C.G;
+    uint8_t* flags = spamm::dmalloc<uint8_t>(npos, s);
+    int64_t* off = spamm::dmalloc<int64_t>(npos + 1, s);
+    SPAMM_CK(cudaMemsetAsync(flags, 0, npos, s));
+    k_sym_flags<<<spamm::grid_for(r.n_c, 256), 256, 0, s>>>(r.ci, r.cj, r.n_c, flags);
+    SPAMM_LAUNCH_CK();
+    spamm::scan_exclusive_u8(flags, npos, off, s);
+    C.nblocks = r.n_c_full;  // 2 * emitted - diagonal, counted by the cull (no sync)
+    c_out = spamm::dmalloc<int64_t>(r.n_c, s);
+    c_mirror = spamm::dmalloc<int64_t>(r.n_c, s);
+    C.keys = spamm::dmalloc<int64_t>(C.nblocks, s);
+    k_sym_layout<<<spamm::grid_for(r.n_c, 256), 256, 0, s>>>(r.ci, r.cj, r.n_c, off, c_out,
+                                                             c_mirror);
+    SPAMM_LAUNCH_CK();
+    k_flag_keys<<<spamm::grid_for(npos, 256), 256, 0, s>>>(flags, off, C.depth, C.keys);
+    SPAMM_LAUNCH_CK();
+    spamm::dfree(flags, s);
+    spamm::dfree(off, s);
+  } else {
+    C.nblocks = r.n_c;
+    C.keys = spamm::dmalloc<int64_t>(r.n_c, s);
+    if (r.n_c > 0) {
+      k_keys_from_nodes<<<spamm::grid_for(r.n_c, 256), 256, 0, s>>>(r.ci, r.cj, r.n_c, C.G, C.keys);
+      SPAMM_LAUNCH_CK();
+    }
+  }
+  C.data = spamm::dmalloc<double>((size_t)C.nblocks * nb2, s);
   tm.mark(1);  // leaf window = the K4 launch only (allocation stays outside)
   if (r.n_c > 0) {
-    spamm::leaf_products<int32_t>(r.n_c, r.seg, r.a_idx, r.b_idx, nullptr, false, a->m.data,
-                                  a->m.nblocks, b->m.data, b->m.nblocks, C.data, C.nb, kernel, s);
+    spamm::leaf_products<int32_t>(r.n_c, r.seg, r.a_idx, r.b_idx, c_out, c_mirror, false,
+                                  a->m.data, a->m.nblocks, b->m.data, b->m.nblocks, C.data, C.nb,
+                                  kernel, s);
   }
   tm.mark(2);
-  if (r.n_c > 0) {
-    k_keys_from_nodes<<<spamm::grid_for(r.n_c, 256), 256, 0, s>>>(r.ci, r.cj, r.n_c, C.G, C.keys);
-    SPAMM_LAUNCH_CK();
-  }
+  spamm::dfree(c_out, s);
+  spamm::dfree(c_mirror, s);
   spamm::finalize(C, s);
+  C.sym = sym;
   tm.mark(3);
   fill_stats(stats, tau, r, C.nb);
   if (stats) {
-    stats->c_blocks = r.n_c;
+    stats->c_blocks = C.nblocks;
+    stats->executed_products = r.n_tasks;
+    stats->symmetric = sym ? 1 : 0;
     stats->ms_cull = tm.ms(0, 1);
     stats->ms_leaf = tm.ms(1, 2);
     stats->ms_finalize = tm.ms(2, 3);
   }
   r.release(s);
-  *c = h;
+}
+
+}  // namespace
+
+extern "C" {
+
+int spamm_sp2_step(const spamm_mat* x, double n_occ, double tau, int32_t kernel, int32_t want_idem,
+                   int32_t timed, void* stream, spamm_mat** x_next, int32_t* branch, double* t_x,
+                   double* t_sq, double* idem, spamm_stats* stats) {
+  if (!x || !x_next || !branch || !t_x || !t_sq || (want_idem && !idem))
+    return fail(SPAMM_EINVAL, "null argument");
+  if (!(tau >= 0.0) || tau == __builtin_inf())
+    return fail(SPAMM_EINVAL, "tau must be finite and >= 0, got " + std::to_string(tau));
+  if (kernel < 0 || kernel > 3) return fail(SPAMM_EINVAL, "unknown leaf kernel");
+  if ((kernel == SPAMM_LEAF_DMMA || kernel == 3) && !spamm::dmma_supported(x->m.nb))
+    return fail(SPAMM_EINVAL, "DMMA leaf kernel needs block size 8, 16, 32 or 64");
+  SPAMM_API_BEGIN
+  cudaStream_t s = S(stream);
+  auto* c = new spamm_mat();
+  multiply_impl(x, x, tau, kernel, timed != 0, s, c->m, stats);
+  const bool fused = spamm::sp2_fused_supported(x->m.nb);
+  // One host sync for tr(X), tr(X^2) and the union size of the update.
+  int64_t* sc = spamm::dmalloc<int64_t>(3, s);
+  SPAMM_CK(cudaMemsetAsync(sc, 0, 3 * sizeof(int64_t), s));
+  if (!x->m.tr_valid) spamm::trace_launch(x->m, reinterpret_cast<double*>(sc), s);
+  spamm::trace_launch(c->m, reinterpret_cast<double*>(sc + 1), s);
+  spamm::UnionPrep prep;
+  if (fused) prep = spamm::sp2_union_prepare(x->m, c->m, sc + 2, s);
+  int64_t h[3];
+  spamm::d2h_sync(h, sc, 3, s);
+  spamm::dfree(sc, s);
+  if (!x->m.tr_valid) {
+    memcpy(&x->m.tr, &h[0], sizeof(double));
+    x->m.tr_valid = true;
+  }
+  memcpy(&c->m.tr, &h[1], sizeof(double));
+  c->m.tr_valid = true;
+  const double tx = x->m.tr, tsq = c->m.tr;
+  // sp2.py:97-99: ties go to SQUARE.
+  const double tex = 2.0 * tx - tsq;
+  const bool square = std::fabs(tsq - n_occ) <= std::fabs(tex - n_occ);
+  spamm_mat* e = square ? nullptr : new spamm_mat();
+  spamm::Mat dummy;
+  if (fused) {
+    spamm::sp2_update_finish(x->m, c->m, prep, h[2], want_idem != 0, !square, idem,
+                             e ? e->m : dummy, s);
+  } else {
+    spamm::sp2_update(x->m, c->m, want_idem != 0, !square, idem, e ? e->m : dummy, s);
+  }
+  if (e) {
+    e->m.stream = s;
+    e->m.sym = x->m.sym && c->m.sym;
+    c->m.release();
+    delete c;
+    *x_next = e;
+  } else {
+    *x_next = c;
+  }
+  *branch = square ? 0 : 1;
+  *t_x = tx;
+  *t_sq = tsq;
   SPAMM_API_END
+}
+
+int spamm_reserve_pool(int64_t bytes, void* stream) {
+  if (bytes < 0) return fail(SPAMM_EINVAL, "negative size");
+  SPAMM_API_BEGIN
+  spamm::reserve_pool((size_t)bytes, S(stream));
+  SPAMM_API_END
+}
+
+int spamm_set_symmetric_products(int32_t enabled) {
+  g_sym_enabled = enabled != 0;
+  return SPAMM_OK;
 }
 
 int spamm_census(const spamm_mat* a, const spamm_mat* b, double tau, void* stream,
@@ -315,7 +473,9 @@ int spamm_census(const spamm_mat* a, const spamm_mat* b, double tau, void* strea
   SPAMM_API_BEGIN
   cudaStream_t s = S(stream);
   spamm::CullResult r;
-  spamm::cull(a->m, b->m, tau, false, r, s);
+  const bool sym = g_sym_enabled && a == b && a->m.sym;
+  if (!sym || !spamm::cull(a->m, b->m, tau, false, r, s, true))
+    spamm::cull(a->m, b->m, tau, false, r, s, false);
   fill_stats(stats, tau, r, a->m.nb);
   r.release(s);
   SPAMM_API_END
@@ -364,8 +524,8 @@ int spamm_gemm_batch(const int64_t* a_pos, const int64_t* b_pos, const int64_t* 
   k_seg_build<<<spamm::grid_for(n_tasks, 256), 256, 0, s>>>(c_pos, flags, off, n_tasks, seg, c_out,
                                                              nseg);
   SPAMM_LAUNCH_CK();
-  spamm::leaf_products<int64_t>(nseg, seg, a_pos, b_pos, c_out, true, a_data, a_blocks, b_data,
-                                b_blocks, c_data, block_size, kernel, s);
+  spamm::leaf_products<int64_t>(nseg, seg, a_pos, b_pos, c_out, nullptr, true, a_data, a_blocks,
+                                b_data, b_blocks, c_data, block_size, kernel, s);
   spamm::dfree(flags, s);
   spamm::dfree(off, s);
   spamm::dfree(seg, s);
@@ -405,6 +565,7 @@ int spamm_sp2_update(const spamm_mat* x, const spamm_mat* x2, int32_t want_idem,
   spamm::sp2_update(x->m, x2->m, want_idem != 0, expand != 0, idem_norm, h ? h->m : dummy, s);
   if (h) {
     h->m.stream = s;
+    h->m.sym = x->m.sym && x2->m.sym;
     *e_out = h;
   }
   SPAMM_API_END

@@ -59,7 +59,8 @@ __global__ void __launch_bounds__(CULL_THREADS)
                   int32_t* __restrict__ ci_o, int32_t* __restrict__ cj_o,
                   int64_t* __restrict__ seg_o, int32_t* __restrict__ K_o,
                   const int32_t* __restrict__ slotA, const int32_t* __restrict__ slotB,
-                  int32_t* __restrict__ aidx, int32_t* __restrict__ bidx, int64_t Mn, int64_t Vn) {
+                  int32_t* __restrict__ aidx, int32_t* __restrict__ bidx, int64_t Mn, int64_t Vn,
+                  int sym, unsigned long long* __restrict__ aux) {
   const int64_t W = int64_t(1) << t1;
   const double* A = nA + tier_offset(t1);
   const double* B = nB + tier_offset(t1);
@@ -74,6 +75,13 @@ __global__ void __launch_bounds__(CULL_THREADS)
 #pragma unroll 1
     for (int c = 0; c < 4; ++c) {
       const int64_t row = 2 * I + (c >> 1), col = 2 * J + (c & 1);
+      // Symmetric mode (A == B == X, X = X^T bitwise): only C nodes with
+      // i <= j are carried; the lower child of a diagonal parent is the
+      // mirror of its (0,1) child and is skipped.
+      if (sym && row > col) {
+        if (!WRITE && lane == 0) cnt4[4 * p + c] = 0;
+        continue;
+      }
       const double* Arow = A + row * W;
       int64_t toff = 0;
       if (WRITE) {
@@ -94,6 +102,12 @@ __global__ void __launch_bounds__(CULL_THREADS)
         const int64_t kk = valid ? 2 * (int64_t)K[q] + (lane & 1) : 0;
         const bool keep = valid && keep_pair(Arow[kk], B[kk * W + col], tau);
         const unsigned mask = __ballot_sync(0xffffffffu, keep);
+        if (!WRITE && sym && row != col) {
+          // mirror triple (col, kk, row) must agree, else the survivor set is
+          // not symmetric (an ulp tie between norm(X_ik) and norm(X_ki^T)).
+          const bool keep_m = valid && keep_pair(A[col * W + kk], B[kk * W + row], tau);
+          if (__any_sync(0xffffffffu, keep != keep_m) && lane == 0) atomicOr(aux + 1, 1ull);
+        }
         if (WRITE) {
           if (keep) {
             const int64_t pos = toff + __popc(mask & lt_mask);
@@ -108,8 +122,13 @@ __global__ void __launch_bounds__(CULL_THREADS)
           cnt += __popc(mask);
         }
       }
-      if (!WRITE && lane == 0)
+      if (!WRITE && lane == 0) {
         cnt4[4 * p + c] = cnt + (cnt > 0 ? (int64_t(1) << NODE_SHIFT) : 0);
+        if (sym && row == col && cnt) {
+          atomicAdd(aux, (unsigned long long)cnt);
+          atomicAdd(aux + 3, 1ull);
+        }
+      }
     }
   }
 }
@@ -131,33 +150,39 @@ void CullResult::release(cudaStream_t s) {
   n_c = n_tasks = 0;
 }
 
-void cull(const Mat& a, const Mat& b, double tau, bool want_tasks, CullResult& r,
-          cudaStream_t s) {
+bool cull(const Mat& a, const Mat& b, double tau, bool want_tasks, CullResult& r, cudaStream_t s,
+          bool sym) {
   const int depth = a.depth;
   r.visited.assign(depth + 1, 0);
   r.culled.assign(depth + 1, 0);
   r.n_c = r.n_tasks = 0;
+  r.sym = sym;
 
   int32_t* ci = dmalloc<int32_t>(1, s);
   int32_t* cj = dmalloc<int32_t>(1, s);
   int64_t* seg = dmalloc<int64_t>(2, s);
   int32_t* K = dmalloc<int32_t>(1, s);
-  int64_t* cnt = dmalloc<int64_t>(1, s);
+  // aux[0]: survivors in diagonal C nodes (symmetric mode), aux[1]: mirror
+  // mismatch flag, aux[2]: packed scan total (root count first), aux[3]:
+  // diagonal C nodes with survivors.
+  int64_t* aux = dmalloc<int64_t>(4, s);
+  SPAMM_CK(cudaMemsetAsync(aux, 0, 4 * sizeof(int64_t), s));
   int32_t* aidx = nullptr;
   int32_t* bidx = nullptr;
   if (depth == 0 && want_tasks) {
     aidx = dmalloc<int32_t>(1, s);
     bidx = dmalloc<int32_t>(1, s);
   }
-  k_cull_root<<<1, 1, 0, s>>>(a.norms, b.norms, tau, ci, cj, seg, K, cnt, a.slot, b.slot, aidx,
-                              bidx);
+  k_cull_root<<<1, 1, 0, s>>>(a.norms, b.norms, tau, ci, cj, seg, K, aux + 2, a.slot, b.slot,
+                              aidx, bidx);
   SPAMM_LAUNCH_CK();
   int64_t V = 0;
-  d2h_sync(&V, cnt, 1, s);
-  dfree(cnt, s);
+  d2h_sync(&V, aux + 2, 1, s);
   r.visited[0] = V;
   r.culled[0] = 1 - V;
   int64_t M = V;
+  int64_t full_prev = V;  // the root node is diagonal: full count == emitted count
+  int64_t diag_nodes = V;
 
   auto free_level = [&]() {
     dfree(ci, s);
@@ -177,16 +202,30 @@ void cull(const Mat& a, const Mat& b, double tau, bool want_tasks, CullResult& r
     const bool leaf = t1 == depth;
     int64_t* cnt4 = dmalloc<int64_t>(4 * M, s);
     int64_t* off4 = dmalloc<int64_t>(4 * M + 1, s);
+    SPAMM_CK(cudaMemsetAsync(aux, 0, 4 * sizeof(int64_t), s));
     k_cull_expand<false, false><<<cull_grid(M), CULL_THREADS, 0, s>>>(
         t1, a.norms, b.norms, tau, M, ci, cj, seg, K, cnt4, nullptr, nullptr, nullptr, nullptr,
-        nullptr, nullptr, nullptr, nullptr, nullptr, 0, 0);
+        nullptr, nullptr, nullptr, nullptr, nullptr, 0, 0, sym ? 1 : 0,
+        reinterpret_cast<unsigned long long*>(aux));
     SPAMM_LAUNCH_CK();
     scan_exclusive_i64(cnt4, 4 * M, off4, s);
-    int64_t packed = 0;
-    d2h_sync(&packed, off4 + 4 * M, 1, s);
+    SPAMM_CK(cudaMemcpyAsync(aux + 2, off4 + 4 * M, sizeof(int64_t), cudaMemcpyDeviceToDevice, s));
+    int64_t h[4];
+    d2h_sync(h, aux, 4, s);
+    diag_nodes = h[3];
+    if (h[1]) {  // survivor set not symmetric: the caller falls back to the full cull
+      dfree(cnt4, s);
+      dfree(off4, s);
+      free_level();
+      dfree(aux, s);
+      return false;
+    }
+    const int64_t packed = h[2];
     const int64_t Vn = packed & TASK_MASK, Mn = packed >> NODE_SHIFT;
-    r.visited[t1] = Vn;
-    r.culled[t1] = 8 * V - Vn;
+    const int64_t full = sym ? 2 * Vn - h[0] : Vn;
+    r.visited[t1] = full;
+    r.culled[t1] = 8 * full_prev - full;
+    full_prev = full;
     if (Vn == 0 || (leaf && !want_tasks)) {
       dfree(cnt4, s);
       dfree(off4, s);
@@ -207,11 +246,11 @@ void cull(const Mat& a, const Mat& b, double tau, bool want_tasks, CullResult& r
       bi = dmalloc<int32_t>(Vn, s);
       k_cull_expand<true, true><<<cull_grid(M), CULL_THREADS, 0, s>>>(
           t1, a.norms, b.norms, tau, M, ci, cj, seg, K, nullptr, off4, ci_o, cj_o, seg_o, K_o,
-          a.slot, b.slot, ai, bi, Mn, Vn);
+          a.slot, b.slot, ai, bi, Mn, Vn, sym ? 1 : 0, nullptr);
     } else {
       k_cull_expand<true, false><<<cull_grid(M), CULL_THREADS, 0, s>>>(
           t1, a.norms, b.norms, tau, M, ci, cj, seg, K, nullptr, off4, ci_o, cj_o, seg_o, K_o,
-          nullptr, nullptr, nullptr, nullptr, Mn, Vn);
+          nullptr, nullptr, nullptr, nullptr, Mn, Vn, sym ? 1 : 0, nullptr);
     }
     SPAMM_LAUNCH_CK();
     dfree(cnt4, s);
@@ -226,9 +265,11 @@ void cull(const Mat& a, const Mat& b, double tau, bool want_tasks, CullResult& r
     V = Vn;
     M = Mn;
   }
+  dfree(aux, s);
   // Tiers after an early exit keep zero counts (kernel.py:114-117).
   if (V > 0 && want_tasks && ci != nullptr) {
     r.n_c = M;
+    r.n_c_full = sym ? 2 * M - diag_nodes : M;
     r.n_tasks = V;
     r.ci = ci;
     r.cj = cj;
@@ -240,6 +281,7 @@ void cull(const Mat& a, const Mat& b, double tau, bool want_tasks, CullResult& r
     free_level();
     if (!want_tasks) r.n_tasks = r.visited[depth];
   }
+  return true;
 }
 
 }  // namespace spamm

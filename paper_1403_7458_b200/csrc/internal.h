@@ -12,6 +12,7 @@ namespace spamm {
 // ---- stream-ordered device memory (cudaMallocAsync on the default pool) ----
 void* dmalloc_bytes(size_t bytes, cudaStream_t s);
 void dfree(void* p, cudaStream_t s);
+void reserve_pool(size_t bytes, cudaStream_t s);
 template <class T>
 T* dmalloc(size_t n, cudaStream_t s) {
   return static_cast<T*>(dmalloc_bytes(n * sizeof(T), s));
@@ -33,9 +34,15 @@ struct Mat {
   int32_t* slot = nullptr;   // G * G, storage slot or -1
   double* norms = nullptr;   // pyramid_size(depth)
   double* norms2 = nullptr;  // pyramid_size(depth)
+  bool sym = false;          // X == X^T bitwise (blocks and null structure)
+  mutable double tr = 0.0;   // cached trace (matrices are immutable)
+  mutable bool tr_valid = false;
   cudaStream_t stream = nullptr;
   void release();
 };
+
+// Exact-symmetry test (block (i,j) == transpose of block (j,i), bitwise).
+bool is_symmetric(const Mat& m, cudaStream_t s);
 
 // Finalise a matrix whose data/keys (nblocks, Morton order) are set: prune
 // exact-zero blocks, build slot map and the bit-exact norm pyramid
@@ -48,6 +55,19 @@ void finalize(Mat& m, cudaStream_t s, double* pre_n2 = nullptr, uint8_t* pre_nz 
 //   expand     -> E = add_scaled(2, X, -1, X2) finalised into `e`.
 void sp2_update(const Mat& x, const Mat& x2, bool want_idem, bool expand, double* idem_norm,
                 Mat& e, cudaStream_t s);
+// The same in two halves, so the union size U can ride on another host sync:
+// prepare launches the key-union flags + scan (U lands in *u_dev, no sync);
+// finish runs the fused pass given U.  Block sizes other than 32 / 64 are not
+// supported by the split form (sp2_update handles them).
+struct UnionPrep {
+  uint8_t* flags = nullptr;
+  int64_t* off = nullptr;
+  int64_t npos = 0;
+};
+UnionPrep sp2_union_prepare(const Mat& x, const Mat& x2, int64_t* u_dev, cudaStream_t s);
+void sp2_update_finish(const Mat& x, const Mat& x2, UnionPrep& prep, int64_t U, bool want_idem,
+                       bool expand, double* idem_norm, Mat& e, cudaStream_t s);
+bool sp2_fused_supported(int nb);
 
 void scatter_slots(const int64_t* keys, int64_t m, int32_t* slot, cudaStream_t s);
 // Leaf norm^2 (einsum recipe) and nonzero flags for m blocks of nb x nb.
@@ -65,6 +85,7 @@ void scan_exclusive_i64(const int64_t* in, int64_t n, int64_t* out, cudaStream_t
 // ---- culling ----
 struct CullResult {
   int64_t n_c = 0;            // C blocks (leaf-tier nodes with >= 1 survivor)
+  int64_t n_c_full = 0;       // C blocks including mirrors (symmetric mode)
   int64_t n_tasks = 0;        // surviving leaf products
   int32_t* ci = nullptr;      // n_c
   int32_t* cj = nullptr;      // n_c
@@ -72,13 +93,17 @@ struct CullResult {
   int32_t* k = nullptr;       // n_tasks
   int32_t* a_idx = nullptr;   // n_tasks (storage slot of A_ik)
   int32_t* b_idx = nullptr;   // n_tasks (storage slot of B_kj)
-  std::vector<int64_t> visited, culled;
+  std::vector<int64_t> visited, culled;  // full (reference) counts in both modes
+  bool sym = false;                      // only C nodes with i <= j were carried
   void release(cudaStream_t s);
 };
 // Tiered culling (kernel.py:96-122).  want_tasks=false: census only
 // (kernel.py:226-239) -- counts for every tier, no leaf task list.
-void cull(const Mat& a, const Mat& b, double tau, bool want_tasks, CullResult& r,
-          cudaStream_t s);
+// sym=true (A == B symmetric): carry only C nodes i <= j, count the full set as
+// 2 * emitted - diagonal; returns false (nothing allocated) if a mirror triple
+// disagrees on the tau test (an ulp tie), so the caller re-runs the full cull.
+bool cull(const Mat& a, const Mat& b, double tau, bool want_tasks, CullResult& r, cudaStream_t s,
+          bool sym = false);
 
 // ---- leaf products ----
 // LEAF_DMMA_CPASYNC: the first-generation DMMA kernel (cp.async ring, one CTA
@@ -86,18 +111,20 @@ void cull(const Mat& a, const Mat& b, double tau, bool want_tasks, CullResult& r
 // Nb in {32, 64}.
 enum LeafKernel { LEAF_AUTO = 0, LEAF_DMMA = 1, LEAF_EXACT = 2, LEAF_DMMA_CPASYNC = 3 };
 // For each segment m: C[c_out ? c_out[m] : m] (+)= sum_{t in seg m} A[a_idx[t]] * B[b_idx[t]]
+// and, when c_mirror && c_mirror[m] >= 0, C[c_mirror[m]] = transpose of that block.
 // a_blocks / b_blocks: number of blocks addressable in A / B (TMA bounds).
 template <class Idx>
 void leaf_products(int64_t n_seg, const int64_t* seg, const Idx* a_idx, const Idx* b_idx,
-                   const int64_t* c_out, bool accumulate, const double* A, int64_t a_blocks,
-                   const double* B, int64_t b_blocks, double* C, int nb, int kernel,
-                   cudaStream_t s);
+                   const int64_t* c_out, const int64_t* c_mirror, bool accumulate,
+                   const double* A, int64_t a_blocks, const double* B, int64_t b_blocks,
+                   double* C, int nb, int kernel, cudaStream_t s);
 bool dmma_supported(int nb);
 bool tma_leaf_supported(int nb);
 template <class Idx>
 void leaf_products_tma(int64_t n_seg, const int64_t* seg, const Idx* a_idx, const Idx* b_idx,
-                       const int64_t* c_out, bool accumulate, const double* A, int64_t a_blocks,
-                       const double* B, int64_t b_blocks, double* C, int nb, cudaStream_t s);
+                       const int64_t* c_out, const int64_t* c_mirror, bool accumulate,
+                       const double* A, int64_t a_blocks, const double* B, int64_t b_blocks,
+                       double* C, int nb, cudaStream_t s);
 
 // ---- element-wise / reductions ----
 void from_dense(const double* dense, int64_t n, int64_t ld, Mat& m, cudaStream_t s);
@@ -105,7 +132,8 @@ void to_dense(const Mat& m, double* dense, int64_t ld, cudaStream_t s);
 void identity(Mat& m, cudaStream_t s);
 void add_scaled(double alpha, const Mat& a, double beta, const Mat& b, Mat& out,
                 cudaStream_t s);
-double trace(const Mat& m, cudaStream_t s);
+double trace(const Mat& m, cudaStream_t s);  // cached per matrix
+void trace_launch(const Mat& m, double* dev_out, cudaStream_t s);  // no host sync
 void gershgorin(const Mat& f, double* eps_min, double* eps_max, double* asym, cudaStream_t s);
 
 }  // namespace spamm

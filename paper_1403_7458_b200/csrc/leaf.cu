@@ -46,7 +46,8 @@ struct DmmaCfg {
 template <int NB, int WARPS_M, int WARPS_N, int STAGES, class Idx>
 __global__ void __launch_bounds__(32 * WARPS_M* WARPS_N)
     k_leaf_dmma(const int64_t* __restrict__ seg, const Idx* __restrict__ a_idx,
-                const Idx* __restrict__ b_idx, const int64_t* __restrict__ c_out, int accumulate,
+                const Idx* __restrict__ b_idx, const int64_t* __restrict__ c_out,
+                const int64_t* __restrict__ c_mirror, int accumulate,
                 const double* __restrict__ A, const double* __restrict__ B, double* __restrict__ C) {
   using Cfg = DmmaCfg<NB, WARPS_M, WARPS_N, STAGES>;
   constexpr int NTHR = Cfg::THREADS, LD = Cfg::LD, TILE = Cfg::TILE;
@@ -130,6 +131,18 @@ __global__ void __launch_bounds__(32 * WARPS_M* WARPS_N)
       v.y = acc[mt][nt][1];
       *reinterpret_cast<double2*>(Cb + (wm * WTM + mt * 8 + r8) * NB + wn * WTN + nt * 8 + 2 * c4) = v;
     }
+  const int64_t mi = c_mirror ? c_mirror[m] : -1;
+  if (mi >= 0) {
+    double* Cm = C + mi * (int64_t)(NB * NB);
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        const int r = wm * WTM + mt * 8 + r8, c = wn * WTN + nt * 8 + 2 * c4;
+        Cm[c * NB + r] = acc[mt][nt][0];
+        Cm[(c + 1) * NB + r] = acc[mt][nt][1];
+      }
+  }
 }
 
 // Exact path, nb <= 64: blocks staged in smem, each thread owns EPT elements.
@@ -137,7 +150,8 @@ template <class Idx, int EPT>
 __global__ void __launch_bounds__(256)
     k_leaf_exact_smem(const int64_t* __restrict__ seg, const Idx* __restrict__ a_idx,
                       const Idx* __restrict__ b_idx, const int64_t* __restrict__ c_out,
-                      int accumulate, const double* __restrict__ A, const double* __restrict__ B,
+                      const int64_t* __restrict__ c_mirror, int accumulate,
+                      const double* __restrict__ A, const double* __restrict__ B,
                       double* __restrict__ C, int nb) {
   extern __shared__ __align__(16) double sm[];
   const int nb2 = nb * nb;
@@ -172,10 +186,15 @@ __global__ void __launch_bounds__(256)
       }
     }
   }
+  const int64_t mi = c_mirror ? c_mirror[m] : -1;
+  double* Cm = mi >= 0 ? C + mi * (int64_t)nb2 : nullptr;
 #pragma unroll
   for (int r = 0; r < EPT; ++r) {
     const int e = threadIdx.x + r * blockDim.x;
-    if (e < nb2) Cb[e] = acc[r];
+    if (e < nb2) {
+      Cb[e] = acc[r];
+      if (Cm) Cm[(e % nb) * nb + e / nb] = acc[r];
+    }
   }
 }
 
@@ -184,7 +203,8 @@ template <class Idx>
 __global__ void __launch_bounds__(256)
     k_leaf_exact_global(const int64_t* __restrict__ seg, const Idx* __restrict__ a_idx,
                         const Idx* __restrict__ b_idx, const int64_t* __restrict__ c_out,
-                        int accumulate, const double* __restrict__ A, const double* __restrict__ B,
+                        const int64_t* __restrict__ c_mirror, int accumulate,
+                        const double* __restrict__ A, const double* __restrict__ B,
                         double* __restrict__ C, int nb) {
   const int64_t nb2 = (int64_t)nb * nb;
   const int64_t m = blockIdx.x;
@@ -199,12 +219,14 @@ __global__ void __launch_bounds__(256)
     for (int kk = 0; kk < nb; ++kk) c = __dadd_rn(c, __dmul_rn(__ldg(a + kk), __ldg(b + (int64_t)kk * nb)));
   }
   Cb[e] = c;
+  const int64_t mi = c_mirror ? c_mirror[m] : -1;
+  if (mi >= 0) C[mi * nb2 + j * nb + i] = c;
 }
 
 template <int NB, int WM, int WN, int ST, class Idx>
 void launch_dmma(int64_t n_seg, const int64_t* seg, const Idx* a_idx, const Idx* b_idx,
-                 const int64_t* c_out, bool acc, const double* A, const double* B, double* C,
-                 cudaStream_t s) {
+                 const int64_t* c_out, const int64_t* c_mirror, bool acc, const double* A,
+                 const double* B, double* C, cudaStream_t s) {
   using Cfg = DmmaCfg<NB, WM, WN, ST>;
   auto kern = k_leaf_dmma<NB, WM, WN, ST, Idx>;
   static bool attr_set = false;
@@ -212,7 +234,8 @@ void launch_dmma(int64_t n_seg, const int64_t* seg, const Idx* a_idx, const Idx*
     SPAMM_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM));
     attr_set = true;
   }
-  kern<<<(unsigned)n_seg, Cfg::THREADS, Cfg::SMEM, s>>>(seg, a_idx, b_idx, c_out, acc ? 1 : 0, A, B, C);
+  kern<<<(unsigned)n_seg, Cfg::THREADS, Cfg::SMEM, s>>>(seg, a_idx, b_idx, c_out, c_mirror,
+                                                        acc ? 1 : 0, A, B, C);
   SPAMM_LAUNCH_CK();
 }
 
@@ -222,14 +245,14 @@ bool dmma_supported(int nb) { return nb == 8 || nb == 16 || nb == 32 || nb == 64
 
 template <class Idx>
 void leaf_products(int64_t n_seg, const int64_t* seg, const Idx* a_idx, const Idx* b_idx,
-                   const int64_t* c_out, bool accumulate, const double* A, int64_t a_blocks,
-                   const double* B, int64_t b_blocks, double* C, int nb, int kernel,
-                   cudaStream_t s) {
+                   const int64_t* c_out, const int64_t* c_mirror, bool accumulate,
+                   const double* A, int64_t a_blocks, const double* B, int64_t b_blocks,
+                   double* C, int nb, int kernel, cudaStream_t s) {
   if (n_seg <= 0) return;
   if (n_seg > 0x7fffffffLL) throw CudaError("too many C blocks for one launch");
   if ((kernel == LEAF_AUTO || kernel == LEAF_DMMA) && tma_leaf_supported(nb)) {
-    leaf_products_tma<Idx>(n_seg, seg, a_idx, b_idx, c_out, accumulate, A, a_blocks, B, b_blocks,
-                           C, nb, s);
+    leaf_products_tma<Idx>(n_seg, seg, a_idx, b_idx, c_out, c_mirror, accumulate, A, a_blocks, B,
+                           b_blocks, C, nb, s);
     return;
   }
   const bool dmma = kernel != LEAF_EXACT && dmma_supported(nb);
@@ -237,10 +260,10 @@ void leaf_products(int64_t n_seg, const int64_t* seg, const Idx* a_idx, const Id
     throw CudaError("DMMA leaf kernel needs block size 8, 16, 32 or 64");
   if (dmma) {
     switch (nb) {
-      case 8: launch_dmma<8, 1, 1, 4, Idx>(n_seg, seg, a_idx, b_idx, c_out, accumulate, A, B, C, s); break;
-      case 16: launch_dmma<16, 1, 1, 4, Idx>(n_seg, seg, a_idx, b_idx, c_out, accumulate, A, B, C, s); break;
-      case 32: launch_dmma<32, 2, 2, 4, Idx>(n_seg, seg, a_idx, b_idx, c_out, accumulate, A, B, C, s); break;
-      case 64: launch_dmma<64, 2, 2, 3, Idx>(n_seg, seg, a_idx, b_idx, c_out, accumulate, A, B, C, s); break;
+      case 8: launch_dmma<8, 1, 1, 4, Idx>(n_seg, seg, a_idx, b_idx, c_out, c_mirror, accumulate, A, B, C, s); break;
+      case 16: launch_dmma<16, 1, 1, 4, Idx>(n_seg, seg, a_idx, b_idx, c_out, c_mirror, accumulate, A, B, C, s); break;
+      case 32: launch_dmma<32, 2, 2, 4, Idx>(n_seg, seg, a_idx, b_idx, c_out, c_mirror, accumulate, A, B, C, s); break;
+      case 64: launch_dmma<64, 2, 2, 3, Idx>(n_seg, seg, a_idx, b_idx, c_out, c_mirror, accumulate, A, B, C, s); break;
     }
     return;
   }
@@ -250,9 +273,9 @@ void leaf_products(int64_t n_seg, const int64_t* seg, const Idx* a_idx, const Id
     const int ept = (nb2 + threads - 1) / threads;
     const size_t smem = 2 * (size_t)nb2 * sizeof(double);
     if (ept <= 1) {
-      k_leaf_exact_smem<Idx, 1><<<(unsigned)n_seg, threads, smem, s>>>(seg, a_idx, b_idx, c_out, accumulate, A, B, C, nb);
+      k_leaf_exact_smem<Idx, 1><<<(unsigned)n_seg, threads, smem, s>>>(seg, a_idx, b_idx, c_out, c_mirror, accumulate, A, B, C, nb);
     } else if (ept <= 4) {
-      k_leaf_exact_smem<Idx, 4><<<(unsigned)n_seg, threads, smem, s>>>(seg, a_idx, b_idx, c_out, accumulate, A, B, C, nb);
+      k_leaf_exact_smem<Idx, 4><<<(unsigned)n_seg, threads, smem, s>>>(seg, a_idx, b_idx, c_out, c_mirror, accumulate, A, B, C, nb);
     } else {
       auto kern = k_leaf_exact_smem<Idx, 16>;
       static bool attr = false;
@@ -260,20 +283,20 @@ void leaf_products(int64_t n_seg, const int64_t* seg, const Idx* a_idx, const Id
         SPAMM_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 64 * 64 * 8));
         attr = true;
       }
-      kern<<<(unsigned)n_seg, threads, smem, s>>>(seg, a_idx, b_idx, c_out, accumulate, A, B, C, nb);
+      kern<<<(unsigned)n_seg, threads, smem, s>>>(seg, a_idx, b_idx, c_out, c_mirror, accumulate, A, B, C, nb);
     }
   } else {
     dim3 grid((unsigned)n_seg, (unsigned)((nb2 + 255) / 256));
-    k_leaf_exact_global<Idx><<<grid, 256, 0, s>>>(seg, a_idx, b_idx, c_out, accumulate, A, B, C, nb);
+    k_leaf_exact_global<Idx><<<grid, 256, 0, s>>>(seg, a_idx, b_idx, c_out, c_mirror, accumulate, A, B, C, nb);
   }
   SPAMM_LAUNCH_CK();
 }
 
 template void leaf_products<int32_t>(int64_t, const int64_t*, const int32_t*, const int32_t*,
-                                     const int64_t*, bool, const double*, int64_t, const double*,
-                                     int64_t, double*, int, int, cudaStream_t);
+                                     const int64_t*, const int64_t*, bool, const double*, int64_t,
+                                     const double*, int64_t, double*, int, int, cudaStream_t);
 template void leaf_products<int64_t>(int64_t, const int64_t*, const int64_t*, const int64_t*,
-                                     const int64_t*, bool, const double*, int64_t, const double*,
-                                     int64_t, double*, int, int, cudaStream_t);
+                                     const int64_t*, const int64_t*, bool, const double*, int64_t,
+                                     const double*, int64_t, double*, int, int, cudaStream_t);
 
 }  // namespace spamm

@@ -91,7 +91,7 @@ __global__ void __launch_bounds__(32 * (WARPS_M * WARPS_N + 1), 1)
     k_leaf_dmma_tma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     int64_t n_seg, const int64_t* __restrict__ seg, const Idx* __restrict__ a_idx,
                     const Idx* __restrict__ b_idx, const int64_t* __restrict__ c_out,
-                    int accumulate, double* __restrict__ C) {
+                    const int64_t* __restrict__ c_mirror, int accumulate, double* __restrict__ C) {
   using Cfg = TmaCfg<NB, WARPS_M, WARPS_N, STAGES>;
   constexpr int WTM = NB / WARPS_M, WTN = NB / WARPS_N, MT = WTM / 8, NT = WTN / 8;
   static_assert(WTN % 8 == 0 && WTM % 8 == 0, "warp tile must be a multiple of 8");
@@ -212,6 +212,20 @@ __global__ void __launch_bounds__(32 * (WARPS_M * WARPS_N + 1), 1)
         v.y = acc[mt][nt][1];
         *reinterpret_cast<double2*>(Cb + (row0 + mt * 8 + r8) * NB + col0 + nt * 8 + 2 * c4) = v;
       }
+    // Symmetric product: the mirror block C_ji = C_ij^T (bitwise what the full
+    // product computes).
+    const int64_t mi = c_mirror ? c_mirror[m] : -1;
+    if (mi >= 0) {
+      double* Cm = C + mi * (int64_t)(NB * NB);
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          const int r = row0 + mt * 8 + r8, c = col0 + nt * 8 + 2 * c4;
+          Cm[c * NB + r] = acc[mt][nt][0];
+          Cm[(c + 1) * NB + r] = acc[mt][nt][1];
+        }
+    }
   }
 }
 
@@ -257,8 +271,8 @@ int sm_count() {
 
 template <int NB, int WM, int WN, int ST, int CTAS_PER_SM, class Idx>
 void launch_tma(int64_t n_seg, const int64_t* seg, const Idx* a_idx, const Idx* b_idx,
-                const int64_t* c_out, bool acc, const double* A, int64_t a_blocks, const double* B,
-                int64_t b_blocks, double* C, cudaStream_t s) {
+                const int64_t* c_out, const int64_t* c_mirror, bool acc, const double* A,
+                int64_t a_blocks, const double* B, int64_t b_blocks, double* C, cudaStream_t s) {
   using Cfg = TmaCfg<NB, WM, WN, ST>;
   auto kern = k_leaf_dmma_tma<NB, WM, WN, ST, Idx>;
   static std::once_flag once;
@@ -269,7 +283,7 @@ void launch_tma(int64_t n_seg, const int64_t* seg, const Idx* a_idx, const Idx* 
   int64_t grid = (int64_t)sm_count() * CTAS_PER_SM;
   if (grid > n_seg) grid = n_seg;
   kern<<<(unsigned)grid, Cfg::THREADS, Cfg::SMEM, s>>>(ta, tb, n_seg, seg, a_idx, b_idx, c_out,
-                                                       acc ? 1 : 0, C);
+                                                       c_mirror, acc ? 1 : 0, C);
   SPAMM_LAUNCH_CK();
 }
 
@@ -279,24 +293,27 @@ bool tma_leaf_supported(int nb) { return nb == 32 || nb == 64; }
 
 template <class Idx>
 void leaf_products_tma(int64_t n_seg, const int64_t* seg, const Idx* a_idx, const Idx* b_idx,
-                       const int64_t* c_out, bool accumulate, const double* A, int64_t a_blocks,
-                       const double* B, int64_t b_blocks, double* C, int nb, cudaStream_t s) {
+                       const int64_t* c_out, const int64_t* c_mirror, bool accumulate,
+                       const double* A, int64_t a_blocks, const double* B, int64_t b_blocks,
+                       double* C, int nb, cudaStream_t s) {
   if (n_seg <= 0) return;
   if (nb == 64)
-    launch_tma<64, 2, 4, 3, 1, Idx>(n_seg, seg, a_idx, b_idx, c_out, accumulate, A, a_blocks, B,
-                                    b_blocks, C, s);
+    launch_tma<64, 2, 4, 3, 1, Idx>(n_seg, seg, a_idx, b_idx, c_out, c_mirror, accumulate, A,
+                                    a_blocks, B, b_blocks, C, s);
   else if (nb == 32)
-    launch_tma<32, 2, 2, 6, 2, Idx>(n_seg, seg, a_idx, b_idx, c_out, accumulate, A, a_blocks, B,
-                                    b_blocks, C, s);
+    launch_tma<32, 2, 2, 6, 2, Idx>(n_seg, seg, a_idx, b_idx, c_out, c_mirror, accumulate, A,
+                                    a_blocks, B, b_blocks, C, s);
   else
     throw CudaError("TMA leaf kernel needs block size 32 or 64");
 }
 
 template void leaf_products_tma<int32_t>(int64_t, const int64_t*, const int32_t*, const int32_t*,
-                                         const int64_t*, bool, const double*, int64_t,
-                                         const double*, int64_t, double*, int, cudaStream_t);
+                                         const int64_t*, const int64_t*, bool, const double*,
+                                         int64_t, const double*, int64_t, double*, int,
+                                         cudaStream_t);
 template void leaf_products_tma<int64_t>(int64_t, const int64_t*, const int64_t*, const int64_t*,
-                                         const int64_t*, bool, const double*, int64_t,
-                                         const double*, int64_t, double*, int, cudaStream_t);
+                                         const int64_t*, const int64_t*, bool, const double*,
+                                         int64_t, const double*, int64_t, double*, int,
+                                         cudaStream_t);
 
 }  // namespace spamm

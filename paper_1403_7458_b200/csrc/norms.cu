@@ -44,6 +44,14 @@ void dfree(void* p, cudaStream_t s) {
   if (p) cudaFreeAsync(p, s);
 }
 
+void reserve_pool(size_t bytes, cudaStream_t s) {
+  // Grow the stream-ordered pool once (release threshold is unlimited, so the
+  // pages stay mapped): later cudaMallocAsync calls never block on a mapping.
+  void* p = dmalloc_bytes(bytes, s);
+  dfree(p, s);
+  SPAMM_CK(cudaStreamSynchronize(s));
+}
+
 void d2h_sync(int64_t* host, const int64_t* dev, int n, cudaStream_t s) {
   static thread_local int64_t* pinned = nullptr;
   if (!pinned) SPAMM_CK(cudaMallocHost(&pinned, 64 * sizeof(int64_t)));

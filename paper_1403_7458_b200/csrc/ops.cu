@@ -319,7 +319,38 @@ __global__ void k_minmax(const double* __restrict__ lo, const double* __restrict
 
 int warp_grid(int64_t nwarps) { return grid_for(nwarps * 32, 32 * WARPS_PER_CTA, 148LL * 64); }
 
+// Exact symmetry: every stored block (i,j) equals the transpose of block (j,i).
+__global__ void k_symmetric(const double* __restrict__ data, const int64_t* __restrict__ keys,
+                            const int32_t* __restrict__ slot, int64_t m, int nb, int64_t G,
+                            int* __restrict__ bad) {
+  const int nb2 = nb * nb;
+  for (int64_t b = blockIdx.x; b < m; b += gridDim.x) {
+    const int64_t key = keys[b], bi = key / G, bj = key % G;
+    const int32_t t = slot[bj * G + bi];
+    bool ok = t >= 0;
+    if (ok)
+      for (int e = threadIdx.x; e < nb2; e += blockDim.x) {
+        const int r = e / nb, c = e % nb;
+        ok &= data[b * nb2 + e] == data[(int64_t)t * nb2 + c * nb + r];
+      }
+    if (!__syncthreads_and(ok) && threadIdx.x == 0) *bad = 1;
+  }
+}
+
 }  // namespace
+
+bool is_symmetric(const Mat& m, cudaStream_t s) {
+  if (m.nblocks == 0) return true;
+  int64_t* flag = dmalloc<int64_t>(1, s);
+  SPAMM_CK(cudaMemsetAsync(flag, 0, sizeof(int64_t), s));
+  k_symmetric<<<grid_for(m.nblocks, 1, 148LL * 16), 256, 0, s>>>(
+      m.data, m.keys, m.slot, m.nblocks, m.nb, m.G, reinterpret_cast<int*>(flag));
+  SPAMM_LAUNCH_CK();
+  int64_t h = 0;
+  d2h_sync(&h, flag, 1, s);
+  dfree(flag, s);
+  return h == 0;
+}
 
 void from_dense(const double* dense, int64_t n, int64_t ld, Mat& m, cudaStream_t s) {
   const int64_t G = int64_t(1) << m.depth, npos = G * G;
@@ -341,6 +372,7 @@ void from_dense(const double* dense, int64_t n, int64_t ld, Mat& m, cudaStream_t
   dfree(flags, s);
   dfree(off, s);
   finalize(m, s);
+  m.sym = is_symmetric(m, s);
 }
 
 void to_dense(const Mat& m, double* dense, int64_t ld, cudaStream_t s) {
@@ -362,6 +394,7 @@ void identity(Mat& m, cudaStream_t s) {
   k_identity<<<grid_for(n_diag, 128), 128, 0, s>>>(m.n_native, m.nb, G, n_diag, m.data, m.keys);
   SPAMM_LAUNCH_CK();
   finalize(m, s);
+  m.sym = true;
 }
 
 void add_scaled(double alpha, const Mat& a, double beta, const Mat& b, Mat& out, cudaStream_t s) {
@@ -389,22 +422,32 @@ void add_scaled(double alpha, const Mat& a, double beta, const Mat& b, Mat& out,
   dfree(flags, s);
   dfree(off, s);
   finalize(out, s);
+  out.sym = a.sym && b.sym;
 }
 
-double trace(const Mat& m, cudaStream_t s) {
-  double* partial = dmalloc<double>(m.G + 1, s);
+void trace_launch(const Mat& m, double* dev_out, cudaStream_t s) {
+  double* partial = dmalloc<double>(m.G, s);
   uint8_t* present = dmalloc<uint8_t>(m.G, s);
   k_trace_blocks<<<grid_for(m.G * 32, 256), 256, 0, s>>>(m.slot, m.data, m.G, m.nb, partial,
                                                           present);
   SPAMM_LAUNCH_CK();
-  k_trace<<<1, 32, 0, s>>>(m.slot, m.data, m.G, m.nb, partial, present, partial + m.G);
+  k_trace<<<1, 32, 0, s>>>(m.slot, m.data, m.G, m.nb, partial, present, dev_out);
   SPAMM_LAUNCH_CK();
-  int64_t bits = 0;
-  d2h_sync(&bits, reinterpret_cast<const int64_t*>(partial + m.G), 1, s);
   dfree(partial, s);
   dfree(present, s);
+}
+
+double trace(const Mat& m, cudaStream_t s) {
+  if (m.tr_valid) return m.tr;
+  int64_t* buf = dmalloc<int64_t>(1, s);
+  trace_launch(m, reinterpret_cast<double*>(buf), s);
+  int64_t bits = 0;
+  d2h_sync(&bits, buf, 1, s);
+  dfree(buf, s);
   double v;
   memcpy(&v, &bits, sizeof(v));
+  m.tr = v;
+  m.tr_valid = true;
   return v;
 }
 

@@ -162,21 +162,44 @@ void sp2_update(const Mat& x, const Mat& x2, bool want_idem, bool expand, double
     if (expand) add_scaled(2.0, x, -1.0, x2, e, s);
     return;
   }
-  const int64_t G = x.G, npos = G * G;
-  uint8_t* flags = dmalloc<uint8_t>(npos, s);
-  int64_t* off = dmalloc<int64_t>(npos + 1, s);
-  k_union_keys<<<grid_for(npos, 256), 256, 0, s>>>(x.slot, x2.slot, x.depth, flags);
-  SPAMM_LAUNCH_CK();
-  scan_exclusive_u8(flags, npos, off, s);
+  int64_t* u_dev = dmalloc<int64_t>(1, s);
+  UnionPrep prep = sp2_union_prepare(x, x2, u_dev, s);
   int64_t U = 0;
-  d2h_sync(&U, off + npos, 1, s);
+  d2h_sync(&U, u_dev, 1, s);
+  dfree(u_dev, s);
+  sp2_update_finish(x, x2, prep, U, want_idem, expand, idem_norm, e, s);
+}
+
+bool sp2_fused_supported(int nb) { return nb == 32 || nb == 64; }
+
+UnionPrep sp2_union_prepare(const Mat& x, const Mat& x2, int64_t* u_dev, cudaStream_t s) {
+  UnionPrep p;
+  p.npos = x.G * x.G;
+  p.flags = dmalloc<uint8_t>(p.npos, s);
+  p.off = dmalloc<int64_t>(p.npos + 1, s);
+  k_union_keys<<<grid_for(p.npos, 256), 256, 0, s>>>(x.slot, x2.slot, x.depth, p.flags);
+  SPAMM_LAUNCH_CK();
+  scan_exclusive_u8(p.flags, p.npos, p.off, s);
+  SPAMM_CK(cudaMemcpyAsync(u_dev, p.off + p.npos, sizeof(int64_t), cudaMemcpyDeviceToDevice, s));
+  return p;
+}
+
+void sp2_update_finish(const Mat& x, const Mat& x2, UnionPrep& prep, int64_t U, bool want_idem,
+                       bool expand, double* idem_norm, Mat& e, cudaStream_t s) {
+  const int nb2 = x.nb * x.nb;
   int64_t* ukeys = dmalloc<int64_t>(U, s);
   if (U > 0) {
-    k_union_compact<<<grid_for(npos, 256), 256, 0, s>>>(flags, off, x.depth, ukeys);
+    k_union_compact<<<grid_for(prep.npos, 256), 256, 0, s>>>(prep.flags, prep.off, x.depth, ukeys);
     SPAMM_LAUNCH_CK();
   }
-  dfree(flags, s);
-  dfree(off, s);
+  dfree(prep.flags, s);
+  dfree(prep.off, s);
+  prep.flags = nullptr;
+  prep.off = nullptr;
+  if (!want_idem && !expand) {
+    dfree(ukeys, s);
+    return;
+  }
   double* nD2 = want_idem ? dmalloc<double>(U, s) : nullptr;
   double* nE2 = expand ? dmalloc<double>(U, s) : nullptr;
   uint8_t* nzE = expand ? dmalloc<uint8_t>(U, s) : nullptr;
@@ -207,6 +230,7 @@ void sp2_update(const Mat& x, const Mat& x2, bool want_idem, bool expand, double
     e.data = E;
     e.keys = ukeys;
     finalize(e, s, nE2, nzE);
+    e.sym = x.sym && x2.sym;
   } else {
     dfree(ukeys, s);
   }

@@ -32,7 +32,7 @@ from . import _native as nat
 from .quadtree import QuadTreeMatrix, _check_conformable
 
 __all__ = ["ProductStats", "multiply", "convolution_census", "leaf_gemm", "gemm_batch",
-           "leaf_tasks", "WORKERS_ENV_VAR"]
+           "leaf_tasks", "set_symmetric_products", "WORKERS_ENV_VAR"]
 
 WORKERS_ENV_VAR = "SPAMM_WORKERS"
 
@@ -52,6 +52,9 @@ class ProductStats:
     ms_leaf: float = 0.0
     ms_finalize: float = 0.0
     c_blocks: int = 0
+    # symmetric SpAMM (X*X, X == X^T): leaf products actually executed
+    executed_products: int = 0
+    symmetric: bool = False
 
     def to_json_dict(self) -> dict:
         return {
@@ -107,7 +110,14 @@ def _stats_from(st: nat.Stats, block_size: int, wall: float) -> ProductStats:
         wall_seconds=float(wall),
         ms_cull=float(st.ms_cull), ms_leaf=float(st.ms_leaf),
         ms_finalize=float(st.ms_finalize), c_blocks=int(st.c_blocks),
+        executed_products=int(st.executed_products), symmetric=bool(st.symmetric),
     )
+
+
+def set_symmetric_products(enabled: bool) -> None:
+    """Toggle the symmetric SpAMM path (on by default; results are bitwise
+    identical either way -- the switch exists for A/B measurements)."""
+    nat.check(nat.load().spamm_set_symmetric_products(1 if enabled else 0))
 
 
 def multiply(a: QuadTreeMatrix, b: QuadTreeMatrix, tau: float, mode: str = "serial",
@@ -205,3 +215,9 @@ def leaf_gemm(a: np.ndarray, b: np.ndarray, c: np.ndarray) -> np.ndarray:
     gemm_batch(z, z, z, ad, bd, cd, kernel="exact")
     c[...] = cd.reshape(nb, nb).cpu().numpy()
     return c
+
+
+def reserve_memory(nbytes: int) -> None:
+    """Pre-grow the library's device memory pool (kept mapped) so steady-state
+    allocations never block on new mappings; e.g. a few x the matrix size."""
+    nat.check(nat.load().spamm_reserve_pool(int(nbytes), nat.current_stream()))

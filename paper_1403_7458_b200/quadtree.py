@@ -115,6 +115,11 @@ class QuadTreeMatrix:
     def stored_leaf_count(self) -> int:
         return int(self._info.stored)
 
+    @property
+    def symmetric(self) -> bool:
+        """Exactly symmetric (X == X^T bitwise); X*X then runs the symmetric path."""
+        return bool(self._info.symmetric)
+
     def norm(self) -> float:
         """Frobenius norm (root of the pyramid)."""
         return float(self.norms_device()[0].item())

@@ -245,6 +245,90 @@ def test_gemm_batch_seam(rng, nb):
             assert rel_fro(got, ref) <= REL_FRO_TOL
 
 
+# -- symmetric SpAMM (X*X with X == X^T) -------------------------------------------
+
+def _sym(rng, n, thr=0.0):
+    d = rng.standard_normal((n, n))
+    d = np.triu(d) + np.triu(d, 1).T
+    d[np.abs(d) < thr] = 0.0
+    return d
+
+
+@pytest.mark.parametrize("nb,kernel", [(4, "exact"), (8, "auto"), (32, "auto"), (32, "exact"),
+                                       (64, "auto"), (64, "exact")])
+def test_symmetric_path_bitwise_equals_full(rng, nb, kernel):
+    d = _sym(rng, 5 * nb + 7, 0.7)
+    x = sp.build_from_dense(d, nb)
+    assert x.symmetric
+    for tau in (0.0, 0.3, 3.0):
+        c_sym, st_sym = sp.multiply(x, x, tau, kernel=kernel)
+        sp.set_symmetric_products(False)
+        try:
+            c_full, st_full = sp.multiply(x, x, tau, kernel=kernel)
+        finally:
+            sp.set_symmetric_products(True)
+        assert st_sym.symmetric and not st_full.symmetric
+        assert st_sym.counts_equal(st_full) and st_sym.flop_estimate == st_full.flop_estimate
+        assert st_sym.executed_products <= st_full.executed_products
+        assert np.array_equal(sp.to_dense(c_sym), sp.to_dense(c_full))
+        assert np.array_equal(pyramid_flat(c_sym._tier_norms), pyramid_flat(c_full._tier_norms))
+        assert c_sym.symmetric
+        cs = sp.convolution_census(x, x, tau)
+        assert cs.counts_equal(st_full)
+
+
+def test_symmetric_flag_propagation(rng):
+    d = _sym(rng, 40)
+    x = sp.build_from_dense(d, 8)
+    assert x.symmetric and sp.identity(40, 8).symmetric
+    assert sp.add_scaled(2.0, x, -1.0, sp.identity(40, 8)).symmetric
+    a = sp.build_from_dense(rng.standard_normal((40, 40)), 8)
+    assert not a.symmetric
+    _, st = sp.multiply(a, a, 0.0)
+    assert not st.symmetric and st.executed_products == st.leaf_products
+    _, st = sp.multiply(x, sp.add_scaled(1.0, x, 0.0, x), 0.0)   # equal but distinct operands
+    assert not st.symmetric
+
+
+def test_symmetric_tie_falls_back_to_full_cull(rng):
+    """Block norms of X_ik and X_ki^T are summed in different orders; if tau
+    splits a mirror pair the survivor set is not symmetric and the full path
+    must run (bitwise the non-symmetric result, symmetric=False)."""
+    nb = 4
+    for attempt in range(50):
+        d = _sym(rng, 32)
+        x = sp.build_from_dense(d, nb)
+        leaf = x._tier_norms[-1]
+        g = leaf.shape[0]
+        found = None
+        for i in range(g):
+            for j in range(i + 1, g):
+                for k in range(g):
+                    p, q = leaf[i, k] * leaf[k, j], leaf[j, k] * leaf[k, i]
+                    if p != q:
+                        found = min(p, q)
+                        break
+                if found:
+                    break
+            if found:
+                break
+        if found:
+            break
+    assert found, "no ulp-asymmetric norm product found"
+    c_sym, st = sp.multiply(x, x, found)
+    assert not st.symmetric
+    sp.set_symmetric_products(False)
+    try:
+        c_full, st_full = sp.multiply(x, x, found)
+    finally:
+        sp.set_symmetric_products(True)
+    assert st.counts_equal(st_full)
+    assert np.array_equal(sp.to_dense(c_sym), sp.to_dense(c_full))
+    ox = O.from_dense(d, nb)
+    v, c, *_ = O.sweep(ox.tier_norms, ox.tier_norms, found)
+    assert st.visited == tuple(v) and st.culled == tuple(c)
+
+
 # -- full-size properties --------------------------------------------------------
 
 def test_cfg4_x0_square_task_set_and_properties():
