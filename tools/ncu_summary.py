@@ -1,0 +1,41 @@
+"""Summarise an ncu --set full report (raw page) into a small JSON per kernel."""
+import csv, io, json, subprocess, sys
+rep = sys.argv[1]
+raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+rows = list(csv.reader(io.StringIO(raw)))
+hdr, units = rows[0], rows[1]
+want = {
+    "gpu__time_duration.sum": "duration",
+    "dram__bytes_read.sum": "dram_read",
+    "dram__bytes_write.sum": "dram_write",
+    "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed": "dram_pct",
+    "sm__pipe_tensor_subpipe_dmma_cycles_active.avg.pct_of_peak_sustained_active": "dmma_pipe_pct_active",
+    "sm__ops_path_tensor_src_fp64.avg.pct_of_peak_sustained_elapsed": "fp64_tensor_pct_elapsed",
+    "sm__warps_active.avg.pct_of_peak_sustained_active": "warps_active_pct",
+    "launch__registers_per_thread": "regs",
+    "lts__t_sector_hit_rate.pct": "l2_hit_pct",
+    "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum": "smem_bank_conflicts",
+    "sm__cycles_elapsed.avg.per_second": "sm_clock",
+    "launch__grid_size": "grid",
+    "launch__block_size": "block",
+    "sm__throughput.avg.pct_of_peak_sustained_elapsed": "sm_throughput_pct",
+    "gpu__compute_memory_throughput.avg.pct_of_peak_sustained_elapsed": "mem_throughput_pct",
+}
+scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9, "usecond": 1e-6,
+         "msecond": 1e-3, "second": 1, "ns": 1e-9, "us": 1e-6, "ms": 1e-3, "s": 1,
+         "Ghz": 1e9, "Mhz": 1e6, "GHz": 1e9, "MHz": 1e6}
+out = []
+for r in rows[2:]:
+    d = {"kernel": r[hdr.index("Kernel Name")][:80]}
+    for i, h in enumerate(hdr):
+        if h in want:
+            v = r[i].replace(",", "")
+            try:
+                v = float(v) * scale.get(units[i], 1)
+            except ValueError:
+                pass
+            d[want[h]] = v
+    if "dram_read" in d and "dram_write" in d:
+        d["dram_bytes"] = d["dram_read"] + d["dram_write"]
+    out.append(d)
+print(json.dumps(out, indent=1))
