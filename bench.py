@@ -15,8 +15,10 @@ the host cores: the oracle port (oracle/spamm_oracle.py + oracle/leafgemm.c,
 numba-equivalent i-k-j leaf kernel, all host threads), one SP2 iteration of
 the same workload per step (bounded sample).
 
-Multi-GPU (torchrun): every rank solves its own replica of the workload
-(weak scaling, no data-path collective); time is the max over ranks.
+Multi-GPU (torchrun): the SP2 solve is sharded (paper_1403_7458_b200/parallel.py):
+each rank multiplies a work-balanced segment of the C-block Morton curve, the
+blocks are all-gathered over NCCL, cuts follow the previous iteration's task
+counts (persistence load balancing).  Strong scaling; time = max over ranks.
 """
 
 from __future__ import annotations
@@ -131,7 +133,9 @@ def config_dict(cfg, n_occ, args, extra=None):
          "block_size": cfg.block_size, "tau": cfg.tau, "n_occ": n_occ,
          "criterion": "||X^2-X||_F<1e-6", "step": "one full SP2 solve H->P",
          "l2": f"flushed between steps ({L2_FLUSH_BYTES >> 20} MiB write)",
-         "parallelism": f"replicas x{args.gpus}", "inputs": "synthetic, seed 0 (synth.py)"}
+         "parallelism": (f"C-curve sharded x{args.gpus}, NCCL all-gather, persistence LB"
+                         if args.gpus > 1 else "single GPU"),
+         "inputs": "synthetic, seed 0 (synth.py)"}
     from paper_1403_7458_b200.quadtree import _padded_geometry
     d["n_padded"] = _padded_geometry(cfg.n, cfg.block_size)[0]
     if extra:
@@ -158,13 +162,22 @@ def run_ours(args):
     f = sp.build_from_dense(h_dev, cfg.block_size)
     flush = torch.empty(L2_FLUSH_BYTES // 8, dtype=torch.float64, device="cuda")
     stream = torch.cuda.current_stream()
+    nb3x2 = 2 * cfg.block_size ** 3
+    sharded = ws > 1
 
-    def step():
-        p, st = sp.sp2_solve(f, n_occ, cfg.tau, timed=True, **crit)
-        return p, st
+    def solve(ff, timed):
+        """One SP2 solve -> (P, reference-equivalent flops of the whole job, flops this rank
+        executed, K4 ms on this rank, multiplies, iterations)."""
+        if not sharded:
+            p, st = sp.sp2_solve(ff, n_occ, cfg.tau, timed=timed, **crit)
+            return p, st.flops, st.executed_flops, st.ms_leaf, len(st.product_stats), st.iteration
+        from paper_1403_7458_b200.parallel import DeviceEngine, ShardedSP2
+        res = ShardedSP2(DeviceEngine()).solve(ff, n_occ, cfg.tau, **crit)
+        return (res.x, sum(res.leaf_products) * nb3x2, sum(res.local_work) * nb3x2, 0.0,
+                len(res.leaf_products), res.iteration)
 
     for _ in range(args.warmup):
-        step()
+        solve(f, True)
     torch.cuda.synchronize()
 
     if ws > 1:
@@ -173,7 +186,6 @@ def run_ours(args):
     flops = 0
     exec_flops = 0
     leaf_ms = 0.0
-    leaf_launches = 0
     n_mult = 0
     iters = []
     dev_ms = 0.0
@@ -183,18 +195,17 @@ def run_ours(args):
             flush.zero_()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            p, st = step()
+            p, fl, xfl, lms, nm, it = solve(f, True)
             e1.record(stream)
             e1.synchronize()
             dev_ms += e0.elapsed_time(e1)
             print(f"[bench] rank {rank} step {e0.elapsed_time(e1):.2f} ms "
-                  f"leaf {st.ms_leaf:.2f} ms iters {st.iteration}", file=sys.stderr, flush=True)
-            flops += st.flops
-            exec_flops += st.executed_flops
-            leaf_ms += st.ms_leaf
-            n_mult += len(st.product_stats)
-            leaf_launches += sum(1 for s in st.product_stats if s.leaf_products > 0)
-            iters.append(st.iteration)
+                  f"leaf {lms:.2f} ms iters {it}", file=sys.stderr, flush=True)
+            flops += fl
+            exec_flops += xfl
+            leaf_ms += lms
+            n_mult += nm
+            iters.append(it)
     launches = lib.spamm_launch_count() - l0
     torch.cuda.synchronize()
     if ws > 1:
@@ -207,9 +218,9 @@ def run_ours(args):
     def e2e_step():
         hd = h_pin.to("cuda", non_blocking=True)
         ff = sp.build_from_dense(hd, cfg.block_size)
-        pp, st = sp.sp2_solve(ff, n_occ, cfg.tau, **crit)
+        pp, fl, *_ = solve(ff, False)
         p_pin.copy_(sp.to_dense_device(pp), non_blocking=True)
-        return st
+        return fl
 
     e2e_step()
     torch.cuda.synchronize()
@@ -219,11 +230,10 @@ def run_ours(args):
         flush.zero_()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        st = e2e_step()
+        e2e_flops += e2e_step()
         e1.record(stream)
         e1.synchronize()
         e2e_ms += e0.elapsed_time(e1)
-        e2e_flops += st.flops
 
     tmax = dev_ms
     e2e_max = e2e_ms
@@ -231,37 +241,45 @@ def run_ours(args):
         t = torch.tensor([dev_ms, e2e_ms], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         tmax, e2e_max = float(t[0]), float(t[1])
-        fl = torch.tensor([flops, e2e_flops], dtype=torch.float64, device="cuda")
-        dist.all_reduce(fl, op=dist.ReduceOp.SUM)
-        flops_all, e2e_flops_all = float(fl[0]), float(fl[1])
+        xf = torch.tensor([exec_flops], dtype=torch.float64, device="cuda")
+        dist.all_reduce(xf, op=dist.ReduceOp.SUM)
+        exec_all = float(xf[0])
     else:
-        flops_all, e2e_flops_all = float(flops), float(e2e_flops)
+        exec_all = float(exec_flops)
+    # sharded: every rank already holds the whole job's (identical) flop count
+    flops_all, e2e_flops_all = float(flops), float(e2e_flops)
 
     if rank == 0:
         peak, peak_src = fp64_peak()
         # roofline on the arithmetic the kernel actually executed (the symmetric
         # path runs about half of the reference's surviving leaf products)
-        achieved = exec_flops / (leaf_ms * 1e-3) / 1e12 if leaf_ms > 0 else 0.0
+        if leaf_ms > 0:
+            achieved = exec_flops / (leaf_ms * 1e-3) / 1e12
+            roof_note = "executed leaf products*2*Nb^3 flops per launch / K4 event time"
+        else:  # sharded runs are not K4-timed: whole-step lower bound, all ranks
+            achieved = exec_all / (tmax * 1e-3) / 1e12 / ws
+            roof_note = "per-GPU executed leaf flops / whole step time (lower bound)"
         out = {
             "metric": METRIC, "value": flops_all / (tmax * 1e-3) / 1e9, "unit": UNIT,
             "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": tmax / args.steps, "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": tmax / args.steps, "higher_is_better": True,
+            "scaling": "strong" if sharded else "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": config_dict(cfg, n_occ, args),
             "sp2_ms_per_iter": tmax / max(n_mult, 1),
             "sp2_iterations": iters[0] if iters else None,
             "multiplies_per_step": n_mult // max(args.steps, 1),
             "leaf_flops_per_step": flops // max(args.steps, 1),
-            "leaf_flops_executed_per_step": exec_flops // max(args.steps, 1),
+            "leaf_flops_executed_per_step": int(exec_all) // max(args.steps, 1),
             "flops_note": ("value counts the reference's surviving-leaf flops "
                            "(ProductStats.flop_estimate); symmetric X*X executes "
                            "leaf_flops_executed_per_step of them and mirrors the rest "
                            "(bitwise identical C)"),
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved / peak, "traffic": ncu_traffic(),
-                         "kernel": "k_leaf_dmma<64,2,2,3> (K4 leaf products)",
+                         "kernel": "k_leaf_dmma_tma<64,2,4,3> (K4 leaf products)",
                          "peak_source": peak_src,
-                         "algorithmic": "executed leaf products*2*Nb^3 flops per launch"},
+                         "algorithmic": roof_note},
             "e2e": {"value": e2e_flops_all / (e2e_max * 1e-3) / 1e9, "unit": UNIT,
                     "h2d_bytes_per_step": int(h.nbytes), "d2h_bytes_per_step": int(h.nbytes)},
             "gpu_launches": int(launches),

@@ -98,6 +98,15 @@ int spamm_mat_to_dense(const spamm_mat* m, double* dense, int64_t ld, void* stre
 /* multiply (kernel.py:157-223): C = A*B culled at tau (strict >). */
 int spamm_multiply(const spamm_mat* a, const spamm_mat* b, double tau, int32_t kernel,
                    int32_t timed, void* stream, spamm_mat** c, spamm_stats* stats);
+/* Shard of a multiply (multi-GPU): only the C blocks whose Morton
+ * position (row bit above column bit) lies in [lo, hi) -- plus, on the
+ * symmetric path, the mirrors of the upper blocks in range.  If `work` is not
+ * NULL (device int32[G*G], Morton-indexed, zeroed by the caller) it receives
+ * the task count of every computed C block (persistence load balancing).
+ * Counters in `stats` cover the shard only. */
+int spamm_multiply_range(const spamm_mat* a, const spamm_mat* b, double tau, int32_t kernel,
+                         int64_t lo, int64_t hi, int32_t* work, void* stream, spamm_mat** c,
+                         spamm_stats* stats);
 /* Symmetric products (default on): when a == b and the matrix is exactly
  * symmetric, multiply computes only C blocks with i <= j and mirrors the rest;
  * counters stay the full reference counts.  0 disables (A/B testing). */
@@ -145,6 +154,12 @@ int spamm_sp2_update(const spamm_mat* x, const spamm_mat* x2, int32_t want_idem,
 int spamm_sp2_step(const spamm_mat* x, double n_occ, double tau, int32_t kernel, int32_t want_idem,
                    int32_t timed, void* stream, spamm_mat** x_next, int32_t* branch, double* t_x,
                    double* t_sq, double* idem, spamm_stats* stats);
+/* Second half of an SP2 iteration when X2 = X*X was produced elsewhere (the
+ * multi-GPU driver assembles it from shards): traces, branch, fused update.
+ * *e_out = 2X - X2 on EXPAND (branch 1), NULL on SQUARE (x_next is X2). */
+int spamm_sp2_finish(const spamm_mat* x, const spamm_mat* x2, double n_occ, int32_t want_idem,
+                     void* stream, int32_t* branch, double* t_x, double* t_sq, double* idem,
+                     spamm_mat** e_out);
 /* gershgorin_bounds (sp2.py:68-76): eps_min, eps_max and max|F-F^T|
  * (caller raises when asym > sym_tol, as the reference does). */
 int spamm_gershgorin(const spamm_mat* f, void* stream, double* eps_min, double* eps_max,

@@ -60,6 +60,8 @@ _SIGS = {
                                ctypes.POINTER(Stats)]),
     "spamm_census": (c_i32, [c_vp, c_vp, c_f64, c_vp, ctypes.POINTER(Stats)]),
     "spamm_set_symmetric_products": (c_i32, [c_i32]),
+    "spamm_multiply_range": (c_i32, [c_vp, c_vp, c_f64, c_i32, c_i64, c_i64, c_vp, c_vp,
+                                     ctypes.POINTER(c_vp), ctypes.POINTER(Stats)]),
     "spamm_reserve_pool": (c_i32, [c_i64, c_vp]),
     "spamm_tasks": (c_i32, [c_vp, c_vp, c_f64, c_vp, c_vp, c_vp, c_i64, ctypes.POINTER(c_i64), c_vp]),
     "spamm_gemm_batch": (c_i32, [c_vp, c_vp, c_vp, c_i64, c_vp, c_i64, c_vp, c_i64, c_vp, c_i32, c_i32,
@@ -72,6 +74,9 @@ _SIGS = {
                                ctypes.POINTER(c_i32), ctypes.POINTER(c_f64),
                                ctypes.POINTER(c_f64), ctypes.POINTER(c_f64),
                                ctypes.POINTER(Stats)]),
+    "spamm_sp2_finish": (c_i32, [c_vp, c_vp, c_f64, c_i32, c_vp, ctypes.POINTER(c_i32),
+                                 ctypes.POINTER(c_f64), ctypes.POINTER(c_f64),
+                                 ctypes.POINTER(c_f64), ctypes.POINTER(c_vp)]),
     "spamm_gershgorin": (c_i32, [c_vp, c_vp, ctypes.POINTER(c_f64), ctypes.POINTER(c_f64),
                                  ctypes.POINTER(c_f64)]),
 }

@@ -162,7 +162,8 @@ void fill_stats(spamm_stats* st, double tau, const spamm::CullResult& r, int nb)
 }
 
 void multiply_impl(const spamm_mat* a, const spamm_mat* b, double tau, int32_t kernel, bool timed,
-                   cudaStream_t s, spamm::Mat& C, spamm_stats* stats);
+                   cudaStream_t s, spamm::Mat& C, spamm_stats* stats, int64_t lo = 0,
+                   int64_t hi = -1, int32_t* work = nullptr);
 
 }  // namespace
 
@@ -321,15 +322,17 @@ int spamm_multiply(const spamm_mat* a, const spamm_mat* b, double tau, int32_t k
 namespace {
 
 void multiply_impl(const spamm_mat* a, const spamm_mat* b, double tau, int32_t kernel, bool timed,
-                   cudaStream_t s, spamm::Mat& C, spamm_stats* stats) {
+                   cudaStream_t s, spamm::Mat& C, spamm_stats* stats, int64_t lo, int64_t hi,
+                   int32_t* work) {
   EventTimer tm(timed, s);
   tm.mark(0);
   spamm::CullResult r;
   // Symmetric SpAMM: X*X with X == X^T bitwise -> compute C_ij for i <= j only
   // and store C_ji = C_ij^T (bitwise what the full product yields).
   bool sym = g_sym_enabled && a == b && a->m.sym;
-  if (sym && !spamm::cull(a->m, b->m, tau, true, r, s, true)) sym = false;  // ulp tie: full path
-  if (!sym) spamm::cull(a->m, b->m, tau, true, r, s, false);
+  if (sym && !spamm::cull(a->m, b->m, tau, true, r, s, true, lo, hi, work))
+    sym = false;  // ulp tie: full path
+  if (!sym) spamm::cull(a->m, b->m, tau, true, r, s, false, lo, hi, work);
   C.n_native = a->m.n_native;
   C.nb = a->m.nb;
   C.chunk_size = a->m.chunk_size;
@@ -391,24 +394,13 @@ void multiply_impl(const spamm_mat* a, const spamm_mat* b, double tau, int32_t k
   r.release(s);
 }
 
-}  // namespace
 
-extern "C" {
-
-int spamm_sp2_step(const spamm_mat* x, double n_occ, double tau, int32_t kernel, int32_t want_idem,
-                   int32_t timed, void* stream, spamm_mat** x_next, int32_t* branch, double* t_x,
-                   double* t_sq, double* idem, spamm_stats* stats) {
-  if (!x || !x_next || !branch || !t_x || !t_sq || (want_idem && !idem))
-    return fail(SPAMM_EINVAL, "null argument");
-  if (!(tau >= 0.0) || tau == __builtin_inf())
-    return fail(SPAMM_EINVAL, "tau must be finite and >= 0, got " + std::to_string(tau));
-  if (kernel < 0 || kernel > 3) return fail(SPAMM_EINVAL, "unknown leaf kernel");
-  if ((kernel == SPAMM_LEAF_DMMA || kernel == 3) && !spamm::dmma_supported(x->m.nb))
-    return fail(SPAMM_EINVAL, "DMMA leaf kernel needs block size 8, 16, 32 or 64");
-  SPAMM_API_BEGIN
-  cudaStream_t s = S(stream);
-  auto* c = new spamm_mat();
-  multiply_impl(x, x, tau, kernel, timed != 0, s, c->m, stats);
+// Second half of an SP2 iteration given X and X2 = X*X (sp2.py:94-101 + the
+// idempotency test): traces (tr X cached) and the union size in one sync, the
+// branch rule, then the fused K6 pass.  *e receives 2X - X2 on EXPAND.
+void sp2_finish(const spamm_mat* x, const spamm_mat* c, double n_occ, bool want_idem,
+                cudaStream_t s, bool* square_out, double* t_x, double* t_sq, double* idem,
+                spamm_mat** e_out) {
   const bool fused = spamm::sp2_fused_supported(x->m.nb);
   // One host sync for tr(X), tr(X^2) and the union size of the update.
   int64_t* sc = spamm::dmalloc<int64_t>(3, s);
@@ -433,14 +425,44 @@ int spamm_sp2_step(const spamm_mat* x, double n_occ, double tau, int32_t kernel,
   spamm_mat* e = square ? nullptr : new spamm_mat();
   spamm::Mat dummy;
   if (fused) {
-    spamm::sp2_update_finish(x->m, c->m, prep, h[2], want_idem != 0, !square, idem,
+    spamm::sp2_update_finish(x->m, c->m, prep, h[2], want_idem, !square, idem,
                              e ? e->m : dummy, s);
   } else {
-    spamm::sp2_update(x->m, c->m, want_idem != 0, !square, idem, e ? e->m : dummy, s);
+    spamm::sp2_update(x->m, c->m, want_idem, !square, idem, e ? e->m : dummy, s);
   }
   if (e) {
     e->m.stream = s;
     e->m.sym = x->m.sym && c->m.sym;
+  }
+  *square_out = square;
+  *t_x = tx;
+  *t_sq = tsq;
+  *e_out = e;
+}
+
+}  // namespace
+
+extern "C" {
+
+int spamm_sp2_step(const spamm_mat* x, double n_occ, double tau, int32_t kernel, int32_t want_idem,
+                   int32_t timed, void* stream, spamm_mat** x_next, int32_t* branch, double* t_x,
+                   double* t_sq, double* idem, spamm_stats* stats) {
+  if (!x || !x_next || !branch || !t_x || !t_sq || (want_idem && !idem))
+    return fail(SPAMM_EINVAL, "null argument");
+  if (!(tau >= 0.0) || tau == __builtin_inf())
+    return fail(SPAMM_EINVAL, "tau must be finite and >= 0, got " + std::to_string(tau));
+  if (kernel < 0 || kernel > 3) return fail(SPAMM_EINVAL, "unknown leaf kernel");
+  if ((kernel == SPAMM_LEAF_DMMA || kernel == 3) && !spamm::dmma_supported(x->m.nb))
+    return fail(SPAMM_EINVAL, "DMMA leaf kernel needs block size 8, 16, 32 or 64");
+  SPAMM_API_BEGIN
+  cudaStream_t s = S(stream);
+  auto* c = new spamm_mat();
+  multiply_impl(x, x, tau, kernel, timed != 0, s, c->m, stats);
+  spamm_mat* e = nullptr;
+  bool square = true;
+  double tx = 0, tsq = 0;
+  sp2_finish(x, c, n_occ, want_idem != 0, s, &square, &tx, &tsq, idem, &e);
+  if (e) {
     c->m.release();
     delete c;
     *x_next = e;
@@ -450,6 +472,57 @@ int spamm_sp2_step(const spamm_mat* x, double n_occ, double tau, int32_t kernel,
   *branch = square ? 0 : 1;
   *t_x = tx;
   *t_sq = tsq;
+  SPAMM_API_END
+}
+
+int spamm_sp2_finish(const spamm_mat* x, const spamm_mat* x2, double n_occ, int32_t want_idem,
+                     void* stream, int32_t* branch, double* t_x, double* t_sq, double* idem,
+                     spamm_mat** e_out) {
+  if (int rc = check_conformable(x, x2)) return rc;
+  if (!branch || !t_x || !t_sq || !e_out || (want_idem && !idem))
+    return fail(SPAMM_EINVAL, "null argument");
+  SPAMM_API_BEGIN
+  bool square = true;
+  double tx = 0, tsq = 0;
+  spamm_mat* e = nullptr;
+  sp2_finish(x, x2, n_occ, want_idem != 0, S(stream), &square, &tx, &tsq, idem, &e);
+  *e_out = e;
+  *branch = square ? 0 : 1;
+  *t_x = tx;
+  *t_sq = tsq;
+  SPAMM_API_END
+}
+
+int spamm_multiply_range(const spamm_mat* a, const spamm_mat* b, double tau, int32_t kernel,
+                         int64_t lo, int64_t hi, int32_t* work, void* stream, spamm_mat** c,
+                         spamm_stats* stats) {
+  if (int rc = check_conformable(a, b)) return rc;
+  if (!(tau >= 0.0) || tau == __builtin_inf())
+    return fail(SPAMM_EINVAL, "tau must be finite and >= 0, got " + std::to_string(tau));
+  if (kernel < 0 || kernel > 3) return fail(SPAMM_EINVAL, "unknown leaf kernel");
+  if (lo < 0 || hi < lo || hi > a->m.G * a->m.G)
+    return fail(SPAMM_EINVAL, "shard range outside [0, G*G]");
+  if (!c) return fail(SPAMM_EINVAL, "null output handle");
+  SPAMM_API_BEGIN
+  auto* h = new spamm_mat();
+  try {
+    if (hi > lo) {
+      multiply_impl(a, b, tau, kernel, false, S(stream), h->m, stats, lo, hi, work);
+    } else {  // empty shard: an empty C
+      h->m.n_native = a->m.n_native;
+      h->m.nb = a->m.nb;
+      h->m.chunk_size = a->m.chunk_size;
+      h->m.depth = a->m.depth;
+      h->m.G = a->m.G;
+      spamm::finalize(h->m, S(stream));
+      if (stats) std::memset(stats, 0, sizeof(*stats));
+    }
+  } catch (...) {
+    h->m.release();
+    delete h;
+    throw;
+  }
+  *c = h;
   SPAMM_API_END
 }
 

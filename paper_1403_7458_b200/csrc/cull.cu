@@ -60,7 +60,8 @@ __global__ void __launch_bounds__(CULL_THREADS)
                   int64_t* __restrict__ seg_o, int32_t* __restrict__ K_o,
                   const int32_t* __restrict__ slotA, const int32_t* __restrict__ slotB,
                   int32_t* __restrict__ aidx, int32_t* __restrict__ bidx, int64_t Mn, int64_t Vn,
-                  int sym, unsigned long long* __restrict__ aux) {
+                  int sym, unsigned long long* __restrict__ aux, int64_t lo, int64_t hi,
+                  int shift, int32_t* __restrict__ work) {
   const int64_t W = int64_t(1) << t1;
   const double* A = nA + tier_offset(t1);
   const double* B = nB + tier_offset(t1);
@@ -82,6 +83,15 @@ __global__ void __launch_bounds__(CULL_THREADS)
         if (!WRITE && lane == 0) cnt4[4 * p + c] = 0;
         continue;
       }
+      // Shard filter (multi-GPU): keep the child only if its Morton subtree
+      // [m << shift, (m + 1) << shift) of leaf C positions meets [lo, hi).
+      if (lo > 0 || hi >= 0) {
+        const int64_t m0 = (int64_t)morton_encode((uint32_t)row, (uint32_t)col) << shift;
+        if (m0 >= hi || m0 + (int64_t(1) << shift) <= lo) {
+          if (!WRITE && lane == 0) cnt4[4 * p + c] = 0;
+          continue;
+        }
+      }
       const double* Arow = A + row * W;
       int64_t toff = 0;
       if (WRITE) {
@@ -93,6 +103,8 @@ __global__ void __launch_bounds__(CULL_THREADS)
           ci_o[node] = (int32_t)row;
           cj_o[node] = (int32_t)col;
           seg_o[node] = toff;
+          if (LEAF && work)
+            work[morton_encode((uint32_t)row, (uint32_t)col)] = (int32_t)((vn - v) & TASK_MASK);
         }
       }
       int64_t cnt = 0;
@@ -151,7 +163,8 @@ void CullResult::release(cudaStream_t s) {
 }
 
 bool cull(const Mat& a, const Mat& b, double tau, bool want_tasks, CullResult& r, cudaStream_t s,
-          bool sym) {
+          bool sym, int64_t lo, int64_t hi, int32_t* work) {
+  // hi < 0: no shard filter (the whole C grid)
   const int depth = a.depth;
   r.visited.assign(depth + 1, 0);
   r.culled.assign(depth + 1, 0);
@@ -206,7 +219,7 @@ bool cull(const Mat& a, const Mat& b, double tau, bool want_tasks, CullResult& r
     k_cull_expand<false, false><<<cull_grid(M), CULL_THREADS, 0, s>>>(
         t1, a.norms, b.norms, tau, M, ci, cj, seg, K, cnt4, nullptr, nullptr, nullptr, nullptr,
         nullptr, nullptr, nullptr, nullptr, nullptr, 0, 0, sym ? 1 : 0,
-        reinterpret_cast<unsigned long long*>(aux));
+        reinterpret_cast<unsigned long long*>(aux), lo, hi, 2 * (depth - t1), nullptr);
     SPAMM_LAUNCH_CK();
     scan_exclusive_i64(cnt4, 4 * M, off4, s);
     SPAMM_CK(cudaMemcpyAsync(aux + 2, off4 + 4 * M, sizeof(int64_t), cudaMemcpyDeviceToDevice, s));
@@ -246,11 +259,12 @@ bool cull(const Mat& a, const Mat& b, double tau, bool want_tasks, CullResult& r
       bi = dmalloc<int32_t>(Vn, s);
       k_cull_expand<true, true><<<cull_grid(M), CULL_THREADS, 0, s>>>(
           t1, a.norms, b.norms, tau, M, ci, cj, seg, K, nullptr, off4, ci_o, cj_o, seg_o, K_o,
-          a.slot, b.slot, ai, bi, Mn, Vn, sym ? 1 : 0, nullptr);
+          a.slot, b.slot, ai, bi, Mn, Vn, sym ? 1 : 0, nullptr, lo, hi, 2 * (depth - t1), work);
     } else {
       k_cull_expand<true, false><<<cull_grid(M), CULL_THREADS, 0, s>>>(
           t1, a.norms, b.norms, tau, M, ci, cj, seg, K, nullptr, off4, ci_o, cj_o, seg_o, K_o,
-          nullptr, nullptr, nullptr, nullptr, Mn, Vn, sym ? 1 : 0, nullptr);
+          nullptr, nullptr, nullptr, nullptr, Mn, Vn, sym ? 1 : 0, nullptr, lo, hi,
+          2 * (depth - t1), nullptr);
     }
     SPAMM_LAUNCH_CK();
     dfree(cnt4, s);

@@ -102,8 +102,12 @@ struct CullResult {
 // sym=true (A == B symmetric): carry only C nodes i <= j, count the full set as
 // 2 * emitted - diagonal; returns false (nothing allocated) if a mirror triple
 // disagrees on the tau test (an ulp tie), so the caller re-runs the full cull.
+// lo/hi (hi >= 0): shard filter -- only C blocks whose Morton position lies in
+// [lo, hi) are produced (ancestors outside are pruned); counters then cover
+// only the shard.  work (Morton-indexed, G*G int32): task count per emitted C
+// block (persistence load balancing).
 bool cull(const Mat& a, const Mat& b, double tau, bool want_tasks, CullResult& r, cudaStream_t s,
-          bool sym = false);
+          bool sym = false, int64_t lo = 0, int64_t hi = -1, int32_t* work = nullptr);
 
 // ---- leaf products ----
 // LEAF_DMMA_CPASYNC: the first-generation DMMA kernel (cp.async ring, one CTA
