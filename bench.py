@@ -170,7 +170,7 @@ def run_ours(args):
         executed, K4 ms on this rank, multiplies, iterations)."""
         if not sharded:
             p, st = sp.sp2_solve(ff, n_occ, cfg.tau, timed=timed, **crit)
-            return p, st.flops, st.executed_flops, st.ms_leaf, len(st.product_stats), st.iteration
+            return p, st.flops, st.executed_flops, st.ms_leaf, len(st.leaf_products), st.iteration
         from paper_1403_7458_b200.parallel import DeviceEngine, ShardedSP2
         res = ShardedSP2(DeviceEngine()).solve(ff, n_occ, cfg.tau, **crit)
         return (res.x, sum(res.leaf_products) * nb3x2, sum(res.local_work) * nb3x2, 0.0,

@@ -160,6 +160,27 @@ int spamm_sp2_step(const spamm_mat* x, double n_occ, double tau, int32_t kernel,
 int spamm_sp2_finish(const spamm_mat* x, const spamm_mat* x2, double n_occ, int32_t want_idem,
                      void* stream, int32_t* branch, double* t_x, double* t_sq, double* idem,
                      spamm_mat** e_out);
+/* sp2_solve (sp2.py:115-143) as one native loop: Gershgorin bounds, X0,
+ * then spamm_sp2_step-equivalent iterations until convergence -- criterion 0
+ * (reference): |tr X2 - tr X| < idem_tol and |tr X - n_occ| < 1e-6 n_occ;
+ * criterion 1: ||X2 - X||_F < fro_tol.  Returns the old X on convergence
+ * (*p_out) and the histories in caller buffers (capacity max_iter + 1). */
+typedef struct {
+  int32_t iterations;
+  int32_t converged;
+  int32_t n_multiplies;
+  double eps_min, eps_max;
+  double* trace_history;      /* [max_iter + 1] */
+  int32_t* branch_history;    /* [max_iter]  0 = SQUARE, 1 = EXPAND */
+  double* idem_history;       /* [max_iter + 1] per multiply (criterion 1) */
+  int64_t* leaf_products;     /* [max_iter + 1] per multiply (reference count) */
+  int64_t* executed_products; /* [max_iter + 1] per multiply (symmetric path) */
+  float* ms_leaf;             /* [max_iter + 1] K4 ms per multiply if timed, or NULL */
+} spamm_sp2_report;
+int spamm_sp2_solve(const spamm_mat* f, double n_occ, double tau, int32_t max_iter,
+                    double idem_tol, int32_t criterion, double fro_tol, double sym_tol,
+                    int32_t kernel, int32_t timed, void* stream, spamm_mat** p_out,
+                    spamm_sp2_report* rep);
 /* gershgorin_bounds (sp2.py:68-76): eps_min, eps_max and max|F-F^T|
  * (caller raises when asym > sym_tol, as the reference does). */
 int spamm_gershgorin(const spamm_mat* f, void* stream, double* eps_min, double* eps_max,

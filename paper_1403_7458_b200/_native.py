@@ -45,6 +45,15 @@ class Stats(ctypes.Structure):
     ]
 
 
+class SP2Report(ctypes.Structure):
+    _fields_ = [
+        ("iterations", c_i32), ("converged", c_i32), ("n_multiplies", c_i32),
+        ("eps_min", c_f64), ("eps_max", c_f64),
+        ("trace_history", c_vp), ("branch_history", c_vp), ("idem_history", c_vp),
+        ("leaf_products", c_vp), ("executed_products", c_vp), ("ms_leaf", c_vp),
+    ]
+
+
 _SIGS = {
     "spamm_abi_version": (c_i32, []),
     "spamm_last_error": (ctypes.c_char_p, []),
@@ -77,6 +86,8 @@ _SIGS = {
     "spamm_sp2_finish": (c_i32, [c_vp, c_vp, c_f64, c_i32, c_vp, ctypes.POINTER(c_i32),
                                  ctypes.POINTER(c_f64), ctypes.POINTER(c_f64),
                                  ctypes.POINTER(c_f64), ctypes.POINTER(c_vp)]),
+    "spamm_sp2_solve": (c_i32, [c_vp, c_f64, c_f64, c_i32, c_f64, c_i32, c_f64, c_f64, c_i32,
+                                c_i32, c_vp, ctypes.POINTER(c_vp), ctypes.POINTER(SP2Report)]),
     "spamm_gershgorin": (c_i32, [c_vp, c_vp, ctypes.POINTER(c_f64), ctypes.POINTER(c_f64),
                                  ctypes.POINTER(c_f64)]),
 }

@@ -652,4 +652,106 @@ int spamm_gershgorin(const spamm_mat* f, void* stream, double* eps_min, double* 
   SPAMM_API_END
 }
 
+int spamm_sp2_solve(const spamm_mat* f, double n_occ, double tau, int32_t max_iter,
+                    double idem_tol, int32_t criterion, double fro_tol, double sym_tol,
+                    int32_t kernel, int32_t timed, void* stream, spamm_mat** p_out,
+                    spamm_sp2_report* rep) {
+  if (!f || !p_out || !rep) return fail(SPAMM_EINVAL, "null argument");
+  if (!(n_occ > 0.0 && n_occ < (double)f->m.n_native))
+    return fail(SPAMM_EINVAL, "n_occ must lie strictly between 0 and " +
+                                  std::to_string(f->m.n_native));
+  if (!(tau >= 0.0) || tau == __builtin_inf())
+    return fail(SPAMM_EINVAL, "tau must be finite and >= 0, got " + std::to_string(tau));
+  if (criterion != 0 && criterion != 1) return fail(SPAMM_EINVAL, "unknown criterion");
+  if (kernel < 0 || kernel > 3) return fail(SPAMM_EINVAL, "unknown leaf kernel");
+  if ((kernel == SPAMM_LEAF_DMMA || kernel == 3) && !spamm::dmma_supported(f->m.nb))
+    return fail(SPAMM_EINVAL, "DMMA leaf kernel needs block size 8, 16, 32 or 64");
+  if (max_iter < 0) return fail(SPAMM_EINVAL, "max_iter must be >= 0");
+  cudaStream_t s = S(stream);
+  // sp2.py:68-89: Gershgorin bounds, X0 = (eps_max I - F) / (eps_max - eps_min)
+  double lo = 0, hi = 0, asym = 0;
+  try {
+    spamm::gershgorin(f->m, &lo, &hi, &asym, s);
+  } catch (const std::exception& e) {
+    return fail(SPAMM_ECUDA, e.what());
+  }
+  if (asym > sym_tol) {
+    char buf[96];
+    snprintf(buf, sizeof(buf), "matrix is not symmetric: max |F - F^T| = %.3e", asym);
+    return fail(SPAMM_EINVAL, buf);
+  }
+  const double spread = hi - lo;
+  if (spread <= 0) return fail(SPAMM_EINVAL, "degenerate spectral bounds: eps_max equals eps_min");
+  rep->eps_min = lo;
+  rep->eps_max = hi;
+  rep->iterations = 0;
+  rep->converged = 0;
+  rep->n_multiplies = 0;
+  SPAMM_API_BEGIN
+  const bool want_idem = criterion == 1;
+  spamm::Mat eye;
+  eye.n_native = f->m.n_native;
+  eye.nb = f->m.nb;
+  eye.depth = f->m.depth;
+  eye.G = f->m.G;
+  eye.chunk_size = f->m.chunk_size;
+  spamm::identity(eye, s);
+  auto* x = new spamm_mat();
+  spamm::add_scaled(hi / spread, eye, -1.0 / spread, f->m, x->m, s);
+  x->m.stream = s;
+  eye.release();
+  int n_tr = 0;
+  rep->trace_history[n_tr++] = spamm::trace(x->m, s);
+  bool pending_trace = false;
+  for (int it = 0; it < max_iter; ++it) {
+    auto* c = new spamm_mat();
+    spamm_stats st;
+    multiply_impl(x, x, tau, kernel, timed != 0, s, c->m, &st);
+    bool square = true;
+    double tx = 0, tsq = 0, idem = 0;
+    spamm_mat* e = nullptr;
+    sp2_finish(x, c, n_occ, want_idem, s, &square, &tx, &tsq, &idem, &e);
+    const int k = rep->n_multiplies++;
+    rep->leaf_products[k] = st.leaf_products;
+    rep->executed_products[k] = st.executed_products;
+    if (rep->ms_leaf) rep->ms_leaf[k] = st.ms_leaf;
+    if (pending_trace) {  // tr of the last accepted X = this step's t_x
+      rep->trace_history[n_tr++] = tx;
+      pending_trace = false;
+    }
+    bool done;
+    if (want_idem) {
+      rep->idem_history[k] = idem;
+      done = idem < fro_tol;
+    } else {
+      done = std::fabs(tsq - tx) < idem_tol && std::fabs(tx - n_occ) < 1e-6 * n_occ;
+    }
+    if (done) {  // sp2.py:133-136: converged on X^2, the old X is returned
+      rep->converged = 1;
+      if (e) {
+        e->m.release();
+        delete e;
+      }
+      c->m.release();
+      delete c;
+      break;
+    }
+    spamm_mat* next = c;
+    if (e) {
+      c->m.release();
+      delete c;
+      next = e;
+    }
+    x->m.release();
+    delete x;
+    x = next;
+    rep->branch_history[rep->iterations] = square ? 0 : 1;
+    rep->iterations += 1;
+    pending_trace = true;
+  }
+  if (pending_trace) rep->trace_history[n_tr++] = spamm::trace(x->m, s);
+  *p_out = x;
+  SPAMM_API_END
+}
+
 }  // extern "C"

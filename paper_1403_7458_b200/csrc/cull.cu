@@ -18,6 +18,9 @@
 // Candidates per tier are 8 x survivors of the previous tier, exactly the
 // reference's expansion, so visited/culled per tier are identical.  The
 // surviving C nodes come out in Morton (Z) order of (i, j).
+#include <algorithm>
+#include <cstring>
+
 #include "internal.h"
 
 namespace spamm {
@@ -147,6 +150,102 @@ __global__ void __launch_bounds__(CULL_THREADS)
 
 int cull_grid(int64_t M) { return grid_for(M * 32, CULL_THREADS, 148LL * 64); }
 
+
+// Host-side cull of the top tiers (K2): the pyramid's tiers
+// 0..T0 are mirrored to pinned host memory when a matrix is finalised, so the
+// small top of the tree is expanded here in C++ with the same IEEE predicate
+// (one double multiply, strict >) and the same order (parents in Morton
+// order, children (0,0),(0,1),(1,0),(1,1), K ascending) as the device passes,
+// instead of paying one kernel chain + host sync per tier.
+struct HostLevel {
+  std::vector<int32_t> ci, cj, K;
+  std::vector<int64_t> seg;
+};
+
+bool host_cull_top(const double* nA, const double* nB, int T0, int depth, double tau, bool sym,
+                   int64_t lo, int64_t hi, CullResult& r, HostLevel& L, int64_t& full_prev,
+                   int64_t& diag_nodes) {
+  const bool keep0 = nA[0] * nB[0] > tau;
+  r.visited[0] = keep0 ? 1 : 0;
+  r.culled[0] = keep0 ? 0 : 1;
+  L.ci.assign(1, 0);
+  L.cj.assign(1, 0);
+  L.seg.assign({0, keep0 ? 1 : 0});
+  L.K.assign(keep0 ? 1 : 0, 0);
+  full_prev = keep0 ? 1 : 0;
+  diag_nodes = full_prev;
+  if (!keep0) {
+    L.ci.clear();
+    L.cj.clear();
+    L.seg.assign(1, 0);
+    return true;
+  }
+  HostLevel N;
+  for (int t1 = 1; t1 <= T0; ++t1) {
+    const int64_t W = int64_t(1) << t1;
+    const double* A = nA + tier_offset(t1);
+    const double* B = nB + tier_offset(t1);
+    const int shift = 2 * (depth - t1);
+    N.ci.clear();
+    N.cj.clear();
+    N.K.clear();
+    N.seg.clear();
+    int64_t D = 0, dn = 0;
+    const int64_t M = (int64_t)L.ci.size();
+    for (int64_t p = 0; p < M; ++p) {
+      const int64_t I = L.ci[p], J = L.cj[p];
+      for (int c = 0; c < 4; ++c) {
+        const int64_t row = 2 * I + (c >> 1), col = 2 * J + (c & 1);
+        if (sym && row > col) continue;
+        if (lo > 0 || hi >= 0) {
+          const int64_t m0 = (int64_t)morton_encode((uint32_t)row, (uint32_t)col) << shift;
+          if (m0 >= hi || m0 + (int64_t(1) << shift) <= lo) continue;
+        }
+        const size_t start = N.K.size();
+        for (int64_t q = L.seg[p]; q < L.seg[p + 1]; ++q)
+          for (int dk = 0; dk < 2; ++dk) {
+            const int64_t kk = 2 * (int64_t)L.K[q] + dk;
+            const bool keep = A[row * W + kk] * B[kk * W + col] > tau;
+            if (sym && row != col && keep != (A[col * W + kk] * B[kk * W + row] > tau))
+              return false;
+            if (keep) N.K.push_back((int32_t)kk);
+          }
+        const int64_t cnt = (int64_t)(N.K.size() - start);
+        if (cnt) {
+          N.ci.push_back((int32_t)row);
+          N.cj.push_back((int32_t)col);
+          N.seg.push_back((int64_t)start);
+          if (sym && row == col) {
+            D += cnt;
+            ++dn;
+          }
+        }
+      }
+    }
+    const int64_t Vn = (int64_t)N.K.size();
+    N.seg.push_back(Vn);
+    const int64_t full = sym ? 2 * Vn - D : Vn;
+    r.visited[t1] = full;
+    r.culled[t1] = 8 * full_prev - full;
+    full_prev = full;
+    diag_nodes = dn;
+    std::swap(L, N);
+    if (Vn == 0) break;
+  }
+  return true;
+}
+
+void* pinned_staging(size_t bytes) {
+  static thread_local void* buf = nullptr;
+  static thread_local size_t cap = 0;
+  if (bytes > cap) {
+    if (buf) cudaFreeHost(buf);
+    cap = std::max(bytes, cap * 2);
+    SPAMM_CK(cudaMallocHost(&buf, cap));
+  }
+  return buf;
+}
+
 }  // namespace
 
 void CullResult::release(cudaStream_t s) {
@@ -182,20 +281,63 @@ bool cull(const Mat& a, const Mat& b, double tau, bool want_tasks, CullResult& r
   SPAMM_CK(cudaMemsetAsync(aux, 0, 4 * sizeof(int64_t), s));
   int32_t* aidx = nullptr;
   int32_t* bidx = nullptr;
-  if (depth == 0 && want_tasks) {
-    aidx = dmalloc<int32_t>(1, s);
-    bidx = dmalloc<int32_t>(1, s);
+  int64_t V = 0, M = 0, full_prev = 0, diag_nodes = 0;
+  int t0 = 0;
+  const int T0 = std::min(a.top_t, b.top_t);
+  if (T0 >= 1 && T0 < depth) {
+    SPAMM_CK(cudaEventSynchronize(a.top_ev));
+    SPAMM_CK(cudaEventSynchronize(b.top_ev));
+    HostLevel L;
+    if (!host_cull_top(a.host_top, b.host_top, T0, depth, tau, sym, lo, hi, r, L, full_prev,
+                       diag_nodes)) {
+      dfree(ci, s);
+      dfree(cj, s);
+      dfree(seg, s);
+      dfree(K, s);
+      dfree(aux, s);
+      return false;
+    }
+    M = (int64_t)L.ci.size();
+    V = (int64_t)L.K.size();
+    t0 = T0;
+    for (int t = T0 + 1; t <= depth; ++t) r.visited[t] = r.culled[t] = 0;
+    dfree(ci, s);
+    dfree(cj, s);
+    dfree(seg, s);
+    dfree(K, s);
+    ci = cj = K = nullptr;
+    seg = nullptr;
+    if (V > 0) {
+      ci = dmalloc<int32_t>(M, s);
+      cj = dmalloc<int32_t>(M, s);
+      seg = dmalloc<int64_t>(M + 1, s);
+      K = dmalloc<int32_t>(V, s);
+      const size_t b1 = M * 4, b2 = (M + 1) * 8, b3 = V * 4;
+      char* st = static_cast<char*>(pinned_staging(2 * b1 + b2 + b3));
+      memcpy(st, L.ci.data(), b1);
+      memcpy(st + b1, L.cj.data(), b1);
+      memcpy(st + 2 * b1, L.seg.data(), b2);
+      memcpy(st + 2 * b1 + b2, L.K.data(), b3);
+      SPAMM_CK(cudaMemcpyAsync(ci, st, b1, cudaMemcpyHostToDevice, s));
+      SPAMM_CK(cudaMemcpyAsync(cj, st + b1, b1, cudaMemcpyHostToDevice, s));
+      SPAMM_CK(cudaMemcpyAsync(seg, st + 2 * b1, b2, cudaMemcpyHostToDevice, s));
+      SPAMM_CK(cudaMemcpyAsync(K, st + 2 * b1 + b2, b3, cudaMemcpyHostToDevice, s));
+    }
+  } else {
+    if (depth == 0 && want_tasks) {
+      aidx = dmalloc<int32_t>(1, s);
+      bidx = dmalloc<int32_t>(1, s);
+    }
+    k_cull_root<<<1, 1, 0, s>>>(a.norms, b.norms, tau, ci, cj, seg, K, aux + 2, a.slot, b.slot,
+                                aidx, bidx);
+    SPAMM_LAUNCH_CK();
+    d2h_sync(&V, aux + 2, 1, s);
+    r.visited[0] = V;
+    r.culled[0] = 1 - V;
+    M = V;
+    full_prev = V;  // the root node is diagonal: full count == emitted count
+    diag_nodes = V;
   }
-  k_cull_root<<<1, 1, 0, s>>>(a.norms, b.norms, tau, ci, cj, seg, K, aux + 2, a.slot, b.slot,
-                              aidx, bidx);
-  SPAMM_LAUNCH_CK();
-  int64_t V = 0;
-  d2h_sync(&V, aux + 2, 1, s);
-  r.visited[0] = V;
-  r.culled[0] = 1 - V;
-  int64_t M = V;
-  int64_t full_prev = V;  // the root node is diagonal: full count == emitted count
-  int64_t diag_nodes = V;
 
   auto free_level = [&]() {
     dfree(ci, s);
@@ -209,7 +351,7 @@ bool cull(const Mat& a, const Mat& b, double tau, bool want_tasks, CullResult& r
     K = aidx = bidx = nullptr;
   };
 
-  int t = 0;
+  int t = t0;
   for (; V > 0 && t < depth; ++t) {
     const int t1 = t + 1;
     const bool leaf = t1 == depth;

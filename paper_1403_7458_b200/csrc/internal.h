@@ -37,9 +37,15 @@ struct Mat {
   bool sym = false;          // X == X^T bitwise (blocks and null structure)
   mutable double tr = 0.0;   // cached trace (matrices are immutable)
   mutable bool tr_valid = false;
+  // Pinned host mirror of norm tiers 0..top_t (written by finalize, ready when
+  // top_ev completes): the cull expands those tiers on the host.
+  double* host_top = nullptr;
+  int top_t = -1;
+  cudaEvent_t top_ev = nullptr;
   cudaStream_t stream = nullptr;
   void release();
 };
+constexpr int HOST_TOP_TIERS = 5;  // tiers 0..5: 1,365 norms (11 KB)
 
 // Exact-symmetry test (block (i,j) == transpose of block (j,i), bitwise).
 bool is_symmetric(const Mat& m, cudaStream_t s);

@@ -12,7 +12,9 @@
 //    ((c00 + c01) + c10) + c11; sqrt per tier (quadtree.py:188,192).
 //  * blocks whose entries are all exactly zero are pruned (quadtree.py:177-180).
 // HBM roofline: S*Nb^2*8 bytes read per pass; K1.
+#include <algorithm>
 #include <mutex>
+#include <vector>
 
 #include "internal.h"
 
@@ -60,7 +62,44 @@ void d2h_sync(int64_t* host, const int64_t* dev, int n, cudaStream_t s) {
   for (int i = 0; i < n; ++i) host[i] = pinned[i];
 }
 
+namespace {
+// Fixed-size pinned buffers + events for the host norm mirrors (allocation
+// of pinned memory and events is slow; matrices come and go every SP2 step).
+std::mutex g_top_mu;
+std::vector<double*> g_top_bufs;
+std::vector<cudaEvent_t> g_top_evs;
+
+void top_acquire(double** buf, cudaEvent_t* ev) {
+  std::lock_guard<std::mutex> lk(g_top_mu);
+  if (g_top_bufs.empty()) {
+    double* b = nullptr;
+    SPAMM_CK(cudaMallocHost(&b, tier_offset(HOST_TOP_TIERS + 1) * sizeof(double)));
+    g_top_bufs.push_back(b);
+  }
+  if (g_top_evs.empty()) {
+    cudaEvent_t e;
+    SPAMM_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    g_top_evs.push_back(e);
+  }
+  *buf = g_top_bufs.back();
+  g_top_bufs.pop_back();
+  *ev = g_top_evs.back();
+  g_top_evs.pop_back();
+}
+
+void top_release(double* buf, cudaEvent_t ev) {
+  if (ev) cudaEventSynchronize(ev);  // the async copy must not land in a reused buffer
+  std::lock_guard<std::mutex> lk(g_top_mu);
+  if (buf) g_top_bufs.push_back(buf);
+  if (ev) g_top_evs.push_back(ev);
+}
+}  // namespace
+
 void Mat::release() {
+  top_release(host_top, top_ev);
+  host_top = nullptr;
+  top_ev = nullptr;
+  top_t = -1;
   cudaStream_t s = stream;
   dfree(data, s);
   dfree(keys, s);
@@ -350,6 +389,14 @@ void finalize(Mat& m, cudaStream_t s, double* pre_n2, uint8_t* pre_nz) {
   m.norms2 = dmalloc<double>(ps, s);
   build_pyramid(m.keys, n2, m.nblocks, m.depth, m.norms, m.norms2, s);
   dfree(n2, s);
+  // Host mirror of the small top of the pyramid for the cull (no sync here).
+  if (m.depth >= 2 && !m.host_top) {
+    m.top_t = std::min(m.depth - 1, HOST_TOP_TIERS);
+    top_acquire(&m.host_top, &m.top_ev);
+    SPAMM_CK(cudaMemcpyAsync(m.host_top, m.norms, tier_offset(m.top_t + 1) * sizeof(double),
+                             cudaMemcpyDeviceToHost, s));
+    SPAMM_CK(cudaEventRecord(m.top_ev, s));
+  }
 }
 
 }  // namespace spamm

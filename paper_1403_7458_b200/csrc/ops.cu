@@ -290,6 +290,48 @@ __global__ void k_gersh_rows(const double* __restrict__ data, const int32_t* __r
   }
 }
 
+// Warp per row: numpy's pairwise tree for length n is the same for every row,
+// so the host flattens it once into leaves (lo, len) and a post-order op list
+// (k >= 0: push leaf k, -1: pop r, pop l, push l + r).  Lanes evaluate leaves
+// in parallel (each leaf is a <=128-element run, 8 accumulators), lane 0 then
+// folds them in tree order -- the identical sequence of additions.
+__global__ void __launch_bounds__(256)
+    k_gersh_rows_warp(const double* __restrict__ data, const int32_t* __restrict__ slot, int64_t G,
+                      int nb, int64_t n, const int64_t* __restrict__ leaf_lo,
+                      const int32_t* __restrict__ leaf_len, int n_leaves,
+                      const int32_t* __restrict__ ops, int n_ops, double* __restrict__ lo,
+                      double* __restrict__ hi) {
+  extern __shared__ double leafv[];  // [8 warps][n_leaves]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* lv = leafv + (int64_t)warp * n_leaves;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n; i += nw) {
+    RowReader rr{data, slot, G, i, nb};
+    for (int k = lane; k < n_leaves; k += 32) lv[k] = pw_leaf(rr, leaf_lo[k], leaf_len[k]);
+    __syncwarp();
+    if (lane == 0) {
+      double st[48];
+      int sp = 0;
+      for (int o = 0; o < n_ops; ++o) {
+        const int op = ops[o];
+        if (op >= 0) {
+          st[sp++] = lv[op];
+        } else {
+          const double r = st[--sp];
+          st[sp - 1] = __dadd_rn(st[sp - 1], r);
+        }
+      }
+      const double rowsum = st[0];
+      const int32_t s = slot[(i / nb) * G + i / nb];
+      const double d = s >= 0 ? data[(int64_t)s * nb * nb + (i % nb) * nb + (i % nb)] : 0.0;
+      const double radius = __dadd_rn(rowsum, -fabs(d));
+      lo[i] = __dadd_rn(d, -radius);
+      hi[i] = __dadd_rn(d, radius);
+    }
+    __syncwarp();
+  }
+}
+
 __global__ void k_minmax(const double* __restrict__ lo, const double* __restrict__ hi, int64_t n,
                          double* __restrict__ out) {
   double mn = lo[0], mx = hi[0];
@@ -464,8 +506,50 @@ void gershgorin(const Mat& f, double* eps_min, double* eps_max, double* asym, cu
         reinterpret_cast<unsigned long long*>(res + 2));
     SPAMM_LAUNCH_CK();
   }
-  k_gersh_rows<<<grid_for(n, 64), 64, 0, s>>>(f.data, f.slot, f.G, f.nb, n, lo, hi);
-  SPAMM_LAUNCH_CK();
+  // numpy pairwise_sum tree for a row of length n, flattened (same for all rows)
+  std::vector<int64_t> leaf_lo;
+  std::vector<int32_t> leaf_len, ops;
+  struct Sched {
+    std::vector<int64_t>& lo;
+    std::vector<int32_t>& len;
+    std::vector<int32_t>& ops;
+    void build(int64_t a, int64_t m) {
+      if (m <= 128) {
+        ops.push_back((int32_t)lo.size());
+        lo.push_back(a);
+        len.push_back((int32_t)m);
+        return;
+      }
+      int64_t m2 = m / 2;
+      m2 -= m2 % 8;
+      build(a, m2);
+      build(a + m2, m - m2);
+      ops.push_back(-1);
+    }
+  } sched{leaf_lo, leaf_len, ops};
+  sched.build(0, n);
+  const int nl = (int)leaf_lo.size(), no = (int)ops.size();
+  const size_t smem = 8 * (size_t)nl * sizeof(double);
+  if (smem <= 200 * 1024) {
+    int64_t* d_lo = dmalloc<int64_t>(nl, s);
+    int32_t* d_len = dmalloc<int32_t>(nl, s);
+    int32_t* d_ops = dmalloc<int32_t>(no, s);
+    SPAMM_CK(cudaMemcpyAsync(d_lo, leaf_lo.data(), nl * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+    SPAMM_CK(cudaMemcpyAsync(d_len, leaf_len.data(), nl * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+    SPAMM_CK(cudaMemcpyAsync(d_ops, ops.data(), no * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+    if (smem > 48 * 1024)
+      SPAMM_CK(cudaFuncSetAttribute(k_gersh_rows_warp, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)smem));
+    k_gersh_rows_warp<<<grid_for(n * 32, 256, 148LL * 16), 256, smem, s>>>(
+        f.data, f.slot, f.G, f.nb, n, d_lo, d_len, nl, d_ops, no, lo, hi);
+    SPAMM_LAUNCH_CK();
+    dfree(d_lo, s);
+    dfree(d_len, s);
+    dfree(d_ops, s);
+  } else {
+    k_gersh_rows<<<grid_for(n, 64), 64, 0, s>>>(f.data, f.slot, f.G, f.nb, n, lo, hi);
+    SPAMM_LAUNCH_CK();
+  }
   k_minmax<<<1, 1024, 0, s>>>(lo, hi, n, res);
   SPAMM_LAUNCH_CK();
   int64_t bits[3];
