@@ -87,6 +87,13 @@ int spamm_mat_from_dense(const double* dense, int64_t n, int64_t ld, int32_t blo
 int spamm_mat_from_blocks(int64_t n_native, int32_t block_size, int64_t chunk_size,
                           int32_t depth, const int64_t* keys, const double* data, int64_t m,
                           void* stream, spamm_mat** out);
+/* Config-5 generator on the device: H_ab = amp exp(-|p_a - p_b| / decay)
+ * s(orig_a, orig_b) (SplitMix64 counter hash, symmetric), H_aa = diag_a;
+ * pos (n x 3), orig (n), diag (n) are device arrays in row order.  Bitwise
+ * equal to synth.cluster_dense_cb (the matrix is exactly symmetric). */
+int spamm_mat_cluster(const double* pos, const int64_t* orig, const double* diag, int64_t n,
+                      int32_t block_size, int64_t chunk_size, double amp, double decay,
+                      uint64_t seed, void* stream, spamm_mat** out);
 /* identity (quadtree.py:308-323). */
 int spamm_mat_identity(int64_t n, int32_t block_size, int64_t chunk_size, void* stream,
                        spamm_mat** out);

@@ -61,6 +61,8 @@ _SIGS = {
     "spamm_mat_from_dense": (c_i32, [c_vp, c_i64, c_i64, c_i32, c_i64, c_vp, ctypes.POINTER(c_vp)]),
     "spamm_mat_from_blocks": (c_i32, [c_i64, c_i32, c_i64, c_i32, c_vp, c_vp, c_i64, c_vp,
                                       ctypes.POINTER(c_vp)]),
+    "spamm_mat_cluster": (c_i32, [c_vp, c_vp, c_vp, c_i64, c_i32, c_i64, c_f64, c_f64,
+                                  ctypes.c_uint64, c_vp, ctypes.POINTER(c_vp)]),
     "spamm_mat_identity": (c_i32, [c_i64, c_i32, c_i64, c_vp, ctypes.POINTER(c_vp)]),
     "spamm_mat_info_get": (c_i32, [c_vp, ctypes.POINTER(MatInfo)]),
     "spamm_mat_free": (c_i32, [c_vp]),

@@ -245,6 +245,31 @@ int spamm_mat_from_blocks(int64_t n_native, int32_t block_size, int64_t chunk_si
   SPAMM_API_END
 }
 
+int spamm_mat_cluster(const double* pos, const int64_t* orig, const double* diag, int64_t n,
+                      int32_t block_size, int64_t chunk_size, double amp, double decay,
+                      uint64_t seed, void* stream, spamm_mat** out) {
+  if (!out || !pos || !orig || !diag) return fail(SPAMM_EINVAL, "null argument");
+  if (n < 1) return fail(SPAMM_EINVAL, "matrix must have at least one row");
+  if (!is_pow2(block_size)) return fail(SPAMM_EINVAL, "block size must be a power of two");
+  SPAMM_API_BEGIN
+  auto* h = new spamm_mat();
+  h->m.n_native = n;
+  h->m.nb = block_size;
+  h->m.depth = padded_depth(n, block_size);
+  h->m.G = int64_t(1) << h->m.depth;
+  h->m.chunk_size = chunk_size;
+  h->m.stream = S(stream);
+  try {
+    spamm::cluster_build(pos, orig, diag, amp, decay, seed, h->m, S(stream));
+  } catch (...) {
+    h->m.release();
+    delete h;
+    throw;
+  }
+  *out = h;
+  SPAMM_API_END
+}
+
 int spamm_mat_identity(int64_t n, int32_t block_size, int64_t chunk_size, void* stream,
                        spamm_mat** out) {
   if (!out) return fail(SPAMM_EINVAL, "null output handle");

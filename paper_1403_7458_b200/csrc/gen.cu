@@ -1,0 +1,141 @@
+// K8: on-device generator of the counter-based cluster Hamiltonian (config 5).
+//
+// BASELINE config 5 (4096 molecules, N = 102,400, Nb = 64) is 84 GB dense:
+// it cannot be built on the host.  synth.cluster_dense_cb defines the matrix
+// as a pure function of (site positions, original row index, seed); this
+// kernel evaluates the same expression with the same IEEE operation sequence
+// (SplitMix64 counter hash, Cody-Waite/Horner exp, sqrt, division), so every
+// block is bitwise equal to the host reference (tests/test_gpu_gen.py), and
+// writes the blocks straight into the Morton-ordered storage.
+#include "internal.h"
+
+namespace spamm {
+
+namespace {
+
+__device__ __forceinline__ uint64_t splitmix64(uint64_t z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+__device__ __forceinline__ double sym_uniform(uint64_t a, uint64_t b, uint64_t n, uint64_t seed) {
+  const uint64_t lo = a < b ? a : b, hi = a < b ? b : a;
+  const uint64_t key = (seed * 0xBF58476D1CE4E5B9ull) ^ (lo * n + hi);
+  const double u = __dmul_rn((double)(splitmix64(key) >> 11), 1.0 / 9007199254740992.0);
+  return __dadd_rn(__dmul_rn(2.0, u), -1.0);
+}
+
+// synth.det_exp: k = rint(x / ln2), r = (x - k ln2_hi) - k ln2_lo, degree-13
+// Horner with coefficients 1/n! (each the correctly rounded reciprocal).
+__device__ __forceinline__ double det_exp(double x) {
+  const double k = rint(__dmul_rn(x, 1.44269504088896338700e+00));
+  const double r = __dadd_rn(__dadd_rn(x, -__dmul_rn(k, 6.93147180369123816490e-01)),
+                             -__dmul_rn(k, 1.90821492927058770002e-10));
+  double p = __ddiv_rn(1.0, 6227020800.0);
+  double fact = 6227020800.0;
+#pragma unroll
+  for (int n = 12; n >= 0; --n) {
+    fact = __ddiv_rn(fact, (double)(n + 1));
+    p = __dadd_rn(__dmul_rn(p, r), __ddiv_rn(1.0, fact));
+  }
+  return ldexp(p, (int)k);
+}
+
+__global__ void k_native_flags(int depth, int64_t nbn, uint8_t* __restrict__ flags) {
+  const int64_t G = int64_t(1) << depth, npos = G * G;
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < npos;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t bi, bj;
+    morton_decode((uint64_t)p, bi, bj);
+    flags[p] = (bi < nbn && bj < nbn) ? 1 : 0;
+  }
+}
+
+__global__ void __launch_bounds__(256)
+    k_cluster_blocks(const double* __restrict__ pos, const int64_t* __restrict__ orig,
+                     const double* __restrict__ diag, int64_t n, int nb, int depth,
+                     const uint8_t* __restrict__ flags, const int64_t* __restrict__ off,
+                     double amp, double decay, uint64_t seed, double* __restrict__ data,
+                     int64_t* __restrict__ keys) {
+  extern __shared__ double sh[];  // rows: x,y,z,orig (4 nb), cols: 4 nb
+  const int64_t G = int64_t(1) << depth, npos = G * G;
+  const int nb2 = nb * nb;
+  double* rx = sh;
+  double* cx = sh + 4 * nb;
+  for (int64_t p = blockIdx.x; p < npos; p += gridDim.x) {
+    if (!flags[p]) continue;
+    uint32_t bi, bj;
+    morton_decode((uint64_t)p, bi, bj);
+    const int64_t d = off[p];
+    __syncthreads();
+    for (int t = threadIdx.x; t < nb; t += blockDim.x) {
+      const int64_t a = (int64_t)bi * nb + t, b = (int64_t)bj * nb + t;
+      if (a < n) {
+        rx[t] = pos[3 * a];
+        rx[nb + t] = pos[3 * a + 1];
+        rx[2 * nb + t] = pos[3 * a + 2];
+        rx[3 * nb + t] = __longlong_as_double(orig[a]);
+      }
+      if (b < n) {
+        cx[t] = pos[3 * b];
+        cx[nb + t] = pos[3 * b + 1];
+        cx[2 * nb + t] = pos[3 * b + 2];
+        cx[3 * nb + t] = __longlong_as_double(orig[b]);
+      }
+    }
+    __syncthreads();
+    double* out = data + d * nb2;
+    for (int e = threadIdx.x; e < nb2; e += blockDim.x) {
+      const int r = e / nb, c = e % nb;
+      const int64_t a = (int64_t)bi * nb + r, b = (int64_t)bj * nb + c;
+      double v = 0.0;
+      if (a < n && b < n) {
+        if (a == b) {
+          v = diag[a];
+        } else {
+          // r2 = sum over axes of (p_a - p_b)^2 in axis order (synth.cluster_dense_cb)
+          double r2 = 0.0;
+#pragma unroll
+          for (int ax = 0; ax < 3; ++ax) {
+            const double dd = __dadd_rn(rx[ax * nb + r], -cx[ax * nb + c]);
+            r2 = __dadd_rn(r2, __dmul_rn(dd, dd));
+          }
+          const double x = __ddiv_rn(-__dsqrt_rn(r2), decay);
+          const double s = sym_uniform((uint64_t)__double_as_longlong(rx[3 * nb + r]),
+                                       (uint64_t)__double_as_longlong(cx[3 * nb + c]),
+                                       (uint64_t)n, seed);
+          v = __dmul_rn(__dmul_rn(amp, det_exp(x)), s);
+        }
+      }
+      out[e] = v;
+    }
+    if (threadIdx.x == 0) keys[d] = (int64_t)bi * G + bj;
+  }
+}
+
+}  // namespace
+
+void cluster_build(const double* pos, const int64_t* orig, const double* diag, double amp,
+                   double decay, uint64_t seed, Mat& m, cudaStream_t s) {
+  const int64_t G = int64_t(1) << m.depth, npos = G * G;
+  const int64_t nbn = (m.n_native + m.nb - 1) / m.nb;
+  uint8_t* flags = dmalloc<uint8_t>(npos, s);
+  int64_t* off = dmalloc<int64_t>(npos + 1, s);
+  k_native_flags<<<grid_for(npos, 256), 256, 0, s>>>(m.depth, nbn, flags);
+  SPAMM_LAUNCH_CK();
+  scan_exclusive_u8(flags, npos, off, s);
+  m.nblocks = nbn * nbn;
+  m.data = dmalloc<double>((size_t)m.nblocks * m.nb * m.nb, s);
+  m.keys = dmalloc<int64_t>(m.nblocks, s);
+  k_cluster_blocks<<<grid_for(m.nblocks, 1, 148LL * 32), 256, 8 * m.nb * sizeof(double), s>>>(
+      pos, orig, diag, m.n_native, m.nb, m.depth, flags, off, amp, decay, seed, m.data, m.keys);
+  SPAMM_LAUNCH_CK();
+  dfree(flags, s);
+  dfree(off, s);
+  finalize(m, s);
+  m.sym = true;  // r2, s and the diagonal are exactly symmetric by construction
+}
+
+}  // namespace spamm

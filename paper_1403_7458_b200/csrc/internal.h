@@ -145,5 +145,8 @@ void add_scaled(double alpha, const Mat& a, double beta, const Mat& b, Mat& out,
 double trace(const Mat& m, cudaStream_t s);  // cached per matrix
 void trace_launch(const Mat& m, double* dev_out, cudaStream_t s);  // no host sync
 void gershgorin(const Mat& f, double* eps_min, double* eps_max, double* asym, cudaStream_t s);
+// Counter-based cluster Hamiltonian (config 5) built on the device (gen.cu).
+void cluster_build(const double* pos, const int64_t* orig, const double* diag, double amp,
+                   double decay, uint64_t seed, Mat& m, cudaStream_t s);
 
 }  // namespace spamm

@@ -149,6 +149,78 @@ def water_cluster(n_mol: int, seed: int = 0, density: float = 0.0334, sites: int
     return np.ascontiguousarray(h), n_mol * occupied
 
 
+_SM_GAMMA = np.uint64(0x9E3779B97F4A7C15)
+_SM_M1 = np.uint64(0xBF58476D1CE4E5B9)
+_SM_M2 = np.uint64(0x94D049BB133111EB)
+
+
+def splitmix64(x) -> np.ndarray:
+    """SplitMix64 finaliser (Steele et al.), uint64 wrap-around arithmetic."""
+    with np.errstate(over="ignore"):
+        z = np.asarray(x, dtype=np.uint64) + _SM_GAMMA
+        z = (z ^ (z >> np.uint64(30))) * _SM_M1
+        z = (z ^ (z >> np.uint64(27))) * _SM_M2
+        return z ^ (z >> np.uint64(31))
+
+
+def hash_sym_uniform(i, j, n: int, seed: int) -> np.ndarray:
+    """Symmetric U[-1, 1) from a counter hash of (min(i,j), max(i,j)): 53-bit
+    mantissa, exact arithmetic -- the CUDA twin (csrc/gen.cu) is bitwise equal."""
+    i = np.asarray(i, dtype=np.uint64)
+    j = np.asarray(j, dtype=np.uint64)
+    lo, hi = np.minimum(i, j), np.maximum(i, j)
+    with np.errstate(over="ignore"):
+        key = (np.uint64(seed) * _SM_M1) ^ (lo * np.uint64(n) + hi)
+    u = (splitmix64(key) >> np.uint64(11)).astype(np.float64) * (1.0 / 9007199254740992.0)
+    return 2.0 * u - 1.0
+
+
+@dataclass
+class ClusterSites:
+    """Row-ordered sites of a cluster Hamiltonian (cfg5 generator input)."""
+
+    pos: np.ndarray      # (n, 3) site coordinates, Hilbert row order
+    orig: np.ndarray     # (n,) original (pre-ordering) row index -> hash counter
+    diag: np.ndarray     # (n,) diagonal values, Hilbert row order
+    n_occ: int
+    seed: int
+    amp: float = 0.3
+    decay: float = 1.5
+
+
+def cluster_sites(n_mol: int, seed: int = 0, density: float = 0.0334, sites: int = 25,
+                  occupied: int = 5, jitter: float = 0.5, diag_sigma: float = 0.2,
+                  amp: float = 0.3, decay: float = 1.5) -> ClusterSites:
+    """O(n) part of the counter-based cluster generator (config 5): geometry,
+    diagonal and Hilbert row order from one PCG64 stream; the O(n^2) couplings
+    are a pure function of (site positions, original indices, seed)."""
+    rng = np.random.default_rng(seed)
+    n = n_mol * sites
+    edge = (n_mol / density) ** (1.0 / 3.0)
+    centres = rng.uniform(0.0, edge, size=(n_mol, 3))
+    pos = np.repeat(centres, sites, axis=0) + rng.normal(0.0, jitter, size=(n, 3))
+    occ = np.tile(np.arange(sites) < occupied, n_mol)
+    d = np.where(occ, -1.0, 1.0) + rng.normal(0.0, diag_sigma, size=n)
+    perm = _hilbert_molecule_order(centres)
+    rows = (perm[:, None] * sites + np.arange(sites)[None, :]).reshape(-1)
+    return ClusterSites(np.ascontiguousarray(pos[rows]), rows.astype(np.int64),
+                        np.ascontiguousarray(d[rows]), n_mol * occupied, seed, amp, decay)
+
+
+def cluster_dense_cb(cs: ClusterSites) -> np.ndarray:
+    """Dense H of the counter-based generator (host reference; small n only):
+    H_ab = amp * exp(-r_ab / decay) * s(orig_a, orig_b), diagonal from cs.diag."""
+    n = len(cs.orig)
+    r2 = np.zeros((n, n))
+    for a in range(3):
+        dd = cs.pos[:, a, None] - cs.pos[None, :, a]
+        r2 += dd * dd
+    s = hash_sym_uniform(cs.orig[:, None], cs.orig[None, :], n, cs.seed)
+    h = cs.amp * det_exp(-np.sqrt(r2) / cs.decay) * s
+    np.fill_diagonal(h, cs.diag)
+    return h
+
+
 @dataclass(frozen=True)
 class ConfigSpec:
     index: int
@@ -167,3 +239,27 @@ CONFIGS = {
     4: ConfigSpec(4, "cfg4-water150-N3750-Nb64-sp2", 150, 3750, 64, 1e-7, "sp2"),
     5: ConfigSpec(5, "cfg5-water4096-N102400-Nb64", 4096, 102400, 64, 1e-8, "multiply"),
 }
+
+
+def device_cluster(cs: ClusterSites, block_size: int, chunk_size: int | None = None):
+    """Build the counter-based cluster H directly in HBM (spamm_mat_cluster);
+    bitwise equal to build_from_dense(cluster_dense_cb(cs), block_size)."""
+    import ctypes
+
+    import torch
+
+    from . import _native as nat
+    from .quadtree import QuadTreeMatrix, _default_chunk_size, _padded_geometry
+    n = len(cs.orig)
+    if chunk_size is None:
+        chunk_size = _default_chunk_size(_padded_geometry(n, block_size)[0], block_size)
+    pos = torch.from_numpy(np.ascontiguousarray(cs.pos, dtype=np.float64)).cuda()
+    orig = torch.from_numpy(np.ascontiguousarray(cs.orig, dtype=np.int64)).cuda()
+    diag = torch.from_numpy(np.ascontiguousarray(cs.diag, dtype=np.float64)).cuda()
+    stream = nat.current_stream()
+    out = ctypes.c_void_p()
+    nat.check(nat.load().spamm_mat_cluster(pos.data_ptr(), orig.data_ptr(), diag.data_ptr(), n,
+                                           int(block_size), int(chunk_size), float(cs.amp),
+                                           float(cs.decay), int(cs.seed), stream,
+                                           ctypes.byref(out)))
+    return QuadTreeMatrix(out, stream)
