@@ -163,7 +163,7 @@ void fill_stats(spamm_stats* st, double tau, const spamm::CullResult& r, int nb)
 
 void multiply_impl(const spamm_mat* a, const spamm_mat* b, double tau, int32_t kernel, bool timed,
                    cudaStream_t s, spamm::Mat& C, spamm_stats* stats, int64_t lo = 0,
-                   int64_t hi = -1, int32_t* work = nullptr);
+                   int64_t hi = -1, int32_t* work = nullptr, bool defer_prune = false);
 
 }  // namespace
 
@@ -290,6 +290,13 @@ int spamm_mat_identity(int64_t n, int32_t block_size, int64_t chunk_size, void* 
 
 int spamm_mat_info_get(const spamm_mat* h, spamm_mat_info* info) {
   if (!h || !info) return fail(SPAMM_EINVAL, "null argument");
+  if (h->m.pend_off) {  // never expose a lazily pruned matrix
+    try {
+      spamm::settle_sync(const_cast<spamm_mat*>(h)->m, h->m.stream);
+    } catch (const std::exception& e) {
+      return fail(SPAMM_ECUDA, e.what());
+    }
+  }
   info->n_native = h->m.n_native;
   info->block_size = h->m.nb;
   info->depth = h->m.depth;
@@ -348,7 +355,7 @@ namespace {
 
 void multiply_impl(const spamm_mat* a, const spamm_mat* b, double tau, int32_t kernel, bool timed,
                    cudaStream_t s, spamm::Mat& C, spamm_stats* stats, int64_t lo, int64_t hi,
-                   int32_t* work) {
+                   int32_t* work, bool defer_prune) {
   EventTimer tm(timed, s);
   tm.mark(0);
   spamm::CullResult r;
@@ -404,7 +411,7 @@ void multiply_impl(const spamm_mat* a, const spamm_mat* b, double tau, int32_t k
   tm.mark(2);
   spamm::dfree(c_out, s);
   spamm::dfree(c_mirror, s);
-  spamm::finalize(C, s);
+  spamm::finalize(C, s, nullptr, nullptr, defer_prune);
   C.sym = sym;
   tm.mark(3);
   fill_stats(stats, tau, r, C.nb);
@@ -428,15 +435,19 @@ void sp2_finish(const spamm_mat* x, const spamm_mat* c, double n_occ, bool want_
                 spamm_mat** e_out) {
   const bool fused = spamm::sp2_fused_supported(x->m.nb);
   // One host sync for tr(X), tr(X^2) and the union size of the update.
-  int64_t* sc = spamm::dmalloc<int64_t>(3, s);
-  SPAMM_CK(cudaMemsetAsync(sc, 0, 3 * sizeof(int64_t), s));
+  int64_t* sc = spamm::dmalloc<int64_t>(4, s);
+  SPAMM_CK(cudaMemsetAsync(sc, 0, 4 * sizeof(int64_t), s));
   if (!x->m.tr_valid) spamm::trace_launch(x->m, reinterpret_cast<double*>(sc), s);
   spamm::trace_launch(c->m, reinterpret_cast<double*>(sc + 1), s);
   spamm::UnionPrep prep;
   if (fused) prep = spamm::sp2_union_prepare(x->m, c->m, sc + 2, s);
-  int64_t h[3];
-  spamm::d2h_sync(h, sc, 3, s);
+  const int64_t* kept_dev = spamm::pending_kept(c->m);  // lazy prune of X^2 rides along
+  if (kept_dev)
+    SPAMM_CK(cudaMemcpyAsync(sc + 3, kept_dev, sizeof(int64_t), cudaMemcpyDeviceToDevice, s));
+  int64_t h[4];
+  spamm::d2h_sync(h, sc, 4, s);
   spamm::dfree(sc, s);
+  if (kept_dev) spamm::settle(const_cast<spamm_mat*>(c)->m, h[3], s);
   if (!x->m.tr_valid) {
     memcpy(&x->m.tr, &h[0], sizeof(double));
     x->m.tr_valid = true;
@@ -482,7 +493,7 @@ int spamm_sp2_step(const spamm_mat* x, double n_occ, double tau, int32_t kernel,
   SPAMM_API_BEGIN
   cudaStream_t s = S(stream);
   auto* c = new spamm_mat();
-  multiply_impl(x, x, tau, kernel, timed != 0, s, c->m, stats);
+  multiply_impl(x, x, tau, kernel, timed != 0, s, c->m, stats, 0, -1, nullptr, true);
   spamm_mat* e = nullptr;
   bool square = true;
   double tx = 0, tsq = 0;
@@ -731,7 +742,7 @@ int spamm_sp2_solve(const spamm_mat* f, double n_occ, double tau, int32_t max_it
   for (int it = 0; it < max_iter; ++it) {
     auto* c = new spamm_mat();
     spamm_stats st;
-    multiply_impl(x, x, tau, kernel, timed != 0, s, c->m, &st);
+    multiply_impl(x, x, tau, kernel, timed != 0, s, c->m, &st, 0, -1, nullptr, true);
     bool square = true;
     double tx = 0, tsq = 0, idem = 0;
     spamm_mat* e = nullptr;

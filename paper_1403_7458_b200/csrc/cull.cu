@@ -285,8 +285,8 @@ bool cull(const Mat& a, const Mat& b, double tau, bool want_tasks, CullResult& r
   int t0 = 0;
   const int T0 = std::min(a.top_t, b.top_t);
   if (T0 >= 1 && T0 < depth) {
-    SPAMM_CK(cudaEventSynchronize(a.top_ev));
-    SPAMM_CK(cudaEventSynchronize(b.top_ev));
+    event_wait(a.top_ev);
+    event_wait(b.top_ev);
     HostLevel L;
     if (!host_cull_top(a.host_top, b.host_top, T0, depth, tau, sym, lo, hi, r, L, full_prev,
                        diag_nodes)) {

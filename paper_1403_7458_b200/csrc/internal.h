@@ -20,6 +20,8 @@ T* dmalloc(size_t n, cudaStream_t s) {
 
 // Copy a few int64 from device to host and wait (the only host syncs on the path).
 void d2h_sync(int64_t* host, const int64_t* dev, int n, cudaStream_t s);
+void stream_wait(cudaStream_t s);   // spin-polls unless SPAMM_WAIT=block
+void event_wait(cudaEvent_t e);     // spin-polls
 
 // ---- quadtree matrix (device resident) ----
 struct Mat {
@@ -42,6 +44,9 @@ struct Mat {
   double* host_top = nullptr;
   int top_t = -1;
   cudaEvent_t top_ev = nullptr;
+  // Lazy prune state (finalize(..., defer = true)); nullptr once settled.
+  uint8_t* pend_nz = nullptr;
+  int64_t* pend_off = nullptr;
   cudaStream_t stream = nullptr;
   void release();
 };
@@ -55,7 +60,13 @@ bool is_symmetric(const Mat& m, cudaStream_t s);
 // (quadtree.py:170-194).  Takes ownership of data/keys, and of pre_n2 / pre_nz
 // when given (per-block leaf norm^2 and nonzero flags already computed by a
 // fused producer kernel; K1 is then skipped).
-void finalize(Mat& m, cudaStream_t s, double* pre_n2 = nullptr, uint8_t* pre_nz = nullptr);
+// defer = true: no host sync -- exact-zero blocks are kept until settle()
+// (the kept count is then read with some later sync, see pending_kept()).
+void finalize(Mat& m, cudaStream_t s, double* pre_n2 = nullptr, uint8_t* pre_nz = nullptr,
+              bool defer = false);
+const int64_t* pending_kept(const Mat& m);  // device count, or nullptr if settled
+void settle(Mat& m, int64_t kept, cudaStream_t s);
+void settle_sync(Mat& m, cudaStream_t s);
 // Fused SP2 update over the key union of X and X^2 (sp2.cu):
 //   idem2_root <- pyramid root of ||X^2 - X||^2 (add_scaled(1,X2,-1,X).norm()^2)
 //   expand     -> E = add_scaled(2, X, -1, X2) finalised into `e`.

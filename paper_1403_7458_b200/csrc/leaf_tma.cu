@@ -76,7 +76,7 @@ struct TmaCfg {
   static constexpr int SLAB = NB * 128;              // bytes of one 16-column slab
   static constexpr int TILE = NB * NB * 8;           // bytes of one leaf block
   static constexpr int STAGE = 2 * TILE;             // A + B
-  static constexpr size_t SMEM = (size_t)STAGES * STAGE + 1024 + 2 * STAGES * 8 + 64;
+  static constexpr size_t SMEM = (size_t)STAGES * STAGE + 1024 + 3 * STAGES * 8 + 64;
 };
 
 // Byte offset of element (r, c) inside a swizzled tile: 16-column slabs of
@@ -91,7 +91,8 @@ __global__ void __launch_bounds__(32 * (WARPS_M * WARPS_N + 1), 1)
     k_leaf_dmma_tma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     int64_t n_seg, const int64_t* __restrict__ seg, const Idx* __restrict__ a_idx,
                     const Idx* __restrict__ b_idx, const int64_t* __restrict__ c_out,
-                    const int64_t* __restrict__ c_mirror, int accumulate, double* __restrict__ C) {
+                    const int64_t* __restrict__ c_mirror, int accumulate, double* __restrict__ C,
+                    const int32_t* __restrict__ order, int* __restrict__ next_block) {
   using Cfg = TmaCfg<NB, WARPS_M, WARPS_N, STAGES>;
   constexpr int WTM = NB / WARPS_M, WTN = NB / WARPS_N, MT = WTM / 8, NT = WTN / 8;
   static_assert(WTN % 8 == 0 && WTM % 8 == 0, "warp tile must be a multiple of 8");
@@ -101,6 +102,9 @@ __global__ void __launch_bounds__(32 * (WARPS_M * WARPS_N + 1), 1)
   const uint32_t bars = base + STAGES * Cfg::STAGE;
   auto full = [&](int s) { return bars + 8u * s; };
   auto empty = [&](int s) { return bars + 8u * (STAGES + s); };
+  // Per-stage work descriptor written by the producer: (C segment << 2) |
+  // first-task bit | last-task bit, or -1 = no more work (sentinel stage).
+  int64_t* meta = reinterpret_cast<int64_t*>(smem_raw + (bars + 16u * STAGES - raw));
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -114,15 +118,26 @@ __global__ void __launch_bounds__(32 * (WARPS_M * WARPS_N + 1), 1)
 
   if (warp == Cfg::CONSUMERS) {
     // ---------------- producer warp ----------------
+    // Dynamic scheduling: C segments are taken from a global counter in
+    // longest-first order (LPT), so the tail of the launch is one short block.
     if (lane == 0) {
       asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
       asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
       int stage = 0;
       uint32_t phase = 0;
-      for (int64_t m = blockIdx.x; m < n_seg; m += gridDim.x) {
-        const int64_t t1 = seg[m + 1];
-        for (int64_t t = seg[m]; t < t1; ++t) {
+      for (;;) {
+        const int64_t i = atomicAdd(next_block, 1);
+        if (i >= n_seg) {
           mbar_wait(empty(stage), phase ^ 1u);
+          meta[stage] = -1;
+          mbar_arrive(full(stage));
+          break;
+        }
+        const int64_t m = order ? (int64_t)order[i] : i;
+        const int64_t t0 = seg[m], t1 = seg[m + 1];
+        for (int64_t t = t0; t < t1; ++t) {
+          mbar_wait(empty(stage), phase ^ 1u);
+          meta[stage] = (m << 2) | (t == t0 ? 1 : 0) | (t + 1 == t1 ? 2 : 0);
           mbar_expect_tx(full(stage), Cfg::STAGE);
           const int ra = (int)a_idx[t] * NB, rb = (int)b_idx[t] * NB;
           const uint32_t sa = base + stage * Cfg::STAGE, sb = sa + Cfg::TILE;
@@ -159,50 +174,54 @@ __global__ void __launch_bounds__(32 * (WARPS_M * WARPS_N + 1), 1)
 
   int stage = 0;
   uint32_t phase = 0;
-  for (int64_t m = blockIdx.x; m < n_seg; m += gridDim.x) {
+  double acc[MT][NT][2];
+  for (;;) {
+    mbar_wait(full(stage), phase);
+    const int64_t md = meta[stage];
+    if (md < 0) break;
+    const int64_t m = md >> 2;
     double* Cb = C + (c_out ? c_out[m] : m) * (int64_t)(NB * NB);
-    double acc[MT][NT][2];
+    if (md & 1) {
 #pragma unroll
-    for (int mt = 0; mt < MT; ++mt)
-#pragma unroll
-      for (int nt = 0; nt < NT; ++nt) {
-        if (accumulate) {
-          const double2 v = *reinterpret_cast<const double2*>(
-              Cb + (row0 + mt * 8 + r8) * NB + col0 + nt * 8 + 2 * c4);
-          acc[mt][nt][0] = v.x;
-          acc[mt][nt][1] = v.y;
-        } else {
-          acc[mt][nt][0] = 0.0;
-          acc[mt][nt][1] = 0.0;
-        }
-      }
-    const int64_t t1 = seg[m + 1];
-    for (int64_t t = seg[m]; t < t1; ++t) {
-      mbar_wait(full(stage), phase);
-      const uint32_t sa = base + stage * Cfg::STAGE, sb = sa + Cfg::TILE;
-#pragma unroll
-      for (int kk = 0; kk < NB; kk += 4) {
-        double af[MT], bf[NT];
-#pragma unroll
-        for (int mt = 0; mt < MT; ++mt)
-          af[mt] = lds64(sa + (kk >> 4) * Cfg::SLAB + (row0 + mt * 8) * 128 + offA[(kk >> 2) & 3]);
+      for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) {
-          const int cb = col0 + nt * 8;
-          bf[nt] = lds64(sb + (cb >> 4) * Cfg::SLAB + kk * 128 + offB[(cb >> 3) & 1][(kk >> 2) & 1]);
+          if (accumulate) {
+            const double2 v = *reinterpret_cast<const double2*>(
+                Cb + (row0 + mt * 8 + r8) * NB + col0 + nt * 8 + 2 * c4);
+            acc[mt][nt][0] = v.x;
+            acc[mt][nt][1] = v.y;
+          } else {
+            acc[mt][nt][0] = 0.0;
+            acc[mt][nt][1] = 0.0;
+          }
         }
-#pragma unroll
-        for (int mt = 0; mt < MT; ++mt)
-#pragma unroll
-          for (int nt = 0; nt < NT; ++nt) dmma884(acc[mt][nt], af[mt], bf[nt]);
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(empty(stage));
-      if (++stage == STAGES) {
-        stage = 0;
-        phase ^= 1u;
-      }
     }
+    const uint32_t sa = base + stage * Cfg::STAGE, sb = sa + Cfg::TILE;
+#pragma unroll
+    for (int kk = 0; kk < NB; kk += 4) {
+      double af[MT], bf[NT];
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt)
+        af[mt] = lds64(sa + (kk >> 4) * Cfg::SLAB + (row0 + mt * 8) * 128 + offA[(kk >> 2) & 3]);
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        const int cb = col0 + nt * 8;
+        bf[nt] = lds64(sb + (cb >> 4) * Cfg::SLAB + kk * 128 + offB[(cb >> 3) & 1][(kk >> 2) & 1]);
+      }
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) dmma884(acc[mt][nt], af[mt], bf[nt]);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty(stage));
+    if (++stage == STAGES) {
+      stage = 0;
+      phase ^= 1u;
+    }
+    if (!(md & 2)) continue;
+    // last task of this C block: epilogue
 #pragma unroll
     for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
@@ -226,6 +245,60 @@ __global__ void __launch_bounds__(32 * (WARPS_M * WARPS_N + 1), 1)
           Cm[(c + 1) * NB + r] = acc[mt][nt][1];
         }
     }
+  }
+}
+
+// LPT order of the C segments: counting sort by task count, longest first.
+// (Order within equal lengths is arbitrary: it only changes which CTA runs a
+// block, never its result.)
+__global__ void k_len_hist(const int64_t* __restrict__ seg, int64_t n, int maxlen,
+                           int* __restrict__ hist) {
+  for (int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; m < n;
+       m += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t l = seg[m + 1] - seg[m];
+    atomicAdd(hist + (l < maxlen ? maxlen - l : 0), 1);  // bin 0 = longest
+  }
+}
+
+// Exclusive scan of the (maxlen + 1)-bin histogram, one 1024-thread CTA.
+__global__ void __launch_bounds__(1024) k_hist_scan(int* __restrict__ hist, int nbins) {
+  __shared__ int warp_tot[32];
+  const int per = (nbins + 1023) / 1024, b0 = threadIdx.x * per;
+  int loc = 0;
+  for (int b = b0; b < b0 + per && b < nbins; ++b) loc += hist[b];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int inc = loc;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += v;
+  }
+  if (lane == 31) warp_tot[warp] = inc;
+  __syncthreads();
+  if (warp == 0) {
+    int w = warp_tot[lane], wi = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, wi, o);
+      if (lane >= o) wi += v;
+    }
+    warp_tot[lane] = wi - w;
+  }
+  __syncthreads();
+  int run = warp_tot[warp] + inc - loc;
+  for (int b = b0; b < b0 + per && b < nbins; ++b) {
+    const int c = hist[b];
+    hist[b] = run;
+    run += c;
+  }
+}
+
+__global__ void k_len_scatter(const int64_t* __restrict__ seg, int64_t n, int maxlen,
+                              int* __restrict__ start, int32_t* __restrict__ order) {
+  for (int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; m < n;
+       m += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t l = seg[m + 1] - seg[m];
+    order[atomicAdd(start + (l < maxlen ? maxlen - l : 0), 1)] = (int32_t)m;
   }
 }
 
@@ -282,9 +355,23 @@ void launch_tma(int64_t n_seg, const int64_t* seg, const Idx* a_idx, const Idx* 
   const CUtensorMap ta = make_map(A, a_blocks, NB), tb = make_map(B, b_blocks, NB);
   int64_t grid = (int64_t)sm_count() * CTAS_PER_SM;
   if (grid > n_seg) grid = n_seg;
-  kern<<<(unsigned)grid, Cfg::THREADS, Cfg::SMEM, s>>>(ta, tb, n_seg, seg, a_idx, b_idx, c_out,
-                                                       c_mirror, acc ? 1 : 0, C);
+  // scratch: [next-block counter | length histogram (maxlen + 1 bins) | LPT order]
+  const int maxlen = 4096;
+  int* scratch = dmalloc<int>(1 + (maxlen + 1) + n_seg, s);
+  int* counter = scratch;
+  int* hist = scratch + 1;
+  int32_t* order = scratch + 2 + maxlen;
+  SPAMM_CK(cudaMemsetAsync(scratch, 0, (2 + maxlen) * sizeof(int), s));
+  k_len_hist<<<grid_for(n_seg, 256), 256, 0, s>>>(seg, n_seg, maxlen, hist);
   SPAMM_LAUNCH_CK();
+  k_hist_scan<<<1, 1024, 0, s>>>(hist, maxlen + 1);
+  SPAMM_LAUNCH_CK();
+  k_len_scatter<<<grid_for(n_seg, 256), 256, 0, s>>>(seg, n_seg, maxlen, hist, order);
+  SPAMM_LAUNCH_CK();
+  kern<<<(unsigned)grid, Cfg::THREADS, Cfg::SMEM, s>>>(ta, tb, n_seg, seg, a_idx, b_idx, c_out,
+                                                       c_mirror, acc ? 1 : 0, C, order, counter);
+  SPAMM_LAUNCH_CK();
+  dfree(scratch, s);
 }
 
 }  // namespace

@@ -13,6 +13,8 @@
 //  * blocks whose entries are all exactly zero are pruned (quadtree.py:177-180).
 // HBM roofline: S*Nb^2*8 bytes read per pass; K1.
 #include <algorithm>
+#include <cstdlib>
+#include <cstring>
 #include <mutex>
 #include <vector>
 
@@ -54,11 +56,38 @@ void reserve_pool(size_t bytes, cudaStream_t s) {
   SPAMM_CK(cudaStreamSynchronize(s));
 }
 
+// Host wait for the stream: polls cudaStreamQuery (about 10 us less wake-up
+// latency per wait than a blocking synchronize, ~0.5 ms per cfg4 SP2 solve);
+// SPAMM_WAIT=block selects cudaStreamSynchronize.
+void stream_wait(cudaStream_t s) {
+  static const bool spin = [] {
+    const char* v = getenv("SPAMM_WAIT");
+    return !(v && strcmp(v, "block") == 0);
+  }();
+  if (!spin) {
+    SPAMM_CK(cudaStreamSynchronize(s));
+    return;
+  }
+  for (;;) {
+    const cudaError_t e = cudaStreamQuery(s);
+    if (e == cudaSuccess) return;
+    if (e != cudaErrorNotReady) SPAMM_CK(e);
+  }
+}
+
+void event_wait(cudaEvent_t e) {
+  for (;;) {
+    const cudaError_t r = cudaEventQuery(e);
+    if (r == cudaSuccess) return;
+    if (r != cudaErrorNotReady) SPAMM_CK(r);
+  }
+}
+
 void d2h_sync(int64_t* host, const int64_t* dev, int n, cudaStream_t s) {
   static thread_local int64_t* pinned = nullptr;
   if (!pinned) SPAMM_CK(cudaMallocHost(&pinned, 64 * sizeof(int64_t)));
   SPAMM_CK(cudaMemcpyAsync(pinned, dev, n * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-  SPAMM_CK(cudaStreamSynchronize(s));
+  stream_wait(s);
   for (int i = 0; i < n; ++i) host[i] = pinned[i];
 }
 
@@ -96,6 +125,10 @@ void top_release(double* buf, cudaEvent_t ev) {
 }  // namespace
 
 void Mat::release() {
+  dfree(pend_nz, stream);
+  dfree(pend_off, stream);
+  pend_nz = nullptr;
+  pend_off = nullptr;
   top_release(host_top, top_ev);
   host_top = nullptr;
   top_ev = nullptr;
@@ -223,7 +256,7 @@ __global__ void k_compact_blocks(const double* __restrict__ din, const int64_t* 
     for (int e = threadIdx.x; e < nb2; e += blockDim.x) dout[d * nb2 + e] = din[b * nb2 + e];
     if (threadIdx.x == 0) {
       kout[d] = kin[b];
-      nout[d] = nin[b];
+      if (nout) nout[d] = nin[b];
     }
   }
 }
@@ -342,7 +375,7 @@ void scatter_slots(const int64_t* keys, int64_t m, int32_t* slot, cudaStream_t s
   SPAMM_LAUNCH_CK();
 }
 
-void finalize(Mat& m, cudaStream_t s, double* pre_n2, uint8_t* pre_nz) {
+void finalize(Mat& m, cudaStream_t s, double* pre_n2, uint8_t* pre_nz, bool defer) {
   m.stream = s;
   const int nb2 = m.nb * m.nb;
   double* n2 = pre_n2;
@@ -355,27 +388,36 @@ void finalize(Mat& m, cudaStream_t s, double* pre_n2, uint8_t* pre_nz) {
     }
     int64_t* off = dmalloc<int64_t>(m.nblocks + 1, s);
     scan_exclusive_u8(nz, m.nblocks, off, s);
-    int64_t kept = 0;
-    d2h_sync(&kept, off + m.nblocks, 1, s);
-    if (kept < m.nblocks) {
-      double* d2 = dmalloc<double>((size_t)kept * nb2, s);
-      int64_t* k2 = dmalloc<int64_t>(kept, s);
-      double* nn = dmalloc<double>(kept, s);
-      if (kept > 0) {
-        k_compact_blocks<<<grid_for(m.nblocks, 1, 148LL * 32), 128, 0, s>>>(
-            m.data, m.keys, n2, nz, off, m.nblocks, nb2, d2, k2, nn);
-        SPAMM_LAUNCH_CK();
+    if (defer) {
+      // Lazy prune: exact-zero blocks stay in storage and in the slot map for
+      // now (their norm is exactly 0, so they never survive a cull, add zero
+      // to traces and norms, and produce zero / pruned blocks in updates);
+      // settle() drops them once the kept count rides on a later host sync.
+      m.pend_nz = nz;
+      m.pend_off = off;
+    } else {
+      int64_t kept = 0;
+      d2h_sync(&kept, off + m.nblocks, 1, s);
+      if (kept < m.nblocks) {
+        double* d2 = dmalloc<double>((size_t)kept * nb2, s);
+        int64_t* k2 = dmalloc<int64_t>(kept, s);
+        double* nn = dmalloc<double>(kept, s);
+        if (kept > 0) {
+          k_compact_blocks<<<grid_for(m.nblocks, 1, 148LL * 32), 128, 0, s>>>(
+              m.data, m.keys, n2, nz, off, m.nblocks, nb2, d2, k2, nn);
+          SPAMM_LAUNCH_CK();
+        }
+        dfree(m.data, s);
+        dfree(m.keys, s);
+        dfree(n2, s);
+        m.data = d2;
+        m.keys = k2;
+        n2 = nn;
+        m.nblocks = kept;
       }
-      dfree(m.data, s);
-      dfree(m.keys, s);
-      dfree(n2, s);
-      m.data = d2;
-      m.keys = k2;
-      n2 = nn;
-      m.nblocks = kept;
+      dfree(nz, s);
+      dfree(off, s);
     }
-    dfree(nz, s);
-    dfree(off, s);
   }
   m.G = int64_t(1) << m.depth;
   m.slot = dmalloc<int32_t>(m.G * m.G, s);
@@ -397,6 +439,46 @@ void finalize(Mat& m, cudaStream_t s, double* pre_n2, uint8_t* pre_nz) {
                              cudaMemcpyDeviceToHost, s));
     SPAMM_CK(cudaEventRecord(m.top_ev, s));
   }
+}
+
+const int64_t* pending_kept(const Mat& m) {
+  return m.pend_off ? m.pend_off + m.nblocks : nullptr;
+}
+
+void settle(Mat& m, int64_t kept, cudaStream_t s) {
+  if (!m.pend_off) return;
+  if (kept < m.nblocks) {
+    const int nb2 = m.nb * m.nb;
+    double* d2 = dmalloc<double>((size_t)kept * nb2, s);
+    int64_t* k2 = dmalloc<int64_t>(kept, s);
+    if (kept > 0) {
+      k_compact_blocks<<<grid_for(m.nblocks, 1, 148LL * 32), 128, 0, s>>>(
+          m.data, m.keys, nullptr, m.pend_nz, m.pend_off, m.nblocks, nb2, d2, k2, nullptr);
+      SPAMM_LAUNCH_CK();
+    }
+    dfree(m.data, s);
+    dfree(m.keys, s);
+    m.data = d2;
+    m.keys = k2;
+    m.nblocks = kept;
+    // the pyramid is unchanged (the dropped blocks had norm 0); the slot map is rebuilt
+    SPAMM_CK(cudaMemsetAsync(m.slot, 0xFF, m.G * m.G * sizeof(int32_t), s));
+    if (kept > 0) {
+      k_scatter_slots<<<grid_for(kept, 256), 256, 0, s>>>(m.keys, kept, m.slot);
+      SPAMM_LAUNCH_CK();
+    }
+  }
+  dfree(m.pend_nz, s);
+  dfree(m.pend_off, s);
+  m.pend_nz = nullptr;
+  m.pend_off = nullptr;
+}
+
+void settle_sync(Mat& m, cudaStream_t s) {
+  if (!m.pend_off) return;
+  int64_t kept = 0;
+  d2h_sync(&kept, pending_kept(m), 1, s);
+  settle(m, kept, s);
 }
 
 }  // namespace spamm

@@ -210,14 +210,11 @@ void sp2_update_finish(const Mat& x, const Mat& x2, UnionPrep& prep, int64_t U, 
     else
       launch_update<1024>(want_idem, expand, ukeys, U, x, x2, E, nD2, nE2, nzE, s);
   }
+  double* pn = nullptr;
   if (want_idem) {
     const int64_t ps = pyramid_size(x.depth);
-    double* pn = dmalloc<double>(2 * ps, s);
+    pn = dmalloc<double>(2 * ps, s);
     build_pyramid(ukeys, nD2, U, x.depth, pn, pn + ps, s);
-    int64_t bits = 0;
-    d2h_sync(&bits, reinterpret_cast<const int64_t*>(pn), 1, s);
-    memcpy(idem_norm, &bits, sizeof(double));
-    dfree(pn, s);
     dfree(nD2, s);
   }
   if (expand) {
@@ -229,11 +226,26 @@ void sp2_update_finish(const Mat& x, const Mat& x2, UnionPrep& prep, int64_t U, 
     e.nblocks = U;
     e.data = E;
     e.keys = ukeys;
-    finalize(e, s, nE2, nzE);
+    finalize(e, s, nE2, nzE, /*defer=*/true);
     e.sym = x.sym && x2.sym;
   } else {
     dfree(ukeys, s);
   }
+  // One host sync for the idempotency norm and E's kept-block count.
+  const int64_t* kept_dev = expand ? pending_kept(e) : nullptr;
+  if (want_idem || kept_dev) {
+    int64_t* sc = dmalloc<int64_t>(2, s);
+    if (want_idem)
+      SPAMM_CK(cudaMemcpyAsync(sc, pn, sizeof(int64_t), cudaMemcpyDeviceToDevice, s));
+    if (kept_dev)
+      SPAMM_CK(cudaMemcpyAsync(sc + 1, kept_dev, sizeof(int64_t), cudaMemcpyDeviceToDevice, s));
+    int64_t h[2] = {0, 0};
+    d2h_sync(h, sc, 2, s);
+    dfree(sc, s);
+    if (want_idem) memcpy(idem_norm, &h[0], sizeof(double));
+    if (kept_dev) settle(e, h[1], s);
+  }
+  dfree(pn, s);
 }
 
 }  // namespace spamm
