@@ -118,6 +118,11 @@ int spamm_multiply_range(const spamm_mat* a, const spamm_mat* b, double tau, int
  * symmetric, multiply computes only C blocks with i <= j and mirrors the rest;
  * counters stay the full reference counts.  0 disables (A/B testing). */
 int spamm_set_symmetric_products(int32_t enabled);
+/* Dense cull (default on): for trees of depth <= 8 the cull evaluates every
+ * leaf triple with its ancestor chain in two passes and one host sync instead
+ * of the tier-by-tier walk; task sets, order and counters are identical.
+ * 0 forces the tier walk (A/B testing). */
+int spamm_set_dense_cull(int32_t enabled);
 /* Pre-grow the library's stream-ordered memory pool by `bytes` (kept mapped),
  * so steady-state allocations never wait on a new device mapping. */
 int spamm_reserve_pool(int64_t bytes, void* stream);

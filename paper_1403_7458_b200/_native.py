@@ -71,6 +71,7 @@ _SIGS = {
                                ctypes.POINTER(Stats)]),
     "spamm_census": (c_i32, [c_vp, c_vp, c_f64, c_vp, ctypes.POINTER(Stats)]),
     "spamm_set_symmetric_products": (c_i32, [c_i32]),
+    "spamm_set_dense_cull": (c_i32, [c_i32]),
     "spamm_multiply_range": (c_i32, [c_vp, c_vp, c_f64, c_i32, c_i64, c_i64, c_vp, c_vp,
                                      ctypes.POINTER(c_vp), ctypes.POINTER(Stats)]),
     "spamm_reserve_pool": (c_i32, [c_i64, c_vp]),

@@ -574,6 +574,11 @@ int spamm_set_symmetric_products(int32_t enabled) {
   return SPAMM_OK;
 }
 
+int spamm_set_dense_cull(int32_t enabled) {
+  spamm::set_dense_cull(enabled != 0);
+  return SPAMM_OK;
+}
+
 int spamm_census(const spamm_mat* a, const spamm_mat* b, double tau, void* stream,
                  spamm_stats* stats) {
   if (int rc = check_conformable(a, b)) return rc;

@@ -235,6 +235,180 @@ bool host_cull_top(const double* nA, const double* nB, int T0, int depth, double
   return true;
 }
 
+// ---------------------------------------------------------------- dense cull
+// For a small tree (depth <= DENSE_MAX_DEPTH, G <= 256) the whole cull is two
+// data-parallel passes and ONE host sync instead of a tier-by-tier walk.  A
+// leaf triple (i,k,j) is a survivor of _sweep iff its own product and every
+// ancestor's product pass (kernel.py:108-113: a triple is only ever tested
+// when its parent survived), so each triple is evaluated directly with its
+// ancestor chain -- the same IEEE predicates, hence the same set and the same
+// per-tier counts as the recursive walk, in the same output order (C blocks
+// in Morton order, k ascending).
+constexpr int DENSE_MAX_DEPTH = 8;
+bool g_dense_enabled = true;
+
+__device__ __forceinline__ bool keep_chain(const double* __restrict__ nA,
+                                           const double* __restrict__ nB, double tau, int t,
+                                           int64_t i, int64_t k, int64_t j) {
+  // tiers t, t-1, ..., 0 (most selective first)
+  for (int u = t; u >= 0; --u) {
+    const int sh = t - u;
+    const int64_t W = int64_t(1) << u;
+    const int64_t off = tier_offset(u);
+    if (!keep_pair(nA[off + (i >> sh) * W + (k >> sh)], nB[off + (k >> sh) * W + (j >> sh)], tau))
+      return false;
+  }
+  return true;
+}
+
+// Survivor counts of every tier t < depth (full enumeration, 8^t triples).
+__global__ void __launch_bounds__(256)
+    k_dense_tiers(const double* __restrict__ nA, const double* __restrict__ nB, double tau,
+                  int depth, unsigned long long* __restrict__ counts) {
+  __shared__ unsigned long long sc[DENSE_MAX_DEPTH];
+  if (threadIdx.x < DENSE_MAX_DEPTH) sc[threadIdx.x] = 0;
+  __syncthreads();
+  const int64_t total = ((int64_t(1) << (3 * depth)) - 1) / 7;
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < total;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    int t = 0;
+    while ((((int64_t(1) << (3 * (t + 1))) - 1) / 7) <= q) ++t;
+    const int64_t r = q - ((int64_t(1) << (3 * t)) - 1) / 7;
+    const int64_t i = r >> (2 * t), k = (r >> t) & ((int64_t(1) << t) - 1),
+                  j = r & ((int64_t(1) << t) - 1);
+    if (keep_chain(nA, nB, tau, t, i, k, j)) atomicAdd(sc + t, 1ull);
+  }
+  __syncthreads();
+  if (threadIdx.x < depth && sc[threadIdx.x]) atomicAdd(counts + threadIdx.x, sc[threadIdx.x]);
+}
+
+// Leaf tier, one warp per C position m (Morton order).  WRITE=false: packed
+// (node flag << 40 | count) per m + symmetric bookkeeping in aux; WRITE=true:
+// compaction into the scanned offsets.
+template <bool WRITE>
+__global__ void __launch_bounds__(CULL_THREADS)
+    k_dense_leaf(int depth, const double* __restrict__ nA, const double* __restrict__ nB,
+                 double tau, int sym, int64_t* __restrict__ cnt, const int64_t* __restrict__ off,
+                 int32_t* __restrict__ ci_o, int32_t* __restrict__ cj_o,
+                 int64_t* __restrict__ seg_o, int32_t* __restrict__ K_o,
+                 const int32_t* __restrict__ slotA, const int32_t* __restrict__ slotB,
+                 int32_t* __restrict__ aidx, int32_t* __restrict__ bidx, int64_t Mn, int64_t Vn,
+                 unsigned long long* __restrict__ aux) {
+  const int64_t G = int64_t(1) << depth;
+  const int lane = threadIdx.x & 31;
+  const unsigned lt_mask = (1u << lane) - 1u;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  if (WRITE && gw == 0 && lane == 0) seg_o[Mn] = Vn;
+  for (int64_t m = gw; m < G * G; m += nw) {
+    uint32_t ui, uj;
+    morton_decode((uint64_t)m, ui, uj);
+    const int64_t i = ui, j = uj;
+    if (sym && i > j) {
+      if (!WRITE && lane == 0) cnt[m] = 0;
+      continue;
+    }
+    int64_t toff = 0;
+    if (WRITE) {
+      const int64_t v = off[m], vn = off[m + 1];
+      if (((vn - v) & TASK_MASK) == 0) continue;
+      const int64_t node = v >> NODE_SHIFT;
+      toff = v & TASK_MASK;
+      if (lane == 0) {
+        ci_o[node] = (int32_t)i;
+        cj_o[node] = (int32_t)j;
+        seg_o[node] = toff;
+      }
+    }
+    int64_t c = 0;
+    for (int64_t k0 = 0; k0 < G; k0 += 32) {
+      const int64_t k = k0 + lane;
+      const bool valid = k < G;
+      const bool keep = valid && keep_chain(nA, nB, tau, depth, i, k, j);
+      const unsigned mask = __ballot_sync(0xffffffffu, keep);
+      if (!WRITE && sym && i != j) {
+        const bool keep_m = valid && keep_chain(nA, nB, tau, depth, j, k, i);
+        if (__any_sync(0xffffffffu, keep != keep_m) && lane == 0) atomicOr(aux + 1, 1ull);
+      }
+      if (WRITE) {
+        if (keep) {
+          const int64_t pos = toff + __popc(mask & lt_mask);
+          K_o[pos] = (int32_t)k;
+          aidx[pos] = slotA[i * G + k];
+          bidx[pos] = slotB[k * G + j];
+        }
+        toff += __popc(mask);
+      } else {
+        c += __popc(mask);
+      }
+    }
+    if (!WRITE && lane == 0) {
+      cnt[m] = c + (c > 0 ? (int64_t(1) << NODE_SHIFT) : 0);
+      if (sym && i == j && c) {
+        atomicAdd(aux, (unsigned long long)c);
+        atomicAdd(aux + 3, 1ull);
+      }
+    }
+  }
+}
+
+bool dense_cull(const Mat& a, const Mat& b, double tau, bool want_tasks, CullResult& r,
+                cudaStream_t s, bool sym) {
+  const int depth = a.depth;
+  const int64_t G = int64_t(1) << depth, npos = G * G;
+  // aux[0]: survivors in diagonal C blocks, [1]: mirror mismatch, [2]: packed
+  // scan total, [3]: diagonal C blocks with survivors, [4 + t]: tier-t survivors
+  int64_t* aux = dmalloc<int64_t>(4 + DENSE_MAX_DEPTH, s);
+  int64_t* cnt = dmalloc<int64_t>(npos, s);
+  int64_t* off = dmalloc<int64_t>(npos + 1, s);
+  SPAMM_CK(cudaMemsetAsync(aux, 0, (4 + DENSE_MAX_DEPTH) * sizeof(int64_t), s));
+  if (depth > 0) {
+    const int64_t tri = ((int64_t(1) << (3 * depth)) - 1) / 7;
+    k_dense_tiers<<<grid_for(tri, 256, 148LL * 8), 256, 0, s>>>(
+        a.norms, b.norms, tau, depth, reinterpret_cast<unsigned long long*>(aux + 4));
+    SPAMM_LAUNCH_CK();
+  }
+  k_dense_leaf<false><<<grid_for(npos * 32, CULL_THREADS, 148LL * 64), CULL_THREADS, 0, s>>>(
+      depth, a.norms, b.norms, tau, sym ? 1 : 0, cnt, nullptr, nullptr, nullptr, nullptr, nullptr,
+      nullptr, nullptr, nullptr, nullptr, 0, 0, reinterpret_cast<unsigned long long*>(aux));
+  SPAMM_LAUNCH_CK();
+  scan_exclusive_i64(cnt, npos, off, s);
+  SPAMM_CK(cudaMemcpyAsync(aux + 2, off + npos, sizeof(int64_t), cudaMemcpyDeviceToDevice, s));
+  int64_t h[4 + DENSE_MAX_DEPTH];
+  d2h_sync(h, aux, 4 + depth, s);
+  dfree(aux, s);
+  dfree(cnt, s);
+  if (h[1]) {  // leaf survivor set not mirror-symmetric (ulp tie): full cull
+    dfree(off, s);
+    return false;
+  }
+  const int64_t V = h[2] & TASK_MASK, M = h[2] >> NODE_SHIFT;
+  for (int t = 0; t < depth; ++t) r.visited[t] = h[4 + t];
+  r.visited[depth] = sym ? 2 * V - h[0] : V;
+  for (int t = 0; t <= depth; ++t)
+    r.culled[t] = (t == 0 ? 1 : 8 * r.visited[t - 1]) - r.visited[t];
+  if (!want_tasks || V == 0) {
+    dfree(off, s);
+    if (!want_tasks) r.n_tasks = r.visited[depth];
+    return true;
+  }
+  r.ci = dmalloc<int32_t>(M, s);
+  r.cj = dmalloc<int32_t>(M, s);
+  r.seg = dmalloc<int64_t>(M + 1, s);
+  r.k = dmalloc<int32_t>(V, s);
+  r.a_idx = dmalloc<int32_t>(V, s);
+  r.b_idx = dmalloc<int32_t>(V, s);
+  k_dense_leaf<true><<<grid_for(npos * 32, CULL_THREADS, 148LL * 64), CULL_THREADS, 0, s>>>(
+      depth, a.norms, b.norms, tau, sym ? 1 : 0, nullptr, off, r.ci, r.cj, r.seg, r.k, a.slot,
+      b.slot, r.a_idx, r.b_idx, M, V, nullptr);
+  SPAMM_LAUNCH_CK();
+  dfree(off, s);
+  r.n_c = M;
+  r.n_c_full = sym ? 2 * M - h[3] : M;
+  r.n_tasks = V;
+  return true;
+}
+
 void* pinned_staging(size_t bytes) {
   static thread_local void* buf = nullptr;
   static thread_local size_t cap = 0;
@@ -247,6 +421,8 @@ void* pinned_staging(size_t bytes) {
 }
 
 }  // namespace
+
+void set_dense_cull(bool enabled) { g_dense_enabled = enabled; }
 
 void CullResult::release(cudaStream_t s) {
   dfree(ci, s);
@@ -269,6 +445,8 @@ bool cull(const Mat& a, const Mat& b, double tau, bool want_tasks, CullResult& r
   r.culled.assign(depth + 1, 0);
   r.n_c = r.n_tasks = 0;
   r.sym = sym;
+  if (g_dense_enabled && depth <= DENSE_MAX_DEPTH && lo <= 0 && hi < 0 && !work)
+    return dense_cull(a, b, tau, want_tasks, r, s, sym);
 
   int32_t* ci = dmalloc<int32_t>(1, s);
   int32_t* cj = dmalloc<int32_t>(1, s);

@@ -123,6 +123,7 @@ struct CullResult {
 // [lo, hi) are produced (ancestors outside are pruned); counters then cover
 // only the shard.  work (Morton-indexed, G*G int32): task count per emitted C
 // block (persistence load balancing).
+void set_dense_cull(bool enabled);
 bool cull(const Mat& a, const Mat& b, double tau, bool want_tasks, CullResult& r, cudaStream_t s,
           bool sym = false, int64_t lo = 0, int64_t hi = -1, int32_t* work = nullptr);
 

@@ -32,7 +32,7 @@ from . import _native as nat
 from .quadtree import QuadTreeMatrix, _check_conformable
 
 __all__ = ["ProductStats", "multiply", "convolution_census", "leaf_gemm", "gemm_batch",
-           "leaf_tasks", "set_symmetric_products", "WORKERS_ENV_VAR"]
+           "leaf_tasks", "set_symmetric_products", "set_dense_cull", "WORKERS_ENV_VAR"]
 
 WORKERS_ENV_VAR = "SPAMM_WORKERS"
 
@@ -118,6 +118,12 @@ def set_symmetric_products(enabled: bool) -> None:
     """Toggle the symmetric SpAMM path (on by default; results are bitwise
     identical either way -- the switch exists for A/B measurements)."""
     nat.check(nat.load().spamm_set_symmetric_products(1 if enabled else 0))
+
+
+def set_dense_cull(enabled: bool) -> None:
+    """Toggle the dense cull for trees of depth <= 8 (on by default; task sets,
+    order and counters are identical to the tier walk -- A/B switch)."""
+    nat.check(nat.load().spamm_set_dense_cull(1 if enabled else 0))
 
 
 def multiply(a: QuadTreeMatrix, b: QuadTreeMatrix, tau: float, mode: str = "serial",

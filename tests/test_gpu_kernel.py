@@ -354,3 +354,60 @@ def test_cfg4_x0_square_task_set_and_properties():
     # run-to-run bitwise determinism at full size
     c3, _ = sp.multiply(x0, x0, cfg.tau)
     assert torch.equal(c.blocks_device(), c3.blocks_device())
+
+
+# -- dense cull (depth <= 8) == tier walk ---------------------------------------
+
+def _walk(fn):
+    sp.set_dense_cull(False)
+    try:
+        return fn()
+    finally:
+        sp.set_dense_cull(True)
+
+
+@pytest.mark.parametrize("case", ["sym", "pair", "sparse", "single", "deep", "nan"])
+def test_dense_cull_equals_tier_walk_and_reference(rng, case):
+    """The dense cull (every leaf triple tested with its ancestor chain) gives
+    the tier walk's task list (same order), counters and C, and the
+    reference _sweep's counters -- including a NaN block, where a parent's
+    NaN norm culls finite children (the reason the chain is tested)."""
+    nb = 4
+    if case == "sym":
+        da = _sym(rng, 61, 0.7)
+        db = da
+    elif case == "pair":
+        da, db = rng.standard_normal((61, 61)), rng.standard_normal((61, 61))
+    elif case == "sparse":
+        da = rng.standard_normal((64, 64))
+        da[np.abs(da) < 1.2] = 0.0
+        db = da.T.copy()
+    elif case == "single":
+        nb, da = 8, rng.standard_normal((7, 7))
+        db = da
+    elif case == "deep":                       # depth 8: G = 256 with Nb = 1
+        nb = 1
+        da = _sym(rng, 200, 0.3)
+        db = da
+    else:
+        da = _sym(rng, 48, 0.5)
+        da[9, 30] = np.nan
+        db = da
+    a = sp.build_from_dense(da, nb)
+    b = a if db is da else sp.build_from_dense(db, nb)
+    oa, ob = O.from_dense(da, nb), O.from_dense(db, nb)
+    norms = np.concatenate([t.ravel() for t in a._tier_norms])
+    fin = norms[np.isfinite(norms) & (norms > 0)]
+    for tau in (0.0, float(np.median(fin) ** 2), float(fin.max() ** 2) * 0.99, 1e300):
+        c_d, st_d = sp.multiply(a, b, tau, kernel="exact")
+        c_w, st_w = _walk(lambda: sp.multiply(a, b, tau, kernel="exact"))
+        assert st_d.counts_equal(st_w)
+        v, cu, ti, *_ = O.sweep(oa.tier_norms, ob.tier_norms, tau)
+        assert st_d.visited == tuple(v) and st_d.culled == tuple(cu)
+        assert st_d.leaf_products == len(ti)
+        assert np.array_equal(sp.to_dense(c_d), sp.to_dense(c_w), equal_nan=True)
+        t_d = sp.leaf_tasks(a, b, tau)
+        t_w = _walk(lambda: sp.leaf_tasks(a, b, tau))
+        assert all(np.array_equal(x, y) for x, y in zip(t_d, t_w))
+        cs = sp.convolution_census(a, b, tau)
+        assert cs.counts_equal(st_d)

@@ -124,6 +124,34 @@ def test_fused_update_bitwise_equals_add_scaled(rng, nb):
     assert idem0 == 0.0 and np.array_equal(sp.to_dense(z), d)
 
 
+@pytest.mark.parametrize("kernel", ["auto", "exact"])
+def test_sp2_step_with_exactly_cancelling_blocks(rng, kernel):
+    """X = [[I, M], [M^T, -I]] (+ a small tail) makes (X^2)_01 = M - M = 0
+    exactly: the native step's lazily pruned X^2 / 2X - X^2 must match the
+    reference's eagerly pruned ones (keys, data, pyramid, traces)."""
+    nb = 16
+    m = rng.standard_normal((2 * nb, 2 * nb))
+    n = 4 * nb
+    x = np.zeros((n, n))
+    x[: 2 * nb, : 2 * nb] = np.eye(2 * nb)
+    x[2 * nb:, 2 * nb:] = -np.eye(2 * nb)
+    x[: 2 * nb, 2 * nb:] = m
+    x[2 * nb:, : 2 * nb] = m.T
+    dx = sp.build_from_dense(x, nb)
+    ox = O.from_dense(x, nb)
+    for n_occ in (10, -10):           # one SQUARE, one EXPAND step (t_x = 0)
+        nxt, br = sp.sp2_step(dx, n_occ, 0.0, kernel=kernel)
+        onxt, obr, *_ = O.sp2_step(ox, n_occ, 0.0)
+        assert br == obr
+        assert np.array_equal(nxt._block_keys, onxt.keys)      # exact cancellation pruned
+        assert nxt.stored_leaf_count == len(onxt.keys)
+        if kernel == "exact":
+            assert np.array_equal(sp.to_dense(nxt), O.to_dense(onxt))
+            assert np.array_equal(pyramid_flat(nxt._tier_norms), pyramid_flat(onxt.tier_norms))
+        else:
+            assert rel(sp.to_dense(nxt), O.to_dense(onxt)) <= REL_FRO_TOL
+
+
 def test_idempotency_and_energy_error():
     h, n_occ = water_cluster(10, seed=4)
     f = sp.build_from_dense(h, 16)
