@@ -374,7 +374,14 @@ void multiply_impl(const spamm_mat* a, const spamm_mat* b, double tau, int32_t k
   const int64_t nb2 = (int64_t)C.nb * C.nb;
   int64_t* c_out = nullptr;
   int64_t* c_mirror = nullptr;
-  if (sym && r.n_c > 0) {
+  if (r.keys) {  // dense cull: layout already built
+    C.nblocks = r.n_c_full;
+    C.keys = r.keys;
+    r.keys = nullptr;
+    c_out = r.c_out;
+    c_mirror = r.c_mirror;
+    r.c_out = r.c_mirror = nullptr;
+  } else if (sym && r.n_c > 0) {
     const int64_t npos = C.G * C.G;
     uint8_t* flags = spamm::dmalloc<uint8_t>(npos, s);
     int64_t* off = spamm::dmalloc<int64_t>(npos + 1, s);
@@ -404,9 +411,12 @@ void multiply_impl(const spamm_mat* a, const spamm_mat* b, double tau, int32_t k
   C.data = spamm::dmalloc<double>((size_t)C.nblocks * nb2, s);
   tm.mark(1);  // leaf window = the K4 launch only (allocation stays outside)
   if (r.n_c > 0) {
+    spamm::LptSchedule lpt;
+    lpt.order = r.order;
+    lpt.counter = r.counter;
     spamm::leaf_products<int32_t>(r.n_c, r.seg, r.a_idx, r.b_idx, c_out, c_mirror, false,
                                   a->m.data, a->m.nblocks, b->m.data, b->m.nblocks, C.data, C.nb,
-                                  kernel, s);
+                                  kernel, s, lpt);
   }
   tm.mark(2);
   spamm::dfree(c_out, s);

@@ -282,18 +282,29 @@ __global__ void __launch_bounds__(256)
   if (threadIdx.x < depth && sc[threadIdx.x]) atomicAdd(counts + threadIdx.x, sc[threadIdx.x]);
 }
 
-// Leaf tier, one warp per C position m (Morton order).  WRITE=false: packed
-// (node flag << 40 | count) per m + symmetric bookkeeping in aux; WRITE=true:
-// compaction into the scanned offsets.
+// Leaf tier, one warp per C position m (Morton order).  Each m gets one
+// packed int64 so a single scan yields every offset the layout needs:
+//   bits  0..26  tasks of the node if it is emitted (symmetric: i <= j only)
+//   bits 27..44  1 if the node is emitted with >= 1 task  -> node index
+//   bits 45..62  1 if C block (i,j) exists at all         -> storage slot
+// (G <= 256: tasks <= 2^24, nodes <= 2^16.)  WRITE=false: counts, the LPT
+// length histogram and the symmetric mirror check.  WRITE=true: the task
+// lists, C keys, storage/mirror slots and the LPT order of the nodes.
+constexpr int DT_NODE = 27, DT_FULL = 45;
+constexpr int64_t DT_TASK_MASK = (int64_t(1) << DT_NODE) - 1;
+constexpr int64_t DT_IDX_MASK = (int64_t(1) << (DT_FULL - DT_NODE)) - 1;
+
 template <bool WRITE>
 __global__ void __launch_bounds__(CULL_THREADS)
     k_dense_leaf(int depth, const double* __restrict__ nA, const double* __restrict__ nB,
                  double tau, int sym, int64_t* __restrict__ cnt, const int64_t* __restrict__ off,
-                 int32_t* __restrict__ ci_o, int32_t* __restrict__ cj_o,
+                 int* __restrict__ hist, int32_t* __restrict__ ci_o, int32_t* __restrict__ cj_o,
                  int64_t* __restrict__ seg_o, int32_t* __restrict__ K_o,
                  const int32_t* __restrict__ slotA, const int32_t* __restrict__ slotB,
-                 int32_t* __restrict__ aidx, int32_t* __restrict__ bidx, int64_t Mn, int64_t Vn,
-                 unsigned long long* __restrict__ aux) {
+                 int32_t* __restrict__ aidx, int32_t* __restrict__ bidx,
+                 int64_t* __restrict__ keys, int64_t* __restrict__ c_out,
+                 int64_t* __restrict__ c_mirror, int32_t* __restrict__ order, int64_t Mn,
+                 int64_t Vn, unsigned long long* __restrict__ aux) {
   const int64_t G = int64_t(1) << depth;
   const int lane = threadIdx.x & 31;
   const unsigned lt_mask = (1u << lane) - 1u;
@@ -304,20 +315,27 @@ __global__ void __launch_bounds__(CULL_THREADS)
     uint32_t ui, uj;
     morton_decode((uint64_t)m, ui, uj);
     const int64_t i = ui, j = uj;
-    if (sym && i > j) {
-      if (!WRITE && lane == 0) cnt[m] = 0;
-      continue;
-    }
+    const bool emitted = !sym || i <= j;
     int64_t toff = 0;
     if (WRITE) {
-      const int64_t v = off[m], vn = off[m + 1];
-      if (((vn - v) & TASK_MASK) == 0) continue;
-      const int64_t node = v >> NODE_SHIFT;
-      toff = v & TASK_MASK;
+      const int64_t v = off[m], d = off[m + 1] - v;
+      if ((d >> DT_FULL) == 0) continue;  // no C block here
+      const int64_t pfull = v >> DT_FULL;
+      const int64_t ntask = d & DT_TASK_MASK;
+      if (lane == 0) keys[pfull] = i * G + j;
+      if (!emitted) continue;  // mirror of an emitted node
+      const int64_t node = (v >> DT_NODE) & DT_IDX_MASK;
+      toff = v & DT_TASK_MASK;
       if (lane == 0) {
         ci_o[node] = (int32_t)i;
         cj_o[node] = (int32_t)j;
         seg_o[node] = toff;
+        if (c_out) {
+          c_out[node] = pfull;
+          c_mirror[node] =
+              i < j ? off[(int64_t)morton_encode((uint32_t)j, (uint32_t)i)] >> DT_FULL : -1;
+        }
+        order[atomicAdd(hist + (G - ntask), 1)] = (int32_t)node;
       }
     }
     int64_t c = 0;
@@ -326,7 +344,7 @@ __global__ void __launch_bounds__(CULL_THREADS)
       const bool valid = k < G;
       const bool keep = valid && keep_chain(nA, nB, tau, depth, i, k, j);
       const unsigned mask = __ballot_sync(0xffffffffu, keep);
-      if (!WRITE && sym && i != j) {
+      if (!WRITE && sym && i < j) {
         const bool keep_m = valid && keep_chain(nA, nB, tau, depth, j, k, i);
         if (__any_sync(0xffffffffu, keep != keep_m) && lane == 0) atomicOr(aux + 1, 1ull);
       }
@@ -343,10 +361,11 @@ __global__ void __launch_bounds__(CULL_THREADS)
       }
     }
     if (!WRITE && lane == 0) {
-      cnt[m] = c + (c > 0 ? (int64_t(1) << NODE_SHIFT) : 0);
-      if (sym && i == j && c) {
-        atomicAdd(aux, (unsigned long long)c);
-        atomicAdd(aux + 3, 1ull);
+      cnt[m] = (emitted ? c + (c > 0 ? int64_t(1) << DT_NODE : 0) : 0) +
+               (c > 0 ? int64_t(1) << DT_FULL : 0);
+      if (c) {
+        atomicAdd(aux, (unsigned long long)c);  // full (reference) leaf count
+        if (emitted) atomicAdd(hist + (G - c), 1);
       }
     }
   }
@@ -356,12 +375,15 @@ bool dense_cull(const Mat& a, const Mat& b, double tau, bool want_tasks, CullRes
                 cudaStream_t s, bool sym) {
   const int depth = a.depth;
   const int64_t G = int64_t(1) << depth, npos = G * G;
-  // aux[0]: survivors in diagonal C blocks, [1]: mirror mismatch, [2]: packed
-  // scan total, [3]: diagonal C blocks with survivors, [4 + t]: tier-t survivors
+  // aux[0]: full leaf survivors, [1]: mirror mismatch, [2]: packed scan
+  // total, [4 + t]: tier-t survivors (t < depth)
   int64_t* aux = dmalloc<int64_t>(4 + DENSE_MAX_DEPTH, s);
   int64_t* cnt = dmalloc<int64_t>(npos, s);
   int64_t* off = dmalloc<int64_t>(npos + 1, s);
+  // LPT schedule scratch: G + 1 length bins (bin 0 = G tasks) + the K4 counter
+  int* sched = dmalloc<int>(G + 2, s);
   SPAMM_CK(cudaMemsetAsync(aux, 0, (4 + DENSE_MAX_DEPTH) * sizeof(int64_t), s));
+  SPAMM_CK(cudaMemsetAsync(sched, 0, (G + 2) * sizeof(int), s));
   if (depth > 0) {
     const int64_t tri = ((int64_t(1) << (3 * depth)) - 1) / 7;
     k_dense_tiers<<<grid_for(tri, 256, 148LL * 8), 256, 0, s>>>(
@@ -369,10 +391,12 @@ bool dense_cull(const Mat& a, const Mat& b, double tau, bool want_tasks, CullRes
     SPAMM_LAUNCH_CK();
   }
   k_dense_leaf<false><<<grid_for(npos * 32, CULL_THREADS, 148LL * 64), CULL_THREADS, 0, s>>>(
-      depth, a.norms, b.norms, tau, sym ? 1 : 0, cnt, nullptr, nullptr, nullptr, nullptr, nullptr,
-      nullptr, nullptr, nullptr, nullptr, 0, 0, reinterpret_cast<unsigned long long*>(aux));
+      depth, a.norms, b.norms, tau, sym ? 1 : 0, cnt, nullptr, sched, nullptr, nullptr, nullptr,
+      nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, 0, 0,
+      reinterpret_cast<unsigned long long*>(aux));
   SPAMM_LAUNCH_CK();
   scan_exclusive_i64(cnt, npos, off, s);
+  if (want_tasks) hist_scan_exclusive(sched, (int)G + 1, s);
   SPAMM_CK(cudaMemcpyAsync(aux + 2, off + npos, sizeof(int64_t), cudaMemcpyDeviceToDevice, s));
   int64_t h[4 + DENSE_MAX_DEPTH];
   d2h_sync(h, aux, 4 + depth, s);
@@ -380,15 +404,18 @@ bool dense_cull(const Mat& a, const Mat& b, double tau, bool want_tasks, CullRes
   dfree(cnt, s);
   if (h[1]) {  // leaf survivor set not mirror-symmetric (ulp tie): full cull
     dfree(off, s);
+    dfree(sched, s);
     return false;
   }
-  const int64_t V = h[2] & TASK_MASK, M = h[2] >> NODE_SHIFT;
+  const int64_t V = h[2] & DT_TASK_MASK, M = (h[2] >> DT_NODE) & DT_IDX_MASK,
+                F = h[2] >> DT_FULL;
   for (int t = 0; t < depth; ++t) r.visited[t] = h[4 + t];
-  r.visited[depth] = sym ? 2 * V - h[0] : V;
+  r.visited[depth] = h[0];
   for (int t = 0; t <= depth; ++t)
     r.culled[t] = (t == 0 ? 1 : 8 * r.visited[t - 1]) - r.visited[t];
   if (!want_tasks || V == 0) {
     dfree(off, s);
+    dfree(sched, s);
     if (!want_tasks) r.n_tasks = r.visited[depth];
     return true;
   }
@@ -398,13 +425,21 @@ bool dense_cull(const Mat& a, const Mat& b, double tau, bool want_tasks, CullRes
   r.k = dmalloc<int32_t>(V, s);
   r.a_idx = dmalloc<int32_t>(V, s);
   r.b_idx = dmalloc<int32_t>(V, s);
+  r.keys = dmalloc<int64_t>(F, s);
+  r.order = dmalloc<int32_t>(M, s);
+  if (sym) {
+    r.c_out = dmalloc<int64_t>(M, s);
+    r.c_mirror = dmalloc<int64_t>(M, s);
+  }
+  r.sched = sched;
+  r.counter = sched + G + 1;
   k_dense_leaf<true><<<grid_for(npos * 32, CULL_THREADS, 148LL * 64), CULL_THREADS, 0, s>>>(
-      depth, a.norms, b.norms, tau, sym ? 1 : 0, nullptr, off, r.ci, r.cj, r.seg, r.k, a.slot,
-      b.slot, r.a_idx, r.b_idx, M, V, nullptr);
+      depth, a.norms, b.norms, tau, sym ? 1 : 0, nullptr, off, sched, r.ci, r.cj, r.seg, r.k,
+      a.slot, b.slot, r.a_idx, r.b_idx, r.keys, r.c_out, r.c_mirror, r.order, M, V, nullptr);
   SPAMM_LAUNCH_CK();
   dfree(off, s);
   r.n_c = M;
-  r.n_c_full = sym ? 2 * M - h[3] : M;
+  r.n_c_full = F;
   r.n_tasks = V;
   return true;
 }
@@ -431,9 +466,17 @@ void CullResult::release(cudaStream_t s) {
   dfree(k, s);
   dfree(a_idx, s);
   dfree(b_idx, s);
+  dfree(keys, s);
+  dfree(c_out, s);
+  dfree(c_mirror, s);
+  dfree(order, s);
+  dfree(sched, s);
   ci = cj = nullptr;
   seg = nullptr;
   k = a_idx = b_idx = nullptr;
+  keys = c_out = c_mirror = nullptr;
+  order = nullptr;
+  sched = counter = nullptr;
   n_c = n_tasks = 0;
 }
 

@@ -112,6 +112,15 @@ struct CullResult {
   int32_t* b_idx = nullptr;   // n_tasks (storage slot of B_kj)
   std::vector<int64_t> visited, culled;  // full (reference) counts in both modes
   bool sym = false;                      // only C nodes with i <= j were carried
+  // Filled by the dense cull only: the C layout (keys of all n_c_full blocks in
+  // Morton order; per emitted node its storage slot and, symmetric, its mirror
+  // slot or -1) and the K4 schedule (LPT order of the n_c nodes + counter).
+  int64_t* keys = nullptr;
+  int64_t* c_out = nullptr;
+  int64_t* c_mirror = nullptr;
+  int32_t* order = nullptr;
+  int* sched = nullptr;                  // hist/counter scratch (counter inside)
+  int* counter = nullptr;
   void release(cudaStream_t s);
 };
 // Tiered culling (kernel.py:96-122).  want_tasks=false: census only
@@ -135,18 +144,26 @@ enum LeafKernel { LEAF_AUTO = 0, LEAF_DMMA = 1, LEAF_EXACT = 2, LEAF_DMMA_CPASYN
 // For each segment m: C[c_out ? c_out[m] : m] (+)= sum_{t in seg m} A[a_idx[t]] * B[b_idx[t]]
 // and, when c_mirror && c_mirror[m] >= 0, C[c_mirror[m]] = transpose of that block.
 // a_blocks / b_blocks: number of blocks addressable in A / B (TMA bounds).
+// Optional precomputed K4 schedule: segments in longest-first order plus a
+// zeroed work counter (the dense cull builds both); otherwise K4 sorts itself.
+struct LptSchedule {
+  const int32_t* order = nullptr;
+  int* counter = nullptr;
+};
 template <class Idx>
 void leaf_products(int64_t n_seg, const int64_t* seg, const Idx* a_idx, const Idx* b_idx,
                    const int64_t* c_out, const int64_t* c_mirror, bool accumulate,
                    const double* A, int64_t a_blocks, const double* B, int64_t b_blocks,
-                   double* C, int nb, int kernel, cudaStream_t s);
+                   double* C, int nb, int kernel, cudaStream_t s, LptSchedule lpt = {});
 bool dmma_supported(int nb);
+// In-place exclusive scan of a small int histogram (one CTA, nbins <= ~1M).
+void hist_scan_exclusive(int* hist, int nbins, cudaStream_t s);
 bool tma_leaf_supported(int nb);
 template <class Idx>
 void leaf_products_tma(int64_t n_seg, const int64_t* seg, const Idx* a_idx, const Idx* b_idx,
                        const int64_t* c_out, const int64_t* c_mirror, bool accumulate,
                        const double* A, int64_t a_blocks, const double* B, int64_t b_blocks,
-                       double* C, int nb, cudaStream_t s);
+                       double* C, int nb, cudaStream_t s, LptSchedule lpt = {});
 
 // ---- element-wise / reductions ----
 void from_dense(const double* dense, int64_t n, int64_t ld, Mat& m, cudaStream_t s);

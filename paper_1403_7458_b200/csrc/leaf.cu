@@ -247,12 +247,12 @@ template <class Idx>
 void leaf_products(int64_t n_seg, const int64_t* seg, const Idx* a_idx, const Idx* b_idx,
                    const int64_t* c_out, const int64_t* c_mirror, bool accumulate,
                    const double* A, int64_t a_blocks, const double* B, int64_t b_blocks,
-                   double* C, int nb, int kernel, cudaStream_t s) {
+                   double* C, int nb, int kernel, cudaStream_t s, LptSchedule lpt) {
   if (n_seg <= 0) return;
   if (n_seg > 0x7fffffffLL) throw CudaError("too many C blocks for one launch");
   if ((kernel == LEAF_AUTO || kernel == LEAF_DMMA) && tma_leaf_supported(nb)) {
     leaf_products_tma<Idx>(n_seg, seg, a_idx, b_idx, c_out, c_mirror, accumulate, A, a_blocks, B,
-                           b_blocks, C, nb, s);
+                           b_blocks, C, nb, s, lpt);
     return;
   }
   const bool dmma = kernel != LEAF_EXACT && dmma_supported(nb);
@@ -294,9 +294,11 @@ void leaf_products(int64_t n_seg, const int64_t* seg, const Idx* a_idx, const Id
 
 template void leaf_products<int32_t>(int64_t, const int64_t*, const int32_t*, const int32_t*,
                                      const int64_t*, const int64_t*, bool, const double*, int64_t,
-                                     const double*, int64_t, double*, int, int, cudaStream_t);
+                                     const double*, int64_t, double*, int, int, cudaStream_t,
+                                     LptSchedule);
 template void leaf_products<int64_t>(int64_t, const int64_t*, const int64_t*, const int64_t*,
                                      const int64_t*, const int64_t*, bool, const double*, int64_t,
-                                     const double*, int64_t, double*, int, int, cudaStream_t);
+                                     const double*, int64_t, double*, int, int, cudaStream_t,
+                                     LptSchedule);
 
 }  // namespace spamm

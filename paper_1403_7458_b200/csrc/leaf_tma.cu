@@ -345,7 +345,8 @@ int sm_count() {
 template <int NB, int WM, int WN, int ST, int CTAS_PER_SM, class Idx>
 void launch_tma(int64_t n_seg, const int64_t* seg, const Idx* a_idx, const Idx* b_idx,
                 const int64_t* c_out, const int64_t* c_mirror, bool acc, const double* A,
-                int64_t a_blocks, const double* B, int64_t b_blocks, double* C, cudaStream_t s) {
+                int64_t a_blocks, const double* B, int64_t b_blocks, double* C, cudaStream_t s,
+                LptSchedule lpt) {
   using Cfg = TmaCfg<NB, WM, WN, ST>;
   auto kern = k_leaf_dmma_tma<NB, WM, WN, ST, Idx>;
   static std::once_flag once;
@@ -355,19 +356,25 @@ void launch_tma(int64_t n_seg, const int64_t* seg, const Idx* a_idx, const Idx* 
   const CUtensorMap ta = make_map(A, a_blocks, NB), tb = make_map(B, b_blocks, NB);
   int64_t grid = (int64_t)sm_count() * CTAS_PER_SM;
   if (grid > n_seg) grid = n_seg;
-  // scratch: [next-block counter | length histogram (maxlen + 1 bins) | LPT order]
-  const int maxlen = 4096;
-  int* scratch = dmalloc<int>(1 + (maxlen + 1) + n_seg, s);
-  int* counter = scratch;
-  int* hist = scratch + 1;
-  int32_t* order = scratch + 2 + maxlen;
-  SPAMM_CK(cudaMemsetAsync(scratch, 0, (2 + maxlen) * sizeof(int), s));
-  k_len_hist<<<grid_for(n_seg, 256), 256, 0, s>>>(seg, n_seg, maxlen, hist);
-  SPAMM_LAUNCH_CK();
-  k_hist_scan<<<1, 1024, 0, s>>>(hist, maxlen + 1);
-  SPAMM_LAUNCH_CK();
-  k_len_scatter<<<grid_for(n_seg, 256), 256, 0, s>>>(seg, n_seg, maxlen, hist, order);
-  SPAMM_LAUNCH_CK();
+  int* scratch = nullptr;
+  const int32_t* order = lpt.order;
+  int* counter = lpt.counter;
+  if (!order) {
+    // scratch: [next-block counter | length histogram (maxlen + 1 bins) | LPT order]
+    const int maxlen = 4096;
+    scratch = dmalloc<int>(1 + (maxlen + 1) + n_seg, s);
+    counter = scratch;
+    int* hist = scratch + 1;
+    int32_t* ord = scratch + 2 + maxlen;
+    SPAMM_CK(cudaMemsetAsync(scratch, 0, (2 + maxlen) * sizeof(int), s));
+    k_len_hist<<<grid_for(n_seg, 256), 256, 0, s>>>(seg, n_seg, maxlen, hist);
+    SPAMM_LAUNCH_CK();
+    k_hist_scan<<<1, 1024, 0, s>>>(hist, maxlen + 1);
+    SPAMM_LAUNCH_CK();
+    k_len_scatter<<<grid_for(n_seg, 256), 256, 0, s>>>(seg, n_seg, maxlen, hist, ord);
+    SPAMM_LAUNCH_CK();
+    order = ord;
+  }
   kern<<<(unsigned)grid, Cfg::THREADS, Cfg::SMEM, s>>>(ta, tb, n_seg, seg, a_idx, b_idx, c_out,
                                                        c_mirror, acc ? 1 : 0, C, order, counter);
   SPAMM_LAUNCH_CK();
@@ -382,25 +389,30 @@ template <class Idx>
 void leaf_products_tma(int64_t n_seg, const int64_t* seg, const Idx* a_idx, const Idx* b_idx,
                        const int64_t* c_out, const int64_t* c_mirror, bool accumulate,
                        const double* A, int64_t a_blocks, const double* B, int64_t b_blocks,
-                       double* C, int nb, cudaStream_t s) {
+                       double* C, int nb, cudaStream_t s, LptSchedule lpt) {
   if (n_seg <= 0) return;
   if (nb == 64)
     launch_tma<64, 2, 4, 3, 1, Idx>(n_seg, seg, a_idx, b_idx, c_out, c_mirror, accumulate, A,
-                                    a_blocks, B, b_blocks, C, s);
+                                    a_blocks, B, b_blocks, C, s, lpt);
   else if (nb == 32)
     launch_tma<32, 2, 2, 6, 2, Idx>(n_seg, seg, a_idx, b_idx, c_out, c_mirror, accumulate, A,
-                                    a_blocks, B, b_blocks, C, s);
+                                    a_blocks, B, b_blocks, C, s, lpt);
   else
     throw CudaError("TMA leaf kernel needs block size 32 or 64");
+}
+
+void hist_scan_exclusive(int* hist, int nbins, cudaStream_t s) {
+  k_hist_scan<<<1, 1024, 0, s>>>(hist, nbins);
+  SPAMM_LAUNCH_CK();
 }
 
 template void leaf_products_tma<int32_t>(int64_t, const int64_t*, const int32_t*, const int32_t*,
                                          const int64_t*, const int64_t*, bool, const double*,
                                          int64_t, const double*, int64_t, double*, int,
-                                         cudaStream_t);
+                                         cudaStream_t, LptSchedule);
 template void leaf_products_tma<int64_t>(int64_t, const int64_t*, const int64_t*, const int64_t*,
                                          const int64_t*, const int64_t*, bool, const double*,
                                          int64_t, const double*, int64_t, double*, int,
-                                         cudaStream_t);
+                                         cudaStream_t, LptSchedule);
 
 }  // namespace spamm
