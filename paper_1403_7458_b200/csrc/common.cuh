@@ -73,4 +73,84 @@ inline int grid_for(int64_t n, int threads, int64_t cap = 148LL * 64) {
   return (int)g;
 }
 
+// One einsum lane's unfused add chain over a 256-element chunk of squares in
+// shared memory (p = chunk base + lane parity): per 8-element group the
+// order (6,4,2,0), groups ascending (numpy's einsum lanes, see norms.cu).
+// Loads are batched 32 at a time ahead of the dependent adds so the chain
+// runs at add latency instead of shared-load latency.
+__device__ __forceinline__ double einsum_lane_chain256(const double* p, double l) {
+#pragma unroll
+  for (int g0 = 0; g0 < 32; g0 += 8) {
+    double v[32];
+#pragma unroll
+    for (int g = 0; g < 8; ++g) {
+      v[4 * g + 0] = p[(g0 + g) * 8 + 6];
+      v[4 * g + 1] = p[(g0 + g) * 8 + 4];
+      v[4 * g + 2] = p[(g0 + g) * 8 + 2];
+      v[4 * g + 3] = p[(g0 + g) * 8 + 0];
+    }
+#pragma unroll
+    for (int q = 0; q < 32; ++q) l = __dadd_rn(l, v[q]);
+  }
+  return l;
+}
+
+// Multi-block chain layout: a 256-element chunk of squares is stored as two
+// parity rows (even / odd elements) permuted so each einsum lane's chain
+// reads its row sequentially: element e -> row (e & 1), position
+// 4 (e >> 3) + 3 - ((e & 7) >> 1).  Rows are CHAIN_ROW doubles apart (16 B
+// bank skew), so 8 chains of different blocks load with one conflict-free
+// LDS.128 wavefront.  chain_pos(k, lane) is the position of the pair lane
+// holds at k (elements k*64 + 2 lane + {0, 1}).
+constexpr int CHAIN_ROW = 130;
+__device__ __forceinline__ int chain_pos(int k, int lane) {
+  return 4 * (k * 8 + (lane >> 2)) + 3 - (lane & 3);
+}
+__device__ __forceinline__ double chain_row128(const double* row, double l) {
+  const double2* r2 = reinterpret_cast<const double2*>(row);
+#pragma unroll
+  for (int b = 0; b < 4; ++b) {
+    double2 v[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = r2[b * 16 + i];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      l = __dadd_rn(l, v[i].x);
+      l = __dadd_rn(l, v[i].y);
+    }
+  }
+  return l;
+}
+
+// Exclusive scan of one int64 per thread across the CTA (blockDim.x a
+// multiple of 32, <= 1024); *total receives the sum.  Every thread of the
+// CTA must call it (it synchronises).
+__device__ __forceinline__ int64_t cta_exclusive_scan(int64_t v, int64_t* total) {
+  __shared__ int64_t warp_sums[33];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  int64_t inc = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int64_t y = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += y;
+  }
+  __syncthreads();  // a previous call may still be reading warp_sums
+  if (lane == 31) warp_sums[warp] = inc;
+  __syncthreads();
+  if (warp == 0) {
+    const int64_t w = lane < nwarps ? warp_sums[lane] : 0;
+    int64_t wi = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t y = __shfl_up_sync(0xffffffffu, wi, o);
+      if (lane >= o) wi += y;
+    }
+    warp_sums[lane] = wi - w;
+    if (lane == 31) warp_sums[32] = wi;
+  }
+  __syncthreads();
+  *total = warp_sums[32];
+  return warp_sums[warp] + inc - v;
+}
+
 }  // namespace spamm

@@ -262,24 +262,36 @@ __device__ __forceinline__ bool keep_chain(const double* __restrict__ nA,
 }
 
 // Survivor counts of every tier t < depth (full enumeration, 8^t triples).
+// Counts are warp-reduced per tier before touching shared memory (a shared
+// 64-bit atomic per survivor serialised this kernel to ~15 us at cfg4).
 __global__ void __launch_bounds__(256)
     k_dense_tiers(const double* __restrict__ nA, const double* __restrict__ nB, double tau,
                   int depth, unsigned long long* __restrict__ counts) {
-  __shared__ unsigned long long sc[DENSE_MAX_DEPTH];
+  __shared__ unsigned int sc[DENSE_MAX_DEPTH];
   if (threadIdx.x < DENSE_MAX_DEPTH) sc[threadIdx.x] = 0;
   __syncthreads();
+  const int lane = threadIdx.x & 31;
   const int64_t total = ((int64_t(1) << (3 * depth)) - 1) / 7;
-  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < total;
-       q += (int64_t)gridDim.x * blockDim.x) {
-    int t = 0;
-    while ((((int64_t(1) << (3 * (t + 1))) - 1) / 7) <= q) ++t;
-    const int64_t r = q - ((int64_t(1) << (3 * t)) - 1) / 7;
-    const int64_t i = r >> (2 * t), k = (r >> t) & ((int64_t(1) << t) - 1),
-                  j = r & ((int64_t(1) << t) - 1);
-    if (keep_chain(nA, nB, tau, t, i, k, j)) atomicAdd(sc + t, 1ull);
+  // warp-uniform trip count so the per-tier reductions see full warps
+  for (int64_t q0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) & ~int64_t(31); q0 < total;
+       q0 += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t q = q0 + lane;
+    int t = -1;
+    if (q < total) {
+      t = 0;
+      while ((((int64_t(1) << (3 * (t + 1))) - 1) / 7) <= q) ++t;
+      const int64_t r = q - ((int64_t(1) << (3 * t)) - 1) / 7;
+      const int64_t i = r >> (2 * t), k = (r >> t) & ((int64_t(1) << t) - 1),
+                    j = r & ((int64_t(1) << t) - 1);
+      if (!keep_chain(nA, nB, tau, t, i, k, j)) t = -1;
+    }
+    for (int u = 0; u < depth; ++u) {
+      const unsigned v = __reduce_add_sync(0xffffffffu, t == u ? 1u : 0u);
+      if (lane == 0 && v) atomicAdd(sc + u, v);
+    }
   }
   __syncthreads();
-  if (threadIdx.x < depth && sc[threadIdx.x]) atomicAdd(counts + threadIdx.x, sc[threadIdx.x]);
+  if (threadIdx.x < depth && sc[threadIdx.x]) atomicAdd(counts + threadIdx.x, (unsigned long long)sc[threadIdx.x]);
 }
 
 // Leaf tier, one warp per C position m (Morton order).  Each m gets one
@@ -311,6 +323,7 @@ __global__ void __launch_bounds__(CULL_THREADS)
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   if (WRITE && gw == 0 && lane == 0) seg_o[Mn] = Vn;
+  unsigned long long full = 0;
   for (int64_t m = gw; m < G * G; m += nw) {
     uint32_t ui, uj;
     morton_decode((uint64_t)m, ui, uj);
@@ -363,11 +376,17 @@ __global__ void __launch_bounds__(CULL_THREADS)
     if (!WRITE && lane == 0) {
       cnt[m] = (emitted ? c + (c > 0 ? int64_t(1) << DT_NODE : 0) : 0) +
                (c > 0 ? int64_t(1) << DT_FULL : 0);
-      if (c) {
-        atomicAdd(aux, (unsigned long long)c);  // full (reference) leaf count
-        if (emitted) atomicAdd(hist + (G - c), 1);
-      }
+      full += c;
+      if (c && emitted) atomicAdd(hist + (G - c), 1);
     }
+  }
+  if (!WRITE) {  // full (reference) leaf count: one global atomic per CTA
+    __shared__ unsigned long long cta_full;
+    if (threadIdx.x == 0) cta_full = 0;
+    __syncthreads();
+    if (lane == 0 && full) atomicAdd(&cta_full, full);
+    __syncthreads();
+    if (threadIdx.x == 0 && cta_full) atomicAdd(aux, cta_full);
   }
 }
 

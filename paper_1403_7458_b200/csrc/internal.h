@@ -39,6 +39,7 @@ struct Mat {
   bool sym = false;          // X == X^T bitwise (blocks and null structure)
   mutable double tr = 0.0;   // cached trace (matrices are immutable)
   mutable bool tr_valid = false;
+  double* tr_dev = nullptr;  // trace written on the device by finalize (small trees)
   // Pinned host mirror of norm tiers 0..top_t (written by finalize, ready when
   // top_ev completes): the cull expands those tiers on the host.
   double* host_top = nullptr;
@@ -50,6 +51,7 @@ struct Mat {
   cudaStream_t stream = nullptr;
   void release();
 };
+constexpr int SMALL_TREE_DEPTH = 6;  // G*G <= 4096: single-CTA finalisation
 constexpr int HOST_TOP_TIERS = 5;  // tiers 0..5: 1,365 norms (11 KB)
 
 // Exact-symmetry test (block (i,j) == transpose of block (j,i), bitwise).
@@ -80,6 +82,7 @@ struct UnionPrep {
   uint8_t* flags = nullptr;
   int64_t* off = nullptr;
   int64_t npos = 0;
+  int64_t* keys = nullptr;  // small trees: union keys already compacted (G*G capacity)
 };
 UnionPrep sp2_union_prepare(const Mat& x, const Mat& x2, int64_t* u_dev, cudaStream_t s);
 void sp2_update_finish(const Mat& x, const Mat& x2, UnionPrep& prep, int64_t U, bool want_idem,

@@ -125,6 +125,8 @@ void top_release(double* buf, cudaEvent_t ev) {
 }  // namespace
 
 void Mat::release() {
+  dfree(tr_dev, stream);
+  tr_dev = nullptr;
   dfree(pend_nz, stream);
   dfree(pend_off, stream);
   pend_nz = nullptr;
@@ -244,6 +246,96 @@ __global__ void k_tiers_small(double* __restrict__ norms2, double* __restrict__ 
   }
 }
 
+// Single-CTA finalisation for small trees (G*G <= 4096): the kept-block
+// scan, slot map, leaf tier, upper tiers (same sums as k_tier_up /
+// k_tiers_small), the trace (same order as k_trace_blocks + k_trace, Nb >= 2)
+// and the pinned host mirror of the top tiers, in one launch instead of ~9.
+// Any of off / slot / tr_out / host_top may be null.
+__global__ void __launch_bounds__(1024)
+    k_finalize_small(const int64_t* __restrict__ keys, const double* __restrict__ n2,
+                     const uint8_t* __restrict__ nz, int64_t nblocks, int depth,
+                     int64_t* __restrict__ off, int32_t* __restrict__ slot,
+                     double* __restrict__ norms, double* __restrict__ norms2,
+                     const double* __restrict__ data, int nb, double* __restrict__ tr_out,
+                     double* host_top, int top_t) {
+  const int64_t G = int64_t(1) << depth, npos = G * G;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  if (off) {
+    const int64_t per = (nblocks + nt - 1) / nt, b0 = tid * per;
+    int64_t loc = 0;
+    for (int64_t b = b0; b < b0 + per && b < nblocks; ++b) loc += nz[b];
+    int64_t tot = 0;
+    int64_t ex = cta_exclusive_scan(loc, &tot);
+    for (int64_t b = b0; b < b0 + per && b < nblocks; ++b) {
+      off[b] = ex;
+      ex += nz[b];
+    }
+    if (tid == 0) off[nblocks] = tot;
+  }
+  double* leaf2 = norms2 + tier_offset(depth);
+  double* leafn = norms + tier_offset(depth);
+  for (int64_t p = tid; p < npos; p += nt) {
+    if (slot) slot[p] = -1;
+    leaf2[p] = 0.0;
+    leafn[p] = 0.0;
+  }
+  __syncthreads();
+  for (int64_t b = tid; b < nblocks; b += nt) {
+    const int64_t k = keys[b];
+    if (slot) slot[k] = (int32_t)b;
+    const double v = n2[b];
+    leaf2[k] = v;
+    leafn[k] = __dsqrt_rn(v);
+  }
+  __syncthreads();
+  for (int t = depth - 1; t >= 0; --t) {
+    const int64_t w = int64_t(1) << t, W = 2 * w, n = w * w;
+    const double* c2 = norms2 + tier_offset(t + 1);
+    double* p2 = norms2 + tier_offset(t);
+    double* pn = norms + tier_offset(t);
+    for (int64_t idx = tid; idx < n; idx += nt) {
+      const int64_t i = idx / w, j = idx % w;
+      const double* r0 = c2 + (2 * i) * W + 2 * j;
+      const double* r1 = r0 + W;
+      const double sm = t == 0 ? __dadd_rn(__dadd_rn(__dadd_rn(r0[0], r0[1]), r1[0]), r1[1])
+                               : __dadd_rn(__dadd_rn(r0[0], r0[1]), __dadd_rn(r1[0], r1[1]));
+      p2[idx] = sm;
+      pn[idx] = __dsqrt_rn(sm);
+    }
+    __syncthreads();
+  }
+  if (tr_out && slot) {
+    __shared__ double part[64];
+    __shared__ int present[64];
+    const int warp = tid >> 5, lane = tid & 31;
+    const int64_t nb2 = (int64_t)nb * nb;
+    for (int64_t b = warp; b < G; b += nt >> 5) {
+      const int32_t sl = slot[b * G + b];
+      if (lane == 0) present[b] = sl >= 0;
+      if (sl < 0) continue;
+      const double* x = data + (int64_t)sl * nb2;
+      double acc = 0.0;
+      for (int d0 = 0; d0 < nb; d0 += 32) {
+        const int d = d0 + lane;
+        const double v = d < nb ? x[(int64_t)d * nb + d] : 0.0;
+        const int cnt = min(32, nb - d0);
+        for (int i = 0; i < cnt; ++i) acc = __dadd_rn(acc, __shfl_sync(0xffffffffu, v, i));
+      }
+      if (lane == 0) part[b] = acc;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      double tot = 0.0;
+      for (int64_t b = 0; b < G; ++b)
+        if (present[b]) tot = __dadd_rn(tot, part[b]);
+      *tr_out = tot;
+    }
+  }
+  if (host_top) {
+    for (int64_t i = tid; i < tier_offset(top_t + 1); i += nt) host_top[i] = norms[i];
+  }
+}
+
 // Gather the kept blocks (nz[b] = 1) to their compacted positions.
 __global__ void k_compact_blocks(const double* __restrict__ din, const int64_t* __restrict__ kin,
                                  const double* __restrict__ nin, const uint8_t* __restrict__ nz,
@@ -268,6 +360,65 @@ __global__ void k_scatter_slots(const int64_t* __restrict__ keys, int64_t m, int
 }
 
 }  // namespace
+
+// Multi-block variant (the production path for Nb = 32 / 64): each warp
+// reduces BPW blocks at once, chains of all of them on lanes 0 .. 2 BPW - 1
+// reading the permuted parity rows (common.cuh) with LDS.128.  Same recipe and
+// bits as k_leaf_norms2; the single-block warp kernel below was bound by
+// shared-load wavefronts (one 16-byte LDS per wavefront).
+template <int NB2, int BPW, int WARPS>
+__global__ void __launch_bounds__(32 * WARPS)
+    k_leaf_norms2_multi(const double* __restrict__ data, int64_t m, double* __restrict__ out,
+                        uint8_t* __restrict__ nz) {
+  constexpr int NCH = NB2 / 256;
+  __shared__ __align__(16) double rows_all[WARPS][BPW * 2 * CHAIN_ROW];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* rows = rows_all[warp];
+  const int64_t stride = (int64_t)gridDim.x * WARPS * BPW;
+  for (int64_t b0 = ((int64_t)blockIdx.x * WARPS + warp) * BPW; b0 < m; b0 += stride) {
+    const double2* x[BPW];
+    double2 r[BPW][4];
+#pragma unroll
+    for (int q = 0; q < BPW; ++q) {
+      x[q] = b0 + q < m ? reinterpret_cast<const double2*>(data + (b0 + q) * NB2) : nullptr;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) r[q][k] = x[q] ? __ldg(x[q] + k * 32 + lane) : make_double2(0.0, 0.0);
+    }
+    double acc = 0.0;
+    unsigned anyq = 0;
+    for (int c = 0; c < NCH; ++c) {
+      __syncwarp();
+#pragma unroll
+      for (int q = 0; q < BPW; ++q)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          double* rq = rows + q * 2 * CHAIN_ROW + chain_pos(k, lane);
+          rq[0] = __dmul_rn(r[q][k].x, r[q][k].x);
+          rq[CHAIN_ROW] = __dmul_rn(r[q][k].y, r[q][k].y);
+          if ((r[q][k].x != 0.0) | (r[q][k].y != 0.0)) anyq |= 1u << q;
+        }
+      __syncwarp();
+      if (c + 1 < NCH) {
+#pragma unroll
+        for (int q = 0; q < BPW; ++q)
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            if (x[q]) r[q][k] = __ldg(x[q] + (c + 1) * 128 + k * 32 + lane);
+      }
+      if (lane < 2 * BPW) acc = chain_row128(rows + lane * CHAIN_ROW, acc);
+    }
+#pragma unroll
+    for (int q = 0; q < BPW; ++q) {
+      const double l0 = __shfl_sync(0xffffffffu, acc, 2 * q);
+      const double l1 = __shfl_sync(0xffffffffu, acc, 2 * q + 1);
+      const bool any = __any_sync(0xffffffffu, (anyq >> q) & 1u);
+      if (lane == 0 && b0 + q < m) {
+        out[b0 + q] = __dadd_rn(l0, l1);
+        if (nz) nz[b0 + q] = any ? 1 : 0;
+      }
+    }
+  }
+}
 
 // Warp-per-block variant for Nb^2 a multiple of 256: the warp streams the block
 // through shared memory in 256-element chunks with fully coalesced loads
@@ -305,18 +456,7 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
         for (int k = 0; k < 4; ++k) r[k] = __ldg(x + (c + 1) * (CH / 2) + k * 32 + lane);
       }
-      if (lane < 2) {
-        const double* p = buf + lane;
-        double l = acc;
-#pragma unroll 8
-        for (int g = 0; g < CH / 8; ++g) {
-          l = __dadd_rn(l, p[g * 8 + 6]);
-          l = __dadd_rn(l, p[g * 8 + 4]);
-          l = __dadd_rn(l, p[g * 8 + 2]);
-          l = __dadd_rn(l, p[g * 8 + 0]);
-        }
-        acc = l;
-      }
+      if (lane < 2) acc = einsum_lane_chain256(buf + lane, acc);
     }
     const double l1 = __shfl_sync(0xffffffffu, acc, 1);
     any = __any_sync(0xffffffffu, any);
@@ -332,11 +472,12 @@ void leaf_norms2(const double* data, int64_t m, int nb, double* norms2, uint8_t*
   if (m <= 0) return;
   const int nb2 = nb * nb;
   if (nb2 == 1024 || nb2 == 4096) {
-    const int grid = grid_for(m * 32, 256, 1LL << 20);
+    constexpr int BPW = 2, WARPS = 4;
+    const int grid = grid_for((m + BPW - 1) / BPW * 32, 32 * WARPS, 1LL << 20);
     if (nb2 == 1024)
-      k_leaf_norms2_warp<1024><<<grid, 256, 0, s>>>(data, m, norms2, nonzero);
+      k_leaf_norms2_multi<1024, BPW, WARPS><<<grid, 32 * WARPS, 0, s>>>(data, m, norms2, nonzero);
     else
-      k_leaf_norms2_warp<4096><<<grid, 256, 0, s>>>(data, m, norms2, nonzero);
+      k_leaf_norms2_multi<4096, BPW, WARPS><<<grid, 32 * WARPS, 0, s>>>(data, m, norms2, nonzero);
   } else {
     const int threads = 128;
     k_leaf_norms2<0><<<grid_for(m, threads, 1LL << 20), threads, 0, s>>>(data, m, nb2, norms2,
@@ -347,6 +488,12 @@ void leaf_norms2(const double* data, int64_t m, int nb, double* norms2, uint8_t*
 
 void build_pyramid(const int64_t* keys, const double* blk_norms2, int64_t m, int depth,
                    double* norms, double* norms2, cudaStream_t s) {
+  if (depth <= SMALL_TREE_DEPTH) {
+    k_finalize_small<<<1, 1024, 0, s>>>(keys, blk_norms2, nullptr, m, depth, nullptr, nullptr,
+                                        norms, norms2, nullptr, 0, nullptr, nullptr, 0);
+    SPAMM_LAUNCH_CK();
+    return;
+  }
   const int64_t G = int64_t(1) << depth;
   double* leaf2 = norms2 + tier_offset(depth);
   double* leafn = norms + tier_offset(depth);
@@ -379,6 +526,40 @@ void finalize(Mat& m, cudaStream_t s, double* pre_n2, uint8_t* pre_nz, bool defe
   m.stream = s;
   const int nb2 = m.nb * m.nb;
   double* n2 = pre_n2;
+  if (defer && m.depth <= SMALL_TREE_DEPTH) {
+    // one launch (after K1 unless the producer already computed the norms)
+    uint8_t* nz = pre_nz;
+    if (m.nblocks > 0 && !n2) {
+      n2 = dmalloc<double>(m.nblocks, s);
+      nz = dmalloc<uint8_t>(m.nblocks, s);
+      leaf_norms2(m.data, m.nblocks, m.nb, n2, nz, s);
+    }
+    m.G = int64_t(1) << m.depth;
+    m.slot = dmalloc<int32_t>(m.G * m.G, s);
+    const int64_t ps = pyramid_size(m.depth);
+    m.norms = dmalloc<double>(ps, s);
+    m.norms2 = dmalloc<double>(ps, s);
+    int64_t* off = m.nblocks > 0 ? dmalloc<int64_t>(m.nblocks + 1, s) : nullptr;
+    const bool want_tr = m.nb >= 2;
+    if (want_tr) m.tr_dev = dmalloc<double>(1, s);
+    if (m.depth >= 2 && !m.host_top) {
+      m.top_t = std::min(m.depth - 1, HOST_TOP_TIERS);
+      top_acquire(&m.host_top, &m.top_ev);
+    }
+    k_finalize_small<<<1, 1024, 0, s>>>(m.keys, n2, nz, m.nblocks, m.depth, off, m.slot, m.norms,
+                                        m.norms2, m.data, m.nb, m.tr_dev,
+                                        m.host_top, m.host_top ? m.top_t : -1);
+    SPAMM_LAUNCH_CK();
+    if (m.host_top) SPAMM_CK(cudaEventRecord(m.top_ev, s));
+    dfree(n2, s);
+    if (m.nblocks > 0) {
+      m.pend_nz = nz;
+      m.pend_off = off;
+    } else {
+      dfree(nz, s);
+    }
+    return;
+  }
   if (m.nblocks > 0) {
     uint8_t* nz = pre_nz;
     if (!n2) {

@@ -468,6 +468,10 @@ void add_scaled(double alpha, const Mat& a, double beta, const Mat& b, Mat& out,
 }
 
 void trace_launch(const Mat& m, double* dev_out, cudaStream_t s) {
+  if (m.tr_dev) {  // computed by the single-CTA finalisation
+    SPAMM_CK(cudaMemcpyAsync(dev_out, m.tr_dev, sizeof(double), cudaMemcpyDeviceToDevice, s));
+    return;
+  }
   double* partial = dmalloc<double>(m.G, s);
   uint8_t* present = dmalloc<uint8_t>(m.G, s);
   k_trace_blocks<<<grid_for(m.G * 32, 256), 256, 0, s>>>(m.slot, m.data, m.G, m.nb, partial,

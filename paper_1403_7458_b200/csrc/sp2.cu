@@ -42,6 +42,30 @@ __global__ void k_union_compact(const uint8_t* __restrict__ flags, const int64_t
   }
 }
 
+// Small trees (G*G <= 4096): union flags, scan and compaction in one CTA.
+__global__ void __launch_bounds__(1024)
+    k_union_small(const int32_t* __restrict__ sa, const int32_t* __restrict__ sb, int depth,
+                  int64_t* __restrict__ keys, int64_t* __restrict__ count) {
+  const int64_t G = int64_t(1) << depth, npos = G * G;
+  const int64_t per = (npos + blockDim.x - 1) / blockDim.x, p0 = threadIdx.x * per;
+  int64_t loc = 0;
+  for (int64_t p = p0; p < p0 + per && p < npos; ++p) {
+    uint32_t bi, bj;
+    morton_decode((uint64_t)p, bi, bj);
+    const int64_t key = (int64_t)bi * G + bj;
+    loc += (sa[key] >= 0 || sb[key] >= 0) ? 1 : 0;
+  }
+  int64_t tot = 0;
+  int64_t o = cta_exclusive_scan(loc, &tot);
+  for (int64_t p = p0; p < p0 + per && p < npos; ++p) {
+    uint32_t bi, bj;
+    morton_decode((uint64_t)p, bi, bj);
+    const int64_t key = (int64_t)bi * G + bj;
+    if (sa[key] >= 0 || sb[key] >= 0) keys[o++] = key;
+  }
+  if (threadIdx.x == 0) *count = tot;
+}
+
 template <int NB2, bool IDEM, bool EXPAND>
 __global__ void __launch_bounds__(256)
     k_sp2_update(const int64_t* __restrict__ ukeys, int64_t U, const double* __restrict__ X,
@@ -100,16 +124,7 @@ __global__ void __launch_bounds__(256)
       }
       __syncwarp();
       if ((IDEM && lane < 2) || (EXPAND && lane >= 2 && lane < 4)) {
-        const double* p = (lane < 2 ? bd : be) + (lane & 1);
-        double l = acc;
-#pragma unroll 8
-        for (int g = 0; g < CH / 8; ++g) {
-          l = __dadd_rn(l, p[g * 8 + 6]);
-          l = __dadd_rn(l, p[g * 8 + 4]);
-          l = __dadd_rn(l, p[g * 8 + 2]);
-          l = __dadd_rn(l, p[g * 8 + 0]);
-        }
-        acc = l;
+        acc = einsum_lane_chain256((lane < 2 ? bd : be) + (lane & 1), acc);
       }
     }
     const double l1 = __shfl_sync(0xffffffffu, acc, 1);
@@ -126,20 +141,126 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// Multi-block K6 (production path): BPW union blocks per warp, the D and E
+// chains of all of them on lanes 0 .. 4 BPW - 1 (lane = 4 q + 2 set + parity)
+// over the permuted parity rows (common.cuh).  Same arithmetic and bits as
+// k_sp2_update.
+template <int NB2, bool IDEM, bool EXPAND, int BPW, int WARPS>
+__global__ void __launch_bounds__(32 * WARPS)
+    k_sp2_update_multi(const int64_t* __restrict__ ukeys, int64_t U, const double* __restrict__ X,
+                       const int32_t* __restrict__ sx, const double* __restrict__ X2,
+                       const int32_t* __restrict__ sx2, double* __restrict__ E,
+                       double* __restrict__ nD2, double* __restrict__ nE2,
+                       uint8_t* __restrict__ nzE) {
+  constexpr int NCH = NB2 / 256;
+  __shared__ __align__(16) double rows_all[WARPS][BPW * 4 * CHAIN_ROW];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* rows = rows_all[warp];
+  const int64_t stride = (int64_t)gridDim.x * WARPS * BPW;
+  for (int64_t u0 = ((int64_t)blockIdx.x * WARPS + warp) * BPW; u0 < U; u0 += stride) {
+    const double2* px[BPW];
+    const double2* px2[BPW];
+    double2* pe[BPW];
+    double2 a[BPW][4], b[BPW][4];
+#pragma unroll
+    for (int q = 0; q < BPW; ++q) {
+      px[q] = px2[q] = nullptr;
+      pe[q] = nullptr;
+      if (u0 + q < U) {
+        const int64_t key = ukeys[u0 + q];
+        const int32_t ix = sx[key], ix2 = sx2[key];
+        if (ix >= 0) px[q] = reinterpret_cast<const double2*>(X + (int64_t)ix * NB2);
+        if (ix2 >= 0) px2[q] = reinterpret_cast<const double2*>(X2 + (int64_t)ix2 * NB2);
+        if (EXPAND) pe[q] = reinterpret_cast<double2*>(E + (u0 + q) * NB2);
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        a[q][k] = px[q] ? __ldg(px[q] + k * 32 + lane) : make_double2(0.0, 0.0);
+        b[q][k] = px2[q] ? __ldg(px2[q] + k * 32 + lane) : make_double2(0.0, 0.0);
+      }
+    }
+    double acc = 0.0;
+    unsigned anyq = 0;
+    for (int c = 0; c < NCH; ++c) {
+      __syncwarp();
+#pragma unroll
+      for (int q = 0; q < BPW; ++q)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          double d0, d1, e0, e1;
+          // D = add_scaled(1.0, X2, -1.0, X): first operand X2, second X
+          d0 = px2[q] ? __dmul_rn(1.0, b[q][k].x) : 0.0;
+          d1 = px2[q] ? __dmul_rn(1.0, b[q][k].y) : 0.0;
+          if (px[q]) {
+            d0 = __dadd_rn(d0, __dmul_rn(-1.0, a[q][k].x));
+            d1 = __dadd_rn(d1, __dmul_rn(-1.0, a[q][k].y));
+          }
+          // E = add_scaled(2.0, X, -1.0, X2): first operand X, second X2
+          e0 = px[q] ? __dmul_rn(2.0, a[q][k].x) : 0.0;
+          e1 = px[q] ? __dmul_rn(2.0, a[q][k].y) : 0.0;
+          if (px2[q]) {
+            e0 = __dadd_rn(e0, __dmul_rn(-1.0, b[q][k].x));
+            e1 = __dadd_rn(e1, __dmul_rn(-1.0, b[q][k].y));
+          }
+          double* rq = rows + q * 4 * CHAIN_ROW + chain_pos(k, lane);
+          if (IDEM) {
+            rq[0] = __dmul_rn(d0, d0);
+            rq[CHAIN_ROW] = __dmul_rn(d1, d1);
+          }
+          if (EXPAND) {
+            rq[2 * CHAIN_ROW] = __dmul_rn(e0, e0);
+            rq[3 * CHAIN_ROW] = __dmul_rn(e1, e1);
+            if (pe[q]) pe[q][c * 128 + k * 32 + lane] = make_double2(e0, e1);
+            if ((e0 != 0.0) | (e1 != 0.0)) anyq |= 1u << q;
+          }
+        }
+      __syncwarp();
+      if (c + 1 < NCH) {
+#pragma unroll
+        for (int q = 0; q < BPW; ++q)
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            if (px[q]) a[q][k] = __ldg(px[q] + (c + 1) * 128 + k * 32 + lane);
+            if (px2[q]) b[q][k] = __ldg(px2[q] + (c + 1) * 128 + k * 32 + lane);
+          }
+      }
+      const int set = (lane >> 1) & 1;
+      if (lane < 4 * BPW && (set ? EXPAND : IDEM))
+        acc = chain_row128(rows + lane * CHAIN_ROW, acc);
+    }
+#pragma unroll
+    for (int q = 0; q < BPW; ++q) {
+      const double d0 = __shfl_sync(0xffffffffu, acc, 4 * q);
+      const double d1 = __shfl_sync(0xffffffffu, acc, 4 * q + 1);
+      const double e0 = __shfl_sync(0xffffffffu, acc, 4 * q + 2);
+      const double e1 = __shfl_sync(0xffffffffu, acc, 4 * q + 3);
+      const bool any = __any_sync(0xffffffffu, (anyq >> q) & 1u);
+      if (lane == 0 && u0 + q < U) {
+        if (IDEM) nD2[u0 + q] = __dadd_rn(d0, d1);
+        if (EXPAND) {
+          nE2[u0 + q] = __dadd_rn(e0, e1);
+          nzE[u0 + q] = any ? 1 : 0;
+        }
+      }
+    }
+  }
+}
+
 template <int NB2>
 void launch_update(bool idem, bool expand, const int64_t* ukeys, int64_t U, const Mat& x,
                    const Mat& x2, double* E, double* nD2, double* nE2, uint8_t* nzE,
                    cudaStream_t s) {
-  const int grid = grid_for(U * 32, 256, 1LL << 20);
+  constexpr int BPW = 2, WARPS = 4;
+  const int grid = grid_for((U + BPW - 1) / BPW * 32, 32 * WARPS, 1LL << 20);
   if (idem && expand)
-    k_sp2_update<NB2, true, true><<<grid, 256, 0, s>>>(ukeys, U, x.data, x.slot, x2.data, x2.slot,
-                                                       E, nD2, nE2, nzE);
+    k_sp2_update_multi<NB2, true, true, BPW, WARPS><<<grid, 32 * WARPS, 0, s>>>(
+        ukeys, U, x.data, x.slot, x2.data, x2.slot, E, nD2, nE2, nzE);
   else if (idem)
-    k_sp2_update<NB2, true, false><<<grid, 256, 0, s>>>(ukeys, U, x.data, x.slot, x2.data,
-                                                        x2.slot, E, nD2, nE2, nzE);
+    k_sp2_update_multi<NB2, true, false, BPW, WARPS><<<grid, 32 * WARPS, 0, s>>>(
+        ukeys, U, x.data, x.slot, x2.data, x2.slot, E, nD2, nE2, nzE);
   else
-    k_sp2_update<NB2, false, true><<<grid, 256, 0, s>>>(ukeys, U, x.data, x.slot, x2.data,
-                                                        x2.slot, E, nD2, nE2, nzE);
+    k_sp2_update_multi<NB2, false, true, BPW, WARPS><<<grid, 32 * WARPS, 0, s>>>(
+        ukeys, U, x.data, x.slot, x2.data, x2.slot, E, nD2, nE2, nzE);
   SPAMM_LAUNCH_CK();
 }
 
@@ -175,6 +296,12 @@ bool sp2_fused_supported(int nb) { return nb == 32 || nb == 64; }
 UnionPrep sp2_union_prepare(const Mat& x, const Mat& x2, int64_t* u_dev, cudaStream_t s) {
   UnionPrep p;
   p.npos = x.G * x.G;
+  if (x.depth <= SMALL_TREE_DEPTH) {
+    p.keys = dmalloc<int64_t>(p.npos, s);
+    k_union_small<<<1, 1024, 0, s>>>(x.slot, x2.slot, x.depth, p.keys, u_dev);
+    SPAMM_LAUNCH_CK();
+    return p;
+  }
   p.flags = dmalloc<uint8_t>(p.npos, s);
   p.off = dmalloc<int64_t>(p.npos + 1, s);
   k_union_keys<<<grid_for(p.npos, 256), 256, 0, s>>>(x.slot, x2.slot, x.depth, p.flags);
@@ -187,8 +314,10 @@ UnionPrep sp2_union_prepare(const Mat& x, const Mat& x2, int64_t* u_dev, cudaStr
 void sp2_update_finish(const Mat& x, const Mat& x2, UnionPrep& prep, int64_t U, bool want_idem,
                        bool expand, double* idem_norm, Mat& e, cudaStream_t s) {
   const int nb2 = x.nb * x.nb;
-  int64_t* ukeys = dmalloc<int64_t>(U, s);
-  if (U > 0) {
+  int64_t* ukeys = prep.keys;
+  prep.keys = nullptr;
+  if (!ukeys) ukeys = dmalloc<int64_t>(U, s);
+  if (U > 0 && prep.flags) {
     k_union_compact<<<grid_for(prep.npos, 256), 256, 0, s>>>(prep.flags, prep.off, x.depth, ukeys);
     SPAMM_LAUNCH_CK();
   }

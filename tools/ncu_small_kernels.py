@@ -1,0 +1,13 @@
+"""Driver for ncu captures of the non-K4 kernels of a cfg4 SP2 solve
+(K1 norms, K6 update, dense cull): runs two SP2 solves."""
+import sys
+import torch
+sys.path.insert(0, "/root/repo")
+import paper_1403_7458_b200 as sp
+from paper_1403_7458_b200.synth import CONFIGS, water_cluster
+cfg = CONFIGS[4]
+h, n_occ = water_cluster(cfg.n_mol, 0)
+f = sp.build_from_dense(torch.from_numpy(h).cuda(), cfg.block_size)
+for _ in range(2):
+    sp.sp2_solve(f, n_occ, cfg.tau, criterion="fro")
+torch.cuda.synchronize()
