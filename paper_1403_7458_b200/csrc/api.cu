@@ -378,9 +378,8 @@ void multiply_impl(const spamm_mat* a, const spamm_mat* b, double tau, int32_t k
     C.nblocks = r.n_c_full;
     C.keys = r.keys;
     r.keys = nullptr;
-    c_out = r.c_out;
+    c_out = r.c_out;  // (freed with r: they live in the cull's block)
     c_mirror = r.c_mirror;
-    r.c_out = r.c_mirror = nullptr;
   } else if (sym && r.n_c > 0) {
     const int64_t npos = C.G * C.G;
     uint8_t* flags = spamm::dmalloc<uint8_t>(npos, s);
@@ -419,8 +418,10 @@ void multiply_impl(const spamm_mat* a, const spamm_mat* b, double tau, int32_t k
                                   kernel, s, lpt);
   }
   tm.mark(2);
-  spamm::dfree(c_out, s);
-  spamm::dfree(c_mirror, s);
+  if (!r.block) {
+    spamm::dfree(c_out, s);
+    spamm::dfree(c_mirror, s);
+  }
   spamm::finalize(C, s, nullptr, nullptr, defer_prune);
   C.sym = sym;
   tm.mark(3);
@@ -444,20 +445,29 @@ void sp2_finish(const spamm_mat* x, const spamm_mat* c, double n_occ, bool want_
                 cudaStream_t s, bool* square_out, double* t_x, double* t_sq, double* idem,
                 spamm_mat** e_out) {
   const bool fused = spamm::sp2_fused_supported(x->m.nb);
-  // One host sync for tr(X), tr(X^2) and the union size of the update.
-  int64_t* sc = spamm::dmalloc<int64_t>(4, s);
-  SPAMM_CK(cudaMemsetAsync(sc, 0, 4 * sizeof(int64_t), s));
-  if (!x->m.tr_valid) spamm::trace_launch(x->m, reinterpret_cast<double*>(sc), s);
-  spamm::trace_launch(c->m, reinterpret_cast<double*>(sc + 1), s);
+  // One host sync (one gather launch) for tr(X), tr(X^2), the union size of
+  // the update and X^2's kept-block count.  Traces computed by the small-tree
+  // finalisation are read where they lie.
+  int64_t* sc = spamm::dmalloc<int64_t>(3, s);
+  const int64_t* src[4] = {nullptr, nullptr, nullptr, nullptr};
+  auto trace_src = [&](const spamm::Mat& m, int64_t* scratch) -> const int64_t* {
+    if (m.tr_dev) return reinterpret_cast<const int64_t*>(m.tr_dev);
+    spamm::trace_launch(m, reinterpret_cast<double*>(scratch), s);
+    return scratch;
+  };
+  if (!x->m.tr_valid) src[0] = trace_src(x->m, sc);
+  src[1] = trace_src(c->m, sc + 1);
   spamm::UnionPrep prep;
-  if (fused) prep = spamm::sp2_union_prepare(x->m, c->m, sc + 2, s);
-  const int64_t* kept_dev = spamm::pending_kept(c->m);  // lazy prune of X^2 rides along
-  if (kept_dev)
-    SPAMM_CK(cudaMemcpyAsync(sc + 3, kept_dev, sizeof(int64_t), cudaMemcpyDeviceToDevice, s));
+  if (fused) {
+    prep = spamm::sp2_union_prepare(x->m, c->m, sc + 2, s);
+    src[2] = sc + 2;
+  }
+  src[3] = spamm::pending_kept(c->m);  // lazy prune of X^2 rides along
+  const bool has_kept = src[3] != nullptr;
   int64_t h[4];
-  spamm::d2h_sync(h, sc, 4, s);
+  spamm::gather_sync(h, src, 4, s);
   spamm::dfree(sc, s);
-  if (kept_dev) spamm::settle(const_cast<spamm_mat*>(c)->m, h[3], s);
+  if (has_kept) spamm::settle(const_cast<spamm_mat*>(c)->m, h[3], s);
   if (!x->m.tr_valid) {
     memcpy(&x->m.tr, &h[0], sizeof(double));
     x->m.tr_valid = true;

@@ -396,13 +396,15 @@ bool dense_cull(const Mat& a, const Mat& b, double tau, bool want_tasks, CullRes
   const int64_t G = int64_t(1) << depth, npos = G * G;
   // aux[0]: full leaf survivors, [1]: mirror mismatch, [2]: packed scan
   // total, [4 + t]: tier-t survivors (t < depth)
-  int64_t* aux = dmalloc<int64_t>(4 + DENSE_MAX_DEPTH, s);
-  int64_t* cnt = dmalloc<int64_t>(npos, s);
-  int64_t* off = dmalloc<int64_t>(npos + 1, s);
-  // LPT schedule scratch: G + 1 length bins (bin 0 = G tasks) + the K4 counter
-  int* sched = dmalloc<int>(G + 2, s);
-  SPAMM_CK(cudaMemsetAsync(aux, 0, (4 + DENSE_MAX_DEPTH) * sizeof(int64_t), s));
-  SPAMM_CK(cudaMemsetAsync(sched, 0, (G + 2) * sizeof(int), s));
+  // [aux | LPT schedule: G + 1 length bins (bin 0 = G tasks) + the K4 counter]
+  // zeroed by one memset; the schedule part is handed to K4 (r.sched).
+  const size_t aux_bytes = (4 + DENSE_MAX_DEPTH) * sizeof(int64_t);
+  char* zbuf = dmalloc<char>(aux_bytes + (G + 2) * sizeof(int), s);
+  int64_t* aux = reinterpret_cast<int64_t*>(zbuf);
+  int* sched = reinterpret_cast<int*>(zbuf + aux_bytes);
+  int64_t* cnt = dmalloc<int64_t>(2 * npos + 1, s);
+  int64_t* off = cnt + npos;
+  SPAMM_CK(cudaMemsetAsync(zbuf, 0, aux_bytes + (G + 2) * sizeof(int), s));
   if (depth > 0) {
     const int64_t tri = ((int64_t(1) << (3 * depth)) - 1) / 7;
     k_dense_tiers<<<grid_for(tri, 256, 148LL * 8), 256, 0, s>>>(
@@ -416,14 +418,14 @@ bool dense_cull(const Mat& a, const Mat& b, double tau, bool want_tasks, CullRes
   SPAMM_LAUNCH_CK();
   scan_exclusive_i64(cnt, npos, off, s);
   if (want_tasks) hist_scan_exclusive(sched, (int)G + 1, s);
-  SPAMM_CK(cudaMemcpyAsync(aux + 2, off + npos, sizeof(int64_t), cudaMemcpyDeviceToDevice, s));
+  const int64_t* src[4 + DENSE_MAX_DEPTH];
+  for (int i = 0; i < 4 + depth; ++i) src[i] = aux + i;
+  src[2] = off + npos;
   int64_t h[4 + DENSE_MAX_DEPTH];
-  d2h_sync(h, aux, 4 + depth, s);
-  dfree(aux, s);
-  dfree(cnt, s);
+  gather_sync(h, src, 4 + depth, s);
   if (h[1]) {  // leaf survivor set not mirror-symmetric (ulp tie): full cull
-    dfree(off, s);
-    dfree(sched, s);
+    dfree(cnt, s);
+    dfree(zbuf, s);
     return false;
   }
   const int64_t V = h[2] & DT_TASK_MASK, M = (h[2] >> DT_NODE) & DT_IDX_MASK,
@@ -433,30 +435,38 @@ bool dense_cull(const Mat& a, const Mat& b, double tau, bool want_tasks, CullRes
   for (int t = 0; t <= depth; ++t)
     r.culled[t] = (t == 0 ? 1 : 8 * r.visited[t - 1]) - r.visited[t];
   if (!want_tasks || V == 0) {
-    dfree(off, s);
-    dfree(sched, s);
+    dfree(cnt, s);
+    dfree(zbuf, s);
     if (!want_tasks) r.n_tasks = r.visited[depth];
     return true;
   }
-  r.ci = dmalloc<int32_t>(M, s);
-  r.cj = dmalloc<int32_t>(M, s);
-  r.seg = dmalloc<int64_t>(M + 1, s);
-  r.k = dmalloc<int32_t>(V, s);
-  r.a_idx = dmalloc<int32_t>(V, s);
-  r.b_idx = dmalloc<int32_t>(V, s);
+  // all outputs carved from one allocation (owned through r.block)
+  // (C's keys are allocated on their own: multiply hands them to the product)
+  const size_t n64 = (M + 1) + (sym ? 2 * M : 0), n32 = 2 * M + 3 * V + M;
+  char* blk = dmalloc<char>(n64 * 8 + n32 * 4, s);
+  int64_t* p64 = reinterpret_cast<int64_t*>(blk);
+  int32_t* p32 = reinterpret_cast<int32_t*>(blk + n64 * 8);
+  r.block = blk;
+  r.seg = p64;
+  p64 += M + 1;
   r.keys = dmalloc<int64_t>(F, s);
-  r.order = dmalloc<int32_t>(M, s);
   if (sym) {
-    r.c_out = dmalloc<int64_t>(M, s);
-    r.c_mirror = dmalloc<int64_t>(M, s);
+    r.c_out = p64;
+    r.c_mirror = p64 + M;
   }
-  r.sched = sched;
+  r.ci = p32;
+  r.cj = p32 + M;
+  r.k = p32 + 2 * M;
+  r.a_idx = r.k + V;
+  r.b_idx = r.a_idx + V;
+  r.order = r.b_idx + V;
+  r.sched = reinterpret_cast<int*>(zbuf);  // frees the aux + schedule buffer
   r.counter = sched + G + 1;
   k_dense_leaf<true><<<grid_for(npos * 32, CULL_THREADS, 148LL * 64), CULL_THREADS, 0, s>>>(
       depth, a.norms, b.norms, tau, sym ? 1 : 0, nullptr, off, sched, r.ci, r.cj, r.seg, r.k,
       a.slot, b.slot, r.a_idx, r.b_idx, r.keys, r.c_out, r.c_mirror, r.order, M, V, nullptr);
   SPAMM_LAUNCH_CK();
-  dfree(off, s);
+  dfree(cnt, s);
   r.n_c = M;
   r.n_c_full = F;
   r.n_tasks = V;
@@ -479,6 +489,20 @@ void* pinned_staging(size_t bytes) {
 void set_dense_cull(bool enabled) { g_dense_enabled = enabled; }
 
 void CullResult::release(cudaStream_t s) {
+  if (block) {  // dense cull: every array but keys lives in one allocation
+    dfree(block, s);
+    dfree(sched, s);
+    dfree(keys, s);
+    block = nullptr;
+    ci = cj = nullptr;
+    seg = nullptr;
+    k = a_idx = b_idx = nullptr;
+    keys = c_out = c_mirror = nullptr;
+    order = nullptr;
+    sched = counter = nullptr;
+    n_c = n_tasks = 0;
+    return;
+  }
   dfree(ci, s);
   dfree(cj, s);
   dfree(seg, s);

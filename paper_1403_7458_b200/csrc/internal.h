@@ -20,6 +20,9 @@ T* dmalloc(size_t n, cudaStream_t s) {
 
 // Copy a few int64 from device to host and wait (the only host syncs on the path).
 void d2h_sync(int64_t* host, const int64_t* dev, int n, cudaStream_t s);
+// One launch copies n (<= 16) device scalars (null source -> 0) straight into
+// pinned host memory, then waits: replaces memset + D2D copies + D2H per sync.
+void gather_sync(int64_t* host, const int64_t* const* src, int n, cudaStream_t s);
 void stream_wait(cudaStream_t s);   // spin-polls unless SPAMM_WAIT=block
 void event_wait(cudaEvent_t e);     // spin-polls
 
@@ -123,6 +126,7 @@ struct CullResult {
   int64_t* c_mirror = nullptr;
   int32_t* order = nullptr;
   int* sched = nullptr;                  // hist/counter scratch (counter inside)
+  void* block = nullptr;                 // dense cull: single allocation of the arrays
   int* counter = nullptr;
   void release(cudaStream_t s);
 };

@@ -83,9 +83,34 @@ void event_wait(cudaEvent_t e) {
   }
 }
 
-void d2h_sync(int64_t* host, const int64_t* dev, int n, cudaStream_t s) {
+struct ScalarSrc {
+  const int64_t* p[16];
+};
+__global__ void k_gather_scalars(ScalarSrc src, int n, int64_t* dst) {
+  const int i = threadIdx.x;
+  if (i < n) dst[i] = src.p[i] ? *src.p[i] : 0;
+}
+
+int64_t* pinned_scalars() {
   static thread_local int64_t* pinned = nullptr;
   if (!pinned) SPAMM_CK(cudaMallocHost(&pinned, 64 * sizeof(int64_t)));
+  return pinned;
+}
+
+void gather_sync(int64_t* host, const int64_t* const* src, int n, cudaStream_t s) {
+  if (n > 16) throw CudaError("gather_sync: too many scalars");
+  ScalarSrc ss{};
+  for (int i = 0; i < n; ++i) ss.p[i] = src[i];
+  int64_t* pinned = pinned_scalars() + 32;  // (d2h_sync uses the first 32)
+  k_gather_scalars<<<1, 32, 0, s>>>(ss, n, pinned);
+  SPAMM_LAUNCH_CK();
+  stream_wait(s);
+  for (int i = 0; i < n; ++i) host[i] = pinned[i];
+}
+
+void d2h_sync(int64_t* host, const int64_t* dev, int n, cudaStream_t s) {
+  if (n > 32) throw CudaError("d2h_sync: too many scalars");
+  int64_t* pinned = pinned_scalars();
   SPAMM_CK(cudaMemcpyAsync(pinned, dev, n * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
   stream_wait(s);
   for (int i = 0; i < n; ++i) host[i] = pinned[i];
@@ -246,72 +271,102 @@ __global__ void k_tiers_small(double* __restrict__ norms2, double* __restrict__ 
   }
 }
 
-// Single-CTA finalisation for small trees (G*G <= 4096): the kept-block
-// scan, slot map, leaf tier, upper tiers (same sums as k_tier_up /
-// k_tiers_small), the trace (same order as k_trace_blocks + k_trace, Nb >= 2)
-// and the pinned host mirror of the top tiers, in one launch instead of ~9.
-// Any of off / slot / tr_out / host_top may be null.
-__global__ void __launch_bounds__(1024)
+// Single-CTA finalisation for small trees (G*G <= 4096, nblocks <= 4096):
+// the kept-block scan, slot map, leaf tier, upper tiers (same sums as
+// k_tier_up / k_tiers_small), the trace (same order as k_trace_blocks +
+// k_trace, Nb >= 2) and the pinned host mirror of the top tiers, in one
+// launch instead of ~9.  The squared pyramid is built in shared memory (one
+// round of global loads, then on-chip), each thread owning 4 consecutive
+// blocks / positions.  Any of nz+off / slot / tr_out / host_top may be null.
+constexpr int FS_THREADS = 1024, FS_PER = 4;  // 4096 positions
+__global__ void __launch_bounds__(FS_THREADS)
     k_finalize_small(const int64_t* __restrict__ keys, const double* __restrict__ n2,
                      const uint8_t* __restrict__ nz, int64_t nblocks, int depth,
                      int64_t* __restrict__ off, int32_t* __restrict__ slot,
                      double* __restrict__ norms, double* __restrict__ norms2,
                      const double* __restrict__ data, int nb, double* __restrict__ tr_out,
                      double* host_top, int top_t) {
+  __shared__ double p2[5461];  // squared pyramid, tiers 0..6
+  __shared__ int32_t dslot[64];
+  __shared__ double part[64];
   const int64_t G = int64_t(1) << depth, npos = G * G;
-  const int tid = threadIdx.x, nt = blockDim.x;
+  const int tid = threadIdx.x;
+  const int64_t leaf_off = tier_offset(depth);
+  // round 1: all loads of this thread's blocks in flight together
+  int64_t kk[FS_PER];
+  double vv[FS_PER];
+  int z[FS_PER];
+#pragma unroll
+  for (int j = 0; j < FS_PER; ++j) {
+    const int64_t b = (int64_t)tid * FS_PER + j;
+    const bool ok = b < nblocks;
+    kk[j] = ok ? keys[b] : -1;
+    vv[j] = ok ? n2[b] : 0.0;
+    z[j] = ok && nz ? nz[b] : 0;
+  }
+#pragma unroll
+  for (int j = 0; j < FS_PER; ++j) {
+    const int64_t p = (int64_t)tid * FS_PER + j;
+    if (p < npos) {
+      p2[leaf_off + p] = 0.0;
+      if (slot) slot[p] = -1;
+    }
+  }
+  if (tid < 64) dslot[tid] = -1;
   if (off) {
-    const int64_t per = (nblocks + nt - 1) / nt, b0 = tid * per;
-    int64_t loc = 0;
-    for (int64_t b = b0; b < b0 + per && b < nblocks; ++b) loc += nz[b];
     int64_t tot = 0;
-    int64_t ex = cta_exclusive_scan(loc, &tot);
-    for (int64_t b = b0; b < b0 + per && b < nblocks; ++b) {
-      off[b] = ex;
-      ex += nz[b];
+    int64_t ex = cta_exclusive_scan(z[0] + z[1] + z[2] + z[3], &tot);
+#pragma unroll
+    for (int j = 0; j < FS_PER; ++j) {
+      const int64_t b = (int64_t)tid * FS_PER + j;
+      if (b < nblocks) off[b] = ex;
+      ex += z[j];
     }
     if (tid == 0) off[nblocks] = tot;
   }
-  double* leaf2 = norms2 + tier_offset(depth);
-  double* leafn = norms + tier_offset(depth);
-  for (int64_t p = tid; p < npos; p += nt) {
-    if (slot) slot[p] = -1;
-    leaf2[p] = 0.0;
-    leafn[p] = 0.0;
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < FS_PER; ++j) {
+    if (kk[j] < 0) continue;
+    const int64_t b = (int64_t)tid * FS_PER + j;
+    p2[leaf_off + kk[j]] = vv[j];
+    if (slot) slot[kk[j]] = (int32_t)b;
+    if (kk[j] / G == kk[j] % G) dslot[kk[j] / G] = (int32_t)b;
   }
   __syncthreads();
-  for (int64_t b = tid; b < nblocks; b += nt) {
-    const int64_t k = keys[b];
-    if (slot) slot[k] = (int32_t)b;
-    const double v = n2[b];
-    leaf2[k] = v;
-    leafn[k] = __dsqrt_rn(v);
+#pragma unroll
+  for (int j = 0; j < FS_PER; ++j) {
+    const int64_t p = (int64_t)tid * FS_PER + j;
+    if (p < npos) {
+      const double v = p2[leaf_off + p];
+      norms2[leaf_off + p] = v;
+      norms[leaf_off + p] = __dsqrt_rn(v);
+    }
   }
-  __syncthreads();
   for (int t = depth - 1; t >= 0; --t) {
     const int64_t w = int64_t(1) << t, W = 2 * w, n = w * w;
-    const double* c2 = norms2 + tier_offset(t + 1);
-    double* p2 = norms2 + tier_offset(t);
-    double* pn = norms + tier_offset(t);
-    for (int64_t idx = tid; idx < n; idx += nt) {
+    const int64_t co = tier_offset(t + 1), po = tier_offset(t);
+    for (int64_t idx = tid; idx < n; idx += FS_THREADS) {
       const int64_t i = idx / w, j = idx % w;
-      const double* r0 = c2 + (2 * i) * W + 2 * j;
+      const double* r0 = p2 + co + (2 * i) * W + 2 * j;
       const double* r1 = r0 + W;
+      // root (t = 0): numpy coalesces the 2x2 into one run of 4 -> sequential
       const double sm = t == 0 ? __dadd_rn(__dadd_rn(__dadd_rn(r0[0], r0[1]), r1[0]), r1[1])
                                : __dadd_rn(__dadd_rn(r0[0], r0[1]), __dadd_rn(r1[0], r1[1]));
-      p2[idx] = sm;
-      pn[idx] = __dsqrt_rn(sm);
+      p2[po + idx] = sm;
+      norms2[po + idx] = sm;
+      norms[po + idx] = __dsqrt_rn(sm);
     }
     __syncthreads();
   }
-  if (tr_out && slot) {
-    __shared__ double part[64];
-    __shared__ int present[64];
+  if (host_top) {
+    for (int64_t i = tid; i < tier_offset(top_t + 1); i += FS_THREADS) host_top[i] = __dsqrt_rn(p2[i]);
+  }
+  if (tr_out) {
     const int warp = tid >> 5, lane = tid & 31;
     const int64_t nb2 = (int64_t)nb * nb;
-    for (int64_t b = warp; b < G; b += nt >> 5) {
-      const int32_t sl = slot[b * G + b];
-      if (lane == 0) present[b] = sl >= 0;
+    for (int64_t b = warp; b < G; b += FS_THREADS / 32) {
+      const int32_t sl = dslot[b];
       if (sl < 0) continue;
       const double* x = data + (int64_t)sl * nb2;
       double acc = 0.0;
@@ -327,12 +382,9 @@ __global__ void __launch_bounds__(1024)
     if (tid == 0) {
       double tot = 0.0;
       for (int64_t b = 0; b < G; ++b)
-        if (present[b]) tot = __dadd_rn(tot, part[b]);
+        if (dslot[b] >= 0) tot = __dadd_rn(tot, part[b]);
       *tr_out = tot;
     }
-  }
-  if (host_top) {
-    for (int64_t i = tid; i < tier_offset(top_t + 1); i += nt) host_top[i] = norms[i];
   }
 }
 

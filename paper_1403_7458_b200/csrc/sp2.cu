@@ -42,27 +42,35 @@ __global__ void k_union_compact(const uint8_t* __restrict__ flags, const int64_t
   }
 }
 
-// Small trees (G*G <= 4096): union flags, scan and compaction in one CTA.
+// Small trees (G*G <= 4096): union flags, scan and compaction in one CTA
+// (1024 threads x 4 consecutive Morton positions, all slot loads in flight).
 __global__ void __launch_bounds__(1024)
     k_union_small(const int32_t* __restrict__ sa, const int32_t* __restrict__ sb, int depth,
                   int64_t* __restrict__ keys, int64_t* __restrict__ count) {
   const int64_t G = int64_t(1) << depth, npos = G * G;
-  const int64_t per = (npos + blockDim.x - 1) / blockDim.x, p0 = threadIdx.x * per;
-  int64_t loc = 0;
-  for (int64_t p = p0; p < p0 + per && p < npos; ++p) {
+  int64_t key[4];
+  int f[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int64_t p = (int64_t)threadIdx.x * 4 + j;
     uint32_t bi, bj;
     morton_decode((uint64_t)p, bi, bj);
-    const int64_t key = (int64_t)bi * G + bj;
-    loc += (sa[key] >= 0 || sb[key] >= 0) ? 1 : 0;
+    key[j] = (int64_t)bi * G + bj;
   }
+  int32_t va[4], vb[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const bool ok = (int64_t)threadIdx.x * 4 + j < npos;
+    va[j] = ok ? sa[key[j]] : -1;
+    vb[j] = ok ? sb[key[j]] : -1;
+  }
+#pragma unroll
+  for (int j = 0; j < 4; ++j) f[j] = (va[j] >= 0) | (vb[j] >= 0);
   int64_t tot = 0;
-  int64_t o = cta_exclusive_scan(loc, &tot);
-  for (int64_t p = p0; p < p0 + per && p < npos; ++p) {
-    uint32_t bi, bj;
-    morton_decode((uint64_t)p, bi, bj);
-    const int64_t key = (int64_t)bi * G + bj;
-    if (sa[key] >= 0 || sb[key] >= 0) keys[o++] = key;
-  }
+  int64_t o = cta_exclusive_scan(f[0] + f[1] + f[2] + f[3], &tot);
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+    if (f[j]) keys[o++] = key[j];
   if (threadIdx.x == 0) *count = tot;
 }
 
@@ -363,14 +371,9 @@ void sp2_update_finish(const Mat& x, const Mat& x2, UnionPrep& prep, int64_t U, 
   // One host sync for the idempotency norm and E's kept-block count.
   const int64_t* kept_dev = expand ? pending_kept(e) : nullptr;
   if (want_idem || kept_dev) {
-    int64_t* sc = dmalloc<int64_t>(2, s);
-    if (want_idem)
-      SPAMM_CK(cudaMemcpyAsync(sc, pn, sizeof(int64_t), cudaMemcpyDeviceToDevice, s));
-    if (kept_dev)
-      SPAMM_CK(cudaMemcpyAsync(sc + 1, kept_dev, sizeof(int64_t), cudaMemcpyDeviceToDevice, s));
+    const int64_t* src[2] = {want_idem ? reinterpret_cast<const int64_t*>(pn) : nullptr, kept_dev};
     int64_t h[2] = {0, 0};
-    d2h_sync(h, sc, 2, s);
-    dfree(sc, s);
+    gather_sync(h, src, 2, s);
     if (want_idem) memcpy(idem_norm, &h[0], sizeof(double));
     if (kept_dev) settle(e, h[1], s);
   }
