@@ -163,7 +163,8 @@ void fill_stats(spamm_stats* st, double tau, const spamm::CullResult& r, int nb)
 
 void multiply_impl(const spamm_mat* a, const spamm_mat* b, double tau, int32_t kernel, bool timed,
                    cudaStream_t s, spamm::Mat& C, spamm_stats* stats, int64_t lo = 0,
-                   int64_t hi = -1, int32_t* work = nullptr, bool defer_prune = false);
+                   int64_t hi = -1, int32_t* work = nullptr, bool defer_prune = false,
+                   spamm::IdemFuse idem = {});
 
 }  // namespace
 
@@ -355,7 +356,7 @@ namespace {
 
 void multiply_impl(const spamm_mat* a, const spamm_mat* b, double tau, int32_t kernel, bool timed,
                    cudaStream_t s, spamm::Mat& C, spamm_stats* stats, int64_t lo, int64_t hi,
-                   int32_t* work, bool defer_prune) {
+                   int32_t* work, bool defer_prune, spamm::IdemFuse idem) {
   EventTimer tm(timed, s);
   tm.mark(0);
   spamm::CullResult r;
@@ -422,7 +423,10 @@ void multiply_impl(const spamm_mat* a, const spamm_mat* b, double tau, int32_t k
     spamm::dfree(c_out, s);
     spamm::dfree(c_mirror, s);
   }
-  spamm::finalize(C, s, nullptr, nullptr, defer_prune);
+  if (idem.x)
+    spamm::finalize(C, s, idem, defer_prune);
+  else
+    spamm::finalize(C, s, nullptr, nullptr, defer_prune);
   C.sym = sym;
   tm.mark(3);
   fill_stats(stats, tau, r, C.nb);
@@ -443,13 +447,13 @@ void multiply_impl(const spamm_mat* a, const spamm_mat* b, double tau, int32_t k
 // branch rule, then the fused K6 pass.  *e receives 2X - X2 on EXPAND.
 void sp2_finish(const spamm_mat* x, const spamm_mat* c, double n_occ, bool want_idem,
                 cudaStream_t s, bool* square_out, double* t_x, double* t_sq, double* idem,
-                spamm_mat** e_out) {
+                spamm_mat** e_out, const double* idem_dev = nullptr) {
   const bool fused = spamm::sp2_fused_supported(x->m.nb);
   // One host sync (one gather launch) for tr(X), tr(X^2), the union size of
   // the update and X^2's kept-block count.  Traces computed by the small-tree
   // finalisation are read where they lie.
   int64_t* sc = spamm::dmalloc<int64_t>(3, s);
-  const int64_t* src[4] = {nullptr, nullptr, nullptr, nullptr};
+  const int64_t* src[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
   auto trace_src = [&](const spamm::Mat& m, int64_t* scratch) -> const int64_t* {
     if (m.tr_dev) return reinterpret_cast<const int64_t*>(m.tr_dev);
     spamm::trace_launch(m, reinterpret_cast<double*>(scratch), s);
@@ -463,9 +467,12 @@ void sp2_finish(const spamm_mat* x, const spamm_mat* c, double n_occ, bool want_
     src[2] = sc + 2;
   }
   src[3] = spamm::pending_kept(c->m);  // lazy prune of X^2 rides along
+  src[4] = reinterpret_cast<const int64_t*>(idem_dev);  // fused ||X^2 - X||_F
   const bool has_kept = src[3] != nullptr;
-  int64_t h[4];
-  spamm::gather_sync(h, src, 4, s);
+  int64_t h[5];
+  spamm::gather_sync(h, src, 5, s);
+  const bool idem_done = want_idem && idem_dev;
+  if (idem_done) memcpy(idem, &h[4], sizeof(double));
   spamm::dfree(sc, s);
   if (has_kept) spamm::settle(const_cast<spamm_mat*>(c)->m, h[3], s);
   if (!x->m.tr_valid) {
@@ -481,10 +488,12 @@ void sp2_finish(const spamm_mat* x, const spamm_mat* c, double n_occ, bool want_
   spamm_mat* e = square ? nullptr : new spamm_mat();
   spamm::Mat dummy;
   if (fused) {
-    spamm::sp2_update_finish(x->m, c->m, prep, h[2], want_idem, !square, idem,
-                             e ? e->m : dummy, s);
+    // with the residual fused into K1 there is nothing left to sync on: E's
+    // exact-zero blocks stay pending (settled when the handle is inspected)
+    spamm::sp2_update_finish(x->m, c->m, prep, h[2], want_idem && !idem_done, !square, idem,
+                             e ? e->m : dummy, s, /*settle_now=*/!idem_done);
   } else {
-    spamm::sp2_update(x->m, c->m, want_idem, !square, idem, e ? e->m : dummy, s);
+    spamm::sp2_update(x->m, c->m, want_idem && !idem_done, !square, idem, e ? e->m : dummy, s);
   }
   if (e) {
     e->m.stream = s;
@@ -513,11 +522,17 @@ int spamm_sp2_step(const spamm_mat* x, double n_occ, double tau, int32_t kernel,
   SPAMM_API_BEGIN
   cudaStream_t s = S(stream);
   auto* c = new spamm_mat();
-  multiply_impl(x, x, tau, kernel, timed != 0, s, c->m, stats, 0, -1, nullptr, true);
+  spamm::IdemFuse fuse;
+  if (want_idem && spamm::idem_fusable(x->m)) {
+    fuse.x = &x->m;
+    fuse.out = spamm::dmalloc<double>(1, s);
+  }
+  multiply_impl(x, x, tau, kernel, timed != 0, s, c->m, stats, 0, -1, nullptr, true, fuse);
   spamm_mat* e = nullptr;
   bool square = true;
   double tx = 0, tsq = 0;
-  sp2_finish(x, c, n_occ, want_idem != 0, s, &square, &tx, &tsq, idem, &e);
+  sp2_finish(x, c, n_occ, want_idem != 0, s, &square, &tx, &tsq, idem, &e, fuse.out);
+  spamm::dfree(fuse.out, s);
   if (e) {
     c->m.release();
     delete c;
@@ -764,14 +779,25 @@ int spamm_sp2_solve(const spamm_mat* f, double n_occ, double tau, int32_t max_it
   int n_tr = 0;
   rep->trace_history[n_tr++] = spamm::trace(x->m, s);
   bool pending_trace = false;
+  double* idem_dev = spamm::dmalloc<double>(1, s);
+  struct IdemFree {
+    double* p;
+    cudaStream_t s;
+    ~IdemFree() { spamm::dfree(p, s); }
+  } idem_free{idem_dev, s};
   for (int it = 0; it < max_iter; ++it) {
     auto* c = new spamm_mat();
     spamm_stats st;
-    multiply_impl(x, x, tau, kernel, timed != 0, s, c->m, &st, 0, -1, nullptr, true);
+    spamm::IdemFuse fuse;
+    if (want_idem && spamm::idem_fusable(x->m)) {
+      fuse.x = &x->m;
+      fuse.out = idem_dev;
+    }
+    multiply_impl(x, x, tau, kernel, timed != 0, s, c->m, &st, 0, -1, nullptr, true, fuse);
     bool square = true;
     double tx = 0, tsq = 0, idem = 0;
     spamm_mat* e = nullptr;
-    sp2_finish(x, c, n_occ, want_idem, s, &square, &tx, &tsq, &idem, &e);
+    sp2_finish(x, c, n_occ, want_idem, s, &square, &tx, &tsq, &idem, &e, fuse.out);
     const int k = rep->n_multiplies++;
     rep->leaf_products[k] = st.leaf_products;
     rep->executed_products[k] = st.executed_products;

@@ -67,6 +67,15 @@ bool is_symmetric(const Mat& m, cudaStream_t s);
 // fused producer kernel; K1 is then skipped).
 // defer = true: no host sync -- exact-zero blocks are kept until settle()
 // (the kept count is then read with some later sync, see pending_kept()).
+// Idempotency residual fused into the finalisation of C = X*X (small trees,
+// Nb 32 / 64): the root norm of add_scaled(1, C, -1, X) (quadtree.py:281-293)
+// is written to *out as the K1 pass reads C, so SP2 needs no separate D pass.
+struct IdemFuse {
+  const Mat* x = nullptr;
+  double* out = nullptr;
+};
+bool idem_fusable(const Mat& x);
+void finalize(Mat& m, cudaStream_t s, IdemFuse idem, bool defer);
 void finalize(Mat& m, cudaStream_t s, double* pre_n2 = nullptr, uint8_t* pre_nz = nullptr,
               bool defer = false);
 const int64_t* pending_kept(const Mat& m);  // device count, or nullptr if settled
@@ -89,7 +98,8 @@ struct UnionPrep {
 };
 UnionPrep sp2_union_prepare(const Mat& x, const Mat& x2, int64_t* u_dev, cudaStream_t s);
 void sp2_update_finish(const Mat& x, const Mat& x2, UnionPrep& prep, int64_t U, bool want_idem,
-                       bool expand, double* idem_norm, Mat& e, cudaStream_t s);
+                       bool expand, double* idem_norm, Mat& e, cudaStream_t s,
+                       bool settle_now = true);
 bool sp2_fused_supported(int nb);
 
 void scatter_slots(const int64_t* keys, int64_t m, int32_t* slot, cudaStream_t s);

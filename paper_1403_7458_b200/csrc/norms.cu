@@ -285,7 +285,9 @@ __global__ void __launch_bounds__(FS_THREADS)
                      int64_t* __restrict__ off, int32_t* __restrict__ slot,
                      double* __restrict__ norms, double* __restrict__ norms2,
                      const double* __restrict__ data, int nb, double* __restrict__ tr_out,
-                     double* host_top, int top_t) {
+                     double* host_top, int top_t, const double* __restrict__ dn2 = nullptr,
+                     const double* __restrict__ xleaf2 = nullptr,
+                     double* __restrict__ idem_out = nullptr) {
   __shared__ double p2[5461];  // squared pyramid, tiers 0..6
   __shared__ int32_t dslot[64];
   __shared__ double part[64];
@@ -386,6 +388,34 @@ __global__ void __launch_bounds__(FS_THREADS)
       *tr_out = tot;
     }
   }
+  if (idem_out) {
+    // D = add_scaled(1, C, -1, X): leaf norm^2 = dn2 at C's blocks, X's own
+    // leaf norm^2 where only X has a block ((-x)^2 == x^2), 0 elsewhere; the
+    // same tier sums, root norm out.
+    __syncthreads();  // p2 (C's pyramid) and slot complete
+#pragma unroll
+    for (int j = 0; j < FS_PER; ++j) {
+      const int64_t p = (int64_t)tid * FS_PER + j;
+      if (p < npos) {
+        const int32_t cs = slot[p];
+        p2[leaf_off + p] = cs >= 0 ? dn2[cs] : xleaf2[p];
+      }
+    }
+    __syncthreads();
+    for (int t = depth - 1; t >= 0; --t) {
+      const int64_t w = int64_t(1) << t, W = 2 * w, n = w * w;
+      const int64_t co = tier_offset(t + 1), po = tier_offset(t);
+      for (int64_t idx = tid; idx < n; idx += FS_THREADS) {
+        const int64_t i = idx / w, j = idx % w;
+        const double* r0 = p2 + co + (2 * i) * W + 2 * j;
+        const double* r1 = r0 + W;
+        p2[po + idx] = t == 0 ? __dadd_rn(__dadd_rn(__dadd_rn(r0[0], r0[1]), r1[0]), r1[1])
+                              : __dadd_rn(__dadd_rn(r0[0], r0[1]), __dadd_rn(r1[0], r1[1]));
+      }
+      __syncthreads();
+    }
+    if (tid == 0) *idem_out = __dsqrt_rn(p2[0]);
+  }
 }
 
 // Gather the kept blocks (nz[b] = 1) to their compacted positions.
@@ -467,6 +497,85 @@ __global__ void __launch_bounds__(32 * WARPS)
       if (lane == 0 && b0 + q < m) {
         out[b0 + q] = __dadd_rn(l0, l1);
         if (nz) nz[b0 + q] = any ? 1 : 0;
+      }
+    }
+  }
+}
+
+// K1 for C = X*X with the idempotency residual fused in: besides C's leaf
+// norm^2 it chains D = fl(c - x) (= add_scaled(1, C, -1, X) blockwise; x = 0
+// where X has no block, which leaves c unchanged) for every C block.  Lanes
+// 4q + 2 set + parity: set 0 = C chain, set 1 = D chain (BPW = 2 -> 8 rows,
+// one LDS.128 wavefront).
+template <int NB2, int WARPS>
+__global__ void __launch_bounds__(32 * WARPS)
+    k_leaf_norms2_cd(const double* __restrict__ data, const int64_t* __restrict__ keys,
+                     int64_t m, const double* __restrict__ xdata,
+                     const int32_t* __restrict__ xslot, double* __restrict__ out,
+                     uint8_t* __restrict__ nz, double* __restrict__ dout) {
+  constexpr int NCH = NB2 / 256, BPW = 2;
+  __shared__ __align__(16) double rows_all[WARPS][BPW * 4 * CHAIN_ROW];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* rows = rows_all[warp];
+  const int64_t stride = (int64_t)gridDim.x * WARPS * BPW;
+  for (int64_t b0 = ((int64_t)blockIdx.x * WARPS + warp) * BPW; b0 < m; b0 += stride) {
+    const double2* c[BPW];
+    const double2* x[BPW];
+    double2 r[BPW][4], y[BPW][4];
+#pragma unroll
+    for (int q = 0; q < BPW; ++q) {
+      c[q] = x[q] = nullptr;
+      if (b0 + q < m) {
+        c[q] = reinterpret_cast<const double2*>(data + (b0 + q) * NB2);
+        const int32_t xs = xslot[keys[b0 + q]];
+        if (xs >= 0) x[q] = reinterpret_cast<const double2*>(xdata + (int64_t)xs * NB2);
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        r[q][k] = c[q] ? __ldg(c[q] + k * 32 + lane) : make_double2(0.0, 0.0);
+        y[q][k] = x[q] ? __ldg(x[q] + k * 32 + lane) : make_double2(0.0, 0.0);
+      }
+    }
+    double acc = 0.0;
+    unsigned anyq = 0;
+    for (int ch = 0; ch < NCH; ++ch) {
+      __syncwarp();
+#pragma unroll
+      for (int q = 0; q < BPW; ++q)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          double* rq = rows + q * 4 * CHAIN_ROW + chain_pos(k, lane);
+          const double d0 = __dsub_rn(r[q][k].x, y[q][k].x);
+          const double d1 = __dsub_rn(r[q][k].y, y[q][k].y);
+          rq[0] = __dmul_rn(r[q][k].x, r[q][k].x);
+          rq[CHAIN_ROW] = __dmul_rn(r[q][k].y, r[q][k].y);
+          rq[2 * CHAIN_ROW] = __dmul_rn(d0, d0);
+          rq[3 * CHAIN_ROW] = __dmul_rn(d1, d1);
+          if ((r[q][k].x != 0.0) | (r[q][k].y != 0.0)) anyq |= 1u << q;
+        }
+      __syncwarp();
+      if (ch + 1 < NCH) {
+#pragma unroll
+        for (int q = 0; q < BPW; ++q)
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            if (c[q]) r[q][k] = __ldg(c[q] + (ch + 1) * 128 + k * 32 + lane);
+            if (x[q]) y[q][k] = __ldg(x[q] + (ch + 1) * 128 + k * 32 + lane);
+          }
+      }
+      if (lane < 4 * BPW) acc = chain_row128(rows + lane * CHAIN_ROW, acc);
+    }
+#pragma unroll
+    for (int q = 0; q < BPW; ++q) {
+      const double c0 = __shfl_sync(0xffffffffu, acc, 4 * q);
+      const double c1 = __shfl_sync(0xffffffffu, acc, 4 * q + 1);
+      const double e0 = __shfl_sync(0xffffffffu, acc, 4 * q + 2);
+      const double e1 = __shfl_sync(0xffffffffu, acc, 4 * q + 3);
+      const bool any = __any_sync(0xffffffffu, (anyq >> q) & 1u);
+      if (lane == 0 && b0 + q < m) {
+        out[b0 + q] = __dadd_rn(c0, c1);
+        nz[b0 + q] = any ? 1 : 0;
+        dout[b0 + q] = __dadd_rn(e0, e1);
       }
     }
   }
@@ -574,17 +683,48 @@ void scatter_slots(const int64_t* keys, int64_t m, int32_t* slot, cudaStream_t s
   SPAMM_LAUNCH_CK();
 }
 
+void finalize_impl(Mat& m, cudaStream_t s, double* pre_n2, uint8_t* pre_nz, bool defer,
+                   IdemFuse idem);
+
+bool idem_fusable(const Mat& x) {
+  return x.depth <= SMALL_TREE_DEPTH && (x.nb == 32 || x.nb == 64);
+}
+
+void finalize(Mat& m, cudaStream_t s, IdemFuse idem, bool defer) {
+  if (!idem.x || !defer || !idem_fusable(m)) throw CudaError("finalize: idempotency fusion unsupported");
+  finalize_impl(m, s, nullptr, nullptr, defer, idem);
+}
+
 void finalize(Mat& m, cudaStream_t s, double* pre_n2, uint8_t* pre_nz, bool defer) {
+  finalize_impl(m, s, pre_n2, pre_nz, defer, IdemFuse{});
+}
+
+void finalize_impl(Mat& m, cudaStream_t s, double* pre_n2, uint8_t* pre_nz, bool defer,
+                   IdemFuse idem) {
   m.stream = s;
   const int nb2 = m.nb * m.nb;
   double* n2 = pre_n2;
   if (defer && m.depth <= SMALL_TREE_DEPTH) {
     // one launch (after K1 unless the producer already computed the norms)
     uint8_t* nz = pre_nz;
+    double* dn2 = nullptr;
     if (m.nblocks > 0 && !n2) {
       n2 = dmalloc<double>(m.nblocks, s);
       nz = dmalloc<uint8_t>(m.nblocks, s);
-      leaf_norms2(m.data, m.nblocks, m.nb, n2, nz, s);
+      if (idem.x) {
+        dn2 = dmalloc<double>(m.nblocks, s);
+        constexpr int WARPS = 4;
+        const int grid = grid_for((m.nblocks + 1) / 2 * 32, 32 * WARPS, 1LL << 20);
+        if (nb2 == 4096)
+          k_leaf_norms2_cd<4096, WARPS><<<grid, 32 * WARPS, 0, s>>>(
+              m.data, m.keys, m.nblocks, idem.x->data, idem.x->slot, n2, nz, dn2);
+        else
+          k_leaf_norms2_cd<1024, WARPS><<<grid, 32 * WARPS, 0, s>>>(
+              m.data, m.keys, m.nblocks, idem.x->data, idem.x->slot, n2, nz, dn2);
+        SPAMM_LAUNCH_CK();
+      } else {
+        leaf_norms2(m.data, m.nblocks, m.nb, n2, nz, s);
+      }
     }
     m.G = int64_t(1) << m.depth;
     m.slot = dmalloc<int32_t>(m.G * m.G, s);
@@ -600,8 +740,11 @@ void finalize(Mat& m, cudaStream_t s, double* pre_n2, uint8_t* pre_nz, bool defe
     }
     k_finalize_small<<<1, 1024, 0, s>>>(m.keys, n2, nz, m.nblocks, m.depth, off, m.slot, m.norms,
                                         m.norms2, m.data, m.nb, m.tr_dev,
-                                        m.host_top, m.host_top ? m.top_t : -1);
+                                        m.host_top, m.host_top ? m.top_t : -1, dn2,
+                                        idem.x ? idem.x->norms2 + tier_offset(m.depth) : nullptr,
+                                        idem.out);
     SPAMM_LAUNCH_CK();
+    dfree(dn2, s);
     if (m.host_top) SPAMM_CK(cudaEventRecord(m.top_ev, s));
     dfree(n2, s);
     if (m.nblocks > 0) {

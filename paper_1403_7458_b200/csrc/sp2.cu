@@ -320,7 +320,7 @@ UnionPrep sp2_union_prepare(const Mat& x, const Mat& x2, int64_t* u_dev, cudaStr
 }
 
 void sp2_update_finish(const Mat& x, const Mat& x2, UnionPrep& prep, int64_t U, bool want_idem,
-                       bool expand, double* idem_norm, Mat& e, cudaStream_t s) {
+                       bool expand, double* idem_norm, Mat& e, cudaStream_t s, bool settle_now) {
   const int nb2 = x.nb * x.nb;
   int64_t* ukeys = prep.keys;
   prep.keys = nullptr;
@@ -369,7 +369,7 @@ void sp2_update_finish(const Mat& x, const Mat& x2, UnionPrep& prep, int64_t U, 
     dfree(ukeys, s);
   }
   // One host sync for the idempotency norm and E's kept-block count.
-  const int64_t* kept_dev = expand ? pending_kept(e) : nullptr;
+  const int64_t* kept_dev = expand && settle_now ? pending_kept(e) : nullptr;
   if (want_idem || kept_dev) {
     const int64_t* src[2] = {want_idem ? reinterpret_cast<const int64_t*>(pn) : nullptr, kept_dev};
     int64_t h[2] = {0, 0};
