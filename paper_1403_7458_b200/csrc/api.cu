@@ -291,7 +291,7 @@ int spamm_mat_identity(int64_t n, int32_t block_size, int64_t chunk_size, void* 
 
 int spamm_mat_info_get(const spamm_mat* h, spamm_mat_info* info) {
   if (!h || !info) return fail(SPAMM_EINVAL, "null argument");
-  if (h->m.pend_off) {  // never expose a lazily pruned matrix
+  if (h->m.pend_nz) {  // never expose a lazily pruned matrix
     try {
       spamm::settle_sync(const_cast<spamm_mat*>(h)->m, h->m.stream);
     } catch (const std::exception& e) {

@@ -50,7 +50,8 @@ struct Mat {
   cudaEvent_t top_ev = nullptr;
   // Lazy prune state (finalize(..., defer = true)); nullptr once settled.
   uint8_t* pend_nz = nullptr;
-  int64_t* pend_off = nullptr;
+  int64_t* pend_off = nullptr;   // kept offsets (+ count at [nblocks]), or null if
+  int64_t* pend_kept = nullptr;  // only the count was produced (small trees)
   cudaStream_t stream = nullptr;
   void release();
 };
@@ -76,8 +77,9 @@ struct IdemFuse {
 };
 bool idem_fusable(const Mat& x);
 void finalize(Mat& m, cudaStream_t s, IdemFuse idem, bool defer);
+// pre_n1 (optional): sqrt of pre_n2, computed by the producer.
 void finalize(Mat& m, cudaStream_t s, double* pre_n2 = nullptr, uint8_t* pre_nz = nullptr,
-              bool defer = false);
+              bool defer = false, double* pre_n1 = nullptr);
 const int64_t* pending_kept(const Mat& m);  // device count, or nullptr if settled
 void settle(Mat& m, int64_t kept, cudaStream_t s);
 void settle_sync(Mat& m, cudaStream_t s);
@@ -104,8 +106,9 @@ bool sp2_fused_supported(int nb);
 
 void scatter_slots(const int64_t* keys, int64_t m, int32_t* slot, cudaStream_t s);
 // Leaf norm^2 (einsum recipe) and nonzero flags for m blocks of nb x nb.
+// norms1 (optional, Nb 32 / 64 only): sqrt of each leaf norm^2
 void leaf_norms2(const double* data, int64_t m, int nb, double* norms2, uint8_t* nonzero,
-                 cudaStream_t s);
+                 cudaStream_t s, double* norms1 = nullptr);
 // Fill the pyramid from per-block leaf norms^2 (keys given); zero elsewhere.
 void build_pyramid(const int64_t* keys, const double* blk_norms2, int64_t m, int depth,
                    double* norms, double* norms2, cudaStream_t s);

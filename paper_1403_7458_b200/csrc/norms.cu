@@ -154,8 +154,10 @@ void Mat::release() {
   tr_dev = nullptr;
   dfree(pend_nz, stream);
   dfree(pend_off, stream);
+  dfree(pend_kept, stream);
   pend_nz = nullptr;
   pend_off = nullptr;
+  pend_kept = nullptr;
   top_release(host_top, top_ev);
   host_top = nullptr;
   top_ev = nullptr;
@@ -272,31 +274,32 @@ __global__ void k_tiers_small(double* __restrict__ norms2, double* __restrict__ 
 }
 
 // Single-CTA finalisation for small trees (G*G <= 4096, nblocks <= 4096):
-// the kept-block scan, slot map, leaf tier, upper tiers (same sums as
+// the kept-block count, slot map, leaf tier, upper tiers (same sums as
 // k_tier_up / k_tiers_small), the trace (same order as k_trace_blocks +
-// k_trace, Nb >= 2) and the pinned host mirror of the top tiers, in one
-// launch instead of ~9.  The squared pyramid is built in shared memory (one
-// round of global loads, then on-chip), each thread owning 4 consecutive
-// blocks / positions.  Any of nz+off / slot / tr_out / host_top may be null.
+// k_trace, Nb >= 2), the pinned host mirror of the top tiers and optionally
+// the idempotency residual root, in one launch instead of ~9.  The squared
+// pyramid is built in shared memory; each thread owns 4 consecutive blocks /
+// positions.  n1 (leaf norms, sqrt of n2) may come from the producer; any of
+// nz+kept / slot / tr_out / host_top / idem_out may be null.
 constexpr int FS_THREADS = 1024, FS_PER = 4;  // 4096 positions
 __global__ void __launch_bounds__(FS_THREADS)
     k_finalize_small(const int64_t* __restrict__ keys, const double* __restrict__ n2,
-                     const uint8_t* __restrict__ nz, int64_t nblocks, int depth,
-                     int64_t* __restrict__ off, int32_t* __restrict__ slot,
-                     double* __restrict__ norms, double* __restrict__ norms2,
-                     const double* __restrict__ data, int nb, double* __restrict__ tr_out,
-                     double* host_top, int top_t, const double* __restrict__ dn2 = nullptr,
-                     const double* __restrict__ xleaf2 = nullptr,
-                     double* __restrict__ idem_out = nullptr) {
+                     const double* __restrict__ n1, const uint8_t* __restrict__ nz,
+                     int64_t nblocks, int depth, int64_t* __restrict__ kept,
+                     int32_t* __restrict__ slot, double* __restrict__ norms,
+                     double* __restrict__ norms2, const double* __restrict__ data, int nb,
+                     double* __restrict__ tr_out, double* host_top, int top_t,
+                     const double* __restrict__ dn2, const double* __restrict__ xleaf2,
+                     double* __restrict__ idem_out) {
   __shared__ double p2[5461];  // squared pyramid, tiers 0..6
   __shared__ int32_t dslot[64];
   __shared__ double part[64];
   const int64_t G = int64_t(1) << depth, npos = G * G;
   const int tid = threadIdx.x;
   const int64_t leaf_off = tier_offset(depth);
-  // round 1: all loads of this thread's blocks in flight together
+  // all loads of this thread's blocks in flight together
   int64_t kk[FS_PER];
-  double vv[FS_PER];
+  double vv[FS_PER], v1[FS_PER];
   int z[FS_PER];
 #pragma unroll
   for (int j = 0; j < FS_PER; ++j) {
@@ -304,6 +307,7 @@ __global__ void __launch_bounds__(FS_THREADS)
     const bool ok = b < nblocks;
     kk[j] = ok ? keys[b] : -1;
     vv[j] = ok ? n2[b] : 0.0;
+    v1[j] = ok && n1 ? n1[b] : 0.0;
     z[j] = ok && nz ? nz[b] : 0;
   }
 #pragma unroll
@@ -311,45 +315,36 @@ __global__ void __launch_bounds__(FS_THREADS)
     const int64_t p = (int64_t)tid * FS_PER + j;
     if (p < npos) {
       p2[leaf_off + p] = 0.0;
+      norms2[leaf_off + p] = 0.0;
+      norms[leaf_off + p] = 0.0;
       if (slot) slot[p] = -1;
     }
   }
   if (tid < 64) dslot[tid] = -1;
-  if (off) {
-    int64_t tot = 0;
-    int64_t ex = cta_exclusive_scan(z[0] + z[1] + z[2] + z[3], &tot);
+  if (kept) {
+    int c = 0;
 #pragma unroll
-    for (int j = 0; j < FS_PER; ++j) {
-      const int64_t b = (int64_t)tid * FS_PER + j;
-      if (b < nblocks) off[b] = ex;
-      ex += z[j];
-    }
-    if (tid == 0) off[nblocks] = tot;
+    for (int j = 0; j < FS_PER; ++j) c += __syncthreads_count(z[j]);
+    if (tid == 0) *kept = c;
   }
   __syncthreads();
+  // scatter (the zero fill above is ordered before these writes by the barrier)
 #pragma unroll
   for (int j = 0; j < FS_PER; ++j) {
     if (kk[j] < 0) continue;
-    const int64_t b = (int64_t)tid * FS_PER + j;
-    p2[leaf_off + kk[j]] = vv[j];
-    if (slot) slot[kk[j]] = (int32_t)b;
-    if (kk[j] / G == kk[j] % G) dslot[kk[j] / G] = (int32_t)b;
+    const int64_t b = (int64_t)tid * FS_PER + j, k = kk[j];
+    p2[leaf_off + k] = vv[j];
+    norms2[leaf_off + k] = vv[j];
+    norms[leaf_off + k] = n1 ? v1[j] : __dsqrt_rn(vv[j]);
+    if (slot) slot[k] = (int32_t)b;
+    if ((k >> depth) == (k & (G - 1))) dslot[k >> depth] = (int32_t)b;
   }
   __syncthreads();
-#pragma unroll
-  for (int j = 0; j < FS_PER; ++j) {
-    const int64_t p = (int64_t)tid * FS_PER + j;
-    if (p < npos) {
-      const double v = p2[leaf_off + p];
-      norms2[leaf_off + p] = v;
-      norms[leaf_off + p] = __dsqrt_rn(v);
-    }
-  }
   for (int t = depth - 1; t >= 0; --t) {
-    const int64_t w = int64_t(1) << t, W = 2 * w, n = w * w;
+    const int w = 1 << t, W = 2 * w, n = w * w;
     const int64_t co = tier_offset(t + 1), po = tier_offset(t);
-    for (int64_t idx = tid; idx < n; idx += FS_THREADS) {
-      const int64_t i = idx / w, j = idx % w;
+    for (int idx = tid; idx < n; idx += FS_THREADS) {
+      const int i = idx >> t, j = idx & (w - 1);
       const double* r0 = p2 + co + (2 * i) * W + 2 * j;
       const double* r1 = r0 + W;
       // root (t = 0): numpy coalesces the 2x2 into one run of 4 -> sequential
@@ -365,20 +360,21 @@ __global__ void __launch_bounds__(FS_THREADS)
     for (int64_t i = tid; i < tier_offset(top_t + 1); i += FS_THREADS) host_top[i] = __dsqrt_rn(p2[i]);
   }
   if (tr_out) {
-    const int warp = tid >> 5, lane = tid & 31;
-    const int64_t nb2 = (int64_t)nb * nb;
-    for (int64_t b = warp; b < G; b += FS_THREADS / 32) {
+    // stage the diagonals of the G diagonal blocks in the (consumed) leaf
+    // region, then one thread per block sums its diagonal in order
+    double* dg = p2 + leaf_off;
+    const int64_t nb2 = (int64_t)nb * nb, nd = G * nb;
+    for (int64_t q = tid; q < nd; q += FS_THREADS) {
+      const int64_t b = q / nb, d = q % nb;
       const int32_t sl = dslot[b];
-      if (sl < 0) continue;
-      const double* x = data + (int64_t)sl * nb2;
+      dg[q] = sl >= 0 ? data[(int64_t)sl * nb2 + d * nb + d] : 0.0;
+    }
+    __syncthreads();
+    if (tid < G && dslot[tid] >= 0) {
+      const double* x = dg + (int64_t)tid * nb;
       double acc = 0.0;
-      for (int d0 = 0; d0 < nb; d0 += 32) {
-        const int d = d0 + lane;
-        const double v = d < nb ? x[(int64_t)d * nb + d] : 0.0;
-        const int cnt = min(32, nb - d0);
-        for (int i = 0; i < cnt; ++i) acc = __dadd_rn(acc, __shfl_sync(0xffffffffu, v, i));
-      }
-      if (lane == 0) part[b] = acc;
+      for (int d = 0; d < nb; ++d) acc = __dadd_rn(acc, x[d]);
+      part[tid] = acc;
     }
     __syncthreads();
     if (tid == 0) {
@@ -392,7 +388,7 @@ __global__ void __launch_bounds__(FS_THREADS)
     // D = add_scaled(1, C, -1, X): leaf norm^2 = dn2 at C's blocks, X's own
     // leaf norm^2 where only X has a block ((-x)^2 == x^2), 0 elsewhere; the
     // same tier sums, root norm out.
-    __syncthreads();  // p2 (C's pyramid) and slot complete
+    __syncthreads();  // p2 (C's pyramid, trace staging) and slot complete
 #pragma unroll
     for (int j = 0; j < FS_PER; ++j) {
       const int64_t p = (int64_t)tid * FS_PER + j;
@@ -403,10 +399,10 @@ __global__ void __launch_bounds__(FS_THREADS)
     }
     __syncthreads();
     for (int t = depth - 1; t >= 0; --t) {
-      const int64_t w = int64_t(1) << t, W = 2 * w, n = w * w;
+      const int w = 1 << t, W = 2 * w, n = w * w;
       const int64_t co = tier_offset(t + 1), po = tier_offset(t);
-      for (int64_t idx = tid; idx < n; idx += FS_THREADS) {
-        const int64_t i = idx / w, j = idx % w;
+      for (int idx = tid; idx < n; idx += FS_THREADS) {
+        const int i = idx >> t, j = idx & (w - 1);
         const double* r0 = p2 + co + (2 * i) * W + 2 * j;
         const double* r1 = r0 + W;
         p2[po + idx] = t == 0 ? __dadd_rn(__dadd_rn(__dadd_rn(r0[0], r0[1]), r1[0]), r1[1])
@@ -451,7 +447,7 @@ __global__ void k_scatter_slots(const int64_t* __restrict__ keys, int64_t m, int
 template <int NB2, int BPW, int WARPS>
 __global__ void __launch_bounds__(32 * WARPS)
     k_leaf_norms2_multi(const double* __restrict__ data, int64_t m, double* __restrict__ out,
-                        uint8_t* __restrict__ nz) {
+                        uint8_t* __restrict__ nz, double* __restrict__ out1 = nullptr) {
   constexpr int NCH = NB2 / 256;
   __shared__ __align__(16) double rows_all[WARPS][BPW * 2 * CHAIN_ROW];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -495,7 +491,9 @@ __global__ void __launch_bounds__(32 * WARPS)
       const double l1 = __shfl_sync(0xffffffffu, acc, 2 * q + 1);
       const bool any = __any_sync(0xffffffffu, (anyq >> q) & 1u);
       if (lane == 0 && b0 + q < m) {
-        out[b0 + q] = __dadd_rn(l0, l1);
+        const double v = __dadd_rn(l0, l1);
+        out[b0 + q] = v;
+        if (out1) out1[b0 + q] = __dsqrt_rn(v);
         if (nz) nz[b0 + q] = any ? 1 : 0;
       }
     }
@@ -512,7 +510,8 @@ __global__ void __launch_bounds__(32 * WARPS)
     k_leaf_norms2_cd(const double* __restrict__ data, const int64_t* __restrict__ keys,
                      int64_t m, const double* __restrict__ xdata,
                      const int32_t* __restrict__ xslot, double* __restrict__ out,
-                     uint8_t* __restrict__ nz, double* __restrict__ dout) {
+                     uint8_t* __restrict__ nz, double* __restrict__ dout,
+                     double* __restrict__ out1) {
   constexpr int NCH = NB2 / 256, BPW = 2;
   __shared__ __align__(16) double rows_all[WARPS][BPW * 4 * CHAIN_ROW];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -573,7 +572,9 @@ __global__ void __launch_bounds__(32 * WARPS)
       const double e1 = __shfl_sync(0xffffffffu, acc, 4 * q + 3);
       const bool any = __any_sync(0xffffffffu, (anyq >> q) & 1u);
       if (lane == 0 && b0 + q < m) {
-        out[b0 + q] = __dadd_rn(c0, c1);
+        const double v = __dadd_rn(c0, c1);
+        out[b0 + q] = v;
+        out1[b0 + q] = __dsqrt_rn(v);
         nz[b0 + q] = any ? 1 : 0;
         dout[b0 + q] = __dadd_rn(e0, e1);
       }
@@ -629,16 +630,18 @@ __global__ void __launch_bounds__(256)
 }
 
 void leaf_norms2(const double* data, int64_t m, int nb, double* norms2, uint8_t* nonzero,
-                 cudaStream_t s) {
+                 cudaStream_t s, double* norms1) {
   if (m <= 0) return;
   const int nb2 = nb * nb;
   if (nb2 == 1024 || nb2 == 4096) {
     constexpr int BPW = 2, WARPS = 4;
     const int grid = grid_for((m + BPW - 1) / BPW * 32, 32 * WARPS, 1LL << 20);
     if (nb2 == 1024)
-      k_leaf_norms2_multi<1024, BPW, WARPS><<<grid, 32 * WARPS, 0, s>>>(data, m, norms2, nonzero);
+      k_leaf_norms2_multi<1024, BPW, WARPS><<<grid, 32 * WARPS, 0, s>>>(data, m, norms2, nonzero,
+                                                                        norms1);
     else
-      k_leaf_norms2_multi<4096, BPW, WARPS><<<grid, 32 * WARPS, 0, s>>>(data, m, norms2, nonzero);
+      k_leaf_norms2_multi<4096, BPW, WARPS><<<grid, 32 * WARPS, 0, s>>>(data, m, norms2, nonzero,
+                                                                        norms1);
   } else {
     const int threads = 128;
     k_leaf_norms2<0><<<grid_for(m, threads, 1LL << 20), threads, 0, s>>>(data, m, nb2, norms2,
@@ -650,8 +653,9 @@ void leaf_norms2(const double* data, int64_t m, int nb, double* norms2, uint8_t*
 void build_pyramid(const int64_t* keys, const double* blk_norms2, int64_t m, int depth,
                    double* norms, double* norms2, cudaStream_t s) {
   if (depth <= SMALL_TREE_DEPTH) {
-    k_finalize_small<<<1, 1024, 0, s>>>(keys, blk_norms2, nullptr, m, depth, nullptr, nullptr,
-                                        norms, norms2, nullptr, 0, nullptr, nullptr, 0);
+    k_finalize_small<<<1, 1024, 0, s>>>(keys, blk_norms2, nullptr, nullptr, m, depth, nullptr,
+                                        nullptr, norms, norms2, nullptr, 0, nullptr, nullptr, 0,
+                                        nullptr, nullptr, nullptr);
     SPAMM_LAUNCH_CK();
     return;
   }
@@ -684,7 +688,7 @@ void scatter_slots(const int64_t* keys, int64_t m, int32_t* slot, cudaStream_t s
 }
 
 void finalize_impl(Mat& m, cudaStream_t s, double* pre_n2, uint8_t* pre_nz, bool defer,
-                   IdemFuse idem);
+                   IdemFuse idem, double* pre_n1 = nullptr);
 
 bool idem_fusable(const Mat& x) {
   return x.depth <= SMALL_TREE_DEPTH && (x.nb == 32 || x.nb == 64);
@@ -695,21 +699,25 @@ void finalize(Mat& m, cudaStream_t s, IdemFuse idem, bool defer) {
   finalize_impl(m, s, nullptr, nullptr, defer, idem);
 }
 
-void finalize(Mat& m, cudaStream_t s, double* pre_n2, uint8_t* pre_nz, bool defer) {
-  finalize_impl(m, s, pre_n2, pre_nz, defer, IdemFuse{});
+void finalize(Mat& m, cudaStream_t s, double* pre_n2, uint8_t* pre_nz, bool defer,
+              double* pre_n1) {
+  finalize_impl(m, s, pre_n2, pre_nz, defer, IdemFuse{}, pre_n1);
 }
 
 void finalize_impl(Mat& m, cudaStream_t s, double* pre_n2, uint8_t* pre_nz, bool defer,
-                   IdemFuse idem) {
+                   IdemFuse idem, double* pre_n1) {
   m.stream = s;
   const int nb2 = m.nb * m.nb;
   double* n2 = pre_n2;
   if (defer && m.depth <= SMALL_TREE_DEPTH) {
     // one launch (after K1 unless the producer already computed the norms)
     uint8_t* nz = pre_nz;
+    double* n1 = pre_n1;
     double* dn2 = nullptr;
+    const bool multi = nb2 == 1024 || nb2 == 4096;
     if (m.nblocks > 0 && !n2) {
-      n2 = dmalloc<double>(m.nblocks, s);
+      n2 = dmalloc<double>(2 * m.nblocks, s);
+      n1 = multi ? n2 + m.nblocks : nullptr;
       nz = dmalloc<uint8_t>(m.nblocks, s);
       if (idem.x) {
         dn2 = dmalloc<double>(m.nblocks, s);
@@ -717,13 +725,13 @@ void finalize_impl(Mat& m, cudaStream_t s, double* pre_n2, uint8_t* pre_nz, bool
         const int grid = grid_for((m.nblocks + 1) / 2 * 32, 32 * WARPS, 1LL << 20);
         if (nb2 == 4096)
           k_leaf_norms2_cd<4096, WARPS><<<grid, 32 * WARPS, 0, s>>>(
-              m.data, m.keys, m.nblocks, idem.x->data, idem.x->slot, n2, nz, dn2);
+              m.data, m.keys, m.nblocks, idem.x->data, idem.x->slot, n2, nz, dn2, n1);
         else
           k_leaf_norms2_cd<1024, WARPS><<<grid, 32 * WARPS, 0, s>>>(
-              m.data, m.keys, m.nblocks, idem.x->data, idem.x->slot, n2, nz, dn2);
+              m.data, m.keys, m.nblocks, idem.x->data, idem.x->slot, n2, nz, dn2, n1);
         SPAMM_LAUNCH_CK();
       } else {
-        leaf_norms2(m.data, m.nblocks, m.nb, n2, nz, s);
+        leaf_norms2(m.data, m.nblocks, m.nb, n2, nz, s, n1);
       }
     }
     m.G = int64_t(1) << m.depth;
@@ -731,30 +739,31 @@ void finalize_impl(Mat& m, cudaStream_t s, double* pre_n2, uint8_t* pre_nz, bool
     const int64_t ps = pyramid_size(m.depth);
     m.norms = dmalloc<double>(ps, s);
     m.norms2 = dmalloc<double>(ps, s);
-    int64_t* off = m.nblocks > 0 ? dmalloc<int64_t>(m.nblocks + 1, s) : nullptr;
-    const bool want_tr = m.nb >= 2;
+    int64_t* kept = m.nblocks > 0 ? dmalloc<int64_t>(1, s) : nullptr;
+    const bool want_tr = m.nb >= 2 && m.nb <= m.G;
     if (want_tr) m.tr_dev = dmalloc<double>(1, s);
     if (m.depth >= 2 && !m.host_top) {
       m.top_t = std::min(m.depth - 1, HOST_TOP_TIERS);
       top_acquire(&m.host_top, &m.top_ev);
     }
-    k_finalize_small<<<1, 1024, 0, s>>>(m.keys, n2, nz, m.nblocks, m.depth, off, m.slot, m.norms,
-                                        m.norms2, m.data, m.nb, m.tr_dev,
-                                        m.host_top, m.host_top ? m.top_t : -1, dn2,
-                                        idem.x ? idem.x->norms2 + tier_offset(m.depth) : nullptr,
-                                        idem.out);
+    k_finalize_small<<<1, 1024, 0, s>>>(
+        m.keys, n2, n1, nz, m.nblocks, m.depth, kept, m.slot, m.norms, m.norms2, m.data, m.nb,
+        m.tr_dev, m.host_top, m.host_top ? m.top_t : -1, dn2,
+        idem.x ? idem.x->norms2 + tier_offset(m.depth) : nullptr, idem.out);
     SPAMM_LAUNCH_CK();
-    dfree(dn2, s);
     if (m.host_top) SPAMM_CK(cudaEventRecord(m.top_ev, s));
-    dfree(n2, s);
+    dfree(dn2, s);
+    dfree(n2, s);  // (a locally computed n1 shares n2's allocation)
+    dfree(pre_n1, s);
     if (m.nblocks > 0) {
       m.pend_nz = nz;
-      m.pend_off = off;
+      m.pend_kept = kept;
     } else {
       dfree(nz, s);
     }
     return;
   }
+  dfree(pre_n1, s);  // (the tiered path takes sqrt per tier itself)
   if (m.nblocks > 0) {
     uint8_t* nz = pre_nz;
     if (!n2) {
@@ -818,13 +827,18 @@ void finalize_impl(Mat& m, cudaStream_t s, double* pre_n2, uint8_t* pre_nz, bool
 }
 
 const int64_t* pending_kept(const Mat& m) {
+  if (m.pend_kept) return m.pend_kept;
   return m.pend_off ? m.pend_off + m.nblocks : nullptr;
 }
 
 void settle(Mat& m, int64_t kept, cudaStream_t s) {
-  if (!m.pend_off) return;
+  if (!m.pend_nz) return;
   if (kept < m.nblocks) {
     const int nb2 = m.nb * m.nb;
+    if (!m.pend_off) {  // only the count was produced: offsets now
+      m.pend_off = dmalloc<int64_t>(m.nblocks + 1, s);
+      scan_exclusive_u8(m.pend_nz, m.nblocks, m.pend_off, s);
+    }
     double* d2 = dmalloc<double>((size_t)kept * nb2, s);
     int64_t* k2 = dmalloc<int64_t>(kept, s);
     if (kept > 0) {
@@ -846,15 +860,18 @@ void settle(Mat& m, int64_t kept, cudaStream_t s) {
   }
   dfree(m.pend_nz, s);
   dfree(m.pend_off, s);
+  dfree(m.pend_kept, s);
   m.pend_nz = nullptr;
   m.pend_off = nullptr;
+  m.pend_kept = nullptr;
 }
 
 void settle_sync(Mat& m, cudaStream_t s) {
-  if (!m.pend_off) return;
+  if (!m.pend_nz) return;
   int64_t kept = 0;
   d2h_sync(&kept, pending_kept(m), 1, s);
   settle(m, kept, s);
 }
 
 }  // namespace spamm
+

@@ -159,7 +159,7 @@ __global__ void __launch_bounds__(32 * WARPS)
                        const int32_t* __restrict__ sx, const double* __restrict__ X2,
                        const int32_t* __restrict__ sx2, double* __restrict__ E,
                        double* __restrict__ nD2, double* __restrict__ nE2,
-                       uint8_t* __restrict__ nzE) {
+                       uint8_t* __restrict__ nzE, double* __restrict__ nE1) {
   constexpr int NCH = NB2 / 256;
   __shared__ __align__(16) double rows_all[WARPS][BPW * 4 * CHAIN_ROW];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -246,7 +246,9 @@ __global__ void __launch_bounds__(32 * WARPS)
       if (lane == 0 && u0 + q < U) {
         if (IDEM) nD2[u0 + q] = __dadd_rn(d0, d1);
         if (EXPAND) {
-          nE2[u0 + q] = __dadd_rn(e0, e1);
+          const double v = __dadd_rn(e0, e1);
+          nE2[u0 + q] = v;
+          if (nE1) nE1[u0 + q] = __dsqrt_rn(v);
           nzE[u0 + q] = any ? 1 : 0;
         }
       }
@@ -257,18 +259,18 @@ __global__ void __launch_bounds__(32 * WARPS)
 template <int NB2>
 void launch_update(bool idem, bool expand, const int64_t* ukeys, int64_t U, const Mat& x,
                    const Mat& x2, double* E, double* nD2, double* nE2, uint8_t* nzE,
-                   cudaStream_t s) {
+                   cudaStream_t s, double* nE1) {
   constexpr int BPW = 2, WARPS = 4;
   const int grid = grid_for((U + BPW - 1) / BPW * 32, 32 * WARPS, 1LL << 20);
   if (idem && expand)
     k_sp2_update_multi<NB2, true, true, BPW, WARPS><<<grid, 32 * WARPS, 0, s>>>(
-        ukeys, U, x.data, x.slot, x2.data, x2.slot, E, nD2, nE2, nzE);
+        ukeys, U, x.data, x.slot, x2.data, x2.slot, E, nD2, nE2, nzE, nE1);
   else if (idem)
     k_sp2_update_multi<NB2, true, false, BPW, WARPS><<<grid, 32 * WARPS, 0, s>>>(
-        ukeys, U, x.data, x.slot, x2.data, x2.slot, E, nD2, nE2, nzE);
+        ukeys, U, x.data, x.slot, x2.data, x2.slot, E, nD2, nE2, nzE, nE1);
   else
     k_sp2_update_multi<NB2, false, true, BPW, WARPS><<<grid, 32 * WARPS, 0, s>>>(
-        ukeys, U, x.data, x.slot, x2.data, x2.slot, E, nD2, nE2, nzE);
+        ukeys, U, x.data, x.slot, x2.data, x2.slot, E, nD2, nE2, nzE, nE1);
   SPAMM_LAUNCH_CK();
 }
 
@@ -339,13 +341,14 @@ void sp2_update_finish(const Mat& x, const Mat& x2, UnionPrep& prep, int64_t U, 
   }
   double* nD2 = want_idem ? dmalloc<double>(U, s) : nullptr;
   double* nE2 = expand ? dmalloc<double>(U, s) : nullptr;
+  double* nE1 = expand ? dmalloc<double>(U, s) : nullptr;
   uint8_t* nzE = expand ? dmalloc<uint8_t>(U, s) : nullptr;
   double* E = expand ? dmalloc<double>((size_t)U * nb2, s) : nullptr;
   if (U > 0) {
     if (nb2 == 4096)
-      launch_update<4096>(want_idem, expand, ukeys, U, x, x2, E, nD2, nE2, nzE, s);
+      launch_update<4096>(want_idem, expand, ukeys, U, x, x2, E, nD2, nE2, nzE, s, nE1);
     else
-      launch_update<1024>(want_idem, expand, ukeys, U, x, x2, E, nD2, nE2, nzE, s);
+      launch_update<1024>(want_idem, expand, ukeys, U, x, x2, E, nD2, nE2, nzE, s, nE1);
   }
   double* pn = nullptr;
   if (want_idem) {
@@ -363,7 +366,7 @@ void sp2_update_finish(const Mat& x, const Mat& x2, UnionPrep& prep, int64_t U, 
     e.nblocks = U;
     e.data = E;
     e.keys = ukeys;
-    finalize(e, s, nE2, nzE, /*defer=*/true);
+    finalize(e, s, nE2, nzE, /*defer=*/true, nE1);
     e.sym = x.sym && x2.sym;
   } else {
     dfree(ukeys, s);
