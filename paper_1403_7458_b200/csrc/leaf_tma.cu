@@ -20,6 +20,9 @@
 
 #include <mutex>
 
+#include <cstdlib>
+#include <cstring>
+
 #include "internal.h"
 
 namespace spamm {
@@ -359,7 +362,16 @@ void launch_tma(int64_t n_seg, const int64_t* seg, const Idx* a_idx, const Idx* 
   int* scratch = nullptr;
   const int32_t* order = lpt.order;
   int* counter = lpt.counter;
-  if (!order) {
+  static const int order_mode = [] {  // experiment switch: 1 = Morton order (no LPT)
+    const char* v = getenv("SPAMM_K4_ORDER");
+    return v && strcmp(v, "morton") == 0 ? 1 : 0;
+  }();
+  if (order_mode == 1) {
+    scratch = dmalloc<int>(1, s);
+    SPAMM_CK(cudaMemsetAsync(scratch, 0, sizeof(int), s));
+    counter = scratch;
+    order = nullptr;
+  } else if (!order) {
     // scratch: [next-block counter | length histogram (maxlen + 1 bins) | LPT order]
     const int maxlen = 4096;
     scratch = dmalloc<int>(1 + (maxlen + 1) + n_seg, s);
