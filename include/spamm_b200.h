@@ -94,6 +94,23 @@ int spamm_mat_from_blocks(int64_t n_native, int32_t block_size, int64_t chunk_si
 int spamm_mat_cluster(const double* pos, const int64_t* orig, const double* diag, int64_t n,
                       int32_t block_size, int64_t chunk_size, double amp, double decay,
                       uint64_t seed, void* stream, spamm_mat** out);
+/* Morton shard of the config-5 generator: only blocks whose Morton position
+ * lies in [lo, hi) are built (multi-GPU: each rank builds what it owns).  The
+ * shard's pyramid covers its own blocks until spamm_mat_set_pyramid installs
+ * the global one; the symmetric flag is off until then. */
+int spamm_mat_cluster_range(const double* pos, const int64_t* orig, const double* diag,
+                            int64_t n, int32_t block_size, int64_t chunk_size, double amp,
+                            double decay, uint64_t seed, int64_t lo, int64_t hi, void* stream,
+                            spamm_mat** out);
+/* Leaf tier of the norm^2 pyramid (device double[G*G], row-major bi*G+bj,
+ * 0 where no block) -- the per-shard contribution to the global pyramid. */
+int spamm_mat_leaf_norms2(const spamm_mat* m, double* out, void* stream);
+/* Install the pyramid built from a full leaf tier of norm^2 (device
+ * double[G*G], e.g. the sum of every shard's leaf tier) with the same tier
+ * sums as _from_blocks (quadtree.py:188-192), and the global symmetry flag:
+ * a shard then culls exactly as the whole matrix would. */
+int spamm_mat_set_pyramid(spamm_mat* m, const double* leaf_norms2, int32_t symmetric,
+                          void* stream);
 /* identity (quadtree.py:308-323). */
 int spamm_mat_identity(int64_t n, int32_t block_size, int64_t chunk_size, void* stream,
                        spamm_mat** out);
@@ -135,6 +152,15 @@ int spamm_census(const spamm_mat* a, const spamm_mat* b, double tau, void* strea
  * the count (also when it exceeds cap; nothing is written then). */
 int spamm_tasks(const spamm_mat* a, const spamm_mat* b, double tau, int32_t* ti, int32_t* tk,
                 int32_t* tj, int64_t cap, int64_t* n_out, void* stream);
+/* Shard versions (C positions in Morton range [lo, hi), the symmetric rule of
+ * spamm_multiply_range): counters, optional per-C-block task counts (device
+ * int32[G*G] zeroed by the caller: the persistence / census load-balancing
+ * input) and the task list the shard executes (the A/B blocks it needs). */
+int spamm_census_range(const spamm_mat* a, const spamm_mat* b, double tau, int64_t lo,
+                       int64_t hi, int32_t* work, void* stream, spamm_stats* stats);
+int spamm_tasks_range(const spamm_mat* a, const spamm_mat* b, double tau, int64_t lo, int64_t hi,
+                      int32_t* ti, int32_t* tk, int32_t* tj, int64_t cap, int64_t* n_out,
+                      void* stream);
 
 /* The compiled seam _gemm_batch(a_pos, b_pos, c_pos, a_data, b_data, c_data)
  * (kernel.py:74-77): c_data[c_pos[t]] += a_data[a_pos[t]] @ b_data[b_pos[t]]

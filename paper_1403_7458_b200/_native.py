@@ -63,6 +63,11 @@ _SIGS = {
                                       ctypes.POINTER(c_vp)]),
     "spamm_mat_cluster": (c_i32, [c_vp, c_vp, c_vp, c_i64, c_i32, c_i64, c_f64, c_f64,
                                   ctypes.c_uint64, c_vp, ctypes.POINTER(c_vp)]),
+    "spamm_mat_cluster_range": (c_i32, [c_vp, c_vp, c_vp, c_i64, c_i32, c_i64, c_f64, c_f64,
+                                        ctypes.c_uint64, c_i64, c_i64, c_vp,
+                                        ctypes.POINTER(c_vp)]),
+    "spamm_mat_leaf_norms2": (c_i32, [c_vp, c_vp, c_vp]),
+    "spamm_mat_set_pyramid": (c_i32, [c_vp, c_vp, c_i32, c_vp]),
     "spamm_mat_identity": (c_i32, [c_i64, c_i32, c_i64, c_vp, ctypes.POINTER(c_vp)]),
     "spamm_mat_info_get": (c_i32, [c_vp, ctypes.POINTER(MatInfo)]),
     "spamm_mat_free": (c_i32, [c_vp]),
@@ -76,6 +81,10 @@ _SIGS = {
                                      ctypes.POINTER(c_vp), ctypes.POINTER(Stats)]),
     "spamm_reserve_pool": (c_i32, [c_i64, c_vp]),
     "spamm_tasks": (c_i32, [c_vp, c_vp, c_f64, c_vp, c_vp, c_vp, c_i64, ctypes.POINTER(c_i64), c_vp]),
+    "spamm_census_range": (c_i32, [c_vp, c_vp, c_f64, c_i64, c_i64, c_vp, c_vp,
+                                   ctypes.POINTER(Stats)]),
+    "spamm_tasks_range": (c_i32, [c_vp, c_vp, c_f64, c_i64, c_i64, c_vp, c_vp, c_vp, c_i64,
+                                  ctypes.POINTER(c_i64), c_vp]),
     "spamm_gemm_batch": (c_i32, [c_vp, c_vp, c_vp, c_i64, c_vp, c_i64, c_vp, c_i64, c_vp, c_i32, c_i32,
                                  c_vp]),
     "spamm_add_scaled": (c_i32, [c_f64, c_vp, c_f64, c_vp, c_vp, ctypes.POINTER(c_vp)]),

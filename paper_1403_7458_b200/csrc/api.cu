@@ -271,6 +271,54 @@ int spamm_mat_cluster(const double* pos, const int64_t* orig, const double* diag
   SPAMM_API_END
 }
 
+int spamm_mat_cluster_range(const double* pos, const int64_t* orig, const double* diag,
+                            int64_t n, int32_t block_size, int64_t chunk_size, double amp,
+                            double decay, uint64_t seed, int64_t lo, int64_t hi, void* stream,
+                            spamm_mat** out) {
+  if (!out || !pos || !orig || !diag) return fail(SPAMM_EINVAL, "null argument");
+  if (n < 1) return fail(SPAMM_EINVAL, "matrix must have at least one row");
+  if (!is_pow2(block_size)) return fail(SPAMM_EINVAL, "block size must be a power of two");
+  const int depth = padded_depth(n, block_size);
+  const int64_t npos = (int64_t(1) << depth) * (int64_t(1) << depth);
+  if (lo < 0 || hi < lo || hi > npos) return fail(SPAMM_EINVAL, "shard range outside [0, G*G]");
+  SPAMM_API_BEGIN
+  auto* h = new spamm_mat();
+  h->m.n_native = n;
+  h->m.nb = block_size;
+  h->m.depth = depth;
+  h->m.G = int64_t(1) << depth;
+  h->m.chunk_size = chunk_size;
+  h->m.stream = S(stream);
+  try {
+    spamm::cluster_build(pos, orig, diag, amp, decay, seed, h->m, S(stream), lo, hi);
+  } catch (...) {
+    h->m.release();
+    delete h;
+    throw;
+  }
+  *out = h;
+  SPAMM_API_END
+}
+
+int spamm_mat_leaf_norms2(const spamm_mat* m, double* out, void* stream) {
+  if (!m || !out) return fail(SPAMM_EINVAL, "null argument");
+  SPAMM_API_BEGIN
+  const int64_t g = m->m.G;
+  SPAMM_CK(cudaMemcpyAsync(out, m->m.norms2 + spamm::tier_offset(m->m.depth),
+                           g * g * sizeof(double), cudaMemcpyDeviceToDevice, S(stream)));
+  SPAMM_API_END
+}
+
+int spamm_mat_set_pyramid(spamm_mat* m, const double* leaf_norms2, int32_t symmetric,
+                          void* stream) {
+  if (!m || !leaf_norms2) return fail(SPAMM_EINVAL, "null argument");
+  SPAMM_API_BEGIN
+  spamm::settle_sync(m->m, S(stream));
+  spamm::set_leaf_pyramid(m->m, leaf_norms2, S(stream));
+  m->m.sym = symmetric != 0;
+  SPAMM_API_END
+}
+
 int spamm_mat_identity(int64_t n, int32_t block_size, int64_t chunk_size, void* stream,
                        spamm_mat** out) {
   if (!out) return fail(SPAMM_EINVAL, "null output handle");
@@ -627,6 +675,58 @@ int spamm_census(const spamm_mat* a, const spamm_mat* b, double tau, void* strea
     spamm::cull(a->m, b->m, tau, false, r, s, false);
   fill_stats(stats, tau, r, a->m.nb);
   r.release(s);
+  SPAMM_API_END
+}
+
+int spamm_census_range(const spamm_mat* a, const spamm_mat* b, double tau, int64_t lo,
+                       int64_t hi, int32_t* work, void* stream, spamm_stats* stats) {
+  if (int rc = check_conformable(a, b)) return rc;
+  if (!(tau >= 0.0) || tau == __builtin_inf())
+    return fail(SPAMM_EINVAL, "tau must be finite and >= 0, got " + std::to_string(tau));
+  if (lo < 0 || hi < lo || hi > a->m.G * a->m.G)
+    return fail(SPAMM_EINVAL, "shard range outside [0, G*G]");
+  SPAMM_API_BEGIN
+  cudaStream_t s = S(stream);
+  spamm::CullResult r;
+  if (hi > lo) {
+    const bool sym = g_sym_enabled && a == b && a->m.sym;
+    if (!sym || !spamm::cull(a->m, b->m, tau, false, r, s, true, lo, hi, work))
+      spamm::cull(a->m, b->m, tau, false, r, s, false, lo, hi, work);
+  } else {
+    r.visited.assign(a->m.depth + 1, 0);
+    r.culled.assign(a->m.depth + 1, 0);
+  }
+  fill_stats(stats, tau, r, a->m.nb);
+  r.release(s);
+  SPAMM_API_END
+}
+
+int spamm_tasks_range(const spamm_mat* a, const spamm_mat* b, double tau, int64_t lo, int64_t hi,
+                      int32_t* ti, int32_t* tk, int32_t* tj, int64_t cap, int64_t* n_out,
+                      void* stream) {
+  if (int rc = check_conformable(a, b)) return rc;
+  if (!(tau >= 0.0) || tau == __builtin_inf()) return fail(SPAMM_EINVAL, "tau must be finite and >= 0");
+  if (!n_out) return fail(SPAMM_EINVAL, "null n_out");
+  if (lo < 0 || hi < lo || hi > a->m.G * a->m.G)
+    return fail(SPAMM_EINVAL, "shard range outside [0, G*G]");
+  SPAMM_API_BEGIN
+  cudaStream_t s = S(stream);
+  *n_out = 0;
+  if (hi > lo) {
+    // the tasks spamm_multiply_range executes: upper C blocks in range on the
+    // symmetric path (mirrors come from the same accumulators), all otherwise
+    spamm::CullResult r;
+    const bool sym = g_sym_enabled && a == b && a->m.sym;
+    if (!sym || !spamm::cull(a->m, b->m, tau, true, r, s, true, lo, hi))
+      spamm::cull(a->m, b->m, tau, true, r, s, false, lo, hi);
+    *n_out = r.n_tasks;
+    if (r.n_tasks > 0 && r.n_tasks <= cap) {
+      k_expand_tasks<<<spamm::grid_for(r.n_c, 1, 148LL * 32), 128, 0, s>>>(r.ci, r.cj, r.seg, r.k,
+                                                                            r.n_c, ti, tk, tj);
+      SPAMM_LAUNCH_CK();
+    }
+    r.release(s);
+  }
   SPAMM_API_END
 }
 

@@ -139,6 +139,9 @@ __global__ void __launch_bounds__(CULL_THREADS)
       }
       if (!WRITE && lane == 0) {
         cnt4[4 * p + c] = cnt + (cnt > 0 ? (int64_t(1) << NODE_SHIFT) : 0);
+        // leaf tier: per-C-block task counts (census with work, persistence LB)
+        if (work && shift == 0 && cnt)
+          work[morton_encode((uint32_t)row, (uint32_t)col)] = (int32_t)cnt;
         if (sym && row == col && cnt) {
           atomicAdd(aux, (unsigned long long)cnt);
           atomicAdd(aux + 3, 1ull);
@@ -625,7 +628,8 @@ bool cull(const Mat& a, const Mat& b, double tau, bool want_tasks, CullResult& r
     k_cull_expand<false, false><<<cull_grid(M), CULL_THREADS, 0, s>>>(
         t1, a.norms, b.norms, tau, M, ci, cj, seg, K, cnt4, nullptr, nullptr, nullptr, nullptr,
         nullptr, nullptr, nullptr, nullptr, nullptr, 0, 0, sym ? 1 : 0,
-        reinterpret_cast<unsigned long long*>(aux), lo, hi, 2 * (depth - t1), nullptr);
+        reinterpret_cast<unsigned long long*>(aux), lo, hi, 2 * (depth - t1),
+        leaf ? work : nullptr);
     SPAMM_LAUNCH_CK();
     scan_exclusive_i64(cnt4, 4 * M, off4, s);
     SPAMM_CK(cudaMemcpyAsync(aux + 2, off4 + 4 * M, sizeof(int64_t), cudaMemcpyDeviceToDevice, s));

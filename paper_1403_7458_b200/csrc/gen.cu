@@ -43,13 +43,14 @@ __device__ __forceinline__ double det_exp(double x) {
   return ldexp(p, (int)k);
 }
 
-__global__ void k_native_flags(int depth, int64_t nbn, uint8_t* __restrict__ flags) {
+__global__ void k_native_flags(int depth, int64_t nbn, int64_t lo, int64_t hi,
+                               uint8_t* __restrict__ flags) {
   const int64_t G = int64_t(1) << depth, npos = G * G;
   for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < npos;
        p += (int64_t)gridDim.x * blockDim.x) {
     uint32_t bi, bj;
     morton_decode((uint64_t)p, bi, bj);
-    flags[p] = (bi < nbn && bj < nbn) ? 1 : 0;
+    flags[p] = (bi < nbn && bj < nbn && p >= lo && p < hi) ? 1 : 0;
   }
 }
 
@@ -118,24 +119,36 @@ __global__ void __launch_bounds__(256)
 }  // namespace
 
 void cluster_build(const double* pos, const int64_t* orig, const double* diag, double amp,
-                   double decay, uint64_t seed, Mat& m, cudaStream_t s) {
+                   double decay, uint64_t seed, Mat& m, cudaStream_t s, int64_t lo,
+                   int64_t hi) {
   const int64_t G = int64_t(1) << m.depth, npos = G * G;
   const int64_t nbn = (m.n_native + m.nb - 1) / m.nb;
+  const bool whole = lo <= 0 && (hi < 0 || hi >= npos);
+  if (hi < 0) hi = npos;
   uint8_t* flags = dmalloc<uint8_t>(npos, s);
   int64_t* off = dmalloc<int64_t>(npos + 1, s);
-  k_native_flags<<<grid_for(npos, 256), 256, 0, s>>>(m.depth, nbn, flags);
+  k_native_flags<<<grid_for(npos, 256), 256, 0, s>>>(m.depth, nbn, lo, hi, flags);
   SPAMM_LAUNCH_CK();
   scan_exclusive_u8(flags, npos, off, s);
-  m.nblocks = nbn * nbn;
+  if (whole) {
+    m.nblocks = nbn * nbn;
+  } else {
+    d2h_sync(&m.nblocks, off + npos, 1, s);
+  }
   m.data = dmalloc<double>((size_t)m.nblocks * m.nb * m.nb, s);
   m.keys = dmalloc<int64_t>(m.nblocks, s);
-  k_cluster_blocks<<<grid_for(m.nblocks, 1, 148LL * 32), 256, 8 * m.nb * sizeof(double), s>>>(
-      pos, orig, diag, m.n_native, m.nb, m.depth, flags, off, amp, decay, seed, m.data, m.keys);
-  SPAMM_LAUNCH_CK();
+  if (m.nblocks > 0) {
+    k_cluster_blocks<<<grid_for(m.nblocks, 1, 148LL * 32), 256, 8 * m.nb * sizeof(double), s>>>(
+        pos, orig, diag, m.n_native, m.nb, m.depth, flags, off, amp, decay, seed, m.data, m.keys);
+    SPAMM_LAUNCH_CK();
+  }
   dfree(flags, s);
   dfree(off, s);
   finalize(m, s);
-  m.sym = true;  // r2, s and the diagonal are exactly symmetric by construction
+  // r2, s and the diagonal are exactly symmetric by construction (a Morton
+  // shard holds part of a symmetric matrix: the caller sets the flag with the
+  // global pyramid, spamm_mat_set_pyramid)
+  m.sym = whole;
 }
 
 }  // namespace spamm

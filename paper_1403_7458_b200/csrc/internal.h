@@ -195,7 +195,12 @@ double trace(const Mat& m, cudaStream_t s);  // cached per matrix
 void trace_launch(const Mat& m, double* dev_out, cudaStream_t s);  // no host sync
 void gershgorin(const Mat& f, double* eps_min, double* eps_max, double* asym, cudaStream_t s);
 // Counter-based cluster Hamiltonian (config 5) built on the device (gen.cu).
+// Build the pyramid of m from a full leaf tier of norm^2 (G*G, row-major
+// bi*G+bj): the same tier sums as finalize, so a Morton shard given the
+// all-reduced leaf tiers of every shard culls exactly like the whole matrix.
+void set_leaf_pyramid(Mat& m, const double* leaf_norms2, cudaStream_t s);
 void cluster_build(const double* pos, const int64_t* orig, const double* diag, double amp,
-                   double decay, uint64_t seed, Mat& m, cudaStream_t s);
+                   double decay, uint64_t seed, Mat& m, cudaStream_t s,
+                   int64_t lo = 0, int64_t hi = -1);
 
 }  // namespace spamm

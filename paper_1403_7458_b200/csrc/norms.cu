@@ -681,6 +681,44 @@ void build_pyramid(const int64_t* keys, const double* blk_norms2, int64_t m, int
   }
 }
 
+namespace {
+__global__ void k_leaf_from_norms2(const double* __restrict__ in, int64_t n,
+                                   double* __restrict__ n2, double* __restrict__ n1) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double v = in[i];
+    n2[i] = v;
+    n1[i] = __dsqrt_rn(v);
+  }
+}
+}  // namespace
+
+void set_leaf_pyramid(Mat& m, const double* leaf_norms2, cudaStream_t s) {
+  const int64_t G = int64_t(1) << m.depth;
+  const int64_t off = tier_offset(m.depth);
+  k_leaf_from_norms2<<<grid_for(G * G, 256), 256, 0, s>>>(leaf_norms2, G * G, m.norms2 + off,
+                                                          m.norms + off);
+  SPAMM_LAUNCH_CK();
+  int t = m.depth - 1;
+  for (; t >= 0 && (int64_t(1) << (2 * t)) > 4096; --t) {
+    const int64_t n = int64_t(1) << (2 * t);
+    k_tier_up<<<grid_for(n, 256), 256, 0, s>>>(m.norms2 + tier_offset(t + 1),
+                                                m.norms2 + tier_offset(t), m.norms + tier_offset(t),
+                                                t);
+    SPAMM_LAUNCH_CK();
+  }
+  if (t >= 0) {
+    k_tiers_small<<<1, 1024, 0, s>>>(m.norms2, m.norms, t);
+    SPAMM_LAUNCH_CK();
+  }
+  if (m.host_top) {  // refresh the host mirror of the top tiers
+    event_wait(m.top_ev);
+    SPAMM_CK(cudaMemcpyAsync(m.host_top, m.norms, tier_offset(m.top_t + 1) * sizeof(double),
+                             cudaMemcpyDeviceToHost, s));
+    SPAMM_CK(cudaEventRecord(m.top_ev, s));
+  }
+}
+
 void scatter_slots(const int64_t* keys, int64_t m, int32_t* slot, cudaStream_t s) {
   if (m <= 0) return;
   k_scatter_slots<<<grid_for(m, 256), 256, 0, s>>>(keys, m, slot);

@@ -120,6 +120,28 @@ class QuadTreeMatrix:
         """Exactly symmetric (X == X^T bitwise); X*X then runs the symmetric path."""
         return bool(self._info.symmetric)
 
+    # -- Morton shards (multi-GPU, parallel.ShardedMultiply) ----------------
+    def leaf_norms2_device(self):
+        """(G*G,) float64 leaf tier of norm^2 (row-major bi*G+bj, 0 where no block)."""
+        import torch
+        g = self.n_blocks
+        out = torch.empty(g * g, dtype=torch.float64, device="cuda")
+        nat.check(nat.load().spamm_mat_leaf_norms2(self._h, out.data_ptr(), nat.current_stream()))
+        return out
+
+    def set_global_pyramid(self, leaf_norms2, symmetric: bool) -> None:
+        """Install the pyramid of the whole matrix (a shard then culls like it)."""
+        import torch
+        leaf = torch.as_tensor(leaf_norms2, dtype=torch.float64).to("cuda").contiguous()
+        stream = nat.current_stream()
+        nat.check(nat.load().spamm_mat_set_pyramid(self._h, leaf.data_ptr(), int(bool(symmetric)),
+                                                   stream))
+        info = nat.MatInfo()
+        nat.check(nat.load().spamm_mat_info_get(self._h, ctypes.byref(info)))
+        self._info = info
+        self._host = None
+        self._root = None
+
     def norm(self) -> float:
         """Frobenius norm (root of the pyramid)."""
         return float(self.norms_device()[0].item())

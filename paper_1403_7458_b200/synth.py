@@ -241,9 +241,12 @@ CONFIGS = {
 }
 
 
-def device_cluster(cs: ClusterSites, block_size: int, chunk_size: int | None = None):
+def device_cluster(cs: ClusterSites, block_size: int, chunk_size: int | None = None,
+                   shard: tuple | None = None):
     """Build the counter-based cluster H directly in HBM (spamm_mat_cluster);
-    bitwise equal to build_from_dense(cluster_dense_cb(cs), block_size)."""
+    bitwise equal to build_from_dense(cluster_dense_cb(cs), block_size).
+    ``shard=(lo, hi)``: only the blocks at Morton positions [lo, hi) (one
+    rank's share for parallel.ShardedMultiply; spamm_mat_cluster_range)."""
     import ctypes
 
     import torch
@@ -258,8 +261,16 @@ def device_cluster(cs: ClusterSites, block_size: int, chunk_size: int | None = N
     diag = torch.from_numpy(np.ascontiguousarray(cs.diag, dtype=np.float64)).cuda()
     stream = nat.current_stream()
     out = ctypes.c_void_p()
-    nat.check(nat.load().spamm_mat_cluster(pos.data_ptr(), orig.data_ptr(), diag.data_ptr(), n,
-                                           int(block_size), int(chunk_size), float(cs.amp),
-                                           float(cs.decay), int(cs.seed), stream,
-                                           ctypes.byref(out)))
+    lib = nat.load()
+    if shard is None:
+        nat.check(lib.spamm_mat_cluster(pos.data_ptr(), orig.data_ptr(), diag.data_ptr(), n,
+                                        int(block_size), int(chunk_size), float(cs.amp),
+                                        float(cs.decay), int(cs.seed), stream,
+                                        ctypes.byref(out)))
+    else:
+        nat.check(lib.spamm_mat_cluster_range(pos.data_ptr(), orig.data_ptr(), diag.data_ptr(),
+                                              n, int(block_size), int(chunk_size),
+                                              float(cs.amp), float(cs.decay), int(cs.seed),
+                                              int(shard[0]), int(shard[1]), stream,
+                                              ctypes.byref(out)))
     return QuadTreeMatrix(out, stream)

@@ -74,3 +74,102 @@ def test_persistence_cuts_balance_cfg4_work():
         cuts = partition_work(w, world)
         parts = [w[a:b].sum() for a, b in zip(cuts, cuts[1:])]
         assert max(parts) / (n_exec / world) < 1.05, parts
+
+
+# -- distributed operand (ShardedMultiply) device pieces -----------------------
+
+def _shard_run(full, shards, tau, sym, leaf=None):
+    """Drive DeviceEngine's shard methods for every shard in turn (one
+    process; the exchange is a direct gather from the owner's shard).
+    ``leaf``: the global leaf tier, if the shards already hold it."""
+    import torch
+    from paper_1403_7458_b200.parallel import DeviceEngine, morton_positions, partition_work
+    eng = DeviceEngine()
+    g = full.n_blocks
+    if leaf is None:
+        leaf = sum(eng.leaf_norms2(s) for s in shards)
+    for s in shards:
+        eng.set_pyramid(s, leaf, sym)
+    work, sym_ok = eng.census_work(shards[0], tau)
+    cuts = partition_work(eng.to_numpy(work), len(shards))
+    if sym and not sym_ok:           # a mirror ulp tie somewhere: every shard runs the full path
+        sym = False
+        for s in shards:
+            eng.set_pyramid(s, leaf, False)
+    out_k, out_b, leaf_total = [], [], 0
+    for r, s in enumerate(shards):
+        need = eng.needed_keys(s, tau, cuts[r], cuts[r + 1])
+        own = torch.isin(need, s.keys_device())
+        halo = need[~own]
+        blocks = []
+        for o in shards:                 # fetch each halo block from its owner
+            hit = torch.isin(halo, o.keys_device())
+            if bool(hit.any()):
+                blocks.append((halo[hit], eng.gather(o, halo[hit])))
+        hk = torch.cat([k for k, _ in blocks]) if blocks else halo
+        hb = torch.cat([b for _, b in blocks]) if blocks else torch.empty((0, 16, 16),
+                                                                          dtype=torch.float64,
+                                                                          device="cuda")
+        assert hk.numel() == halo.numel()
+        ext = eng.extend(s, hk, hb, leaf, sym)
+        c, lp, _ = eng.multiply_range(ext, tau, cuts[r], cuts[r + 1])
+        out_k.append(c.keys_device().clone())
+        out_b.append(c.blocks_device().clone())
+        leaf_total += lp
+    return torch.cat(out_k), torch.cat(out_b), leaf_total
+
+
+@pytest.mark.parametrize("nshards", [2, 3])
+def test_distributed_operand_shards_reproduce_product(nshards):
+    import torch
+    from paper_1403_7458_b200.parallel import even_cuts, morton_positions
+    from paper_1403_7458_b200.synth import water_cluster
+    h, _ = water_cluster(20, seed=6)
+    full = sp.build_from_dense(h, 16)
+    assert full.symmetric
+    tau = 1e-6
+    ref, st = sp.multiply(full, full, tau)
+    g = full.n_blocks
+    keys, blocks = full.keys_device(), full.blocks_device()
+    mk = morton_positions(keys, g)
+    own_cuts = even_cuts(g * g, nshards)
+    shards = []
+    for r in range(nshards):
+        m = (mk >= own_cuts[r]) & (mk < own_cuts[r + 1])
+        shards.append(sp.QuadTreeMatrix.from_blocks(full.n_native, 16, full.chunk_size,
+                                                    keys[m], blocks[m], full.depth))
+    ck, cb, lp = _shard_run(full, shards, tau, True)
+    assert lp == st.leaf_products
+    order = torch.argsort(ck)
+    rk = ref.keys_device()
+    rorder = torch.argsort(rk)
+    assert torch.equal(ck[order], rk[rorder])
+    assert torch.equal(cb[order], ref.blocks_device()[rorder])    # bitwise: same K4 per block
+
+
+def test_cluster_shards_match_whole_matrix():
+    import torch
+    from paper_1403_7458_b200.parallel import even_cuts
+    from paper_1403_7458_b200.synth import cluster_sites, device_cluster
+    cs = cluster_sites(64, seed=3)
+    whole = device_cluster(cs, 16)
+    g = whole.n_blocks
+    cuts = even_cuts(g * g, 3)
+    shards = [device_cluster(cs, 16, shard=(cuts[r], cuts[r + 1])) for r in range(3)]
+    assert sum(s.stored_leaf_count for s in shards) == whole.stored_leaf_count
+    assert not any(s.symmetric for s in shards)           # until the global pyramid is set
+    k = torch.cat([s.keys_device() for s in shards])
+    b = torch.cat([s.blocks_device() for s in shards])
+    wk = whole.keys_device()
+    assert torch.equal(k, wk) and torch.equal(b, whole.blocks_device())   # Morton order kept
+    leaf = sum(s.leaf_norms2_device() for s in shards)
+    assert torch.equal(leaf, whole.leaf_norms2_device())
+    for s in shards:
+        s.set_global_pyramid(leaf, True)
+        assert s.symmetric
+        assert torch.equal(s.norms_device(), whole.norms_device())
+    ck, cb, lp = _shard_run(whole, shards, 1e-5, True, leaf=leaf)
+    ref, st = sp.multiply(whole, whole, 1e-5)
+    assert lp == st.leaf_products
+    o, ro = torch.argsort(ck), torch.argsort(ref.keys_device())
+    assert torch.equal(cb[o], ref.blocks_device()[ro])
