@@ -495,7 +495,8 @@ void multiply_impl(const spamm_mat* a, const spamm_mat* b, double tau, int32_t k
 // branch rule, then the fused K6 pass.  *e receives 2X - X2 on EXPAND.
 void sp2_finish(const spamm_mat* x, const spamm_mat* c, double n_occ, bool want_idem,
                 cudaStream_t s, bool* square_out, double* t_x, double* t_sq, double* idem,
-                spamm_mat** e_out, const double* idem_dev = nullptr) {
+                spamm_mat** e_out, const double* idem_dev = nullptr,
+                spamm::IdemFuse* fused_union = nullptr) {
   const bool fused = spamm::sp2_fused_supported(x->m.nb);
   // One host sync (one gather launch) for tr(X), tr(X^2), the union size of
   // the update and X^2's kept-block count.  Traces computed by the small-tree
@@ -510,7 +511,12 @@ void sp2_finish(const spamm_mat* x, const spamm_mat* c, double n_occ, bool want_
   if (!x->m.tr_valid) src[0] = trace_src(x->m, sc);
   src[1] = trace_src(c->m, sc + 1);
   spamm::UnionPrep prep;
-  if (fused) {
+  if (fused && fused_union && fused_union->ukeys) {  // built by X^2's finalisation
+    prep.npos = x->m.G * x->m.G;
+    prep.keys = fused_union->ukeys;
+    fused_union->ukeys = nullptr;  // ownership moves to the update
+    src[2] = fused_union->ucount;
+  } else if (fused) {
     prep = spamm::sp2_union_prepare(x->m, c->m, sc + 2, s);
     src[2] = sc + 2;
   }
@@ -573,14 +579,17 @@ int spamm_sp2_step(const spamm_mat* x, double n_occ, double tau, int32_t kernel,
   spamm::IdemFuse fuse;
   if (want_idem && spamm::idem_fusable(x->m)) {
     fuse.x = &x->m;
-    fuse.out = spamm::dmalloc<double>(1, s);
+    fuse.out = spamm::dmalloc<double>(2, s);
+    fuse.ucount = reinterpret_cast<int64_t*>(fuse.out + 1);
+    fuse.ukeys = spamm::dmalloc<int64_t>(x->m.G * x->m.G, s);
   }
   multiply_impl(x, x, tau, kernel, timed != 0, s, c->m, stats, 0, -1, nullptr, true, fuse);
   spamm_mat* e = nullptr;
   bool square = true;
   double tx = 0, tsq = 0;
-  sp2_finish(x, c, n_occ, want_idem != 0, s, &square, &tx, &tsq, idem, &e, fuse.out);
+  sp2_finish(x, c, n_occ, want_idem != 0, s, &square, &tx, &tsq, idem, &e, fuse.out, &fuse);
   spamm::dfree(fuse.out, s);
+  spamm::dfree(fuse.ukeys, s);
   if (e) {
     c->m.release();
     delete c;
@@ -879,7 +888,7 @@ int spamm_sp2_solve(const spamm_mat* f, double n_occ, double tau, int32_t max_it
   int n_tr = 0;
   rep->trace_history[n_tr++] = spamm::trace(x->m, s);
   bool pending_trace = false;
-  double* idem_dev = spamm::dmalloc<double>(1, s);
+  double* idem_dev = spamm::dmalloc<double>(2, s);  // [residual | union size]
   struct IdemFree {
     double* p;
     cudaStream_t s;
@@ -892,12 +901,15 @@ int spamm_sp2_solve(const spamm_mat* f, double n_occ, double tau, int32_t max_it
     if (want_idem && spamm::idem_fusable(x->m)) {
       fuse.x = &x->m;
       fuse.out = idem_dev;
+      fuse.ucount = reinterpret_cast<int64_t*>(idem_dev + 1);
+      fuse.ukeys = spamm::dmalloc<int64_t>(x->m.G * x->m.G, s);
     }
     multiply_impl(x, x, tau, kernel, timed != 0, s, c->m, &st, 0, -1, nullptr, true, fuse);
     bool square = true;
     double tx = 0, tsq = 0, idem = 0;
     spamm_mat* e = nullptr;
-    sp2_finish(x, c, n_occ, want_idem, s, &square, &tx, &tsq, &idem, &e, fuse.out);
+    sp2_finish(x, c, n_occ, want_idem, s, &square, &tx, &tsq, &idem, &e, fuse.out, &fuse);
+    spamm::dfree(fuse.ukeys, s);  // (null once the update took it)
     const int k = rep->n_multiplies++;
     rep->leaf_products[k] = st.leaf_products;
     rep->executed_products[k] = st.executed_products;

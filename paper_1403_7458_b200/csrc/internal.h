@@ -74,6 +74,10 @@ bool is_symmetric(const Mat& m, cudaStream_t s);
 struct IdemFuse {
   const Mat* x = nullptr;
   double* out = nullptr;
+  // optional: the key union of X and X^2 for the SP2 update (Morton order,
+  // capacity G*G) and its size, produced by the same launch
+  int64_t* ukeys = nullptr;
+  int64_t* ucount = nullptr;
 };
 bool idem_fusable(const Mat& x);
 void finalize(Mat& m, cudaStream_t s, IdemFuse idem, bool defer);

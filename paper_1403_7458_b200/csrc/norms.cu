@@ -290,7 +290,8 @@ __global__ void __launch_bounds__(FS_THREADS)
                      double* __restrict__ norms2, const double* __restrict__ data, int nb,
                      double* __restrict__ tr_out, double* host_top, int top_t,
                      const double* __restrict__ dn2, const double* __restrict__ xleaf2,
-                     double* __restrict__ idem_out) {
+                     double* __restrict__ idem_out, const int32_t* __restrict__ xslot = nullptr,
+                     int64_t* __restrict__ ukeys = nullptr, int64_t* __restrict__ ucount = nullptr) {
   __shared__ double p2[5461];  // squared pyramid, tiers 0..6
   __shared__ int32_t dslot[64];
   __shared__ double part[64];
@@ -383,6 +384,26 @@ __global__ void __launch_bounds__(FS_THREADS)
         if (dslot[b] >= 0) tot = __dadd_rn(tot, part[b]);
       *tr_out = tot;
     }
+  }
+  if (ukeys) {
+    // key union of X and this matrix (X^2) in Morton order, for the SP2 update
+    __syncthreads();  // slot complete
+    int64_t key[FS_PER];
+    int f[FS_PER];
+#pragma unroll
+    for (int j = 0; j < FS_PER; ++j) {
+      const int64_t p = (int64_t)tid * FS_PER + j;
+      uint32_t bi, bj;
+      morton_decode((uint64_t)p, bi, bj);
+      key[j] = (int64_t)bi * G + bj;
+      f[j] = p < npos && (xslot[key[j]] >= 0 || slot[key[j]] >= 0) ? 1 : 0;
+    }
+    int64_t tot = 0;
+    int64_t o = cta_exclusive_scan(f[0] + f[1] + f[2] + f[3], &tot);
+#pragma unroll
+    for (int j = 0; j < FS_PER; ++j)
+      if (f[j]) ukeys[o++] = key[j];
+    if (tid == 0) *ucount = tot;
   }
   if (idem_out) {
     // D = add_scaled(1, C, -1, X): leaf norm^2 = dn2 at C's blocks, X's own
@@ -787,7 +808,8 @@ void finalize_impl(Mat& m, cudaStream_t s, double* pre_n2, uint8_t* pre_nz, bool
     k_finalize_small<<<1, 1024, 0, s>>>(
         m.keys, n2, n1, nz, m.nblocks, m.depth, kept, m.slot, m.norms, m.norms2, m.data, m.nb,
         m.tr_dev, m.host_top, m.host_top ? m.top_t : -1, dn2,
-        idem.x ? idem.x->norms2 + tier_offset(m.depth) : nullptr, idem.out);
+        idem.x ? idem.x->norms2 + tier_offset(m.depth) : nullptr, idem.out,
+        idem.x ? idem.x->slot : nullptr, idem.ukeys, idem.ucount);
     SPAMM_LAUNCH_CK();
     if (m.host_top) SPAMM_CK(cudaEventRecord(m.top_ev, s));
     dfree(dn2, s);
