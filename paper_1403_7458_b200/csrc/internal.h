@@ -55,7 +55,7 @@ struct Mat {
   cudaStream_t stream = nullptr;
   void release();
 };
-constexpr int SMALL_TREE_DEPTH = 6;  // G*G <= 4096: single-CTA finalisation
+constexpr int SMALL_TREE_DEPTH = 7;  // G*G <= 16384: single-CTA finalisation
 constexpr int HOST_TOP_TIERS = 5;  // tiers 0..5: 1,365 norms (11 KB)
 
 // Exact-symmetry test (block (i,j) == transpose of block (j,i), bitwise).

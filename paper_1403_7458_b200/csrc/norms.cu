@@ -281,7 +281,10 @@ __global__ void k_tiers_small(double* __restrict__ norms2, double* __restrict__ 
 // pyramid is built in shared memory; each thread owns 4 consecutive blocks /
 // positions.  n1 (leaf norms, sqrt of n2) may come from the producer; any of
 // nz+kept / slot / tr_out / host_top / idem_out may be null.
-constexpr int FS_THREADS = 1024, FS_PER = 4;  // 4096 positions
+// PER = positions per thread: 4 for G*G <= 4096, 16 for depth 7 (G*G =
+// 16384; the squared pyramid then takes 175 KB of dynamic shared memory).
+constexpr int FS_THREADS = 1024;
+template <int FS_PER>
 __global__ void __launch_bounds__(FS_THREADS)
     k_finalize_small(const int64_t* __restrict__ keys, const double* __restrict__ n2,
                      const double* __restrict__ n1, const uint8_t* __restrict__ nz,
@@ -292,28 +295,17 @@ __global__ void __launch_bounds__(FS_THREADS)
                      const double* __restrict__ dn2, const double* __restrict__ xleaf2,
                      double* __restrict__ idem_out, const int32_t* __restrict__ xslot = nullptr,
                      int64_t* __restrict__ ukeys = nullptr, int64_t* __restrict__ ucount = nullptr) {
-  __shared__ double p2[5461];  // squared pyramid, tiers 0..6
-  __shared__ int32_t dslot[64];
-  __shared__ double part[64];
+  extern __shared__ __align__(16) double p2[];  // squared pyramid, tiers 0..depth
+  __shared__ int32_t dslot[128];
+  __shared__ double part[128];
   const int64_t G = int64_t(1) << depth, npos = G * G;
   const int tid = threadIdx.x;
   const int64_t leaf_off = tier_offset(depth);
-  // all loads of this thread's blocks in flight together
-  int64_t kk[FS_PER];
-  double vv[FS_PER], v1[FS_PER];
-  int z[FS_PER];
-#pragma unroll
+  // zero fill (coalesced: position j * 1024 + tid), then the kept count and
+  // the scatter of this thread's blocks (also strided by the CTA width)
+#pragma unroll 4
   for (int j = 0; j < FS_PER; ++j) {
-    const int64_t b = (int64_t)tid * FS_PER + j;
-    const bool ok = b < nblocks;
-    kk[j] = ok ? keys[b] : -1;
-    vv[j] = ok ? n2[b] : 0.0;
-    v1[j] = ok && n1 ? n1[b] : 0.0;
-    z[j] = ok && nz ? nz[b] : 0;
-  }
-#pragma unroll
-  for (int j = 0; j < FS_PER; ++j) {
-    const int64_t p = (int64_t)tid * FS_PER + j;
+    const int64_t p = (int64_t)j * FS_THREADS + tid;
     if (p < npos) {
       p2[leaf_off + p] = 0.0;
       norms2[leaf_off + p] = 0.0;
@@ -321,22 +313,27 @@ __global__ void __launch_bounds__(FS_THREADS)
       if (slot) slot[p] = -1;
     }
   }
-  if (tid < 64) dslot[tid] = -1;
+  if (tid < 128) dslot[tid] = -1;
   if (kept) {
     int c = 0;
-#pragma unroll
-    for (int j = 0; j < FS_PER; ++j) c += __syncthreads_count(z[j]);
+#pragma unroll 4
+    for (int j = 0; j < FS_PER; ++j) {
+      const int64_t b = (int64_t)j * FS_THREADS + tid;
+      c += __syncthreads_count(b < nblocks && nz ? nz[b] : 0);
+    }
     if (tid == 0) *kept = c;
   }
   __syncthreads();
   // scatter (the zero fill above is ordered before these writes by the barrier)
-#pragma unroll
+#pragma unroll 4
   for (int j = 0; j < FS_PER; ++j) {
-    if (kk[j] < 0) continue;
-    const int64_t b = (int64_t)tid * FS_PER + j, k = kk[j];
-    p2[leaf_off + k] = vv[j];
-    norms2[leaf_off + k] = vv[j];
-    norms[leaf_off + k] = n1 ? v1[j] : __dsqrt_rn(vv[j]);
+    const int64_t b = (int64_t)j * FS_THREADS + tid;
+    if (b >= nblocks) continue;
+    const int64_t k = keys[b];
+    const double v = n2[b];
+    p2[leaf_off + k] = v;
+    norms2[leaf_off + k] = v;
+    norms[leaf_off + k] = n1 ? n1[b] : __dsqrt_rn(v);
     if (slot) slot[k] = (int32_t)b;
     if ((k >> depth) == (k & (G - 1))) dslot[k >> depth] = (int32_t)b;
   }
@@ -387,22 +384,27 @@ __global__ void __launch_bounds__(FS_THREADS)
   }
   if (ukeys) {
     // key union of X and this matrix (X^2) in Morton order, for the SP2 update
+    // (each thread owns FS_PER consecutive positions: count, scan, write)
     __syncthreads();  // slot complete
-    int64_t key[FS_PER];
-    int f[FS_PER];
-#pragma unroll
+    int fs = 0;
+#pragma unroll 4
     for (int j = 0; j < FS_PER; ++j) {
       const int64_t p = (int64_t)tid * FS_PER + j;
       uint32_t bi, bj;
       morton_decode((uint64_t)p, bi, bj);
-      key[j] = (int64_t)bi * G + bj;
-      f[j] = p < npos && (xslot[key[j]] >= 0 || slot[key[j]] >= 0) ? 1 : 0;
+      const int64_t key = (int64_t)bi * G + bj;
+      fs += p < npos && (xslot[key] >= 0 || slot[key] >= 0) ? 1 : 0;
     }
     int64_t tot = 0;
-    int64_t o = cta_exclusive_scan(f[0] + f[1] + f[2] + f[3], &tot);
-#pragma unroll
-    for (int j = 0; j < FS_PER; ++j)
-      if (f[j]) ukeys[o++] = key[j];
+    int64_t o = cta_exclusive_scan(fs, &tot);
+#pragma unroll 4
+    for (int j = 0; j < FS_PER; ++j) {
+      const int64_t p = (int64_t)tid * FS_PER + j;
+      uint32_t bi, bj;
+      morton_decode((uint64_t)p, bi, bj);
+      const int64_t key = (int64_t)bi * G + bj;
+      if (p < npos && (xslot[key] >= 0 || slot[key] >= 0)) ukeys[o++] = key;
+    }
     if (tid == 0) *ucount = tot;
   }
   if (idem_out) {
@@ -410,9 +412,9 @@ __global__ void __launch_bounds__(FS_THREADS)
     // leaf norm^2 where only X has a block ((-x)^2 == x^2), 0 elsewhere; the
     // same tier sums, root norm out.
     __syncthreads();  // p2 (C's pyramid, trace staging) and slot complete
-#pragma unroll
+#pragma unroll 4
     for (int j = 0; j < FS_PER; ++j) {
-      const int64_t p = (int64_t)tid * FS_PER + j;
+      const int64_t p = (int64_t)j * FS_THREADS + tid;
       if (p < npos) {
         const int32_t cs = slot[p];
         p2[leaf_off + p] = cs >= 0 ? dn2[cs] : xleaf2[p];
@@ -433,6 +435,23 @@ __global__ void __launch_bounds__(FS_THREADS)
     }
     if (tid == 0) *idem_out = __dsqrt_rn(p2[0]);
   }
+}
+
+template <class... Args>
+void launch_finalize_small(int depth, cudaStream_t s, Args... args) {
+  const size_t smem = (size_t)pyramid_size(depth) * sizeof(double);
+  if (depth <= 6) {
+    k_finalize_small<4><<<1, FS_THREADS, smem, s>>>(args...);
+  } else {
+    static std::once_flag once;
+    std::call_once(once, [] {
+      SPAMM_CK(cudaFuncSetAttribute(k_finalize_small<16>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)(pyramid_size(7) * sizeof(double))));
+    });
+    k_finalize_small<16><<<1, FS_THREADS, smem, s>>>(args...);
+  }
+  SPAMM_LAUNCH_CK();
 }
 
 // Gather the kept blocks (nz[b] = 1) to their compacted positions.
@@ -674,10 +693,12 @@ void leaf_norms2(const double* data, int64_t m, int nb, double* norms2, uint8_t*
 void build_pyramid(const int64_t* keys, const double* blk_norms2, int64_t m, int depth,
                    double* norms, double* norms2, cudaStream_t s) {
   if (depth <= SMALL_TREE_DEPTH) {
-    k_finalize_small<<<1, 1024, 0, s>>>(keys, blk_norms2, nullptr, nullptr, m, depth, nullptr,
-                                        nullptr, norms, norms2, nullptr, 0, nullptr, nullptr, 0,
-                                        nullptr, nullptr, nullptr);
-    SPAMM_LAUNCH_CK();
+    launch_finalize_small(depth, s, keys, blk_norms2, (const double*)nullptr,
+                          (const uint8_t*)nullptr, m, depth, (int64_t*)nullptr,
+                          (int32_t*)nullptr, norms, norms2, (const double*)nullptr, 0,
+                          (double*)nullptr, (double*)nullptr, 0, (const double*)nullptr,
+                          (const double*)nullptr, (double*)nullptr, (const int32_t*)nullptr,
+                          (int64_t*)nullptr, (int64_t*)nullptr);
     return;
   }
   const int64_t G = int64_t(1) << depth;
@@ -805,12 +826,14 @@ void finalize_impl(Mat& m, cudaStream_t s, double* pre_n2, uint8_t* pre_nz, bool
       m.top_t = std::min(m.depth - 1, HOST_TOP_TIERS);
       top_acquire(&m.host_top, &m.top_ev);
     }
-    k_finalize_small<<<1, 1024, 0, s>>>(
-        m.keys, n2, n1, nz, m.nblocks, m.depth, kept, m.slot, m.norms, m.norms2, m.data, m.nb,
-        m.tr_dev, m.host_top, m.host_top ? m.top_t : -1, dn2,
-        idem.x ? idem.x->norms2 + tier_offset(m.depth) : nullptr, idem.out,
-        idem.x ? idem.x->slot : nullptr, idem.ukeys, idem.ucount);
-    SPAMM_LAUNCH_CK();
+    launch_finalize_small(
+        m.depth, s, (const int64_t*)m.keys, (const double*)n2, (const double*)n1,
+        (const uint8_t*)nz, m.nblocks, m.depth, kept, m.slot, m.norms, m.norms2,
+        (const double*)m.data, m.nb, m.tr_dev, m.host_top, m.host_top ? m.top_t : -1,
+        (const double*)dn2,
+        idem.x ? (const double*)(idem.x->norms2 + tier_offset(m.depth)) : (const double*)nullptr,
+        idem.out, idem.x ? (const int32_t*)idem.x->slot : (const int32_t*)nullptr, idem.ukeys,
+        idem.ucount);
     if (m.host_top) SPAMM_CK(cudaEventRecord(m.top_ev, s));
     dfree(dn2, s);
     dfree(n2, s);  // (a locally computed n1 shares n2's allocation)

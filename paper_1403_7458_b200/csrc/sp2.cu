@@ -42,34 +42,34 @@ __global__ void k_union_compact(const uint8_t* __restrict__ flags, const int64_t
   }
 }
 
-// Small trees (G*G <= 4096): union flags, scan and compaction in one CTA
-// (1024 threads x 4 consecutive Morton positions, all slot loads in flight).
+// Small trees (G*G <= 16384): union flags, scan and compaction in one CTA
+// (1024 threads x PER consecutive Morton positions, all slot loads in flight).
+template <int PER>
 __global__ void __launch_bounds__(1024)
     k_union_small(const int32_t* __restrict__ sa, const int32_t* __restrict__ sb, int depth,
                   int64_t* __restrict__ keys, int64_t* __restrict__ count) {
   const int64_t G = int64_t(1) << depth, npos = G * G;
-  int64_t key[4];
-  int f[4];
+  int64_t key[PER];
+  int f[PER];
 #pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const int64_t p = (int64_t)threadIdx.x * 4 + j;
+  for (int j = 0; j < PER; ++j) {
+    const int64_t p = (int64_t)threadIdx.x * PER + j;
     uint32_t bi, bj;
     morton_decode((uint64_t)p, bi, bj);
     key[j] = (int64_t)bi * G + bj;
   }
-  int32_t va[4], vb[4];
+  int fs = 0;
 #pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const bool ok = (int64_t)threadIdx.x * 4 + j < npos;
-    va[j] = ok ? sa[key[j]] : -1;
-    vb[j] = ok ? sb[key[j]] : -1;
+  for (int j = 0; j < PER; ++j) {
+    const bool ok = (int64_t)threadIdx.x * PER + j < npos;
+    const int32_t va = ok ? sa[key[j]] : -1, vb = ok ? sb[key[j]] : -1;
+    f[j] = (va >= 0) | (vb >= 0);
+    fs += f[j];
   }
-#pragma unroll
-  for (int j = 0; j < 4; ++j) f[j] = (va[j] >= 0) | (vb[j] >= 0);
   int64_t tot = 0;
-  int64_t o = cta_exclusive_scan(f[0] + f[1] + f[2] + f[3], &tot);
+  int64_t o = cta_exclusive_scan(fs, &tot);
 #pragma unroll
-  for (int j = 0; j < 4; ++j)
+  for (int j = 0; j < PER; ++j)
     if (f[j]) keys[o++] = key[j];
   if (threadIdx.x == 0) *count = tot;
 }
@@ -308,7 +308,10 @@ UnionPrep sp2_union_prepare(const Mat& x, const Mat& x2, int64_t* u_dev, cudaStr
   p.npos = x.G * x.G;
   if (x.depth <= SMALL_TREE_DEPTH) {
     p.keys = dmalloc<int64_t>(p.npos, s);
-    k_union_small<<<1, 1024, 0, s>>>(x.slot, x2.slot, x.depth, p.keys, u_dev);
+    if (x.depth <= 6)
+      k_union_small<4><<<1, 1024, 0, s>>>(x.slot, x2.slot, x.depth, p.keys, u_dev);
+    else
+      k_union_small<16><<<1, 1024, 0, s>>>(x.slot, x2.slot, x.depth, p.keys, u_dev);
     SPAMM_LAUNCH_CK();
     return p;
   }
