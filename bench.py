@@ -276,8 +276,11 @@ def run_ours(args):
                            "leaf_flops_executed_per_step of them and mirrors the rest "
                            "(bitwise identical C)"),
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                         "frac": achieved / peak, "traffic": ncu_traffic(),
-                         "kernel": "k_leaf_dmma_tma<64,2,4,3> (K4 leaf products)",
+                         "frac": achieved / peak,
+                         "traffic": ncu_traffic() if args.config == 4 else None,
+                         "kernel": ("k_leaf_dmma_tma<64,2,4,3> (K4 leaf products)"
+                                    if cfg.block_size == 64 else
+                                    "k_leaf_dmma_tma<32,2,2,6> (K4 leaf products)"),
                          "peak_source": peak_src,
                          "algorithmic": roof_note},
             "e2e": {"value": e2e_flops_all / (e2e_max * 1e-3) / 1e9, "unit": UNIT,

@@ -273,17 +273,41 @@ __global__ void k_tiers_small(double* __restrict__ norms2, double* __restrict__ 
   }
 }
 
-// Single-CTA finalisation for small trees (G*G <= 4096, nblocks <= 4096):
-// the kept-block count, slot map, leaf tier, upper tiers (same sums as
-// k_tier_up / k_tiers_small), the trace (same order as k_trace_blocks +
-// k_trace, Nb >= 2), the pinned host mirror of the top tiers and optionally
-// the idempotency residual root, in one launch instead of ~9.  The squared
-// pyramid is built in shared memory; each thread owns 4 consecutive blocks /
-// positions.  n1 (leaf norms, sqrt of n2) may come from the producer; any of
-// nz+kept / slot / tr_out / host_top / idem_out may be null.
-// PER = positions per thread: 4 for G*G <= 4096, 16 for depth 7 (G*G =
-// 16384; the squared pyramid then takes 175 KB of dynamic shared memory).
+// Finalisation for small trees (G*G <= 16384): the kept-block count, slot
+// map, leaf tier, upper tiers (same sums as k_tier_up / k_tiers_small), the
+// trace (same order as k_trace_blocks + k_trace, Nb >= 2), the pinned host
+// mirror of the top tiers and, for X^2 in SP2, the idempotency residual root
+// and the key union with X -- one launch of three independent CTAs instead of
+// ~12 small launches:
+//   CTA 0: slot map, leaf tier and pyramid (squared pyramid in shared
+//          memory), kept count, host mirror;
+//   CTA 1: the D = X^2 - X pyramid (X's leaf norm^2 everywhere, overwritten
+//          by the fused D chains at X^2's blocks) -> root norm;
+//   CTA 2: trace (diagonal blocks found from the keys) and the key union
+//          (X^2's blocks flagged from its keys, X's from its slot map).
+// Each thread owns FS_PER positions / blocks.  Any output may be null.
 constexpr int FS_THREADS = 1024;
+
+__device__ __forceinline__ void fs_tiers(double* p2, double* norms, double* norms2, int depth) {
+  const int tid = threadIdx.x;
+  for (int t = depth - 1; t >= 0; --t) {
+    const int w = 1 << t, W = 2 * w, n = w * w;
+    const int64_t co = tier_offset(t + 1), po = tier_offset(t);
+    for (int idx = tid; idx < n; idx += FS_THREADS) {
+      const int i = idx >> t, j = idx & (w - 1);
+      const double* r0 = p2 + co + (2 * i) * W + 2 * j;
+      const double* r1 = r0 + W;
+      // root (t = 0): numpy coalesces the 2x2 into one run of 4 -> sequential
+      const double sm = t == 0 ? __dadd_rn(__dadd_rn(__dadd_rn(r0[0], r0[1]), r1[0]), r1[1])
+                               : __dadd_rn(__dadd_rn(r0[0], r0[1]), __dadd_rn(r1[0], r1[1]));
+      p2[po + idx] = sm;
+      if (norms2) norms2[po + idx] = sm;
+      if (norms) norms[po + idx] = __dsqrt_rn(sm);
+    }
+    __syncthreads();
+  }
+}
+
 template <int FS_PER>
 __global__ void __launch_bounds__(FS_THREADS)
     k_finalize_small(const int64_t* __restrict__ keys, const double* __restrict__ n2,
@@ -301,155 +325,153 @@ __global__ void __launch_bounds__(FS_THREADS)
   const int64_t G = int64_t(1) << depth, npos = G * G;
   const int tid = threadIdx.x;
   const int64_t leaf_off = tier_offset(depth);
-  // zero fill (coalesced: position j * 1024 + tid), then the kept count and
-  // the scatter of this thread's blocks (also strided by the CTA width)
-#pragma unroll 4
-  for (int j = 0; j < FS_PER; ++j) {
-    const int64_t p = (int64_t)j * FS_THREADS + tid;
-    if (p < npos) {
-      p2[leaf_off + p] = 0.0;
-      norms2[leaf_off + p] = 0.0;
-      norms[leaf_off + p] = 0.0;
-      if (slot) slot[p] = -1;
-    }
-  }
-  if (tid < 128) dslot[tid] = -1;
-  if (kept) {
-    int c = 0;
-#pragma unroll 4
-    for (int j = 0; j < FS_PER; ++j) {
-      const int64_t b = (int64_t)j * FS_THREADS + tid;
-      c += __syncthreads_count(b < nblocks && nz ? nz[b] : 0);
-    }
-    if (tid == 0) *kept = c;
-  }
-  __syncthreads();
-  // scatter (the zero fill above is ordered before these writes by the barrier)
-#pragma unroll 4
-  for (int j = 0; j < FS_PER; ++j) {
-    const int64_t b = (int64_t)j * FS_THREADS + tid;
-    if (b >= nblocks) continue;
-    const int64_t k = keys[b];
-    const double v = n2[b];
-    p2[leaf_off + k] = v;
-    norms2[leaf_off + k] = v;
-    norms[leaf_off + k] = n1 ? n1[b] : __dsqrt_rn(v);
-    if (slot) slot[k] = (int32_t)b;
-    if ((k >> depth) == (k & (G - 1))) dslot[k >> depth] = (int32_t)b;
-  }
-  __syncthreads();
-  for (int t = depth - 1; t >= 0; --t) {
-    const int w = 1 << t, W = 2 * w, n = w * w;
-    const int64_t co = tier_offset(t + 1), po = tier_offset(t);
-    for (int idx = tid; idx < n; idx += FS_THREADS) {
-      const int i = idx >> t, j = idx & (w - 1);
-      const double* r0 = p2 + co + (2 * i) * W + 2 * j;
-      const double* r1 = r0 + W;
-      // root (t = 0): numpy coalesces the 2x2 into one run of 4 -> sequential
-      const double sm = t == 0 ? __dadd_rn(__dadd_rn(__dadd_rn(r0[0], r0[1]), r1[0]), r1[1])
-                               : __dadd_rn(__dadd_rn(r0[0], r0[1]), __dadd_rn(r1[0], r1[1]));
-      p2[po + idx] = sm;
-      norms2[po + idx] = sm;
-      norms[po + idx] = __dsqrt_rn(sm);
-    }
-    __syncthreads();
-  }
-  if (host_top) {
-    for (int64_t i = tid; i < tier_offset(top_t + 1); i += FS_THREADS) host_top[i] = __dsqrt_rn(p2[i]);
-  }
-  if (tr_out) {
-    // stage the diagonals of the G diagonal blocks in the (consumed) leaf
-    // region, then one thread per block sums its diagonal in order
-    double* dg = p2 + leaf_off;
-    const int64_t nb2 = (int64_t)nb * nb, nd = G * nb;
-    for (int64_t q = tid; q < nd; q += FS_THREADS) {
-      const int64_t b = q / nb, d = q % nb;
-      const int32_t sl = dslot[b];
-      dg[q] = sl >= 0 ? data[(int64_t)sl * nb2 + d * nb + d] : 0.0;
-    }
-    __syncthreads();
-    if (tid < G && dslot[tid] >= 0) {
-      const double* x = dg + (int64_t)tid * nb;
-      double acc = 0.0;
-      for (int d = 0; d < nb; ++d) acc = __dadd_rn(acc, x[d]);
-      part[tid] = acc;
-    }
-    __syncthreads();
-    if (tid == 0) {
-      double tot = 0.0;
-      for (int64_t b = 0; b < G; ++b)
-        if (dslot[b] >= 0) tot = __dadd_rn(tot, part[b]);
-      *tr_out = tot;
-    }
-  }
-  if (ukeys) {
-    // key union of X and this matrix (X^2) in Morton order, for the SP2 update
-    // (each thread owns FS_PER consecutive positions: count, scan, write)
-    __syncthreads();  // slot complete
-    int fs = 0;
-#pragma unroll 4
-    for (int j = 0; j < FS_PER; ++j) {
-      const int64_t p = (int64_t)tid * FS_PER + j;
-      uint32_t bi, bj;
-      morton_decode((uint64_t)p, bi, bj);
-      const int64_t key = (int64_t)bi * G + bj;
-      fs += p < npos && (xslot[key] >= 0 || slot[key] >= 0) ? 1 : 0;
-    }
-    int64_t tot = 0;
-    int64_t o = cta_exclusive_scan(fs, &tot);
-#pragma unroll 4
-    for (int j = 0; j < FS_PER; ++j) {
-      const int64_t p = (int64_t)tid * FS_PER + j;
-      uint32_t bi, bj;
-      morton_decode((uint64_t)p, bi, bj);
-      const int64_t key = (int64_t)bi * G + bj;
-      if (p < npos && (xslot[key] >= 0 || slot[key] >= 0)) ukeys[o++] = key;
-    }
-    if (tid == 0) *ucount = tot;
-  }
-  if (idem_out) {
-    // D = add_scaled(1, C, -1, X): leaf norm^2 = dn2 at C's blocks, X's own
-    // leaf norm^2 where only X has a block ((-x)^2 == x^2), 0 elsewhere; the
-    // same tier sums, root norm out.
-    __syncthreads();  // p2 (C's pyramid, trace staging) and slot complete
+
+  if (blockIdx.x == 0) {
+    // ---- slot map, leaf tier, pyramid, kept count, host mirror ----
 #pragma unroll 4
     for (int j = 0; j < FS_PER; ++j) {
       const int64_t p = (int64_t)j * FS_THREADS + tid;
       if (p < npos) {
-        const int32_t cs = slot[p];
-        p2[leaf_off + p] = cs >= 0 ? dn2[cs] : xleaf2[p];
+        p2[leaf_off + p] = 0.0;
+        norms2[leaf_off + p] = 0.0;
+        norms[leaf_off + p] = 0.0;
+        if (slot) slot[p] = -1;
+      }
+    }
+    if (kept) {
+      int c = 0;
+#pragma unroll 4
+      for (int j = 0; j < FS_PER; ++j) {
+        const int64_t b = (int64_t)j * FS_THREADS + tid;
+        c += __syncthreads_count(b < nblocks && nz ? nz[b] : 0);
+      }
+      if (tid == 0) *kept = c;
+    }
+    __syncthreads();
+    // scatter (the zero fill above is ordered before these writes by the barrier)
+#pragma unroll 4
+    for (int j = 0; j < FS_PER; ++j) {
+      const int64_t b = (int64_t)j * FS_THREADS + tid;
+      if (b >= nblocks) continue;
+      const int64_t k = keys[b];
+      const double v = n2[b];
+      p2[leaf_off + k] = v;
+      norms2[leaf_off + k] = v;
+      norms[leaf_off + k] = n1 ? n1[b] : __dsqrt_rn(v);
+      if (slot) slot[k] = (int32_t)b;
+    }
+    __syncthreads();
+    fs_tiers(p2, norms, norms2, depth);
+    if (host_top) {
+      for (int64_t i = tid; i < tier_offset(top_t + 1); i += FS_THREADS)
+        host_top[i] = __dsqrt_rn(p2[i]);
+    }
+  } else if (blockIdx.x == 1) {
+    // ---- D = add_scaled(1, X^2, -1, X): root norm ----
+    if (!idem_out) return;
+#pragma unroll 4
+    for (int j = 0; j < FS_PER; ++j) {
+      const int64_t p = (int64_t)j * FS_THREADS + tid;
+      if (p < npos) p2[leaf_off + p] = xleaf2[p];  // X-only blocks: (-x)^2 == x^2
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int j = 0; j < FS_PER; ++j) {
+      const int64_t b = (int64_t)j * FS_THREADS + tid;
+      if (b < nblocks) p2[leaf_off + keys[b]] = dn2[b];
+    }
+    __syncthreads();
+    fs_tiers(p2, nullptr, nullptr, depth);
+    if (tid == 0) *idem_out = __dsqrt_rn(p2[0]);
+  } else {
+    // ---- trace and key union ----
+    if (tid < 128) dslot[tid] = -1;
+    uint8_t* cflag = reinterpret_cast<uint8_t*>(p2 + (tr_out ? G * nb : 0));  // after the staging
+    if (ukeys) {
+#pragma unroll 4
+      for (int j = 0; j < FS_PER; ++j) {
+        const int64_t p = (int64_t)j * FS_THREADS + tid;
+        if (p < npos) cflag[p] = 0;
       }
     }
     __syncthreads();
-    for (int t = depth - 1; t >= 0; --t) {
-      const int w = 1 << t, W = 2 * w, n = w * w;
-      const int64_t co = tier_offset(t + 1), po = tier_offset(t);
-      for (int idx = tid; idx < n; idx += FS_THREADS) {
-        const int i = idx >> t, j = idx & (w - 1);
-        const double* r0 = p2 + co + (2 * i) * W + 2 * j;
-        const double* r1 = r0 + W;
-        p2[po + idx] = t == 0 ? __dadd_rn(__dadd_rn(__dadd_rn(r0[0], r0[1]), r1[0]), r1[1])
-                              : __dadd_rn(__dadd_rn(r0[0], r0[1]), __dadd_rn(r1[0], r1[1]));
+#pragma unroll 4
+    for (int j = 0; j < FS_PER; ++j) {
+      const int64_t b = (int64_t)j * FS_THREADS + tid;
+      if (b >= nblocks) continue;
+      const int64_t k = keys[b];
+      const uint32_t bi = (uint32_t)(k >> depth), bj = (uint32_t)(k & (G - 1));
+      if (bi == bj) dslot[bi] = (int32_t)b;
+      if (ukeys) cflag[morton_encode(bi, bj)] = 1;
+    }
+    __syncthreads();
+    if (tr_out) {
+      // stage the diagonals of the G diagonal blocks, then one thread per
+      // block sums its diagonal in order, thread 0 the blocks in order
+      double* dg = p2;
+      const int64_t nb2 = (int64_t)nb * nb, nd = G * nb;
+      for (int64_t q = tid; q < nd; q += FS_THREADS) {
+        const int64_t b = q / nb, d = q % nb;
+        const int32_t sl = dslot[b];
+        dg[q] = sl >= 0 ? data[(int64_t)sl * nb2 + d * nb + d] : 0.0;
       }
       __syncthreads();
+      if (tid < G && dslot[tid] >= 0) {
+        const double* x = dg + (int64_t)tid * nb;
+        double acc = 0.0;
+        for (int d = 0; d < nb; ++d) acc = __dadd_rn(acc, x[d]);
+        part[tid] = acc;
+      }
+      __syncthreads();
+      if (tid == 0) {
+        double tot = 0.0;
+        for (int64_t b = 0; b < G; ++b)
+          if (dslot[b] >= 0) tot = __dadd_rn(tot, part[b]);
+        *tr_out = tot;
+      }
     }
-    if (tid == 0) *idem_out = __dsqrt_rn(p2[0]);
+    if (ukeys) {
+      // key union of X and X^2 in Morton order (FS_PER consecutive positions
+      // per thread: count, scan, write)
+      int fs = 0;
+#pragma unroll 4
+      for (int j = 0; j < FS_PER; ++j) {
+        const int64_t p = (int64_t)tid * FS_PER + j;
+        uint32_t bi, bj;
+        morton_decode((uint64_t)p, bi, bj);
+        fs += p < npos && (cflag[p] || xslot[(int64_t)bi * G + bj] >= 0) ? 1 : 0;
+      }
+      int64_t tot = 0;
+      int64_t o = cta_exclusive_scan(fs, &tot);
+#pragma unroll 4
+      for (int j = 0; j < FS_PER; ++j) {
+        const int64_t p = (int64_t)tid * FS_PER + j;
+        uint32_t bi, bj;
+        morton_decode((uint64_t)p, bi, bj);
+        const int64_t key = (int64_t)bi * G + bj;
+        if (p < npos && (cflag[p] || xslot[key] >= 0)) ukeys[o++] = key;
+      }
+      if (tid == 0) *ucount = tot;
+    }
   }
 }
 
 template <class... Args>
-void launch_finalize_small(int depth, cudaStream_t s, Args... args) {
-  const size_t smem = (size_t)pyramid_size(depth) * sizeof(double);
-  if (depth <= 6) {
-    k_finalize_small<4><<<1, FS_THREADS, smem, s>>>(args...);
+void launch_finalize_small(int depth, int nb, cudaStream_t s, Args... args) {
+  // the larger of the squared pyramid and (diagonal staging + union flags)
+  const int64_t G = int64_t(1) << depth;
+  const size_t smem = std::max((size_t)pyramid_size(depth) * sizeof(double),
+                               (size_t)(G * nb) * sizeof(double) + (size_t)(G * G) + 64);
+  if (smem > 220 * 1024) throw CudaError("finalize: shared memory budget exceeded");
+  if (depth <= 6 && smem <= 48 * 1024) {
+    k_finalize_small<4><<<3, FS_THREADS, smem, s>>>(args...);
   } else {
     static std::once_flag once;
     std::call_once(once, [] {
       SPAMM_CK(cudaFuncSetAttribute(k_finalize_small<16>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)(pyramid_size(7) * sizeof(double))));
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     });
-    k_finalize_small<16><<<1, FS_THREADS, smem, s>>>(args...);
+    k_finalize_small<16><<<3, FS_THREADS, smem, s>>>(args...);
   }
   SPAMM_LAUNCH_CK();
 }
@@ -693,7 +715,7 @@ void leaf_norms2(const double* data, int64_t m, int nb, double* norms2, uint8_t*
 void build_pyramid(const int64_t* keys, const double* blk_norms2, int64_t m, int depth,
                    double* norms, double* norms2, cudaStream_t s) {
   if (depth <= SMALL_TREE_DEPTH) {
-    launch_finalize_small(depth, s, keys, blk_norms2, (const double*)nullptr,
+    launch_finalize_small(depth, 0, s, keys, blk_norms2, (const double*)nullptr,
                           (const uint8_t*)nullptr, m, depth, (int64_t*)nullptr,
                           (int32_t*)nullptr, norms, norms2, (const double*)nullptr, 0,
                           (double*)nullptr, (double*)nullptr, 0, (const double*)nullptr,
@@ -827,7 +849,7 @@ void finalize_impl(Mat& m, cudaStream_t s, double* pre_n2, uint8_t* pre_nz, bool
       top_acquire(&m.host_top, &m.top_ev);
     }
     launch_finalize_small(
-        m.depth, s, (const int64_t*)m.keys, (const double*)n2, (const double*)n1,
+        m.depth, m.nb, s, (const int64_t*)m.keys, (const double*)n2, (const double*)n1,
         (const uint8_t*)nz, m.nblocks, m.depth, kept, m.slot, m.norms, m.norms2,
         (const double*)m.data, m.nb, m.tr_dev, m.host_top, m.host_top ? m.top_t : -1,
         (const double*)dn2,
