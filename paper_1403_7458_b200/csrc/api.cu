@@ -5,6 +5,8 @@
 #include <string>
 
 #include "../../include/spamm_b200.h"
+#include <vector>
+
 #include "internal.h"
 
 struct spamm_mat {
@@ -894,6 +896,20 @@ int spamm_sp2_solve(const spamm_mat* f, double n_occ, double tau, int32_t max_it
     cudaStream_t s;
     ~IdemFree() { spamm::dfree(p, s); }
   } idem_free{idem_dev, s};
+  // Retired matrices are released after the next product is queued: their
+  // (stream-ordered) frees then cost host time while K4 runs, not between
+  // the branch decision and the next cull.
+  struct Graveyard {
+    std::vector<spamm_mat*> v;
+    void flush() {
+      for (auto* m : v) {
+        m->m.release();
+        delete m;
+      }
+      v.clear();
+    }
+    ~Graveyard() { flush(); }
+  } dead;
   for (int it = 0; it < max_iter; ++it) {
     auto* c = new spamm_mat();
     spamm_stats st;
@@ -905,6 +921,7 @@ int spamm_sp2_solve(const spamm_mat* f, double n_occ, double tau, int32_t max_it
       fuse.ukeys = spamm::dmalloc<int64_t>(x->m.G * x->m.G, s);
     }
     multiply_impl(x, x, tau, kernel, timed != 0, s, c->m, &st, 0, -1, nullptr, true, fuse);
+    dead.flush();
     bool square = true;
     double tx = 0, tsq = 0, idem = 0;
     spamm_mat* e = nullptr;
@@ -937,12 +954,10 @@ int spamm_sp2_solve(const spamm_mat* f, double n_occ, double tau, int32_t max_it
     }
     spamm_mat* next = c;
     if (e) {
-      c->m.release();
-      delete c;
+      dead.v.push_back(c);
       next = e;
     }
-    x->m.release();
-    delete x;
+    dead.v.push_back(x);
     x = next;
     rep->branch_history[rep->iterations] = square ? 0 : 1;
     rep->iterations += 1;
