@@ -411,3 +411,25 @@ def test_dense_cull_equals_tier_walk_and_reference(rng, case):
         assert all(np.array_equal(x, y) for x, y in zip(t_d, t_w))
         cs = sp.convolution_census(a, b, tau)
         assert cs.counts_equal(st_d)
+
+
+# -- determinism (regression: a K4 stage-refill race once corrupted ~1 block
+#    in 40 launches at Nb = 32; results must be bitwise run-to-run) -----------
+
+@pytest.mark.parametrize("cfg_index", [3, 4])
+def test_products_bitwise_repeatable(cfg_index):
+    import torch
+    cfg = CONFIGS[cfg_index]
+    h, n_occ = water_cluster(cfg.n_mol, seed=0)
+    f = sp.build_from_dense(h, cfg.block_size)
+    x = sp.sp2_init(f, sp.gershgorin_bounds(f))
+    for _ in range(6):
+        x, _ = sp.sp2_step(x, n_occ, cfg.tau)
+    ref = None
+    for _ in range(40 if cfg_index == 3 else 12):
+        c, _ = sp.multiply(x, x, cfg.tau)
+        d = c.blocks_device().clone()
+        if ref is None:
+            ref = d
+        else:
+            assert torch.equal(d, ref)
