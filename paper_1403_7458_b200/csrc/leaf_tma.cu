@@ -123,41 +123,68 @@ __global__ void __launch_bounds__(32 * (WARPS_M * WARPS_N + 1), 1)
     // ---------------- producer warp ----------------
     // Dynamic scheduling: C segments are taken from a global counter in
     // longest-first order (LPT), so the tail of the launch is one short block.
-    // (A warp-wide variant that preloaded task indices and claimed the next
-    // block ahead refilled stages sooner and exposed a rare stage WAR race --
-    // corrupted blocks in ~1 of 40 launches at cfg3; this form is clean.)
+    // The whole warp runs the loop (lane 0 issues barriers and TMA): task
+    // indices are loaded 32 at a time, coalesced, and handed out by shuffle,
+    // and the next block is claimed and its bounds loaded while the current
+    // one streams -- no global-load latency between two stages (this bound
+    // the Nb = 32 kernel, whose stages are only ~500 cycles of DMMA).
     if (lane == 0) {
       asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
       asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
-      int stage = 0;
-      uint32_t phase = 0;
-      for (;;) {
-        const int64_t i = atomicAdd(next_block, 1);
-        if (i >= n_seg) {
+    }
+    int stage = 0;
+    uint32_t phase = 0;
+    auto claim = [&](int64_t& m, int64_t& t0, int64_t& t1) -> bool {
+      int64_t i = 0;
+      if (lane == 0) i = atomicAdd(next_block, 1);
+      i = __shfl_sync(0xffffffffu, i, 0);
+      if (i >= n_seg) return false;
+      m = order ? (int64_t)order[i] : i;
+      t0 = seg[m];
+      t1 = seg[m + 1];
+      return true;
+    };
+    int64_t m = 0, t0 = 0, t1 = 0;
+    bool have = claim(m, t0, t1);
+    while (have) {
+      int64_t mn = 0, t0n = 0, t1n = 0;
+      const bool next = claim(mn, t0n, t1n);  // in flight while this block streams
+      for (int64_t c0 = t0; c0 < t1; c0 += 32) {
+        const int64_t t = c0 + lane;
+        const int ra_l = t < t1 ? (int)a_idx[t] * NB : 0;
+        const int rb_l = t < t1 ? (int)b_idx[t] * NB : 0;
+        const int cnt = t1 - c0 < 32 ? (int)(t1 - c0) : 32;
+        for (int q = 0; q < cnt; ++q) {
+          const int ra = __shfl_sync(0xffffffffu, ra_l, q);
+          const int rb = __shfl_sync(0xffffffffu, rb_l, q);
           mbar_wait(empty(stage), phase ^ 1u);
-          meta[stage] = -1;
-          mbar_arrive(full(stage));
-          break;
-        }
-        const int64_t m = order ? (int64_t)order[i] : i;
-        const int64_t t0 = seg[m], t1 = seg[m + 1];
-        for (int64_t t = t0; t < t1; ++t) {
-          mbar_wait(empty(stage), phase ^ 1u);
-          meta[stage] = (m << 2) | (t == t0 ? 1 : 0) | (t + 1 == t1 ? 2 : 0);
-          mbar_expect_tx(full(stage), Cfg::STAGE);
-          const int ra = (int)a_idx[t] * NB, rb = (int)b_idx[t] * NB;
-          const uint32_t sa = base + stage * Cfg::STAGE, sb = sa + Cfg::TILE;
+          if (lane == 0) {
+            const int64_t tq = c0 + q;
+            meta[stage] = (m << 2) | (tq == t0 ? 1 : 0) | (tq + 1 == t1 ? 2 : 0);
+            mbar_expect_tx(full(stage), Cfg::STAGE);
+            const uint32_t sa = base + stage * Cfg::STAGE, sb = sa + Cfg::TILE;
 #pragma unroll
-          for (int sl = 0; sl < NB / 16; ++sl) {
-            tma_load_2d(sa + sl * Cfg::SLAB, &tmA, full(stage), sl * 16, ra);
-            tma_load_2d(sb + sl * Cfg::SLAB, &tmB, full(stage), sl * 16, rb);
+            for (int sl = 0; sl < NB / 16; ++sl) {
+              tma_load_2d(sa + sl * Cfg::SLAB, &tmA, full(stage), sl * 16, ra);
+              tma_load_2d(sb + sl * Cfg::SLAB, &tmB, full(stage), sl * 16, rb);
+            }
           }
+          __syncwarp();
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1u;
           }
         }
       }
+      have = next;
+      m = mn;
+      t0 = t0n;
+      t1 = t1n;
+    }
+    mbar_wait(empty(stage), phase ^ 1u);
+    if (lane == 0) {
+      meta[stage] = -1;
+      mbar_arrive(full(stage));
     }
     return;
   }
@@ -178,11 +205,21 @@ __global__ void __launch_bounds__(32 * (WARPS_M * WARPS_N + 1), 1)
     for (int g = 0; g < 2; ++g)
       offB[h][g] = (uint32_t)((((h * 4 + (r8 >> 1)) ^ (g * 4 + c4)) << 4) + ((r8 & 1) << 3) + c4 * 128);
 
-  int stage = 0;
+  int stage = 0, held = -1;
   uint32_t phase = 0;
   double acc[MT][NT][2];
   for (;;) {
     mbar_wait(full(stage), phase);
+    // Stage release: the previous stage is handed back only here, after the
+    // wait loop -- every DMMA that read it was issued in the preceding basic
+    // block, and an issued DMMA has its fragments.  (Releasing right after
+    // the k-loop let the arrive be scheduled above the final DMMAs, and a fast
+    // refill could overwrite fragments still in flight.)
+    if (held >= 0) {
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty(held));
+    }
     const int64_t md = meta[stage];
     if (md < 0) break;
     const int64_t m = md >> 2;
@@ -224,11 +261,7 @@ __global__ void __launch_bounds__(32 * (WARPS_M * WARPS_N + 1), 1)
     // arrived: order this warp's generic-proxy shared loads before that
     // (a WAR hazard otherwise -- observed as rare corrupted blocks with
     // 16-KB stages and 4 CTAs/SM).
-#ifndef SPAMM_NO_PROXY_FENCE
-    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-#endif
-    __syncwarp();
-    if (lane == 0) mbar_arrive(empty(stage));
+    held = stage;
     if (++stage == STAGES) {
       stage = 0;
       phase ^= 1u;
