@@ -277,6 +277,12 @@ __global__ void __launch_bounds__(32 * (WARPS_M * WARPS_N + 1), 1)
         v.y = acc[mt][nt][1];
         *reinterpret_cast<double2*>(Cb + (row0 + mt * 8 + r8) * NB + col0 + nt * 8 + 2 * c4) = v;
       }
+    // The stores above consumed every accumulator, so every DMMA -- and every
+    // fragment read of the held stage -- is complete: hand the stage back now
+    // rather than after the mirror stores and the next wait.
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty(held));
+    held = -1;
     // Symmetric product: the mirror block C_ji = C_ij^T (bitwise what the full
     // product computes).
     const int64_t mi = c_mirror ? c_mirror[m] : -1;
