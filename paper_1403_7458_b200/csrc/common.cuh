@@ -73,28 +73,6 @@ inline int grid_for(int64_t n, int threads, int64_t cap = 148LL * 64) {
   return (int)g;
 }
 
-// One einsum lane's unfused add chain over a 256-element chunk of squares in
-// shared memory (p = chunk base + lane parity): per 8-element group the
-// order (6,4,2,0), groups ascending (numpy's einsum lanes, see norms.cu).
-// Loads are batched 32 at a time ahead of the dependent adds so the chain
-// runs at add latency instead of shared-load latency.
-__device__ __forceinline__ double einsum_lane_chain256(const double* p, double l) {
-#pragma unroll
-  for (int g0 = 0; g0 < 32; g0 += 8) {
-    double v[32];
-#pragma unroll
-    for (int g = 0; g < 8; ++g) {
-      v[4 * g + 0] = p[(g0 + g) * 8 + 6];
-      v[4 * g + 1] = p[(g0 + g) * 8 + 4];
-      v[4 * g + 2] = p[(g0 + g) * 8 + 2];
-      v[4 * g + 3] = p[(g0 + g) * 8 + 0];
-    }
-#pragma unroll
-    for (int q = 0; q < 32; ++q) l = __dadd_rn(l, v[q]);
-  }
-  return l;
-}
-
 // Multi-block chain layout: a 256-element chunk of squares is stored as two
 // parity rows (even / odd elements) permuted so each einsum lane's chain
 // reads its row sequentially: element e -> row (e & 1), position

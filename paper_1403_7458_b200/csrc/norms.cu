@@ -506,8 +506,8 @@ __global__ void k_scatter_slots(const int64_t* __restrict__ keys, int64_t m, int
 // Multi-block variant (the production path for Nb = 32 / 64): each warp
 // reduces BPW blocks at once, chains of all of them on lanes 0 .. 2 BPW - 1
 // reading the permuted parity rows (common.cuh) with LDS.128.  Same recipe and
-// bits as k_leaf_norms2; the single-block warp kernel below was bound by
-// shared-load wavefronts (one 16-byte LDS per wavefront).
+// bits as k_leaf_norms2 (an earlier one-block-per-warp form, lanes 0/1
+// chaining from LDS.64, was bound by shared-load wavefronts: L1 83 %).
 template <int NB2, int BPW, int WARPS>
 __global__ void __launch_bounds__(32 * WARPS)
     k_leaf_norms2_multi(const double* __restrict__ data, int64_t m, double* __restrict__ out,
@@ -642,53 +642,6 @@ __global__ void __launch_bounds__(32 * WARPS)
         nz[b0 + q] = any ? 1 : 0;
         dout[b0 + q] = __dadd_rn(e0, e1);
       }
-    }
-  }
-}
-
-// Warp-per-block variant for Nb^2 a multiple of 256: the warp streams the block
-// through shared memory in 256-element chunks with fully coalesced loads
-// (next chunk in flight while the current one is reduced), squares are formed
-// by all 32 lanes, and lanes 0 / 1 run the two einsum lanes' add chains (the
-// only inherently serial part).  Same recipe, same result bits as k_leaf_norms2.
-template <int NB2>
-__global__ void __launch_bounds__(256)
-    k_leaf_norms2_warp(const double* __restrict__ data, int64_t m, double* __restrict__ out,
-                       uint8_t* __restrict__ nz) {
-  constexpr int CH = 256, NCH = NB2 / CH;
-  __shared__ __align__(16) double sq[8][CH];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double* buf = sq[warp];
-  const int64_t nw = (int64_t)gridDim.x * 8;
-  for (int64_t b = (int64_t)blockIdx.x * 8 + warp; b < m; b += nw) {
-    const double2* x = reinterpret_cast<const double2*>(data + b * NB2);
-    double2 r[4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) r[k] = __ldg(x + k * 32 + lane);
-    double acc = 0.0;
-    bool any = false;
-    for (int c = 0; c < NCH; ++c) {
-      __syncwarp();
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        double2 p;
-        p.x = __dmul_rn(r[k].x, r[k].x);
-        p.y = __dmul_rn(r[k].y, r[k].y);
-        any |= (r[k].x != 0.0) | (r[k].y != 0.0);
-        *reinterpret_cast<double2*>(buf + k * 64 + 2 * lane) = p;
-      }
-      __syncwarp();
-      if (c + 1 < NCH) {
-#pragma unroll
-        for (int k = 0; k < 4; ++k) r[k] = __ldg(x + (c + 1) * (CH / 2) + k * 32 + lane);
-      }
-      if (lane < 2) acc = einsum_lane_chain256(buf + lane, acc);
-    }
-    const double l1 = __shfl_sync(0xffffffffu, acc, 1);
-    any = __any_sync(0xffffffffu, any);
-    if (lane == 0) {
-      out[b] = __dadd_rn(acc, l1);
-      if (nz) nz[b] = any ? 1 : 0;
     }
   }
 }

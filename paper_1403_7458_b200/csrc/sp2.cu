@@ -74,85 +74,11 @@ __global__ void __launch_bounds__(1024)
   if (threadIdx.x == 0) *count = tot;
 }
 
-template <int NB2, bool IDEM, bool EXPAND>
-__global__ void __launch_bounds__(256)
-    k_sp2_update(const int64_t* __restrict__ ukeys, int64_t U, const double* __restrict__ X,
-                 const int32_t* __restrict__ sx, const double* __restrict__ X2,
-                 const int32_t* __restrict__ sx2, double* __restrict__ E,
-                 double* __restrict__ nD2, double* __restrict__ nE2, uint8_t* __restrict__ nzE) {
-  constexpr int CH = 256, NCH = NB2 / CH;
-  __shared__ __align__(16) double sq[8][2][CH];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double* bd = sq[warp][0];
-  double* be = sq[warp][1];
-  const int64_t nw = (int64_t)gridDim.x * 8;
-  for (int64_t u = (int64_t)blockIdx.x * 8 + warp; u < U; u += nw) {
-    const int64_t key = ukeys[u];
-    const int32_t ix = sx[key], ix2 = sx2[key];
-    const double2* px = ix >= 0 ? reinterpret_cast<const double2*>(X + (int64_t)ix * NB2) : nullptr;
-    const double2* px2 = ix2 >= 0 ? reinterpret_cast<const double2*>(X2 + (int64_t)ix2 * NB2) : nullptr;
-    double2* pe = EXPAND ? reinterpret_cast<double2*>(E + u * NB2) : nullptr;
-    double acc = 0.0;  // lanes 0/1: D chain, lanes 2/3: E chain
-    bool any = false;
-    for (int c = 0; c < NCH; ++c) {
-      double2 a[4], b[4];
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const int i = c * (CH / 2) + k * 32 + lane;
-        a[k] = px ? __ldg(px + i) : make_double2(0.0, 0.0);
-        b[k] = px2 ? __ldg(px2 + i) : make_double2(0.0, 0.0);
-      }
-      __syncwarp();
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        double d0, d1, e0, e1;
-        // D = add_scaled(1.0, X2, -1.0, X): first operand X2, second X
-        d0 = px2 ? __dmul_rn(1.0, b[k].x) : 0.0;
-        d1 = px2 ? __dmul_rn(1.0, b[k].y) : 0.0;
-        if (px) {
-          d0 = __dadd_rn(d0, __dmul_rn(-1.0, a[k].x));
-          d1 = __dadd_rn(d1, __dmul_rn(-1.0, a[k].y));
-        }
-        // E = add_scaled(2.0, X, -1.0, X2): first operand X, second X2
-        e0 = px ? __dmul_rn(2.0, a[k].x) : 0.0;
-        e1 = px ? __dmul_rn(2.0, a[k].y) : 0.0;
-        if (px2) {
-          e0 = __dadd_rn(e0, __dmul_rn(-1.0, b[k].x));
-          e1 = __dadd_rn(e1, __dmul_rn(-1.0, b[k].y));
-        }
-        if (IDEM)
-          *reinterpret_cast<double2*>(bd + k * 64 + 2 * lane) =
-              make_double2(__dmul_rn(d0, d0), __dmul_rn(d1, d1));
-        if (EXPAND) {
-          *reinterpret_cast<double2*>(be + k * 64 + 2 * lane) =
-              make_double2(__dmul_rn(e0, e0), __dmul_rn(e1, e1));
-          pe[c * (CH / 2) + k * 32 + lane] = make_double2(e0, e1);
-          any |= (e0 != 0.0) | (e1 != 0.0);
-        }
-      }
-      __syncwarp();
-      if ((IDEM && lane < 2) || (EXPAND && lane >= 2 && lane < 4)) {
-        acc = einsum_lane_chain256((lane < 2 ? bd : be) + (lane & 1), acc);
-      }
-    }
-    const double l1 = __shfl_sync(0xffffffffu, acc, 1);
-    const double l2 = __shfl_sync(0xffffffffu, acc, 2);
-    const double l3 = __shfl_sync(0xffffffffu, acc, 3);
-    any = __any_sync(0xffffffffu, any);
-    if (lane == 0) {
-      if (IDEM) nD2[u] = __dadd_rn(acc, l1);
-      if (EXPAND) {
-        nE2[u] = __dadd_rn(l2, l3);
-        nzE[u] = any ? 1 : 0;
-      }
-    }
-  }
-}
-
-// Multi-block K6 (production path): BPW union blocks per warp, the D and E
-// chains of all of them on lanes 0 .. 4 BPW - 1 (lane = 4 q + 2 set + parity)
-// over the permuted parity rows (common.cuh).  Same arithmetic and bits as
-// k_sp2_update.
+// K6: BPW union blocks per warp; D = fl(fl(1*x2) + fl(-1*x)) (norm^2 only) and
+// E = fl(fl(2*x) + fl(-1*x2)) (written) with exactly the reference's rounding
+// (absent operand = no term); the D and E chains of all of them run on lanes
+// 0 .. 4 BPW - 1 (lane = 4 q + 2 set + parity) over the permuted parity rows
+// (common.cuh).
 template <int NB2, bool IDEM, bool EXPAND, int BPW, int WARPS>
 __global__ void __launch_bounds__(32 * WARPS)
     k_sp2_update_multi(const int64_t* __restrict__ ukeys, int64_t U, const double* __restrict__ X,
