@@ -455,18 +455,9 @@ void leaf_products_tma(int64_t n_seg, const int64_t* seg, const Idx* a_idx, cons
   if (nb == 64)
     launch_tma<64, 2, 4, 3, 1, Idx>(n_seg, seg, a_idx, b_idx, c_out, c_mirror, accumulate, A,
                                     a_blocks, B, b_blocks, C, s, lpt);
-  else if (nb == 32) {  // 4 CTAs/SM x 4 consumer warps (measured best: 31.2 TF/s on cfg3)
-    static const int v = [] {
-      const char* e = getenv("SPAMM_K4_32");
-      return e ? atoi(e) : 0;
-    }();
-    if (v == 1)
-      launch_tma<32, 2, 2, 6, 2, Idx>(n_seg, seg, a_idx, b_idx, c_out, c_mirror, accumulate, A,
-                                      a_blocks, B, b_blocks, C, s, lpt);
-    else
-      launch_tma<32, 2, 2, 3, 4, Idx>(n_seg, seg, a_idx, b_idx, c_out, c_mirror, accumulate, A,
-                                      a_blocks, B, b_blocks, C, s, lpt);
-  }
+  else if (nb == 32)  // 4 CTAs/SM x 4 consumer warps (fastest of 9 measured configurations)
+    launch_tma<32, 2, 2, 3, 4, Idx>(n_seg, seg, a_idx, b_idx, c_out, c_mirror, accumulate, A,
+                                    a_blocks, B, b_blocks, C, s, lpt);
   else
     throw CudaError("TMA leaf kernel needs block size 32 or 64");
 }
