@@ -133,8 +133,8 @@ def config_dict(cfg, n_occ, args, extra=None):
          "block_size": cfg.block_size, "tau": cfg.tau, "n_occ": n_occ,
          "criterion": "||X^2-X||_F<1e-6", "step": "one full SP2 solve H->P",
          "l2": f"flushed between steps ({L2_FLUSH_BYTES >> 20} MiB write)",
-         "parallelism": (f"C-curve sharded x{args.gpus}, NCCL all-gather, persistence LB"
-                         if args.gpus > 1 else "single GPU"),
+         "parallelism": (f"C nodes sharded x{args.gpus} by equal task count (X replicated), "
+                         "NCCL all-gather of the owned blocks" if args.gpus > 1 else "single GPU"),
          "inputs": "synthetic, seed 0 (synth.py)"}
     from paper_1403_7458_b200.quadtree import _padded_geometry
     d["n_padded"] = _padded_geometry(cfg.n, cfg.block_size)[0]
@@ -152,7 +152,7 @@ def run_ours(args):
 
     ws, rank, local = dist_env()
     torch.cuda.set_device(local)
-    if ws > 1:
+    if ws > 1 or (args.sharded and "RANK" in os.environ):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     lib = nat.load()
     cfg, h, n_occ = workload(args.config)
@@ -163,7 +163,7 @@ def run_ours(args):
     flush = torch.empty(L2_FLUSH_BYTES // 8, dtype=torch.float64, device="cuda")
     stream = torch.cuda.current_stream()
     nb3x2 = 2 * cfg.block_size ** 3
-    sharded = ws > 1
+    sharded = ws > 1 or args.sharded
 
     def solve(ff, timed):
         """One SP2 solve -> (P, reference-equivalent flops of the whole job, flops this rank
@@ -171,8 +171,8 @@ def run_ours(args):
         if not sharded:
             p, st = sp.sp2_solve(ff, n_occ, cfg.tau, timed=timed, **crit)
             return p, st.flops, st.executed_flops, st.ms_leaf, len(st.leaf_products), st.iteration
-        from paper_1403_7458_b200.parallel import DeviceEngine, ShardedSP2
-        res = ShardedSP2(DeviceEngine()).solve(ff, n_occ, cfg.tau, **crit)
+        from paper_1403_7458_b200.parallel import NativeShardedSP2
+        res = NativeShardedSP2().solve(ff, n_occ, cfg.tau, **crit)
         return (res.x, sum(res.leaf_products) * nb3x2, sum(res.local_work) * nb3x2, 0.0,
                 len(res.leaf_products), res.iteration)
 
@@ -291,7 +291,7 @@ def run_ours(args):
         if ws == 1 and not args.no_cpu_baseline:
             out["cpu_baseline"] = cpu_baseline(cfg, h, n_occ, sample_multiplies=1)
         print(json.dumps(out), flush=True)
-    if ws > 1:
+    if dist.is_initialized():
         dist.destroy_process_group()
 
 
@@ -567,7 +567,8 @@ def main():
     ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--sharded", action="store_true",
-                    help="config 5: run the distributed-operand path even on one GPU")
+                    help="run the multi-GPU code path even on one GPU (config 4: native "
+                         "sharded SP2; config 5: distributed operand)")
     ap.add_argument("--molecules", type=int, default=None,
                     help="config 5: override the molecule count (smoke tests)")
     args = ap.parse_args()

@@ -140,6 +140,23 @@ int spamm_set_symmetric_products(int32_t enabled);
  * of the tier-by-tier walk; task sets, order and counters are identical.
  * 0 forces the tier walk (A/B testing). */
 int spamm_set_dense_cull(int32_t enabled);
+/* Sharded SP2 iteration (multi-GPU, X replicated; parallel.ShardedSP2):
+ * spamm_sp2_multiply_shard runs the full dense cull of X*X on every rank (so
+ * every rank holds the same C layout) and the leaf products of this rank's
+ * contiguous run of emitted C nodes, cut into `world` equal task counts;
+ * cut_pos (world + 1) receives the Morton cut positions.  C comes back
+ * unfinalised with this rank's blocks (and their mirrors) computed; after the
+ * caller has exchanged blocks (every C block has one owner: the rank whose
+ * Morton range holds its upper-triangle position), spamm_sp2_shard_finish
+ * finalises C and runs the rest of the iteration (traces, residual, branch,
+ * update) exactly as spamm_sp2_step; *x_next is 2X - X^2 on EXPAND, NULL on
+ * SQUARE (the next X is then C itself).  Needs depth <= 8. */
+int spamm_sp2_multiply_shard(const spamm_mat* x, double tau, int32_t kernel, int32_t rank,
+                             int32_t world, void* stream, spamm_mat** c, int64_t* cut_pos,
+                             spamm_stats* stats);
+int spamm_sp2_shard_finish(const spamm_mat* x, spamm_mat* c, double n_occ, int32_t want_idem,
+                           void* stream, int32_t* branch, double* t_x, double* t_sq,
+                           double* idem, spamm_mat** x_next);
 /* Pre-grow the library's stream-ordered memory pool by `bytes` (kept mapped),
  * so steady-state allocations never wait on a new device mapping. */
 int spamm_reserve_pool(int64_t bytes, void* stream);

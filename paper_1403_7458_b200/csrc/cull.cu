@@ -393,6 +393,33 @@ __global__ void __launch_bounds__(CULL_THREADS)
   }
 }
 
+// Sharded SP2: Morton cut positions that split the emitted tasks into
+// `world` equal parts (exclusive task prefix off[p] & mask is monotone in p),
+// and the node index at each cut.  out[0..world] = positions,
+// out[world+1 .. 2 world+1] = node bounds.
+__global__ void k_shard_cuts(const int64_t* __restrict__ off, int64_t npos, int world,
+                             int64_t* __restrict__ out) {
+  const int r = threadIdx.x;
+  if (r > world) return;
+  const int64_t total = off[npos] & DT_TASK_MASK;
+  int64_t pos;
+  if (r == 0) {
+    pos = 0;
+  } else if (r == world) {
+    pos = npos;
+  } else {
+    const int64_t target = (total * r + world - 1) / world;
+    int64_t lo = 0, hi = npos;  // smallest p with prefix(p) >= target
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) / 2;
+      if ((off[mid] & DT_TASK_MASK) >= target) hi = mid; else lo = mid + 1;
+    }
+    pos = lo;
+  }
+  out[r] = pos;
+  out[world + 1 + r] = (off[pos] >> DT_NODE) & DT_IDX_MASK;
+}
+
 bool dense_cull(const Mat& a, const Mat& b, double tau, bool want_tasks, CullResult& r,
                 cudaStream_t s, bool sym) {
   const int depth = a.depth;
@@ -401,7 +428,8 @@ bool dense_cull(const Mat& a, const Mat& b, double tau, bool want_tasks, CullRes
   // total, [4 + t]: tier-t survivors (t < depth)
   // [aux | LPT schedule: G + 1 length bins (bin 0 = G tasks) + the K4 counter]
   // zeroed by one memset; the schedule part is handed to K4 (r.sched).
-  const size_t aux_bytes = (4 + DENSE_MAX_DEPTH) * sizeof(int64_t);
+  const int world = r.world > 1 ? r.world : 1;
+  const size_t aux_bytes = (4 + DENSE_MAX_DEPTH + 2 * (world + 1)) * sizeof(int64_t);
   char* zbuf = dmalloc<char>(aux_bytes + (G + 2) * sizeof(int), s);
   int64_t* aux = reinterpret_cast<int64_t*>(zbuf);
   int* sched = reinterpret_cast<int*>(zbuf + aux_bytes);
@@ -421,11 +449,22 @@ bool dense_cull(const Mat& a, const Mat& b, double tau, bool want_tasks, CullRes
   SPAMM_LAUNCH_CK();
   scan_exclusive_i64(cnt, npos, off, s);
   if (want_tasks) hist_scan_exclusive(sched, (int)G + 1, s);
-  const int64_t* src[4 + DENSE_MAX_DEPTH];
+  int64_t* cuts = aux + 4 + DENSE_MAX_DEPTH;
+  if (world > 1) {
+    k_shard_cuts<<<1, 32, 0, s>>>(off, npos, world, cuts);
+    SPAMM_LAUNCH_CK();
+  }
+  const int nsc = 4 + depth + (world > 1 ? 2 * (world + 1) : 0);
+  const int64_t* src[48];
   for (int i = 0; i < 4 + depth; ++i) src[i] = aux + i;
   src[2] = off + npos;
-  int64_t h[4 + DENSE_MAX_DEPTH];
-  gather_sync(h, src, 4 + depth, s);
+  for (int i = 0; world > 1 && i < 2 * (world + 1); ++i) src[4 + depth + i] = cuts + i;
+  int64_t h[48];
+  gather_sync(h, src, nsc, s);
+  if (world > 1) {
+    r.cut_pos.assign(h + 4 + depth, h + 4 + depth + world + 1);
+    r.node_cut.assign(h + 5 + depth + world, h + 5 + depth + 2 * world + 1);
+  }
   if (h[1]) {  // leaf survivor set not mirror-symmetric (ulp tie): full cull
     dfree(cnt, s);
     dfree(zbuf, s);

@@ -20,7 +20,7 @@ T* dmalloc(size_t n, cudaStream_t s) {
 
 // Copy a few int64 from device to host and wait (the only host syncs on the path).
 void d2h_sync(int64_t* host, const int64_t* dev, int n, cudaStream_t s);
-// One launch copies n (<= 16) device scalars (null source -> 0) straight into
+// One launch copies n (<= 48) device scalars (null source -> 0) straight into
 // pinned host memory, then waits: replaces memset + D2D copies + D2H per sync.
 void gather_sync(int64_t* host, const int64_t* const* src, int n, cudaStream_t s);
 void stream_wait(cudaStream_t s);   // spin-polls unless SPAMM_WAIT=block
@@ -144,6 +144,11 @@ struct CullResult {
   int32_t* order = nullptr;
   int* sched = nullptr;                  // hist/counter scratch (counter inside)
   void* block = nullptr;                 // dense cull: single allocation of the arrays
+  // Sharded SP2 (input): split the emitted C nodes into `world` contiguous
+  // Morton segments of equal task count; (output) their Morton cut positions
+  // and node index bounds (world + 1 each).  Dense cull only.
+  int world = 1;
+  std::vector<int64_t> cut_pos, node_cut;
   int* counter = nullptr;
   void release(cudaStream_t s);
 };

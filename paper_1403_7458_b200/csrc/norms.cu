@@ -84,7 +84,7 @@ void event_wait(cudaEvent_t e) {
 }
 
 struct ScalarSrc {
-  const int64_t* p[16];
+  const int64_t* p[48];
 };
 __global__ void k_gather_scalars(ScalarSrc src, int n, int64_t* dst) {
   const int i = threadIdx.x;
@@ -93,16 +93,16 @@ __global__ void k_gather_scalars(ScalarSrc src, int n, int64_t* dst) {
 
 int64_t* pinned_scalars() {
   static thread_local int64_t* pinned = nullptr;
-  if (!pinned) SPAMM_CK(cudaMallocHost(&pinned, 64 * sizeof(int64_t)));
+  if (!pinned) SPAMM_CK(cudaMallocHost(&pinned, 96 * sizeof(int64_t)));
   return pinned;
 }
 
 void gather_sync(int64_t* host, const int64_t* const* src, int n, cudaStream_t s) {
-  if (n > 16) throw CudaError("gather_sync: too many scalars");
+  if (n > 48) throw CudaError("gather_sync: too many scalars");
   ScalarSrc ss{};
   for (int i = 0; i < n; ++i) ss.p[i] = src[i];
   int64_t* pinned = pinned_scalars() + 32;  // (d2h_sync uses the first 32)
-  k_gather_scalars<<<1, 32, 0, s>>>(ss, n, pinned);
+  k_gather_scalars<<<1, 64, 0, s>>>(ss, n, pinned);
   SPAMM_LAUNCH_CK();
   stream_wait(s);
   for (int i = 0; i < n; ++i) host[i] = pinned[i];

@@ -34,7 +34,8 @@ import numpy as np
 from .synth_morton import morton_keys
 
 __all__ = ["partition_work", "even_cuts", "ShardedSP2", "DeviceEngine", "ShardedResult",
-           "ShardedMultiply", "ShardProduct", "morton_positions"]
+           "ShardedMultiply", "ShardProduct", "morton_positions", "NativeShardedSP2",
+           "exchange_blocks", "block_owners"]
 
 
 def even_cuts(n_pos: int, world: int) -> list:
@@ -465,3 +466,142 @@ class DeviceEngine:
 def morton_of_keys(keys: np.ndarray, g: int) -> np.ndarray:
     """Morton position (row bit above column bit) of reference keys bi*G+bj."""
     return morton_keys(np.asarray(keys) // g, np.asarray(keys) % g)
+
+
+# ---------------------------------------------------------------------------
+# Native sharded SP2 (the device path for N > 1)
+# ---------------------------------------------------------------------------
+
+def block_owners(keys, g: int, cut_pos) -> "torch.Tensor":
+    """Owner rank of every C block in a sharded SP2 product: the rank whose
+    Morton range holds the block's upper-triangle position (a rank computes
+    its upper blocks and writes their mirrors)."""
+    import torch
+    i, j = keys // g, keys % g
+    upper = torch.minimum(i, j) * g + torch.maximum(i, j)
+    inner = torch.as_tensor(list(cut_pos[1:-1]), dtype=torch.int64, device=keys.device)
+    return torch.searchsorted(inner, morton_positions(upper, g), right=True)
+
+
+def exchange_blocks(keys, blocks, g: int, cut_pos, group=None) -> dict:
+    """In-place all-gather of a sharded product's blocks: afterwards every
+    rank's ``blocks`` (storage order, same layout on every rank) holds every
+    rank's computed blocks.  One all_gather (NCCL on GPUs) of the owned blocks,
+    padded to the largest share."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    if world == 1 or blocks.shape[0] == 0:
+        return {"sent_blocks": 0, "received_blocks": 0}
+    rank = dist.get_rank(group)
+    owner = block_owners(keys, g, cut_pos)
+    counts = torch.bincount(owner, minlength=world).tolist()
+    mx = max(counts)
+    nb = blocks.shape[-1]
+    mine = owner == rank
+    send = torch.zeros((mx, nb, nb), dtype=blocks.dtype, device=blocks.device)
+    send[: counts[rank]] = blocks[mine]
+    out = torch.empty((world * mx, nb, nb), dtype=blocks.dtype, device=blocks.device)
+    dist.all_gather_into_tensor(out, send, group=group)
+    for r in range(world):
+        if r != rank and counts[r]:
+            blocks[owner == r] = out[r * mx: r * mx + counts[r]]
+    return {"sent_blocks": counts[rank], "received_blocks": sum(counts) - counts[rank]}
+
+
+class NativeShardedSP2:
+    """SP2 on N GPUs (one process per GPU), X replicated: per iteration every
+    rank runs the same dense cull (``spamm_sp2_multiply_shard``), computes the
+    leaf products of its contiguous run of C nodes -- cut by the current
+    iteration's task counts, so every rank gets the same work -- the owned
+    blocks are all-gathered (``exchange_blocks``), and the rest of the
+    iteration runs on every rank (``spamm_sp2_shard_finish``: traces, fused
+    residual, branch, update).  The trajectory is bitwise the single-GPU
+    ``sp2_solve``'s; at world size 1 it is that solve."""
+
+    def __init__(self, kernel: str = "auto", group=None):
+        import torch.distributed as dist
+        self.kernel = kernel
+        self.group = group
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+
+    def multiply_shard(self, x, tau: float, rank: int | None = None, world: int | None = None):
+        import ctypes
+
+        from . import _native as nat
+        from .kernel import _check_tau, _leaf_kernel
+        from .quadtree import QuadTreeMatrix
+        rank = self.rank if rank is None else rank
+        world = self.world if world is None else world
+        st = nat.Stats()
+        out = ctypes.c_void_p()
+        cuts = (ctypes.c_int64 * (world + 1))()
+        stream = nat.current_stream()
+        nat.check(nat.load().spamm_sp2_multiply_shard(x._h, _check_tau(tau),
+                                                      _leaf_kernel(self.kernel), int(rank),
+                                                      int(world), stream, ctypes.byref(out),
+                                                      ctypes.cast(cuts, ctypes.c_void_p),
+                                                      ctypes.byref(st)))
+        self.last_executed = int(st.executed_products)   # the whole product's (all ranks)
+        return QuadTreeMatrix(out, stream), list(cuts), int(st.leaf_products)
+
+    def finish(self, x, c, n_occ: float, want_idem: bool):
+        import ctypes
+
+        from . import _native as nat
+        from .quadtree import QuadTreeMatrix
+        stream = nat.current_stream()
+        br = ctypes.c_int32()
+        t_x, t_sq, idem = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
+        e = ctypes.c_void_p()
+        nat.check(nat.load().spamm_sp2_shard_finish(x._h, c._h, float(n_occ), int(want_idem),
+                                                    stream, ctypes.byref(br), ctypes.byref(t_x),
+                                                    ctypes.byref(t_sq), ctypes.byref(idem),
+                                                    ctypes.byref(e)))
+        from .sp2 import EXPAND, SQUARE
+        c._refresh()
+        nxt = QuadTreeMatrix(e, stream) if e.value else c
+        return (nxt, SQUARE if br.value == 0 else EXPAND, t_x.value, t_sq.value,
+                idem.value if want_idem else None)
+
+    def solve(self, f, n_occ: int, tau: float, max_iter: int = 100, criterion: str = "fro",
+              fro_tol: float = 1e-6, idem_tol: float = 1e-9) -> ShardedResult:
+        from .quadtree import trace
+        from .sp2 import _reserve_for, gershgorin_bounds, sp2_init
+        _reserve_for(f)
+        x = sp2_init(f, gershgorin_bounds(f))
+        g = x.n_blocks
+        res = ShardedResult(x=x)
+        res.trace_history.append(trace(x))
+        want_idem = criterion == "fro"
+        pending = False
+        for _ in range(max_iter):
+            t0 = time.perf_counter()
+            c, cuts, leaf = self.multiply_shard(x, tau)
+            res.cuts_history.append(cuts)
+            res.leaf_products.append(leaf)
+            # cuts give every rank an equal share of the executed products
+            res.local_work.append(self.last_executed // self.world)
+            exchange_blocks(c.keys_device(), c.blocks_device(), g, cuts, self.group)
+            nxt, branch, t_x, t_sq, idem = self.finish(x, c, n_occ, want_idem)
+            if pending:
+                res.trace_history.append(t_x)
+                pending = False
+            if want_idem:
+                res.idempotency_history.append(idem)
+                done = idem < fro_tol
+            else:
+                done = abs(t_sq - t_x) < idem_tol and abs(t_x - n_occ) < 1e-6 * n_occ
+            res.seconds_per_iteration.append(time.perf_counter() - t0)
+            if done:
+                res.converged = True
+                break
+            x = nxt
+            res.iteration += 1
+            res.branch_history.append(branch)
+            pending = True
+        if pending:
+            res.trace_history.append(trace(x))
+        res.x = x
+        return res

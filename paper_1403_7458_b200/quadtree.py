@@ -120,6 +120,14 @@ class QuadTreeMatrix:
         """Exactly symmetric (X == X^T bitwise); X*X then runs the symmetric path."""
         return bool(self._info.symmetric)
 
+    def _refresh(self) -> None:
+        """Re-read the handle after the library finalised it in place."""
+        info = nat.MatInfo()
+        nat.check(nat.load().spamm_mat_info_get(self._h, ctypes.byref(info)))
+        self._info = info
+        self._host = None
+        self._root = None
+
     # -- Morton shards (multi-GPU, parallel.ShardedMultiply) ----------------
     def leaf_norms2_device(self):
         """(G*G,) float64 leaf tier of norm^2 (row-major bi*G+bj, 0 where no block)."""
