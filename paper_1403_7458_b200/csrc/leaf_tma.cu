@@ -72,13 +72,19 @@ __device__ __forceinline__ double lds64(uint32_t addr) {
   return v;
 }
 
-template <int NB, int WARPS_M, int WARPS_N, int STAGES>
+// A stage holds the k-range [h KH, (h + 1) KH) of one task, KH = NB / KS:
+// A as KH/16 column slabs of NB rows, B as NB/16 column slabs of KH rows (so
+// KS = 2 gives twice the stages of half the size: finer-grained refills and
+// a deeper look-ahead in the same shared memory).
+template <int NB, int WARPS_M, int WARPS_N, int STAGES, int KS = 1>
 struct TmaCfg {
   static constexpr int CONSUMERS = WARPS_M * WARPS_N;
   static constexpr int THREADS = 32 * (CONSUMERS + 1);
-  static constexpr int SLAB = NB * 128;              // bytes of one 16-column slab
-  static constexpr int TILE = NB * NB * 8;           // bytes of one leaf block
-  static constexpr int STAGE = 2 * TILE;             // A + B
+  static constexpr int KH = NB / KS;                 // k-extent of a stage
+  static constexpr int SLAB = NB * 128;              // A: one 16-column slab, NB rows
+  static constexpr int SLAB_B = KH * 128;            // B: one 16-column slab, KH rows
+  static constexpr int A_BYTES = (KH / 16) * SLAB;
+  static constexpr int STAGE = A_BYTES + (NB / 16) * SLAB_B;   // = 2 NB KH 8
   static constexpr size_t SMEM = (size_t)STAGES * STAGE + 1024 + 3 * STAGES * 8 + 64;
 };
 
@@ -89,14 +95,15 @@ __host__ __device__ constexpr int swz(int r, int c) {
   return (c >> 4) * (NB * 128) + r * 128 + ((((c & 15) >> 1) ^ (r & 7)) << 4) + ((c & 1) << 3);
 }
 
-template <int NB, int WARPS_M, int WARPS_N, int STAGES, class Idx>
+template <int NB, int WARPS_M, int WARPS_N, int STAGES, int KS, class Idx>
 __global__ void __launch_bounds__(32 * (WARPS_M * WARPS_N + 1), 1)
     k_leaf_dmma_tma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     int64_t n_seg, const int64_t* __restrict__ seg, const Idx* __restrict__ a_idx,
                     const Idx* __restrict__ b_idx, const int64_t* __restrict__ c_out,
                     const int64_t* __restrict__ c_mirror, int accumulate, double* __restrict__ C,
                     const int32_t* __restrict__ order, int* __restrict__ next_block) {
-  using Cfg = TmaCfg<NB, WARPS_M, WARPS_N, STAGES>;
+  using Cfg = TmaCfg<NB, WARPS_M, WARPS_N, STAGES, KS>;
+  constexpr int KH = Cfg::KH;
   constexpr int WTM = NB / WARPS_M, WTN = NB / WARPS_N, MT = WTM / 8, NT = WTN / 8;
   static_assert(WTN % 8 == 0 && WTM % 8 == 0, "warp tile must be a multiple of 8");
   extern __shared__ uint8_t smem_raw[];
@@ -157,22 +164,27 @@ __global__ void __launch_bounds__(32 * (WARPS_M * WARPS_N + 1), 1)
         for (int q = 0; q < cnt; ++q) {
           const int ra = __shfl_sync(0xffffffffu, ra_l, q);
           const int rb = __shfl_sync(0xffffffffu, rb_l, q);
-          mbar_wait(empty(stage), phase ^ 1u);
-          if (lane == 0) {
-            const int64_t tq = c0 + q;
-            meta[stage] = (m << 2) | (tq == t0 ? 1 : 0) | (tq + 1 == t1 ? 2 : 0);
-            mbar_expect_tx(full(stage), Cfg::STAGE);
-            const uint32_t sa = base + stage * Cfg::STAGE, sb = sa + Cfg::TILE;
+#pragma unroll 1
+          for (int h = 0; h < KS; ++h) {
+            mbar_wait(empty(stage), phase ^ 1u);
+            if (lane == 0) {
+              const int64_t tq = c0 + q;
+              meta[stage] = (m << 2) | (tq == t0 && h == 0 ? 1 : 0) |
+                            (tq + 1 == t1 && h == KS - 1 ? 2 : 0);
+              mbar_expect_tx(full(stage), Cfg::STAGE);
+              const uint32_t sa = base + stage * Cfg::STAGE, sb = sa + Cfg::A_BYTES;
 #pragma unroll
-            for (int sl = 0; sl < NB / 16; ++sl) {
-              tma_load_2d(sa + sl * Cfg::SLAB, &tmA, full(stage), sl * 16, ra);
-              tma_load_2d(sb + sl * Cfg::SLAB, &tmB, full(stage), sl * 16, rb);
+              for (int sl = 0; sl < KH / 16; ++sl)
+                tma_load_2d(sa + sl * Cfg::SLAB, &tmA, full(stage), h * KH + sl * 16, ra);
+#pragma unroll
+              for (int sl = 0; sl < NB / 16; ++sl)
+                tma_load_2d(sb + sl * Cfg::SLAB_B, &tmB, full(stage), sl * 16, rb + h * KH);
             }
-          }
-          __syncwarp();
-          if (++stage == STAGES) {
-            stage = 0;
-            phase ^= 1u;
+            __syncwarp();
+            if (++stage == STAGES) {
+              stage = 0;
+              phase ^= 1u;
+            }
           }
         }
       }
@@ -240,9 +252,9 @@ __global__ void __launch_bounds__(32 * (WARPS_M * WARPS_N + 1), 1)
           }
         }
     }
-    const uint32_t sa = base + stage * Cfg::STAGE, sb = sa + Cfg::TILE;
+    const uint32_t sa = base + stage * Cfg::STAGE, sb = sa + Cfg::A_BYTES;
 #pragma unroll
-    for (int kk = 0; kk < NB; kk += 4) {
+    for (int kk = 0; kk < KH; kk += 4) {
       double af[MT], bf[NT];
 #pragma unroll
       for (int mt = 0; mt < MT; ++mt)
@@ -250,7 +262,7 @@ __global__ void __launch_bounds__(32 * (WARPS_M * WARPS_N + 1), 1)
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt) {
         const int cb = col0 + nt * 8;
-        bf[nt] = lds64(sb + (cb >> 4) * Cfg::SLAB + kk * 128 + offB[(cb >> 3) & 1][(kk >> 2) & 1]);
+        bf[nt] = lds64(sb + (cb >> 4) * Cfg::SLAB_B + kk * 128 + offB[(cb >> 3) & 1][(kk >> 2) & 1]);
       }
 #pragma unroll
       for (int mt = 0; mt < MT; ++mt)
@@ -369,12 +381,12 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-CUtensorMap make_map(const double* data, int64_t nblocks, int nb) {
+CUtensorMap make_map(const double* data, int64_t nblocks, int nb, int box_rows) {
   CUtensorMap m;
   const int64_t rows = nblocks > 0 ? nblocks * nb : nb;
   cuuint64_t dims[2] = {(cuuint64_t)nb, (cuuint64_t)rows};
   cuuint64_t strides[1] = {(cuuint64_t)nb * sizeof(double)};
-  cuuint32_t box[2] = {16, (cuuint32_t)nb};
+  cuuint32_t box[2] = {16, (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(data), dims,
                            strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -394,18 +406,18 @@ int sm_count() {
   return n;
 }
 
-template <int NB, int WM, int WN, int ST, int CTAS_PER_SM, class Idx>
+template <int NB, int WM, int WN, int ST, int CTAS_PER_SM, int KS, class Idx>
 void launch_tma(int64_t n_seg, const int64_t* seg, const Idx* a_idx, const Idx* b_idx,
                 const int64_t* c_out, const int64_t* c_mirror, bool acc, const double* A,
                 int64_t a_blocks, const double* B, int64_t b_blocks, double* C, cudaStream_t s,
                 LptSchedule lpt) {
-  using Cfg = TmaCfg<NB, WM, WN, ST>;
-  auto kern = k_leaf_dmma_tma<NB, WM, WN, ST, Idx>;
+  using Cfg = TmaCfg<NB, WM, WN, ST, KS>;
+  auto kern = k_leaf_dmma_tma<NB, WM, WN, ST, KS, Idx>;
   static std::once_flag once;
   std::call_once(once, [&] {
     SPAMM_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM));
   });
-  const CUtensorMap ta = make_map(A, a_blocks, NB), tb = make_map(B, b_blocks, NB);
+  const CUtensorMap ta = make_map(A, a_blocks, NB, NB), tb = make_map(B, b_blocks, NB, NB / KS);
   int64_t grid = (int64_t)sm_count() * CTAS_PER_SM;
   if (grid > n_seg) grid = n_seg;
   int* scratch = nullptr;
@@ -452,12 +464,15 @@ void leaf_products_tma(int64_t n_seg, const int64_t* seg, const Idx* a_idx, cons
                        const double* A, int64_t a_blocks, const double* B, int64_t b_blocks,
                        double* C, int nb, cudaStream_t s, LptSchedule lpt) {
   if (n_seg <= 0) return;
+  // (KS = 2 -- twice the stages at half the k-extent -- measured slower for both:
+  //  33.2 vs 34.9 TF/s at Nb = 64, 26.6 vs 29.4 at Nb = 32: more barrier
+  //  round trips per flop outweigh the deeper look-ahead.)
   if (nb == 64)
-    launch_tma<64, 2, 4, 3, 1, Idx>(n_seg, seg, a_idx, b_idx, c_out, c_mirror, accumulate, A,
-                                    a_blocks, B, b_blocks, C, s, lpt);
+    launch_tma<64, 2, 4, 3, 1, 1, Idx>(n_seg, seg, a_idx, b_idx, c_out, c_mirror, accumulate, A,
+                                       a_blocks, B, b_blocks, C, s, lpt);
   else if (nb == 32)  // 4 CTAs/SM x 4 consumer warps (fastest of 9 measured configurations)
-    launch_tma<32, 2, 2, 3, 4, Idx>(n_seg, seg, a_idx, b_idx, c_out, c_mirror, accumulate, A,
-                                    a_blocks, B, b_blocks, C, s, lpt);
+    launch_tma<32, 2, 2, 3, 4, 1, Idx>(n_seg, seg, a_idx, b_idx, c_out, c_mirror, accumulate, A,
+                                       a_blocks, B, b_blocks, C, s, lpt);
   else
     throw CudaError("TMA leaf kernel needs block size 32 or 64");
 }
