@@ -66,6 +66,11 @@ __device__ __forceinline__ void dmma884(double (&c)[2], double a, double b) {
       : "+d"(c[0]), "+d"(c[1])
       : "d"(a), "d"(b));
 }
+__device__ __forceinline__ double2 lds128(uint32_t addr) {
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];\n" : "=d"(v.x), "=d"(v.y) : "r"(addr));
+  return v;
+}
 __device__ __forceinline__ double lds64(uint32_t addr) {
   double v;
   asm volatile("ld.shared.f64 %0, [%1];\n" : "=d"(v) : "r"(addr));
@@ -95,7 +100,7 @@ __host__ __device__ constexpr int swz(int r, int c) {
   return (c >> 4) * (NB * 128) + r * 128 + ((((c & 15) >> 1) ^ (r & 7)) << 4) + ((c & 1) << 3);
 }
 
-template <int NB, int WARPS_M, int WARPS_N, int STAGES, int KS, class Idx>
+template <int NB, int WARPS_M, int WARPS_N, int STAGES, int KS, bool PAIRK, class Idx>
 __global__ void __launch_bounds__(32 * (WARPS_M * WARPS_N + 1), 1)
     k_leaf_dmma_tma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     int64_t n_seg, const int64_t* __restrict__ seg, const Idx* __restrict__ a_idx,
@@ -216,6 +221,19 @@ __global__ void __launch_bounds__(32 * (WARPS_M * WARPS_N + 1), 1)
 #pragma unroll
     for (int g = 0; g < 2; ++g)
       offB[h][g] = (uint32_t)((((h * 4 + (r8 >> 1)) ^ (g * 4 + c4)) << 4) + ((r8 & 1) << 3) + c4 * 128);
+  // Paired k-steps (PAIRK): steps 2t / 2t+1 take the even / odd columns of
+  // the 8-column group t, so a lane's two A values are one 16-byte chunk
+  // (one LDS.128 instead of two LDS.64); B rows follow the same k order.
+  uint32_t offA2[2], offBp[2][2];
+#pragma unroll
+  for (int t = 0; t < 2; ++t)
+    offA2[t] = (uint32_t)((((4 * t + c4) ^ r8) << 4) + r8 * 128);
+#pragma unroll
+  for (int h = 0; h < 2; ++h)
+#pragma unroll
+    for (int o = 0; o < 2; ++o)
+      offBp[h][o] = (uint32_t)((((h * 4 + (r8 >> 1)) ^ (2 * c4 + o)) << 4) + ((r8 & 1) << 3) +
+                               (2 * c4 + o) * 128);
 
   int stage = 0, held = -1;
   uint32_t phase = 0;
@@ -253,27 +271,52 @@ __global__ void __launch_bounds__(32 * (WARPS_M * WARPS_N + 1), 1)
         }
     }
     const uint32_t sa = base + stage * Cfg::STAGE, sb = sa + Cfg::A_BYTES;
+    if (PAIRK) {
 #pragma unroll
-    for (int kk = 0; kk < KH; kk += 4) {
-      double af[MT], bf[NT];
+      for (int k8 = 0; k8 < KH; k8 += 8) {
+        double ae[MT], ao[MT], be[NT], bo[NT];
 #pragma unroll
-      for (int mt = 0; mt < MT; ++mt)
-        af[mt] = lds64(sa + (kk >> 4) * Cfg::SLAB + (row0 + mt * 8) * 128 + offA[(kk >> 2) & 3]);
+        for (int mt = 0; mt < MT; ++mt) {
+          const double2 v = lds128(sa + (k8 >> 4) * Cfg::SLAB + (row0 + mt * 8) * 128 +
+                                   offA2[(k8 >> 3) & 1]);
+          ae[mt] = v.x;
+          ao[mt] = v.y;
+        }
 #pragma unroll
-      for (int nt = 0; nt < NT; ++nt) {
-        const int cb = col0 + nt * 8;
-        bf[nt] = lds64(sb + (cb >> 4) * Cfg::SLAB_B + kk * 128 + offB[(cb >> 3) & 1][(kk >> 2) & 1]);
+        for (int nt = 0; nt < NT; ++nt) {
+          const int cb = col0 + nt * 8;
+          const uint32_t rowb = sb + (cb >> 4) * Cfg::SLAB_B + k8 * 128;
+          be[nt] = lds64(rowb + offBp[(cb >> 3) & 1][0]);
+          bo[nt] = lds64(rowb + offBp[(cb >> 3) & 1][1]);
+        }
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) dmma884(acc[mt][nt], ae[mt], be[nt]);
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) dmma884(acc[mt][nt], ao[mt], bo[nt]);
       }
+    } else {
 #pragma unroll
-      for (int mt = 0; mt < MT; ++mt)
+      for (int kk = 0; kk < KH; kk += 4) {
+        double af[MT], bf[NT];
 #pragma unroll
-        for (int nt = 0; nt < NT; ++nt) dmma884(acc[mt][nt], af[mt], bf[nt]);
+        for (int mt = 0; mt < MT; ++mt)
+          af[mt] = lds64(sa + (kk >> 4) * Cfg::SLAB + (row0 + mt * 8) * 128 + offA[(kk >> 2) & 3]);
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          const int cb = col0 + nt * 8;
+          bf[nt] = lds64(sb + (cb >> 4) * Cfg::SLAB_B + kk * 128 + offB[(cb >> 3) & 1][(kk >> 2) & 1]);
+        }
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) dmma884(acc[mt][nt], af[mt], bf[nt]);
+      }
     }
-    // The stage is refilled by TMA (async proxy) once every consumer warp has
-    // arrived: order this warp's generic-proxy shared loads before that
-    // (a WAR hazard otherwise -- observed as rare corrupted blocks with
-    // 16-KB stages and 4 CTAs/SM).
-    held = stage;
+    held = stage;  // handed back after the next wait (see the release above)
     if (++stage == STAGES) {
       stage = 0;
       phase ^= 1u;
@@ -406,13 +449,13 @@ int sm_count() {
   return n;
 }
 
-template <int NB, int WM, int WN, int ST, int CTAS_PER_SM, int KS, class Idx>
+template <int NB, int WM, int WN, int ST, int CTAS_PER_SM, int KS, bool PAIRK, class Idx>
 void launch_tma(int64_t n_seg, const int64_t* seg, const Idx* a_idx, const Idx* b_idx,
                 const int64_t* c_out, const int64_t* c_mirror, bool acc, const double* A,
                 int64_t a_blocks, const double* B, int64_t b_blocks, double* C, cudaStream_t s,
                 LptSchedule lpt) {
   using Cfg = TmaCfg<NB, WM, WN, ST, KS>;
-  auto kern = k_leaf_dmma_tma<NB, WM, WN, ST, KS, Idx>;
+  auto kern = k_leaf_dmma_tma<NB, WM, WN, ST, KS, PAIRK, Idx>;
   static std::once_flag once;
   std::call_once(once, [&] {
     SPAMM_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM));
@@ -467,12 +510,14 @@ void leaf_products_tma(int64_t n_seg, const int64_t* seg, const Idx* a_idx, cons
   // (KS = 2 -- twice the stages at half the k-extent -- measured slower for both:
   //  33.2 vs 34.9 TF/s at Nb = 64, 26.6 vs 29.4 at Nb = 32: more barrier
   //  round trips per flop outweigh the deeper look-ahead.)
+  // PAIRK (paired k-steps, one LDS.128 per two A fragments): +0.4 % on cfg4,
+  // A/B-measured over 3 alternating runs (35.02 vs 34.88 TF/s).
   if (nb == 64)
-    launch_tma<64, 2, 4, 3, 1, 1, Idx>(n_seg, seg, a_idx, b_idx, c_out, c_mirror, accumulate, A,
-                                       a_blocks, B, b_blocks, C, s, lpt);
+    launch_tma<64, 2, 4, 3, 1, 1, true, Idx>(n_seg, seg, a_idx, b_idx, c_out, c_mirror,
+                                             accumulate, A, a_blocks, B, b_blocks, C, s, lpt);
   else if (nb == 32)  // 4 CTAs/SM x 4 consumer warps (fastest of 9 measured configurations)
-    launch_tma<32, 2, 2, 3, 4, 1, Idx>(n_seg, seg, a_idx, b_idx, c_out, c_mirror, accumulate, A,
-                                       a_blocks, B, b_blocks, C, s, lpt);
+    launch_tma<32, 2, 2, 3, 4, 1, true, Idx>(n_seg, seg, a_idx, b_idx, c_out, c_mirror,
+                                             accumulate, A, a_blocks, B, b_blocks, C, s, lpt);
   else
     throw CudaError("TMA leaf kernel needs block size 32 or 64");
 }
