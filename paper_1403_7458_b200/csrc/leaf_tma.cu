@@ -224,6 +224,19 @@ __global__ void __launch_bounds__(32 * (WARPS_M * WARPS_N + 1), 1)
   // Paired k-steps (PAIRK): steps 2t / 2t+1 take the even / odd columns of
   // the 8-column group t, so a lane's two A values are one 16-byte chunk
   // (one LDS.128 instead of two LDS.64); B rows follow the same k order.
+  // PAIRN (with PAIRK, two 8-column n-tiles per warp): tile nt takes the
+  // columns col0 + 2 q + nt, so a lane's two B values (tiles 0 and 1) are one
+  // 16-byte chunk, and its four C values of a row are contiguous.
+  // (measured: +3.8 % at Nb = 32, where K4 is shared-load bound; -4 % at
+  //  Nb = 64, so only the former uses it)
+  constexpr bool PAIRN = PAIRK && NT == 2 && WTN == 16 && NB == 32;
+  uint32_t offBn[2];
+#pragma unroll
+  for (int o = 0; o < 2; ++o)
+    offBn[o] = (uint32_t)(((r8 ^ (2 * c4 + o)) << 4) + (2 * c4 + o) * 128);
+  auto ccol = [&](int nt, int e) {  // C column held in acc[.][nt][e]
+    return PAIRN ? col0 + 4 * c4 + 2 * e + nt : col0 + nt * 8 + 2 * c4 + e;
+  };
   uint32_t offA2[2], offBp[2][2];
 #pragma unroll
   for (int t = 0; t < 2; ++t)
@@ -259,7 +272,11 @@ __global__ void __launch_bounds__(32 * (WARPS_M * WARPS_N + 1), 1)
       for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) {
-          if (accumulate) {
+          if (accumulate && PAIRN) {
+            const double* row = Cb + (row0 + mt * 8 + r8) * NB;
+            acc[mt][nt][0] = row[ccol(nt, 0)];
+            acc[mt][nt][1] = row[ccol(nt, 1)];
+          } else if (accumulate) {
             const double2 v = *reinterpret_cast<const double2*>(
                 Cb + (row0 + mt * 8 + r8) * NB + col0 + nt * 8 + 2 * c4);
             acc[mt][nt][0] = v.x;
@@ -282,12 +299,21 @@ __global__ void __launch_bounds__(32 * (WARPS_M * WARPS_N + 1), 1)
           ae[mt] = v.x;
           ao[mt] = v.y;
         }
+        if (PAIRN) {
+          const uint32_t rowb = sb + (col0 >> 4) * Cfg::SLAB_B + k8 * 128;
+          const double2 ve = lds128(rowb + offBn[0]), vo = lds128(rowb + offBn[1]);
+          be[0] = ve.x;
+          be[NT - 1] = ve.y;
+          bo[0] = vo.x;
+          bo[NT - 1] = vo.y;
+        } else {
 #pragma unroll
-        for (int nt = 0; nt < NT; ++nt) {
-          const int cb = col0 + nt * 8;
-          const uint32_t rowb = sb + (cb >> 4) * Cfg::SLAB_B + k8 * 128;
-          be[nt] = lds64(rowb + offBp[(cb >> 3) & 1][0]);
-          bo[nt] = lds64(rowb + offBp[(cb >> 3) & 1][1]);
+          for (int nt = 0; nt < NT; ++nt) {
+            const int cb = col0 + nt * 8;
+            const uint32_t rowb = sb + (cb >> 4) * Cfg::SLAB_B + k8 * 128;
+            be[nt] = lds64(rowb + offBp[(cb >> 3) & 1][0]);
+            bo[nt] = lds64(rowb + offBp[(cb >> 3) & 1][1]);
+          }
         }
 #pragma unroll
         for (int mt = 0; mt < MT; ++mt)
@@ -323,15 +349,24 @@ __global__ void __launch_bounds__(32 * (WARPS_M * WARPS_N + 1), 1)
     }
     if (!(md & 2)) continue;
     // last task of this C block: epilogue
+    if (PAIRN) {
 #pragma unroll
-    for (int mt = 0; mt < MT; ++mt)
-#pragma unroll
-      for (int nt = 0; nt < NT; ++nt) {
-        double2 v;
-        v.x = acc[mt][nt][0];
-        v.y = acc[mt][nt][1];
-        *reinterpret_cast<double2*>(Cb + (row0 + mt * 8 + r8) * NB + col0 + nt * 8 + 2 * c4) = v;
+      for (int mt = 0; mt < MT; ++mt) {
+        double* row = Cb + (row0 + mt * 8 + r8) * NB + col0 + 4 * c4;
+        *reinterpret_cast<double2*>(row) = make_double2(acc[mt][0][0], acc[mt][NT - 1][0]);
+        *reinterpret_cast<double2*>(row + 2) = make_double2(acc[mt][0][1], acc[mt][NT - 1][1]);
       }
+    } else {
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          double2 v;
+          v.x = acc[mt][nt][0];
+          v.y = acc[mt][nt][1];
+          *reinterpret_cast<double2*>(Cb + (row0 + mt * 8 + r8) * NB + col0 + nt * 8 + 2 * c4) = v;
+        }
+    }
     // The stores above consumed every accumulator, so every DMMA -- and every
     // fragment read of the held stage -- is complete: hand the stage back now
     // rather than after the mirror stores and the next wait.
@@ -347,9 +382,15 @@ __global__ void __launch_bounds__(32 * (WARPS_M * WARPS_N + 1), 1)
       for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) {
-          const int r = row0 + mt * 8 + r8, c = col0 + nt * 8 + 2 * c4;
-          Cm[c * NB + r] = acc[mt][nt][0];
-          Cm[(c + 1) * NB + r] = acc[mt][nt][1];
+          const int r = row0 + mt * 8 + r8;
+          if (PAIRN) {
+            Cm[ccol(nt, 0) * NB + r] = acc[mt][nt][0];
+            Cm[ccol(nt, 1) * NB + r] = acc[mt][nt][1];
+          } else {
+            const int c = col0 + nt * 8 + 2 * c4;
+            Cm[c * NB + r] = acc[mt][nt][0];
+            Cm[(c + 1) * NB + r] = acc[mt][nt][1];
+          }
         }
     }
   }
