@@ -236,6 +236,30 @@ int spamm_sp2_solve(const spamm_mat* f, double n_occ, double tau, int32_t max_it
                     double idem_tol, int32_t criterion, double fro_tol, double sym_tol,
                     int32_t kernel, int32_t timed, void* stream, spamm_mat** p_out,
                     spamm_sp2_report* rep);
+/* spamm_sp2_solve plus bulk copies that ride the solve's leaf-product windows
+ * (pipeline.py): the transfers are cut into chunks of <= chunk_bytes (0: 24 MiB);
+ * each multiply issues the next chunk on `stream` (a copy stream) ordered after
+ * the cull, just before its K4 launch, so PCIe traffic overlaps the DMMA-bound
+ * kernel instead of the loop's host syncs (a small host wait queued behind a
+ * bulk D2H costs ~60 us, measured).  Chunks left when the loop ends are issued
+ * then.  Direction is inferred from the pointers (cudaMemcpyDefault); the
+ * caller orders `stream` after the solve for completion.  No reference
+ * counterpart (the reference is CPU-only). */
+typedef struct spamm_transfer {
+  void* dst;
+  const void* src;
+  int64_t bytes;
+} spamm_transfer;
+typedef struct spamm_side_copies {
+  void* stream;
+  const spamm_transfer* items;
+  int32_t n_items;
+  int64_t chunk_bytes;
+} spamm_side_copies;
+int spamm_sp2_solve_ex(const spamm_mat* f, double n_occ, double tau, int32_t max_iter,
+                       double idem_tol, int32_t criterion, double fro_tol, double sym_tol,
+                       int32_t kernel, int32_t timed, void* stream, spamm_mat** p_out,
+                       spamm_sp2_report* rep, const spamm_side_copies* side);
 /* gershgorin_bounds (sp2.py:68-76): eps_min, eps_max and max|F-F^T|
  * (caller raises when asym > sym_tol, as the reference does). */
 int spamm_gershgorin(const spamm_mat* f, void* stream, double* eps_min, double* eps_max,

@@ -54,6 +54,15 @@ class SP2Report(ctypes.Structure):
     ]
 
 
+class Transfer(ctypes.Structure):
+    _fields_ = [("dst", c_vp), ("src", c_vp), ("bytes", c_i64)]
+
+
+class SideCopies(ctypes.Structure):
+    _fields_ = [("stream", c_vp), ("items", ctypes.POINTER(Transfer)), ("n_items", c_i32),
+                ("chunk_bytes", c_i64)]
+
+
 _SIGS = {
     "spamm_abi_version": (c_i32, []),
     "spamm_last_error": (ctypes.c_char_p, []),
@@ -105,6 +114,9 @@ _SIGS = {
                                  ctypes.POINTER(c_f64), ctypes.POINTER(c_vp)]),
     "spamm_sp2_solve": (c_i32, [c_vp, c_f64, c_f64, c_i32, c_f64, c_i32, c_f64, c_f64, c_i32,
                                 c_i32, c_vp, ctypes.POINTER(c_vp), ctypes.POINTER(SP2Report)]),
+    "spamm_sp2_solve_ex": (c_i32, [c_vp, c_f64, c_f64, c_i32, c_f64, c_i32, c_f64, c_f64,
+                                   c_i32, c_i32, c_vp, ctypes.POINTER(c_vp),
+                                   ctypes.POINTER(SP2Report), ctypes.POINTER(SideCopies)]),
     "spamm_gershgorin": (c_i32, [c_vp, c_vp, ctypes.POINTER(c_f64), ctypes.POINTER(c_f64),
                                  ctypes.POINTER(c_f64)]),
 }

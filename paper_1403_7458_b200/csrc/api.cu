@@ -1,5 +1,7 @@
 // C ABI (include/spamm_b200.h): argument checks, handle management and the
 // multiply driver (cull -> leaf products -> C finalisation).
+#include <algorithm>
+#include <climits>
 #include <cmath>
 #include <cstring>
 #include <string>
@@ -162,6 +164,47 @@ void fill_stats(spamm_stats* st, double tau, const spamm::CullResult& r, int nb)
   st->symmetric = r.sym ? 1 : 0;
   st->flop_estimate = st->leaf_products * 2 * (int64_t)nb * nb * nb;
 }
+
+// Bulk copies riding the K4 windows of an SP2 solve (spamm_sp2_solve_ex).
+struct SideQueue {
+  const spamm_side_copies* cfg = nullptr;
+  int item = 0;
+  int64_t off = 0;
+  cudaEvent_t ev = nullptr;
+  bool pending() const { return cfg && item < cfg->n_items; }
+  // issue up to `budget` bytes on the copy stream, ordered after `comp`'s
+  // current position
+  void issue(cudaStream_t comp, int64_t budget) {
+    if (!pending()) return;
+    auto cs = reinterpret_cast<cudaStream_t>(cfg->stream);
+    if (!ev) SPAMM_CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    SPAMM_CK(cudaEventRecord(ev, comp));
+    SPAMM_CK(cudaStreamWaitEvent(cs, ev, 0));
+    while (budget > 0 && pending()) {
+      const spamm_transfer& t = cfg->items[item];
+      const int64_t take = std::min(budget, t.bytes - off);
+      if (take > 0) {
+        SPAMM_CK(cudaMemcpyAsync(static_cast<char*>(t.dst) + off,
+                                 static_cast<const char*>(t.src) + off, (size_t)take,
+                                 cudaMemcpyDefault, cs));
+        off += take;
+        budget -= take;
+      }
+      if (off >= t.bytes) {
+        ++item;
+        off = 0;
+      }
+    }
+  }
+  void window(cudaStream_t comp) {
+    issue(comp, cfg && cfg->chunk_bytes > 0 ? cfg->chunk_bytes : (int64_t)24 << 20);
+  }
+  void drain(cudaStream_t comp) { issue(comp, INT64_MAX); }
+  ~SideQueue() {
+    if (ev) cudaEventDestroy(ev);
+  }
+};
+thread_local SideQueue* g_side = nullptr;
 
 void multiply_impl(const spamm_mat* a, const spamm_mat* b, double tau, int32_t kernel, bool timed,
                    cudaStream_t s, spamm::Mat& C, spamm_stats* stats, int64_t lo = 0,
@@ -416,6 +459,7 @@ void multiply_impl(const spamm_mat* a, const spamm_mat* b, double tau, int32_t k
   if (sym && !spamm::cull(a->m, b->m, tau, true, r, s, true, lo, hi, work))
     sym = false;  // ulp tie: full path
   if (!sym) spamm::cull(a->m, b->m, tau, true, r, s, false, lo, hi, work);
+  spamm::htrace("mul_culled");
   C.n_native = a->m.n_native;
   C.nb = a->m.nb;
   C.chunk_size = a->m.chunk_size;
@@ -459,6 +503,7 @@ void multiply_impl(const spamm_mat* a, const spamm_mat* b, double tau, int32_t k
     }
   }
   C.data = spamm::dmalloc<double>((size_t)C.nblocks * nb2, s);
+  if (g_side) g_side->window(s);  // PCIe chunk alongside K4
   tm.mark(1);  // leaf window = the K4 launch only (allocation stays outside)
   if (r.n_c > 0) {
     spamm::LptSchedule lpt;
@@ -469,6 +514,7 @@ void multiply_impl(const spamm_mat* a, const spamm_mat* b, double tau, int32_t k
                                   kernel, s, lpt);
   }
   tm.mark(2);
+  spamm::htrace("mul_k4");
   if (!r.block) {
     spamm::dfree(c_out, s);
     spamm::dfree(c_mirror, s);
@@ -478,6 +524,7 @@ void multiply_impl(const spamm_mat* a, const spamm_mat* b, double tau, int32_t k
   else
     spamm::finalize(C, s, nullptr, nullptr, defer_prune);
   C.sym = sym;
+  spamm::htrace("mul_final");
   tm.mark(3);
   fill_stats(stats, tau, r, C.nb);
   if (stats) {
@@ -600,6 +647,7 @@ void sp2_finish(const spamm_mat* x, const spamm_mat* c, double n_occ, bool want_
   const bool has_kept = src[3] != nullptr;
   int64_t h[5];
   spamm::gather_sync(h, src, 5, s);
+  spamm::htrace("fin_synced");
   const bool idem_done = want_idem && idem_dev;
   if (idem_done) memcpy(idem, &h[4], sizeof(double));
   spamm::dfree(sc, s);
@@ -616,6 +664,7 @@ void sp2_finish(const spamm_mat* x, const spamm_mat* c, double n_occ, bool want_
   const bool square = std::fabs(tsq - n_occ) <= std::fabs(tex - n_occ);
   spamm_mat* e = square ? nullptr : new spamm_mat();
   spamm::Mat dummy;
+  spamm::htrace("fin_branch");
   if (fused) {
     // with the residual fused into K1 there is nothing left to sync on: E's
     // exact-zero blocks stay pending (settled when the handle is inspected)
@@ -632,6 +681,7 @@ void sp2_finish(const spamm_mat* x, const spamm_mat* c, double n_occ, bool want_
   *t_x = tx;
   *t_sq = tsq;
   *e_out = e;
+  spamm::htrace("fin_end");
 }
 
 }  // namespace
@@ -973,7 +1023,21 @@ int spamm_sp2_solve(const spamm_mat* f, double n_occ, double tau, int32_t max_it
                     double idem_tol, int32_t criterion, double fro_tol, double sym_tol,
                     int32_t kernel, int32_t timed, void* stream, spamm_mat** p_out,
                     spamm_sp2_report* rep) {
+  return spamm_sp2_solve_ex(f, n_occ, tau, max_iter, idem_tol, criterion, fro_tol, sym_tol,
+                            kernel, timed, stream, p_out, rep, nullptr);
+}
+
+int spamm_sp2_solve_ex(const spamm_mat* f, double n_occ, double tau, int32_t max_iter,
+                       double idem_tol, int32_t criterion, double fro_tol, double sym_tol,
+                       int32_t kernel, int32_t timed, void* stream, spamm_mat** p_out,
+                       spamm_sp2_report* rep, const spamm_side_copies* side) {
   if (!f || !p_out || !rep) return fail(SPAMM_EINVAL, "null argument");
+  if (side && (!side->stream || side->n_items < 0 || (side->n_items > 0 && !side->items)))
+    return fail(SPAMM_EINVAL, "side copies: null stream or items");
+  for (int i = 0; side && i < side->n_items; ++i)
+    if (side->items[i].bytes < 0 || (side->items[i].bytes > 0 &&
+                                     (!side->items[i].dst || !side->items[i].src)))
+      return fail(SPAMM_EINVAL, "side copies: bad transfer " + std::to_string(i));
   if (!(n_occ > 0.0 && n_occ < (double)f->m.n_native))
     return fail(SPAMM_EINVAL, "n_occ must lie strictly between 0 and " +
                                   std::to_string(f->m.n_native));
@@ -1005,6 +1069,13 @@ int spamm_sp2_solve(const spamm_mat* f, double n_occ, double tau, int32_t max_it
   rep->converged = 0;
   rep->n_multiplies = 0;
   SPAMM_API_BEGIN
+  SideQueue sideq;
+  sideq.cfg = side && side->n_items > 0 ? side : nullptr;
+  struct SideScope {  // the hook lives for this solve only (also on throw)
+    SideQueue* q;
+    explicit SideScope(SideQueue* q_) : q(q_) { g_side = q_->cfg ? q_ : nullptr; }
+    ~SideScope() { g_side = nullptr; }
+  } side_scope(&sideq);
   const bool want_idem = criterion == 1;
   spamm::Mat eye;
   eye.n_native = f->m.n_native;
@@ -1050,8 +1121,11 @@ int spamm_sp2_solve(const spamm_mat* f, double n_occ, double tau, int32_t max_it
       fuse.ucount = reinterpret_cast<int64_t*>(idem_dev + 1);
       fuse.ukeys = spamm::dmalloc<int64_t>(x->m.G * x->m.G, s);
     }
+    spamm::htrace("it_mul");
     multiply_impl(x, x, tau, kernel, timed != 0, s, c->m, &st, 0, -1, nullptr, true, fuse);
+    spamm::htrace("it_mul_done");
     dead.flush();
+    spamm::htrace("it_flushed");
     bool square = true;
     double tx = 0, tsq = 0, idem = 0;
     spamm_mat* e = nullptr;
@@ -1094,7 +1168,10 @@ int spamm_sp2_solve(const spamm_mat* f, double n_occ, double tau, int32_t max_it
     pending_trace = true;
   }
   if (pending_trace) rep->trace_history[n_tr++] = spamm::trace(x->m, s);
+  g_side = nullptr;
+  sideq.drain(s);
   *p_out = x;
+  spamm::htrace_dump();
   SPAMM_API_END
 }
 

@@ -428,6 +428,7 @@ bool dense_cull(const Mat& a, const Mat& b, double tau, bool want_tasks, CullRes
   // total, [4 + t]: tier-t survivors (t < depth)
   // [aux | LPT schedule: G + 1 length bins (bin 0 = G tasks) + the K4 counter]
   // zeroed by one memset; the schedule part is handed to K4 (r.sched).
+  htrace("dc_start");
   const int world = r.world > 1 ? r.world : 1;
   const size_t aux_bytes = (4 + DENSE_MAX_DEPTH + 2 * (world + 1)) * sizeof(int64_t);
   char* zbuf = dmalloc<char>(aux_bytes + (G + 2) * sizeof(int), s);

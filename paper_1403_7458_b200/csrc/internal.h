@@ -23,7 +23,12 @@ void d2h_sync(int64_t* host, const int64_t* dev, int n, cudaStream_t s);
 // One launch copies n (<= 48) device scalars (null source -> 0) straight into
 // pinned host memory, then waits: replaces memset + D2D copies + D2H per sync.
 void gather_sync(int64_t* host, const int64_t* const* src, int n, cudaStream_t s);
+void copy_to_pinned(double* host, const double* dev, int64_t n, cudaStream_t s);
 void stream_wait(cudaStream_t s);   // spin-polls unless SPAMM_WAIT=block
+// Host-side timeline marks (SPAMM_HTRACE=1): label -> steady clock; htrace_dump
+// prints the mean host time between consecutive labels (diagnostics only).
+void htrace(const char* label);
+void htrace_dump();
 void event_wait(cudaEvent_t e);     // spin-polls
 
 // ---- quadtree matrix (device resident) ----

@@ -1,3 +1,6 @@
+#include <chrono>
+#include <map>
+#include <string>
 // K1: bit-exact Frobenius-norm pyramid + storage finalisation.
 //
 // Reference: QuadTreeMatrix._from_blocks, quadtree.py:170-194.
@@ -83,6 +86,40 @@ void event_wait(cudaEvent_t e) {
   }
 }
 
+namespace {
+struct HMark {
+  const char* label;
+  std::chrono::steady_clock::time_point t;
+};
+thread_local std::vector<HMark> g_hmarks;
+bool htrace_on() {
+  static const bool on = [] {
+    const char* v = getenv("SPAMM_HTRACE");
+    return v && *v && strcmp(v, "0") != 0;
+  }();
+  return on;
+}
+}  // namespace
+
+void htrace(const char* label) {
+  if (htrace_on()) g_hmarks.push_back({label, std::chrono::steady_clock::now()});
+}
+
+void htrace_dump() {
+  if (!htrace_on() || g_hmarks.size() < 2) return;
+  std::map<std::pair<std::string, std::string>, std::pair<long, double>> agg;
+  for (size_t i = 1; i < g_hmarks.size(); ++i) {
+    auto& a = agg[{g_hmarks[i - 1].label, g_hmarks[i].label}];
+    a.first += 1;
+    a.second += std::chrono::duration<double, std::micro>(g_hmarks[i].t - g_hmarks[i - 1].t).count();
+  }
+  fprintf(stderr, "[htrace] %zu marks\n", g_hmarks.size());
+  for (auto& [k, v] : agg)
+    fprintf(stderr, "[htrace] %-14s -> %-14s n=%5ld mean %8.2f us total %9.1f us\n",
+            k.first.c_str(), k.second.c_str(), v.first, v.second / v.first, v.second);
+  g_hmarks.clear();
+}
+
 struct ScalarSrc {
   const int64_t* p[48];
 };
@@ -104,16 +141,33 @@ void gather_sync(int64_t* host, const int64_t* const* src, int n, cudaStream_t s
   int64_t* pinned = pinned_scalars() + 32;  // (d2h_sync uses the first 32)
   k_gather_scalars<<<1, 64, 0, s>>>(ss, n, pinned);
   SPAMM_LAUNCH_CK();
+  htrace("gs_wait");
   stream_wait(s);
+  htrace("gs_done");
   for (int i = 0; i < n; ++i) host[i] = pinned[i];
 }
 
+__global__ void k_copy_f64(double* __restrict__ dst, const double* __restrict__ src, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = src[i];
+}
+
+// Small device -> pinned host copies by kernel stores (see d2h_sync).
+void copy_to_pinned(double* host, const double* dev, int64_t n, cudaStream_t s) {
+  if (n <= 0) return;
+  k_copy_f64<<<grid_for(n, 256, 148), 256, 0, s>>>(host, dev, n);
+  SPAMM_LAUNCH_CK();
+}
+
+// (a kernel store to pinned memory, not cudaMemcpyAsync: a small D2H memcpy
+// queues behind any bulk D2H on the copy engines -- ~0.8 ms instead of ~20 us
+// while pipeline.py downloads a density matrix)
 void d2h_sync(int64_t* host, const int64_t* dev, int n, cudaStream_t s) {
   if (n > 32) throw CudaError("d2h_sync: too many scalars");
-  int64_t* pinned = pinned_scalars();
-  SPAMM_CK(cudaMemcpyAsync(pinned, dev, n * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-  stream_wait(s);
-  for (int i = 0; i < n; ++i) host[i] = pinned[i];
+  const int64_t* src[32];
+  for (int i = 0; i < n; ++i) src[i] = dev + i;
+  gather_sync(host, src, n, s);
 }
 
 namespace {
@@ -732,8 +786,7 @@ void set_leaf_pyramid(Mat& m, const double* leaf_norms2, cudaStream_t s) {
   }
   if (m.host_top) {  // refresh the host mirror of the top tiers
     event_wait(m.top_ev);
-    SPAMM_CK(cudaMemcpyAsync(m.host_top, m.norms, tier_offset(m.top_t + 1) * sizeof(double),
-                             cudaMemcpyDeviceToHost, s));
+    copy_to_pinned(m.host_top, m.norms, tier_offset(m.top_t + 1), s);
     SPAMM_CK(cudaEventRecord(m.top_ev, s));
   }
 }
@@ -880,8 +933,7 @@ void finalize_impl(Mat& m, cudaStream_t s, double* pre_n2, uint8_t* pre_nz, bool
   if (m.depth >= 2 && !m.host_top) {
     m.top_t = std::min(m.depth - 1, HOST_TOP_TIERS);
     top_acquire(&m.host_top, &m.top_ev);
-    SPAMM_CK(cudaMemcpyAsync(m.host_top, m.norms, tier_offset(m.top_t + 1) * sizeof(double),
-                             cudaMemcpyDeviceToHost, s));
+    copy_to_pinned(m.host_top, m.norms, tier_offset(m.top_t + 1), s);
     SPAMM_CK(cudaEventRecord(m.top_ev, s));
   }
 }

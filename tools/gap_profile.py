@@ -62,3 +62,27 @@ for k, v in sorted(busy_by.items(), key=lambda t: -t[1])[:16]:
 print("idle by transition (ms/solve, count/solve, mean us):")
 for k, (n, t) in sorted(pairs.items(), key=lambda t: -t[1][1])[:20]:
     print(f"  {t / NS / 1e3:7.3f} {n / NS:6.1f} {t / n:7.1f}  {k[0]} -> {k[1]}")
+
+# host runtime calls issued inside the largest gap classes (what the host did)
+cpu = sorted([e for e in ev if e.get("cat") in ("cuda_runtime", "cuda_driver") and "dur" in e],
+             key=lambda e: e["ts"])
+top = sorted(pairs.items(), key=lambda t: -t[1][1])[:3]
+for (xa, ya), _ in top:
+    agg = collections.defaultdict(lambda: [0, 0.0])
+    span = nwin = 0
+    for s in solves:
+        a0, a1 = s["ts"], s["ts"] + s["dur"]
+        g = [e for e in gpu if a0 <= e["ts"] <= a1]
+        for x, y in zip(g, g[1:]):
+            if (short(x["name"]), short(y["name"])) != (xa, ya):
+                continue
+            w0, w1 = x["ts"] + x["dur"], y["ts"]
+            nwin += 1
+            span += w1 - w0
+            for c in cpu:
+                if w0 - 5 <= c["ts"] <= w1:
+                    agg[c["name"]][0] += 1
+                    agg[c["name"]][1] += c["dur"]
+    print(f"\nhost calls in gaps {xa} -> {ya} ({nwin} gaps, mean {span / max(nwin, 1):.1f} us):")
+    for k, (n, t) in sorted(agg.items(), key=lambda t: -t[1][1])[:12]:
+        print(f"  {n / max(nwin, 1):5.1f} calls/gap {t / max(nwin, 1):7.1f} us/gap  {k}")
