@@ -11,7 +11,7 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libspamm_b200.so")
+LIB_PATH = os.environ.get("SPAMM_LIB_PATH") or os.path.join(_HERE, "libspamm_b200.so")  # (override: A/B builds)
 
 SPAMM_OK = 0
 SPAMM_EINVAL = 1

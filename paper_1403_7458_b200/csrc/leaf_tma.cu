@@ -61,6 +61,35 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar)
       : "memory");
 }
+// L2 cache-policy variants (hint bit 0: operand tiles evict_last; bit 1:
+// product stores evict_first).
+__device__ __forceinline__ void tma_load_2d_pol(uint32_t dst, const CUtensorMap* map, uint32_t bar,
+                                                int c0, int c1, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3}], [%4], %5;\n" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void st2_pol(double* p, double2 v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;\n" ::"l"(p), "d"(v.x),
+               "d"(v.y), "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ void st1_pol(double* p, double v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;\n" ::"l"(p), "d"(v), "l"(pol)
+               : "memory");
+}
 __device__ __forceinline__ void dmma884(double (&c)[2], double a, double b) {
   asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
       : "+d"(c[0]), "+d"(c[1])
@@ -106,7 +135,7 @@ __global__ void __launch_bounds__(32 * (WARPS_M * WARPS_N + 1), 1)
                     int64_t n_seg, const int64_t* __restrict__ seg, const Idx* __restrict__ a_idx,
                     const Idx* __restrict__ b_idx, const int64_t* __restrict__ c_out,
                     const int64_t* __restrict__ c_mirror, int accumulate, double* __restrict__ C,
-                    const int32_t* __restrict__ order, int* __restrict__ next_block) {
+                    const int32_t* __restrict__ order, int* __restrict__ next_block, int hint) {
   using Cfg = TmaCfg<NB, WARPS_M, WARPS_N, STAGES, KS>;
   constexpr int KH = Cfg::KH;
   constexpr int WTM = NB / WARPS_M, WTN = NB / WARPS_N, MT = WTM / 8, NT = WTN / 8;
@@ -179,11 +208,23 @@ __global__ void __launch_bounds__(32 * (WARPS_M * WARPS_N + 1), 1)
               mbar_expect_tx(full(stage), Cfg::STAGE);
               const uint32_t sa = base + stage * Cfg::STAGE, sb = sa + Cfg::A_BYTES;
 #pragma unroll
-              for (int sl = 0; sl < KH / 16; ++sl)
-                tma_load_2d(sa + sl * Cfg::SLAB, &tmA, full(stage), h * KH + sl * 16, ra);
+              if (hint & 1) {
+                const uint64_t pol = policy_evict_last();
 #pragma unroll
-              for (int sl = 0; sl < NB / 16; ++sl)
-                tma_load_2d(sb + sl * Cfg::SLAB_B, &tmB, full(stage), sl * 16, rb + h * KH);
+                for (int sl = 0; sl < KH / 16; ++sl)
+                  tma_load_2d_pol(sa + sl * Cfg::SLAB, &tmA, full(stage), h * KH + sl * 16, ra, pol);
+#pragma unroll
+                for (int sl = 0; sl < NB / 16; ++sl)
+                  tma_load_2d_pol(sb + sl * Cfg::SLAB_B, &tmB, full(stage), sl * 16, rb + h * KH,
+                                  pol);
+              } else {
+#pragma unroll
+                for (int sl = 0; sl < KH / 16; ++sl)
+                  tma_load_2d(sa + sl * Cfg::SLAB, &tmA, full(stage), h * KH + sl * 16, ra);
+#pragma unroll
+                for (int sl = 0; sl < NB / 16; ++sl)
+                  tma_load_2d(sb + sl * Cfg::SLAB_B, &tmB, full(stage), sl * 16, rb + h * KH);
+              }
             }
             __syncwarp();
             if (++stage == STAGES) {
@@ -349,13 +390,27 @@ __global__ void __launch_bounds__(32 * (WARPS_M * WARPS_N + 1), 1)
     }
     if (!(md & 2)) continue;
     // last task of this C block: epilogue
+    const bool ef = hint & 2;
+    const uint64_t spol = ef ? policy_evict_first() : 0;
     if (PAIRN) {
 #pragma unroll
       for (int mt = 0; mt < MT; ++mt) {
         double* row = Cb + (row0 + mt * 8 + r8) * NB + col0 + 4 * c4;
-        *reinterpret_cast<double2*>(row) = make_double2(acc[mt][0][0], acc[mt][NT - 1][0]);
-        *reinterpret_cast<double2*>(row + 2) = make_double2(acc[mt][0][1], acc[mt][NT - 1][1]);
+        if (ef) {
+          st2_pol(row, make_double2(acc[mt][0][0], acc[mt][NT - 1][0]), spol);
+          st2_pol(row + 2, make_double2(acc[mt][0][1], acc[mt][NT - 1][1]), spol);
+        } else {
+          *reinterpret_cast<double2*>(row) = make_double2(acc[mt][0][0], acc[mt][NT - 1][0]);
+          *reinterpret_cast<double2*>(row + 2) = make_double2(acc[mt][0][1], acc[mt][NT - 1][1]);
+        }
       }
+    } else if (ef) {
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+          st2_pol(Cb + (row0 + mt * 8 + r8) * NB + col0 + nt * 8 + 2 * c4,
+                  make_double2(acc[mt][nt][0], acc[mt][nt][1]), spol);
     } else {
 #pragma unroll
       for (int mt = 0; mt < MT; ++mt)
@@ -384,12 +439,22 @@ __global__ void __launch_bounds__(32 * (WARPS_M * WARPS_N + 1), 1)
         for (int nt = 0; nt < NT; ++nt) {
           const int r = row0 + mt * 8 + r8;
           if (PAIRN) {
-            Cm[ccol(nt, 0) * NB + r] = acc[mt][nt][0];
-            Cm[ccol(nt, 1) * NB + r] = acc[mt][nt][1];
+            if (ef) {
+              st1_pol(Cm + ccol(nt, 0) * NB + r, acc[mt][nt][0], spol);
+              st1_pol(Cm + ccol(nt, 1) * NB + r, acc[mt][nt][1], spol);
+            } else {
+              Cm[ccol(nt, 0) * NB + r] = acc[mt][nt][0];
+              Cm[ccol(nt, 1) * NB + r] = acc[mt][nt][1];
+            }
           } else {
             const int c = col0 + nt * 8 + 2 * c4;
-            Cm[c * NB + r] = acc[mt][nt][0];
-            Cm[(c + 1) * NB + r] = acc[mt][nt][1];
+            if (ef) {
+              st1_pol(Cm + c * NB + r, acc[mt][nt][0], spol);
+              st1_pol(Cm + (c + 1) * NB + r, acc[mt][nt][1], spol);
+            } else {
+              Cm[c * NB + r] = acc[mt][nt][0];
+              Cm[(c + 1) * NB + r] = acc[mt][nt][1];
+            }
           }
         }
     }
@@ -532,8 +597,24 @@ void launch_tma(int64_t n_seg, const int64_t* seg, const Idx* a_idx, const Idx* 
     SPAMM_LAUNCH_CK();
     order = ord;
   }
+  static const int hint = [] {  // L2 policy bits (see tma_load_2d_pol)
+    const char* v = getenv("SPAMM_K4_HINT");
+    const char* pv = getenv("SPAMM_L2_PERSIST");
+    if (pv && atoi(pv) > 0) {  // evict_last lines live in the persisting set-aside
+      int dev = 0, mx = 0;
+      SPAMM_CK(cudaGetDevice(&dev));
+      SPAMM_CK(cudaDeviceGetAttribute(&mx, cudaDevAttrMaxPersistingL2CacheSize, dev));
+      const size_t want = std::min<size_t>((size_t)mx, (size_t)atoi(pv) << 20);
+      SPAMM_CK(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want));
+      size_t got = 0;
+      SPAMM_CK(cudaDeviceGetLimit(&got, cudaLimitPersistingL2CacheSize));
+      fprintf(stderr, "[spamm] persisting L2 set-aside %zu MiB (max %d MiB)\n", got >> 20, mx >> 20);
+    }
+    return v ? atoi(v) : 0;
+  }();
   kern<<<(unsigned)grid, Cfg::THREADS, Cfg::SMEM, s>>>(ta, tb, n_seg, seg, a_idx, b_idx, c_out,
-                                                       c_mirror, acc ? 1 : 0, C, order, counter);
+                                                       c_mirror, acc ? 1 : 0, C, order, counter,
+                                                       hint);
   SPAMM_LAUNCH_CK();
   dfree(scratch, s);
 }
