@@ -20,6 +20,7 @@
 #include <cstdio>
 #include <stdexcept>
 #include <string>
+#include <utility>
 
 namespace spamm {
 
@@ -43,6 +44,30 @@ extern std::atomic<long long> g_launch_count;
     SPAMM_CK(cudaGetLastError());                                  \
     ::spamm::g_launch_count.fetch_add(1, std::memory_order_relaxed); \
   } while (0)
+
+// Programmatic dependent launch (PDL) on the SP2 chain: a kernel launched
+// with launch_pdl may be scheduled before its stream predecessor finishes and
+// must call pdl_wait() before touching anything the predecessor writes (all
+// such kernels call it first thing).  ~2.4 us less per kernel boundary
+// (tools/pdl/pdl_bench.cu: 4.1 -> 1.7 us per dependent small kernel).
+// SPAMM_PDL=0 launches them plainly.
+bool pdl_enabled();
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+template <class... KArgs, class... Args>
+inline void launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                       Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  SPAMM_CK(cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...));
+}
 
 __host__ __device__ inline int64_t tier_offset(int t) { return ((int64_t(1) << (2 * t)) - 1) / 3; }
 __host__ __device__ inline int64_t pyramid_size(int depth) { return tier_offset(depth + 1); }

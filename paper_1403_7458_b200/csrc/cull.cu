@@ -270,6 +270,7 @@ __device__ __forceinline__ bool keep_chain(const double* __restrict__ nA,
 __global__ void __launch_bounds__(256)
     k_dense_tiers(const double* __restrict__ nA, const double* __restrict__ nB, double tau,
                   int depth, unsigned long long* __restrict__ counts) {
+  pdl_wait();
   __shared__ unsigned int sc[DENSE_MAX_DEPTH];
   if (threadIdx.x < DENSE_MAX_DEPTH) sc[threadIdx.x] = 0;
   __syncthreads();
@@ -320,6 +321,7 @@ __global__ void __launch_bounds__(CULL_THREADS)
                  int64_t* __restrict__ keys, int64_t* __restrict__ c_out,
                  int64_t* __restrict__ c_mirror, int32_t* __restrict__ order, int64_t Mn,
                  int64_t Vn, unsigned long long* __restrict__ aux) {
+  pdl_wait();
   const int64_t G = int64_t(1) << depth;
   const int lane = threadIdx.x & 31;
   const unsigned lt_mask = (1u << lane) - 1u;
@@ -439,11 +441,11 @@ bool dense_cull(const Mat& a, const Mat& b, double tau, bool want_tasks, CullRes
   SPAMM_CK(cudaMemsetAsync(zbuf, 0, aux_bytes + (G + 2) * sizeof(int), s));
   if (depth > 0) {
     const int64_t tri = ((int64_t(1) << (3 * depth)) - 1) / 7;
-    k_dense_tiers<<<grid_for(tri, 256, 148LL * 8), 256, 0, s>>>(
+    launch_pdl(k_dense_tiers, grid_for(tri, 256, 148LL * 8), 256, 0, s,
         a.norms, b.norms, tau, depth, reinterpret_cast<unsigned long long*>(aux + 4));
     SPAMM_LAUNCH_CK();
   }
-  k_dense_leaf<false><<<grid_for(npos * 32, CULL_THREADS, 148LL * 64), CULL_THREADS, 0, s>>>(
+  launch_pdl(k_dense_leaf<false>, grid_for(npos * 32, CULL_THREADS, 148LL * 64), CULL_THREADS, 0, s,
       depth, a.norms, b.norms, tau, sym ? 1 : 0, cnt, nullptr, sched, nullptr, nullptr, nullptr,
       nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, 0, 0,
       reinterpret_cast<unsigned long long*>(aux));
@@ -505,7 +507,7 @@ bool dense_cull(const Mat& a, const Mat& b, double tau, bool want_tasks, CullRes
   r.order = r.b_idx + V;
   r.sched = reinterpret_cast<int*>(zbuf);  // frees the aux + schedule buffer
   r.counter = sched + G + 1;
-  k_dense_leaf<true><<<grid_for(npos * 32, CULL_THREADS, 148LL * 64), CULL_THREADS, 0, s>>>(
+  launch_pdl(k_dense_leaf<true>, grid_for(npos * 32, CULL_THREADS, 148LL * 64), CULL_THREADS, 0, s,
       depth, a.norms, b.norms, tau, sym ? 1 : 0, nullptr, off, sched, r.ci, r.cj, r.seg, r.k,
       a.slot, b.slot, r.a_idx, r.b_idx, r.keys, r.c_out, r.c_mirror, r.order, M, V, nullptr);
   SPAMM_LAUNCH_CK();

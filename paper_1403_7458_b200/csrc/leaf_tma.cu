@@ -136,6 +136,7 @@ __global__ void __launch_bounds__(32 * (WARPS_M * WARPS_N + 1), 1)
                     const Idx* __restrict__ b_idx, const int64_t* __restrict__ c_out,
                     const int64_t* __restrict__ c_mirror, int accumulate, double* __restrict__ C,
                     const int32_t* __restrict__ order, int* __restrict__ next_block, int hint) {
+  pdl_wait();
   using Cfg = TmaCfg<NB, WARPS_M, WARPS_N, STAGES, KS>;
   constexpr int KH = Cfg::KH;
   constexpr int WTM = NB / WARPS_M, WTN = NB / WARPS_N, MT = WTM / 8, NT = WTN / 8;
@@ -475,6 +476,7 @@ __global__ void k_len_hist(const int64_t* __restrict__ seg, int64_t n, int maxle
 
 // Exclusive scan of the (maxlen + 1)-bin histogram, one 1024-thread CTA.
 __global__ void __launch_bounds__(1024) k_hist_scan(int* __restrict__ hist, int nbins) {
+  pdl_wait();
   __shared__ int warp_tot[32];
   const int per = (nbins + 1023) / 1024, b0 = threadIdx.x * per;
   int loc = 0;
@@ -591,7 +593,7 @@ void launch_tma(int64_t n_seg, const int64_t* seg, const Idx* a_idx, const Idx* 
     SPAMM_CK(cudaMemsetAsync(scratch, 0, (2 + maxlen) * sizeof(int), s));
     k_len_hist<<<grid_for(n_seg, 256), 256, 0, s>>>(seg, n_seg, maxlen, hist);
     SPAMM_LAUNCH_CK();
-    k_hist_scan<<<1, 1024, 0, s>>>(hist, maxlen + 1);
+    launch_pdl(k_hist_scan, 1, 1024, 0, s, hist, maxlen + 1);
     SPAMM_LAUNCH_CK();
     k_len_scatter<<<grid_for(n_seg, 256), 256, 0, s>>>(seg, n_seg, maxlen, hist, ord);
     SPAMM_LAUNCH_CK();
@@ -612,7 +614,7 @@ void launch_tma(int64_t n_seg, const int64_t* seg, const Idx* a_idx, const Idx* 
     }
     return v ? atoi(v) : 0;
   }();
-  kern<<<(unsigned)grid, Cfg::THREADS, Cfg::SMEM, s>>>(ta, tb, n_seg, seg, a_idx, b_idx, c_out,
+  launch_pdl(kern, (unsigned)grid, Cfg::THREADS, Cfg::SMEM, s, ta, tb, n_seg, seg, a_idx, b_idx, c_out,
                                                        c_mirror, acc ? 1 : 0, C, order, counter,
                                                        hint);
   SPAMM_LAUNCH_CK();
@@ -645,7 +647,7 @@ void leaf_products_tma(int64_t n_seg, const int64_t* seg, const Idx* a_idx, cons
 }
 
 void hist_scan_exclusive(int* hist, int nbins, cudaStream_t s) {
-  k_hist_scan<<<1, 1024, 0, s>>>(hist, nbins);
+  launch_pdl(k_hist_scan, 1, 1024, 0, s, hist, nbins);
   SPAMM_LAUNCH_CK();
 }
 

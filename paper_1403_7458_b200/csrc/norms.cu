@@ -62,12 +62,24 @@ void reserve_pool(size_t bytes, cudaStream_t s) {
 // Host wait for the stream: polls cudaStreamQuery (about 10 us less wake-up
 // latency per wait than a blocking synchronize, ~0.5 ms per cfg4 SP2 solve);
 // SPAMM_WAIT=block selects cudaStreamSynchronize.
-void stream_wait(cudaStream_t s) {
-  static const bool spin = [] {
-    const char* v = getenv("SPAMM_WAIT");
-    return !(v && strcmp(v, "block") == 0);
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* v = getenv("SPAMM_PDL");
+    return !(v && strcmp(v, "0") == 0);
   }();
-  if (!spin) {
+  return on;
+}
+
+bool wait_blocking() {
+  static const bool block = [] {
+    const char* v = getenv("SPAMM_WAIT");
+    return v && strcmp(v, "block") == 0;
+  }();
+  return block;
+}
+
+void stream_wait(cudaStream_t s) {
+  if (wait_blocking()) {
     SPAMM_CK(cudaStreamSynchronize(s));
     return;
   }
@@ -123,9 +135,16 @@ void htrace_dump() {
 struct ScalarSrc {
   const int64_t* p[48];
 };
-__global__ void k_gather_scalars(ScalarSrc src, int n, int64_t* dst) {
+// Writes the scalars, then (after a system-scope fence) the sequence number
+// the host spins on: the host sees completion as soon as the PCIe writes land,
+// without a driver round trip per poll.
+__global__ void k_gather_scalars(ScalarSrc src, int n, int64_t* dst, int64_t* flag, int64_t seq) {
+  pdl_wait();
   const int i = threadIdx.x;
   if (i < n) dst[i] = src.p[i] ? *src.p[i] : 0;
+  __threadfence_system();
+  __syncthreads();
+  if (i == 0) *reinterpret_cast<volatile int64_t*>(flag) = seq;
 }
 
 int64_t* pinned_scalars() {
@@ -138,11 +157,26 @@ void gather_sync(int64_t* host, const int64_t* const* src, int n, cudaStream_t s
   if (n > 48) throw CudaError("gather_sync: too many scalars");
   ScalarSrc ss{};
   for (int i = 0; i < n; ++i) ss.p[i] = src[i];
-  int64_t* pinned = pinned_scalars() + 32;  // (d2h_sync uses the first 32)
-  k_gather_scalars<<<1, 64, 0, s>>>(ss, n, pinned);
+  int64_t* pinned = pinned_scalars() + 32;  // values [32, 80), sequence flag [80]
+  volatile int64_t* flag = pinned_scalars() + 80;
+  static thread_local int64_t seq = 0;
+  ++seq;
+  launch_pdl(k_gather_scalars, 1, 64, 0, s, ss, n, pinned, const_cast<int64_t*>(flag), seq);
   SPAMM_LAUNCH_CK();
   htrace("gs_wait");
-  stream_wait(s);
+  if (wait_blocking()) {
+    stream_wait(s);
+  } else {
+    // spin on the flag; every 4096 polls ask the driver (surfaces a failed
+    // kernel, and ends the wait if the stream completed)
+    for (unsigned spins = 1; *flag != seq; ++spins) {
+      if ((spins & 4095u) == 0) {
+        const cudaError_t e = cudaStreamQuery(s);
+        if (e == cudaSuccess) break;
+        if (e != cudaErrorNotReady) SPAMM_CK(e);
+      }
+    }
+  }
   htrace("gs_done");
   for (int i = 0; i < n; ++i) host[i] = pinned[i];
 }
@@ -375,6 +409,7 @@ __global__ void __launch_bounds__(FS_THREADS)
                      const double* __restrict__ dn2, const double* __restrict__ xleaf2,
                      double* __restrict__ idem_out, const int32_t* __restrict__ xslot = nullptr,
                      int64_t* __restrict__ ukeys = nullptr, int64_t* __restrict__ ucount = nullptr) {
+  pdl_wait();
   extern __shared__ __align__(16) double p2[];  // squared pyramid, tiers 0..depth
   __shared__ int32_t dslot[128];
   __shared__ double part[128];
@@ -520,14 +555,14 @@ void launch_finalize_small(int depth, int nb, cudaStream_t s, Args... args) {
                                (size_t)(G * nb) * sizeof(double) + (size_t)(G * G) + 64);
   if (smem > 220 * 1024) throw CudaError("finalize: shared memory budget exceeded");
   if (depth <= 6 && smem <= 48 * 1024) {
-    k_finalize_small<4><<<3, FS_THREADS, smem, s>>>(args...);
+    launch_pdl(k_finalize_small<4>, 3, FS_THREADS, smem, s, args...);
   } else {
     static std::once_flag once;
     std::call_once(once, [] {
       SPAMM_CK(cudaFuncSetAttribute(k_finalize_small<16>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     });
-    k_finalize_small<16><<<3, FS_THREADS, smem, s>>>(args...);
+    launch_pdl(k_finalize_small<16>, 3, FS_THREADS, smem, s, args...);
   }
   SPAMM_LAUNCH_CK();
 }
@@ -630,6 +665,7 @@ __global__ void __launch_bounds__(32 * WARPS)
                      const int32_t* __restrict__ xslot, double* __restrict__ out,
                      uint8_t* __restrict__ nz, double* __restrict__ dout,
                      double* __restrict__ out1) {
+  pdl_wait();
   constexpr int NCH = NB2 / 256, BPW = 2;
   __shared__ __align__(16) double rows_all[WARPS][BPW * 4 * CHAIN_ROW];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -834,10 +870,10 @@ void finalize_impl(Mat& m, cudaStream_t s, double* pre_n2, uint8_t* pre_nz, bool
         constexpr int WARPS = 4;
         const int grid = grid_for((m.nblocks + 1) / 2 * 32, 32 * WARPS, 1LL << 20);
         if (nb2 == 4096)
-          k_leaf_norms2_cd<4096, WARPS><<<grid, 32 * WARPS, 0, s>>>(
+          launch_pdl(k_leaf_norms2_cd<4096, WARPS>, grid, 32 * WARPS, 0, s,
               m.data, m.keys, m.nblocks, idem.x->data, idem.x->slot, n2, nz, dn2, n1);
         else
-          k_leaf_norms2_cd<1024, WARPS><<<grid, 32 * WARPS, 0, s>>>(
+          launch_pdl(k_leaf_norms2_cd<1024, WARPS>, grid, 32 * WARPS, 0, s,
               m.data, m.keys, m.nblocks, idem.x->data, idem.x->slot, n2, nz, dn2, n1);
         SPAMM_LAUNCH_CK();
       } else {

@@ -70,6 +70,7 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_tile_sums(const T* in, int64_t
 template <class T>
 __global__ void __launch_bounds__(SCAN_THREADS)
     k_tile_scan(const T* in, int64_t n, const int64_t* tile_off, int64_t* out) {
+  pdl_wait();
   const int64_t base = (int64_t)blockIdx.x * SCAN_TILE + (int64_t)threadIdx.x * SCAN_ITEMS;
   int64_t v[SCAN_ITEMS];
   int64_t sum = 0;
@@ -101,7 +102,7 @@ void scan_impl(const T* in, int64_t n, int64_t* out, cudaStream_t s) {
   }
   const int64_t tiles = (n + SCAN_TILE - 1) / SCAN_TILE;
   if (tiles == 1) {
-    k_tile_scan<T><<<1, SCAN_THREADS, 0, s>>>(in, n, nullptr, out);
+    launch_pdl(k_tile_scan<T>, 1, SCAN_THREADS, 0, s, in, n, nullptr, out);
     SPAMM_LAUNCH_CK();
     return;
   }
@@ -110,7 +111,7 @@ void scan_impl(const T* in, int64_t n, int64_t* out, cudaStream_t s) {
   k_tile_sums<T><<<(unsigned)tiles, SCAN_THREADS, 0, s>>>(in, n, sums);
   SPAMM_LAUNCH_CK();
   scan_impl<int64_t>(sums, tiles, offs, s);
-  k_tile_scan<T><<<(unsigned)tiles, SCAN_THREADS, 0, s>>>(in, n, offs, out);
+  launch_pdl(k_tile_scan<T>, (unsigned)tiles, SCAN_THREADS, 0, s, in, n, offs, out);
   SPAMM_LAUNCH_CK();
   dfree(sums, s);
   dfree(offs, s);

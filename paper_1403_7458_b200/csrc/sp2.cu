@@ -86,6 +86,7 @@ __global__ void __launch_bounds__(32 * WARPS)
                        const int32_t* __restrict__ sx2, double* __restrict__ E,
                        double* __restrict__ nD2, double* __restrict__ nE2,
                        uint8_t* __restrict__ nzE, double* __restrict__ nE1) {
+  pdl_wait();
   constexpr int NCH = NB2 / 256;
   __shared__ __align__(16) double rows_all[WARPS][BPW * 4 * CHAIN_ROW];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -189,13 +190,13 @@ void launch_update(bool idem, bool expand, const int64_t* ukeys, int64_t U, cons
   constexpr int BPW = 2, WARPS = 4;
   const int grid = grid_for((U + BPW - 1) / BPW * 32, 32 * WARPS, 1LL << 20);
   if (idem && expand)
-    k_sp2_update_multi<NB2, true, true, BPW, WARPS><<<grid, 32 * WARPS, 0, s>>>(
+    launch_pdl(k_sp2_update_multi<NB2, true, true, BPW, WARPS>, grid, 32 * WARPS, 0, s,
         ukeys, U, x.data, x.slot, x2.data, x2.slot, E, nD2, nE2, nzE, nE1);
   else if (idem)
-    k_sp2_update_multi<NB2, true, false, BPW, WARPS><<<grid, 32 * WARPS, 0, s>>>(
+    launch_pdl(k_sp2_update_multi<NB2, true, false, BPW, WARPS>, grid, 32 * WARPS, 0, s,
         ukeys, U, x.data, x.slot, x2.data, x2.slot, E, nD2, nE2, nzE, nE1);
   else
-    k_sp2_update_multi<NB2, false, true, BPW, WARPS><<<grid, 32 * WARPS, 0, s>>>(
+    launch_pdl(k_sp2_update_multi<NB2, false, true, BPW, WARPS>, grid, 32 * WARPS, 0, s,
         ukeys, U, x.data, x.slot, x2.data, x2.slot, E, nD2, nE2, nzE, nE1);
   SPAMM_LAUNCH_CK();
 }
