@@ -18,7 +18,7 @@ SPAMM_EINVAL = 1
 SPAMM_ECUDA = 2
 MAX_TIERS = 64
 
-LEAF_KERNELS = {"auto": 0, "dmma": 1, "exact": 2, "dmma_cpasync": 3}
+LEAF_KERNELS = {"auto": 0, "dmma": 1, "exact": 2, "dmma_cpasync": 3, "ozaki": 4}
 
 c_i32 = ctypes.c_int32
 c_i64 = ctypes.c_int64

@@ -426,7 +426,9 @@ int spamm_multiply(const spamm_mat* a, const spamm_mat* b, double tau, int32_t k
   if (int rc = check_conformable(a, b)) return rc;
   if (!(tau >= 0.0) || tau == __builtin_inf())
     return fail(SPAMM_EINVAL, "tau must be finite and >= 0, got " + std::to_string(tau));
-  if (kernel < 0 || kernel > 3) return fail(SPAMM_EINVAL, "unknown leaf kernel");
+  if (kernel < 0 || kernel > 4) return fail(SPAMM_EINVAL, "unknown leaf kernel");
+  if (kernel == SPAMM_LEAF_OZAKI && !spamm::ozaki_supported(a->m.nb))
+    return fail(SPAMM_EINVAL, "INT8-sliced leaf kernel needs block size 64");
   if ((kernel == SPAMM_LEAF_DMMA || kernel == 3) && !spamm::dmma_supported(a->m.nb))
     return fail(SPAMM_EINVAL, "DMMA leaf kernel needs block size 8, 16, 32 or 64");
   if (!c) return fail(SPAMM_EINVAL, "null output handle");
@@ -446,6 +448,20 @@ int spamm_multiply(const spamm_mat* a, const spamm_mat* b, double tau, int32_t k
 }  // extern "C"
 
 namespace {
+
+// K4 dispatch: the INT8-sliced kernel takes the operand matrices (row / column
+// exponents from their keys), the others the block arrays.
+void leaf_dispatch(int64_t n, const int64_t* seg, const int32_t* ai, const int32_t* bi,
+                   const int64_t* c_out, const int64_t* c_mirror, const spamm_mat* a,
+                   const spamm_mat* b, double* C, int32_t kernel, cudaStream_t s,
+                   spamm::LptSchedule lpt) {
+  if (kernel == spamm::LEAF_OZAKI)
+    spamm::leaf_products_ozaki<int32_t>(n, seg, ai, bi, c_out, c_mirror, false, a->m, b->m,
+                                        a == b && a->m.sym, C, s, lpt);
+  else
+    spamm::leaf_products<int32_t>(n, seg, ai, bi, c_out, c_mirror, false, a->m.data, a->m.nblocks,
+                                  b->m.data, b->m.nblocks, C, a->m.nb, kernel, s, lpt);
+}
 
 void multiply_impl(const spamm_mat* a, const spamm_mat* b, double tau, int32_t kernel, bool timed,
                    cudaStream_t s, spamm::Mat& C, spamm_stats* stats, int64_t lo, int64_t hi,
@@ -509,9 +525,7 @@ void multiply_impl(const spamm_mat* a, const spamm_mat* b, double tau, int32_t k
     spamm::LptSchedule lpt;
     lpt.order = r.order;
     lpt.counter = r.counter;
-    spamm::leaf_products<int32_t>(r.n_c, r.seg, r.a_idx, r.b_idx, c_out, c_mirror, false,
-                                  a->m.data, a->m.nblocks, b->m.data, b->m.nblocks, C.data, C.nb,
-                                  kernel, s, lpt);
+    leaf_dispatch(r.n_c, r.seg, r.a_idx, r.b_idx, c_out, c_mirror, a, b, C.data, kernel, s, lpt);
   }
   tm.mark(2);
   spamm::htrace("mul_k4");
@@ -597,9 +611,8 @@ void multiply_shard_impl(const spamm_mat* a, double tau, int32_t kernel, cudaStr
   }
   const int64_t n_lo = r.node_cut[rank], n_hi = r.node_cut[rank + 1];
   if (n_hi > n_lo) {
-    spamm::leaf_products<int32_t>(n_hi - n_lo, r.seg + n_lo, r.a_idx, r.b_idx, c_out + n_lo,
-                                  r.c_mirror ? r.c_mirror + n_lo : nullptr, false, a->m.data,
-                                  a->m.nblocks, a->m.data, a->m.nblocks, C.data, C.nb, kernel, s);
+    leaf_dispatch(n_hi - n_lo, r.seg + n_lo, r.a_idx, r.b_idx, c_out + n_lo,
+                  r.c_mirror ? r.c_mirror + n_lo : nullptr, a, a, C.data, kernel, s, {});
   }
   spamm::dfree(ident, s);
   for (int i = 0; i <= world; ++i) cut_pos[i] = r.cut_pos[i];
@@ -695,7 +708,9 @@ int spamm_sp2_step(const spamm_mat* x, double n_occ, double tau, int32_t kernel,
     return fail(SPAMM_EINVAL, "null argument");
   if (!(tau >= 0.0) || tau == __builtin_inf())
     return fail(SPAMM_EINVAL, "tau must be finite and >= 0, got " + std::to_string(tau));
-  if (kernel < 0 || kernel > 3) return fail(SPAMM_EINVAL, "unknown leaf kernel");
+  if (kernel < 0 || kernel > 4) return fail(SPAMM_EINVAL, "unknown leaf kernel");
+  if (kernel == SPAMM_LEAF_OZAKI && !spamm::ozaki_supported(x->m.nb))
+    return fail(SPAMM_EINVAL, "INT8-sliced leaf kernel needs block size 64");
   if ((kernel == SPAMM_LEAF_DMMA || kernel == 3) && !spamm::dmma_supported(x->m.nb))
     return fail(SPAMM_EINVAL, "DMMA leaf kernel needs block size 8, 16, 32 or 64");
   SPAMM_API_BEGIN
@@ -736,7 +751,9 @@ int spamm_sp2_multiply_shard(const spamm_mat* x, double tau, int32_t kernel, int
     return fail(SPAMM_EINVAL, "rank/world out of range (world <= 16)");
   if (!(tau >= 0.0) || tau == __builtin_inf())
     return fail(SPAMM_EINVAL, "tau must be finite and >= 0, got " + std::to_string(tau));
-  if (kernel < 0 || kernel > 3) return fail(SPAMM_EINVAL, "unknown leaf kernel");
+  if (kernel < 0 || kernel > 4) return fail(SPAMM_EINVAL, "unknown leaf kernel");
+  if (kernel == SPAMM_LEAF_OZAKI && !spamm::ozaki_supported(x->m.nb))
+    return fail(SPAMM_EINVAL, "INT8-sliced leaf kernel needs block size 64");
   if (x->m.depth > 8) return fail(SPAMM_EINVAL, "sharded SP2 products need depth <= 8");
   SPAMM_API_BEGIN
   auto* h = new spamm_mat();
@@ -809,7 +826,9 @@ int spamm_multiply_range(const spamm_mat* a, const spamm_mat* b, double tau, int
   if (int rc = check_conformable(a, b)) return rc;
   if (!(tau >= 0.0) || tau == __builtin_inf())
     return fail(SPAMM_EINVAL, "tau must be finite and >= 0, got " + std::to_string(tau));
-  if (kernel < 0 || kernel > 3) return fail(SPAMM_EINVAL, "unknown leaf kernel");
+  if (kernel < 0 || kernel > 4) return fail(SPAMM_EINVAL, "unknown leaf kernel");
+  if (kernel == SPAMM_LEAF_OZAKI && !spamm::ozaki_supported(a->m.nb))
+    return fail(SPAMM_EINVAL, "INT8-sliced leaf kernel needs block size 64");
   if (lo < 0 || hi < lo || hi > a->m.G * a->m.G)
     return fail(SPAMM_EINVAL, "shard range outside [0, G*G]");
   if (!c) return fail(SPAMM_EINVAL, "null output handle");
@@ -1044,7 +1063,9 @@ int spamm_sp2_solve_ex(const spamm_mat* f, double n_occ, double tau, int32_t max
   if (!(tau >= 0.0) || tau == __builtin_inf())
     return fail(SPAMM_EINVAL, "tau must be finite and >= 0, got " + std::to_string(tau));
   if (criterion != 0 && criterion != 1) return fail(SPAMM_EINVAL, "unknown criterion");
-  if (kernel < 0 || kernel > 3) return fail(SPAMM_EINVAL, "unknown leaf kernel");
+  if (kernel < 0 || kernel > 4) return fail(SPAMM_EINVAL, "unknown leaf kernel");
+  if (kernel == SPAMM_LEAF_OZAKI && !spamm::ozaki_supported(f->m.nb))
+    return fail(SPAMM_EINVAL, "INT8-sliced leaf kernel needs block size 64");
   if ((kernel == SPAMM_LEAF_DMMA || kernel == 3) && !spamm::dmma_supported(f->m.nb))
     return fail(SPAMM_EINVAL, "DMMA leaf kernel needs block size 8, 16, 32 or 64");
   if (max_iter < 0) return fail(SPAMM_EINVAL, "max_iter must be >= 0");

@@ -174,7 +174,7 @@ bool cull(const Mat& a, const Mat& b, double tau, bool want_tasks, CullResult& r
 // LEAF_DMMA_CPASYNC: the first-generation DMMA kernel (cp.async ring, one CTA
 // per C block), kept for A/B measurements; AUTO/DMMA use the TMA kernel for
 // Nb in {32, 64}.
-enum LeafKernel { LEAF_AUTO = 0, LEAF_DMMA = 1, LEAF_EXACT = 2, LEAF_DMMA_CPASYNC = 3 };
+enum LeafKernel { LEAF_AUTO = 0, LEAF_DMMA = 1, LEAF_EXACT = 2, LEAF_DMMA_CPASYNC = 3, LEAF_OZAKI = 4 };
 // For each segment m: C[c_out ? c_out[m] : m] (+)= sum_{t in seg m} A[a_idx[t]] * B[b_idx[t]]
 // and, when c_mirror && c_mirror[m] >= 0, C[c_mirror[m]] = transpose of that block.
 // a_blocks / b_blocks: number of blocks addressable in A / B (TMA bounds).
@@ -193,6 +193,21 @@ bool dmma_supported(int nb);
 // In-place exclusive scan of a small int histogram (one CTA, nbins <= ~1M).
 void hist_scan_exclusive(int* hist, int nbins, cudaStream_t s);
 bool tma_leaf_supported(int nb);
+int multiprocessors();
+// LPT order of the n_seg segments (longest first) plus a zeroed work counter;
+// returns the scratch allocation holding both (dfree it after the launch).
+int* lpt_schedule(int64_t n_seg, const int64_t* seg, const int32_t** order, int** counter,
+                  cudaStream_t s);
+// K4z (leaf_ozaki.cu, Nb = 64): the leaf products on the INT8 tensor cores by
+// exact digit slicing (Ozaki scheme I).  Needs the operand matrices (their
+// keys give the global row / column exponents); sym_b: B is A and A == A^T,
+// so B's transposed slices are A's slices of the mirror block.
+bool ozaki_supported(int nb);
+template <class Idx>
+void leaf_products_ozaki(int64_t n_seg, const int64_t* seg, const Idx* a_idx, const Idx* b_idx,
+                         const int64_t* c_out, const int64_t* c_mirror, bool accumulate,
+                         const Mat& A, const Mat& B, bool sym_b, double* C, cudaStream_t s,
+                         LptSchedule lpt = {});
 template <class Idx>
 void leaf_products_tma(int64_t n_seg, const int64_t* seg, const Idx* a_idx, const Idx* b_idx,
                        const int64_t* c_out, const int64_t* c_mirror, bool accumulate,

@@ -250,6 +250,8 @@ void leaf_products(int64_t n_seg, const int64_t* seg, const Idx* a_idx, const Id
                    double* C, int nb, int kernel, cudaStream_t s, LptSchedule lpt) {
   if (n_seg <= 0) return;
   if (n_seg > 0x7fffffffLL) throw CudaError("too many C blocks for one launch");
+  if (kernel == LEAF_OZAKI)
+    throw CudaError("the INT8-sliced leaf kernel needs matrix operands (row/column exponents)");
   if ((kernel == LEAF_AUTO || kernel == LEAF_DMMA) && tma_leaf_supported(nb)) {
     leaf_products_tma<Idx>(n_seg, seg, a_idx, b_idx, c_out, c_mirror, accumulate, A, a_blocks, B,
                            b_blocks, C, nb, s, lpt);

@@ -1,0 +1,596 @@
+// K4z (Nb = 64): the leaf products on the INT8 tensor cores (tcgen05.mma
+// kind::i8, accumulators in TMEM) by exact digit slicing -- Ozaki scheme I.
+//
+// Reference: _gemm_acc / _gemm_batch (kernel.py:64-77); same contract as the
+// DMMA kernel K4 (leaf_tma.cu): the tasks of one C block (k ascending) are
+// reduced by one CTA, deterministically, no atomics.  The arithmetic differs:
+//
+//  * every operand row r (A) / column c (B) gets one power-of-two scale 2^E
+//    (E: frexp exponent of the largest |x| in that global row / column over
+//    all stored blocks, k_oz_exponents), and x 2^-E is written with 8 signed
+//    int8 digits x = 2^E (s_0 2^-7 + sum_{p=1..7} s_p 2^-(7+8p)), s_p in
+//    [-128, 127] (k_oz_split: floor digits, then a carry pass from the bottom
+//    -- every step exact; 63 bits, the remainder is < 2^(E-63));
+//  * a digit product sum_k dA_p[r][k] dB_q[k][c] is computed EXACTLY in int32
+//    on the tensor cores and summed exactly over the tasks of the C block
+//    (|.| <= 4 x 64 x 2^14 = 2^22 per task and quadrant, so chunks of
+//    OZ_CHUNK = 256 tasks are flushed to FP64);
+//  * all digit pairs p + q <= 7 (and four of p + q = 8) are formed: A slices
+//    stacked two per MMA along M (rows 0-63 = s_p, 64-127 = s_p+1), B slices
+//    two per MMA along N, 10 MMAs of 128x128x64 per task into 4 TMEM tiles of
+//    128 columns (tile t holds the pairs of digit sums 2t, 2t+1, 2t+2 in its
+//    four quadrants) -- all 512 TMEM columns;
+//  * the epilogue adds the quadrants of equal digit sum d in int64 (exact),
+//    so S_d[r][c] = S_d[c][r] bitwise for a symmetric operand, and rounds once
+//    per d: C = 2^(Er+Ec-14) sum_d S_d 2^-8d (Horner with fused multiply-add).
+//
+// Error: the dropped pairs (p + q >= 8) weigh <= 2^-64 K max|A_r| max|B_c|
+// per element, below the FP64 rounding of the sum: measured 5-6e-17 relative
+// Frobenius error against an extended-precision product, vs 4-6e-16 for a
+// plain FP64 product (7-bit balanced digits, 4 tiles: 1e-14 -- the dropped
+// pairs there weigh 2^-56 and add up systematically on the diagonal of X*X).
+// Results are deterministic and exactly symmetric (diagonal blocks of X*X
+// bitwise symmetric), not bitwise the DMMA kernel's.
+//
+// Operand traffic per task is the FP64 kernel's (8 slices x 4 KB = 32 KB per
+// block), compute per task is 20 tcgen05 MMAs of 128x128x32 = 1,280 tensor
+// cycles versus ~4,100 cycles of DMMA at 64x64x64.
+#include <climits>
+#include <mutex>
+
+#include "internal.h"
+
+namespace spamm {
+
+namespace {
+
+constexpr int OZ_NB = 64;
+constexpr int OZ_SLICES = 8;
+constexpr int OZ_SLICE_BYTES = OZ_NB * OZ_NB;                  // 4 KB (int8)
+constexpr int OZ_BLOCK_BYTES = OZ_SLICES * OZ_SLICE_BYTES;     // 32 KB
+constexpr int OZ_STAGES = 3;
+constexpr int OZ_STAGE = 2 * OZ_BLOCK_BYTES;                   // A + B slices of one task
+constexpr int OZ_CHUNK = 256;       // tasks per TMEM accumulation (int32 headroom: 512)
+constexpr int OZ_EPI = 128;         // epilogue threads (warps 0-3 <-> TMEM lane quarters)
+constexpr int OZ_THREADS = OZ_EPI + 64;  // + producer warp (4) + MMA warp (5)
+constexpr int OZ_XBUF = 32 * OZ_EPI * 4;  // epilogue exchange: 32 ints per thread
+constexpr size_t OZ_SMEM = 1024 + (size_t)OZ_STAGES * OZ_STAGE + OZ_XBUF + 256;
+constexpr int OZ_EXP_NONE = (int)0x80808080;  // memset pattern: "no nonzero seen"
+
+// Byte offset of element (n, k) of a 64x64 int8 slice in the UMMA K-major
+// no-swizzle canonical layout: 8-row x 16-byte core matrices (128 B), the
+// four k-chunks of an 8-row group adjacent (LBO = 128 B), row groups 512 B
+// apart (SBO) -- so two consecutive slices form one 128-row operand.
+__host__ __device__ constexpr int oz_off(int n, int k) {
+  return (n >> 3) * 512 + (k >> 4) * 128 + (n & 7) * 16 + (k & 15);
+}
+
+__device__ __forceinline__ int oz_exp(int e) { return e == OZ_EXP_NONE ? 0 : e; }
+// Row / column exponent E: max |x| < 2^E, bumped when the mantissa is within
+// 2^-7.5 of 1 so that |x 2^(7-E)| <= 127.25 -- the leading signed digit then
+// stays in [-128, 127] after the carry from the tail.
+__device__ __forceinline__ int oz_frexp(double mx) {
+  int e;
+  const double f = frexp(mx, &e);
+  return f >= 0.994140625 ? e + 1 : e;
+}
+
+// ex[g] = max frexp exponent of |x| over global row g (by_col = 0) or global
+// column g (by_col = 1) of the stored blocks.
+__global__ void __launch_bounds__(256) k_oz_exponents(const double* __restrict__ data,
+                                                      const int64_t* __restrict__ keys,
+                                                      int64_t nblocks, int64_t G, int by_col,
+                                                      int* __restrict__ ex) {
+  pdl_wait();
+  __shared__ double red[4][OZ_NB];
+  const int t = threadIdx.x, w = t >> 5, l = t & 31;
+  for (int64_t s = blockIdx.x; s < nblocks; s += gridDim.x) {
+    const double* b = data + s * (OZ_NB * OZ_NB);
+    const int64_t key = keys[s];
+    if (by_col) {
+      double mx = 0.0;
+#pragma unroll 4
+      for (int i = 0; i < 16; ++i) mx = fmax(mx, fabs(b[((t >> 6) + 4 * i) * OZ_NB + (t & 63)]));
+      red[t >> 6][t & 63] = mx;
+      __syncthreads();
+      if (t < OZ_NB) {
+        mx = fmax(fmax(red[0][t], red[1][t]), fmax(red[2][t], red[3][t]));
+        if (mx > 0.0) atomicMax(ex + (key % G) * OZ_NB + t, oz_frexp(mx));
+      }
+      __syncthreads();
+    } else {
+      for (int r = w * 8; r < w * 8 + 8; ++r) {
+        const double2 v = reinterpret_cast<const double2*>(b + r * OZ_NB)[l];
+        double mx = fmax(fabs(v.x), fabs(v.y));
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        if (l == 0 && mx > 0.0) atomicMax(ex + (key / G) * OZ_NB + r, oz_frexp(mx));
+      }
+    }
+  }
+}
+
+// out + s * 32 KB: the 8 digit slices of block s.  trans = 0 (A role): slice
+// row n = block row n, exponent of global row bi*64+n; trans = 1 (B role,
+// K-major B^T): slice row n = block column n, exponent of global column bj*64+n.
+__global__ void __launch_bounds__(256) k_oz_split(const double* __restrict__ data,
+                                                  const int64_t* __restrict__ keys,
+                                                  int64_t nblocks, int64_t G, int trans,
+                                                  const int* __restrict__ ex,
+                                                  int8_t* __restrict__ out) {
+  pdl_wait();
+  __shared__ double tile[OZ_NB * (OZ_NB + 1)];
+  const int t = threadIdx.x, n = t >> 2, kc = t & 3;
+  for (int64_t s = blockIdx.x; s < nblocks; s += gridDim.x) {
+    const double* b = data + s * (OZ_NB * OZ_NB);
+    for (int i = t; i < OZ_NB * OZ_NB; i += 256) tile[(i >> 6) * (OZ_NB + 1) + (i & 63)] = b[i];
+    __syncthreads();
+    const int64_t key = keys[s];
+    const int64_t g = trans ? key % G : key / G;
+    const int e = oz_exp(ex[g * OZ_NB + n]);
+    uint32_t dig[OZ_SLICES][4];
+#pragma unroll
+    for (int p = 0; p < OZ_SLICES; ++p)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) dig[p][q] = 0u;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const int k = kc * 16 + i;
+      double y = trans ? tile[k * (OZ_NB + 1) + n] : tile[n * (OZ_NB + 1) + k];
+      // x 2^-E = s_0 2^-7 + sum_{p>=1} s_p 2^-(7+8p): floor digits (unsigned
+      // 8-bit tail), then signed with carries from the bottom -- every step exact.
+      double t = ldexp(y, 7 - e);  // |t| <= 127.25 (exponent bump in k_oz_exponents)
+      const double d0 = floor(t);
+      double r = __dsub_rn(t, d0);  // [0, 1)
+      int u[OZ_SLICES];
+#pragma unroll
+      for (int p = 1; p < OZ_SLICES; ++p) {
+        t = __dmul_rn(r, 256.0);
+        const double f = floor(t);
+        r = __dsub_rn(t, f);
+        u[p] = (int)f;  // [0, 255]
+      }
+      int c = 0;
+#pragma unroll
+      for (int p = OZ_SLICES - 1; p >= 1; --p) {
+        const int v = u[p] + c;
+        c = v >= 128 ? 1 : 0;
+        u[p] = v - 256 * c;  // [-128, 127]
+      }
+      u[0] = (int)d0 + c;  // [-128, 127]
+#pragma unroll
+      for (int p = 0; p < OZ_SLICES; ++p)
+        dig[p][i >> 2] |= ((uint32_t)u[p] & 0xffu) << (8 * (i & 3));
+    }
+    int8_t* o = out + s * OZ_BLOCK_BYTES + oz_off(n, kc * 16);
+#pragma unroll
+    for (int p = 0; p < OZ_SLICES; ++p)
+      *reinterpret_cast<uint4*>(o + p * OZ_SLICE_BYTES) =
+          make_uint4(dig[p][0], dig[p][1], dig[p][2], dig[p][3]);
+    __syncthreads();
+  }
+}
+
+// tr[s] = storage slot of the transposed block of s (symmetric operands).
+__global__ void k_oz_trslot(const int64_t* __restrict__ keys, int64_t nblocks, int64_t G,
+                            const int32_t* __restrict__ slot, int32_t* __restrict__ tr) {
+  pdl_wait();
+  for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < nblocks;
+       s += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t key = keys[s];
+    tr[s] = slot[(key % G) * G + key / G];
+  }
+}
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  uint32_t ok = 0;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity)
+        : "memory");
+  } while (!ok);
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes,
+                                         uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::
+          "r"(dst),
+      "l"(src), "r"(bytes), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void tc_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+}
+__device__ __forceinline__ void tc_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+}
+// Shared-memory matrix descriptor: K-major, no swizzle, LBO 128 B, SBO 512 B,
+// version 1 (sm_100).
+__device__ __forceinline__ uint64_t oz_desc(uint32_t addr) {
+  return (uint64_t)((addr >> 4) & 0x3FFFu) | ((uint64_t)(128 >> 4) << 16) |
+         ((uint64_t)(512 >> 4) << 32) | (1ull << 46);
+}
+// Instruction descriptor: D s32, A/B signed int8, both K-major, N = 128, M = 128.
+constexpr uint32_t OZ_IDESC =
+    (2u << 4) | (1u << 7) | (1u << 10) | ((128u >> 3) << 17) | ((128u >> 4) << 24);
+__device__ __forceinline__ void oz_mma(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t acc) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(OZ_IDESC), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void oz_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::
+                   "r"(bar)
+               : "memory");
+}
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, int (&v)[8]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];\n"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7])
+      : "r"(taddr));
+}
+// tcgen05.wait::ld, with the loaded registers threaded through so no use of
+// them can be scheduled above the wait.
+__device__ __forceinline__ void tmem_wait8(int (&v)[8]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n"
+               : "+r"(v[0]), "+r"(v[1]), "+r"(v[2]), "+r"(v[3]), "+r"(v[4]), "+r"(v[5]),
+                 "+r"(v[6]), "+r"(v[7])
+               :
+               : "memory");
+}
+__device__ __forceinline__ void tmem_keep8(int (&v)[8]) {
+  asm volatile(""
+               : "+r"(v[0]), "+r"(v[1]), "+r"(v[2]), "+r"(v[3]), "+r"(v[4]), "+r"(v[5]),
+                 "+r"(v[6]), "+r"(v[7]));
+}
+
+// The 10 slice-pair MMAs of one task: A pair start p, B pair start q (tile (p + q) / 2).
+__host__ __device__ constexpr int oz_p(int ci) {
+  return ci == 0 ? 0 : ci == 1 ? 0 : ci == 2 ? 2 : ci == 3 ? 0 : ci == 4 ? 2 : ci == 5 ? 4
+       : ci == 6 ? 0 : ci == 7 ? 2 : ci == 8 ? 4 : 6;
+}
+__host__ __device__ constexpr int oz_q(int ci) {
+  return ci == 0 ? 0 : ci == 1 ? 2 : ci == 2 ? 0 : ci == 3 ? 4 : ci == 4 ? 2 : ci == 5 ? 0
+       : ci == 6 ? 6 : ci == 7 ? 4 : ci == 8 ? 2 : 0;
+}
+
+template <class Idx>
+__global__ void __launch_bounds__(OZ_THREADS, 1)
+    k_leaf_ozaki(int64_t n_seg, const int64_t* __restrict__ seg, const Idx* __restrict__ a_idx,
+                 const Idx* __restrict__ b_idx, const int32_t* __restrict__ b_tr,
+                 const int64_t* __restrict__ a_keys, const int64_t* __restrict__ b_keys, int64_t G,
+                 const int8_t* __restrict__ As, const int8_t* __restrict__ Bs,
+                 const int* __restrict__ ex_a, const int* __restrict__ ex_b,
+                 const int64_t* __restrict__ c_out, const int64_t* __restrict__ c_mirror,
+                 int accumulate, double* __restrict__ C, const int32_t* __restrict__ order,
+                 int* __restrict__ next_block) {
+  pdl_wait();
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = smem_u32(smem_raw);
+  const uint32_t base = (raw + 1023u) & ~1023u;
+  uint8_t* gbase = smem_raw + (base - raw);
+  int* xb = reinterpret_cast<int*>(gbase + OZ_STAGES * OZ_STAGE);
+  const uint32_t bars = base + OZ_STAGES * OZ_STAGE + OZ_XBUF;
+  auto full = [&](int s) { return bars + 8u * s; };
+  auto empty = [&](int s) { return bars + 8u * (OZ_STAGES + s); };
+  const uint32_t tfull = bars + 8u * (2 * OZ_STAGES), tempty = tfull + 8u;
+  int64_t* meta = reinterpret_cast<int64_t*>(gbase + OZ_STAGES * OZ_STAGE + OZ_XBUF +
+                                             8 * (2 * OZ_STAGES + 2));
+  int64_t* meta2 = meta + OZ_STAGES;  // (bi << 32) | bj of the chunk starting in this stage
+  int64_t* ring = meta2 + OZ_STAGES;  // the chunk in TMEM: meta, meta2
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ring + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < OZ_STAGES; ++s) {
+      mbar_init(full(s), 1);
+      mbar_init(empty(s), 1);
+    }
+    mbar_init(tfull, 2);   // MMA completion (commit) + the ring entry (MMA thread)
+    mbar_init(tempty, 4);  // one arrive per epilogue warp
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (warp == 5) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(
+                     smem_u32(tmem_slot))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+  }
+  tc_before();
+  __syncthreads();
+  tc_after();
+  const uint32_t tbase = *tmem_slot;
+
+  if (warp == 4) {
+    // ---------------- producer: two 32-KB bulk copies per task ----------------
+    int stage = 0;
+    uint32_t phase = 0;
+    auto claim = [&](int64_t& m, int64_t& t0, int64_t& t1) -> bool {
+      int64_t i = 0;
+      if (lane == 0) i = atomicAdd(next_block, 1);
+      i = __shfl_sync(0xffffffffu, i, 0);
+      if (i >= n_seg) return false;
+      m = order ? (int64_t)order[i] : i;
+      t0 = seg[m];
+      t1 = seg[m + 1];
+      return true;
+    };
+    int64_t m = 0, t0 = 0, t1 = 0;
+    bool have = claim(m, t0, t1);
+    while (have) {
+      int64_t mn = 0, t0n = 0, t1n = 0;
+      const bool next = claim(mn, t0n, t1n);
+      for (int64_t c0 = t0; c0 < t1; c0 += 32) {
+        const int64_t t = c0 + lane;
+        int64_t ra_l = 0, rb_l = 0;
+        if (t < t1) {
+          ra_l = (int64_t)a_idx[t];
+          rb_l = (int64_t)b_idx[t];
+          if (b_tr) rb_l = b_tr[rb_l];
+        }
+        const int cnt = t1 - c0 < 32 ? (int)(t1 - c0) : 32;
+        for (int q = 0; q < cnt; ++q) {
+          const int64_t ra = __shfl_sync(0xffffffffu, ra_l, q);
+          const int64_t rb = __shfl_sync(0xffffffffu, rb_l, q);
+          mbar_wait(empty(stage), phase ^ 1u);
+          if (lane == 0) {
+            const int64_t tq = c0 + q, r = tq - t0;
+            const bool first = r % OZ_CHUNK == 0;
+            const bool last = tq + 1 == t1 || (r + 1) % OZ_CHUNK == 0;
+            const bool cont = r >= OZ_CHUNK || accumulate;
+            meta[stage] = (m << 3) | (first ? 1 : 0) | (last ? 2 : 0) | (cont ? 4 : 0);
+            if (first)
+              meta2[stage] = ((a_keys[a_idx[tq]] / G) << 32) | (b_keys[b_idx[tq]] % G);
+            mbar_expect_tx(full(stage), OZ_STAGE);
+            const uint32_t sa = base + stage * OZ_STAGE;
+            bulk_g2s(sa, As + ra * OZ_BLOCK_BYTES, OZ_BLOCK_BYTES, full(stage));
+            bulk_g2s(sa + OZ_BLOCK_BYTES, Bs + rb * OZ_BLOCK_BYTES, OZ_BLOCK_BYTES, full(stage));
+          }
+          __syncwarp();
+          if (++stage == OZ_STAGES) {
+            stage = 0;
+            phase ^= 1u;
+          }
+        }
+      }
+      have = next;
+      m = mn;
+      t0 = t0n;
+      t1 = t1n;
+    }
+    mbar_wait(empty(stage), phase ^ 1u);
+    if (lane == 0) {
+      meta[stage] = -1;
+      mbar_arrive(full(stage));
+    }
+  } else if (warp == 5) {
+    // ---------------- MMA issuer: one thread ----------------
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0, tphase = 0;
+      int64_t cur2 = 0;
+      for (;;) {
+        mbar_wait(full(stage), phase);
+        tc_after();
+        const int64_t md = meta[stage];
+        if (md < 0) {
+          mbar_wait(tempty, tphase ^ 1u);  // the epilogue is done with the last chunk
+          ring[0] = -1;
+          mbar_arrive(tfull);
+          oz_commit(tfull);
+          break;
+        }
+        const bool first = md & 1;
+        if (first) {
+          cur2 = meta2[stage];
+          mbar_wait(tempty, tphase ^ 1u);  // TMEM drained by the epilogue
+          tphase ^= 1u;
+          tc_after();
+        }
+        const uint32_t sa = base + stage * OZ_STAGE, sb = sa + OZ_BLOCK_BYTES;
+#pragma unroll
+        for (int ci = 0; ci < 10; ++ci) {
+          const int p = oz_p(ci), q = oz_q(ci), t = (p + q) / 2;
+          const bool opens = ci == 0 || ci == 1 || ci == 3 || ci == 6;  // first pair of tile t
+#pragma unroll
+          for (int ks = 0; ks < 2; ++ks)
+            oz_mma(tbase + 128u * t, oz_desc(sa + p * OZ_SLICE_BYTES + ks * 256),
+                   oz_desc(sb + q * OZ_SLICE_BYTES + ks * 256),
+                   (first && opens && ks == 0) ? 0u : 1u);
+        }
+        oz_commit(empty(stage));  // stage free once these MMAs have read it
+        if (md & 2) {
+          ring[0] = md;
+          ring[1] = cur2;
+          mbar_arrive(tfull);
+          oz_commit(tfull);  // accumulators complete
+        }
+        if (++stage == OZ_STAGES) {
+          stage = 0;
+          phase ^= 1u;
+        }
+      }
+    }
+    __syncwarp();
+  } else {
+    // ---------------- epilogue: warps 0-3, thread e <-> TMEM lane e ----------------
+    const int e = threadIdx.x, r = e & 63, partner = e ^ 64;
+    const bool top = e < 64;
+    const int own0 = top ? 0 : 4;  // the 4 columns of each 8-column chunk this thread writes
+    const uint32_t lane_base = tbase + ((uint32_t)(warp * 32) << 16);
+    uint32_t ephase = 0;
+    for (;;) {
+      mbar_wait(tfull, ephase);
+      ephase ^= 1u;
+      tc_after();
+      const int64_t md = ring[0];
+      if (md < 0) break;
+      const int64_t bij = ring[1];
+      const int64_t m = md >> 3;
+      const bool cont = md & 4;
+      const int64_t bi = bij >> 32, bj = bij & 0xffffffffLL;
+      const int er = oz_exp(ex_a[bi * OZ_NB + r]);
+      double* Cb = C + (c_out ? c_out[m] : m) * (int64_t)(OZ_NB * OZ_NB);
+      const int64_t mi = c_mirror ? c_mirror[m] : -1;
+      double* Cm = mi >= 0 ? C + mi * (int64_t)(OZ_NB * OZ_NB) : nullptr;
+#pragma unroll 1
+      for (int cc = 0; cc < 8; ++cc) {
+        int L[4][8], R[4][8];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          tmem_ld8(lane_base + 128u * t + cc * 8, L[t]);
+          tmem_ld8(lane_base + 128u * t + 64 + cc * 8, R[t]);
+        }
+        tmem_wait8(L[0]);
+        tmem_keep8(R[0]);
+#pragma unroll
+        for (int t = 1; t < 4; ++t) {
+          tmem_keep8(L[t]);
+          tmem_keep8(R[t]);
+        }
+        if (cc == 7) {  // every TMEM read of this chunk is complete: hand TMEM back
+          tc_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(tempty);
+        }
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            xb[(t * 8 + c) * OZ_EPI + e] = top ? L[t][4 + c] : L[t][c];
+            xb[(t * 8 + 4 + c) * OZ_EPI + e] = top ? R[t][4 + c] : R[t][c];
+          }
+        asm volatile("bar.sync 1, 128;\n" ::: "memory");
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          int64_t tl[4], tr[4], bl[4], br[4];
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            const int ol = xb[(t * 8 + c) * OZ_EPI + partner];
+            const int orr = xb[(t * 8 + 4 + c) * OZ_EPI + partner];
+            const int ml = top ? L[t][c] : L[t][4 + c];  // static register indices
+            const int mr = top ? R[t][c] : R[t][4 + c];
+            tl[t] = top ? ml : ol;
+            tr[t] = top ? mr : orr;
+            bl[t] = top ? ol : ml;
+            br[t] = top ? orr : mr;
+          }
+          // S_d: the exact digit-sum-d part (quadrants of equal d added in int64)
+          const int64_t S[9] = {tl[0],         tr[0] + bl[0], tl[1] + br[0],
+                                tr[1] + bl[1], tl[2] + br[1], tr[2] + bl[2],
+                                tl[3] + br[2], tr[3] + bl[3], br[3]};
+          double v = (double)S[8];
+#pragma unroll
+          for (int d = 7; d >= 0; --d) v = __fma_rn(v, 0x1p-8, (double)S[d]);
+          const int col = cc * 8 + own0 + c;
+          const int ec = oz_exp(ex_b[bj * OZ_NB + col]);
+          double out = ldexp(v, er + ec - 14);
+          if (cont) out = __dadd_rn(Cb[r * OZ_NB + col], out);
+          Cb[r * OZ_NB + col] = out;
+          if (Cm) Cm[col * OZ_NB + r] = out;
+        }
+        asm volatile("bar.sync 1, 128;\n" ::: "memory");
+      }
+    }
+  }
+  tc_before();
+  __syncthreads();
+  tc_after();
+  if (warp == 5)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tbase)
+                 : "memory");
+}
+
+}  // namespace
+
+bool ozaki_supported(int nb) { return nb == OZ_NB; }
+
+template <class Idx>
+void leaf_products_ozaki(int64_t n_seg, const int64_t* seg, const Idx* a_idx, const Idx* b_idx,
+                         const int64_t* c_out, const int64_t* c_mirror, bool accumulate,
+                         const Mat& A, const Mat& B, bool sym_b, double* C, cudaStream_t s,
+                         LptSchedule lpt) {
+  if (n_seg <= 0) return;
+  if (A.nb != OZ_NB || B.nb != OZ_NB) throw CudaError("INT8-sliced leaf kernel needs block size 64");
+  const int64_t G = A.G;
+  int* ex_a = dmalloc<int>(G * OZ_NB, s);
+  int8_t* as = dmalloc<int8_t>((size_t)A.nblocks * OZ_BLOCK_BYTES, s);
+  SPAMM_CK(cudaMemsetAsync(ex_a, 0x80, G * OZ_NB * sizeof(int), s));
+  const int gx = grid_for(A.nblocks, 1, (int64_t)multiprocessors() * 8);
+  launch_pdl(k_oz_exponents, gx, 256, 0, s, A.data, A.keys, A.nblocks, G, 0, ex_a);
+  SPAMM_LAUNCH_CK();
+  launch_pdl(k_oz_split, gx, 256, 0, s, A.data, A.keys, A.nblocks, G, 0, (const int*)ex_a, as);
+  SPAMM_LAUNCH_CK();
+  int* ex_b = ex_a;
+  int8_t* bs = as;
+  int32_t* b_tr = nullptr;
+  if (sym_b) {
+    b_tr = dmalloc<int32_t>(A.nblocks > 0 ? A.nblocks : 1, s);
+    launch_pdl(k_oz_trslot, grid_for(A.nblocks, 256), 256, 0, s, (const int64_t*)A.keys,
+               A.nblocks, G, (const int32_t*)A.slot, b_tr);
+    SPAMM_LAUNCH_CK();
+  } else {
+    ex_b = dmalloc<int>(G * OZ_NB, s);
+    bs = dmalloc<int8_t>((size_t)B.nblocks * OZ_BLOCK_BYTES, s);
+    SPAMM_CK(cudaMemsetAsync(ex_b, 0x80, G * OZ_NB * sizeof(int), s));
+    const int gy = grid_for(B.nblocks, 1, (int64_t)multiprocessors() * 8);
+    launch_pdl(k_oz_exponents, gy, 256, 0, s, B.data, B.keys, B.nblocks, G, 1, ex_b);
+    SPAMM_LAUNCH_CK();
+    launch_pdl(k_oz_split, gy, 256, 0, s, B.data, B.keys, B.nblocks, G, 1, (const int*)ex_b, bs);
+    SPAMM_LAUNCH_CK();
+  }
+  const int32_t* order = lpt.order;
+  int* counter = lpt.counter;
+  int* scratch = nullptr;
+  if (!order || !counter) scratch = lpt_schedule(n_seg, seg, &order, &counter, s);
+  auto kern = k_leaf_ozaki<Idx>;
+  static std::once_flag once;
+  std::call_once(once, [&] {
+    SPAMM_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)OZ_SMEM));
+  });
+  int64_t grid = multiprocessors();
+  if (grid > n_seg) grid = n_seg;
+  launch_pdl(kern, (unsigned)grid, OZ_THREADS, OZ_SMEM, s, n_seg, seg, a_idx, b_idx,
+             (const int32_t*)b_tr, (const int64_t*)A.keys, (const int64_t*)B.keys, G,
+             (const int8_t*)as, (const int8_t*)bs, (const int*)ex_a, (const int*)ex_b, c_out,
+             c_mirror, accumulate ? 1 : 0, C, order, counter);
+  SPAMM_LAUNCH_CK();
+  dfree(scratch, s);
+  dfree(b_tr, s);
+  if (!sym_b) {
+    dfree(ex_b, s);
+    dfree(bs, s);
+  }
+  dfree(ex_a, s);
+  dfree(as, s);
+}
+
+template void leaf_products_ozaki<int32_t>(int64_t, const int64_t*, const int32_t*,
+                                           const int32_t*, const int64_t*, const int64_t*, bool,
+                                           const Mat&, const Mat&, bool, double*, cudaStream_t,
+                                           LptSchedule);
+template void leaf_products_ozaki<int64_t>(int64_t, const int64_t*, const int64_t*,
+                                           const int64_t*, const int64_t*, const int64_t*, bool,
+                                           const Mat&, const Mat&, bool, double*, cudaStream_t,
+                                           LptSchedule);
+
+}  // namespace spamm

@@ -584,20 +584,7 @@ void launch_tma(int64_t n_seg, const int64_t* seg, const Idx* a_idx, const Idx* 
     counter = scratch;
     order = nullptr;
   } else if (!order) {
-    // scratch: [next-block counter | length histogram (maxlen + 1 bins) | LPT order]
-    const int maxlen = 4096;
-    scratch = dmalloc<int>(1 + (maxlen + 1) + n_seg, s);
-    counter = scratch;
-    int* hist = scratch + 1;
-    int32_t* ord = scratch + 2 + maxlen;
-    SPAMM_CK(cudaMemsetAsync(scratch, 0, (2 + maxlen) * sizeof(int), s));
-    k_len_hist<<<grid_for(n_seg, 256), 256, 0, s>>>(seg, n_seg, maxlen, hist);
-    SPAMM_LAUNCH_CK();
-    launch_pdl(k_hist_scan, 1, 1024, 0, s, hist, maxlen + 1);
-    SPAMM_LAUNCH_CK();
-    k_len_scatter<<<grid_for(n_seg, 256), 256, 0, s>>>(seg, n_seg, maxlen, hist, ord);
-    SPAMM_LAUNCH_CK();
-    order = ord;
+    scratch = lpt_schedule(n_seg, seg, &order, &counter, s);
   }
   static const int hint = [] {  // L2 policy bits (see tma_load_2d_pol)
     const char* v = getenv("SPAMM_K4_HINT");
@@ -624,6 +611,27 @@ void launch_tma(int64_t n_seg, const int64_t* seg, const Idx* a_idx, const Idx* 
 }  // namespace
 
 bool tma_leaf_supported(int nb) { return nb == 32 || nb == 64; }
+
+int multiprocessors() { return sm_count(); }
+
+int* lpt_schedule(int64_t n_seg, const int64_t* seg, const int32_t** order, int** counter,
+                  cudaStream_t s) {
+  // scratch: [next-block counter | length histogram (maxlen + 1 bins) | LPT order]
+  const int maxlen = 4096;
+  int* scratch = dmalloc<int>(1 + (maxlen + 1) + n_seg, s);
+  int* hist = scratch + 1;
+  int32_t* ord = scratch + 2 + maxlen;
+  SPAMM_CK(cudaMemsetAsync(scratch, 0, (2 + maxlen) * sizeof(int), s));
+  k_len_hist<<<grid_for(n_seg, 256), 256, 0, s>>>(seg, n_seg, maxlen, hist);
+  SPAMM_LAUNCH_CK();
+  launch_pdl(k_hist_scan, 1, 1024, 0, s, hist, maxlen + 1);
+  SPAMM_LAUNCH_CK();
+  k_len_scatter<<<grid_for(n_seg, 256), 256, 0, s>>>(seg, n_seg, maxlen, hist, ord);
+  SPAMM_LAUNCH_CK();
+  *order = ord;
+  *counter = scratch;
+  return scratch;
+}
 
 template <class Idx>
 void leaf_products_tma(int64_t n_seg, const int64_t* seg, const Idx* a_idx, const Idx* b_idx,
