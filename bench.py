@@ -53,9 +53,36 @@ def fp64_peak():
         return 37.2, "nominal 148 SM x 128 flop/clk x 1.965 GHz (fallback)"
 
 
-def ncu_traffic():
-    """dram bytes per K4 launch from the committed ncu --set full summary, if any."""
-    path = os.path.join(ROOT, "profiles", "ncu_leaf_r01.json")
+def i8_peak():
+    """Measured INT8 tcgen05 peak at K4z's MMA shape (tools/i8_peak.cu ->
+    profiles/i8_peak_r01.json, M = N = 128, K = 32); MEASURED_PEAKS.json has no
+    INT8 entry."""
+    path = os.path.join(ROOT, "profiles", "i8_peak_r01.json")
+    try:
+        with open(path) as f:
+            res = json.load(f)["results"]
+        best = max(r["tops"] for r in res if r.get("op") == "tcgen05_i8_m128n128k32")
+        return best, "measured tcgen05 kind::i8 M128 N128 peak, tools/i8_peak.cu (profiles/i8_peak_r01.json)"
+    except (OSError, KeyError, ValueError):
+        return 4500.0, "nominal B200 dense INT8 (fallback)"
+
+
+# K4z executes 20 tcgen05 MMAs of 128x128x32 int8 per leaf product (10 digit
+# pairs x 2 k-steps, leaf_ozaki.cu): int8 ops per executed leaf product.
+K4Z_OPS_PER_PRODUCT = 20 * 2 * 128 * 128 * 32
+
+
+def leaf_kernel_in_use(block_size: int) -> str:
+    """What kernel="auto" resolves to (api.cu leaf_dispatch)."""
+    if block_size == 64 and os.environ.get("SPAMM_AUTO_LEAF") != "dmma":
+        return "ozaki"
+    return "dmma"
+
+
+def ncu_traffic(kernel: str = "dmma"):
+    """dram bytes per K4 launch from the committed ncu summary, if any."""
+    path = os.path.join(ROOT, "profiles",
+                        "ncu_leaf_ozaki_r01.json" if kernel == "ozaki" else "ncu_leaf_r01.json")
     try:
         with open(path) as f:
             return json.load(f).get("dram_bytes_per_launch")
@@ -270,6 +297,38 @@ def run_ours(args):
         else:  # sharded runs are not K4-timed: whole-step lower bound, all ranks
             achieved = exec_all / (tmax * 1e-3) / 1e12 / ws
             roof_note = "per-GPU executed leaf flops / whole step time (lower bound)"
+        k4 = leaf_kernel_in_use(cfg.block_size)
+        if k4 == "ozaki":
+            tasks = exec_flops / (2 * cfg.block_size ** 3)
+            ipeak, ipeak_src = i8_peak()
+            if leaf_ms > 0:
+                iach = tasks * K4Z_OPS_PER_PRODUCT / (leaf_ms * 1e-3) / 1e12
+                inote = ("executed leaf products x 20 int8 MMAs of 128x128x32 per launch "
+                         "/ K4z event time")
+            else:
+                iach = tasks * K4Z_OPS_PER_PRODUCT / (tmax * 1e-3) / 1e12
+                inote = "int8 MMA ops of this rank / whole step time (lower bound)"
+            roofline = {"bound": "tensor", "achieved": iach, "peak": ipeak, "unit": "TOPS",
+                        "frac": iach / ipeak,
+                        "traffic": ncu_traffic("ozaki") if args.config == 4 else None,
+                        "kernel": "k_leaf_ozaki<int> (K4z: FP64 leaf products as exact "
+                                  "signed-8-bit digit products on the INT8 tensor cores)",
+                        "peak_source": ipeak_src, "algorithmic": inote,
+                        "fp64_equivalent": {
+                            "achieved": achieved, "unit": "TFLOP/s", "dmma_peak": peak,
+                            "frac_of_dmma_peak": achieved / peak, "dmma_peak_source": peak_src,
+                            "note": "executed leaf products x 2 Nb^3 / K4z time: the FP64 "
+                                    "rate the INT8 path delivers, against the FP64 "
+                                    "tensor-core roofline it replaces"}}
+        else:
+            roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                        "frac": achieved / peak,
+                        "traffic": ncu_traffic() if args.config == 4 else None,
+                        "kernel": ("k_leaf_dmma_tma<64,2,4,3,KS=1,PAIRK> (K4 leaf products)"
+                                   if cfg.block_size == 64 else
+                                   "k_leaf_dmma_tma<32,2,2,3,KS=4,PAIRK+PAIRN> (K4 leaf products)"),
+                        "peak_source": peak_src,
+                        "algorithmic": roof_note}
         out = {
             "metric": METRIC, "value": flops_all / (tmax * 1e-3) / 1e9, "unit": UNIT,
             "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
@@ -286,14 +345,8 @@ def run_ours(args):
                            "(ProductStats.flop_estimate); symmetric X*X executes "
                            "leaf_flops_executed_per_step of them and mirrors the rest "
                            "(bitwise identical C)"),
-            "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                         "frac": achieved / peak,
-                         "traffic": ncu_traffic() if args.config == 4 else None,
-                         "kernel": ("k_leaf_dmma_tma<64,2,4,3,KS=1,PAIRK> (K4 leaf products)"
-                                    if cfg.block_size == 64 else
-                                    "k_leaf_dmma_tma<32,2,2,3,KS=4,PAIRK+PAIRN> (K4 leaf products)"),
-                         "peak_source": peak_src,
-                         "algorithmic": roof_note},
+            "leaf_kernel": k4,
+            "roofline": roofline,
             "e2e": {"value": e2e_flops_all / (e2e_max * 1e-3) / 1e9, "unit": UNIT,
                     "h2d_bytes_per_step": int(h.nbytes), "d2h_bytes_per_step": int(h.nbytes),
                     "api": "pipeline.sp2_solve_many over the steps' pinned host H (H2D, "

@@ -33,7 +33,7 @@ extern "C" {
 #define SPAMM_MAX_TIERS 64
 
 /* Leaf-product kernels (spamm_multiply / spamm_gemm_batch `kernel`). */
-#define SPAMM_LEAF_AUTO 0  /* DMMA for Nb in {8,16,32,64}, else exact        */
+#define SPAMM_LEAF_AUTO 0  /* INT8-sliced for Nb = 64 (matrix entry points), DMMA for Nb in {8,16,32}, else exact; SPAMM_AUTO_LEAF=dmma keeps DMMA at 64 */
 #define SPAMM_LEAF_DMMA 1  /* FP64 tensor cores (mma.sync f64 -> DMMA)       */
 #define SPAMM_LEAF_EXACT 2 /* CUDA-core, reference order: bitwise identical  */
 #define SPAMM_LEAF_DMMA_CPASYNC 3 /* first-generation DMMA kernel (A/B tests)  */

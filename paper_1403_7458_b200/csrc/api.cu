@@ -3,6 +3,7 @@
 #include <algorithm>
 #include <climits>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -450,16 +451,29 @@ int spamm_multiply(const spamm_mat* a, const spamm_mat* b, double tau, int32_t k
 namespace {
 
 // K4 dispatch: the INT8-sliced kernel takes the operand matrices (row / column
-// exponents from their keys), the others the block arrays.
+// exponents from their keys), the others the block arrays.  AUTO picks it for
+// Nb = 64 (faster than DMMA and closer to the exact product), DMMA otherwise.
 void leaf_dispatch(int64_t n, const int64_t* seg, const int32_t* ai, const int32_t* bi,
                    const int64_t* c_out, const int64_t* c_mirror, const spamm_mat* a,
                    const spamm_mat* b, double* C, int32_t kernel, cudaStream_t s,
                    spamm::LptSchedule lpt) {
-  if (kernel == spamm::LEAF_OZAKI)
+  static const bool auto_ozaki = [] {  // SPAMM_AUTO_LEAF=dmma: AUTO keeps the DMMA kernel
+    const char* v = getenv("SPAMM_AUTO_LEAF");
+    return !(v && strcmp(v, "dmma") == 0);
+  }();
+  const bool sym_b = a == b && a->m.sym;
+  if (kernel == spamm::LEAF_OZAKI) {
     spamm::leaf_products_ozaki<int32_t>(n, seg, ai, bi, c_out, c_mirror, false, a->m, b->m,
-                                        a == b && a->m.sym, C, s, lpt);
-  else
-    spamm::leaf_products<int32_t>(n, seg, ai, bi, c_out, c_mirror, false, a->m.data, a->m.nblocks,
+                                        sym_b, C, s, lpt);
+    return;
+  }
+  // AUTO also needs room for the digit slices (the operands' size again): a
+  // matrix that nearly fills HBM (config 5 on one GPU) stays on DMMA.
+  if (kernel == spamm::LEAF_AUTO && auto_ozaki && spamm::ozaki_supported(a->m.nb) &&
+      spamm::leaf_products_ozaki<int32_t>(n, seg, ai, bi, c_out, c_mirror, false, a->m, b->m,
+                                          sym_b, C, s, lpt, /*try_only=*/true))
+    return;
+  spamm::leaf_products<int32_t>(n, seg, ai, bi, c_out, c_mirror, false, a->m.data, a->m.nblocks,
                                   b->m.data, b->m.nblocks, C, a->m.nb, kernel, s, lpt);
 }
 

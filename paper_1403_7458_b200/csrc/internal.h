@@ -203,11 +203,13 @@ int* lpt_schedule(int64_t n_seg, const int64_t* seg, const int32_t** order, int*
 // keys give the global row / column exponents); sym_b: B is A and A == A^T,
 // so B's transposed slices are A's slices of the mirror block.
 bool ozaki_supported(int nb);
+// try_only: return false (nothing launched, nothing left allocated) when the
+// digit-slice scratch (the operands' size again) cannot be allocated.
 template <class Idx>
-void leaf_products_ozaki(int64_t n_seg, const int64_t* seg, const Idx* a_idx, const Idx* b_idx,
+bool leaf_products_ozaki(int64_t n_seg, const int64_t* seg, const Idx* a_idx, const Idx* b_idx,
                          const int64_t* c_out, const int64_t* c_mirror, bool accumulate,
                          const Mat& A, const Mat& B, bool sym_b, double* C, cudaStream_t s,
-                         LptSchedule lpt = {});
+                         LptSchedule lpt = {}, bool try_only = false);
 template <class Idx>
 void leaf_products_tma(int64_t n_seg, const int64_t* seg, const Idx* a_idx, const Idx* b_idx,
                        const int64_t* c_out, const int64_t* c_mirror, bool accumulate,

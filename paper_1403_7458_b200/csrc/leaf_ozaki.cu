@@ -9,8 +9,9 @@
 //    (E: frexp exponent of the largest |x| in that global row / column over
 //    all stored blocks, k_oz_exponents), and x 2^-E is written with 8 signed
 //    int8 digits x = 2^E (s_0 2^-7 + sum_{p=1..7} s_p 2^-(7+8p)), s_p in
-//    [-128, 127] (k_oz_split: floor digits, then a carry pass from the bottom
-//    -- every step exact; 63 bits, the remainder is < 2^(E-63));
+//    [-128, 127] (k_oz_split: floor digits of |x|, a carry pass from the
+//    bottom, the sign applied last -- every step exact; 63 bits, the remainder
+//    is < 2^(E-63));
 //  * a digit product sum_k dA_p[r][k] dB_q[k][c] is computed EXACTLY in int32
 //    on the tensor cores and summed exactly over the tasks of the C block
 //    (|.| <= 4 x 64 x 2^14 = 2^22 per task and quadrant, so chunks of
@@ -36,7 +37,11 @@
 // block), compute per task is 20 tcgen05 MMAs of 128x128x32 = 1,280 tensor
 // cycles versus ~4,100 cycles of DMMA at 64x64x64.
 #include <climits>
+#include <cstdlib>
+#include <cstring>
 #include <mutex>
+#include <vector>
+#include <cstdio>
 
 #include "internal.h"
 
@@ -50,10 +55,14 @@ constexpr int OZ_SLICE_BYTES = OZ_NB * OZ_NB;                  // 4 KB (int8)
 constexpr int OZ_BLOCK_BYTES = OZ_SLICES * OZ_SLICE_BYTES;     // 32 KB
 constexpr int OZ_STAGES = 3;
 constexpr int OZ_STAGE = 2 * OZ_BLOCK_BYTES;                   // A + B slices of one task
-constexpr int OZ_CHUNK = 256;       // tasks per TMEM accumulation (int32 headroom: 512)
-constexpr int OZ_EPI = 128;         // epilogue threads (warps 0-3 <-> TMEM lane quarters)
-constexpr int OZ_THREADS = OZ_EPI + 64;  // + producer warp (4) + MMA warp (5)
-constexpr int OZ_XBUF = 32 * OZ_EPI * 4;  // epilogue exchange: 32 ints per thread
+constexpr int OZ_CHUNK = 128;       // tasks per TMEM accumulation (quadrant sums stay < 2^30)
+// Epilogue: 8 warps in two groups of 4 (warp w reads TMEM lane quarter w % 4);
+// group g converts the columns 32g..32g+31 of the C block.
+constexpr int OZ_EPI = 256;
+constexpr int OZ_GROUP = 128;
+constexpr int OZ_PRODUCER = OZ_EPI / 32, OZ_MMA = OZ_PRODUCER + 1;  // warps 8, 9
+constexpr int OZ_THREADS = OZ_EPI + 64;
+constexpr int OZ_XBUF = 32 * OZ_EPI * 4;  // epilogue exchange: 32 ints per thread (32 KB)
 constexpr size_t OZ_SMEM = 1024 + (size_t)OZ_STAGES * OZ_STAGE + OZ_XBUF + 256;
 constexpr int OZ_EXP_NONE = (int)0x80808080;  // memset pattern: "no nonzero seen"
 
@@ -137,11 +146,14 @@ __global__ void __launch_bounds__(256) k_oz_split(const double* __restrict__ dat
     for (int i = 0; i < 16; ++i) {
       const int k = kc * 16 + i;
       double y = trans ? tile[k * (OZ_NB + 1) + n] : tile[n * (OZ_NB + 1) + k];
-      // x 2^-E = s_0 2^-7 + sum_{p>=1} s_p 2^-(7+8p): floor digits (unsigned
-      // 8-bit tail), then signed with carries from the bottom -- every step exact.
-      double t = ldexp(y, 7 - e);  // |t| <= 127.25 (exponent bump in k_oz_exponents)
+      // x 2^-E = s_0 2^-7 + sum_{p>=1} s_p 2^-(7+8p): floor digits of |x|
+      // (unsigned 8-bit tail), signed with carries from the bottom, negated for
+      // x < 0 (carry at > 128 there, so the negated digits stay in [-128, 127])
+      // -- every step exact.
+      const bool neg = y < 0.0;
+      double t = ldexp(fabs(y), 7 - e);  // <= 127.25 (exponent bump in k_oz_exponents)
       const double d0 = floor(t);
-      double r = __dsub_rn(t, d0);  // [0, 1)
+      double r = __dsub_rn(t, d0);  // [0, 1), exact
       int u[OZ_SLICES];
 #pragma unroll
       for (int p = 1; p < OZ_SLICES; ++p) {
@@ -150,14 +162,18 @@ __global__ void __launch_bounds__(256) k_oz_split(const double* __restrict__ dat
         r = __dsub_rn(t, f);
         u[p] = (int)f;  // [0, 255]
       }
+      const int thr = neg ? 129 : 128;
       int c = 0;
 #pragma unroll
       for (int p = OZ_SLICES - 1; p >= 1; --p) {
         const int v = u[p] + c;
-        c = v >= 128 ? 1 : 0;
-        u[p] = v - 256 * c;  // [-128, 127]
+        c = v >= thr ? 1 : 0;
+        u[p] = v - 256 * c;
       }
-      u[0] = (int)d0 + c;  // [-128, 127]
+      u[0] = (int)d0 + c;  // <= 127: d0 = 127 leaves r < 1/4, no carry
+      if (neg)
+#pragma unroll
+        for (int p = 0; p < OZ_SLICES; ++p) u[p] = -u[p];
 #pragma unroll
       for (int p = 0; p < OZ_SLICES; ++p)
         dig[p][i >> 2] |= ((uint32_t)u[p] & 0xffu) << (8 * (i & 3));
@@ -213,6 +229,19 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
           "r"(dst),
       "l"(src), "r"(bytes), "r"(bar)
       : "memory");
+}
+__device__ __forceinline__ void bulk_g2s_pol(uint32_t dst, const void* src, uint32_t bytes,
+                                             uint32_t bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1], %2, [%3], %4;\n" ::"r"(dst),
+      "l"(src), "r"(bytes), "r"(bar), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t pol_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(p));
+  return p;
 }
 __device__ __forceinline__ void tc_before() {
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
@@ -282,7 +311,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
                  const int* __restrict__ ex_a, const int* __restrict__ ex_b,
                  const int64_t* __restrict__ c_out, const int64_t* __restrict__ c_mirror,
                  int accumulate, double* __restrict__ C, const int32_t* __restrict__ order,
-                 int* __restrict__ next_block) {
+                 int* __restrict__ next_block, int hint, long long* __restrict__ prof) {
   pdl_wait();
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
@@ -306,10 +335,10 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
       mbar_init(empty(s), 1);
     }
     mbar_init(tfull, 2);   // MMA completion (commit) + the ring entry (MMA thread)
-    mbar_init(tempty, 4);  // one arrive per epilogue warp
+    mbar_init(tempty, OZ_EPI / 32);  // one arrive per epilogue warp
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
-  if (warp == 5) {
+  if (warp == OZ_MMA) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(
                      smem_u32(tmem_slot))
                  : "memory");
@@ -320,7 +349,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
   tc_after();
   const uint32_t tbase = *tmem_slot;
 
-  if (warp == 4) {
+  if (warp == OZ_PRODUCER) {
     // ---------------- producer: two 32-KB bulk copies per task ----------------
     int stage = 0;
     uint32_t phase = 0;
@@ -362,8 +391,16 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
               meta2[stage] = ((a_keys[a_idx[tq]] / G) << 32) | (b_keys[b_idx[tq]] % G);
             mbar_expect_tx(full(stage), OZ_STAGE);
             const uint32_t sa = base + stage * OZ_STAGE;
-            bulk_g2s(sa, As + ra * OZ_BLOCK_BYTES, OZ_BLOCK_BYTES, full(stage));
-            bulk_g2s(sa + OZ_BLOCK_BYTES, Bs + rb * OZ_BLOCK_BYTES, OZ_BLOCK_BYTES, full(stage));
+            if (hint & 1) {  // operand slices evict_last (re-read by many C blocks)
+              const uint64_t pol = pol_evict_last();
+              bulk_g2s_pol(sa, As + ra * OZ_BLOCK_BYTES, OZ_BLOCK_BYTES, full(stage), pol);
+              bulk_g2s_pol(sa + OZ_BLOCK_BYTES, Bs + rb * OZ_BLOCK_BYTES, OZ_BLOCK_BYTES,
+                           full(stage), pol);
+            } else {
+              bulk_g2s(sa, As + ra * OZ_BLOCK_BYTES, OZ_BLOCK_BYTES, full(stage));
+              bulk_g2s(sa + OZ_BLOCK_BYTES, Bs + rb * OZ_BLOCK_BYTES, OZ_BLOCK_BYTES,
+                       full(stage));
+            }
           }
           __syncwarp();
           if (++stage == OZ_STAGES) {
@@ -382,14 +419,18 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
       meta[stage] = -1;
       mbar_arrive(full(stage));
     }
-  } else if (warp == 5) {
+  } else if (warp == OZ_MMA) {
     // ---------------- MMA issuer: one thread ----------------
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0, tphase = 0;
       int64_t cur2 = 0;
+      long long w_full = 0, w_tempty = 0, n_tasks = 0;
+      const long long t_start = prof ? clock64() : 0;
       for (;;) {
+        long long t0 = prof ? clock64() : 0;
         mbar_wait(full(stage), phase);
+        if (prof) w_full += clock64() - t0;
         tc_after();
         const int64_t md = meta[stage];
         if (md < 0) {
@@ -397,12 +438,21 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
           ring[0] = -1;
           mbar_arrive(tfull);
           oz_commit(tfull);
+          if (prof) {
+            long long* o = prof + blockIdx.x * 8;
+            o[0] = clock64() - t_start;
+            o[1] = w_full;
+            o[2] = w_tempty;
+            o[3] = n_tasks;
+          }
           break;
         }
         const bool first = md & 1;
         if (first) {
           cur2 = meta2[stage];
+          t0 = prof ? clock64() : 0;
           mbar_wait(tempty, tphase ^ 1u);  // TMEM drained by the epilogue
+          if (prof) w_tempty += clock64() - t0;
           tphase ^= 1u;
           tc_after();
         }
@@ -418,6 +468,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
                    (first && opens && ks == 0) ? 0u : 1u);
         }
         oz_commit(empty(stage));  // stage free once these MMAs have read it
+        ++n_tasks;
         if (md & 2) {
           ring[0] = md;
           ring[1] = cur2;
@@ -432,28 +483,43 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
     }
     __syncwarp();
   } else {
-    // ---------------- epilogue: warps 0-3, thread e <-> TMEM lane e ----------------
-    const int e = threadIdx.x, r = e & 63, partner = e ^ 64;
+    // ---------------- epilogue: warps 0-7, TMEM lane (warp % 4) * 32 + lane ----------------
+    const int grp = warp >> 2;
+    const int e = (warp & 3) * 32 + lane, r = e & 63, partner = e ^ 64;
     const bool top = e < 64;
     const int own0 = top ? 0 : 4;  // the 4 columns of each 8-column chunk this thread writes
-    const uint32_t lane_base = tbase + ((uint32_t)(warp * 32) << 16);
+    int* xg = xb + grp * (32 * OZ_GROUP);
+    const uint32_t lane_base = tbase + ((uint32_t)((warp & 3) * 32) << 16);
     uint32_t ephase = 0;
+    long long e_wait = 0, e_hold = 0, e_all = 0, n_blk = 0;
     for (;;) {
+      long long te0 = prof ? clock64() : 0;
       mbar_wait(tfull, ephase);
+      if (prof && threadIdx.x == 0) e_wait += clock64() - te0;
+      te0 = prof ? clock64() : 0;
       ephase ^= 1u;
       tc_after();
       const int64_t md = ring[0];
-      if (md < 0) break;
+      if (md < 0) {
+        if (prof && threadIdx.x == 0) {
+          prof[blockIdx.x * 8 + 4] = e_wait;
+          prof[blockIdx.x * 8 + 5] = e_hold;
+          prof[blockIdx.x * 8 + 6] = e_all;
+          prof[blockIdx.x * 8 + 7] = n_blk;
+        }
+        break;
+      }
       const int64_t bij = ring[1];
       const int64_t m = md >> 3;
       const bool cont = md & 4;
       const int64_t bi = bij >> 32, bj = bij & 0xffffffffLL;
-      const int er = oz_exp(ex_a[bi * OZ_NB + r]);
+      const int er = oz_exp(ex_a[bi * OZ_NB + r]) - 14;
       double* Cb = C + (c_out ? c_out[m] : m) * (int64_t)(OZ_NB * OZ_NB);
       const int64_t mi = c_mirror ? c_mirror[m] : -1;
       double* Cm = mi >= 0 ? C + mi * (int64_t)(OZ_NB * OZ_NB) : nullptr;
 #pragma unroll 1
-      for (int cc = 0; cc < 8; ++cc) {
+      for (int cl = 0; cl < 4; ++cl) {
+        const int cc = grp * 4 + cl;
         int L[4][8], R[4][8];
 #pragma unroll
         for (int t = 0; t < 4; ++t) {
@@ -467,55 +533,91 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
           tmem_keep8(L[t]);
           tmem_keep8(R[t]);
         }
-        if (cc == 7) {  // every TMEM read of this chunk is complete: hand TMEM back
+        if (cl == 3) {  // this warp's TMEM reads are complete: hand TMEM back
           tc_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(tempty);
+          if (prof && threadIdx.x == 0) e_hold += clock64() - te0;
         }
+        // hand the partner the 4 columns it owns: one 16-byte store per (tile, half)
+        int4* xg4 = reinterpret_cast<int4*>(xg);
 #pragma unroll
-        for (int t = 0; t < 4; ++t)
+        for (int t = 0; t < 4; ++t) {
+          xg4[(t * 2) * OZ_GROUP + e] = top ? make_int4(L[t][4], L[t][5], L[t][6], L[t][7])
+                                            : make_int4(L[t][0], L[t][1], L[t][2], L[t][3]);
+          xg4[(t * 2 + 1) * OZ_GROUP + e] = top ? make_int4(R[t][4], R[t][5], R[t][6], R[t][7])
+                                                : make_int4(R[t][0], R[t][1], R[t][2], R[t][3]);
+        }
+        const int col0 = cc * 8 + own0;
+        const int4 ec4 = *reinterpret_cast<const int4*>(ex_b + bj * OZ_NB + col0);
+        asm volatile("bar.sync %0, 128;\n" ::"r"(1 + grp) : "memory");
+        int oL[4][4], oR[4][4];
 #pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            xb[(t * 8 + c) * OZ_EPI + e] = top ? L[t][4 + c] : L[t][c];
-            xb[(t * 8 + 4 + c) * OZ_EPI + e] = top ? R[t][4 + c] : R[t][c];
-          }
-        asm volatile("bar.sync 1, 128;\n" ::: "memory");
+        for (int t = 0; t < 4; ++t) {
+          const int4 a = xg4[(t * 2) * OZ_GROUP + partner];
+          const int4 b = xg4[(t * 2 + 1) * OZ_GROUP + partner];
+          oL[t][0] = a.x; oL[t][1] = a.y; oL[t][2] = a.z; oL[t][3] = a.w;
+          oR[t][0] = b.x; oR[t][1] = b.y; oR[t][2] = b.z; oR[t][3] = b.w;
+        }
+        const int ecs[4] = {ec4.x, ec4.y, ec4.z, ec4.w};
+        double res[4];
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
-          int64_t tl[4], tr[4], bl[4], br[4];
+          int tl[4], tr[4], bl[4], br[4];
 #pragma unroll
           for (int t = 0; t < 4; ++t) {
-            const int ol = xb[(t * 8 + c) * OZ_EPI + partner];
-            const int orr = xb[(t * 8 + 4 + c) * OZ_EPI + partner];
             const int ml = top ? L[t][c] : L[t][4 + c];  // static register indices
             const int mr = top ? R[t][c] : R[t][4 + c];
-            tl[t] = top ? ml : ol;
-            tr[t] = top ? mr : orr;
-            bl[t] = top ? ol : ml;
-            br[t] = top ? orr : mr;
+            tl[t] = top ? ml : oL[t][c];
+            tr[t] = top ? mr : oR[t][c];
+            bl[t] = top ? oL[t][c] : ml;
+            br[t] = top ? oR[t][c] : mr;
           }
-          // S_d: the exact digit-sum-d part (quadrants of equal d added in int64)
-          const int64_t S[9] = {tl[0],         tr[0] + bl[0], tl[1] + br[0],
-                                tr[1] + bl[1], tl[2] + br[1], tr[2] + bl[2],
-                                tl[3] + br[2], tr[3] + bl[3], br[3]};
+          // S_d: the exact digit-sum-d part (|quadrant| < 2^30: int32 sums exact)
+          const int S[9] = {tl[0],         tr[0] + bl[0], tl[1] + br[0],
+                            tr[1] + bl[1], tl[2] + br[1], tr[2] + bl[2],
+                            tl[3] + br[2], tr[3] + bl[3], br[3]};
           double v = (double)S[8];
 #pragma unroll
           for (int d = 7; d >= 0; --d) v = __fma_rn(v, 0x1p-8, (double)S[d]);
-          const int col = cc * 8 + own0 + c;
-          const int ec = oz_exp(ex_b[bj * OZ_NB + col]);
-          double out = ldexp(v, er + ec - 14);
-          if (cont) out = __dadd_rn(Cb[r * OZ_NB + col], out);
-          Cb[r * OZ_NB + col] = out;
-          if (Cm) Cm[col * OZ_NB + r] = out;
+          const int k = er + oz_exp(ecs[c]);  // C = v 2^k
+          res[c] = (k >= -1022 && k <= 1023)
+                       ? __dmul_rn(v, __longlong_as_double((long long)(k + 1023) << 52))
+                       : ldexp(v, k);
         }
-        asm volatile("bar.sync 1, 128;\n" ::: "memory");
+        double2* row = reinterpret_cast<double2*>(Cb + r * OZ_NB + col0);
+        if (cont) {
+          const double2 p0 = row[0], p1 = row[1];
+          res[0] = __dadd_rn(p0.x, res[0]);
+          res[1] = __dadd_rn(p0.y, res[1]);
+          res[2] = __dadd_rn(p1.x, res[2]);
+          res[3] = __dadd_rn(p1.y, res[3]);
+        }
+        if (hint & 2) {  // products streamed past L2 (evict_first)
+          __stcs(row, make_double2(res[0], res[1]));
+          __stcs(row + 1, make_double2(res[2], res[3]));
+          if (Cm)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) __stcs(Cm + (col0 + c) * OZ_NB + r, res[c]);
+        } else {
+          row[0] = make_double2(res[0], res[1]);
+          row[1] = make_double2(res[2], res[3]);
+          if (Cm)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) Cm[(col0 + c) * OZ_NB + r] = res[c];
+        }
+        asm volatile("bar.sync %0, 128;\n" ::"r"(1 + grp) : "memory");
+      }
+      if (prof && threadIdx.x == 0) {
+        e_all += clock64() - te0;
+        ++n_blk;
       }
     }
   }
   tc_before();
   __syncthreads();
   tc_after();
-  if (warp == 5)
+  if (warp == OZ_MMA)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tbase)
                  : "memory");
 }
@@ -525,15 +627,36 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
 bool ozaki_supported(int nb) { return nb == OZ_NB; }
 
 template <class Idx>
-void leaf_products_ozaki(int64_t n_seg, const int64_t* seg, const Idx* a_idx, const Idx* b_idx,
+bool leaf_products_ozaki(int64_t n_seg, const int64_t* seg, const Idx* a_idx, const Idx* b_idx,
                          const int64_t* c_out, const int64_t* c_mirror, bool accumulate,
                          const Mat& A, const Mat& B, bool sym_b, double* C, cudaStream_t s,
-                         LptSchedule lpt) {
-  if (n_seg <= 0) return;
+                         LptSchedule lpt, bool try_only) {
+  if (n_seg <= 0) return true;
   if (A.nb != OZ_NB || B.nb != OZ_NB) throw CudaError("INT8-sliced leaf kernel needs block size 64");
   const int64_t G = A.G;
+  // The two big scratch buffers (the operands' size again) first; with
+  // try_only an allocation failure returns false (nothing launched) so the
+  // caller can fall back to the DMMA kernel.
+  int8_t* as = nullptr;
+  int8_t* bs = nullptr;
+  const size_t a_bytes = (size_t)A.nblocks * OZ_BLOCK_BYTES;
+  const size_t b_bytes = sym_b ? 0 : (size_t)B.nblocks * OZ_BLOCK_BYTES;
+  if (try_only) {
+    if (a_bytes && cudaMallocAsync(reinterpret_cast<void**>(&as), a_bytes, s) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    if (b_bytes && cudaMallocAsync(reinterpret_cast<void**>(&bs), b_bytes, s) != cudaSuccess) {
+      cudaGetLastError();
+      dfree(as, s);
+      return false;
+    }
+  } else {
+    as = static_cast<int8_t*>(dmalloc_bytes(a_bytes, s));
+    bs = static_cast<int8_t*>(dmalloc_bytes(b_bytes, s));
+  }
+  if (sym_b) bs = as;
   int* ex_a = dmalloc<int>(G * OZ_NB, s);
-  int8_t* as = dmalloc<int8_t>((size_t)A.nblocks * OZ_BLOCK_BYTES, s);
   SPAMM_CK(cudaMemsetAsync(ex_a, 0x80, G * OZ_NB * sizeof(int), s));
   const int gx = grid_for(A.nblocks, 1, (int64_t)multiprocessors() * 8);
   launch_pdl(k_oz_exponents, gx, 256, 0, s, A.data, A.keys, A.nblocks, G, 0, ex_a);
@@ -541,7 +664,6 @@ void leaf_products_ozaki(int64_t n_seg, const int64_t* seg, const Idx* a_idx, co
   launch_pdl(k_oz_split, gx, 256, 0, s, A.data, A.keys, A.nblocks, G, 0, (const int*)ex_a, as);
   SPAMM_LAUNCH_CK();
   int* ex_b = ex_a;
-  int8_t* bs = as;
   int32_t* b_tr = nullptr;
   if (sym_b) {
     b_tr = dmalloc<int32_t>(A.nblocks > 0 ? A.nblocks : 1, s);
@@ -550,7 +672,6 @@ void leaf_products_ozaki(int64_t n_seg, const int64_t* seg, const Idx* a_idx, co
     SPAMM_LAUNCH_CK();
   } else {
     ex_b = dmalloc<int>(G * OZ_NB, s);
-    bs = dmalloc<int8_t>((size_t)B.nblocks * OZ_BLOCK_BYTES, s);
     SPAMM_CK(cudaMemsetAsync(ex_b, 0x80, G * OZ_NB * sizeof(int), s));
     const int gy = grid_for(B.nblocks, 1, (int64_t)multiprocessors() * 8);
     launch_pdl(k_oz_exponents, gy, 256, 0, s, B.data, B.keys, B.nblocks, G, 1, ex_b);
@@ -561,7 +682,28 @@ void leaf_products_ozaki(int64_t n_seg, const int64_t* seg, const Idx* a_idx, co
   const int32_t* order = lpt.order;
   int* counter = lpt.counter;
   int* scratch = nullptr;
-  if (!order || !counter) scratch = lpt_schedule(n_seg, seg, &order, &counter, s);
+  // C blocks are claimed in Morton order: neighbouring CTAs share operand rows
+  // and columns in L2 (measured 28.2 vs 28.9 ms of K4z per cfg4 solve against
+  // the longest-first order, whose tail advantage the short, uniform K4z
+  // blocks do not need).  SPAMM_K4_ORDER=lpt selects the LPT order.
+  static const bool morton = [] {
+    const char* v = getenv("SPAMM_K4_ORDER");
+    return !(v && strcmp(v, "lpt") == 0);
+  }();
+  if (morton) {
+    scratch = dmalloc<int>(1, s);
+    SPAMM_CK(cudaMemsetAsync(scratch, 0, sizeof(int), s));
+    counter = scratch;
+    order = nullptr;
+  } else if (!order || !counter) {
+    scratch = lpt_schedule(n_seg, seg, &order, &counter, s);
+  }
+  static const int hint = [] {  // L2 policy experiment bits (see the kernel)
+    const char* v = getenv("SPAMM_K4Z_HINT");
+    return v ? atoi(v) : 0;
+  }();
+  static const bool want_prof = getenv("SPAMM_K4Z_PROF") != nullptr;
+  long long* prof = nullptr;
   auto kern = k_leaf_ozaki<Idx>;
   static std::once_flag once;
   std::call_once(once, [&] {
@@ -569,11 +711,28 @@ void leaf_products_ozaki(int64_t n_seg, const int64_t* seg, const Idx* a_idx, co
   });
   int64_t grid = multiprocessors();
   if (grid > n_seg) grid = n_seg;
+  if (want_prof) {
+    prof = dmalloc<long long>((size_t)grid * 8, s);
+    SPAMM_CK(cudaMemsetAsync(prof, 0, (size_t)grid * 64, s));
+  }
   launch_pdl(kern, (unsigned)grid, OZ_THREADS, OZ_SMEM, s, n_seg, seg, a_idx, b_idx,
              (const int32_t*)b_tr, (const int64_t*)A.keys, (const int64_t*)B.keys, G,
              (const int8_t*)as, (const int8_t*)bs, (const int*)ex_a, (const int*)ex_b, c_out,
-             c_mirror, accumulate ? 1 : 0, C, order, counter);
+             c_mirror, accumulate ? 1 : 0, C, order, counter, hint, prof);
   SPAMM_LAUNCH_CK();
+  if (prof) {  // SPAMM_K4Z_PROF=1: per-launch cycle breakdown (diagnostics; syncs)
+    std::vector<long long> h((size_t)grid * 8);
+    SPAMM_CK(cudaMemcpyAsync(h.data(), prof, h.size() * 8, cudaMemcpyDeviceToHost, s));
+    SPAMM_CK(cudaStreamSynchronize(s));
+    double a[8] = {0};
+    for (int64_t b = 0; b < grid; ++b)
+      for (int i = 0; i < 8; ++i) a[i] += (double)h[b * 8 + i] / grid;
+    fprintf(stderr,
+            "[k4z] cycles %.0f: mma waits full %.0f tempty %.0f, tasks %.0f (%.0f cyc/task); "
+            "epi wait %.0f hold %.0f all %.0f blocks %.0f\n",
+            a[0], a[1], a[2], a[3], a[0] / (a[3] > 0 ? a[3] : 1), a[4], a[5], a[6], a[7]);
+    dfree(prof, s);
+  }
   dfree(scratch, s);
   dfree(b_tr, s);
   if (!sym_b) {
@@ -582,15 +741,16 @@ void leaf_products_ozaki(int64_t n_seg, const int64_t* seg, const Idx* a_idx, co
   }
   dfree(ex_a, s);
   dfree(as, s);
+  return true;
 }
 
-template void leaf_products_ozaki<int32_t>(int64_t, const int64_t*, const int32_t*,
+template bool leaf_products_ozaki<int32_t>(int64_t, const int64_t*, const int32_t*,
                                            const int32_t*, const int64_t*, const int64_t*, bool,
                                            const Mat&, const Mat&, bool, double*, cudaStream_t,
-                                           LptSchedule);
-template void leaf_products_ozaki<int64_t>(int64_t, const int64_t*, const int64_t*,
+                                           LptSchedule, bool);
+template bool leaf_products_ozaki<int64_t>(int64_t, const int64_t*, const int64_t*,
                                            const int64_t*, const int64_t*, const int64_t*, bool,
                                            const Mat&, const Mat&, bool, double*, cudaStream_t,
-                                           LptSchedule);
+                                           LptSchedule, bool);
 
 }  // namespace spamm

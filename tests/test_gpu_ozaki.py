@@ -1,0 +1,139 @@
+"""K4z, the INT8-sliced leaf kernel (leaf_ozaki.cu), against the reference
+semantics: the surviving task set and counters are the cull's (identical to
+the DMMA and exact kernels), C agrees with the reference-order product within
+the north-star tolerance (1e-12 relative Frobenius) and is closer than FP64
+itself to the exactly rounded product; symmetric inputs give bitwise symmetric
+C; segments longer than the int32 flush chunk; SP2 decisions identical."""
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+import paper_1403_7458_b200 as sp  # noqa: E402
+from paper_1403_7458_b200.synth import CONFIGS, decay_pair, water_cluster  # noqa: E402
+
+REL_FRO_TOL = 1e-12
+
+
+def rel_fro(x, ref):
+    return float(np.linalg.norm(x - ref) / np.linalg.norm(ref))
+
+
+def extended(da, db, n):
+    xa = np.zeros((n, n), np.longdouble)
+    xb = np.zeros((n, n), np.longdouble)
+    xa[:da.shape[0], :da.shape[1]] = da
+    xb[:db.shape[0], :db.shape[1]] = db
+    return xa @ xb
+
+
+def err_vs(c, ex):
+    return float(np.linalg.norm((c - ex).astype(np.float64)) / np.linalg.norm(ex.astype(np.float64)))
+
+
+@pytest.mark.parametrize("case", ["decay_ab", "decay_aa", "water", "wide", "wide_sym"])
+def test_products_vs_reference_and_extended_precision(case):
+    rng = np.random.default_rng(7)
+    if case.startswith("decay"):
+        da, db = decay_pair(1024, 0.1, (0, 1))
+        if case == "decay_aa":
+            db = da
+    elif case == "water":
+        da, _ = water_cluster(30, seed=0)
+        db = da
+    else:
+        x = rng.uniform(-1, 1, (512, 512)) * np.exp(rng.uniform(-30, 5, (512, 512)))
+        da = db = x + x.T if case == "wide_sym" else x
+    a = sp.build_from_dense(da, 64)
+    b = a if db is da else sp.build_from_dense(db, 64)
+    for tau in (0.0, 1e-8):
+        ce, se = sp.multiply(a, b, tau, kernel="exact")
+        co, so = sp.multiply(a, b, tau, kernel="ozaki")
+        assert so.counts_equal(se) and so.flop_estimate == se.flop_estimate
+        de, do = sp.to_dense(ce), sp.to_dense(co)
+        assert rel_fro(do, de) < REL_FRO_TOL
+        if tau == 0.0:
+            ex = extended(da, db, de.shape[0])
+            # one rounding of the digit-pair sum: closer to the exact product than
+            # the reference's own FP64 loop (measured 5-6e-17 vs 4-9e-16)
+            assert err_vs(do, ex) < 2e-16
+            assert err_vs(do, ex) < err_vs(de, ex)
+        if a is b and a.symmetric:
+            assert np.array_equal(do, do.T)
+            assert co.symmetric
+
+
+def test_symmetric_path_bitwise_equals_full_path():
+    h, _ = water_cluster(30, seed=0)
+    x = sp.build_from_dense(h, 64)
+    assert x.symmetric
+    c_sym, st_sym = sp.multiply(x, x, 1e-6, kernel="ozaki")
+    sp.set_symmetric_products(False)
+    try:
+        c_full, st_full = sp.multiply(x, x, 1e-6, kernel="ozaki")
+    finally:
+        sp.set_symmetric_products(True)
+    assert st_sym.symmetric and not st_full.symmetric
+    assert np.array_equal(sp.to_dense(c_sym), sp.to_dense(c_full))
+
+
+def test_deterministic_repeats():
+    da, db = decay_pair(1024, 0.05, (3, 4))
+    a, b = sp.build_from_dense(da, 64), sp.build_from_dense(db, 64)
+    c0 = sp.to_dense(sp.multiply(a, b, 1e-10, kernel="ozaki")[0])
+    for _ in range(3):
+        assert np.array_equal(sp.to_dense(sp.multiply(a, b, 1e-10, kernel="ozaki")[0]), c0)
+
+
+def test_long_segments_flush_in_chunks():
+    """G = 132 leaf blocks per side, tau = 0: every C block reduces 132 tasks,
+    more than the 128-task int32 chunk, so each block is flushed to FP64 twice."""
+    n = 132 * 64
+    g = torch.Generator(device="cuda").manual_seed(5)
+    d = torch.rand((n, n), dtype=torch.float64, device="cuda", generator=g) * 2 - 1
+    i = torch.arange(n, device="cuda", dtype=torch.float64)
+    d *= torch.exp(-0.002 * (i[:, None] - i[None, :]).abs())
+    a = sp.build_from_dense(d, 64)
+    cd, sd = sp.multiply(a, a, 0.0, kernel="dmma")
+    co, so = sp.multiply(a, a, 0.0, kernel="ozaki")
+    assert so.counts_equal(sd) and so.leaf_products == 132 ** 3
+    ref = (d @ d).cpu().numpy()
+    assert rel_fro(sp.to_dense(co), ref) < 1e-14
+    assert rel_fro(sp.to_dense(co), sp.to_dense(cd)) < 1e-14
+
+
+def test_zero_rows_and_empty_products():
+    rng = np.random.default_rng(11)
+    d = rng.standard_normal((300, 300))
+    d[17, :] = 0.0
+    d[:, 200:264] = 0.0
+    a = sp.build_from_dense(d, 64)
+    c, st = sp.multiply(a, a, 0.0, kernel="ozaki")
+    ref = d @ d
+    assert rel_fro(sp.to_dense(c), ref) < 1e-15
+    assert not sp.to_dense(c)[17].any()
+    z = sp.build_from_dense(np.zeros((200, 200)), 64)
+    c, st = sp.multiply(z, z, 0.0, kernel="ozaki")
+    assert st.leaf_products == 0 and not sp.to_dense(c).any()
+
+
+def test_block_size_guard():
+    a = sp.build_from_dense(np.eye(64), 32)
+    with pytest.raises(ValueError, match="block size 64"):
+        sp.multiply(a, a, 0.0, kernel="ozaki")
+
+
+def test_sp2_cfg4_same_decisions_as_dmma():
+    cfg = CONFIGS[4]
+    h, n_occ = water_cluster(cfg.n_mol, seed=0)
+    f = sp.build_from_dense(torch.from_numpy(h).cuda(), cfg.block_size)
+    kw = dict(criterion="fro", fro_tol=1e-6)
+    pd, sd = sp.sp2_solve(f, n_occ, cfg.tau, kernel="dmma", **kw)
+    po, so = sp.sp2_solve(f, n_occ, cfg.tau, kernel="ozaki", **kw)
+    assert so.iteration == sd.iteration and so.converged and sd.converged
+    assert so.branch_history == sd.branch_history
+    assert so.leaf_products == sd.leaf_products
+    assert rel_fro(sp.to_dense(po), sp.to_dense(pd)) < REL_FRO_TOL
+    assert po.symmetric

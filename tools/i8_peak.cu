@@ -1,0 +1,113 @@
+// INT8 tensor-core peak for sm_100a: back-to-back tcgen05.mma kind::i8
+// (cta_group::1, A and B from shared memory, D in TMEM), one CTA per SM.
+// The roofline denominator of the INT8-sliced leaf kernel K4z (MEASURED_PEAKS
+// has no INT8 entry).  Shapes: M = 128, N = 128 (K4z's) and 256, K = 32.
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o i8_peak i8_peak.cu
+#include <cstdio>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { \
+  printf("CUDA error %s at %s:%d\n", cudaGetErrorString(e), __FILE__, __LINE__); return 1; } } while (0)
+
+__device__ __forceinline__ uint64_t desc(uint32_t addr) {  // K-major, no swizzle
+  return (uint64_t)((addr >> 4) & 0x3FFFu) | ((uint64_t)(128 >> 4) << 16) |
+         ((uint64_t)(256 >> 4) << 32) | (1ull << 46);
+}
+
+template <int N>
+__global__ void __launch_bounds__(128, 1) k_i8_peak(int iters, int* out) {
+  __shared__ __align__(1024) int8_t a[128 * 32];
+  __shared__ __align__(1024) int8_t b[256 * 32];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tslot;
+  for (int i = threadIdx.x; i < 128 * 32; i += 128) a[i] = (int8_t)(i & 7);
+  for (int i = threadIdx.x; i < 256 * 32; i += 128) b[i] = (int8_t)((i >> 3) & 7);
+  const uint32_t bar_a = (uint32_t)__cvta_generic_to_shared(&bar);
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(bar_a));
+    asm volatile("fence.mbarrier_init.release.cluster;\n");
+  }
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  if (threadIdx.x < 32) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(
+        (uint32_t)__cvta_generic_to_shared(&tslot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n");
+  const uint32_t tb = tslot;
+  constexpr uint32_t idesc =
+      (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((128u >> 4) << 24);
+  if (threadIdx.x == 0) {
+    const uint64_t da = desc((uint32_t)__cvta_generic_to_shared(a));
+    const uint64_t db = desc((uint32_t)__cvta_generic_to_shared(b));
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const uint32_t d = tb + (uint32_t)((j % (512 / N)) * N);
+        asm volatile(
+            "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+            " tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
+            "l"(da), "l"(db), "r"(idesc), "r"(1));
+      }
+    }
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::
+                     "r"(bar_a));
+    uint32_t ok = 0;
+    do {
+      asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n"
+                   " selp.u32 %0, 1, 0, p;\n}\n" : "=r"(ok) : "r"(bar_a) : "memory");
+    } while (!ok);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n");
+  if (threadIdx.x < 32) {
+    int v;
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];\n" : "=r"(v) : "r"(tb));
+    asm volatile("tcgen05.wait::ld.sync.aligned;\n");
+    if (v == 12345) out[0] = v;
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tb));
+  }
+}
+
+template <int N>
+int run(int sms, int clock_khz, int* out, bool last) {
+  const int iters = 20000;
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  k_i8_peak<N><<<sms, 128>>>(100, out);
+  CK(cudaDeviceSynchronize());
+  float best = 1e30f;
+  for (int r = 0; r < 5; ++r) {
+    CK(cudaEventRecord(e0));
+    k_i8_peak<N><<<sms, 128>>>(iters, out);
+    CK(cudaEventRecord(e1));
+    CK(cudaEventSynchronize(e1));
+    float ms;
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    if (ms < best) best = ms;
+  }
+  const double ops = 2.0 * 128 * N * 32 * 8.0 * iters * sms;
+  printf("{\"op\": \"tcgen05_i8_m128n%dk32\", \"ms\": %.4f, \"tops\": %.1f, "
+         "\"cycles_per_mma\": %.2f}%s\n",
+         N, best, ops / (best * 1e-3) / 1e12,
+         best * 1e-3 * clock_khz * 1e3 / (8.0 * iters), last ? "" : ",");
+  return 0;
+}
+
+int main() {
+  int dev = 0, sms = 0, clk = 0;
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  CK(cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, dev));
+  int* out;
+  CK(cudaMalloc(&out, 4));
+  printf("{\"sms\": %d, \"clock_khz\": %d, \"results\": [\n", sms, clk);
+  if (run<128>(sms, clk, out, false)) return 1;
+  if (run<256>(sms, clk, out, true)) return 1;
+  printf("]}\n");
+  return 0;
+}
