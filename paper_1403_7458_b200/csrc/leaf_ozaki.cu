@@ -92,7 +92,7 @@ __global__ void __launch_bounds__(256) k_oz_exponents(const double* __restrict__
                                                       int* __restrict__ ex) {
   pdl_wait();
   __shared__ double red[4][OZ_NB];
-  const int t = threadIdx.x, w = t >> 5, l = t & 31;
+  const int t = threadIdx.x;
   for (int64_t s = blockIdx.x; s < nblocks; s += gridDim.x) {
     const double* b = data + s * (OZ_NB * OZ_NB);
     const int64_t key = keys[s];
@@ -108,20 +108,53 @@ __global__ void __launch_bounds__(256) k_oz_exponents(const double* __restrict__
       }
       __syncthreads();
     } else {
-      for (int r = w * 8; r < w * 8 + 8; ++r) {
-        const double2 v = reinterpret_cast<const double2*>(b + r * OZ_NB)[l];
-        double mx = fmax(fabs(v.x), fabs(v.y));
+      // thread t: 16 consecutive elements of row t / 4 (8 independent 16-byte loads)
+      const double2* q = reinterpret_cast<const double2*>(b + (t >> 2) * OZ_NB + (t & 3) * 16);
+      double2 v[8];
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-        if (l == 0 && mx > 0.0) atomicMax(ex + (key / G) * OZ_NB + r, oz_frexp(mx));
-      }
+      for (int i = 0; i < 8; ++i) v[i] = q[i];
+      double mx = 0.0;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) mx = fmax(mx, fmax(fabs(v[i].x), fabs(v[i].y)));
+      mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+      mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+      if ((t & 3) == 0 && mx > 0.0) atomicMax(ex + (key / G) * OZ_NB + (t >> 2), oz_frexp(mx));
     }
   }
+}
+
+// The 8 signed digits of x against the scale 2^E, packed as bytes (slice p =
+// byte 7 - p): V = floor(|x| 2^(63-E)) from the bit pattern (|x| 2^-E < 1, so
+// V < 2^63; the bytes of V are the floor digits), then the carry pass as one
+// add -- W = V + 0x80 (0x7F for x < 0) in each of the 7 low bytes -- whose
+// bytes XOR the same constant are the signed digits (negated for x < 0, the
+// carry threshold 129 there keeping them in [-128, 127]).
+__device__ __forceinline__ uint64_t oz_digits(double x, int e) {
+  const uint64_t bits = (uint64_t)__double_as_longlong(x);
+  const bool neg = bits >> 63;
+  int be = (int)((bits >> 52) & 0x7FF);
+  uint64_t m = bits & 0xFFFFFFFFFFFFFull;
+  if (be) m |= 1ull << 52;
+  else be = 1;  // subnormal (or zero: m = 0)
+  const int sh = be - 1012 - e;  // |x| 2^(63-E) = m 2^sh, sh <= 10
+  const uint64_t v = sh >= 0 ? m << sh : (sh > -64 ? m >> -sh : 0ull);
+  const uint64_t off = neg ? 0x007F7F7F7F7F7F7Full : 0x0080808080808080ull;
+  const uint64_t w = v + off;
+  const uint64_t top = neg ? (uint64_t)((-(int)(w >> 56)) & 0xFF) : (w >> 56);
+  return ((w ^ off) & 0x00FFFFFFFFFFFFFFull) | (top << 56);
+}
+
+// Bytes `byte` of four packed digit words -> one 32-bit word (element order).
+__device__ __forceinline__ uint32_t oz_gather4(uint32_t a, uint32_t b, uint32_t c, uint32_t d,
+                                               int byte) {
+  const uint32_t sel = (uint32_t)byte | ((uint32_t)(4 + byte) << 4);
+  return __byte_perm(__byte_perm(a, b, sel), __byte_perm(c, d, sel), 0x5410);
 }
 
 // out + s * 32 KB: the 8 digit slices of block s.  trans = 0 (A role): slice
 // row n = block row n, exponent of global row bi*64+n; trans = 1 (B role,
 // K-major B^T): slice row n = block column n, exponent of global column bj*64+n.
+// Thread t: slice row n = t / 4, k = 16 (t % 4) .. +15 (one 16-byte store per slice).
 __global__ void __launch_bounds__(256) k_oz_split(const double* __restrict__ data,
                                                   const int64_t* __restrict__ keys,
                                                   int64_t nblocks, int64_t G, int trans,
@@ -132,58 +165,42 @@ __global__ void __launch_bounds__(256) k_oz_split(const double* __restrict__ dat
   const int t = threadIdx.x, n = t >> 2, kc = t & 3;
   for (int64_t s = blockIdx.x; s < nblocks; s += gridDim.x) {
     const double* b = data + s * (OZ_NB * OZ_NB);
-    for (int i = t; i < OZ_NB * OZ_NB; i += 256) tile[(i >> 6) * (OZ_NB + 1) + (i & 63)] = b[i];
-    __syncthreads();
+    double y[16];
+    if (trans) {
+      for (int i = t; i < OZ_NB * OZ_NB; i += 256) tile[(i >> 6) * (OZ_NB + 1) + (i & 63)] = b[i];
+      __syncthreads();
+#pragma unroll
+      for (int i = 0; i < 16; ++i) y[i] = tile[(kc * 16 + i) * (OZ_NB + 1) + n];
+      __syncthreads();
+    } else {
+      const double2* q = reinterpret_cast<const double2*>(b + n * OZ_NB + kc * 16);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const double2 v = q[i];
+        y[2 * i] = v.x;
+        y[2 * i + 1] = v.y;
+      }
+    }
     const int64_t key = keys[s];
-    const int64_t g = trans ? key % G : key / G;
-    const int e = oz_exp(ex[g * OZ_NB + n]);
-    uint32_t dig[OZ_SLICES][4];
-#pragma unroll
-    for (int p = 0; p < OZ_SLICES; ++p)
-#pragma unroll
-      for (int q = 0; q < 4; ++q) dig[p][q] = 0u;
+    const int e = oz_exp(ex[(trans ? key % G : key / G) * OZ_NB + n]);
+    uint32_t hi[16], lo[16];
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
-      const int k = kc * 16 + i;
-      double y = trans ? tile[k * (OZ_NB + 1) + n] : tile[n * (OZ_NB + 1) + k];
-      // x 2^-E = s_0 2^-7 + sum_{p>=1} s_p 2^-(7+8p): floor digits of |x|
-      // (unsigned 8-bit tail), signed with carries from the bottom, negated for
-      // x < 0 (carry at > 128 there, so the negated digits stay in [-128, 127])
-      // -- every step exact.
-      const bool neg = y < 0.0;
-      double t = ldexp(fabs(y), 7 - e);  // <= 127.25 (exponent bump in k_oz_exponents)
-      const double d0 = floor(t);
-      double r = __dsub_rn(t, d0);  // [0, 1), exact
-      int u[OZ_SLICES];
-#pragma unroll
-      for (int p = 1; p < OZ_SLICES; ++p) {
-        t = __dmul_rn(r, 256.0);
-        const double f = floor(t);
-        r = __dsub_rn(t, f);
-        u[p] = (int)f;  // [0, 255]
-      }
-      const int thr = neg ? 129 : 128;
-      int c = 0;
-#pragma unroll
-      for (int p = OZ_SLICES - 1; p >= 1; --p) {
-        const int v = u[p] + c;
-        c = v >= thr ? 1 : 0;
-        u[p] = v - 256 * c;
-      }
-      u[0] = (int)d0 + c;  // <= 127: d0 = 127 leaves r < 1/4, no carry
-      if (neg)
-#pragma unroll
-        for (int p = 0; p < OZ_SLICES; ++p) u[p] = -u[p];
-#pragma unroll
-      for (int p = 0; p < OZ_SLICES; ++p)
-        dig[p][i >> 2] |= ((uint32_t)u[p] & 0xffu) << (8 * (i & 3));
+      const uint64_t d = oz_digits(y[i], e);
+      hi[i] = (uint32_t)(d >> 32);  // slices 0..3 = bytes 3..0
+      lo[i] = (uint32_t)d;          // slices 4..7 = bytes 3..0
     }
     int8_t* o = out + s * OZ_BLOCK_BYTES + oz_off(n, kc * 16);
 #pragma unroll
-    for (int p = 0; p < OZ_SLICES; ++p)
+    for (int p = 0; p < OZ_SLICES; ++p) {
+      const uint32_t* h = p < 4 ? hi : lo;
+      const int byte = 3 - (p & 3);
       *reinterpret_cast<uint4*>(o + p * OZ_SLICE_BYTES) =
-          make_uint4(dig[p][0], dig[p][1], dig[p][2], dig[p][3]);
-    __syncthreads();
+          make_uint4(oz_gather4(h[0], h[1], h[2], h[3], byte),
+                     oz_gather4(h[4], h[5], h[6], h[7], byte),
+                     oz_gather4(h[8], h[9], h[10], h[11], byte),
+                     oz_gather4(h[12], h[13], h[14], h[15], byte));
+    }
   }
 }
 

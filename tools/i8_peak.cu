@@ -73,6 +73,94 @@ __global__ void __launch_bounds__(128, 1) k_i8_peak(int iters, int* out) {
   }
 }
 
+// K4z's per-task MMA pattern from one 64-KB stage (8 A slices + 8 B slices in
+// the K-major no-swizzle layout, SBO 512 B): 10 slice pairs x 2 k-steps into
+// 4 tiles, no TMA traffic -- isolates the tensor-pipe rate of the pattern.
+__device__ __forceinline__ uint64_t desc512(uint32_t addr) {
+  return (uint64_t)((addr >> 4) & 0x3FFFu) | ((uint64_t)(128 >> 4) << 16) |
+         ((uint64_t)(512 >> 4) << 32) | (1ull << 46);
+}
+__global__ void __launch_bounds__(128, 1) k_i8_k4z_pattern(int iters, int* out) {
+  extern __shared__ __align__(1024) int8_t sm[];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tslot;
+  for (int i = threadIdx.x; i < 65536; i += 128) sm[i] = (int8_t)((i * 7) & 15);
+  const uint32_t bar_a = (uint32_t)__cvta_generic_to_shared(&bar);
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(bar_a));
+    asm volatile("fence.mbarrier_init.release.cluster;\n");
+  }
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  if (threadIdx.x < 32) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(
+        (uint32_t)__cvta_generic_to_shared(&tslot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n");
+  const uint32_t tb = tslot;
+  constexpr uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((128u >> 3) << 17) | ((128u >> 4) << 24);
+  const int P[10] = {0, 0, 2, 0, 2, 4, 0, 2, 4, 6}, Q[10] = {0, 2, 0, 4, 2, 0, 6, 4, 2, 0};
+  if (threadIdx.x == 0) {
+    const uint32_t sa = (uint32_t)__cvta_generic_to_shared(sm), sb = sa + 32768;
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+      for (int c = 0; c < 10; ++c)
+#pragma unroll
+        for (int ks = 0; ks < 2; ++ks) {
+          const uint32_t d = tb + 128u * ((P[c] + Q[c]) / 2);
+          asm volatile(
+              "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+              " tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
+              "l"(desc512(sa + P[c] * 4096 + ks * 256)), "l"(desc512(sb + Q[c] * 4096 + ks * 256)),
+              "r"(idesc), "r"(1));
+        }
+    }
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::
+                     "r"(bar_a));
+    uint32_t ok = 0;
+    do {
+      asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n"
+                   " selp.u32 %0, 1, 0, p;\n}\n" : "=r"(ok) : "r"(bar_a) : "memory");
+    } while (!ok);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n");
+  if (threadIdx.x < 32) {
+    int v;
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];\n" : "=r"(v) : "r"(tb));
+    asm volatile("tcgen05.wait::ld.sync.aligned;\n");
+    if (v == 12345) out[0] = v;
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tb));
+  }
+}
+
+int run_pattern(int sms, int clock_khz, int* out) {
+  const int iters = 2000;
+  CK(cudaFuncSetAttribute(k_i8_k4z_pattern, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536 + 1024));
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  k_i8_k4z_pattern<<<sms, 128, 65536 + 1024>>>(10, out);
+  CK(cudaDeviceSynchronize());
+  float best = 1e30f;
+  for (int r = 0; r < 5; ++r) {
+    CK(cudaEventRecord(e0));
+    k_i8_k4z_pattern<<<sms, 128, 65536 + 1024>>>(iters, out);
+    CK(cudaEventRecord(e1));
+    CK(cudaEventSynchronize(e1));
+    float ms;
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    if (ms < best) best = ms;
+  }
+  printf("{\"op\": \"k4z_task_pattern\", \"ms\": %.4f, \"cycles_per_task\": %.1f, "
+         "\"tops\": %.1f},\n", best, best * 1e-3 * clock_khz * 1e3 / iters,
+         20.0 * 2 * 128 * 128 * 32 * iters * sms / (best * 1e-3) / 1e12);
+  return 0;
+}
+
 template <int N>
 int run(int sms, int clock_khz, int* out, bool last) {
   const int iters = 20000;
@@ -106,6 +194,7 @@ int main() {
   int* out;
   CK(cudaMalloc(&out, 4));
   printf("{\"sms\": %d, \"clock_khz\": %d, \"results\": [\n", sms, clk);
+  if (run_pattern(sms, clk, out)) return 1;
   if (run<128>(sms, clk, out, false)) return 1;
   if (run<256>(sms, clk, out, true)) return 1;
   printf("]}\n");
