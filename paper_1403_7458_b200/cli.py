@@ -13,7 +13,7 @@ reported data; 2 on argument or input errors) as the reference.  Every
 command writes ``<out>.manifest.json``; ``rerun`` replays it.  ``--mode``,
 ``--workers`` and ``--deterministic`` are accepted and validated as in the
 reference; the device path is deterministic for any setting.  Extra flags:
-``--leaf-kernel {auto,exact}`` (exact = the reference's rounding, bitwise)
+``--leaf-kernel {auto,ozaki,dmma,exact}`` (exact = the reference's rounding, bitwise)
 and, for ``sp2``, ``--criterion {trace,fro}`` / ``--fro-tol`` (BASELINE's
 ||X^2 - X||_F stopping rule).  The reference's ``gen``, ``sweep size`` and
 ``sweep pe`` (input generators and the decomposition simulator) are outside
@@ -144,9 +144,10 @@ def _exec_flags(p) -> None:
                    help=f"tasked-mode worker count (default ${WORKERS_ENV_VAR} or cpu count)")
     p.add_argument("--deterministic", action=argparse.BooleanOptionalAction, default=True,
                    help="fix the accumulation order (the device path always does)")
-    p.add_argument("--leaf-kernel", choices=["auto", "exact"], default="auto",
-                   help="auto: FP64 tensor cores (rel. Frobenius <= 1e-12); exact: "
-                        "bitwise the reference's rounding")
+    p.add_argument("--leaf-kernel", choices=["auto", "ozaki", "dmma", "exact"], default="auto",
+                   help="auto: INT8-digit tensor-core products for block size 64 (ozaki), "
+                        "FP64 tensor cores (dmma) otherwise (rel. Frobenius <= 1e-12); "
+                        "exact: bitwise the reference's rounding")
 
 
 def _format_flag(p) -> None:
