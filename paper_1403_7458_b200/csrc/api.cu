@@ -450,6 +450,14 @@ int spamm_multiply(const spamm_mat* a, const spamm_mat* b, double tau, int32_t k
 
 namespace {
 
+bool auto_ozaki_enabled() {  // SPAMM_AUTO_LEAF=dmma: AUTO keeps the DMMA kernel
+  static const bool on = [] {
+    const char* v = getenv("SPAMM_AUTO_LEAF");
+    return !(v && strcmp(v, "dmma") == 0);
+  }();
+  return on;
+}
+
 // K4 dispatch: the INT8-sliced kernel takes the operand matrices (row / column
 // exponents from their keys), the others the block arrays.  AUTO picks it for
 // Nb = 64 (faster than DMMA and closer to the exact product), DMMA otherwise.
@@ -457,10 +465,7 @@ void leaf_dispatch(int64_t n, const int64_t* seg, const int32_t* ai, const int32
                    const int64_t* c_out, const int64_t* c_mirror, const spamm_mat* a,
                    const spamm_mat* b, double* C, int32_t kernel, cudaStream_t s,
                    spamm::LptSchedule lpt) {
-  static const bool auto_ozaki = [] {  // SPAMM_AUTO_LEAF=dmma: AUTO keeps the DMMA kernel
-    const char* v = getenv("SPAMM_AUTO_LEAF");
-    return !(v && strcmp(v, "dmma") == 0);
-  }();
+  const bool auto_ozaki = auto_ozaki_enabled();
   const bool sym_b = a == b && a->m.sym;
   if (kernel == spamm::LEAF_OZAKI) {
     spamm::leaf_products_ozaki<int32_t>(n, seg, ai, bi, c_out, c_mirror, false, a->m, b->m,
@@ -477,11 +482,86 @@ void leaf_dispatch(int64_t n, const int64_t* seg, const int32_t* ai, const int32
                                   b->m.data, b->m.nblocks, C, a->m.nb, kernel, s, lpt);
 }
 
+// K4z's operand pre-passes (row exponents, digit slices) depend only on the
+// operands, so they run on a side stream while the cull and its host sync
+// run on s; K4z then waits for them (one event each way).
+struct OzakiAhead {
+  spamm::OzakiOperands op;
+  cudaEvent_t ready = nullptr;
+  bool ok = false;
+  cudaStream_t s = nullptr;
+  ~OzakiAhead() {  // error paths: nothing launched K4z, give the scratch back
+    if (!ok) return;
+    if (ready) cudaEventDestroy(ready);
+    try {
+      spamm::ozaki_release(op, s);
+    } catch (...) {
+    }
+  }
+};
+size_t device_total_bytes() {
+  static const size_t total = [] {
+    size_t f = 0, t = 0;
+    SPAMM_CK(cudaMemGetInfo(&f, &t));
+    return t;
+  }();
+  return total;
+}
+cudaStream_t ozaki_side_stream() {
+  thread_local cudaStream_t side = [] {
+    cudaStream_t t = nullptr;
+    SPAMM_CK(cudaStreamCreateWithFlags(&t, cudaStreamNonBlocking));
+    return t;
+  }();
+  return side;
+}
+void ozaki_ahead(const spamm_mat* a, const spamm_mat* b, int32_t kernel, cudaStream_t s,
+                 OzakiAhead& oz) {
+  // AUTO prepares ahead only when the slices are small next to HBM (they are
+  // allocated before C, whose size the cull has not told yet); larger
+  // operands take the post-cull path (leaf_dispatch), which tries the
+  // allocation after C's and falls back to DMMA (config 5 on one GPU).
+  const size_t slices = (size_t)(a->m.nblocks + (a == b && a->m.sym ? 0 : b->m.nblocks)) *
+                        a->m.nb * a->m.nb * 8;
+  const bool want = kernel == spamm::LEAF_OZAKI ||
+                    (kernel == spamm::LEAF_AUTO && auto_ozaki_enabled() &&
+                     spamm::ozaki_supported(a->m.nb) && slices <= device_total_bytes() / 8);
+  if (!want) return;
+  oz.s = s;
+  static const bool use_side = [] {
+    const char* v = getenv("SPAMM_OZ_SIDE");
+    return !(v && strcmp(v, "0") == 0);
+  }();
+  if (!use_side) {
+    oz.ok = spamm::ozaki_prepare(a->m, b->m, a == b && a->m.sym, s, oz.op,
+                                 /*try_only=*/kernel == spamm::LEAF_AUTO);
+    if (oz.ok) {
+      SPAMM_CK(cudaEventCreateWithFlags(&oz.ready, cudaEventDisableTiming));
+      SPAMM_CK(cudaEventRecord(oz.ready, s));
+    }
+    return;
+  }
+  cudaStream_t side = ozaki_side_stream();
+  cudaEvent_t operands;
+  SPAMM_CK(cudaEventCreateWithFlags(&operands, cudaEventDisableTiming));
+  SPAMM_CK(cudaEventRecord(operands, s));
+  SPAMM_CK(cudaStreamWaitEvent(side, operands, 0));
+  SPAMM_CK(cudaEventDestroy(operands));
+  oz.ok = spamm::ozaki_prepare(a->m, b->m, a == b && a->m.sym, side, oz.op,
+                               /*try_only=*/kernel == spamm::LEAF_AUTO);
+  if (oz.ok) {
+    SPAMM_CK(cudaEventCreateWithFlags(&oz.ready, cudaEventDisableTiming));
+    SPAMM_CK(cudaEventRecord(oz.ready, side));
+  }
+}
+
 void multiply_impl(const spamm_mat* a, const spamm_mat* b, double tau, int32_t kernel, bool timed,
                    cudaStream_t s, spamm::Mat& C, spamm_stats* stats, int64_t lo, int64_t hi,
                    int32_t* work, bool defer_prune, spamm::IdemFuse idem) {
   EventTimer tm(timed, s);
   tm.mark(0);
+  OzakiAhead oz;
+  ozaki_ahead(a, b, kernel, s, oz);
   spamm::CullResult r;
   // Symmetric SpAMM: X*X with X == X^T bitwise -> compute C_ij for i <= j only
   // and store C_ji = C_ij^T (bitwise what the full product yields).
@@ -535,7 +615,20 @@ void multiply_impl(const spamm_mat* a, const spamm_mat* b, double tau, int32_t k
   C.data = spamm::dmalloc<double>((size_t)C.nblocks * nb2, s);
   if (g_side) g_side->window(s);  // PCIe chunk alongside K4
   tm.mark(1);  // leaf window = the K4 launch only (allocation stays outside)
-  if (r.n_c > 0) {
+  if (oz.ok) {  // K4z on the operands prepared alongside the cull
+    SPAMM_CK(cudaStreamWaitEvent(s, oz.ready, 0));
+    SPAMM_CK(cudaEventDestroy(oz.ready));
+    oz.ready = nullptr;
+    if (r.n_c > 0) {
+      spamm::LptSchedule lpt;
+      lpt.order = r.order;
+      lpt.counter = r.counter;
+      spamm::ozaki_launch<int32_t>(r.n_c, r.seg, r.a_idx, r.b_idx, c_out, c_mirror, false,
+                                   a->m, b->m, oz.op, C.data, s, lpt);
+    }
+    spamm::ozaki_release(oz.op, s);
+    oz.ok = false;
+  } else if (r.n_c > 0) {
     spamm::LptSchedule lpt;
     lpt.order = r.order;
     lpt.counter = r.counter;

@@ -53,6 +53,20 @@ extern std::atomic<long long> g_launch_count;
 // SPAMM_PDL=0 launches them plainly.
 bool pdl_enabled();
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+// launch_plain: a kernel whose stream predecessor is a cudaStreamWaitEvent
+// (work of another stream) must not be launched programmatically -- the early
+// start would only wait for the last kernel of its own stream.
+template <class... KArgs, class... Args>
+inline void launch_plain(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                         Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cfg.numAttrs = 0;
+  SPAMM_CK(cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...));
+}
 template <class... KArgs, class... Args>
 inline void launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
                        Args&&... args) {

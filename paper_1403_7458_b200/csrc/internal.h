@@ -205,6 +205,27 @@ int* lpt_schedule(int64_t n_seg, const int64_t* seg, const int32_t** order, int*
 bool ozaki_supported(int nb);
 // try_only: return false (nothing launched, nothing left allocated) when the
 // digit-slice scratch (the operands' size again) cannot be allocated.
+// The operand side of K4z split out, so the pre-passes (row exponents, digit
+// slices, transposed slots) can run on another stream while the cull runs:
+// prepare (launches on s), launch K4z (s must be ordered after prepare's
+// stream), release.
+struct OzakiOperands {
+  int8_t* as = nullptr;
+  int8_t* bs = nullptr;
+  int* ex_a = nullptr;
+  int* ex_b = nullptr;
+  int32_t* b_tr = nullptr;
+  int64_t G = 0;
+  bool sym_b = false;
+};
+bool ozaki_prepare(const Mat& A, const Mat& B, bool sym_b, cudaStream_t s, OzakiOperands& op,
+                   bool try_only);
+template <class Idx>
+void ozaki_launch(int64_t n_seg, const int64_t* seg, const Idx* a_idx, const Idx* b_idx,
+                  const int64_t* c_out, const int64_t* c_mirror, bool accumulate, const Mat& A,
+                  const Mat& B, const OzakiOperands& op, double* C, cudaStream_t s,
+                  LptSchedule lpt = {});
+void ozaki_release(OzakiOperands& op, cudaStream_t s);
 template <class Idx>
 bool leaf_products_ozaki(int64_t n_seg, const int64_t* seg, const Idx* a_idx, const Idx* b_idx,
                          const int64_t* c_out, const int64_t* c_mirror, bool accumulate,

@@ -643,59 +643,90 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
 
 bool ozaki_supported(int nb) { return nb == OZ_NB; }
 
-template <class Idx>
-bool leaf_products_ozaki(int64_t n_seg, const int64_t* seg, const Idx* a_idx, const Idx* b_idx,
-                         const int64_t* c_out, const int64_t* c_mirror, bool accumulate,
-                         const Mat& A, const Mat& B, bool sym_b, double* C, cudaStream_t s,
-                         LptSchedule lpt, bool try_only) {
-  if (n_seg <= 0) return true;
+static void oz_dbg(const char* what, cudaStream_t s) {
+  static const bool on = getenv("SPAMM_OZ_DEBUG") != nullptr;
+  if (!on) return;
+  const cudaError_t e = cudaStreamSynchronize(s);
+  fprintf(stderr, "[oz] %s: %s\n", what, cudaGetErrorString(e));
+}
+
+bool ozaki_prepare(const Mat& A, const Mat& B, bool sym_b, cudaStream_t s, OzakiOperands& op,
+                   bool try_only) {
+  op = OzakiOperands();
+  oz_dbg("enter", s);
   if (A.nb != OZ_NB || B.nb != OZ_NB) throw CudaError("INT8-sliced leaf kernel needs block size 64");
   const int64_t G = A.G;
+  op.G = G;
+  op.sym_b = sym_b;
   // The two big scratch buffers (the operands' size again) first; with
   // try_only an allocation failure returns false (nothing launched) so the
   // caller can fall back to the DMMA kernel.
-  int8_t* as = nullptr;
-  int8_t* bs = nullptr;
   const size_t a_bytes = (size_t)A.nblocks * OZ_BLOCK_BYTES;
   const size_t b_bytes = sym_b ? 0 : (size_t)B.nblocks * OZ_BLOCK_BYTES;
   if (try_only) {
-    if (a_bytes && cudaMallocAsync(reinterpret_cast<void**>(&as), a_bytes, s) != cudaSuccess) {
+    if (a_bytes && cudaMallocAsync(reinterpret_cast<void**>(&op.as), a_bytes, s) != cudaSuccess) {
       cudaGetLastError();
+      op.as = nullptr;
       return false;
     }
-    if (b_bytes && cudaMallocAsync(reinterpret_cast<void**>(&bs), b_bytes, s) != cudaSuccess) {
+    if (b_bytes && cudaMallocAsync(reinterpret_cast<void**>(&op.bs), b_bytes, s) != cudaSuccess) {
       cudaGetLastError();
-      dfree(as, s);
+      dfree(op.as, s);
+      op.as = op.bs = nullptr;
       return false;
     }
   } else {
-    as = static_cast<int8_t*>(dmalloc_bytes(a_bytes, s));
-    bs = static_cast<int8_t*>(dmalloc_bytes(b_bytes, s));
+    op.as = static_cast<int8_t*>(dmalloc_bytes(a_bytes, s));
+    op.bs = static_cast<int8_t*>(dmalloc_bytes(b_bytes, s));
   }
-  if (sym_b) bs = as;
-  int* ex_a = dmalloc<int>(G * OZ_NB, s);
-  SPAMM_CK(cudaMemsetAsync(ex_a, 0x80, G * OZ_NB * sizeof(int), s));
+  op.ex_a = dmalloc<int>(G * OZ_NB, s);
+  SPAMM_CK(cudaMemsetAsync(op.ex_a, 0x80, G * OZ_NB * sizeof(int), s));
   const int gx = grid_for(A.nblocks, 1, (int64_t)multiprocessors() * 8);
-  launch_pdl(k_oz_exponents, gx, 256, 0, s, A.data, A.keys, A.nblocks, G, 0, ex_a);
+  launch_plain(k_oz_exponents, gx, 256, 0, s, A.data, A.keys, A.nblocks, G, 0, op.ex_a);
   SPAMM_LAUNCH_CK();
-  launch_pdl(k_oz_split, gx, 256, 0, s, A.data, A.keys, A.nblocks, G, 0, (const int*)ex_a, as);
+  oz_dbg("exponents A", s);
+  launch_pdl(k_oz_split, gx, 256, 0, s, A.data, A.keys, A.nblocks, G, 0, (const int*)op.ex_a,
+             op.as);
   SPAMM_LAUNCH_CK();
-  int* ex_b = ex_a;
-  int32_t* b_tr = nullptr;
+  oz_dbg("split A", s);
   if (sym_b) {
-    b_tr = dmalloc<int32_t>(A.nblocks > 0 ? A.nblocks : 1, s);
+    op.ex_b = op.ex_a;
+    op.bs = op.as;
+    op.b_tr = dmalloc<int32_t>(A.nblocks > 0 ? A.nblocks : 1, s);
     launch_pdl(k_oz_trslot, grid_for(A.nblocks, 256), 256, 0, s, (const int64_t*)A.keys,
-               A.nblocks, G, (const int32_t*)A.slot, b_tr);
+               A.nblocks, G, (const int32_t*)A.slot, op.b_tr);
     SPAMM_LAUNCH_CK();
   } else {
-    ex_b = dmalloc<int>(G * OZ_NB, s);
-    SPAMM_CK(cudaMemsetAsync(ex_b, 0x80, G * OZ_NB * sizeof(int), s));
+    op.ex_b = dmalloc<int>(G * OZ_NB, s);
+    SPAMM_CK(cudaMemsetAsync(op.ex_b, 0x80, G * OZ_NB * sizeof(int), s));
     const int gy = grid_for(B.nblocks, 1, (int64_t)multiprocessors() * 8);
-    launch_pdl(k_oz_exponents, gy, 256, 0, s, B.data, B.keys, B.nblocks, G, 1, ex_b);
+    launch_pdl(k_oz_exponents, gy, 256, 0, s, B.data, B.keys, B.nblocks, G, 1, op.ex_b);
     SPAMM_LAUNCH_CK();
-    launch_pdl(k_oz_split, gy, 256, 0, s, B.data, B.keys, B.nblocks, G, 1, (const int*)ex_b, bs);
+    launch_pdl(k_oz_split, gy, 256, 0, s, B.data, B.keys, B.nblocks, G, 1, (const int*)op.ex_b,
+               op.bs);
     SPAMM_LAUNCH_CK();
+    oz_dbg("B passes", s);
   }
+  return true;
+}
+
+void ozaki_release(OzakiOperands& op, cudaStream_t s) {
+  dfree(op.b_tr, s);
+  if (!op.sym_b) {
+    dfree(op.ex_b, s);
+    dfree(op.bs, s);
+  }
+  dfree(op.ex_a, s);
+  dfree(op.as, s);
+  op = OzakiOperands();
+}
+
+template <class Idx>
+void ozaki_launch(int64_t n_seg, const int64_t* seg, const Idx* a_idx, const Idx* b_idx,
+                  const int64_t* c_out, const int64_t* c_mirror, bool accumulate, const Mat& A,
+                  const Mat& B, const OzakiOperands& op, double* C, cudaStream_t s,
+                  LptSchedule lpt) {
+  if (n_seg <= 0) return;
   const int32_t* order = lpt.order;
   int* counter = lpt.counter;
   int* scratch = nullptr;
@@ -732,11 +763,13 @@ bool leaf_products_ozaki(int64_t n_seg, const int64_t* seg, const Idx* a_idx, co
     prof = dmalloc<long long>((size_t)grid * 8, s);
     SPAMM_CK(cudaMemsetAsync(prof, 0, (size_t)grid * 64, s));
   }
-  launch_pdl(kern, (unsigned)grid, OZ_THREADS, OZ_SMEM, s, n_seg, seg, a_idx, b_idx,
-             (const int32_t*)b_tr, (const int64_t*)A.keys, (const int64_t*)B.keys, G,
-             (const int8_t*)as, (const int8_t*)bs, (const int*)ex_a, (const int*)ex_b, c_out,
-             c_mirror, accumulate ? 1 : 0, C, order, counter, hint, prof);
+  // (plain launch: K4z follows a wait on the pre-pass stream, see launch_plain)
+  launch_plain(kern, (unsigned)grid, OZ_THREADS, OZ_SMEM, s, n_seg, seg, a_idx, b_idx,
+             (const int32_t*)op.b_tr, (const int64_t*)A.keys, (const int64_t*)B.keys, op.G,
+             (const int8_t*)op.as, (const int8_t*)op.bs, (const int*)op.ex_a, (const int*)op.ex_b,
+             c_out, c_mirror, accumulate ? 1 : 0, C, order, counter, hint, prof);
   SPAMM_LAUNCH_CK();
+  oz_dbg("k4z", s);
   if (prof) {  // SPAMM_K4Z_PROF=1: per-launch cycle breakdown (diagnostics; syncs)
     std::vector<long long> h((size_t)grid * 8);
     SPAMM_CK(cudaMemcpyAsync(h.data(), prof, h.size() * 8, cudaMemcpyDeviceToHost, s));
@@ -751,16 +784,24 @@ bool leaf_products_ozaki(int64_t n_seg, const int64_t* seg, const Idx* a_idx, co
     dfree(prof, s);
   }
   dfree(scratch, s);
-  dfree(b_tr, s);
-  if (!sym_b) {
-    dfree(ex_b, s);
-    dfree(bs, s);
-  }
-  dfree(ex_a, s);
-  dfree(as, s);
+}
+
+template <class Idx>
+bool leaf_products_ozaki(int64_t n_seg, const int64_t* seg, const Idx* a_idx, const Idx* b_idx,
+                         const int64_t* c_out, const int64_t* c_mirror, bool accumulate,
+                         const Mat& A, const Mat& B, bool sym_b, double* C, cudaStream_t s,
+                         LptSchedule lpt, bool try_only) {
+  if (n_seg <= 0) return true;
+  OzakiOperands op;
+  if (!ozaki_prepare(A, B, sym_b, s, op, try_only)) return false;
+  ozaki_launch<Idx>(n_seg, seg, a_idx, b_idx, c_out, c_mirror, accumulate, A, B, op, C, s, lpt);
+  ozaki_release(op, s);
   return true;
 }
 
+template void ozaki_launch<int32_t>(int64_t, const int64_t*, const int32_t*, const int32_t*,
+                                    const int64_t*, const int64_t*, bool, const Mat&, const Mat&,
+                                    const OzakiOperands&, double*, cudaStream_t, LptSchedule);
 template bool leaf_products_ozaki<int32_t>(int64_t, const int64_t*, const int32_t*,
                                            const int32_t*, const int64_t*, const int64_t*, bool,
                                            const Mat&, const Mat&, bool, double*, cudaStream_t,
