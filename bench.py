@@ -8,7 +8,11 @@ solve H -> P through the public API (Gershgorin bounds, X0, every SpAMM X^2,
 traces, EXPAND updates, idempotency tests), inputs resident in HBM.
 ``value`` = surviving-leaf flops of all multiplies (ProductStats.flop_estimate,
 kernel.py:248) / device time, in GFLOP/s.  ``sp2_ms_per_iter`` is the
-second half of BASELINE's metric.
+second half of BASELINE's metric.  The leaf products run on K4z (FP64
+products as exact signed-8-bit digit products on the INT8 tensor cores,
+DESIGN.md 4.3a; ``SPAMM_AUTO_LEAF=dmma`` selects the FP64 DMMA kernel), and
+the roofline object reports K4z against the measured INT8 tcgen05 peak with
+its FP64-equivalent rate against the DMMA peak beside it.
 
 ``--impl reference`` times the reference algorithm's CPU implementation on
 the host cores: the oracle port (oracle/spamm_oracle.py + oracle/leafgemm.c,

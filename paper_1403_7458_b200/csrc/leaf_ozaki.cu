@@ -663,6 +663,8 @@ bool ozaki_prepare(const Mat& A, const Mat& B, bool sym_b, cudaStream_t s, Ozaki
   // caller can fall back to the DMMA kernel.
   const size_t a_bytes = (size_t)A.nblocks * OZ_BLOCK_BYTES;
   const size_t b_bytes = sym_b ? 0 : (size_t)B.nblocks * OZ_BLOCK_BYTES;
+  static const bool force_fail = getenv("SPAMM_OZ_FORCE_NOMEM") != nullptr;  // test hook
+  if (try_only && force_fail) return false;
   if (try_only) {
     if (a_bytes && cudaMallocAsync(reinterpret_cast<void**>(&op.as), a_bytes, s) != cudaSuccess) {
       cudaGetLastError();

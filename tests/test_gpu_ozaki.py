@@ -137,3 +137,26 @@ def test_sp2_cfg4_same_decisions_as_dmma():
     assert so.leaf_products == sd.leaf_products
     assert rel_fro(sp.to_dense(po), sp.to_dense(pd)) < REL_FRO_TOL
     assert po.symmetric
+
+
+def test_auto_falls_back_to_dmma_without_slice_memory():
+    """AUTO needs the digit slices (the operand's size again); when they cannot
+    be allocated it runs the DMMA kernel (config 5's 84-GB H on one GPU).  The
+    SPAMM_OZ_FORCE_NOMEM hook makes every slice allocation fail."""
+    import os
+    import subprocess
+    import sys
+    code = (
+        "import numpy as np, paper_1403_7458_b200 as sp\n"
+        "from paper_1403_7458_b200.synth import water_cluster\n"
+        "h, _ = water_cluster(30, seed=0)\n"
+        "x = sp.build_from_dense(h, 64)\n"
+        "ca, _ = sp.multiply(x, x, 1e-8)\n"
+        "cd, _ = sp.multiply(x, x, 1e-8, kernel='dmma')\n"
+        "assert np.array_equal(sp.to_dense(ca), sp.to_dense(cd))\n"
+        "print('fallback ok')\n")
+    env = dict(os.environ, SPAMM_OZ_FORCE_NOMEM="1")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True,
+                         text=True, timeout=300)
+    assert out.returncode == 0 and "fallback ok" in out.stdout, out.stderr[-2000:]
