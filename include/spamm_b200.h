@@ -33,13 +33,13 @@ extern "C" {
 #define SPAMM_MAX_TIERS 64
 
 /* Leaf-product kernels (spamm_multiply / spamm_gemm_batch `kernel`). */
-#define SPAMM_LEAF_AUTO 0  /* INT8-sliced for Nb = 64 (matrix entry points), DMMA for Nb in {8,16,32}, else exact; SPAMM_AUTO_LEAF=dmma keeps DMMA at 64 */
+#define SPAMM_LEAF_AUTO 0  /* INT8-sliced for Nb in {32, 64} (matrix entry points), DMMA for Nb in {8,16}, else exact; SPAMM_AUTO_LEAF=dmma keeps DMMA */
 #define SPAMM_LEAF_DMMA 1  /* FP64 tensor cores (mma.sync f64 -> DMMA)       */
 #define SPAMM_LEAF_EXACT 2 /* CUDA-core, reference order: bitwise identical  */
 #define SPAMM_LEAF_DMMA_CPASYNC 3 /* first-generation DMMA kernel (A/B tests)  */
 /* FP64 products on the INT8 tensor cores (tcgen05 kind::i8, TMEM) by exact
  * digit slicing (Ozaki scheme I, 8 slices of 7 bits, per-row/column power-of-2
- * scales); Nb = 64 only; FP64-level error, deterministic, not bitwise DMMA.
+ * scales); Nb = 32 or 64; FP64-level error, deterministic, not bitwise DMMA.
  * Accepted by the matrix entry points (spamm_multiply*, spamm_sp2_*), not by
  * spamm_gemm_batch (it needs the operands' row / column exponents). */
 #define SPAMM_LEAF_OZAKI 4

@@ -429,7 +429,7 @@ int spamm_multiply(const spamm_mat* a, const spamm_mat* b, double tau, int32_t k
     return fail(SPAMM_EINVAL, "tau must be finite and >= 0, got " + std::to_string(tau));
   if (kernel < 0 || kernel > 4) return fail(SPAMM_EINVAL, "unknown leaf kernel");
   if (kernel == SPAMM_LEAF_OZAKI && !spamm::ozaki_supported(a->m.nb))
-    return fail(SPAMM_EINVAL, "INT8-sliced leaf kernel needs block size 64");
+    return fail(SPAMM_EINVAL, "INT8-sliced leaf kernel needs block size 32 or 64");
   if ((kernel == SPAMM_LEAF_DMMA || kernel == 3) && !spamm::dmma_supported(a->m.nb))
     return fail(SPAMM_EINVAL, "DMMA leaf kernel needs block size 8, 16, 32 or 64");
   if (!c) return fail(SPAMM_EINVAL, "null output handle");
@@ -450,12 +450,24 @@ int spamm_multiply(const spamm_mat* a, const spamm_mat* b, double tau, int32_t k
 
 namespace {
 
+// AUTO's choice of K4z for block size nb (SPAMM_AUTO_LEAF=dmma: never).
+bool auto_ozaki_for(int nb);
 bool auto_ozaki_enabled() {  // SPAMM_AUTO_LEAF=dmma: AUTO keeps the DMMA kernel
   static const bool on = [] {
     const char* v = getenv("SPAMM_AUTO_LEAF");
     return !(v && strcmp(v, "dmma") == 0);
   }();
   return on;
+}
+bool auto_ozaki_for(int nb) {
+  // Nb = 32: K4z is L2-bandwidth bound (16 KB of slices per 2 Nb^3 flops)
+  // and only ~15 % faster than DMMA there (cfg3: 10.9 vs 12.5 ms per solve);
+  // SPAMM_AUTO_OZ32=0 keeps DMMA at Nb = 32.
+  static const bool oz32 = [] {
+    const char* v = getenv("SPAMM_AUTO_OZ32");
+    return !(v && strcmp(v, "0") == 0);
+  }();
+  return auto_ozaki_enabled() && (nb == 64 || (nb == 32 && oz32));
 }
 
 // K4 dispatch: the INT8-sliced kernel takes the operand matrices (row / column
@@ -474,7 +486,7 @@ void leaf_dispatch(int64_t n, const int64_t* seg, const int32_t* ai, const int32
   }
   // AUTO also needs room for the digit slices (the operands' size again): a
   // matrix that nearly fills HBM (config 5 on one GPU) stays on DMMA.
-  if (kernel == spamm::LEAF_AUTO && auto_ozaki && spamm::ozaki_supported(a->m.nb) &&
+  if (kernel == spamm::LEAF_AUTO && auto_ozaki && auto_ozaki_for(a->m.nb) &&
       spamm::leaf_products_ozaki<int32_t>(n, seg, ai, bi, c_out, c_mirror, false, a->m, b->m,
                                           sym_b, C, s, lpt, /*try_only=*/true))
     return;
@@ -525,7 +537,7 @@ void ozaki_ahead(const spamm_mat* a, const spamm_mat* b, int32_t kernel, cudaStr
                         a->m.nb * a->m.nb * 8;
   const bool want = kernel == spamm::LEAF_OZAKI ||
                     (kernel == spamm::LEAF_AUTO && auto_ozaki_enabled() &&
-                     spamm::ozaki_supported(a->m.nb) && slices <= device_total_bytes() / 8);
+                     auto_ozaki_for(a->m.nb) && slices <= device_total_bytes() / 8);
   if (!want) return;
   oz.s = s;
   static const bool use_side = [] {
@@ -817,7 +829,7 @@ int spamm_sp2_step(const spamm_mat* x, double n_occ, double tau, int32_t kernel,
     return fail(SPAMM_EINVAL, "tau must be finite and >= 0, got " + std::to_string(tau));
   if (kernel < 0 || kernel > 4) return fail(SPAMM_EINVAL, "unknown leaf kernel");
   if (kernel == SPAMM_LEAF_OZAKI && !spamm::ozaki_supported(x->m.nb))
-    return fail(SPAMM_EINVAL, "INT8-sliced leaf kernel needs block size 64");
+    return fail(SPAMM_EINVAL, "INT8-sliced leaf kernel needs block size 32 or 64");
   if ((kernel == SPAMM_LEAF_DMMA || kernel == 3) && !spamm::dmma_supported(x->m.nb))
     return fail(SPAMM_EINVAL, "DMMA leaf kernel needs block size 8, 16, 32 or 64");
   SPAMM_API_BEGIN
@@ -860,7 +872,7 @@ int spamm_sp2_multiply_shard(const spamm_mat* x, double tau, int32_t kernel, int
     return fail(SPAMM_EINVAL, "tau must be finite and >= 0, got " + std::to_string(tau));
   if (kernel < 0 || kernel > 4) return fail(SPAMM_EINVAL, "unknown leaf kernel");
   if (kernel == SPAMM_LEAF_OZAKI && !spamm::ozaki_supported(x->m.nb))
-    return fail(SPAMM_EINVAL, "INT8-sliced leaf kernel needs block size 64");
+    return fail(SPAMM_EINVAL, "INT8-sliced leaf kernel needs block size 32 or 64");
   if (x->m.depth > 8) return fail(SPAMM_EINVAL, "sharded SP2 products need depth <= 8");
   SPAMM_API_BEGIN
   auto* h = new spamm_mat();
@@ -935,7 +947,7 @@ int spamm_multiply_range(const spamm_mat* a, const spamm_mat* b, double tau, int
     return fail(SPAMM_EINVAL, "tau must be finite and >= 0, got " + std::to_string(tau));
   if (kernel < 0 || kernel > 4) return fail(SPAMM_EINVAL, "unknown leaf kernel");
   if (kernel == SPAMM_LEAF_OZAKI && !spamm::ozaki_supported(a->m.nb))
-    return fail(SPAMM_EINVAL, "INT8-sliced leaf kernel needs block size 64");
+    return fail(SPAMM_EINVAL, "INT8-sliced leaf kernel needs block size 32 or 64");
   if (lo < 0 || hi < lo || hi > a->m.G * a->m.G)
     return fail(SPAMM_EINVAL, "shard range outside [0, G*G]");
   if (!c) return fail(SPAMM_EINVAL, "null output handle");
@@ -1172,7 +1184,7 @@ int spamm_sp2_solve_ex(const spamm_mat* f, double n_occ, double tau, int32_t max
   if (criterion != 0 && criterion != 1) return fail(SPAMM_EINVAL, "unknown criterion");
   if (kernel < 0 || kernel > 4) return fail(SPAMM_EINVAL, "unknown leaf kernel");
   if (kernel == SPAMM_LEAF_OZAKI && !spamm::ozaki_supported(f->m.nb))
-    return fail(SPAMM_EINVAL, "INT8-sliced leaf kernel needs block size 64");
+    return fail(SPAMM_EINVAL, "INT8-sliced leaf kernel needs block size 32 or 64");
   if ((kernel == SPAMM_LEAF_DMMA || kernel == 3) && !spamm::dmma_supported(f->m.nb))
     return fail(SPAMM_EINVAL, "DMMA leaf kernel needs block size 8, 16, 32 or 64");
   if (max_iter < 0) return fail(SPAMM_EINVAL, "max_iter must be >= 0");

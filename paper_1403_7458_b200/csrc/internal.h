@@ -216,8 +216,17 @@ struct OzakiOperands {
   int* ex_b = nullptr;
   int32_t* b_tr = nullptr;
   int64_t G = 0;
+  int nb = 64;
   bool sym_b = false;
 };
+// Nb = 32 variant (leaf_ozaki32.cu): operand passes (row / column exponents
+// when `exponents`, digit slices) and the K4z launch.
+void oz32_operand_passes(const Mat& M, bool trans, int* ex, int8_t* out, cudaStream_t s,
+                         bool exponents);
+template <class Idx>
+void oz32_launch(int64_t n_seg, const int64_t* seg, const Idx* a_idx, const Idx* b_idx,
+                 const int64_t* c_out, const int64_t* c_mirror, bool accumulate, const Mat& A,
+                 const Mat& B, const OzakiOperands& op, double* C, cudaStream_t s, int* counter);
 bool ozaki_prepare(const Mat& A, const Mat& B, bool sym_b, cudaStream_t s, OzakiOperands& op,
                    bool try_only);
 template <class Idx>

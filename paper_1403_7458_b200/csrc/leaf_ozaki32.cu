@@ -1,0 +1,453 @@
+// K4z for Nb = 32: the same exact signed-8-bit digit products as leaf_ozaki.cu
+// (scheme, scales and digit split described there), laid out for 32x32 blocks.
+//
+// A 32-row block gives 32 TMEM lanes per digit slice, so one 128-lane MMA
+// operand stacks FOUR slices (p .. p+3) of A and one 128-column operand four
+// slices of B: a single tcgen05.mma (M = N = 128, K = 32 = the whole block)
+// forms 16 digit pairs.  Three MMAs per leaf product -- anchors (0,0), (0,4),
+// (4,0) -- form every pair with p + q <= 7 exactly once (and some with
+// p + q <= 10), into two 128-column tiles whose 32x32 sub-blocks (i, j) hold
+// digit sum D + i + j (D = 0 for the first, 4 for the other two).  Two tiles
+// are 256 TMEM columns, so the accumulators are double-buffered: the epilogue
+// of one C block overlaps the MMAs of the next.
+//
+// Epilogue: the 16 sub-blocks of a C element (r, c) live in four TMEM lane
+// quarters (one per warp) and four column groups; each warp loads its quarter,
+// the values go through shared memory, and the owning thread adds the
+// sub-blocks of equal digit sum in int32 (exact) and rounds once per level
+// (Horner, FMA), as in leaf_ozaki.cu -- so results are deterministic and a
+// symmetric X gives a bitwise symmetric X*X.
+#include <climits>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+
+#include "internal.h"
+#include "ozaki_common.cuh"
+
+namespace spamm {
+
+namespace {
+
+using namespace ozk;
+
+constexpr int Z_NB = 32;
+constexpr int Z_SLICES = 8;
+constexpr int Z_SLICE_BYTES = Z_NB * Z_NB;                 // 1 KB
+constexpr int Z_BLOCK_BYTES = Z_SLICES * Z_SLICE_BYTES;    // 8 KB
+// A stage holds up to Z_TPS tasks of one accumulation chunk (A and B slices
+// of each): one barrier round trip per Z_TPS tasks -- with only 3 MMAs per
+// task (~200 tensor cycles) the per-task synchronisation would otherwise
+// dominate.
+constexpr int Z_TPS = 4;
+constexpr int Z_TASK = 2 * Z_BLOCK_BYTES;                  // 16 KB
+constexpr int Z_STAGES = 3;
+constexpr int Z_STAGE = Z_TPS * Z_TASK;                    // 64 KB
+constexpr int Z_CHUNK = 128;  // tasks per accumulation: |sub-block| <= 128 x 32 x 2^14 = 2^26
+constexpr int Z_EPI = 128;    // 4 epilogue warps = the 4 TMEM lane quarters
+constexpr int Z_THREADS = Z_EPI + 64;
+constexpr int Z_XBUF = 2 * 4 * 4 * 8 * 32 * 4;             // [tile][j][w][c8][r] ints, 32 KB
+constexpr size_t Z_SMEM = 1024 + (size_t)Z_STAGES * Z_STAGE + Z_XBUF + 512;
+constexpr uint32_t Z_SBO = 256;  // 8-row group stride: 2 k-chunks x 128 B
+
+// element (n, k) of a 32x32 slice: 8-row x 16-byte core matrices, the two
+// k-chunks of a row group adjacent (LBO 128 B), row groups 256 B apart -- four
+// consecutive slices form one 128-row operand.
+__host__ __device__ constexpr int z_off(int n, int k) {
+  return (n >> 3) * 256 + (k >> 4) * 128 + (n & 7) * 16 + (k & 15);
+}
+
+// ex[g] = max exponent over global row g (by_col = 0) / column g (by_col = 1):
+// thread t of a 256-thread CTA: block 4 s' + t / 64, line (t % 64) / 2, half t % 2.
+__global__ void __launch_bounds__(256) k_oz32_exponents(const double* __restrict__ data,
+                                                        const int64_t* __restrict__ keys,
+                                                        int64_t nblocks, int64_t G, int by_col,
+                                                        int* __restrict__ ex) {
+  pdl_wait();
+  const int t = threadIdx.x, sub = t >> 6, line = (t & 63) >> 1, half = t & 1;
+  for (int64_t s0 = (int64_t)blockIdx.x * 4; s0 < nblocks; s0 += (int64_t)gridDim.x * 4) {
+    const int64_t s = s0 + sub;
+    double mx = 0.0;
+    int64_t key = 0;
+    if (s < nblocks) {
+      const double* b = data + s * (Z_NB * Z_NB);
+      key = keys[s];
+      if (by_col) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) mx = fmax(mx, fabs(b[(half * 16 + i) * Z_NB + line]));
+      } else {
+        const double2* q = reinterpret_cast<const double2*>(b + line * Z_NB + half * 16);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const double2 v = q[i];
+          mx = fmax(mx, fmax(fabs(v.x), fabs(v.y)));
+        }
+      }
+    }
+    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+    if (s < nblocks && half == 0 && mx > 0.0)
+      atomicMax(ex + (by_col ? key % G : key / G) * Z_NB + line, oz_frexp(mx));
+  }
+}
+
+// out + s * 8 KB: the 8 digit slices of block s (trans: B role, slice row n =
+// block column n).  Thread t: block 4 s' + t / 64, slice row (t % 64) / 2,
+// k = 16 (t % 2) .. +15.
+__global__ void __launch_bounds__(256) k_oz32_split(const double* __restrict__ data,
+                                                    const int64_t* __restrict__ keys,
+                                                    int64_t nblocks, int64_t G, int trans,
+                                                    const int* __restrict__ ex,
+                                                    int8_t* __restrict__ out) {
+  pdl_wait();
+  const int t = threadIdx.x, sub = t >> 6, n = (t & 63) >> 1, kc = t & 1;
+  for (int64_t s0 = (int64_t)blockIdx.x * 4; s0 < nblocks; s0 += (int64_t)gridDim.x * 4) {
+    const int64_t s = s0 + sub;
+    if (s >= nblocks) continue;
+    const double* b = data + s * (Z_NB * Z_NB);
+    double y[16];
+    if (trans) {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) y[i] = b[(kc * 16 + i) * Z_NB + n];
+    } else {
+      const double2* q = reinterpret_cast<const double2*>(b + n * Z_NB + kc * 16);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const double2 v = q[i];
+        y[2 * i] = v.x;
+        y[2 * i + 1] = v.y;
+      }
+    }
+    const int64_t key = keys[s];
+    const int e = oz_exp(ex[(trans ? key % G : key / G) * Z_NB + n]);
+    uint32_t hi[16], lo[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const uint64_t d = oz_digits(y[i], e);
+      hi[i] = (uint32_t)(d >> 32);
+      lo[i] = (uint32_t)d;
+    }
+    int8_t* o = out + s * Z_BLOCK_BYTES + z_off(n, kc * 16);
+#pragma unroll
+    for (int p = 0; p < Z_SLICES; ++p) {
+      const uint32_t* h = p < 4 ? hi : lo;
+      const int byte = 3 - (p & 3);
+      *reinterpret_cast<uint4*>(o + p * Z_SLICE_BYTES) =
+          make_uint4(oz_gather4(h[0], h[1], h[2], h[3], byte),
+                     oz_gather4(h[4], h[5], h[6], h[7], byte),
+                     oz_gather4(h[8], h[9], h[10], h[11], byte),
+                     oz_gather4(h[12], h[13], h[14], h[15], byte));
+    }
+  }
+}
+
+template <class Idx>
+__global__ void __launch_bounds__(Z_THREADS, 1)
+    k_leaf_ozaki32(int64_t n_seg, const int64_t* __restrict__ seg, const Idx* __restrict__ a_idx,
+                   const Idx* __restrict__ b_idx, const int32_t* __restrict__ b_tr,
+                   const int64_t* __restrict__ a_keys, const int64_t* __restrict__ b_keys,
+                   int64_t G, const int8_t* __restrict__ As, const int8_t* __restrict__ Bs,
+                   const int* __restrict__ ex_a, const int* __restrict__ ex_b,
+                   const int64_t* __restrict__ c_out, const int64_t* __restrict__ c_mirror,
+                   int accumulate, double* __restrict__ C, const int32_t* __restrict__ order,
+                   int* __restrict__ next_block) {
+  pdl_wait();
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = smem_u32(smem_raw);
+  const uint32_t base = (raw + 1023u) & ~1023u;
+  uint8_t* gbase = smem_raw + (base - raw);
+  int* xb = reinterpret_cast<int*>(gbase + Z_STAGES * Z_STAGE);
+  const uint32_t bars = base + Z_STAGES * Z_STAGE + Z_XBUF;
+  auto full = [&](int s) { return bars + 8u * s; };
+  auto empty = [&](int s) { return bars + 8u * (Z_STAGES + s); };
+  auto tfull = [&](int b) { return bars + 8u * (2 * Z_STAGES + b); };
+  auto tempty = [&](int b) { return bars + 8u * (2 * Z_STAGES + 2 + b); };
+  int64_t* meta = reinterpret_cast<int64_t*>(gbase + Z_STAGES * Z_STAGE + Z_XBUF +
+                                             8 * (2 * Z_STAGES + 4));
+  int64_t* meta2 = meta + Z_STAGES;  // (bi << 32) | bj of the chunk starting in this stage
+  int64_t* ring = meta2 + Z_STAGES;  // per accumulator buffer: meta, meta2
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ring + 4);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < Z_STAGES; ++s) {
+      mbar_init(full(s), 1);
+      mbar_init(empty(s), 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(tfull(b), 2);  // MMA completion (commit) + the ring entry
+      mbar_init(tempty(b), Z_EPI / 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (warp == 5) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(
+                     smem_u32(tmem_slot))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+  }
+  tc_before();
+  __syncthreads();
+  tc_after();
+  const uint32_t tbase = *tmem_slot;
+
+  if (warp == 4) {
+    // ---------------- producer: two 8-KB bulk copies per task, Z_TPS per stage ----------------
+    int stage = 0, slot = 0, n_in = 0;
+    uint32_t phase = 0;
+    auto claim = [&](int64_t& m, int64_t& t0, int64_t& t1) -> bool {
+      int64_t i = 0;
+      if (lane == 0) i = atomicAdd(next_block, 1);
+      i = __shfl_sync(0xffffffffu, i, 0);
+      if (i >= n_seg) return false;
+      m = order ? (int64_t)order[i] : i;
+      t0 = seg[m];
+      t1 = seg[m + 1];
+      return true;
+    };
+    int64_t m = 0, t0 = 0, t1 = 0;
+    bool have = claim(m, t0, t1);
+    while (have) {
+      int64_t mn = 0, t0n = 0, t1n = 0;
+      const bool next = claim(mn, t0n, t1n);
+      for (int64_t c0 = t0; c0 < t1; c0 += 32) {
+        const int64_t t = c0 + lane;
+        int64_t ra_l = 0, rb_l = 0;
+        if (t < t1) {
+          ra_l = (int64_t)a_idx[t];
+          rb_l = (int64_t)b_idx[t];
+          if (b_tr) rb_l = b_tr[rb_l];
+        }
+        const int cnt = t1 - c0 < 32 ? (int)(t1 - c0) : 32;
+        for (int q = 0; q < cnt; ++q) {
+          const int64_t ra = __shfl_sync(0xffffffffu, ra_l, q);
+          const int64_t rb = __shfl_sync(0xffffffffu, rb_l, q);
+          const int64_t tq = c0 + q, r = tq - t0;
+          if (slot == 0) {  // open a stage: up to Z_TPS tasks of this chunk
+            const int64_t cend = t0 + (r / Z_CHUNK + 1) * Z_CHUNK;
+            const int64_t left = (cend < t1 ? cend : t1) - tq;
+            n_in = left < Z_TPS ? (int)left : Z_TPS;
+            mbar_wait(empty(stage), phase ^ 1u);
+            if (lane == 0) {
+              const bool first = r % Z_CHUNK == 0;
+              const bool last = tq + n_in == t1 || (r + n_in) % Z_CHUNK == 0;
+              const bool cont = r >= Z_CHUNK || accumulate;
+              meta[stage] = (m << 8) | ((int64_t)n_in << 3) | (first ? 1 : 0) | (last ? 2 : 0) |
+                            (cont ? 4 : 0);
+              if (first)
+                meta2[stage] = ((a_keys[a_idx[tq]] / G) << 32) | (b_keys[b_idx[tq]] % G);
+              mbar_expect_tx(full(stage), (uint32_t)(n_in * Z_TASK));
+            }
+          }
+          if (lane == 0) {
+            const uint32_t sa = base + stage * Z_STAGE + slot * Z_TASK;
+            bulk_g2s(sa, As + ra * Z_BLOCK_BYTES, Z_BLOCK_BYTES, full(stage));
+            bulk_g2s(sa + Z_BLOCK_BYTES, Bs + rb * Z_BLOCK_BYTES, Z_BLOCK_BYTES, full(stage));
+          }
+          __syncwarp();
+          if (++slot == n_in) {
+            slot = 0;
+            if (++stage == Z_STAGES) {
+              stage = 0;
+              phase ^= 1u;
+            }
+          }
+        }
+      }
+      have = next;
+      m = mn;
+      t0 = t0n;
+      t1 = t1n;
+    }
+    mbar_wait(empty(stage), phase ^ 1u);
+    if (lane == 0) {
+      meta[stage] = -1;
+      mbar_arrive(full(stage));
+    }
+  } else if (warp == 5) {
+    // ---------------- MMA issuer: one thread, 3 MMAs per task ----------------
+    if (lane == 0) {
+      int stage = 0, nchunk = 0;
+      uint32_t phase = 0, tph[2] = {0u, 0u};
+      int64_t cur2 = 0;
+      for (;;) {
+        mbar_wait(full(stage), phase);
+        tc_after();
+        const int64_t md = meta[stage];
+        const int b = nchunk & 1;
+        if (md < 0) {
+          mbar_wait(tempty(b), tph[b] ^ 1u);  // the epilogue is done with this buffer
+          ring[2 * b] = -1;
+          mbar_arrive(tfull(b));
+          oz_commit(tfull(b));
+          break;
+        }
+        const bool first = md & 1;
+        const int n_in = (int)((md >> 3) & 31);
+        if (first) {
+          cur2 = meta2[stage];
+          mbar_wait(tempty(b), tph[b] ^ 1u);  // accumulator buffer b drained
+          tph[b] ^= 1u;
+          tc_after();
+        }
+        const uint32_t d0 = tbase + 256u * b;
+        for (int q = 0; q < n_in; ++q) {
+          const uint32_t sa = base + stage * Z_STAGE + q * Z_TASK, sb = sa + Z_BLOCK_BYTES;
+          const uint32_t init = (first && q == 0) ? 0u : 1u;
+          oz_mma(d0, oz_desc(sa, Z_SBO), oz_desc(sb, Z_SBO), init);
+          oz_mma(d0 + 128u, oz_desc(sa, Z_SBO), oz_desc(sb + 4 * Z_SLICE_BYTES, Z_SBO), init);
+          oz_mma(d0 + 128u, oz_desc(sa + 4 * Z_SLICE_BYTES, Z_SBO), oz_desc(sb, Z_SBO), 1u);
+        }
+        oz_commit(empty(stage));
+        if (md & 2) {
+          ring[2 * b] = md;
+          ring[2 * b + 1] = cur2;
+          mbar_arrive(tfull(b));
+          oz_commit(tfull(b));
+          ++nchunk;
+        }
+        if (++stage == Z_STAGES) {
+          stage = 0;
+          phase ^= 1u;
+        }
+      }
+    }
+    __syncwarp();
+  } else {
+    // ---------------- epilogue: warp w = TMEM lane quarter w = A slice offset ----------------
+    const int w = warp, r = lane;
+    const uint32_t lane_base = tbase + ((uint32_t)(w * 32) << 16);
+    uint32_t eph[2] = {0u, 0u};
+    for (int nchunk = 0;; ++nchunk) {
+      const int b = nchunk & 1;
+      mbar_wait(tfull(b), eph[b]);
+      eph[b] ^= 1u;
+      tc_after();
+      const int64_t md = ring[2 * b];
+      if (md < 0) break;
+      const int64_t bij = ring[2 * b + 1];
+      const int64_t m = md >> 8;
+      const bool cont = md & 4;
+      const int64_t bi = bij >> 32, bj = bij & 0xffffffffLL;
+      const int er = oz_exp(ex_a[bi * Z_NB + r]) - 14;
+      double* Cb = C + (c_out ? c_out[m] : m) * (int64_t)(Z_NB * Z_NB);
+      const int64_t mi = c_mirror ? c_mirror[m] : -1;
+      double* Cm = mi >= 0 ? C + mi * (int64_t)(Z_NB * Z_NB) : nullptr;
+      const uint32_t tb = lane_base + 256u * b;
+#pragma unroll 1
+      for (int cc = 0; cc < 4; ++cc) {
+        int V[2][4][8];  // [tile][j][c8] of TMEM lane (w, r)
+#pragma unroll
+        for (int T = 0; T < 2; ++T)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) tmem_ld8(tb + 128u * T + 32u * j + 8u * cc, V[T][j]);
+        tmem_wait8(V[0][0]);
+#pragma unroll
+        for (int T = 0; T < 2; ++T)
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            if (T || j) tmem_keep8(V[T][j]);
+        if (cc == 3) {  // every TMEM read of this buffer is done: hand it back
+          tc_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(tempty(b));
+        }
+        // xbuf[T][j][w][c8][r]
+#pragma unroll
+        for (int T = 0; T < 2; ++T)
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int c8 = 0; c8 < 8; ++c8) xb[(((T * 4 + j) * 4 + w) * 8 + c8) * 32 + r] = V[T][j][c8];
+        asm volatile("bar.sync 1, 128;\n" ::: "memory");
+        // this thread: row r, columns 2w, 2w+1 of the chunk
+        double res[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int c8 = 2 * w + h;
+          int S[11];
+#pragma unroll
+          for (int d = 0; d < 11; ++d) S[d] = 0;
+#pragma unroll
+          for (int T = 0; T < 2; ++T)
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+#pragma unroll
+              for (int i = 0; i < 4; ++i)
+                S[4 * T + i + j] += xb[(((T * 4 + j) * 4 + i) * 8 + c8) * 32 + r];
+          double v = (double)S[10];
+#pragma unroll
+          for (int d = 9; d >= 0; --d) v = __fma_rn(v, 0x1p-8, (double)S[d]);
+          const int col = cc * 8 + c8;
+          const int k = er + oz_exp(ex_b[bj * Z_NB + col]);  // C = v 2^k
+          res[h] = (k >= -1022 && k <= 1023)
+                       ? __dmul_rn(v, __longlong_as_double((long long)(k + 1023) << 52))
+                       : ldexp(v, k);
+        }
+        const int col0 = cc * 8 + 2 * w;
+        double2* p = reinterpret_cast<double2*>(Cb + r * Z_NB + col0);
+        if (cont) {
+          const double2 o = *p;
+          res[0] = __dadd_rn(o.x, res[0]);
+          res[1] = __dadd_rn(o.y, res[1]);
+        }
+        *p = make_double2(res[0], res[1]);
+        if (Cm) {
+          Cm[col0 * Z_NB + r] = res[0];
+          Cm[(col0 + 1) * Z_NB + r] = res[1];
+        }
+        asm volatile("bar.sync 1, 128;\n" ::: "memory");
+      }
+    }
+  }
+  tc_before();
+  __syncthreads();
+  tc_after();
+  if (warp == 5)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tbase)
+                 : "memory");
+}
+
+}  // namespace
+
+void oz32_operand_passes(const Mat& M, bool trans, int* ex, int8_t* out, cudaStream_t s,
+                         bool exponents) {
+  const int grid = grid_for((M.nblocks + 3) / 4, 1, (int64_t)multiprocessors() * 8);
+  if (exponents) {
+    launch_plain(k_oz32_exponents, grid, 256, 0, s, (const double*)M.data, (const int64_t*)M.keys,
+                 M.nblocks, M.G, trans ? 1 : 0, ex);
+    SPAMM_LAUNCH_CK();
+  }
+  launch_pdl(k_oz32_split, grid, 256, 0, s, (const double*)M.data, (const int64_t*)M.keys,
+             M.nblocks, M.G, trans ? 1 : 0, (const int*)ex, out);
+  SPAMM_LAUNCH_CK();
+}
+
+template <class Idx>
+void oz32_launch(int64_t n_seg, const int64_t* seg, const Idx* a_idx, const Idx* b_idx,
+                 const int64_t* c_out, const int64_t* c_mirror, bool accumulate, const Mat& A,
+                 const Mat& B, const OzakiOperands& op, double* C, cudaStream_t s,
+                 int* counter) {
+  auto kern = k_leaf_ozaki32<Idx>;
+  static std::once_flag once;
+  std::call_once(once, [&] {
+    SPAMM_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Z_SMEM));
+  });
+  int64_t grid = multiprocessors();
+  if (grid > n_seg) grid = n_seg;
+  launch_plain(kern, (unsigned)grid, Z_THREADS, Z_SMEM, s, n_seg, seg, a_idx, b_idx,
+               (const int32_t*)op.b_tr, (const int64_t*)A.keys, (const int64_t*)B.keys, op.G,
+               (const int8_t*)op.as, (const int8_t*)op.bs, (const int*)op.ex_a,
+               (const int*)op.ex_b, c_out, c_mirror, accumulate ? 1 : 0, C,
+               (const int32_t*)nullptr, counter);
+  SPAMM_LAUNCH_CK();
+}
+
+template void oz32_launch<int32_t>(int64_t, const int64_t*, const int32_t*, const int32_t*,
+                                   const int64_t*, const int64_t*, bool, const Mat&, const Mat&,
+                                   const OzakiOperands&, double*, cudaStream_t, int*);
+template void oz32_launch<int64_t>(int64_t, const int64_t*, const int64_t*, const int64_t*,
+                                   const int64_t*, const int64_t*, bool, const Mat&, const Mat&,
+                                   const OzakiOperands&, double*, cudaStream_t, int*);
+
+}  // namespace spamm

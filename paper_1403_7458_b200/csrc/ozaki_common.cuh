@@ -1,0 +1,149 @@
+// Device helpers shared by the INT8-sliced leaf kernels (leaf_ozaki.cu for
+// Nb = 64, leaf_ozaki32.cu for Nb = 32): the digit split, mbarrier / bulk-copy
+// / tcgen05 PTX wrappers.  See leaf_ozaki.cu for the scheme.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace spamm {
+namespace ozk {
+
+constexpr int OZ_EXP_NONE = (int)0x80808080;  // memset pattern: "no nonzero seen"
+
+__device__ __forceinline__ int oz_exp(int e) { return e == OZ_EXP_NONE ? 0 : e; }
+// Row / column exponent E: max |x| < 2^E, bumped when the mantissa is within
+// 2^-7.5 of 1 so that |x 2^(7-E)| <= 127.25 -- the leading signed digit then
+// stays in [-128, 127] after the carry from the tail.
+__device__ __forceinline__ int oz_frexp(double mx) {
+  int e;
+  const double f = frexp(mx, &e);
+  return f >= 0.994140625 ? e + 1 : e;
+}
+
+
+// The 8 signed digits of x against the scale 2^E, packed as bytes (slice p =
+// byte 7 - p): V = floor(|x| 2^(63-E)) from the bit pattern (|x| 2^-E < 1, so
+// V < 2^63; the bytes of V are the floor digits), then the carry pass as one
+// add -- W = V + 0x80 (0x7F for x < 0) in each of the 7 low bytes -- whose
+// bytes XOR the same constant are the signed digits (negated for x < 0, the
+// carry threshold 129 there keeping them in [-128, 127]).
+__device__ __forceinline__ uint64_t oz_digits(double x, int e) {
+  const uint64_t bits = (uint64_t)__double_as_longlong(x);
+  const bool neg = bits >> 63;
+  int be = (int)((bits >> 52) & 0x7FF);
+  uint64_t m = bits & 0xFFFFFFFFFFFFFull;
+  if (be) m |= 1ull << 52;
+  else be = 1;  // subnormal (or zero: m = 0)
+  const int sh = be - 1012 - e;  // |x| 2^(63-E) = m 2^sh, sh <= 10
+  const uint64_t v = sh >= 0 ? m << sh : (sh > -64 ? m >> -sh : 0ull);
+  const uint64_t off = neg ? 0x007F7F7F7F7F7F7Full : 0x0080808080808080ull;
+  const uint64_t w = v + off;
+  const uint64_t top = neg ? (uint64_t)((-(int)(w >> 56)) & 0xFF) : (w >> 56);
+  return ((w ^ off) & 0x00FFFFFFFFFFFFFFull) | (top << 56);
+}
+
+// Bytes `byte` of four packed digit words -> one 32-bit word (element order).
+__device__ __forceinline__ uint32_t oz_gather4(uint32_t a, uint32_t b, uint32_t c, uint32_t d,
+                                               int byte) {
+  const uint32_t sel = (uint32_t)byte | ((uint32_t)(4 + byte) << 4);
+  return __byte_perm(__byte_perm(a, b, sel), __byte_perm(c, d, sel), 0x5410);
+}
+
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  uint32_t ok = 0;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity)
+        : "memory");
+  } while (!ok);
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes,
+                                         uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::
+          "r"(dst),
+      "l"(src), "r"(bytes), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s_pol(uint32_t dst, const void* src, uint32_t bytes,
+                                             uint32_t bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1], %2, [%3], %4;\n" ::"r"(dst),
+      "l"(src), "r"(bytes), "r"(bar), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t pol_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void tc_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+}
+__device__ __forceinline__ void tc_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+}
+// Shared-memory matrix descriptor: K-major, no swizzle, LBO 128 B (the two
+// 16-byte k-chunks of one MMA), SBO = stride of 8-row groups, version 1 (sm_100).
+__device__ __forceinline__ uint64_t oz_desc(uint32_t addr, uint32_t sbo = 512) {
+  return (uint64_t)((addr >> 4) & 0x3FFFu) | ((uint64_t)(128 >> 4) << 16) |
+         ((uint64_t)(sbo >> 4) << 32) | (1ull << 46);
+}
+// Instruction descriptor: D s32, A/B signed int8, both K-major, N = 128, M = 128.
+constexpr uint32_t OZ_IDESC =
+    (2u << 4) | (1u << 7) | (1u << 10) | ((128u >> 3) << 17) | ((128u >> 4) << 24);
+__device__ __forceinline__ void oz_mma(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t acc) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(OZ_IDESC), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void oz_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::
+                   "r"(bar)
+               : "memory");
+}
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, int (&v)[8]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];\n"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7])
+      : "r"(taddr));
+}
+// tcgen05.wait::ld, with the loaded registers threaded through so no use of
+// them can be scheduled above the wait.
+__device__ __forceinline__ void tmem_wait8(int (&v)[8]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n"
+               : "+r"(v[0]), "+r"(v[1]), "+r"(v[2]), "+r"(v[3]), "+r"(v[4]), "+r"(v[5]),
+                 "+r"(v[6]), "+r"(v[7])
+               :
+               : "memory");
+}
+__device__ __forceinline__ void tmem_keep8(int (&v)[8]) {
+  asm volatile(""
+               : "+r"(v[0]), "+r"(v[1]), "+r"(v[2]), "+r"(v[3]), "+r"(v[4]), "+r"(v[5]),
+                 "+r"(v[6]), "+r"(v[7]));
+}
+
+
+}  // namespace ozk
+}  // namespace spamm

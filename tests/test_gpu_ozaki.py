@@ -33,8 +33,9 @@ def err_vs(c, ex):
     return float(np.linalg.norm((c - ex).astype(np.float64)) / np.linalg.norm(ex.astype(np.float64)))
 
 
+@pytest.mark.parametrize("nb", [64, 32])
 @pytest.mark.parametrize("case", ["decay_ab", "decay_aa", "water", "wide", "wide_sym"])
-def test_products_vs_reference_and_extended_precision(case):
+def test_products_vs_reference_and_extended_precision(case, nb):
     rng = np.random.default_rng(7)
     if case.startswith("decay"):
         da, db = decay_pair(1024, 0.1, (0, 1))
@@ -46,8 +47,8 @@ def test_products_vs_reference_and_extended_precision(case):
     else:
         x = rng.uniform(-1, 1, (512, 512)) * np.exp(rng.uniform(-30, 5, (512, 512)))
         da = db = x + x.T if case == "wide_sym" else x
-    a = sp.build_from_dense(da, 64)
-    b = a if db is da else sp.build_from_dense(db, 64)
+    a = sp.build_from_dense(da, nb)
+    b = a if db is da else sp.build_from_dense(db, nb)
     for tau in (0.0, 1e-8):
         ce, se = sp.multiply(a, b, tau, kernel="exact")
         co, so = sp.multiply(a, b, tau, kernel="ozaki")
@@ -65,9 +66,10 @@ def test_products_vs_reference_and_extended_precision(case):
             assert co.symmetric
 
 
-def test_symmetric_path_bitwise_equals_full_path():
+@pytest.mark.parametrize("nb", [64, 32])
+def test_symmetric_path_bitwise_equals_full_path(nb):
     h, _ = water_cluster(30, seed=0)
-    x = sp.build_from_dense(h, 64)
+    x = sp.build_from_dense(h, nb)
     assert x.symmetric
     c_sym, st_sym = sp.multiply(x, x, 1e-6, kernel="ozaki")
     sp.set_symmetric_products(False)
@@ -87,15 +89,16 @@ def test_deterministic_repeats():
         assert np.array_equal(sp.to_dense(sp.multiply(a, b, 1e-10, kernel="ozaki")[0]), c0)
 
 
-def test_long_segments_flush_in_chunks():
+@pytest.mark.parametrize("nb", [64, 32])
+def test_long_segments_flush_in_chunks(nb):
     """G = 132 leaf blocks per side, tau = 0: every C block reduces 132 tasks,
     more than the 128-task int32 chunk, so each block is flushed to FP64 twice."""
-    n = 132 * 64
+    n = 132 * nb
     g = torch.Generator(device="cuda").manual_seed(5)
     d = torch.rand((n, n), dtype=torch.float64, device="cuda", generator=g) * 2 - 1
     i = torch.arange(n, device="cuda", dtype=torch.float64)
     d *= torch.exp(-0.002 * (i[:, None] - i[None, :]).abs())
-    a = sp.build_from_dense(d, 64)
+    a = sp.build_from_dense(d, nb)
     cd, sd = sp.multiply(a, a, 0.0, kernel="dmma")
     co, so = sp.multiply(a, a, 0.0, kernel="ozaki")
     assert so.counts_equal(sd) and so.leaf_products == 132 ** 3
@@ -120,13 +123,14 @@ def test_zero_rows_and_empty_products():
 
 
 def test_block_size_guard():
-    a = sp.build_from_dense(np.eye(64), 32)
-    with pytest.raises(ValueError, match="block size 64"):
+    a = sp.build_from_dense(np.eye(64), 16)
+    with pytest.raises(ValueError, match="block size 32 or 64"):
         sp.multiply(a, a, 0.0, kernel="ozaki")
 
 
-def test_sp2_cfg4_same_decisions_as_dmma():
-    cfg = CONFIGS[4]
+@pytest.mark.parametrize("cfg_index", [4, 3])
+def test_sp2_same_decisions_as_dmma(cfg_index):
+    cfg = CONFIGS[cfg_index]
     h, n_occ = water_cluster(cfg.n_mol, seed=0)
     f = sp.build_from_dense(torch.from_numpy(h).cuda(), cfg.block_size)
     kw = dict(criterion="fro", fro_tol=1e-6)
