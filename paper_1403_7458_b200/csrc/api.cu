@@ -502,9 +502,12 @@ struct OzakiAhead {
   cudaEvent_t ready = nullptr;
   bool ok = false;
   cudaStream_t s = nullptr;
-  ~OzakiAhead() {  // error paths: nothing launched K4z, give the scratch back
+  ~OzakiAhead() {  // early-exit / error paths: give the scratch back after the pre-passes
     if (!ok) return;
-    if (ready) cudaEventDestroy(ready);
+    if (ready) {
+      cudaStreamWaitEvent(s, ready, 0);  // the frees below are ordered on s
+      cudaEventDestroy(ready);
+    }
     try {
       spamm::ozaki_release(op, s);
     } catch (...) {
@@ -689,6 +692,8 @@ void multiply_shard_impl(const spamm_mat* a, double tau, int32_t kernel, cudaStr
                          spamm::Mat& C, spamm_stats* stats, int rank, int world,
                          int64_t* cut_pos) {
   if (a->m.depth > 8) throw std::invalid_argument("sharded SP2 products need depth <= 8");
+  OzakiAhead oz;  // K4z operand pre-passes alongside the cull (as in multiply_impl)
+  ozaki_ahead(a, a, kernel, s, oz);
   spamm::CullResult r;
   r.world = world;
   bool sym = g_sym_enabled && a->m.sym;
@@ -729,7 +734,17 @@ void multiply_shard_impl(const spamm_mat* a, double tau, int32_t kernel, cudaStr
     c_out = ident;
   }
   const int64_t n_lo = r.node_cut[rank], n_hi = r.node_cut[rank + 1];
-  if (n_hi > n_lo) {
+  if (oz.ok) {
+    SPAMM_CK(cudaStreamWaitEvent(s, oz.ready, 0));
+    SPAMM_CK(cudaEventDestroy(oz.ready));
+    oz.ready = nullptr;
+    if (n_hi > n_lo)
+      spamm::ozaki_launch<int32_t>(n_hi - n_lo, r.seg + n_lo, r.a_idx, r.b_idx, c_out + n_lo,
+                                   r.c_mirror ? r.c_mirror + n_lo : nullptr, false, a->m, a->m,
+                                   oz.op, C.data, s);
+    spamm::ozaki_release(oz.op, s);
+    oz.ok = false;
+  } else if (n_hi > n_lo) {
     leaf_dispatch(n_hi - n_lo, r.seg + n_lo, r.a_idx, r.b_idx, c_out + n_lo,
                   r.c_mirror ? r.c_mirror + n_lo : nullptr, a, a, C.data, kernel, s, {});
   }
