@@ -71,14 +71,18 @@ def i8_peak():
         return 4500.0, "nominal B200 dense INT8 (fallback)"
 
 
-# K4z executes 20 tcgen05 MMAs of 128x128x32 int8 per leaf product (10 digit
-# pairs x 2 k-steps, leaf_ozaki.cu): int8 ops per executed leaf product.
-K4Z_OPS_PER_PRODUCT = 20 * 2 * 128 * 128 * 32
+# int8 ops K4z executes per leaf product: 20 tcgen05 MMAs of 128x128x32 at
+# Nb = 64 (10 digit-pair stacks x 2 k-steps, leaf_ozaki.cu), 3 at Nb = 32
+# (leaf_ozaki32.cu).
+def k4z_ops_per_product(block_size: int) -> int:
+    return (20 if block_size == 64 else 3) * 2 * 128 * 128 * 32
 
 
 def leaf_kernel_in_use(block_size: int) -> str:
-    """What kernel="auto" resolves to (api.cu leaf_dispatch)."""
-    if block_size == 64 and os.environ.get("SPAMM_AUTO_LEAF") != "dmma":
+    """What kernel="auto" resolves to (api.cu auto_ozaki_for)."""
+    if os.environ.get("SPAMM_AUTO_LEAF") == "dmma":
+        return "dmma"
+    if block_size == 64 or (block_size == 32 and os.environ.get("SPAMM_AUTO_OZ32") != "0"):
         return "ozaki"
     return "dmma"
 
@@ -306,17 +310,19 @@ def run_ours(args):
             tasks = exec_flops / (2 * cfg.block_size ** 3)
             ipeak, ipeak_src = i8_peak()
             if leaf_ms > 0:
-                iach = tasks * K4Z_OPS_PER_PRODUCT / (leaf_ms * 1e-3) / 1e12
-                inote = ("executed leaf products x 20 int8 MMAs of 128x128x32 per launch "
-                         "/ K4z event time")
+                iach = tasks * k4z_ops_per_product(cfg.block_size) / (leaf_ms * 1e-3) / 1e12
+                inote = (f"executed leaf products x "
+                         f"{20 if cfg.block_size == 64 else 3} int8 MMAs of 128x128x32 per "
+                         "launch / K4z event time")
             else:
-                iach = tasks * K4Z_OPS_PER_PRODUCT / (tmax * 1e-3) / 1e12
+                iach = tasks * k4z_ops_per_product(cfg.block_size) / (tmax * 1e-3) / 1e12
                 inote = "int8 MMA ops of this rank / whole step time (lower bound)"
             roofline = {"bound": "tensor", "achieved": iach, "peak": ipeak, "unit": "TOPS",
                         "frac": iach / ipeak,
                         "traffic": ncu_traffic("ozaki") if args.config == 4 else None,
-                        "kernel": "k_leaf_ozaki<int> (K4z: FP64 leaf products as exact "
-                                  "signed-8-bit digit products on the INT8 tensor cores)",
+                        "kernel": (f"k_leaf_ozaki{'' if cfg.block_size == 64 else '32'}<int> "
+                                   "(K4z: FP64 leaf products as exact signed-8-bit digit "
+                                   "products on the INT8 tensor cores)"),
                         "peak_source": ipeak_src, "algorithmic": inote,
                         "fp64_equivalent": {
                             "achieved": achieved, "unit": "TFLOP/s", "dmma_peak": peak,
