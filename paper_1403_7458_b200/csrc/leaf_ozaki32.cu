@@ -8,8 +8,9 @@
 // (4,0) -- form every pair with p + q <= 7 exactly once (and some with
 // p + q <= 10), into two 128-column tiles whose 32x32 sub-blocks (i, j) hold
 // digit sum D + i + j (D = 0 for the first, 4 for the other two).  Two tiles
-// are 256 TMEM columns, so the accumulators are double-buffered: the epilogue
-// of one C block overlaps the MMAs of the next.
+// are 256 TMEM columns, so two CTAs fit on an SM (the default shape: the
+// epilogue of one CTA overlaps the MMAs of the other), or one CTA can
+// double-buffer its accumulators.
 //
 // Epilogue: the 16 sub-blocks of a C element (r, c) live in four TMEM lane
 // quarters (one per warp) and four column groups; each warp loads its quarter,
@@ -40,15 +41,20 @@ constexpr int Z_BLOCK_BYTES = Z_SLICES * Z_SLICE_BYTES;    // 8 KB
 // of each): one barrier round trip per Z_TPS tasks -- with only 3 MMAs per
 // task (~200 tensor cycles) the per-task synchronisation would otherwise
 // dominate.
-constexpr int Z_TPS = 4;
 constexpr int Z_TASK = 2 * Z_BLOCK_BYTES;                  // 16 KB
-constexpr int Z_STAGES = 3;
-constexpr int Z_STAGE = Z_TPS * Z_TASK;                    // 64 KB
+// Kernel shapes: NBUF accumulator sets of 256 TMEM columns (2: double
+// buffered, one CTA per SM; 1: two CTAs per SM share the 512 columns),
+// STAGES x TPS tasks of operand ring.
+template <int NBUF, int TPS, int STAGES>
+struct ZCfg {
+  static constexpr int STAGE = TPS * Z_TASK;
+  static constexpr size_t SMEM = 1024 + (size_t)STAGES * STAGE + 32768 + 512;
+  static constexpr int CTAS = NBUF == 2 ? 1 : 2;
+};
 constexpr int Z_CHUNK = 128;  // tasks per accumulation: |sub-block| <= 128 x 32 x 2^14 = 2^26
 constexpr int Z_EPI = 128;    // 4 epilogue warps = the 4 TMEM lane quarters
 constexpr int Z_THREADS = Z_EPI + 64;
 constexpr int Z_XBUF = 2 * 4 * 4 * 8 * 32 * 4;             // [tile][j][w][c8][r] ints, 32 KB
-constexpr size_t Z_SMEM = 1024 + (size_t)Z_STAGES * Z_STAGE + Z_XBUF + 512;
 constexpr uint32_t Z_SBO = 256;  // 8-row group stride: 2 k-chunks x 128 B
 
 // element (n, k) of a 32x32 slice: 8-row x 16-byte core matrices, the two
@@ -141,8 +147,8 @@ __global__ void __launch_bounds__(256) k_oz32_split(const double* __restrict__ d
   }
 }
 
-template <class Idx>
-__global__ void __launch_bounds__(Z_THREADS, 1)
+template <class Idx, int NBUF, int Z_TPS, int Z_STAGES>
+__global__ void __launch_bounds__(Z_THREADS, NBUF == 2 ? 1 : 2)
     k_leaf_ozaki32(int64_t n_seg, const int64_t* __restrict__ seg, const Idx* __restrict__ a_idx,
                    const Idx* __restrict__ b_idx, const int32_t* __restrict__ b_tr,
                    const int64_t* __restrict__ a_keys, const int64_t* __restrict__ b_keys,
@@ -152,6 +158,8 @@ __global__ void __launch_bounds__(Z_THREADS, 1)
                    int accumulate, double* __restrict__ C, const int32_t* __restrict__ order,
                    int* __restrict__ next_block) {
   pdl_wait();
+  constexpr int Z_STAGE = ZCfg<NBUF, Z_TPS, Z_STAGES>::STAGE;
+  constexpr uint32_t TCOLS = 256u * NBUF;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;
@@ -181,8 +189,8 @@ __global__ void __launch_bounds__(Z_THREADS, 1)
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   if (warp == 5) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(
-                     smem_u32(tmem_slot))
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+                     smem_u32(tmem_slot)), "r"(TCOLS)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
   }
@@ -274,7 +282,7 @@ __global__ void __launch_bounds__(Z_THREADS, 1)
         mbar_wait(full(stage), phase);
         tc_after();
         const int64_t md = meta[stage];
-        const int b = nchunk & 1;
+        const int b = NBUF == 2 ? (nchunk & 1) : 0;
         if (md < 0) {
           mbar_wait(tempty(b), tph[b] ^ 1u);  // the epilogue is done with this buffer
           ring[2 * b] = -1;
@@ -319,7 +327,7 @@ __global__ void __launch_bounds__(Z_THREADS, 1)
     const uint32_t lane_base = tbase + ((uint32_t)(w * 32) << 16);
     uint32_t eph[2] = {0u, 0u};
     for (int nchunk = 0;; ++nchunk) {
-      const int b = nchunk & 1;
+      const int b = NBUF == 2 ? (nchunk & 1) : 0;
       mbar_wait(tfull(b), eph[b]);
       eph[b] ^= 1u;
       tc_after();
@@ -404,7 +412,8 @@ __global__ void __launch_bounds__(Z_THREADS, 1)
   __syncthreads();
   tc_after();
   if (warp == 5)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tbase)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tbase),
+                 "r"(TCOLS)
                  : "memory");
 }
 
@@ -423,24 +432,47 @@ void oz32_operand_passes(const Mat& M, bool trans, int* ex, int8_t* out, cudaStr
   SPAMM_LAUNCH_CK();
 }
 
-template <class Idx>
-void oz32_launch(int64_t n_seg, const int64_t* seg, const Idx* a_idx, const Idx* b_idx,
-                 const int64_t* c_out, const int64_t* c_mirror, bool accumulate, const Mat& A,
-                 const Mat& B, const OzakiOperands& op, double* C, cudaStream_t s,
-                 int* counter) {
-  auto kern = k_leaf_ozaki32<Idx>;
+template <class Idx, int NBUF, int TPS, int STAGES>
+void oz32_launch_cfg(int64_t n_seg, const int64_t* seg, const Idx* a_idx, const Idx* b_idx,
+                     const int64_t* c_out, const int64_t* c_mirror, bool accumulate, const Mat& A,
+                     const Mat& B, const OzakiOperands& op, double* C, cudaStream_t s,
+                     int* counter) {
+  using Cfg = ZCfg<NBUF, TPS, STAGES>;
+  auto kern = k_leaf_ozaki32<Idx, NBUF, TPS, STAGES>;
   static std::once_flag once;
   std::call_once(once, [&] {
-    SPAMM_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Z_SMEM));
+    SPAMM_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)Cfg::SMEM));
   });
-  int64_t grid = multiprocessors();
+  int64_t grid = (int64_t)multiprocessors() * Cfg::CTAS;
   if (grid > n_seg) grid = n_seg;
-  launch_plain(kern, (unsigned)grid, Z_THREADS, Z_SMEM, s, n_seg, seg, a_idx, b_idx,
+  launch_plain(kern, (unsigned)grid, Z_THREADS, Cfg::SMEM, s, n_seg, seg, a_idx, b_idx,
                (const int32_t*)op.b_tr, (const int64_t*)A.keys, (const int64_t*)B.keys, op.G,
                (const int8_t*)op.as, (const int8_t*)op.bs, (const int*)op.ex_a,
                (const int*)op.ex_b, c_out, c_mirror, accumulate ? 1 : 0, C,
                (const int32_t*)nullptr, counter);
   SPAMM_LAUNCH_CK();
+}
+
+template <class Idx>
+void oz32_launch(int64_t n_seg, const int64_t* seg, const Idx* a_idx, const Idx* b_idx,
+                 const int64_t* c_out, const int64_t* c_mirror, bool accumulate, const Mat& A,
+                 const Mat& B, const OzakiOperands& op, double* C, cudaStream_t s,
+                 int* counter) {
+  // Two CTAs per SM (256 TMEM columns each, 2 stages of 2 tasks): the kernel
+  // is latency-bound, and a second CTA hides it better than double-buffered
+  // accumulators in one (cfg3 K4z 8.0 vs 10.9 ms per solve; 1 task x 4 stages:
+  // 9.7 ms).  SPAMM_OZ32_SHAPE=1: one CTA per SM, double-buffered TMEM.
+  static const int shape = [] {
+    const char* v = getenv("SPAMM_OZ32_SHAPE");
+    return v ? atoi(v) : 2;
+  }();
+  if (shape == 1)
+    oz32_launch_cfg<Idx, 2, 4, 3>(n_seg, seg, a_idx, b_idx, c_out, c_mirror, accumulate, A, B,
+                                  op, C, s, counter);
+  else
+    oz32_launch_cfg<Idx, 1, 2, 2>(n_seg, seg, a_idx, b_idx, c_out, c_mirror, accumulate, A, B,
+                                  op, C, s, counter);
 }
 
 template void oz32_launch<int32_t>(int64_t, const int64_t*, const int32_t*, const int32_t*,
