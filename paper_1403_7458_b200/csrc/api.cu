@@ -504,10 +504,7 @@ struct OzakiAhead {
   cudaStream_t s = nullptr;
   ~OzakiAhead() {  // early-exit / error paths: give the scratch back after the pre-passes
     if (!ok) return;
-    if (ready) {
-      cudaStreamWaitEvent(s, ready, 0);  // the frees below are ordered on s
-      cudaEventDestroy(ready);
-    }
+    if (ready) cudaStreamWaitEvent(s, ready, 0);  // the frees below are ordered on s
     try {
       spamm::ozaki_release(op, s);
     } catch (...) {
@@ -550,22 +547,20 @@ void ozaki_ahead(const spamm_mat* a, const spamm_mat* b, int32_t kernel, cudaStr
   if (!use_side) {
     oz.ok = spamm::ozaki_prepare(a->m, b->m, a == b && a->m.sym, s, oz.op,
                                  /*try_only=*/kernel == spamm::LEAF_AUTO);
-    if (oz.ok) {
-      SPAMM_CK(cudaEventCreateWithFlags(&oz.ready, cudaEventDisableTiming));
-      SPAMM_CK(cudaEventRecord(oz.ready, s));
-    }
-    return;
+    return;  // (same stream: no event needed)
   }
   cudaStream_t side = ozaki_side_stream();
-  cudaEvent_t operands;
-  SPAMM_CK(cudaEventCreateWithFlags(&operands, cudaEventDisableTiming));
-  SPAMM_CK(cudaEventRecord(operands, s));
-  SPAMM_CK(cudaStreamWaitEvent(side, operands, 0));
-  SPAMM_CK(cudaEventDestroy(operands));
+  // two reusable events per host thread: each is waited on right after it is
+  // recorded, and a thread has one multiply in flight
+  thread_local cudaEvent_t ev[2] = {nullptr, nullptr};
+  for (auto& e : ev)
+    if (!e) SPAMM_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  SPAMM_CK(cudaEventRecord(ev[0], s));
+  SPAMM_CK(cudaStreamWaitEvent(side, ev[0], 0));
   oz.ok = spamm::ozaki_prepare(a->m, b->m, a == b && a->m.sym, side, oz.op,
                                /*try_only=*/kernel == spamm::LEAF_AUTO);
   if (oz.ok) {
-    SPAMM_CK(cudaEventCreateWithFlags(&oz.ready, cudaEventDisableTiming));
+    oz.ready = ev[1];
     SPAMM_CK(cudaEventRecord(oz.ready, side));
   }
 }
@@ -631,8 +626,7 @@ void multiply_impl(const spamm_mat* a, const spamm_mat* b, double tau, int32_t k
   if (g_side) g_side->window(s);  // PCIe chunk alongside K4
   tm.mark(1);  // leaf window = the K4 launch only (allocation stays outside)
   if (oz.ok) {  // K4z on the operands prepared alongside the cull
-    SPAMM_CK(cudaStreamWaitEvent(s, oz.ready, 0));
-    SPAMM_CK(cudaEventDestroy(oz.ready));
+    if (oz.ready) SPAMM_CK(cudaStreamWaitEvent(s, oz.ready, 0));
     oz.ready = nullptr;
     if (r.n_c > 0) {
       spamm::LptSchedule lpt;
@@ -735,8 +729,7 @@ void multiply_shard_impl(const spamm_mat* a, double tau, int32_t kernel, cudaStr
   }
   const int64_t n_lo = r.node_cut[rank], n_hi = r.node_cut[rank + 1];
   if (oz.ok) {
-    SPAMM_CK(cudaStreamWaitEvent(s, oz.ready, 0));
-    SPAMM_CK(cudaEventDestroy(oz.ready));
+    if (oz.ready) SPAMM_CK(cudaStreamWaitEvent(s, oz.ready, 0));
     oz.ready = nullptr;
     if (n_hi > n_lo)
       spamm::ozaki_launch<int32_t>(n_hi - n_lo, r.seg + n_lo, r.a_idx, r.b_idx, c_out + n_lo,

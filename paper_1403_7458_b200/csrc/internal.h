@@ -218,6 +218,9 @@ struct OzakiOperands {
   int64_t G = 0;
   int nb = 64;
   bool sym_b = false;
+  bool as_cached = false;            // `as` is the per-thread kept buffer
+  bool tail_cached = false;          // ex_a / b_tr live in it too
+  void (*release_cache)() = nullptr;  // marks it free again
 };
 // Nb = 32 variant (leaf_ozaki32.cu): operand passes (row / column exponents
 // when `exponents`, digit slices) and the K4z launch.

@@ -539,7 +539,50 @@ bool ozaki_prepare(const Mat& A, const Mat& B, bool sym_b, cudaStream_t s, Ozaki
   const size_t b_bytes = sym_b ? 0 : (size_t)B.nblocks * blk_bytes;
   static const bool force_fail = getenv("SPAMM_OZ_FORCE_NOMEM") != nullptr;  // test hook
   if (try_only && force_fail) return false;
-  if (try_only) {
+  // The A slices of the SP2 loop's X*X (one size, every iteration): a
+  // per-thread buffer kept across multiplies instead of a pool round trip per
+  // product (operands up to 1 GB; reuse is ordered by the caller's stream, on
+  // which the previous K4z ran before this pre-pass starts).
+  struct SliceCache {
+    int8_t* p = nullptr;
+    size_t bytes = 0;
+    bool busy = false;
+  };
+  thread_local SliceCache cache;
+  // (sym: the row exponents and the transposed-slot map ride in the same buffer)
+  const size_t extra = sym_b ? (size_t)G * nb * 4 + (size_t)(A.nblocks > 0 ? A.nblocks : 1) * 4 : 0;
+  const size_t want = a_bytes + extra;
+  if (a_bytes && want <= (size_t(1) << 30) && !cache.busy) {
+    if (cache.bytes < want) {
+      if (cache.p) cudaFree(cache.p);
+      cache.p = nullptr;
+      cache.bytes = 0;
+      if (cudaMalloc(reinterpret_cast<void**>(&cache.p), want) == cudaSuccess) {
+        cache.bytes = want;
+      } else {
+        cudaGetLastError();
+        cache.p = nullptr;
+      }
+    }
+    if (cache.p) {
+      op.as = cache.p;
+      op.as_cached = true;
+      cache.busy = true;
+    }
+  }
+  op.release_cache = [](void) { cache.busy = false; };
+  if (op.as_cached) {
+    if (!try_only) op.bs = static_cast<int8_t*>(dmalloc_bytes(b_bytes, s));
+    else if (b_bytes &&
+             cudaMallocAsync(reinterpret_cast<void**>(&op.bs), b_bytes, s) != cudaSuccess) {
+      cudaGetLastError();
+      op.bs = nullptr;
+      cache.busy = false;
+      op.as = nullptr;
+      op.as_cached = false;
+      return false;
+    }
+  } else if (try_only) {
     if (a_bytes && cudaMallocAsync(reinterpret_cast<void**>(&op.as), a_bytes, s) != cudaSuccess) {
       cudaGetLastError();
       op.as = nullptr;
@@ -555,14 +598,20 @@ bool ozaki_prepare(const Mat& A, const Mat& B, bool sym_b, cudaStream_t s, Ozaki
     op.as = static_cast<int8_t*>(dmalloc_bytes(a_bytes, s));
     op.bs = static_cast<int8_t*>(dmalloc_bytes(b_bytes, s));
   }
-  op.ex_a = dmalloc<int>(G * nb, s);
+  if (op.as_cached && sym_b) {
+    op.ex_a = reinterpret_cast<int*>(op.as + a_bytes);
+    op.b_tr = op.ex_a + G * nb;
+    op.tail_cached = true;
+  } else {
+    op.ex_a = dmalloc<int>(G * nb, s);
+  }
   SPAMM_CK(cudaMemsetAsync(op.ex_a, 0x80, G * nb * sizeof(int), s));
   if (nb == 32) {
     oz32_operand_passes(A, false, op.ex_a, op.as, s, true);
     if (sym_b) {
       op.ex_b = op.ex_a;
       op.bs = op.as;
-      op.b_tr = dmalloc<int32_t>(A.nblocks > 0 ? A.nblocks : 1, s);
+      if (!op.tail_cached) op.b_tr = dmalloc<int32_t>(A.nblocks > 0 ? A.nblocks : 1, s);
       launch_pdl(k_oz_trslot, grid_for(A.nblocks, 256), 256, 0, s, (const int64_t*)A.keys,
                  A.nblocks, G, (const int32_t*)A.slot, op.b_tr);
       SPAMM_LAUNCH_CK();
@@ -584,7 +633,7 @@ bool ozaki_prepare(const Mat& A, const Mat& B, bool sym_b, cudaStream_t s, Ozaki
   if (sym_b) {
     op.ex_b = op.ex_a;
     op.bs = op.as;
-    op.b_tr = dmalloc<int32_t>(A.nblocks > 0 ? A.nblocks : 1, s);
+    if (!op.tail_cached) op.b_tr = dmalloc<int32_t>(A.nblocks > 0 ? A.nblocks : 1, s);
     launch_pdl(k_oz_trslot, grid_for(A.nblocks, 256), 256, 0, s, (const int64_t*)A.keys,
                A.nblocks, G, (const int32_t*)A.slot, op.b_tr);
     SPAMM_LAUNCH_CK();
@@ -603,13 +652,17 @@ bool ozaki_prepare(const Mat& A, const Mat& B, bool sym_b, cudaStream_t s, Ozaki
 }
 
 void ozaki_release(OzakiOperands& op, cudaStream_t s) {
-  dfree(op.b_tr, s);
+  if (!op.tail_cached) dfree(op.b_tr, s);
   if (!op.sym_b) {
     dfree(op.ex_b, s);
     dfree(op.bs, s);
   }
-  dfree(op.ex_a, s);
-  dfree(op.as, s);
+  if (!op.tail_cached) dfree(op.ex_a, s);
+  if (op.as_cached) {
+    if (op.release_cache) op.release_cache();
+  } else {
+    dfree(op.as, s);
+  }
   op = OzakiOperands();
 }
 
