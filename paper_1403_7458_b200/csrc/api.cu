@@ -198,7 +198,11 @@ struct SideQueue {
     }
   }
   void window(cudaStream_t comp) {
-    issue(comp, cfg && cfg->chunk_bytes > 0 ? cfg->chunk_bytes : (int64_t)24 << 20);
+    static const int64_t dflt = [] {  // SPAMM_SIDE_CHUNK_MB: default chunk of the riding copies
+      const char* v = getenv("SPAMM_SIDE_CHUNK_MB");
+      return (int64_t)(v && atoi(v) > 0 ? atoi(v) : 24) << 20;
+    }();
+    issue(comp, cfg && cfg->chunk_bytes > 0 ? cfg->chunk_bytes : dflt);
   }
   void drain(cudaStream_t comp) { issue(comp, INT64_MAX); }
   ~SideQueue() {
