@@ -356,6 +356,9 @@ def run_ours(args):
                            "leaf_flops_executed_per_step of them and mirrors the rest "
                            "(bitwise identical C)"),
             "leaf_kernel": k4,
+            "leaf_arithmetic": ("signed int8 digit products on tcgen05 (kind::i8), exact int32 "
+                                "accumulation, FP64 assembly; inputs/outputs FP64"
+                                if k4 == "ozaki" else "FP64 tensor cores (DMMA)"),
             "roofline": roofline,
             "e2e": {"value": e2e_flops_all / (e2e_max * 1e-3) / 1e9, "unit": UNIT,
                     "h2d_bytes_per_step": int(h.nbytes), "d2h_bytes_per_step": int(h.nbytes),
