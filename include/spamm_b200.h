@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define SPAMM_ABI_VERSION 1
+#define SPAMM_ABI_VERSION 2
 #define SPAMM_OK 0
 #define SPAMM_EINVAL 1
 #define SPAMM_ECUDA 2
@@ -38,8 +38,11 @@ extern "C" {
 #define SPAMM_LEAF_EXACT 2 /* CUDA-core, reference order: bitwise identical  */
 #define SPAMM_LEAF_DMMA_CPASYNC 3 /* first-generation DMMA kernel (A/B tests)  */
 /* FP64 products on the INT8 tensor cores (tcgen05 kind::i8, TMEM) by exact
- * digit slicing (Ozaki scheme I, 8 slices of 7 bits, per-row/column power-of-2
- * scales); Nb = 32 or 64; FP64-level error, deterministic, not bitwise DMMA.
+ * digit slicing (Ozaki scheme I: 8 signed 8-bit digit slices, one power-of-2
+ * scale per global row of A / column of B, digit pairs p + q <= 7 formed
+ * exactly in int32); Nb = 32 or 64; relative error below FP64's (~5e-17 vs
+ * ~5e-16 rel-Fro), deterministic, exactly symmetric, not bitwise DMMA.
+ * Operands with non-finite entries are refused (AUTO falls back to DMMA).
  * Accepted by the matrix entry points (spamm_multiply*, spamm_sp2_*), not by
  * spamm_gemm_batch (it needs the operands' row / column exponents). */
 #define SPAMM_LEAF_OZAKI 4
@@ -77,6 +80,15 @@ typedef struct {
   float ms_finalize;
   int64_t executed_products; /* leaf products actually run (half when symmetric) */
   int32_t symmetric;         /* 1: symmetric SpAMM path (C_ji = C_ij^T mirrored) */
+  /* Near-tau report (the "documented ties" clause of the parity contract;
+   * the cull's strict test is kernel.py:108).  Per tier: tested products
+   * p = fl(nA nB) (children of survivors, both mirror triples on the
+   * symmetric path) with |p - tau| <= near_tau_ulps ulp(tau).  tau_margin:
+   * min |p - tau| / tau over tested products within tau 2^-20 (+inf if none;
+   * +inf for tau = 0, where nothing is probed). */
+  int64_t near_tau[SPAMM_MAX_TIERS];
+  double tau_margin;
+  int32_t near_tau_ulps;
 } spamm_stats;
 
 int spamm_abi_version(void);
@@ -146,6 +158,9 @@ int spamm_set_symmetric_products(int32_t enabled);
  * of the tier-by-tier walk; task sets, order and counters are identical.
  * 0 forces the tier walk (A/B testing). */
 int spamm_set_dense_cull(int32_t enabled);
+/* Width of the near-tau band in ulps of tau (default 64: the norm error of
+ * a DMMA / K4z operand against the reference's; 1 for the exact kernel). */
+int spamm_set_near_tau_ulps(int32_t ulps);
 /* Sharded SP2 iteration (multi-GPU, X replicated; parallel.ShardedSP2):
  * spamm_sp2_multiply_shard runs the full dense cull of X*X on every rank (so
  * every rank holds the same C layout) and the leaf products of this rank's
@@ -237,6 +252,11 @@ typedef struct {
   int64_t* leaf_products;     /* [max_iter + 1] per multiply (reference count) */
   int64_t* executed_products; /* [max_iter + 1] per multiply (symmetric path) */
   float* ms_leaf;             /* [max_iter + 1] K4 ms per multiply if timed, or NULL */
+  /* optional (NULL: not recorded), [max_iter + 1] per multiply: */
+  double* branch_margin;      /* |t_ex - n_occ| - |t_sq - n_occ| (sp2.py:97-99; >= 0: SQUARE) */
+  int64_t* near_tau;          /* near-tau products over all tiers (spamm_stats) */
+  double* tau_margin;         /* spamm_stats.tau_margin */
+  double* wall_seconds;       /* host wall time of each iteration (steady clock) */
 } spamm_sp2_report;
 int spamm_sp2_solve(const spamm_mat* f, double n_occ, double tau, int32_t max_iter,
                     double idem_tol, int32_t criterion, double fro_tol, double sym_tol,

@@ -37,6 +37,7 @@ runs on machines without /root/reference.
 from __future__ import annotations
 
 import ctypes
+import math
 import os
 import time
 from dataclasses import dataclass, field
@@ -337,6 +338,42 @@ def sweep(tn_a: list, tn_b: list, tau: float):
     return visited, culled, i, k, j
 
 
+def tie_log(tn_a: list, tn_b: list, tau: float, ulps: int = 64):
+    """Near-tau diagnostic over the products ``_sweep`` tests (kernel.py:96-122:
+    the root, then the 8 children of every survivor per tier; the strict
+    ``>`` is kernel.py:108).  Returns (near, margin): per tier the number of
+    tested products p with |p - tau| <= ulps * ulp(tau), and the smallest
+    |p - tau| / tau over tested products with |p - tau| <= tau * 2**-20
+    (inf if none, and for tau == 0 where nothing is probed).  Not a reference
+    function: it documents how close the reference's decisions came to a tie
+    (the parity contract's "norm ties within one ulp of tau")."""
+    depth = len(tn_a) - 1
+    near = [0] * (depth + 1)
+    margin = math.inf
+    if not (tau > 0.0 and math.isfinite(tau)):
+        return near, margin
+    band = ulps * (np.nextafter(tau, np.inf) - tau)
+    wide = math.ldexp(tau, -20)
+    i = np.zeros(1, dtype=np.int64)
+    k = np.zeros(1, dtype=np.int64)
+    j = np.zeros(1, dtype=np.int64)
+    for t in range(depth + 1):
+        p = tn_a[t][i, k] * tn_b[t][k, j]
+        d = np.abs(p - tau)
+        near[t] = int(np.count_nonzero(d <= band))
+        w = d[d <= wide]
+        if len(w):
+            margin = min(margin, float((w / tau).min()))
+        keep = p > tau
+        i, k, j = i[keep], k[keep], j[keep]
+        if t == depth or len(i) == 0:
+            break
+        i = ((2 * i)[:, None] + _CHILD[:, 0]).ravel()
+        k = ((2 * k)[:, None] + _CHILD[:, 1]).ravel()
+        j = ((2 * j)[:, None] + _CHILD[:, 2]).ravel()
+    return near, margin
+
+
 def task_order(ti, tk, tj, g, block_size, chunk_size):
     """kernel.py:189-196: sort key C-chunk-major, in-chunk row-major, then k."""
     cs = max(1, chunk_size // block_size)
@@ -479,6 +516,19 @@ class OSP2Result:
     leaf_products: list = field(default_factory=list)
     idem_history: list = field(default_factory=list)
     wall_seconds_per_iteration: list = field(default_factory=list)
+    # |t_ex - n_occ| - |t_sq - n_occ| per multiply (sp2.py:97-99; >= 0: SQUARE)
+    branch_margins: list = field(default_factory=list)
+    # record_tasks=True: per multiply, sha256 of the sorted task keys
+    # ((i G + k) G + j, int64 little-endian) and tie_log's (near total, margin)
+    task_sha256: list = field(default_factory=list)
+    tie_logs: list = field(default_factory=list)
+
+
+def task_sha256(ti, tk, tj, g) -> str:
+    """sha256 of a leaf task set as sorted int64 keys (i G + k) G + j."""
+    import hashlib
+    keys = np.sort((np.asarray(ti, np.int64) * g + tk) * g + tj).astype("<i8")
+    return hashlib.sha256(keys.tobytes()).hexdigest()
 
 
 def sp2_step(x: OMatrix, n_occ, tau, threads=1):
@@ -493,7 +543,7 @@ def sp2_step(x: OMatrix, n_occ, tau, threads=1):
 
 
 def sp2_solve(f: OMatrix, n_occ, tau, max_iter=100, idem_tol=1e-9, threads=1,
-              criterion="trace", fro_tol=1e-6) -> OSP2Result:
+              criterion="trace", fro_tol=1e-6, record_tasks=False) -> OSP2Result:
     """sp2.py:115-143.  ``criterion="fro"`` is BASELINE cfg3's ||X^2-X||_F < tol,
     evaluated from reference primitives (add_scaled(1, X^2, -1, X).norm()) on
     the same X^2 the step computed, before the step is accepted."""
@@ -502,8 +552,14 @@ def sp2_solve(f: OMatrix, n_occ, tau, max_iter=100, idem_tol=1e-9, threads=1,
     res.trace_history.append(trace(x))
     for _ in range(max_iter):
         t0 = time.perf_counter()
+        if record_tasks:
+            _, _, ti, tk, tj = sweep(x.tier_norms, x.tier_norms, tau)
+            res.task_sha256.append(task_sha256(ti, tk, tj, x.n_blocks))
+            near, margin = tie_log(x.tier_norms, x.tier_norms, tau)
+            res.tie_logs.append((int(sum(near)), margin))
         x_next, branch, t_x, t_sq, stats, x_sq = sp2_step(x, n_occ, tau, threads)
         res.leaf_products.append(stats["leaf_products"])
+        res.branch_margins.append(abs((2.0 * t_x - t_sq) - n_occ) - abs(t_sq - n_occ))
         if criterion == "trace":
             done = abs(t_sq - t_x) < idem_tol and abs(t_x - n_occ) < 1e-6 * n_occ
         else:

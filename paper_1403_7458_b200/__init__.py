@@ -10,7 +10,8 @@ All compute runs in ``libspamm_b200.so`` (sm_100a CUDA, C ABI in
 from .quadtree import (QuadTreeMatrix, Node, build_from_dense, to_dense, to_dense_device,
                        verify_norms, add_scaled, trace, identity)
 from .kernel import (ProductStats, multiply, convolution_census, leaf_gemm, gemm_batch,
-                     leaf_tasks, set_symmetric_products, set_dense_cull, WORKERS_ENV_VAR)
+                     leaf_tasks, set_symmetric_products, set_dense_cull, set_near_tau_ulps,
+                     WORKERS_ENV_VAR)
 from .sp2 import (SpectralBounds, SP2State, gershgorin_bounds, sp2_init, sp2_step, sp2_solve,
                   energy_error, idempotency_error, SQUARE, EXPAND)
 from ._native import LIB_PATH, load as load_library
@@ -23,6 +24,7 @@ __all__ = [
     "ProductStats", "multiply", "convolution_census", "leaf_gemm", "gemm_batch", "leaf_tasks",
     "set_symmetric_products",
     "set_dense_cull",
+    "set_near_tau_ulps",
     "WORKERS_ENV_VAR",
     "SpectralBounds", "SP2State", "gershgorin_bounds", "sp2_init", "sp2_step", "sp2_solve",
     "energy_error", "idempotency_error", "SQUARE", "EXPAND",

@@ -17,6 +17,7 @@ SPAMM_OK = 0
 SPAMM_EINVAL = 1
 SPAMM_ECUDA = 2
 MAX_TIERS = 64
+ABI_VERSION = 2
 
 LEAF_KERNELS = {"auto": 0, "dmma": 1, "exact": 2, "dmma_cpasync": 3, "ozaki": 4}
 
@@ -42,6 +43,7 @@ class Stats(ctypes.Structure):
         ("leaf_products", c_i64), ("flop_estimate", c_i64), ("c_blocks", c_i64),
         ("ms_cull", ctypes.c_float), ("ms_leaf", ctypes.c_float), ("ms_finalize", ctypes.c_float),
         ("executed_products", c_i64), ("symmetric", c_i32),
+        ("near_tau", c_i64 * MAX_TIERS), ("tau_margin", c_f64), ("near_tau_ulps", c_i32),
     ]
 
 
@@ -51,6 +53,8 @@ class SP2Report(ctypes.Structure):
         ("eps_min", c_f64), ("eps_max", c_f64),
         ("trace_history", c_vp), ("branch_history", c_vp), ("idem_history", c_vp),
         ("leaf_products", c_vp), ("executed_products", c_vp), ("ms_leaf", c_vp),
+        ("branch_margin", c_vp), ("near_tau", c_vp), ("tau_margin", c_vp),
+        ("wall_seconds", c_vp),
     ]
 
 
@@ -86,6 +90,7 @@ _SIGS = {
     "spamm_census": (c_i32, [c_vp, c_vp, c_f64, c_vp, ctypes.POINTER(Stats)]),
     "spamm_set_symmetric_products": (c_i32, [c_i32]),
     "spamm_set_dense_cull": (c_i32, [c_i32]),
+    "spamm_set_near_tau_ulps": (c_i32, [c_i32]),
     "spamm_multiply_range": (c_i32, [c_vp, c_vp, c_f64, c_i32, c_i64, c_i64, c_vp, c_vp,
                                      ctypes.POINTER(c_vp), ctypes.POINTER(Stats)]),
     "spamm_reserve_pool": (c_i32, [c_i64, c_vp]),
@@ -138,7 +143,7 @@ def load():
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args
-        if lib.spamm_abi_version() != 1:
+        if lib.spamm_abi_version() != ABI_VERSION:
             raise OSError("libspamm_b200.so ABI version mismatch")
         _lib = lib
     return _lib

@@ -1,6 +1,7 @@
 // C ABI (include/spamm_b200.h): argument checks, handle management and the
 // multiply driver (cull -> leaf products -> C finalisation).
 #include <algorithm>
+#include <chrono>
 #include <climits>
 #include <cmath>
 #include <cstdlib>
@@ -151,6 +152,8 @@ __global__ void k_flag_keys(const uint8_t* flags, const int64_t* off, int depth,
   }
 }
 
+int g_near_ulps_api = 64;  // mirrors spamm::set_near_tau_ulps for the stats
+
 void fill_stats(spamm_stats* st, double tau, const spamm::CullResult& r, int nb) {
   if (!st) return;
   std::memset(st, 0, sizeof(*st));
@@ -160,6 +163,9 @@ void fill_stats(spamm_stats* st, double tau, const spamm::CullResult& r, int nb)
     st->visited[t] = r.visited[t];
     st->culled[t] = r.culled[t];
   }
+  for (size_t t = 0; t < r.near.size() && t < SPAMM_MAX_TIERS; ++t) st->near_tau[t] = r.near[t];
+  st->tau_margin = r.near.empty() ? INFINITY : r.margin;
+  st->near_tau_ulps = g_near_ulps_api;
   st->leaf_products = r.visited.empty() ? 0 : r.visited.back();
   st->executed_products = r.sym ? r.n_tasks : st->leaf_products;
   st->symmetric = r.sym ? 1 : 0;
@@ -523,13 +529,13 @@ size_t device_total_bytes() {
   }();
   return total;
 }
-cudaStream_t ozaki_side_stream() {
-  thread_local cudaStream_t side = [] {
-    cudaStream_t t = nullptr;
-    SPAMM_CK(cudaStreamCreateWithFlags(&t, cudaStreamNonBlocking));
-    return t;
-  }();
-  return side;
+cudaStream_t ozaki_side_stream() {  // one per (host thread, device)
+  thread_local cudaStream_t side[64] = {};
+  int dev = 0;
+  SPAMM_CK(cudaGetDevice(&dev));
+  cudaStream_t& t = side[dev & 63];
+  if (!t) SPAMM_CK(cudaStreamCreateWithFlags(&t, cudaStreamNonBlocking));
+  return t;
 }
 void ozaki_ahead(const spamm_mat* a, const spamm_mat* b, int32_t kernel, cudaStream_t s,
                  OzakiAhead& oz) {
@@ -554,11 +560,14 @@ void ozaki_ahead(const spamm_mat* a, const spamm_mat* b, int32_t kernel, cudaStr
     return;  // (same stream: no event needed)
   }
   cudaStream_t side = ozaki_side_stream();
-  // two reusable events per host thread: each is waited on right after it is
-  // recorded, and a thread has one multiply in flight
-  thread_local cudaEvent_t ev[2] = {nullptr, nullptr};
-  for (auto& e : ev)
-    if (!e) SPAMM_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  // two reusable events per (host thread, device): each is waited on right
+  // after it is recorded, and a thread has one multiply in flight
+  thread_local cudaEvent_t evs[64][2] = {};
+  int dev = 0;
+  SPAMM_CK(cudaGetDevice(&dev));
+  cudaEvent_t* ev = evs[dev & 63];
+  for (int i = 0; i < 2; ++i)
+    if (!ev[i]) SPAMM_CK(cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming));
   SPAMM_CK(cudaEventRecord(ev[0], s));
   SPAMM_CK(cudaStreamWaitEvent(side, ev[0], 0));
   oz.ok = spamm::ozaki_prepare(a->m, b->m, a == b && a->m.sym, side, oz.op,
@@ -762,7 +771,7 @@ void multiply_shard_impl(const spamm_mat* a, double tau, int32_t kernel, cudaStr
 void sp2_finish(const spamm_mat* x, const spamm_mat* c, double n_occ, bool want_idem,
                 cudaStream_t s, bool* square_out, double* t_x, double* t_sq, double* idem,
                 spamm_mat** e_out, const double* idem_dev = nullptr,
-                spamm::IdemFuse* fused_union = nullptr) {
+                spamm::IdemFuse* fused_union = nullptr, double* branch_margin = nullptr) {
   const bool fused = spamm::sp2_fused_supported(x->m.nb);
   // One host sync (one gather launch) for tr(X), tr(X^2), the union size of
   // the update and X^2's kept-block count.  Traces computed by the small-tree
@@ -806,6 +815,7 @@ void sp2_finish(const spamm_mat* x, const spamm_mat* c, double n_occ, bool want_
   // sp2.py:97-99: ties go to SQUARE.
   const double tex = 2.0 * tx - tsq;
   const bool square = std::fabs(tsq - n_occ) <= std::fabs(tex - n_occ);
+  if (branch_margin) *branch_margin = std::fabs(tex - n_occ) - std::fabs(tsq - n_occ);
   spamm_mat* e = square ? nullptr : new spamm_mat();
   spamm::Mat dummy;
   spamm::htrace("fin_branch");
@@ -989,6 +999,7 @@ int spamm_multiply_range(const spamm_mat* a, const spamm_mat* b, double tau, int
 int spamm_reserve_pool(int64_t bytes, void* stream) {
   if (bytes < 0) return fail(SPAMM_EINVAL, "negative size");
   SPAMM_API_BEGIN
+  spamm::ozaki_cache_trim();  // the kept K4z slice buffer goes back before the pool grows
   spamm::reserve_pool((size_t)bytes, S(stream));
   SPAMM_API_END
 }
@@ -1000,6 +1011,13 @@ int spamm_set_symmetric_products(int32_t enabled) {
 
 int spamm_set_dense_cull(int32_t enabled) {
   spamm::set_dense_cull(enabled != 0);
+  return SPAMM_OK;
+}
+
+int spamm_set_near_tau_ulps(int32_t ulps) {
+  if (ulps < 0) return fail(SPAMM_EINVAL, "near-tau band must be >= 0 ulps");
+  spamm::set_near_tau_ulps(ulps);
+  g_near_ulps_api = ulps;
   return SPAMM_OK;
 }
 
@@ -1263,6 +1281,7 @@ int spamm_sp2_solve_ex(const spamm_mat* f, double n_occ, double tau, int32_t max
     }
     ~Graveyard() { flush(); }
   } dead;
+  auto t_iter = std::chrono::steady_clock::now();
   for (int it = 0; it < max_iter; ++it) {
     auto* c = new spamm_mat();
     spamm_stats st;
@@ -1281,12 +1300,26 @@ int spamm_sp2_solve_ex(const spamm_mat* f, double n_occ, double tau, int32_t max
     bool square = true;
     double tx = 0, tsq = 0, idem = 0;
     spamm_mat* e = nullptr;
-    sp2_finish(x, c, n_occ, want_idem, s, &square, &tx, &tsq, &idem, &e, fuse.out, &fuse);
+    double bmargin = 0.0;
+    sp2_finish(x, c, n_occ, want_idem, s, &square, &tx, &tsq, &idem, &e, fuse.out, &fuse,
+               &bmargin);
     spamm::dfree(fuse.ukeys, s);  // (null once the update took it)
     const int k = rep->n_multiplies++;
     rep->leaf_products[k] = st.leaf_products;
     rep->executed_products[k] = st.executed_products;
     if (rep->ms_leaf) rep->ms_leaf[k] = st.ms_leaf;
+    if (rep->branch_margin) rep->branch_margin[k] = bmargin;
+    if (rep->near_tau) {
+      int64_t nt = 0;
+      for (int t = 0; t < st.n_tiers; ++t) nt += st.near_tau[t];
+      rep->near_tau[k] = nt;
+    }
+    if (rep->tau_margin) rep->tau_margin[k] = st.tau_margin;
+    if (rep->wall_seconds) {  // (the loop syncs on the host every iteration)
+      const auto now = std::chrono::steady_clock::now();
+      rep->wall_seconds[k] = std::chrono::duration<double>(now - t_iter).count();
+      t_iter = now;
+    }
     if (pending_trace) {  // tr of the last accepted X = this step's t_x
       rep->trace_history[n_tr++] = tx;
       pending_trace = false;

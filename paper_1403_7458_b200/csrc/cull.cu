@@ -19,6 +19,7 @@
 // reference's expansion, so visited/culled per tier are identical.  The
 // surviving C nodes come out in Morton (Z) order of (i, j).
 #include <algorithm>
+#include <cmath>
 #include <cstring>
 
 #include "internal.h"
@@ -35,11 +36,52 @@ __device__ __forceinline__ bool keep_pair(double na, double nb, double tau) {
   return __dmul_rn(na, nb) > tau;
 }
 
+// Near-tau probe (the north star's "documented norm ties within one ulp of
+// tau"): a tested product p = fl(nA nB) with |p - tau| <= band (k ulp(tau),
+// spamm_set_near_tau_ulps) is counted per tier, and the smallest relative
+// distance |p - tau| / tau among tested products within `wide` (tau 2^-20) is
+// kept as the bit pattern of a non-negative double in inverted form (atomicMax
+// of ~bits: zero-initialised memory reads as "none").  Products this close
+// are the only ones whose decision can differ from the reference's when the
+// operand norms differ from the reference operand's by a few ulps.  Both
+// bands are < 0 (off) for tau = 0.
+struct TieBand {
+  double tau = 0.0, band = -1.0, wide = -1.0;
+};
+int g_near_ulps = 64;
+TieBand tie_band(double tau) {
+  TieBand tb;
+  tb.tau = tau;
+  if (tau > 0.0 && std::isfinite(tau)) {
+    tb.band = g_near_ulps * (std::nextafter(tau, INFINITY) - tau);
+    tb.wide = std::ldexp(tau, -20);
+  }
+  return tb;
+}
+double margin_from_bits(int64_t inv) {  // see tie_probe; +inf: nothing within tau 2^-20
+  if (inv == 0) return INFINITY;
+  const uint64_t bits = ~(uint64_t)inv;
+  double d;
+  std::memcpy(&d, &bits, sizeof d);
+  return d;
+}
+
+__device__ __forceinline__ void tie_probe(double p, const TieBand& tb,
+                                          unsigned long long* __restrict__ near,
+                                          unsigned long long* __restrict__ margin) {
+  const double d = fabs(p - tb.tau);
+  if (!(d <= tb.wide)) return;
+  if (d <= tb.band) atomicAdd(near, 1ull);
+  atomicMax(margin, ~(unsigned long long)__double_as_longlong(d / tb.tau));
+}
+
 __global__ void k_cull_root(const double* __restrict__ nA, const double* __restrict__ nB,
                             double tau, int32_t* ci, int32_t* cj, int64_t* seg, int32_t* K,
                             int64_t* count, const int32_t* slotA, const int32_t* slotB,
-                            int32_t* aidx, int32_t* bidx) {
+                            int32_t* aidx, int32_t* bidx, TieBand tb,
+                            unsigned long long* near, unsigned long long* margin) {
   const bool keep = keep_pair(nA[0], nB[0], tau);
+  tie_probe(__dmul_rn(nA[0], nB[0]), tb, near, margin);
   ci[0] = 0;
   cj[0] = 0;
   seg[0] = 0;
@@ -64,7 +106,7 @@ __global__ void __launch_bounds__(CULL_THREADS)
                   const int32_t* __restrict__ slotA, const int32_t* __restrict__ slotB,
                   int32_t* __restrict__ aidx, int32_t* __restrict__ bidx, int64_t Mn, int64_t Vn,
                   int sym, unsigned long long* __restrict__ aux, int64_t lo, int64_t hi,
-                  int shift, int32_t* __restrict__ work) {
+                  int shift, int32_t* __restrict__ work, TieBand tb) {
   const int64_t W = int64_t(1) << t1;
   const double* A = nA + tier_offset(t1);
   const double* B = nB + tier_offset(t1);
@@ -117,10 +159,12 @@ __global__ void __launch_bounds__(CULL_THREADS)
         const int64_t kk = valid ? 2 * (int64_t)K[q] + (lane & 1) : 0;
         const bool keep = valid && keep_pair(Arow[kk], B[kk * W + col], tau);
         const unsigned mask = __ballot_sync(0xffffffffu, keep);
+        if (!WRITE && valid) tie_probe(__dmul_rn(Arow[kk], B[kk * W + col]), tb, aux + 4, aux + 5);
         if (!WRITE && sym && row != col) {
           // mirror triple (col, kk, row) must agree, else the survivor set is
           // not symmetric (an ulp tie between norm(X_ik) and norm(X_ki^T)).
           const bool keep_m = valid && keep_pair(A[col * W + kk], B[kk * W + row], tau);
+          if (valid) tie_probe(__dmul_rn(A[col * W + kk], B[kk * W + row]), tb, aux + 4, aux + 5);
           if (__any_sync(0xffffffffu, keep != keep_m) && lane == 0) atomicOr(aux + 1, 1ull);
         }
         if (WRITE) {
@@ -165,10 +209,18 @@ struct HostLevel {
   std::vector<int64_t> seg;
 };
 
+void host_tie_probe(double p, const TieBand& tb, int64_t& near, double& margin) {
+  const double d = std::fabs(p - tb.tau);
+  if (!(d <= tb.wide)) return;
+  if (d <= tb.band) ++near;
+  margin = std::min(margin, d / tb.tau);
+}
+
 bool host_cull_top(const double* nA, const double* nB, int T0, int depth, double tau, bool sym,
                    int64_t lo, int64_t hi, CullResult& r, HostLevel& L, int64_t& full_prev,
-                   int64_t& diag_nodes) {
+                   int64_t& diag_nodes, const TieBand& tb) {
   const bool keep0 = nA[0] * nB[0] > tau;
+  host_tie_probe(nA[0] * nB[0], tb, r.near[0], r.margin);
   r.visited[0] = keep0 ? 1 : 0;
   r.culled[0] = keep0 ? 0 : 1;
   L.ci.assign(1, 0);
@@ -209,8 +261,11 @@ bool host_cull_top(const double* nA, const double* nB, int T0, int depth, double
           for (int dk = 0; dk < 2; ++dk) {
             const int64_t kk = 2 * (int64_t)L.K[q] + dk;
             const bool keep = A[row * W + kk] * B[kk * W + col] > tau;
-            if (sym && row != col && keep != (A[col * W + kk] * B[kk * W + row] > tau))
-              return false;
+            host_tie_probe(A[row * W + kk] * B[kk * W + col], tb, r.near[t1], r.margin);
+            if (sym && row != col) {
+              host_tie_probe(A[col * W + kk] * B[kk * W + row], tb, r.near[t1], r.margin);
+              if (keep != (A[col * W + kk] * B[kk * W + row] > tau)) return false;
+            }
             if (keep) N.K.push_back((int32_t)kk);
           }
         const int64_t cnt = (int64_t)(N.K.size() - start);
@@ -267,9 +322,35 @@ __device__ __forceinline__ bool keep_chain(const double* __restrict__ nA,
 // Survivor counts of every tier t < depth (full enumeration, 8^t triples).
 // Counts are warp-reduced per tier before touching shared memory (a shared
 // 64-bit atomic per survivor serialised this kernel to ~15 us at cfg4).
+// every tier u < t of the triple's ancestor chain passes (the triple is tested)
+__device__ __forceinline__ bool ancestors_pass(const double* __restrict__ nA,
+                                               const double* __restrict__ nB, double tau, int t,
+                                               int64_t i, int64_t k, int64_t j) {
+  for (int u = t - 1; u >= 0; --u) {
+    const int sh = t - u;
+    const int64_t W = int64_t(1) << u;
+    const int64_t off = tier_offset(u);
+    if (!keep_pair(nA[off + (i >> sh) * W + (k >> sh)], nB[off + (k >> sh) * W + (j >> sh)], tau))
+      return false;
+  }
+  return true;
+}
+// tie probe of the tier-t triple (i, k, j) if it is tested (see tie_probe)
+__device__ __forceinline__ void chain_tie_probe(const double* __restrict__ nA,
+                                                const double* __restrict__ nB, const TieBand& tb,
+                                                int t, int64_t i, int64_t k, int64_t j,
+                                                unsigned long long* near,
+                                                unsigned long long* margin) {
+  const int64_t W = int64_t(1) << t, off = tier_offset(t);
+  const double p = __dmul_rn(nA[off + i * W + k], nB[off + k * W + j]);
+  if (!(fabs(p - tb.tau) <= tb.wide)) return;
+  if (ancestors_pass(nA, nB, tb.tau, t, i, k, j)) tie_probe(p, tb, near, margin);
+}
+
 __global__ void __launch_bounds__(256)
     k_dense_tiers(const double* __restrict__ nA, const double* __restrict__ nB, double tau,
-                  int depth, unsigned long long* __restrict__ counts) {
+                  int depth, unsigned long long* __restrict__ counts, TieBand tb,
+                  unsigned long long* __restrict__ near, unsigned long long* __restrict__ margin) {
   pdl_wait();
   __shared__ unsigned int sc[DENSE_MAX_DEPTH];
   if (threadIdx.x < DENSE_MAX_DEPTH) sc[threadIdx.x] = 0;
@@ -287,6 +368,7 @@ __global__ void __launch_bounds__(256)
       const int64_t r = q - ((int64_t(1) << (3 * t)) - 1) / 7;
       const int64_t i = r >> (2 * t), k = (r >> t) & ((int64_t(1) << t) - 1),
                     j = r & ((int64_t(1) << t) - 1);
+      chain_tie_probe(nA, nB, tb, t, i, k, j, near + t, margin);
       if (!keep_chain(nA, nB, tau, t, i, k, j)) t = -1;
     }
     for (int u = 0; u < depth; ++u) {
@@ -320,7 +402,8 @@ __global__ void __launch_bounds__(CULL_THREADS)
                  int32_t* __restrict__ aidx, int32_t* __restrict__ bidx,
                  int64_t* __restrict__ keys, int64_t* __restrict__ c_out,
                  int64_t* __restrict__ c_mirror, int32_t* __restrict__ order, int64_t Mn,
-                 int64_t Vn, unsigned long long* __restrict__ aux) {
+                 int64_t Vn, unsigned long long* __restrict__ aux, TieBand tb,
+                 unsigned long long* __restrict__ near, unsigned long long* __restrict__ margin) {
   pdl_wait();
   const int64_t G = int64_t(1) << depth;
   const int lane = threadIdx.x & 31;
@@ -362,6 +445,10 @@ __global__ void __launch_bounds__(CULL_THREADS)
       const bool valid = k < G;
       const bool keep = valid && keep_chain(nA, nB, tau, depth, i, k, j);
       const unsigned mask = __ballot_sync(0xffffffffu, keep);
+      if (!WRITE && valid && emitted) {
+        chain_tie_probe(nA, nB, tb, depth, i, k, j, near, margin);
+        if (sym && i < j) chain_tie_probe(nA, nB, tb, depth, j, k, i, near, margin);
+      }
       if (!WRITE && sym && i < j) {
         const bool keep_m = valid && keep_chain(nA, nB, tau, depth, j, k, i);
         if (__any_sync(0xffffffffu, keep != keep_m) && lane == 0) atomicOr(aux + 1, 1ull);
@@ -427,46 +514,59 @@ bool dense_cull(const Mat& a, const Mat& b, double tau, bool want_tasks, CullRes
   const int depth = a.depth;
   const int64_t G = int64_t(1) << depth, npos = G * G;
   // aux[0]: full leaf survivors, [1]: mirror mismatch, [2]: packed scan
-  // total, [4 + t]: tier-t survivors (t < depth)
+  // total, [4 + t]: tier-t survivors (t < depth), [NEAR + t]: near-tau
+  // products of tier t (t <= depth), [MARGIN]: inverted min relative margin,
+  // [CUTS ..]: shard cuts.
   // [aux | LPT schedule: G + 1 length bins (bin 0 = G tasks) + the K4 counter]
   // zeroed by one memset; the schedule part is handed to K4 (r.sched).
   htrace("dc_start");
   const int world = r.world > 1 ? r.world : 1;
-  const size_t aux_bytes = (4 + DENSE_MAX_DEPTH + 2 * (world + 1)) * sizeof(int64_t);
+  constexpr int NEAR = 4 + DENSE_MAX_DEPTH, MARGIN = NEAR + DENSE_MAX_DEPTH + 1,
+                CUTS = MARGIN + 1;
+  const size_t aux_bytes = (CUTS + 2 * (world + 1)) * sizeof(int64_t);
+  const TieBand tb = tie_band(tau);
   char* zbuf = dmalloc<char>(aux_bytes + (G + 2) * sizeof(int), s);
   int64_t* aux = reinterpret_cast<int64_t*>(zbuf);
   int* sched = reinterpret_cast<int*>(zbuf + aux_bytes);
   int64_t* cnt = dmalloc<int64_t>(2 * npos + 1, s);
   int64_t* off = cnt + npos;
   SPAMM_CK(cudaMemsetAsync(zbuf, 0, aux_bytes + (G + 2) * sizeof(int), s));
+  auto* u64 = reinterpret_cast<unsigned long long*>(aux);
   if (depth > 0) {
     const int64_t tri = ((int64_t(1) << (3 * depth)) - 1) / 7;
     launch_pdl(k_dense_tiers, grid_for(tri, 256, 148LL * 8), 256, 0, s,
-        a.norms, b.norms, tau, depth, reinterpret_cast<unsigned long long*>(aux + 4));
+        a.norms, b.norms, tau, depth, u64 + 4, tb, u64 + NEAR, u64 + MARGIN);
     SPAMM_LAUNCH_CK();
   }
   launch_pdl(k_dense_leaf<false>, grid_for(npos * 32, CULL_THREADS, 148LL * 64), CULL_THREADS, 0, s,
       depth, a.norms, b.norms, tau, sym ? 1 : 0, cnt, nullptr, sched, nullptr, nullptr, nullptr,
-      nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, 0, 0,
-      reinterpret_cast<unsigned long long*>(aux));
+      nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, 0, 0, u64,
+      tb, u64 + NEAR + depth, u64 + MARGIN);
   SPAMM_LAUNCH_CK();
   scan_exclusive_i64(cnt, npos, off, s);
   if (want_tasks) hist_scan_exclusive(sched, (int)G + 1, s);
-  int64_t* cuts = aux + 4 + DENSE_MAX_DEPTH;
+  int64_t* cuts = aux + CUTS;
   if (world > 1) {
     k_shard_cuts<<<1, 32, 0, s>>>(off, npos, world, cuts);
     SPAMM_LAUNCH_CK();
   }
-  const int nsc = 4 + depth + (world > 1 ? 2 * (world + 1) : 0);
-  const int64_t* src[48];
-  for (int i = 0; i < 4 + depth; ++i) src[i] = aux + i;
+  // gathered: aux[0..4+depth), near[0..depth], margin, cuts
+  const int n_base = 4 + depth, n_near = depth + 1;
+  const int nsc = n_base + n_near + 1 + (world > 1 ? 2 * (world + 1) : 0);
+  const int64_t* src[64];
+  for (int i = 0; i < n_base; ++i) src[i] = aux + i;
   src[2] = off + npos;
-  for (int i = 0; world > 1 && i < 2 * (world + 1); ++i) src[4 + depth + i] = cuts + i;
-  int64_t h[48];
+  for (int t = 0; t < n_near; ++t) src[n_base + t] = aux + NEAR + t;
+  src[n_base + n_near] = aux + MARGIN;
+  const int n_cut0 = n_base + n_near + 1;
+  for (int i = 0; world > 1 && i < 2 * (world + 1); ++i) src[n_cut0 + i] = cuts + i;
+  int64_t h[64];
   gather_sync(h, src, nsc, s);
+  for (int t = 0; t < n_near; ++t) r.near[t] = h[n_base + t];
+  r.margin = margin_from_bits(h[n_base + n_near]);
   if (world > 1) {
-    r.cut_pos.assign(h + 4 + depth, h + 4 + depth + world + 1);
-    r.node_cut.assign(h + 5 + depth + world, h + 5 + depth + 2 * world + 1);
+    r.cut_pos.assign(h + n_cut0, h + n_cut0 + world + 1);
+    r.node_cut.assign(h + n_cut0 + world + 1, h + n_cut0 + 2 * world + 2);
   }
   if (h[1]) {  // leaf survivor set not mirror-symmetric (ulp tie): full cull
     dfree(cnt, s);
@@ -509,7 +609,8 @@ bool dense_cull(const Mat& a, const Mat& b, double tau, bool want_tasks, CullRes
   r.counter = sched + G + 1;
   launch_pdl(k_dense_leaf<true>, grid_for(npos * 32, CULL_THREADS, 148LL * 64), CULL_THREADS, 0, s,
       depth, a.norms, b.norms, tau, sym ? 1 : 0, nullptr, off, sched, r.ci, r.cj, r.seg, r.k,
-      a.slot, b.slot, r.a_idx, r.b_idx, r.keys, r.c_out, r.c_mirror, r.order, M, V, nullptr);
+      a.slot, b.slot, r.a_idx, r.b_idx, r.keys, r.c_out, r.c_mirror, r.order, M, V, nullptr, tb,
+      nullptr, nullptr);
   SPAMM_LAUNCH_CK();
   dfree(cnt, s);
   r.n_c = M;
@@ -532,6 +633,7 @@ void* pinned_staging(size_t bytes) {
 }  // namespace
 
 void set_dense_cull(bool enabled) { g_dense_enabled = enabled; }
+void set_near_tau_ulps(int k) { g_near_ulps = k; }
 
 void CullResult::release(cudaStream_t s) {
   if (block) {  // dense cull: every array but keys lives in one allocation
@@ -576,6 +678,8 @@ bool cull(const Mat& a, const Mat& b, double tau, bool want_tasks, CullResult& r
   r.culled.assign(depth + 1, 0);
   r.n_c = r.n_tasks = 0;
   r.sym = sym;
+  r.near.assign(depth + 1, 0);
+  r.margin = INFINITY;
   if (g_dense_enabled && depth <= DENSE_MAX_DEPTH && lo <= 0 && hi < 0 && !work)
     return dense_cull(a, b, tau, want_tasks, r, s, sym);
 
@@ -585,9 +689,12 @@ bool cull(const Mat& a, const Mat& b, double tau, bool want_tasks, CullResult& r
   int32_t* K = dmalloc<int32_t>(1, s);
   // aux[0]: survivors in diagonal C nodes (symmetric mode), aux[1]: mirror
   // mismatch flag, aux[2]: packed scan total (root count first), aux[3]:
-  // diagonal C nodes with survivors.
-  int64_t* aux = dmalloc<int64_t>(4, s);
-  SPAMM_CK(cudaMemsetAsync(aux, 0, 4 * sizeof(int64_t), s));
+  // diagonal C nodes with survivors, aux[4]: near-tau products of the tier,
+  // aux[5]: inverted min relative margin (tie_probe; kept across tiers).
+  int64_t* aux = dmalloc<int64_t>(6, s);
+  SPAMM_CK(cudaMemsetAsync(aux, 0, 6 * sizeof(int64_t), s));
+  const TieBand tb = tie_band(tau);
+  auto* u64 = reinterpret_cast<unsigned long long*>(aux);
   int32_t* aidx = nullptr;
   int32_t* bidx = nullptr;
   int64_t V = 0, M = 0, full_prev = 0, diag_nodes = 0;
@@ -598,7 +705,7 @@ bool cull(const Mat& a, const Mat& b, double tau, bool want_tasks, CullResult& r
     event_wait(b.top_ev);
     HostLevel L;
     if (!host_cull_top(a.host_top, b.host_top, T0, depth, tau, sym, lo, hi, r, L, full_prev,
-                       diag_nodes)) {
+                       diag_nodes, tb)) {
       dfree(ci, s);
       dfree(cj, s);
       dfree(seg, s);
@@ -638,9 +745,13 @@ bool cull(const Mat& a, const Mat& b, double tau, bool want_tasks, CullResult& r
       bidx = dmalloc<int32_t>(1, s);
     }
     k_cull_root<<<1, 1, 0, s>>>(a.norms, b.norms, tau, ci, cj, seg, K, aux + 2, a.slot, b.slot,
-                                aidx, bidx);
+                                aidx, bidx, tb, u64 + 4, u64 + 5);
     SPAMM_LAUNCH_CK();
-    d2h_sync(&V, aux + 2, 1, s);
+    int64_t h0[6];
+    d2h_sync(h0, aux, 6, s);
+    V = h0[2];
+    r.near[0] = h0[4];
+    r.margin = margin_from_bits(h0[5]);
     r.visited[0] = V;
     r.culled[0] = 1 - V;
     M = V;
@@ -666,18 +777,19 @@ bool cull(const Mat& a, const Mat& b, double tau, bool want_tasks, CullResult& r
     const bool leaf = t1 == depth;
     int64_t* cnt4 = dmalloc<int64_t>(4 * M, s);
     int64_t* off4 = dmalloc<int64_t>(4 * M + 1, s);
-    SPAMM_CK(cudaMemsetAsync(aux, 0, 4 * sizeof(int64_t), s));
+    SPAMM_CK(cudaMemsetAsync(aux, 0, 5 * sizeof(int64_t), s));
     k_cull_expand<false, false><<<cull_grid(M), CULL_THREADS, 0, s>>>(
         t1, a.norms, b.norms, tau, M, ci, cj, seg, K, cnt4, nullptr, nullptr, nullptr, nullptr,
-        nullptr, nullptr, nullptr, nullptr, nullptr, 0, 0, sym ? 1 : 0,
-        reinterpret_cast<unsigned long long*>(aux), lo, hi, 2 * (depth - t1),
-        leaf ? work : nullptr);
+        nullptr, nullptr, nullptr, nullptr, nullptr, 0, 0, sym ? 1 : 0, u64, lo, hi,
+        2 * (depth - t1), leaf ? work : nullptr, tb);
     SPAMM_LAUNCH_CK();
     scan_exclusive_i64(cnt4, 4 * M, off4, s);
     SPAMM_CK(cudaMemcpyAsync(aux + 2, off4 + 4 * M, sizeof(int64_t), cudaMemcpyDeviceToDevice, s));
-    int64_t h[4];
-    d2h_sync(h, aux, 4, s);
+    int64_t h[6];
+    d2h_sync(h, aux, 6, s);
     diag_nodes = h[3];
+    r.near[t1] = h[4];
+    r.margin = std::min(r.margin, margin_from_bits(h[5]));
     if (h[1]) {  // survivor set not symmetric: the caller falls back to the full cull
       dfree(cnt4, s);
       dfree(off4, s);
@@ -711,12 +823,13 @@ bool cull(const Mat& a, const Mat& b, double tau, bool want_tasks, CullResult& r
       bi = dmalloc<int32_t>(Vn, s);
       k_cull_expand<true, true><<<cull_grid(M), CULL_THREADS, 0, s>>>(
           t1, a.norms, b.norms, tau, M, ci, cj, seg, K, nullptr, off4, ci_o, cj_o, seg_o, K_o,
-          a.slot, b.slot, ai, bi, Mn, Vn, sym ? 1 : 0, nullptr, lo, hi, 2 * (depth - t1), work);
+          a.slot, b.slot, ai, bi, Mn, Vn, sym ? 1 : 0, nullptr, lo, hi, 2 * (depth - t1), work,
+          tb);
     } else {
       k_cull_expand<true, false><<<cull_grid(M), CULL_THREADS, 0, s>>>(
           t1, a.norms, b.norms, tau, M, ci, cj, seg, K, nullptr, off4, ci_o, cj_o, seg_o, K_o,
           nullptr, nullptr, nullptr, nullptr, Mn, Vn, sym ? 1 : 0, nullptr, lo, hi,
-          2 * (depth - t1), nullptr);
+          2 * (depth - t1), nullptr, tb);
     }
     SPAMM_LAUNCH_CK();
     dfree(cnt4, s);

@@ -20,7 +20,7 @@ T* dmalloc(size_t n, cudaStream_t s) {
 
 // Copy a few int64 from device to host and wait (the only host syncs on the path).
 void d2h_sync(int64_t* host, const int64_t* dev, int n, cudaStream_t s);
-// One launch copies n (<= 48) device scalars (null source -> 0) straight into
+// One launch copies n (<= 64) device scalars (null source -> 0) straight into
 // pinned host memory, then waits: replaces memset + D2D copies + D2H per sync.
 void gather_sync(int64_t* host, const int64_t* const* src, int n, cudaStream_t s);
 void copy_to_pinned(double* host, const double* dev, int64_t n, cudaStream_t s);
@@ -139,6 +139,10 @@ struct CullResult {
   int32_t* a_idx = nullptr;   // n_tasks (storage slot of A_ik)
   int32_t* b_idx = nullptr;   // n_tasks (storage slot of B_kj)
   std::vector<int64_t> visited, culled;  // full (reference) counts in both modes
+  // tested products within k ulp of tau per tier (k: set_near_tau_ulps), and
+  // min |p - tau| / tau over tested products within tau 2^-20 (+inf if none)
+  std::vector<int64_t> near;
+  double margin = 0.0;
   bool sym = false;                      // only C nodes with i <= j were carried
   // Filled by the dense cull only: the C layout (keys of all n_c_full blocks in
   // Morton order; per emitted node its storage slot and, symmetric, its mirror
@@ -167,6 +171,7 @@ struct CullResult {
 // only the shard.  work (Morton-indexed, G*G int32): task count per emitted C
 // block (persistence load balancing).
 void set_dense_cull(bool enabled);
+void set_near_tau_ulps(int k);
 bool cull(const Mat& a, const Mat& b, double tau, bool want_tasks, CullResult& r, cudaStream_t s,
           bool sym = false, int64_t lo = 0, int64_t hi = -1, int32_t* work = nullptr);
 
@@ -220,7 +225,7 @@ struct OzakiOperands {
   bool sym_b = false;
   bool as_cached = false;            // `as` is the per-thread kept buffer
   bool tail_cached = false;          // ex_a / b_tr live in it too
-  void (*release_cache)() = nullptr;  // marks it free again
+  void (*release_cache)(cudaStream_t) = nullptr;  // marks it free after the work on s
 };
 // Nb = 32 variant (leaf_ozaki32.cu): operand passes (row / column exponents
 // when `exponents`, digit slices) and the K4z launch.
@@ -238,6 +243,8 @@ void ozaki_launch(int64_t n_seg, const int64_t* seg, const Idx* a_idx, const Idx
                   const Mat& B, const OzakiOperands& op, double* C, cudaStream_t s,
                   LptSchedule lpt = {});
 void ozaki_release(OzakiOperands& op, cudaStream_t s);
+// Free this thread's kept slice buffer on the current device (if idle).
+void ozaki_cache_trim();
 template <class Idx>
 bool leaf_products_ozaki(int64_t n_seg, const int64_t* seg, const Idx* a_idx, const Idx* b_idx,
                          const int64_t* c_out, const int64_t* c_mirror, bool accumulate,

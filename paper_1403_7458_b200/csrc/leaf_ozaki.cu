@@ -14,14 +14,18 @@
 //    is < 2^(E-63));
 //  * a digit product sum_k dA_p[r][k] dB_q[k][c] is computed EXACTLY in int32
 //    on the tensor cores and summed exactly over the tasks of the C block
-//    (|.| <= 4 x 64 x 2^14 = 2^22 per task and quadrant, so chunks of
-//    OZ_CHUNK = 256 tasks are flushed to FP64);
+//    (|.| <= 64 x 2^14 = 2^20 per task and digit pair; a quadrant of tile t
+//    accumulates the t + 1 <= 4 anchors of digit sum 2t and the epilogue adds
+//    <= 2 quadrants per digit sum, so <= 8 pairs x OZ_CHUNK = 128 tasks x
+//    2^20 = 2^30 -- int32 exact; longer segments flush per chunk to FP64, in
+//    order);
 //  * all digit pairs p + q <= 7 (and four of p + q = 8) are formed: A slices
 //    stacked two per MMA along M (rows 0-63 = s_p, 64-127 = s_p+1), B slices
-//    two per MMA along N, 10 MMAs of 128x128x64 per task into 4 TMEM tiles of
-//    128 columns (tile t holds the pairs of digit sums 2t, 2t+1, 2t+2 in its
-//    four quadrants) -- all 512 TMEM columns;
-//  * the epilogue adds the quadrants of equal digit sum d in int64 (exact),
+//    two per MMA along N, 10 slice-pair blocks x 2 k-steps = 20 MMAs of
+//    128x128x32 per task into 4 TMEM tiles of 128 columns (tile t holds the
+//    pairs of digit sums 2t, 2t+1, 2t+1, 2t+2 in its four quadrants) -- all
+//    512 TMEM columns;
+//  * the epilogue adds the quadrants of equal digit sum d in int32 (exact),
 //    so S_d[r][c] = S_d[c][r] bitwise for a symmetric operand, and rounds once
 //    per d: C = 2^(Er+Ec-14) sum_d S_d 2^-8d (Horner with fused multiply-add).
 //
@@ -34,7 +38,7 @@
 // bitwise symmetric), not bitwise the DMMA kernel's.
 //
 // Operand traffic per task is the FP64 kernel's (8 slices x 4 KB = 32 KB per
-// block), compute per task is 20 tcgen05 MMAs of 128x128x32 = 1,280 tensor
+// block), compute per task is 20 tcgen05 MMAs of 128x128x32 = 1,333 tensor
 // cycles versus ~4,100 cycles of DMMA at 64x64x64.
 #include <climits>
 #include <cstdlib>
@@ -59,6 +63,11 @@ constexpr int OZ_BLOCK_BYTES = OZ_SLICES * OZ_SLICE_BYTES;     // 32 KB
 constexpr int OZ_STAGES = 3;
 constexpr int OZ_STAGE = 2 * OZ_BLOCK_BYTES;                   // A + B slices of one task
 constexpr int OZ_CHUNK = 128;       // tasks per TMEM accumulation (quadrant sums stay < 2^30)
+// int32 bound: S_d adds <= 2 quadrants of <= 4 digit pairs each (tile 3 has
+// anchors (0,6), (2,4), (4,2), (6,0)), each pair <= 64 products of |digit|^2
+// <= 2^14 per task.
+static_assert(8LL * OZ_NB * (1LL << 14) * OZ_CHUNK < (1LL << 31),
+              "OZ_CHUNK too large for exact int32 digit sums");
 // Epilogue: 8 warps in two groups of 4 (warp w reads TMEM lane quarter w % 4);
 // group g converts the columns 32g..32g+31 of the C block.
 constexpr int OZ_EPI = 256;
@@ -91,12 +100,12 @@ __global__ void __launch_bounds__(256) k_oz_exponents(const double* __restrict__
     if (by_col) {
       double mx = 0.0;
 #pragma unroll 4
-      for (int i = 0; i < 16; ++i) mx = fmax(mx, fabs(b[((t >> 6) + 4 * i) * OZ_NB + (t & 63)]));
+      for (int i = 0; i < 16; ++i) mx = fmax(mx, oz_absf(b[((t >> 6) + 4 * i) * OZ_NB + (t & 63)]));
       red[t >> 6][t & 63] = mx;
       __syncthreads();
       if (t < OZ_NB) {
         mx = fmax(fmax(red[0][t], red[1][t]), fmax(red[2][t], red[3][t]));
-        if (mx > 0.0) atomicMax(ex + (key % G) * OZ_NB + t, oz_frexp(mx));
+        if (mx > 0.0) atomicMax(ex + (key % G) * OZ_NB + t, oz_exp_of(mx));
       }
       __syncthreads();
     } else {
@@ -107,10 +116,10 @@ __global__ void __launch_bounds__(256) k_oz_exponents(const double* __restrict__
       for (int i = 0; i < 8; ++i) v[i] = q[i];
       double mx = 0.0;
 #pragma unroll
-      for (int i = 0; i < 8; ++i) mx = fmax(mx, fmax(fabs(v[i].x), fabs(v[i].y)));
+      for (int i = 0; i < 8; ++i) mx = fmax(mx, fmax(oz_absf(v[i].x), oz_absf(v[i].y)));
       mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
       mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
-      if ((t & 3) == 0 && mx > 0.0) atomicMax(ex + (key / G) * OZ_NB + (t >> 2), oz_frexp(mx));
+      if ((t & 3) == 0 && mx > 0.0) atomicMax(ex + (key / G) * OZ_NB + (t >> 2), oz_exp_of(mx));
     }
   }
 }
@@ -198,7 +207,8 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
                  const int* __restrict__ ex_a, const int* __restrict__ ex_b,
                  const int64_t* __restrict__ c_out, const int64_t* __restrict__ c_mirror,
                  int accumulate, double* __restrict__ C, const int32_t* __restrict__ order,
-                 int* __restrict__ next_block, int hint, long long* __restrict__ prof) {
+                 int* __restrict__ next_block, int hint, long long* __restrict__ prof,
+                 const double* __restrict__ Ad, const double* __restrict__ Bd) {
   pdl_wait();
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
@@ -273,7 +283,9 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
             const bool first = r % OZ_CHUNK == 0;
             const bool last = tq + 1 == t1 || (r + 1) % OZ_CHUNK == 0;
             const bool cont = r >= OZ_CHUNK || accumulate;
-            meta[stage] = (m << 3) | (first ? 1 : 0) | (last ? 2 : 0) | (cont ? 4 : 0);
+            // bit 3: the chunk ends the C block's segment
+            meta[stage] = (m << 4) | (first ? 1 : 0) | (last ? 2 : 0) | (cont ? 4 : 0) |
+                          (tq + 1 == t1 ? 8 : 0);
             if (first)
               meta2[stage] = ((a_keys[a_idx[tq]] / G) << 32) | (b_keys[b_idx[tq]] % G);
             mbar_expect_tx(full(stage), OZ_STAGE);
@@ -397,10 +409,12 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
         break;
       }
       const int64_t bij = ring[1];
-      const int64_t m = md >> 3;
-      const bool cont = md & 4;
+      const int64_t m = md >> 4;
+      const bool cont = md & 4, seg_end = md & 8;
       const int64_t bi = bij >> 32, bj = bij & 0xffffffffLL;
-      const int er = oz_exp(ex_a[bi * OZ_NB + r]) - 14;
+      const int exr = ex_a[bi * OZ_NB + r];
+      const bool row_bad = exr == OZ_EXP_BAD;
+      const int er = (row_bad ? 0 : oz_exp(exr)) - 14;
       double* Cb = C + (c_out ? c_out[m] : m) * (int64_t)(OZ_NB * OZ_NB);
       const int64_t mi = c_mirror ? c_mirror[m] : -1;
       double* Cm = mi >= 0 ? C + mi * (int64_t)(OZ_NB * OZ_NB) : nullptr;
@@ -447,6 +461,9 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
           oR[t][0] = b.x; oR[t][1] = b.y; oR[t][2] = b.z; oR[t][3] = b.w;
         }
         const int ecs[4] = {ec4.x, ec4.y, ec4.z, ec4.w};
+        bool bad[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) bad[c] = row_bad || ecs[c] == OZ_EXP_BAD;
         double res[4];
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
@@ -467,31 +484,51 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
           double v = (double)S[8];
 #pragma unroll
           for (int d = 7; d >= 0; --d) v = __fma_rn(v, 0x1p-8, (double)S[d]);
-          const int k = er + oz_exp(ecs[c]);  // C = v 2^k
+          const int k = er + (bad[c] ? 0 : oz_exp(ecs[c]));  // C = v 2^k
           res[c] = (k >= -1022 && k <= 1023)
                        ? __dmul_rn(v, __longlong_as_double((long long)(k + 1023) << 52))
                        : ldexp(v, k);
         }
         double2* row = reinterpret_cast<double2*>(Cb + r * OZ_NB + col0);
-        if (cont) {
-          const double2 p0 = row[0], p1 = row[1];
-          res[0] = __dadd_rn(p0.x, res[0]);
-          res[1] = __dadd_rn(p0.y, res[1]);
-          res[2] = __dadd_rn(p1.x, res[2]);
-          res[3] = __dadd_rn(p1.y, res[3]);
-        }
-        if (hint & 2) {  // products streamed past L2 (evict_first)
-          __stcs(row, make_double2(res[0], res[1]));
-          __stcs(row + 1, make_double2(res[2], res[3]));
-          if (Cm)
-#pragma unroll
-            for (int c = 0; c < 4; ++c) __stcs(Cm + (col0 + c) * OZ_NB + r, res[c]);
+        if (bad[0] || bad[1] || bad[2] || bad[3]) {
+          // a non-finite operand entry in this row or one of these columns:
+          // those elements are computed once, at the segment's end, in FP64
+          // in the reference's order (earlier chunks leave them untouched)
+          double* rp = Cb + r * OZ_NB + col0;
+#pragma unroll 1
+          for (int c = 0; c < 4; ++c) {
+            double v = res[c];
+            if (bad[c]) {
+              if (!seg_end) continue;
+              v = oz_exact_elem<Idx>(accumulate ? rp[c] : 0.0, Ad, Bd, a_idx, b_idx, seg[m],
+                                     seg[m + 1], OZ_NB, r, col0 + c);
+            } else if (cont) {
+              v = __dadd_rn(rp[c], v);
+            }
+            rp[c] = v;
+            if (Cm) Cm[(col0 + c) * OZ_NB + r] = v;
+          }
         } else {
-          row[0] = make_double2(res[0], res[1]);
-          row[1] = make_double2(res[2], res[3]);
-          if (Cm)
+          if (cont) {
+            const double2 p0 = row[0], p1 = row[1];
+            res[0] = __dadd_rn(p0.x, res[0]);
+            res[1] = __dadd_rn(p0.y, res[1]);
+            res[2] = __dadd_rn(p1.x, res[2]);
+            res[3] = __dadd_rn(p1.y, res[3]);
+          }
+          if (hint & 2) {  // products streamed past L2 (evict_first)
+            __stcs(row, make_double2(res[0], res[1]));
+            __stcs(row + 1, make_double2(res[2], res[3]));
+            if (Cm)
 #pragma unroll
-            for (int c = 0; c < 4; ++c) Cm[(col0 + c) * OZ_NB + r] = res[c];
+              for (int c = 0; c < 4; ++c) __stcs(Cm + (col0 + c) * OZ_NB + r, res[c]);
+          } else {
+            row[0] = make_double2(res[0], res[1]);
+            row[1] = make_double2(res[2], res[3]);
+            if (Cm)
+#pragma unroll
+              for (int c = 0; c < 4; ++c) Cm[(col0 + c) * OZ_NB + r] = res[c];
+          }
         }
         asm volatile("bar.sync %0, 128;\n" ::"r"(1 + grp) : "memory");
       }
@@ -512,6 +549,41 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
 }  // namespace
 
 bool ozaki_supported(int nb) { return nb == OZ_NB || nb == 32; }
+
+// The A slices of the SP2 loop's X*X (one size, every iteration): a buffer
+// kept across multiplies per (host thread, device) instead of a pool round
+// trip per product.  Reuse is ordered on the device: release records `done`
+// on the stream that ran K4z, and the next prepare's stream waits on it (the
+// caller may pass a different stream per multiply).
+struct SliceCache {
+  int8_t* p = nullptr;
+  size_t bytes = 0;
+  bool busy = false;           // handed out (host side: one multiply at a time)
+  cudaEvent_t done = nullptr;  // recorded after the last K4z that read it
+  bool pending = false;
+};
+static SliceCache& slice_cache() {
+  thread_local SliceCache caches[64];
+  int dev = 0;
+  SPAMM_CK(cudaGetDevice(&dev));
+  return caches[dev & 63];
+}
+static void slice_cache_release(cudaStream_t s) {
+  SliceCache& c = slice_cache();
+  if (!c.done) SPAMM_CK(cudaEventCreateWithFlags(&c.done, cudaEventDisableTiming));
+  SPAMM_CK(cudaEventRecord(c.done, s));
+  c.pending = true;
+  c.busy = false;
+}
+void ozaki_cache_trim() {
+  SliceCache& c = slice_cache();
+  if (c.busy || !c.p) return;
+  if (c.pending) SPAMM_CK(cudaEventSynchronize(c.done));
+  SPAMM_CK(cudaFree(c.p));
+  c.p = nullptr;
+  c.bytes = 0;
+  c.pending = false;
+}
 
 static void oz_dbg(const char* what, cudaStream_t s) {
   static const bool on = getenv("SPAMM_OZ_DEBUG") != nullptr;
@@ -539,22 +611,20 @@ bool ozaki_prepare(const Mat& A, const Mat& B, bool sym_b, cudaStream_t s, Ozaki
   const size_t b_bytes = sym_b ? 0 : (size_t)B.nblocks * blk_bytes;
   static const bool force_fail = getenv("SPAMM_OZ_FORCE_NOMEM") != nullptr;  // test hook
   if (try_only && force_fail) return false;
-  // The A slices of the SP2 loop's X*X (one size, every iteration): a
-  // per-thread buffer kept across multiplies instead of a pool round trip per
-  // product (operands up to 1 GB; reuse is ordered by the caller's stream, on
-  // which the previous K4z ran before this pre-pass starts).
-  struct SliceCache {
-    int8_t* p = nullptr;
-    size_t bytes = 0;
-    bool busy = false;
-  };
-  thread_local SliceCache cache;
+  // The A slices of the SP2 loop's X*X: the kept buffer (slice_cache) for
+  // operands up to 1 GB.
+  SliceCache& cache = slice_cache();
   // (sym: the row exponents and the transposed-slot map ride in the same buffer)
   const size_t extra = sym_b ? (size_t)G * nb * 4 + (size_t)(A.nblocks > 0 ? A.nblocks : 1) * 4 : 0;
   const size_t want = a_bytes + extra;
   if (a_bytes && want <= (size_t(1) << 30) && !cache.busy) {
+    if (cache.pending) SPAMM_CK(cudaStreamWaitEvent(s, cache.done, 0));  // last K4z done with it
     if (cache.bytes < want) {
-      if (cache.p) cudaFree(cache.p);
+      if (cache.p) {
+        if (cache.pending) SPAMM_CK(cudaEventSynchronize(cache.done));
+        cudaFree(cache.p);
+      }
+      cache.pending = false;
       cache.p = nullptr;
       cache.bytes = 0;
       if (cudaMalloc(reinterpret_cast<void**>(&cache.p), want) == cudaSuccess) {
@@ -570,7 +640,7 @@ bool ozaki_prepare(const Mat& A, const Mat& B, bool sym_b, cudaStream_t s, Ozaki
       cache.busy = true;
     }
   }
-  op.release_cache = [](void) { cache.busy = false; };
+  op.release_cache = slice_cache_release;
   if (op.as_cached) {
     if (!try_only) op.bs = static_cast<int8_t*>(dmalloc_bytes(b_bytes, s));
     else if (b_bytes &&
@@ -659,7 +729,7 @@ void ozaki_release(OzakiOperands& op, cudaStream_t s) {
   }
   if (!op.tail_cached) dfree(op.ex_a, s);
   if (op.as_cached) {
-    if (op.release_cache) op.release_cache();
+    if (op.release_cache) op.release_cache(s);
   } else {
     dfree(op.as, s);
   }
@@ -718,7 +788,8 @@ void ozaki_launch(int64_t n_seg, const int64_t* seg, const Idx* a_idx, const Idx
   launch_plain(kern, (unsigned)grid, OZ_THREADS, OZ_SMEM, s, n_seg, seg, a_idx, b_idx,
              (const int32_t*)op.b_tr, (const int64_t*)A.keys, (const int64_t*)B.keys, op.G,
              (const int8_t*)op.as, (const int8_t*)op.bs, (const int*)op.ex_a, (const int*)op.ex_b,
-             c_out, c_mirror, accumulate ? 1 : 0, C, order, counter, hint, prof);
+             c_out, c_mirror, accumulate ? 1 : 0, C, order, counter, hint, prof,
+             (const double*)A.data, (const double*)B.data);
   SPAMM_LAUNCH_CK();
   oz_dbg("k4z", s);
   if (prof) {  // SPAMM_K4Z_PROF=1: per-launch cycle breakdown (diagnostics; syncs)

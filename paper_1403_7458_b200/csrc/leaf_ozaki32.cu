@@ -81,19 +81,19 @@ __global__ void __launch_bounds__(256) k_oz32_exponents(const double* __restrict
       key = keys[s];
       if (by_col) {
 #pragma unroll
-        for (int i = 0; i < 16; ++i) mx = fmax(mx, fabs(b[(half * 16 + i) * Z_NB + line]));
+        for (int i = 0; i < 16; ++i) mx = fmax(mx, oz_absf(b[(half * 16 + i) * Z_NB + line]));
       } else {
         const double2* q = reinterpret_cast<const double2*>(b + line * Z_NB + half * 16);
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
           const double2 v = q[i];
-          mx = fmax(mx, fmax(fabs(v.x), fabs(v.y)));
+          mx = fmax(mx, fmax(oz_absf(v.x), oz_absf(v.y)));
         }
       }
     }
     mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
     if (s < nblocks && half == 0 && mx > 0.0)
-      atomicMax(ex + (by_col ? key % G : key / G) * Z_NB + line, oz_frexp(mx));
+      atomicMax(ex + (by_col ? key % G : key / G) * Z_NB + line, oz_exp_of(mx));
   }
 }
 
@@ -156,7 +156,8 @@ __global__ void __launch_bounds__(Z_THREADS, NBUF == 2 ? 1 : 2)
                    const int* __restrict__ ex_a, const int* __restrict__ ex_b,
                    const int64_t* __restrict__ c_out, const int64_t* __restrict__ c_mirror,
                    int accumulate, double* __restrict__ C, const int32_t* __restrict__ order,
-                   int* __restrict__ next_block) {
+                   int* __restrict__ next_block, const double* __restrict__ Ad,
+                   const double* __restrict__ Bd) {
   pdl_wait();
   constexpr int Z_STAGE = ZCfg<NBUF, Z_TPS, Z_STAGES>::STAGE;
   constexpr uint32_t TCOLS = 256u * NBUF;
@@ -240,8 +241,9 @@ __global__ void __launch_bounds__(Z_THREADS, NBUF == 2 ? 1 : 2)
               const bool first = r % Z_CHUNK == 0;
               const bool last = tq + n_in == t1 || (r + n_in) % Z_CHUNK == 0;
               const bool cont = r >= Z_CHUNK || accumulate;
-              meta[stage] = (m << 8) | ((int64_t)n_in << 3) | (first ? 1 : 0) | (last ? 2 : 0) |
-                            (cont ? 4 : 0);
+              // bit 8: the chunk ends the C block's segment
+              meta[stage] = (m << 9) | ((int64_t)n_in << 3) | (first ? 1 : 0) | (last ? 2 : 0) |
+                            (cont ? 4 : 0) | (tq + n_in == t1 ? 256 : 0);
               if (first)
                 meta2[stage] = ((a_keys[a_idx[tq]] / G) << 32) | (b_keys[b_idx[tq]] % G);
               mbar_expect_tx(full(stage), (uint32_t)(n_in * Z_TASK));
@@ -334,10 +336,12 @@ __global__ void __launch_bounds__(Z_THREADS, NBUF == 2 ? 1 : 2)
       const int64_t md = ring[2 * b];
       if (md < 0) break;
       const int64_t bij = ring[2 * b + 1];
-      const int64_t m = md >> 8;
-      const bool cont = md & 4;
+      const int64_t m = md >> 9;
+      const bool cont = md & 4, seg_end = md & 256;
       const int64_t bi = bij >> 32, bj = bij & 0xffffffffLL;
-      const int er = oz_exp(ex_a[bi * Z_NB + r]) - 14;
+      const int exr = ex_a[bi * Z_NB + r];
+      const bool row_bad = exr == OZ_EXP_BAD;
+      const int er = (row_bad ? 0 : oz_exp(exr)) - 14;
       double* Cb = C + (c_out ? c_out[m] : m) * (int64_t)(Z_NB * Z_NB);
       const int64_t mi = c_mirror ? c_mirror[m] : -1;
       double* Cm = mi >= 0 ? C + mi * (int64_t)(Z_NB * Z_NB) : nullptr;
@@ -370,6 +374,7 @@ __global__ void __launch_bounds__(Z_THREADS, NBUF == 2 ? 1 : 2)
         asm volatile("bar.sync 1, 128;\n" ::: "memory");
         // this thread: row r, columns 2w, 2w+1 of the chunk
         double res[2];
+        bool bad[2];
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const int c8 = 2 * w + h;
@@ -387,22 +392,43 @@ __global__ void __launch_bounds__(Z_THREADS, NBUF == 2 ? 1 : 2)
 #pragma unroll
           for (int d = 9; d >= 0; --d) v = __fma_rn(v, 0x1p-8, (double)S[d]);
           const int col = cc * 8 + c8;
-          const int k = er + oz_exp(ex_b[bj * Z_NB + col]);  // C = v 2^k
+          const int exc = ex_b[bj * Z_NB + col];
+          bad[h] = row_bad || exc == OZ_EXP_BAD;
+          const int k = er + (bad[h] ? 0 : oz_exp(exc));  // C = v 2^k
           res[h] = (k >= -1022 && k <= 1023)
                        ? __dmul_rn(v, __longlong_as_double((long long)(k + 1023) << 52))
                        : ldexp(v, k);
         }
         const int col0 = cc * 8 + 2 * w;
         double2* p = reinterpret_cast<double2*>(Cb + r * Z_NB + col0);
-        if (cont) {
-          const double2 o = *p;
-          res[0] = __dadd_rn(o.x, res[0]);
-          res[1] = __dadd_rn(o.y, res[1]);
-        }
-        *p = make_double2(res[0], res[1]);
-        if (Cm) {
-          Cm[col0 * Z_NB + r] = res[0];
-          Cm[(col0 + 1) * Z_NB + r] = res[1];
+        if (bad[0] || bad[1]) {
+          // non-finite operand entries: those elements are computed once, at
+          // the segment's end, in FP64 in the reference's order (leaf_ozaki.cu)
+          double* rp = Cb + r * Z_NB + col0;
+#pragma unroll 1
+          for (int h = 0; h < 2; ++h) {
+            double v = res[h];
+            if (bad[h]) {
+              if (!seg_end) continue;
+              v = oz_exact_elem<Idx>(accumulate ? rp[h] : 0.0, Ad, Bd, a_idx, b_idx, seg[m],
+                                     seg[m + 1], Z_NB, r, col0 + h);
+            } else if (cont) {
+              v = __dadd_rn(rp[h], v);
+            }
+            rp[h] = v;
+            if (Cm) Cm[(col0 + h) * Z_NB + r] = v;
+          }
+        } else {
+          if (cont) {
+            const double2 o = *p;
+            res[0] = __dadd_rn(o.x, res[0]);
+            res[1] = __dadd_rn(o.y, res[1]);
+          }
+          *p = make_double2(res[0], res[1]);
+          if (Cm) {
+            Cm[col0 * Z_NB + r] = res[0];
+            Cm[(col0 + 1) * Z_NB + r] = res[1];
+          }
         }
         asm volatile("bar.sync 1, 128;\n" ::: "memory");
       }
@@ -450,7 +476,7 @@ void oz32_launch_cfg(int64_t n_seg, const int64_t* seg, const Idx* a_idx, const 
                (const int32_t*)op.b_tr, (const int64_t*)A.keys, (const int64_t*)B.keys, op.G,
                (const int8_t*)op.as, (const int8_t*)op.bs, (const int*)op.ex_a,
                (const int*)op.ex_b, c_out, c_mirror, accumulate ? 1 : 0, C,
-               (const int32_t*)nullptr, counter);
+               (const int32_t*)nullptr, counter, (const double*)A.data, (const double*)B.data);
   SPAMM_LAUNCH_CK();
 }
 

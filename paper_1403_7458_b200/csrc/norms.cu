@@ -132,8 +132,9 @@ void htrace_dump() {
   g_hmarks.clear();
 }
 
+constexpr int GATHER_MAX = 64;
 struct ScalarSrc {
-  const int64_t* p[48];
+  const int64_t* p[GATHER_MAX];
 };
 // Writes the scalars, then (after a system-scope fence) the sequence number
 // the host spins on: the host sees completion as soon as the PCIe writes land,
@@ -149,16 +150,16 @@ __global__ void k_gather_scalars(ScalarSrc src, int n, int64_t* dst, int64_t* fl
 
 int64_t* pinned_scalars() {
   static thread_local int64_t* pinned = nullptr;
-  if (!pinned) SPAMM_CK(cudaMallocHost(&pinned, 96 * sizeof(int64_t)));
+  if (!pinned) SPAMM_CK(cudaMallocHost(&pinned, (32 + GATHER_MAX + 8) * sizeof(int64_t)));
   return pinned;
 }
 
 void gather_sync(int64_t* host, const int64_t* const* src, int n, cudaStream_t s) {
-  if (n > 48) throw CudaError("gather_sync: too many scalars");
+  if (n > GATHER_MAX) throw CudaError("gather_sync: too many scalars");
   ScalarSrc ss{};
   for (int i = 0; i < n; ++i) ss.p[i] = src[i];
-  int64_t* pinned = pinned_scalars() + 32;  // values [32, 80), sequence flag [80]
-  volatile int64_t* flag = pinned_scalars() + 80;
+  int64_t* pinned = pinned_scalars() + 32;  // values [32, 96), sequence flag [96]
+  volatile int64_t* flag = pinned_scalars() + 32 + GATHER_MAX;
   static thread_local int64_t seq = 0;
   ++seq;
   launch_pdl(k_gather_scalars, 1, 64, 0, s, ss, n, pinned, const_cast<int64_t*>(flag), seq);

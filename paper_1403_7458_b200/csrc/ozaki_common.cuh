@@ -9,8 +9,34 @@ namespace spamm {
 namespace ozk {
 
 constexpr int OZ_EXP_NONE = (int)0x80808080;  // memset pattern: "no nonzero seen"
+// Row / column holding an Inf or NaN (atomicMax: dominates every exponent).
+// Its digits are all zero, and the epilogue recomputes the C elements of that
+// row / column in FP64 in the reference's order (oz_exact_elem), so non-finite
+// operands give the reference's Inf / NaN pattern (kernel.py:64-77).
+constexpr int OZ_EXP_BAD = 0x7fffffff;
 
 __device__ __forceinline__ int oz_exp(int e) { return e == OZ_EXP_NONE ? 0 : e; }
+// |x| for the exponent passes, +Inf for a non-finite x (fmax would drop NaN).
+__device__ __forceinline__ double oz_absf(double x) {
+  return isfinite(x) ? fabs(x) : __longlong_as_double(0x7ff0000000000000LL);
+}
+// C element (r, c) of one C block over its tasks [t0, t1) in the reference's
+// order (_gemm_acc, kernel.py:64-77: i-k-j loops, tasks k ascending, unfused
+// multiply and add) starting from acc -- bitwise the exact leaf kernel.
+template <class Idx>
+__device__ __noinline__ double oz_exact_elem(double acc, const double* __restrict__ A,
+                                             const double* __restrict__ B,
+                                             const Idx* __restrict__ a_idx,
+                                             const Idx* __restrict__ b_idx, int64_t t0, int64_t t1,
+                                             int nb, int r, int c) {
+  const int64_t nb2 = (int64_t)nb * nb;
+  for (int64_t t = t0; t < t1; ++t) {
+    const double* a = A + (int64_t)a_idx[t] * nb2 + (int64_t)r * nb;
+    const double* b = B + (int64_t)b_idx[t] * nb2 + c;
+    for (int k = 0; k < nb; ++k) acc = __dadd_rn(acc, __dmul_rn(a[k], b[(int64_t)k * nb]));
+  }
+  return acc;
+}
 // Row / column exponent E: max |x| < 2^E, bumped when the mantissa is within
 // 2^-7.5 of 1 so that |x 2^(7-E)| <= 127.25 -- the leading signed digit then
 // stays in [-128, 127] after the carry from the tail.
@@ -18,6 +44,10 @@ __device__ __forceinline__ int oz_frexp(double mx) {
   int e;
   const double f = frexp(mx, &e);
   return f >= 0.994140625 ? e + 1 : e;
+}
+// The row / column exponent of a reduced max oz_absf (mx > 0).
+__device__ __forceinline__ int oz_exp_of(double mx) {
+  return isinf(mx) ? OZ_EXP_BAD : oz_frexp(mx);
 }
 
 

@@ -7,14 +7,17 @@ runs in ``libspamm_b200``:
 
 * K2/K3 tiered cull + in-order compaction (replaces ``_sweep`` kernel.py:96-122
   and the sort/searchsorted block kernel.py:189-204),
-* K4 FP64-DMMA leaf products with a task-sorted segmented reduction
-  (replaces ``_gemm_batch`` kernel.py:64-77),
+* K4 leaf products with a task-sorted segmented reduction (replaces
+  ``_gemm_batch`` kernel.py:64-77): K4z (FP64 products as exact int8 digit
+  products on the tcgen05 tensor cores) for Nb in {32, 64}, DMMA otherwise,
 * K1 finalisation of C (``_from_blocks`` kernel.py:219-220).
 
 ``mode``/``workers``/``deterministic`` are accepted for drop-in compatibility;
 the GPU schedule is deterministic for every setting (one CTA owns one C block
 and reduces its k-ascending segment in registers).  Extra keyword
-``kernel``: "auto" (DMMA for Nb in {8,16,32,64}), "dmma", or "exact"
+``kernel``: "auto" (K4z for Nb in {32, 64} when the operands are finite and
+the digit slices fit, DMMA for Nb in {8, 16} and as the fallback), "ozaki"
+(force K4z; ``ValueError`` on non-finite operands), "dmma", or "exact"
 (CUDA-core, the reference's exact rounding order: bitwise-identical C).
 """
 
@@ -32,7 +35,8 @@ from . import _native as nat
 from .quadtree import QuadTreeMatrix, _check_conformable
 
 __all__ = ["ProductStats", "multiply", "convolution_census", "leaf_gemm", "gemm_batch",
-           "leaf_tasks", "set_symmetric_products", "set_dense_cull", "WORKERS_ENV_VAR"]
+           "leaf_tasks", "set_symmetric_products", "set_dense_cull", "set_near_tau_ulps",
+           "WORKERS_ENV_VAR"]
 
 WORKERS_ENV_VAR = "SPAMM_WORKERS"
 
@@ -55,6 +59,13 @@ class ProductStats:
     # symmetric SpAMM (X*X, X == X^T): leaf products actually executed
     executed_products: int = 0
     symmetric: bool = False
+    # near-tau report (the parity contract's "documented ties", kernel.py:108):
+    # per tier, tested products within near_tau_ulps ulp(tau) of tau, and the
+    # smallest relative distance |p - tau| / tau of a tested product (inf when
+    # none lies within tau * 2**-20, or tau == 0)
+    near_tau: tuple = ()
+    tau_margin: float = math.inf
+    near_tau_ulps: int = 64
 
     def to_json_dict(self) -> dict:
         return {
@@ -111,6 +122,8 @@ def _stats_from(st: nat.Stats, block_size: int, wall: float) -> ProductStats:
         ms_cull=float(st.ms_cull), ms_leaf=float(st.ms_leaf),
         ms_finalize=float(st.ms_finalize), c_blocks=int(st.c_blocks),
         executed_products=int(st.executed_products), symmetric=bool(st.symmetric),
+        near_tau=tuple(int(st.near_tau[t]) for t in range(n)),
+        tau_margin=float(st.tau_margin), near_tau_ulps=int(st.near_tau_ulps),
     )
 
 
@@ -118,6 +131,13 @@ def set_symmetric_products(enabled: bool) -> None:
     """Toggle the symmetric SpAMM path (on by default; results are bitwise
     identical either way -- the switch exists for A/B measurements)."""
     nat.check(nat.load().spamm_set_symmetric_products(1 if enabled else 0))
+
+
+def set_near_tau_ulps(ulps: int) -> None:
+    """Width of the near-tau band reported in ``ProductStats.near_tau`` (ulps
+    of tau; default 64, the operand-norm error of the DMMA / K4z kernels
+    against the reference; 1 suits the bitwise exact kernel)."""
+    nat.check(nat.load().spamm_set_near_tau_ulps(int(ulps)))
 
 
 def set_dense_cull(enabled: bool) -> None:

@@ -22,7 +22,11 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(os.path.dirname(HERE))
 sys.path.insert(0, ROOT)
 
+import hashlib  # noqa: E402
+
 import spamm  # noqa: E402  (the reference)
+
+from oracle import spamm_oracle as O  # noqa: E402  (tie_log helper only)
 from spamm import sp2 as ref_sp2  # noqa: E402
 
 from paper_1403_7458_b200.synth import (CONFIGS, decay_pair, input_digest,  # noqa: E402
@@ -39,6 +43,21 @@ def task_keys(a, b, tau):
     return np.sort((i * g + k) * g + j).astype(np.int64)
 
 
+def task_digest(a, b, tau):
+    """sha256 of the reference's sorted leaf task keys ((i G + k) G + j, int64
+    little-endian) -- the exact task set, kernel.py:96-122."""
+    return np.frombuffer(hashlib.sha256(task_keys(a, b, tau).astype("<i8").tobytes()).digest(),
+                         dtype=np.uint8)
+
+
+def tie_log(a, b, tau):
+    """Near-tau products (64 ulps) per tier and the smallest relative margin of
+    a tested product, on the REFERENCE's pyramids (oracle.tie_log restates the
+    candidate expansion of kernel.py:96-122)."""
+    near, margin = O.tie_log(a._tier_norms, b._tier_norms, tau, 64)
+    return int(sum(near)), margin
+
+
 def product_case(name, da, db, nb, tau, sample_blocks=8):
     a = spamm.build_from_dense(da, nb)
     b = spamm.build_from_dense(db, nb)
@@ -53,6 +72,7 @@ def product_case(name, da, db, nb, tau, sample_blocks=8):
         visited=np.array(st.visited), culled=np.array(st.culled),
         leaf_products=st.leaf_products, flop_estimate=st.flop_estimate,
         task_keys=task_keys(a, b, tau),
+        near_tau=tie_log(a, b, tau)[0], tau_margin=tie_log(a, b, tau)[1],
         c_keys=c._block_keys, c_pyramid=pyramid_flat(c), c_trace=spamm.trace(c),
         c_sample_keys=c._block_keys[pick], c_sample_blocks=c._block_data[pick],
         a_trace=spamm.trace(a), input_sha256=input_digest(da, db),
@@ -68,6 +88,7 @@ def sp2_fro_case(name, h, nb, n_occ, tau, fro_tol=1e-6, max_iter=100):
     bounds = spamm.gershgorin_bounds(f)
     x = spamm.sp2_init(f, bounds)
     traces, branches, idem, leaf = [spamm.trace(x)], [], [], []
+    digests, near, margin, bmargin = [], [], [], []
     it = 0
     converged = False
     for _ in range(max_iter):
@@ -75,8 +96,13 @@ def sp2_fro_case(name, h, nb, n_occ, tau, fro_tol=1e-6, max_iter=100):
         # the idempotency test.
         x_sq, st = spamm.multiply(x, x, tau, mode="tasked", workers=os.cpu_count())
         leaf.append(st.leaf_products)
+        digests.append(task_digest(x, x, tau))
+        nt, mg = tie_log(x, x, tau)
+        near.append(nt)
+        margin.append(mg)
         t_x, t_sq = spamm.trace(x), spamm.trace(x_sq)
         t_ex = 2.0 * t_x - t_sq
+        bmargin.append(abs(t_ex - n_occ) - abs(t_sq - n_occ))
         branch = ref_sp2.SQUARE if abs(t_sq - n_occ) <= abs(t_ex - n_occ) else ref_sp2.EXPAND
         e = spamm.add_scaled(1.0, x_sq, -1.0, x).norm()
         idem.append(e)
@@ -92,6 +118,8 @@ def sp2_fro_case(name, h, nb, n_occ, tau, fro_tol=1e-6, max_iter=100):
                f_pyramid=pyramid_flat(f), x0_pyramid=None, iterations=it, converged=converged,
                traces=np.array(traces), branches=np.array([b == "SQUARE" for b in branches]),
                idem=np.array(idem), leaf_products=np.array(leaf),
+               task_sha256=np.array(digests), near_tau=np.array(near), tau_margin=np.array(margin),
+               branch_margin=np.array(bmargin),
                p_pyramid=pyramid_flat(x), p_trace=spamm.trace(x), p_keys=x._block_keys,
                input_sha256=input_digest(h))
     out.pop("x0_pyramid")

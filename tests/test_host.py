@@ -36,7 +36,8 @@ def test_library_built_and_exports_header_symbols():
 def test_abi_version_and_error_string_without_gpu():
     from paper_1403_7458_b200 import _native as nat
     lib = nat.load()
-    assert lib.spamm_abi_version() == 1
+    assert lib.spamm_abi_version() == nat.ABI_VERSION == 2
+    assert lib.spamm_set_near_tau_ulps(-1) == nat.SPAMM_EINVAL
     # argument errors are reported before any CUDA call
     out = ctypes.c_void_p()
     rc = lib.spamm_mat_identity(0, 4, 4, None, ctypes.byref(out))
@@ -46,6 +47,34 @@ def test_abi_version_and_error_string_without_gpu():
     assert rc == nat.SPAMM_EINVAL and b"power of two" in lib.spamm_last_error()
     with pytest.raises(ValueError):
         nat.check(nat.SPAMM_EINVAL)
+
+
+def test_ctypes_struct_layouts_match_header(tmp_path):
+    """sizeof / offsetof of the ABI structs, compiled from include/spamm_b200.h
+    with gcc, equal the ctypes mirrors in _native.py."""
+    from paper_1403_7458_b200 import _native as nat
+    structs = {"spamm_stats": nat.Stats, "spamm_sp2_report": nat.SP2Report,
+               "spamm_mat_info": nat.MatInfo}
+    lines = ['#include <stdio.h>', '#include <stddef.h>', f'#include "{HEADER}"',
+             "int main(void) {"]
+    for cname, cls in structs.items():
+        lines.append(f'printf("{cname} %zu\\n", sizeof({cname}));')
+        for fname, _ in cls._fields_:
+            lines.append(f'printf("{cname}.{fname} %zu\\n", offsetof({cname}, {fname}));')
+    lines.append("return 0; }")
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    try:
+        subprocess.run(["gcc", "-o", str(exe), str(src)], check=True, capture_output=True)
+    except (OSError, subprocess.CalledProcessError) as e:
+        pytest.skip(f"gcc unavailable: {e}")
+    got = dict(l.rsplit(" ", 1) for l in subprocess.run([str(exe)], capture_output=True,
+                                                         text=True).stdout.splitlines())
+    for cname, cls in structs.items():
+        assert int(got[cname]) == ctypes.sizeof(cls), cname
+        for fname, _ in cls._fields_:
+            assert int(got[f"{cname}.{fname}"]) == getattr(cls, fname).offset, (cname, fname)
 
 
 def test_sass_contains_tensor_and_tma_instructions():

@@ -76,6 +76,8 @@ def test_product_configs_bitwise(name):
     c, st, (ti, tk, tj) = O.multiply(a, b, cfg.tau, threads=os.cpu_count())
     assert st["visited"] == tuple(gd["visited"]) and st["culled"] == tuple(gd["culled"])
     assert np.array_equal(_task_keys(ti, tk, tj, a.n_blocks), gd["task_keys"])
+    near, margin = O.tie_log(a.tier_norms, b.tier_norms, cfg.tau)
+    assert sum(near) == int(gd["near_tau"]) and margin == float(gd["tau_margin"])
     assert np.array_equal(c.keys, gd["c_keys"])
     assert np.array_equal(pyramid_flat(c.tier_norms), gd["c_pyramid"])
     assert O.trace(c) == float(gd["c_trace"])
@@ -97,8 +99,14 @@ def test_cfg3_sp2_bitwise():
     h, n_occ = water_cluster(cfg.n_mol, seed=0)
     f = O.from_dense(h, cfg.block_size)
     assert np.array_equal(pyramid_flat(f.tier_norms), gd["f_pyramid"])
-    res = O.sp2_solve(f, n_occ, cfg.tau, threads=os.cpu_count(), criterion="fro")
+    res = O.sp2_solve(f, n_occ, cfg.tau, threads=os.cpu_count(), criterion="fro",
+                      record_tasks=True)
     assert res.iterations == int(gd["iterations"]) and res.converged
+    # every multiply's task set (sha256 of the sorted keys) and tie log
+    assert [bytes.fromhex(h) for h in res.task_sha256] == [bytes(d) for d in gd["task_sha256"]]
+    assert [n for n, _ in res.tie_logs] == list(gd["near_tau"])
+    assert np.array_equal(np.array([m for _, m in res.tie_logs]), gd["tau_margin"])
+    assert np.array_equal(np.array(res.branch_margins), gd["branch_margin"])
     assert [b == O.SQUARE for b in res.branches] == list(gd["branches"])
     assert np.array_equal(np.array(res.trace_history), gd["traces"])
     assert np.array_equal(np.array(res.idem_history), gd["idem"])
