@@ -129,6 +129,17 @@ int spamm_mat_leaf_norms2(const spamm_mat* m, double* out, void* stream);
  * a shard then culls exactly as the whole matrix would. */
 int spamm_mat_set_pyramid(spamm_mat* m, const double* leaf_norms2, int32_t symmetric,
                           void* stream);
+/* K4z scale exponents (multi-GPU: a shard's extended operand must scale
+ * its rows as the whole matrix does, so the driver all-reduces them with MAX
+ * and installs the result).  spamm_mat_oz_exponents writes the exponents of
+ * m's global rows (by_col = 0) or columns (1) over its stored blocks into
+ * device int32[G * Nb]: per row, the largest scale exponent of its entries,
+ * INT32_MAX if one is Inf / NaN, (int32)0x80808080 if the row is empty.
+ * spamm_mat_set_oz_exponents copies them into m (NULL clears); K4z then uses
+ * them instead of computing its own.  Block size 32 or 64. */
+int spamm_mat_oz_exponents(const spamm_mat* m, int32_t by_col, int32_t* ex, void* stream);
+int spamm_mat_set_oz_exponents(spamm_mat* m, const int32_t* ex_row, const int32_t* ex_col,
+                               void* stream);
 /* identity (quadtree.py:308-323). */
 int spamm_mat_identity(int64_t n, int32_t block_size, int64_t chunk_size, void* stream,
                        spamm_mat** out);
@@ -215,6 +226,12 @@ int spamm_add_scaled(double alpha, const spamm_mat* a, double beta, const spamm_
                      void* stream, spamm_mat** out);
 /* trace (quadtree.py:296-305). */
 int spamm_trace(const spamm_mat* m, void* stream, double* out);
+/* The per-diagonal-block parts of trace (device double[G]: block b's
+ * diagonal summed sequentially, +0.0 where block (b, b) is absent): for
+ * block size > 1, trace = their sequential sum in block order -- so a
+ * Morton-sharded matrix's trace is all-reduce(diag_traces) summed in order,
+ * bitwise the whole matrix's. */
+int spamm_mat_diag_traces(const spamm_mat* m, double* out, void* stream);
 /* Fused SP2 update (sp2.py:92-101 EXPAND branch + BASELINE cfg3's idempotency
  * test): one pass over the key union of X and X2 = X*X.
  *   want_idem: *idem_norm = add_scaled(1.0, X2, -1.0, X).norm() (bit-exact),

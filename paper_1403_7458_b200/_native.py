@@ -81,6 +81,8 @@ _SIGS = {
                                         ctypes.POINTER(c_vp)]),
     "spamm_mat_leaf_norms2": (c_i32, [c_vp, c_vp, c_vp]),
     "spamm_mat_set_pyramid": (c_i32, [c_vp, c_vp, c_i32, c_vp]),
+    "spamm_mat_oz_exponents": (c_i32, [c_vp, c_i32, c_vp, c_vp]),
+    "spamm_mat_set_oz_exponents": (c_i32, [c_vp, c_vp, c_vp, c_vp]),
     "spamm_mat_identity": (c_i32, [c_i64, c_i32, c_i64, c_vp, ctypes.POINTER(c_vp)]),
     "spamm_mat_info_get": (c_i32, [c_vp, ctypes.POINTER(MatInfo)]),
     "spamm_mat_free": (c_i32, [c_vp]),
@@ -108,6 +110,7 @@ _SIGS = {
                                  c_vp]),
     "spamm_add_scaled": (c_i32, [c_f64, c_vp, c_f64, c_vp, c_vp, ctypes.POINTER(c_vp)]),
     "spamm_trace": (c_i32, [c_vp, c_vp, ctypes.POINTER(c_f64)]),
+    "spamm_mat_diag_traces": (c_i32, [c_vp, c_vp, c_vp]),
     "spamm_sp2_update": (c_i32, [c_vp, c_vp, c_i32, c_i32, c_vp, ctypes.POINTER(c_f64),
                                  ctypes.POINTER(c_vp)]),
     "spamm_sp2_step": (c_i32, [c_vp, c_f64, c_f64, c_i32, c_i32, c_i32, c_vp, ctypes.POINTER(c_vp),

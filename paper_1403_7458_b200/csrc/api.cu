@@ -375,6 +375,35 @@ int spamm_mat_set_pyramid(spamm_mat* m, const double* leaf_norms2, int32_t symme
   SPAMM_API_END
 }
 
+int spamm_mat_oz_exponents(const spamm_mat* m, int32_t by_col, int32_t* ex, void* stream) {
+  if (!m || !ex) return fail(SPAMM_EINVAL, "null argument");
+  if (!spamm::ozaki_supported(m->m.nb))
+    return fail(SPAMM_EINVAL, "INT8-sliced leaf kernel needs block size 32 or 64");
+  SPAMM_API_BEGIN
+  spamm::ozaki_exponents(m->m, by_col != 0, ex, S(stream));
+  SPAMM_API_END
+}
+
+int spamm_mat_set_oz_exponents(spamm_mat* m, const int32_t* ex_row, const int32_t* ex_col,
+                               void* stream) {
+  if (!m) return fail(SPAMM_EINVAL, "null argument");
+  if (!spamm::ozaki_supported(m->m.nb))
+    return fail(SPAMM_EINVAL, "INT8-sliced leaf kernel needs block size 32 or 64");
+  SPAMM_API_BEGIN
+  cudaStream_t s = S(stream);
+  const size_t n = (size_t)m->m.G * m->m.nb;
+  auto install = [&](int*& dst, const int32_t* src) {
+    spamm::dfree(dst, s);
+    dst = nullptr;
+    if (!src) return;
+    dst = spamm::dmalloc<int>(n, s);
+    SPAMM_CK(cudaMemcpyAsync(dst, src, n * sizeof(int), cudaMemcpyDeviceToDevice, s));
+  };
+  install(m->m.oz_ex_row, ex_row);
+  install(m->m.oz_ex_col, ex_col);
+  SPAMM_API_END
+}
+
 int spamm_mat_identity(int64_t n, int32_t block_size, int64_t chunk_size, void* stream,
                        spamm_mat** out) {
   if (!out) return fail(SPAMM_EINVAL, "null output handle");
@@ -1158,6 +1187,14 @@ int spamm_trace(const spamm_mat* m, void* stream, double* out) {
   if (!m || !out) return fail(SPAMM_EINVAL, "null argument");
   SPAMM_API_BEGIN
   *out = spamm::trace(m->m, S(stream));
+  SPAMM_API_END
+}
+
+int spamm_mat_diag_traces(const spamm_mat* m, double* out, void* stream) {
+  if (!m || !out) return fail(SPAMM_EINVAL, "null argument");
+  SPAMM_API_BEGIN
+  spamm::settle_sync(const_cast<spamm_mat*>(m)->m, S(stream));
+  spamm::diag_traces(m->m, out, S(stream));
   SPAMM_API_END
 }
 

@@ -57,6 +57,10 @@ struct Mat {
   uint8_t* pend_nz = nullptr;
   int64_t* pend_off = nullptr;   // kept offsets (+ count at [nblocks]), or null if
   int64_t* pend_kept = nullptr;  // only the count was produced (small trees)
+  // K4z row / column exponents installed from outside (multi-GPU: all-reduced
+  // over the shards), G * nb each; nullptr: computed per multiply
+  int* oz_ex_row = nullptr;
+  int* oz_ex_col = nullptr;
   cudaStream_t stream = nullptr;
   void release();
 };
@@ -225,6 +229,7 @@ struct OzakiOperands {
   bool sym_b = false;
   bool as_cached = false;            // `as` is the per-thread kept buffer
   bool tail_cached = false;          // ex_a / b_tr live in it too
+  bool ex_a_ext = false, ex_b_ext = false;  // exponents owned by the matrix (Mat::oz_ex_*)
   void (*release_cache)(cudaStream_t) = nullptr;  // marks it free after the work on s
 };
 // Nb = 32 variant (leaf_ozaki32.cu): operand passes (row / column exponents
@@ -245,6 +250,11 @@ void ozaki_launch(int64_t n_seg, const int64_t* seg, const Idx* a_idx, const Idx
 void ozaki_release(OzakiOperands& op, cudaStream_t s);
 // Free this thread's kept slice buffer on the current device (if idle).
 void ozaki_cache_trim();
+// K4z exponents of M's global rows (by_col = false) or columns: ex[G * nb]
+// = max over stored blocks of the scale exponent (OZ_EXP_BAD for a
+// non-finite entry, the memset pattern where the row / column is empty).
+void ozaki_exponents(const Mat& M, bool by_col, int* ex, cudaStream_t s);
+void oz32_exponents(const Mat& M, bool by_col, int* ex, cudaStream_t s);
 template <class Idx>
 bool leaf_products_ozaki(int64_t n_seg, const int64_t* seg, const Idx* a_idx, const Idx* b_idx,
                          const int64_t* c_out, const int64_t* c_mirror, bool accumulate,
@@ -264,6 +274,9 @@ void add_scaled(double alpha, const Mat& a, double beta, const Mat& b, Mat& out,
                 cudaStream_t s);
 double trace(const Mat& m, cudaStream_t s);  // cached per matrix
 void trace_launch(const Mat& m, double* dev_out, cudaStream_t s);  // no host sync
+// Per diagonal block b (G doubles): the sequential sum of its diagonal, +0.0
+// if absent -- trace() adds these in block order (multi-GPU: all-reduced).
+void diag_traces(const Mat& m, double* out, cudaStream_t s);
 void gershgorin(const Mat& f, double* eps_min, double* eps_max, double* asym, cudaStream_t s);
 // Counter-based cluster Hamiltonian (config 5) built on the device (gen.cu).
 // Build the pyramid of m from a full leaf tier of norm^2 (G*G, row-major

@@ -668,16 +668,26 @@ bool ozaki_prepare(const Mat& A, const Mat& B, bool sym_b, cudaStream_t s, Ozaki
     op.as = static_cast<int8_t*>(dmalloc_bytes(a_bytes, s));
     op.bs = static_cast<int8_t*>(dmalloc_bytes(b_bytes, s));
   }
+  // Row exponents installed on the matrix (spamm_mat_set_oz_exponents: the
+  // multi-GPU driver all-reduces them so that a shard's extended operand
+  // scales its rows exactly as the whole matrix would) are used as given.
+  const bool ex_a_given = A.oz_ex_row != nullptr;
   if (op.as_cached && sym_b) {
     op.ex_a = reinterpret_cast<int*>(op.as + a_bytes);
     op.b_tr = op.ex_a + G * nb;
     op.tail_cached = true;
-  } else {
+  } else if (!ex_a_given) {
     op.ex_a = dmalloc<int>(G * nb, s);
   }
-  SPAMM_CK(cudaMemsetAsync(op.ex_a, 0x80, G * nb * sizeof(int), s));
+  if (ex_a_given) {
+    op.ex_a_ext = true;
+    op.ex_a = A.oz_ex_row;
+  } else {
+    SPAMM_CK(cudaMemsetAsync(op.ex_a, 0x80, G * nb * sizeof(int), s));
+  }
+  const bool ex_b_given = !sym_b && B.oz_ex_col != nullptr;
   if (nb == 32) {
-    oz32_operand_passes(A, false, op.ex_a, op.as, s, true);
+    oz32_operand_passes(A, false, op.ex_a, op.as, s, !ex_a_given);
     if (sym_b) {
       op.ex_b = op.ex_a;
       op.bs = op.as;
@@ -686,18 +696,28 @@ bool ozaki_prepare(const Mat& A, const Mat& B, bool sym_b, cudaStream_t s, Ozaki
                  A.nblocks, G, (const int32_t*)A.slot, op.b_tr);
       SPAMM_LAUNCH_CK();
     } else {
-      op.ex_b = dmalloc<int>(G * nb, s);
-      SPAMM_CK(cudaMemsetAsync(op.ex_b, 0x80, G * nb * sizeof(int), s));
-      oz32_operand_passes(B, true, op.ex_b, op.bs, s, true);
+      if (ex_b_given) {
+        op.ex_b_ext = true;
+        op.ex_b = B.oz_ex_col;
+      } else {
+        op.ex_b = dmalloc<int>(G * nb, s);
+        SPAMM_CK(cudaMemsetAsync(op.ex_b, 0x80, G * nb * sizeof(int), s));
+      }
+      oz32_operand_passes(B, true, op.ex_b, op.bs, s, !ex_b_given);
     }
     return true;
   }
   const int gx = grid_for(A.nblocks, 1, (int64_t)multiprocessors() * 8);
-  launch_plain(k_oz_exponents, gx, 256, 0, s, A.data, A.keys, A.nblocks, G, 0, op.ex_a);
-  SPAMM_LAUNCH_CK();
-  oz_dbg("exponents A", s);
-  launch_pdl(k_oz_split, gx, 256, 0, s, A.data, A.keys, A.nblocks, G, 0, (const int*)op.ex_a,
-             op.as);
+  if (!ex_a_given) {
+    launch_plain(k_oz_exponents, gx, 256, 0, s, A.data, A.keys, A.nblocks, G, 0, op.ex_a);
+    SPAMM_LAUNCH_CK();
+    oz_dbg("exponents A", s);
+    launch_pdl(k_oz_split, gx, 256, 0, s, A.data, A.keys, A.nblocks, G, 0, (const int*)op.ex_a,
+               op.as);
+  } else {  // (first launch after the cross-stream wait: plain)
+    launch_plain(k_oz_split, gx, 256, 0, s, A.data, A.keys, A.nblocks, G, 0,
+                 (const int*)op.ex_a, op.as);
+  }
   SPAMM_LAUNCH_CK();
   oz_dbg("split A", s);
   if (sym_b) {
@@ -708,11 +728,16 @@ bool ozaki_prepare(const Mat& A, const Mat& B, bool sym_b, cudaStream_t s, Ozaki
                A.nblocks, G, (const int32_t*)A.slot, op.b_tr);
     SPAMM_LAUNCH_CK();
   } else {
-    op.ex_b = dmalloc<int>(G * OZ_NB, s);
-    SPAMM_CK(cudaMemsetAsync(op.ex_b, 0x80, G * OZ_NB * sizeof(int), s));
     const int gy = grid_for(B.nblocks, 1, (int64_t)multiprocessors() * 8);
-    launch_pdl(k_oz_exponents, gy, 256, 0, s, B.data, B.keys, B.nblocks, G, 1, op.ex_b);
-    SPAMM_LAUNCH_CK();
+    if (ex_b_given) {
+      op.ex_b_ext = true;
+      op.ex_b = B.oz_ex_col;
+    } else {
+      op.ex_b = dmalloc<int>(G * OZ_NB, s);
+      SPAMM_CK(cudaMemsetAsync(op.ex_b, 0x80, G * OZ_NB * sizeof(int), s));
+      launch_pdl(k_oz_exponents, gy, 256, 0, s, B.data, B.keys, B.nblocks, G, 1, op.ex_b);
+      SPAMM_LAUNCH_CK();
+    }
     launch_pdl(k_oz_split, gy, 256, 0, s, B.data, B.keys, B.nblocks, G, 1, (const int*)op.ex_b,
                op.bs);
     SPAMM_LAUNCH_CK();
@@ -724,16 +749,30 @@ bool ozaki_prepare(const Mat& A, const Mat& B, bool sym_b, cudaStream_t s, Ozaki
 void ozaki_release(OzakiOperands& op, cudaStream_t s) {
   if (!op.tail_cached) dfree(op.b_tr, s);
   if (!op.sym_b) {
-    dfree(op.ex_b, s);
+    if (!op.ex_b_ext) dfree(op.ex_b, s);
     dfree(op.bs, s);
   }
-  if (!op.tail_cached) dfree(op.ex_a, s);
+  if (!op.tail_cached && !op.ex_a_ext) dfree(op.ex_a, s);
   if (op.as_cached) {
     if (op.release_cache) op.release_cache(s);
   } else {
     dfree(op.as, s);
   }
   op = OzakiOperands();
+}
+
+void ozaki_exponents(const Mat& M, bool by_col, int* ex, cudaStream_t s) {
+  if (!ozaki_supported(M.nb)) throw CudaError("INT8-sliced leaf kernel needs block size 32 or 64");
+  SPAMM_CK(cudaMemsetAsync(ex, 0x80, M.G * M.nb * sizeof(int), s));
+  if (M.nblocks == 0) return;
+  if (M.nb == 32) {
+    oz32_exponents(M, by_col, ex, s);
+    return;
+  }
+  const int gx = grid_for(M.nblocks, 1, (int64_t)multiprocessors() * 8);
+  launch_plain(k_oz_exponents, gx, 256, 0, s, (const double*)M.data, (const int64_t*)M.keys,
+               M.nblocks, M.G, by_col ? 1 : 0, ex);
+  SPAMM_LAUNCH_CK();
 }
 
 template <class Idx>

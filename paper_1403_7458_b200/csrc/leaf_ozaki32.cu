@@ -453,8 +453,19 @@ void oz32_operand_passes(const Mat& M, bool trans, int* ex, int8_t* out, cudaStr
                  M.nblocks, M.G, trans ? 1 : 0, ex);
     SPAMM_LAUNCH_CK();
   }
-  launch_pdl(k_oz32_split, grid, 256, 0, s, (const double*)M.data, (const int64_t*)M.keys,
-             M.nblocks, M.G, trans ? 1 : 0, (const int*)ex, out);
+  if (exponents)
+    launch_pdl(k_oz32_split, grid, 256, 0, s, (const double*)M.data, (const int64_t*)M.keys,
+               M.nblocks, M.G, trans ? 1 : 0, (const int*)ex, out);
+  else  // first launch after the caller's cross-stream wait: plain
+    launch_plain(k_oz32_split, grid, 256, 0, s, (const double*)M.data, (const int64_t*)M.keys,
+                 M.nblocks, M.G, trans ? 1 : 0, (const int*)ex, out);
+  SPAMM_LAUNCH_CK();
+}
+
+void oz32_exponents(const Mat& M, bool by_col, int* ex, cudaStream_t s) {
+  const int grid = grid_for((M.nblocks + 3) / 4, 1, (int64_t)multiprocessors() * 8);
+  launch_plain(k_oz32_exponents, grid, 256, 0, s, (const double*)M.data, (const int64_t*)M.keys,
+               M.nblocks, M.G, by_col ? 1 : 0, ex);
   SPAMM_LAUNCH_CK();
 }
 

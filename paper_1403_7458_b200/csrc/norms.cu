@@ -243,6 +243,9 @@ void top_release(double* buf, cudaEvent_t ev) {
 void Mat::release() {
   dfree(tr_dev, stream);
   tr_dev = nullptr;
+  dfree(oz_ex_row, stream);
+  dfree(oz_ex_col, stream);
+  oz_ex_row = oz_ex_col = nullptr;
   dfree(pend_nz, stream);
   dfree(pend_off, stream);
   dfree(pend_kept, stream);

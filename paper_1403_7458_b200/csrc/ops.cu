@@ -483,6 +483,14 @@ void trace_launch(const Mat& m, double* dev_out, cudaStream_t s) {
   dfree(present, s);
 }
 
+void diag_traces(const Mat& m, double* out, cudaStream_t s) {
+  SPAMM_CK(cudaMemsetAsync(out, 0, m.G * sizeof(double), s));  // absent blocks: +0.0
+  uint8_t* present = dmalloc<uint8_t>(m.G, s);
+  k_trace_blocks<<<grid_for(m.G * 32, 256), 256, 0, s>>>(m.slot, m.data, m.G, m.nb, out, present);
+  SPAMM_LAUNCH_CK();
+  dfree(present, s);
+}
+
 double trace(const Mat& m, cudaStream_t s) {
   if (m.tr_valid) return m.tr;
   int64_t* buf = dmalloc<int64_t>(1, s);

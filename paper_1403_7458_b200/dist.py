@@ -1,0 +1,640 @@
+"""Distributed SP2: X, X^2 and the update sharded along the Morton curve,
+one process per GPU (BASELINE north_star "Multi-GPU sharding").
+
+Reference semantics: the paper over-decomposes the (i, k, j) convolution
+space and rebalances from the previous iteration's measured work
+(persistence load balancing), which the reference
+only simulates (chare_sim.py:249-328 ``greedy_comm_balance``, with the prior
+measured cost at :272).  Here it runs:
+
+* **Ownership.**  The G x G block grid in the storage's Morton order is cut
+  into ``world`` contiguous segments ``cuts``.  Block (i, j) belongs to the
+  rank whose segment holds its Morton position -- or, while X is exactly
+  symmetric (the symmetric SpAMM path), the position of its upper-triangle
+  twin (min(i, j), max(i, j)), so a rank owns a block and its mirror.  X,
+  X^2 and 2X - X^2 share one ownership, so every elementwise step is local.
+* **Global structure, no replicated data.**  Each rank holds only its own
+  blocks.  The leaf tier of norm^2 (G^2 doubles: 32 KB at cfg4, 32 MB at
+  cfg5; one owner per position, so the sum is exact) is all-reduced and the
+  same tier sums as ``_from_blocks`` (quadtree.py:188-192) give every rank
+  the whole matrix's pyramid, so every rank culls exactly like one GPU would.
+  The K4z row scales are all-reduced with MAX for the same reason.
+* **Cull and gather.**  A rank culls only its own C segment (the upper
+  blocks of it on the symmetric path; a mirror ulp tie anywhere makes every
+  rank take the full path, as one GPU would), lists the operand blocks its
+  tasks read, and fetches the ones it does not own from their owners: an
+  all-to-all of counts, keys and blocks (NCCL over NVLink on GPUs).
+* **Multiply, reduce four kinds of scalars.**  The leaf products of the
+  segment run locally with no C reduction across GPUs.  tr X, tr X^2 (per
+  diagonal block, summed in block order) and the idempotency residual (leaf
+  tier of ||X^2 - X||^2, its root taken in the pyramid's order) are one
+  all-reduce, so the branch and convergence decisions are bitwise the single
+  GPU's.
+* **Persistence load balancing.**  The per-C-block task counts of this
+  iteration (all-reduced) cut the next iteration's segments; blocks whose
+  owner changed move with one all-to-all.
+
+The result is bitwise the single-GPU ``sp2_solve`` (same task sets, same
+per-block products and reductions).  ``engine`` isolates the device work:
+:class:`DeviceShardEngine` calls the sm_100a library; the CPU tests supply
+an oracle-backed engine and run the same driver under gloo.
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+__all__ = ["Comm", "owners", "pyramid_root2", "seq_sum", "DistributedSP2", "DistResult",
+           "DeviceShardEngine", "partition_work", "even_cuts"]
+
+UPPER, POS = "upper", "pos"
+
+
+# ---------------------------------------------------------------------------
+# helpers (host logic shared with parallel.py)
+# ---------------------------------------------------------------------------
+
+def even_cuts(n_pos: int, world: int) -> list:
+    """Equal-length Morton segments [cuts[r], cuts[r+1])."""
+    return [(n_pos * r) // world for r in range(world + 1)]
+
+
+def partition_work(work, world: int) -> list:
+    """Cut a Morton-indexed work vector into ``world`` contiguous segments of
+    (nearly) equal total work: cut r is the first position whose inclusive
+    prefix sum reaches r/world of the total (deterministic on every rank)."""
+    work = np.asarray(work, dtype=np.int64).reshape(-1)
+    n = len(work)
+    total = int(work.sum())
+    if total == 0 or world == 1:
+        return even_cuts(n, world)
+    csum = np.cumsum(work)
+    cuts = [0]
+    for r in range(1, world):
+        target = (total * r + world - 1) // world
+        pos = int(np.searchsorted(csum, target, side="left")) + 1
+        cuts.append(min(max(pos, cuts[-1]), n))
+    cuts.append(n)
+    return cuts
+
+
+def _spread(x):
+    x = (x | (x << 16)) & 0x0000FFFF0000FFFF
+    x = (x | (x << 8)) & 0x00FF00FF00FF00FF
+    x = (x | (x << 4)) & 0x0F0F0F0F0F0F0F0F
+    x = (x | (x << 2)) & 0x3333333333333333
+    return (x | (x << 1)) & 0x5555555555555555
+
+
+def owners(keys, g: int, cuts, mode: str):
+    """Owner rank of the blocks ``keys`` (bi * G + bj; torch int64, any
+    device): the segment holding the Morton position of (bi, bj) (``POS``)
+    or of (min, max) (``UPPER``: a block and its mirror share an owner)."""
+    import torch
+    i, j = keys // g, keys % g
+    if mode == UPPER:
+        i, j = torch.minimum(i, j), torch.maximum(i, j)
+    pos = (_spread(i) << 1) | _spread(j)
+    inner = torch.as_tensor(list(cuts[1:-1]), dtype=torch.int64, device=keys.device)
+    return torch.searchsorted(inner, pos, right=True)
+
+
+def seq_sum(v) -> float:
+    """Sequential sum in index order (trace: quadtree.py:305's block order)."""
+    t = 0.0
+    for x in np.asarray(v, dtype=np.float64).tolist():
+        t = t + x
+    return t
+
+
+def pyramid_root2(leaf) -> float:
+    """Root norm^2 of a pyramid built from a G x G leaf tier of norm^2 with
+    the tier sums of _from_blocks (quadtree.py:188-192): (c00 + c01) +
+    (c10 + c11), the root as ((c00 + c01) + c10) + c11 (numpy's contiguous
+    run)."""
+    a = np.asarray(leaf, dtype=np.float64)
+    g = int(round(np.sqrt(a.size)))
+    a = a.reshape(g, g)
+    while a.shape[0] > 1:
+        h = a.shape[0] // 2
+        q = a.reshape(h, 2, h, 2)
+        if h == 1:
+            a = ((q[:, 0, :, 0] + q[:, 0, :, 1]) + q[:, 1, :, 0]) + q[:, 1, :, 1]
+        else:
+            a = (q[:, 0, :, 0] + q[:, 0, :, 1]) + (q[:, 1, :, 0] + q[:, 1, :, 1])
+    return float(a[0, 0])
+
+
+class Comm:
+    """torch.distributed collectives with the world-size-1 shortcuts.  With
+    the gloo backend (the CPU tests, and one-GPU multi-process tests) device
+    tensors travel through host memory; with NCCL host tensors travel through
+    the device.  ``calls`` / ``bytes`` count what went over the wire."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.group = group
+        self.on = dist.is_available() and dist.is_initialized()
+        self.rank = dist.get_rank(group) if self.on else 0
+        self.world = dist.get_world_size(group) if self.on else 1
+        self.gloo = self.on and dist.get_backend(group) == "gloo"
+        self.calls = 0
+        self.bytes = 0
+
+    def _io(self, t):
+        """(tensor on the backend's device, device to return to or None)."""
+        import torch
+        if self.gloo and t.is_cuda:
+            return t.cpu(), t.device
+        if not self.gloo and not t.is_cuda:
+            return t.to(torch.device("cuda", torch.cuda.current_device())), t.device
+        return t, None
+
+    @staticmethod
+    def _back(t, dev):
+        return t.to(dev) if dev is not None else t
+
+    def _reduce(self, t, op):
+        import torch.distributed as dist
+        if self.world == 1:
+            return t
+        self.calls += 1
+        self.bytes += t.numel() * t.element_size()
+        x, dev = self._io(t.contiguous())
+        dist.all_reduce(x, op=op, group=self.group)
+        return self._back(x, dev)
+
+    def all_sum(self, t):
+        import torch.distributed as dist
+        return self._reduce(t, dist.ReduceOp.SUM)
+
+    def all_max(self, t):
+        import torch.distributed as dist
+        return self._reduce(t, dist.ReduceOp.MAX)
+
+    def all_min(self, t):
+        import torch.distributed as dist
+        return self._reduce(t, dist.ReduceOp.MIN)
+
+    def all_to_all_rows(self, send, send_counts):
+        """Rows of ``send`` grouped by destination rank (``send_counts`` per
+        rank, a python list) -> (the rows every rank sent here, by source
+        rank; the per-source counts)."""
+        import torch
+        import torch.distributed as dist
+        if self.world == 1:
+            return send, list(send_counts)
+        shape = tuple(send.shape[1:])
+        row = int(np.prod(shape)) if shape else 1
+        flat, dev = self._io(send.reshape(-1).contiguous())
+        sc = torch.tensor([int(c) for c in send_counts], dtype=torch.int64, device=flat.device)
+        rc = torch.empty_like(sc)
+        dist.all_to_all_single(rc, sc, group=self.group)
+        recv_counts = [int(v) for v in rc.tolist()]
+        out = torch.empty(sum(recv_counts) * row, dtype=send.dtype, device=flat.device)
+        dist.all_to_all_single(out, flat, output_split_sizes=[c * row for c in recv_counts],
+                               input_split_sizes=[int(c) * row for c in send_counts],
+                               group=self.group)
+        self.calls += 2
+        self.bytes += flat.numel() * flat.element_size()
+        return self._back(out, dev).reshape((-1,) + shape), recv_counts
+
+    def all_gather_rows(self, t):
+        """Concatenate every rank's rows (variable counts), rank order."""
+        import torch
+        import torch.distributed as dist
+        if self.world == 1:
+            return t
+        x, dev = self._io(t.contiguous())
+        n = torch.tensor([x.shape[0]], dtype=torch.int64, device=x.device)
+        sizes = [torch.zeros_like(n) for _ in range(self.world)]
+        dist.all_gather(sizes, n, group=self.group)
+        sizes = [int(v) for v in sizes]
+        pad = torch.zeros((max(sizes),) + tuple(x.shape[1:]), dtype=x.dtype, device=x.device)
+        pad[: x.shape[0]] = x
+        parts = [torch.empty_like(pad) for _ in range(self.world)]
+        dist.all_gather(parts, pad, group=self.group)
+        return self._back(torch.cat([p[:v] for p, v in zip(parts, sizes)]), dev)
+
+
+# ---------------------------------------------------------------------------
+# the driver
+# ---------------------------------------------------------------------------
+
+@dataclass
+class DistResult:
+    x: object                       # this rank's blocks of P
+    iteration: int = 0
+    converged: bool = False
+    trace_history: list = field(default_factory=list)
+    branch_history: list = field(default_factory=list)
+    idempotency_history: list = field(default_factory=list)
+    branch_margins: list = field(default_factory=list)
+    leaf_products: list = field(default_factory=list)    # whole product, per multiply
+    local_executed: list = field(default_factory=list)   # leaf products this rank ran
+    cuts_history: list = field(default_factory=list)
+    mode_history: list = field(default_factory=list)
+    halo_blocks: list = field(default_factory=list)      # operand blocks fetched per multiply
+    moved_blocks: list = field(default_factory=list)     # blocks re-homed by the rebalance
+    owned_blocks: list = field(default_factory=list)
+    seconds_per_iteration: list = field(default_factory=list)
+    cuts: list = field(default_factory=list)
+    mode: str = POS
+    symmetric: bool = False
+    leaf: object = None             # global leaf tier of norm^2 of x
+
+
+class DistributedSP2:
+    """SP2 with X, X^2 and 2X - X^2 Morton-sharded over a process group."""
+
+    def __init__(self, engine, group=None):
+        self.engine = engine
+        self.comm = Comm(group)
+        self.rank, self.world = self.comm.rank, self.comm.world
+
+    # -- data movement -------------------------------------------------------
+    def redistribute(self, m, g: int, cuts, mode: str):
+        """Move every block of the local matrix ``m`` to its owner under
+        (cuts, mode); returns the new local matrix and the blocks sent."""
+        import torch
+        eng = self.engine
+        keys = eng.keys(m)
+        dest = owners(keys, g, cuts, mode)
+        stay = dest == self.rank
+        if self.world == 1:
+            return m, 0
+        go = ~stay
+        order = torch.argsort(dest[go], stable=True)
+        sk = keys[go][order]
+        sb = eng.blocks(m)[go][order]
+        counts = torch.bincount(dest[go], minlength=self.world).tolist()
+        rk, _ = self.comm.all_to_all_rows(sk, counts)
+        rb, _ = self.comm.all_to_all_rows(sb, counts)
+        out = eng.rebuild(m, keys[stay], eng.blocks(m)[stay], rk, rb)
+        return out, int(go.sum())
+
+    def _globalize(self, x, sym: bool):
+        """All-reduce the leaf tier (and the K4z row scales) and install them."""
+        eng = self.engine
+        leaf = self.comm.all_sum(eng.leaf_norms2(x))
+        eng.install_pyramid(x, leaf, sym)
+        ex = eng.oz_exponents(x)
+        if ex is not None:
+            ex = tuple(self.comm.all_max(e) if e is not None else None for e in ex)
+        return leaf, ex
+
+    def _halo(self, x, g, cuts, mode, tau, lo, hi, sym):
+        """Fetch the operand blocks this rank's tasks read from their owners."""
+        import torch
+        eng = self.engine
+        ti, tk, tj = eng.tasks(x, tau, lo, hi, sym)
+        parts = [ti * g + tk, tk * g + tj]
+        if sym:
+            parts.append(tj * g + tk)      # K4z's B operand on the symmetric path: X_jk^T
+        need = torch.unique(torch.cat(parts)) if len(ti) else parts[0]
+        own = owners(need, g, cuts, mode)
+        remote = own != self.rank
+        req, req_owner = need[remote], own[remote]
+        order = torch.argsort(req_owner, stable=True)
+        req, req_owner = req[order], req_owner[order]
+        counts = torch.bincount(req_owner, minlength=self.world).tolist()
+        wanted, rc = self.comm.all_to_all_rows(req, counts)     # keys others need from me
+        blocks = eng.gather(x, wanted)
+        got, _ = self.comm.all_to_all_rows(blocks, rc)
+        return req, got
+
+    # -- solve ---------------------------------------------------------------
+    def solve(self, f, n_occ, tau: float, max_iter: int = 100, criterion: str = "fro",
+              fro_tol: float = 1e-6, idem_tol: float = 1e-9, balance: str = "persistence"):
+        """``f`` replicated on every rank (Gershgorin bounds and X0 bitwise
+        the single GPU's, then each rank keeps its own blocks of X0)."""
+        eng = self.engine
+        g = eng.grid(f)
+        bounds = eng.gershgorin(f)
+        x0 = eng.sp2_init(f, bounds)
+        sym = bool(eng.symmetric(x0))
+        mode = UPPER if sym else POS
+        # iteration 0 cut from a census of X0 * X0 (identical on every rank)
+        work0 = eng.census_work(x0, tau, sym)
+        cuts = partition_work(eng.to_numpy(work0), self.world) if balance != "even" else \
+            even_cuts(g * g, self.world)
+        x = eng.select(x0, owners(eng.keys(x0), g, cuts, mode) == self.rank)
+        del x0
+        return self._loop(x, g, cuts, mode, sym, n_occ, tau, max_iter, criterion, fro_tol,
+                          idem_tol, balance)
+
+    def solve_sharded(self, x, g: int, cuts, mode: str, sym: bool, n_occ, tau: float,
+                      max_iter: int = 100, criterion: str = "fro", fro_tol: float = 1e-6,
+                      idem_tol: float = 1e-9, balance: str = "persistence"):
+        """Start from a local shard of X0 (owned under (cuts, mode)) -- the
+        path for operands no GPU can hold (config 5)."""
+        return self._loop(x, g, cuts, mode, sym, n_occ, tau, max_iter, criterion, fro_tol,
+                          idem_tol, balance)
+
+    def _loop(self, x, g, cuts, mode, sym, n_occ, tau, max_iter, criterion, fro_tol,
+              idem_tol, balance):
+        import torch
+        eng, comm = self.engine, self.comm
+        want_idem = criterion == "fro"
+        res = DistResult(x=x)
+        leaf, ex = self._globalize(x, sym)
+        tr_pending = False
+        for it in range(max_iter):
+            t0 = time.perf_counter()
+            res.cuts_history.append(list(cuts))
+            res.mode_history.append(mode)
+            res.owned_blocks.append(eng.count(x))
+            lo, hi = cuts[self.rank], cuts[self.rank + 1]
+            # one symmetric-path decision for the whole grid (a mirror ulp tie
+            # anywhere sends every rank down the full path, as on one GPU)
+            sym_eff = sym
+            if sym:
+                ok = eng.census_symmetric_ok(x, tau, lo, hi)
+                sym_eff = bool(comm.all_min(torch.tensor([1 if ok else 0],
+                                                         dtype=torch.int64)).item())
+            mode_c = UPPER if sym_eff else POS
+            req, got = self._halo(x, g, cuts, mode, tau, lo, hi, sym_eff)
+            res.halo_blocks.append(int(req.numel()))
+            ext = eng.extend(x, req, got, leaf, sym_eff, ex)
+            c, work, leaf_r, exec_r = eng.multiply_range(ext, tau, lo, hi, sym_eff)
+            del ext
+            res.local_executed.append(int(exec_r))
+            if mode != mode_c:                      # symmetry lost: re-home X by position
+                x, _ = self.redistribute(x, g, cuts, mode_c)
+                mode = mode_c
+            # traces (per diagonal block) + residual leaf tier + counts: one all-reduce
+            parts = [eng.diag_traces(x), eng.diag_traces(c)]
+            if want_idem:
+                parts.append(eng.residual_leaf_norms2(c, x))
+            vec = comm.all_sum(torch.cat([p.to(torch.float64) for p in parts]))
+            vec = eng.to_numpy(vec)
+            t_x, t_sq = seq_sum(vec[:g]), seq_sum(vec[g:2 * g])
+            idem = float(np.sqrt(pyramid_root2(vec[2 * g:]))) if want_idem else None
+            cnt = comm.all_sum(torch.tensor([int(leaf_r)], dtype=torch.int64))
+            res.leaf_products.append(int(cnt.item()))
+            if it == 0 or tr_pending:           # tr of X0, then of every accepted X
+                res.trace_history.append(t_x)
+                tr_pending = False
+            t_ex = 2.0 * t_x - t_sq
+            square = abs(t_sq - n_occ) <= abs(t_ex - n_occ)            # sp2.py:97-99
+            res.branch_margins.append(abs(t_ex - n_occ) - abs(t_sq - n_occ))
+            if want_idem:
+                res.idempotency_history.append(idem)
+                done = idem < fro_tol
+            else:
+                done = abs(t_sq - t_x) < idem_tol and abs(t_x - n_occ) < 1e-6 * n_occ
+            if done:
+                res.converged = True
+                res.seconds_per_iteration.append(time.perf_counter() - t0)
+                break
+            x = c if square else eng.expand(x, c)
+            sym = sym_eff
+            res.iteration += 1
+            res.branch_history.append("SQUARE" if square else "EXPAND")
+            tr_pending = True
+            # persistence load balancing: next cut from this iteration's counts
+            if balance == "persistence" and self.world > 1:
+                w = comm.all_sum(work.to(torch.int64))
+                new_cuts = partition_work(eng.to_numpy(w), self.world)
+                if new_cuts != cuts:
+                    x, moved = self.redistribute(x, g, new_cuts, mode)
+                    res.moved_blocks.append(moved)
+                    cuts = new_cuts
+            leaf, ex = self._globalize(x, sym)
+            res.seconds_per_iteration.append(time.perf_counter() - t0)
+        if tr_pending:
+            vec = eng.to_numpy(comm.all_sum(eng.diag_traces(x).to(torch.float64)))
+            res.trace_history.append(seq_sum(vec[:g]))
+        res.x, res.cuts, res.mode, res.symmetric, res.leaf = x, cuts, mode, sym, leaf
+        return res
+
+    def gather(self, res):
+        """The whole P on every rank (tests / small problems)."""
+        eng = self.engine
+        keys = self.comm.all_gather_rows(eng.keys(res.x))
+        blocks = self.comm.all_gather_rows(eng.blocks(res.x))
+        return eng.assemble(res.x, keys, blocks)
+
+
+# ---------------------------------------------------------------------------
+# device engine (libspamm_b200)
+# ---------------------------------------------------------------------------
+
+class DeviceShardEngine:
+    """The driver's device work on one GPU per rank (libspamm_b200)."""
+
+    def __init__(self, kernel: str = "auto"):
+        self.kernel = kernel
+
+    # -- access ---------------------------------------------------------------
+    def grid(self, m):
+        return m.n_blocks
+
+    def count(self, m):
+        return int(m.stored_leaf_count)
+
+    def keys(self, m):
+        return m.keys_device()
+
+    def blocks(self, m):
+        return m.blocks_device()
+
+    def to_numpy(self, t):
+        return t.detach().cpu().numpy()
+
+    def _from_blocks(self, like, keys, blocks):
+        import torch
+
+        from .quadtree import QuadTreeMatrix
+        nb = like.block_size
+        return QuadTreeMatrix.from_blocks(like.n_native, nb, like.chunk_size,
+                                          keys.to(torch.int64).contiguous(),
+                                          blocks.reshape(-1, nb, nb).contiguous(), like.depth)
+
+    def select(self, m, mask):
+        return self._from_blocks(m, self.keys(m)[mask], self.blocks(m)[mask])
+
+    def rebuild(self, m, keys, blocks, more_keys, more_blocks):
+        import torch
+        return self._from_blocks(m, torch.cat([keys, more_keys.to(keys.device)]),
+                                 torch.cat([blocks, more_blocks.to(blocks.device)]))
+
+    def assemble(self, like, keys, blocks):
+        return self._from_blocks(like, keys, blocks)
+
+    def gather(self, m, keys):
+        import torch
+        nb = m.block_size
+        if keys.numel() == 0:
+            return torch.empty((0, nb, nb), dtype=torch.float64, device="cuda")
+        own = self.keys(m)
+        order = torch.argsort(own)
+        pos = torch.searchsorted(own[order], keys.to(own.device))
+        pos = order[pos.clamp(max=own.numel() - 1)]
+        if not bool((own[pos] == keys.to(own.device)).all()):
+            raise RuntimeError("DistributedSP2: a requested block is not owned by this rank")
+        return self.blocks(m)[pos].contiguous()
+
+    # -- replicated start ------------------------------------------------------
+    def gershgorin(self, f):
+        from .sp2 import _reserve_for, gershgorin_bounds
+        _reserve_for(f)
+        return gershgorin_bounds(f)
+
+    def sp2_init(self, f, bounds):
+        from .sp2 import sp2_init
+        return sp2_init(f, bounds)
+
+    def symmetric(self, m):
+        return bool(m.symmetric)
+
+    # -- global structure --------------------------------------------------------
+    def leaf_norms2(self, m):
+        return m.leaf_norms2_device()
+
+    def install_pyramid(self, m, leaf, sym):
+        m.set_global_pyramid(leaf, sym)
+
+    def _ozaki(self, m):
+        return self.kernel in ("auto", "ozaki") and m.block_size in (32, 64)
+
+    def oz_exponents(self, m):
+        """K4z row exponents (and column ones; equal for a symmetric X but
+        computed anyway -- the product may leave the symmetric path)."""
+        import torch
+
+        from . import _native as nat
+        if not self._ozaki(m):
+            return None
+        out = []
+        for by_col in (0, 1):
+            ex = torch.empty(m.n_blocks * m.block_size, dtype=torch.int32, device="cuda")
+            nat.check(nat.load().spamm_mat_oz_exponents(m._h, by_col, ex.data_ptr(),
+                                                        nat.current_stream()))
+            out.append(ex)
+        return tuple(out)
+
+    def _set_sym(self, on: bool):
+        from . import _native as nat
+        nat.check(nat.load().spamm_set_symmetric_products(1 if on else 0))
+
+    # -- products ----------------------------------------------------------------
+    def census_work(self, m, tau, sym):
+        import ctypes
+
+        import torch
+
+        from . import _native as nat
+        g = m.n_blocks
+        work = torch.zeros(g * g, dtype=torch.int32, device="cuda")
+        st = nat.Stats()
+        self._set_sym(sym)
+        try:
+            nat.check(nat.load().spamm_census_range(m._h, m._h, float(tau), 0, g * g,
+                                                    work.data_ptr(), nat.current_stream(),
+                                                    ctypes.byref(st)))
+        finally:
+            self._set_sym(True)
+        return work.to(torch.int64)
+
+    def census_symmetric_ok(self, m, tau, lo, hi):
+        """Whether the symmetric cull holds on [lo, hi) (no mirror ulp tie)."""
+        import ctypes
+
+        from . import _native as nat
+        if hi <= lo:
+            return True
+        st = nat.Stats()
+        nat.check(nat.load().spamm_census_range(m._h, m._h, float(tau), int(lo), int(hi), None,
+                                                nat.current_stream(), ctypes.byref(st)))
+        return bool(st.symmetric)
+
+    def tasks(self, m, tau, lo, hi, sym):
+        import ctypes
+
+        import torch
+
+        from . import _native as nat
+        lib, stream = nat.load(), nat.current_stream()
+        empty = torch.empty(0, dtype=torch.int64, device="cuda")
+        if hi <= lo:
+            return empty, empty, empty
+        n = ctypes.c_int64()
+        self._set_sym(sym)
+        try:
+            nat.check(lib.spamm_tasks_range(m._h, m._h, float(tau), int(lo), int(hi), None, None,
+                                            None, 0, ctypes.byref(n), stream))
+            cap = int(n.value)
+            if cap == 0:
+                return empty, empty, empty
+            t = [torch.empty(cap, dtype=torch.int32, device="cuda") for _ in range(3)]
+            nat.check(lib.spamm_tasks_range(m._h, m._h, float(tau), int(lo), int(hi),
+                                            t[0].data_ptr(), t[1].data_ptr(), t[2].data_ptr(),
+                                            cap, ctypes.byref(n), stream))
+        finally:
+            self._set_sym(True)
+        return tuple(x.to(torch.int64) for x in t)
+
+    def extend(self, m, keys, blocks, leaf, sym, ex):
+        """The rank's operand: its own blocks plus the fetched ones, with the
+        whole matrix's pyramid, symmetry flag and K4z row scales (with
+        nothing fetched -- one rank -- the shard itself)."""
+        from . import _native as nat
+        if keys.numel():
+            ext = self.rebuild(m, self.keys(m), self.blocks(m), keys,
+                               blocks.reshape(-1, m.block_size, m.block_size))
+            ext.set_global_pyramid(leaf, sym)
+        else:
+            ext = m
+            if bool(m.symmetric) != bool(sym):
+                ext.set_global_pyramid(leaf, sym)
+        if ex is not None and self._ozaki(m):
+            row, col = ex
+            nat.check(nat.load().spamm_mat_set_oz_exponents(
+                ext._h, row.data_ptr(), col.data_ptr() if col is not None else None,
+                nat.current_stream()))
+        return ext
+
+    def multiply_range(self, m, tau, lo, hi, sym):
+        import ctypes
+
+        import torch
+
+        from . import _native as nat
+        from .kernel import _leaf_kernel
+        from .quadtree import QuadTreeMatrix
+        g = m.n_blocks
+        work = torch.zeros(g * g, dtype=torch.int32, device="cuda")
+        st = nat.Stats()
+        out = ctypes.c_void_p()
+        stream = nat.current_stream()
+        self._set_sym(sym)
+        try:
+            nat.check(nat.load().spamm_multiply_range(m._h, m._h, float(tau),
+                                                      _leaf_kernel(self.kernel), int(lo),
+                                                      int(hi), work.data_ptr(), stream,
+                                                      ctypes.byref(out), ctypes.byref(st)))
+        finally:
+            self._set_sym(True)
+        c = QuadTreeMatrix(out, stream)
+        return c, work, int(st.leaf_products), int(st.executed_products)
+
+    # -- SP2 pieces -------------------------------------------------------------
+    def diag_traces(self, m):
+        import torch
+
+        from . import _native as nat
+        out = torch.empty(m.n_blocks, dtype=torch.float64, device="cuda")
+        nat.check(nat.load().spamm_mat_diag_traces(m._h, out.data_ptr(), nat.current_stream()))
+        return out
+
+    def residual_leaf_norms2(self, c, x):
+        from .quadtree import add_scaled
+        return add_scaled(1.0, c, -1.0, x).leaf_norms2_device()
+
+    def expand(self, x, c):
+        from .quadtree import add_scaled
+        return add_scaled(2.0, x, -1.0, c)

@@ -1,0 +1,331 @@
+"""Distributed SP2 (paper_1403_7458_b200/dist.py) host logic on CPU: gloo,
+world sizes 2 and 3, an oracle-backed engine standing in for the GPUs.
+
+X, X^2 and the update stay sharded along the Morton curve (no rank holds X
+after the start), the halo is fetched by all-to-all, the scalars come from
+one all-reduce, and the cut moves with the previous iteration's work
+(persistence load balancing).  The trajectory and the final P must equal the
+single-process oracle SP2 bitwise -- also when the symmetric path is dropped
+mid-solve (a mirror ulp tie on one rank) and for an F that is symmetric only
+to within sym_tol (position ownership from the start)."""
+
+import os
+import socket
+from dataclasses import dataclass
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import spamm_oracle as O
+from paper_1403_7458_b200.dist import (POS, UPPER, DistributedSP2, even_cuts, owners,
+                                       partition_work, pyramid_root2, seq_sum)
+from paper_1403_7458_b200.synth import water_cluster
+from paper_1403_7458_b200.synth_morton import morton_keys
+
+
+@dataclass
+class Loc:
+    m: O.OMatrix
+    sym: bool = False
+
+
+def _leaf2(m: O.OMatrix):
+    g = m.n_blocks
+    leaf = np.zeros(g * g)
+    if len(m.keys):
+        leaf[m.keys] = O.leaf_norms2_recipe(m.data)
+    return leaf
+
+
+class OracleDistEngine:
+    """CPU engine with the device engine's semantics: a rank's product is its
+    C segment (upper blocks + mirrors on the symmetric path)."""
+
+    def __init__(self, tie_at=None):
+        self.tie_at = tie_at        # (rank, call index): report a mirror ulp tie there
+        self.calls = 0
+
+    # access
+    def grid(self, x):
+        return getattr(x, "m", x).n_blocks
+
+    def count(self, x):
+        return len(x.m.keys)
+
+    def keys(self, x):
+        return torch.from_numpy(np.asarray(x.m.keys, dtype=np.int64))
+
+    def blocks(self, x):
+        return torch.from_numpy(np.ascontiguousarray(x.m.data))
+
+    def to_numpy(self, t):
+        return t.numpy()
+
+    def _mk(self, like, keys, data, sym=False):
+        keys = np.asarray(keys, dtype=np.int64)
+        data = np.asarray(data, dtype=np.float64).reshape(-1, like.m.block_size, like.m.block_size)
+        order = np.argsort(keys, kind="stable")
+        m = O.from_blocks(like.m.n_native, like.m.block_size, like.m.chunk_size, keys[order],
+                          data[order], like.m.depth)
+        return Loc(m, sym)
+
+    def select(self, x, mask):
+        mask = mask.numpy()
+        return self._mk(x, x.m.keys[mask], x.m.data[mask], x.sym)
+
+    def rebuild(self, x, keys, blocks, mk, mb):
+        return self._mk(x, np.concatenate([keys.numpy(), mk.numpy()]),
+                        np.concatenate([blocks.numpy(), mb.numpy().reshape(-1, *x.m.data.shape[1:])]),
+                        x.sym)
+
+    def assemble(self, like, keys, blocks):
+        return self._mk(like, keys.numpy(), blocks.numpy()).m
+
+    def gather(self, x, keys):
+        k = keys.numpy()
+        pos = np.searchsorted(x.m.keys, k)
+        assert np.array_equal(x.m.keys[np.minimum(pos, len(x.m.keys) - 1)], k), "not owned"
+        return torch.from_numpy(np.ascontiguousarray(x.m.data[pos]))
+
+    # replicated start
+    def gershgorin(self, f):
+        return O.gershgorin_bounds(f)
+
+    def sp2_init(self, f, bounds):
+        x = O.sp2_init(f, bounds)
+        d = O.to_dense(x)
+        return Loc(x, bool(np.array_equal(d, d.T)))
+
+    def symmetric(self, x):
+        return x.sym
+
+    # global structure
+    def leaf_norms2(self, x):
+        return torch.from_numpy(_leaf2(x.m))
+
+    def install_pyramid(self, x, leaf, sym):
+        g = x.m.n_blocks
+        x.m.tier_norms = O.pyramid_from_leaf_norms2(leaf.numpy().reshape(g, g))
+        x.sym = bool(sym)
+
+    def oz_exponents(self, x):
+        return None
+
+    # products
+    def _tasks(self, x, tau, lo, hi, sym):
+        g = x.m.n_blocks
+        _, _, ti, tk, tj = O.sweep(x.m.tier_norms, x.m.tier_norms, tau)
+        if sym:
+            keep = ti <= tj
+            ti, tk, tj = ti[keep], tk[keep], tj[keep]
+        mt = morton_keys(ti, tj)
+        keep = (mt >= lo) & (mt < hi)
+        return ti[keep], tk[keep], tj[keep]
+
+    def census_work(self, x, tau, sym):
+        g = x.m.n_blocks
+        ti, _, tj = self._tasks(x, tau, 0, g * g, sym)
+        work = np.zeros(g * g, dtype=np.int64)
+        np.add.at(work, morton_keys(ti, tj), 1)
+        return torch.from_numpy(work)
+
+    def census_symmetric_ok(self, x, tau, lo, hi):
+        import torch.distributed as dist
+        self.calls += 1
+        if self.tie_at is not None and (dist.get_rank(), self.calls) == self.tie_at:
+            return False
+        g = x.m.n_blocks
+        _, _, ti, tk, tj = O.sweep(x.m.tier_norms, x.m.tier_norms, tau)
+        fwd = set(((ti * g + tk) * g + tj).tolist())
+        up = (ti < tj) & (morton_keys(ti, tj) >= lo) & (morton_keys(ti, tj) < hi)
+        a, k, b = ti[up], tk[up], tj[up]
+        if not all(((bb * g + kk) * g + aa) in fwd for aa, kk, bb in zip(a, k, b)):
+            return False
+        lw = (ti > tj) & (morton_keys(tj, ti) >= lo) & (morton_keys(tj, ti) < hi)
+        a, k, b = ti[lw], tk[lw], tj[lw]
+        return all(((bb * g + kk) * g + aa) in fwd for aa, kk, bb in zip(a, k, b))
+
+    def tasks(self, x, tau, lo, hi, sym):
+        return tuple(torch.from_numpy(v) for v in self._tasks(x, tau, lo, hi, sym))
+
+    def extend(self, x, keys, blocks, leaf, sym, ex):
+        ext = self.rebuild(x, self.keys(x), self.blocks(x), keys, blocks)
+        self.install_pyramid(ext, leaf, sym)
+        return ext
+
+    def multiply_range(self, x, tau, lo, hi, sym):
+        m = x.m
+        g, nb = m.n_blocks, m.block_size
+        ti, tk, tj = self._tasks(x, tau, lo, hi, sym)
+        work = np.zeros(g * g, dtype=np.int64)
+        np.add.at(work, morton_keys(ti, tj), 1)
+        a_pos = np.searchsorted(m.keys, ti * g + tk)
+        b_pos = np.searchsorted(m.keys, tk * g + tj)
+        assert np.array_equal(m.keys[np.minimum(a_pos, len(m.keys) - 1)], ti * g + tk)
+        assert np.array_equal(m.keys[np.minimum(b_pos, len(m.keys) - 1)], tk * g + tj)
+        ckeys, c_pos = np.unique(ti * g + tj, return_inverse=True)
+        c = np.zeros((len(ckeys), nb, nb))
+        order = np.lexsort((tk, c_pos))
+        O.gemm_batch(a_pos[order], b_pos[order], c_pos[order], m.data, m.data, c)
+        keys, data = [ckeys], [c]
+        full = len(ti)
+        if sym:
+            ci, cj = ckeys // g, ckeys % g
+            mir = ci != cj
+            keys.append(cj[mir] * g + ci[mir])
+            data.append(np.transpose(c[mir], (0, 2, 1)))
+            full = 2 * len(ti) - int((ti == tj).sum())
+        out = self._mk(x, np.concatenate(keys), np.concatenate(data), sym)
+        return out, torch.from_numpy(work), full, len(ti)
+
+    # SP2 pieces
+    def diag_traces(self, x):
+        m = x.m
+        g = m.n_blocks
+        out = np.zeros(g)
+        for s, key in enumerate(m.keys):
+            bi, bj = divmod(int(key), g)
+            if bi == bj:
+                acc = 0.0
+                for d in range(m.block_size):
+                    acc = acc + float(m.data[s, d, d])
+                out[bi] = acc
+        return torch.from_numpy(out)
+
+    def residual_leaf_norms2(self, c, x):
+        return torch.from_numpy(_leaf2(O.add_scaled(1.0, c.m, -1.0, x.m)))
+
+    def expand(self, x, c):
+        return Loc(O.add_scaled(2.0, x.m, -1.0, c.m), x.sym and c.sym)
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, h, n_occ, nb, tau, out_dir, tie_at):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        f = O.from_dense(h, nb)
+        drv = DistributedSP2(OracleDistEngine(tie_at))
+        res = drv.solve(f, n_occ, tau, criterion="fro")
+        p = drv.gather(res)
+        np.savez(os.path.join(out_dir, f"rank{rank}.npz"), p=O.to_dense(p),
+                 traces=np.array(res.trace_history), iters=res.iteration,
+                 idem=np.array(res.idempotency_history), leaf=np.array(res.leaf_products),
+                 branches=np.array([b == "SQUARE" for b in res.branch_history]),
+                 bmargin=np.array(res.branch_margins),
+                 cuts=np.array(res.cuts_history), modes=np.array(res.mode_history),
+                 exec=np.array(res.local_executed), halo=np.array(res.halo_blocks),
+                 moved=np.array(res.moved_blocks, dtype=np.int64),
+                 owned=np.array(res.owned_blocks), total=len(f.keys))
+    finally:
+        dist.destroy_process_group()
+
+
+def _run(tmp_path, world, h, n_occ, nb, tau, tie_at=None):
+    port = _free_port()
+    torch.multiprocessing.spawn(_worker, args=(world, port, h, n_occ, nb, tau, str(tmp_path),
+                                               tie_at), nprocs=world, join=True)
+    return [np.load(tmp_path / f"rank{r}.npz") for r in range(world)]
+
+
+def _check_bitwise(outs, ref):
+    for o in outs:
+        assert int(o["iters"]) == ref.iterations
+        assert np.array_equal(o["traces"], np.array(ref.trace_history))
+        assert np.array_equal(o["idem"], np.array(ref.idem_history))
+        assert np.array_equal(o["bmargin"], np.array(ref.branch_margins))
+        assert list(o["branches"]) == [b == O.SQUARE for b in ref.branches]
+        assert list(o["leaf"]) == ref.leaf_products
+        assert np.array_equal(o["p"], O.to_dense(ref.x))
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_distributed_sp2_gloo_bitwise_single_process(tmp_path, world):
+    h, n_occ = water_cluster(16, seed=5)
+    nb, tau = 16, 1e-6
+    ref = O.sp2_solve(O.from_dense(h, nb), n_occ, tau, criterion="fro")
+    outs = _run(tmp_path, world, h, n_occ, nb, tau)
+    _check_bitwise(outs, ref)
+    o = outs[0]
+    assert all((x == UPPER) for x in o["modes"])                  # symmetric throughout
+    assert all(np.array_equal(o["cuts"], p["cuts"]) for p in outs)
+    # X stays distributed: no rank owns more than its share plus a margin
+    for p in outs:
+        assert p["owned"].max() < 0.75 * int(p["total"]) + 8
+        assert p["halo"].sum() > 0 and p["exec"].sum() > 0
+    # persistence LB: the cut follows the measured work, blocks move with it
+    assert any(not np.array_equal(o["cuts"][0], c) for c in o["cuts"][1:])
+    assert sum(int(p["moved"].sum()) for p in outs) > 0
+    ex = np.array([p["exec"] for p in outs])                      # (world, iterations)
+    assert (ex.max(axis=0) - ex.min(axis=0) <= 0.35 * ex.mean(axis=0) + 64).all()
+
+
+def test_distributed_sp2_symmetric_path_lost_midway(tmp_path):
+    """A mirror ulp tie reported by rank 1 at its 4th multiply: every rank
+    takes the full path from then on, X is re-homed by position, and the
+    result is still bitwise the single process's (the symmetric path is
+    bitwise the full path)."""
+    h, n_occ = water_cluster(16, seed=5)
+    nb, tau = 16, 1e-6
+    ref = O.sp2_solve(O.from_dense(h, nb), n_occ, tau, criterion="fro")
+    outs = _run(tmp_path, 2, h, n_occ, nb, tau, tie_at=(1, 4))
+    _check_bitwise(outs, ref)
+    modes = list(outs[0]["modes"])
+    assert modes[:4] == [UPPER] * 4 and all(m == POS for m in modes[4:])
+
+
+def test_distributed_sp2_nearly_symmetric_f_uses_position_ownership(tmp_path):
+    h, n_occ = water_cluster(16, seed=6)
+    h = h.copy()
+    h[3, 40] += 1e-13                       # |F - F^T| = 1e-13 < sym_tol: not bitwise symmetric
+    nb, tau = 16, 1e-6
+    ref = O.sp2_solve(O.from_dense(h, nb), n_occ, tau, criterion="fro")
+    outs = _run(tmp_path, 2, h, n_occ, nb, tau)
+    _check_bitwise(outs, ref)
+    assert all(m == POS for m in outs[0]["modes"])
+
+
+# -- host helpers ---------------------------------------------------------------
+
+def test_owners_upper_mode_pairs_mirrors_and_tiles_positions():
+    g = 32
+    i, j = np.meshgrid(np.arange(g), np.arange(g), indexing="ij")
+    k = torch.from_numpy((i * g + j).ravel())
+    km = torch.from_numpy((j * g + i).ravel())
+    cuts = [0, 170, 600, g * g]
+    assert torch.equal(owners(k, g, cuts, UPPER), owners(km, g, cuts, UPPER))
+    own = owners(k, g, cuts, POS).numpy()
+    pos = morton_keys(i.ravel(), j.ravel())
+    for r in range(3):
+        assert np.array_equal(own == r, (pos >= cuts[r]) & (pos < cuts[r + 1]))
+
+
+def test_pyramid_root_and_seq_sum_match_oracle(rng):
+    for g in (1, 2, 4, 16):
+        leaf = np.abs(rng.standard_normal((g, g))) * np.exp(rng.standard_normal((g, g)) * 5)
+        assert np.sqrt(pyramid_root2(leaf)) == O.pyramid_from_leaf_norms2(leaf)[0][0, 0]
+    v = rng.standard_normal(100)
+    t = 0.0
+    for x in v:
+        t += x
+    assert seq_sum(v) == t
+
+
+def test_partition_work_properties():
+    rng = np.random.default_rng(0)
+    w = rng.integers(0, 50, 256)
+    for world in (1, 2, 3, 8):
+        cuts = partition_work(w, world)
+        assert cuts[0] == 0 and cuts[-1] == 256 and len(cuts) == world + 1
+        parts = [w[a:b].sum() for a, b in zip(cuts, cuts[1:])]
+        assert sum(parts) == w.sum()
+        assert max(parts) - w.sum() / world <= w.max()
+    assert partition_work(np.zeros(64, dtype=np.int64), 4) == even_cuts(64, 4)

@@ -84,7 +84,7 @@ def test_cfg4_x0_square_full_c_default_kernel():
     ox0 = O.sp2_init(of, O.gershgorin_bounds(of))
     assert np.array_equal(pyramid_flat(x0._tier_norms), pyramid_flat(ox0.tier_norms))
     st, _ = _check_product(x0, x0, ox0, ox0, cfg.tau)
-    assert st.symmetric and st.leaf_products == 140577
+    assert st.symmetric and st.leaf_products == int(golden("cfg4_sp2")["leaf_products"][0])
 
 
 @pytest.mark.parametrize("cfg_index", [3, 4])
