@@ -189,6 +189,26 @@ int spamm_sp2_multiply_shard(const spamm_mat* x, double tau, int32_t kernel, int
 int spamm_sp2_shard_finish(const spamm_mat* x, spamm_mat* c, double n_occ, int32_t want_idem,
                            void* stream, int32_t* branch, double* t_x, double* t_sq,
                            double* idem, spamm_mat** x_next);
+/* One SP2 iteration on this rank's Morton shard (multi-GPU, dist.py).
+ * `x` is the rank's share of X (the whole matrix's pyramid installed with
+ * spamm_mat_set_pyramid), `ext` its operand: x plus the fetched halo blocks
+ * (ext == x on one rank).  C = X^2 is computed for the C positions the rank
+ * owns -- Morton range [lo, hi) (hi < 0: all), on the symmetric path the
+ * upper positions in range plus their mirrors -- with `work` (optional,
+ * device int32[G*G], zeroed by the caller) receiving the task count per C
+ * position.  `allreduce` (NULL on one rank) sums a device double vector over
+ * the ranks in place on `stream`; it is called once, on [per-diagonal-block
+ * traces of X (G) | of X^2 (G) | leaf tier of ||X^2 - X||^2 (G*G)], from which
+ * tr X, tr X^2 and ||X^2 - X||_F of the WHOLE matrices follow in the orders
+ * of trace() and the pyramid (bitwise the single-GPU values).  Then the
+ * branch rule (sp2.py:97-99) and the fused update on the shard: *x_next =
+ * this rank's share of X^2 (SQUARE) or 2X - X^2 (EXPAND). */
+typedef int (*spamm_allreduce_fn)(void* ctx, double* buf, int64_t n, void* stream);
+int spamm_shard_sp2_step(const spamm_mat* ext, const spamm_mat* x, double n_occ, double tau,
+                         int32_t kernel, int64_t lo, int64_t hi, int32_t* work,
+                         int32_t want_idem, spamm_allreduce_fn allreduce, void* ctx,
+                         void* stream, spamm_mat** x_next, int32_t* branch, double* t_x,
+                         double* t_sq, double* idem, spamm_stats* stats);
 /* Pre-grow the library's stream-ordered memory pool by `bytes` (kept mapped),
  * so steady-state allocations never wait on a new device mapping. */
 int spamm_reserve_pool(int64_t bytes, void* stream);

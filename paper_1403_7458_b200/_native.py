@@ -67,6 +67,9 @@ class SideCopies(ctypes.Structure):
                 ("chunk_bytes", c_i64)]
 
 
+# multi-GPU all-reduce callback of spamm_shard_sp2_step (dist.py)
+ALLREDUCE_FN = ctypes.CFUNCTYPE(c_i32, c_vp, c_vp, c_i64, c_vp)
+
 _SIGS = {
     "spamm_abi_version": (c_i32, []),
     "spamm_last_error": (ctypes.c_char_p, []),
@@ -96,6 +99,11 @@ _SIGS = {
     "spamm_multiply_range": (c_i32, [c_vp, c_vp, c_f64, c_i32, c_i64, c_i64, c_vp, c_vp,
                                      ctypes.POINTER(c_vp), ctypes.POINTER(Stats)]),
     "spamm_reserve_pool": (c_i32, [c_i64, c_vp]),
+    "spamm_shard_sp2_step": (c_i32, [c_vp, c_vp, c_f64, c_f64, c_i32, c_i64, c_i64, c_vp, c_i32,
+                                     ALLREDUCE_FN, c_vp, c_vp, ctypes.POINTER(c_vp),
+                                     ctypes.POINTER(c_i32), ctypes.POINTER(c_f64),
+                                     ctypes.POINTER(c_f64), ctypes.POINTER(c_f64),
+                                     ctypes.POINTER(Stats)]),
     "spamm_sp2_multiply_shard": (c_i32, [c_vp, c_f64, c_i32, c_i32, c_i32, c_vp,
                                          ctypes.POINTER(c_vp), c_vp, ctypes.POINTER(Stats)]),
     "spamm_sp2_shard_finish": (c_i32, [c_vp, c_vp, c_f64, c_i32, c_vp, ctypes.POINTER(c_i32),

@@ -711,6 +711,22 @@ void multiply_impl(const spamm_mat* a, const spamm_mat* b, double tau, int32_t k
 }
 
 
+// Multi-GPU shard scalars from the all-reduced vector [diag X (G) | diag X^2
+// (G)]: tr X and tr X^2 as the sequential sums of the per-diagonal-block parts
+// in block order (trace(), quadtree.py:305); out[2] (the residual norm) is
+// the root of the D pyramid, written by the caller.
+__global__ void k_shard_traces(const double* __restrict__ vec, int64_t G, double* __restrict__ out) {
+  if (threadIdx.x == 0) {
+    double a = 0.0;
+    for (int64_t b = 0; b < G; ++b) a = __dadd_rn(a, vec[b]);
+    out[0] = a;
+  } else if (threadIdx.x == 32) {
+    double a = 0.0;
+    for (int64_t b = 0; b < G; ++b) a = __dadd_rn(a, vec[G + b]);
+    out[1] = a;
+  }
+}
+
 __global__ void k_iota64(int64_t* out, int64_t n) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
@@ -800,7 +816,10 @@ void multiply_shard_impl(const spamm_mat* a, double tau, int32_t kernel, cudaStr
 void sp2_finish(const spamm_mat* x, const spamm_mat* c, double n_occ, bool want_idem,
                 cudaStream_t s, bool* square_out, double* t_x, double* t_sq, double* idem,
                 spamm_mat** e_out, const double* idem_dev = nullptr,
-                spamm::IdemFuse* fused_union = nullptr, double* branch_margin = nullptr) {
+                spamm::IdemFuse* fused_union = nullptr, double* branch_margin = nullptr,
+                const double* given_dev = nullptr) {
+  // given_dev (multi-GPU shard): device [tr X, tr X^2, ||X^2 - X||_F] of the
+  // WHOLE matrices (all-reduced); x / c are then this rank's shards.
   const bool fused = spamm::sp2_fused_supported(x->m.nb);
   // One host sync (one gather launch) for tr(X), tr(X^2), the union size of
   // the update and X^2's kept-block count.  Traces computed by the small-tree
@@ -812,8 +831,13 @@ void sp2_finish(const spamm_mat* x, const spamm_mat* c, double n_occ, bool want_
     spamm::trace_launch(m, reinterpret_cast<double*>(scratch), s);
     return scratch;
   };
-  if (!x->m.tr_valid) src[0] = trace_src(x->m, sc);
-  src[1] = trace_src(c->m, sc + 1);
+  if (given_dev) {
+    src[0] = reinterpret_cast<const int64_t*>(given_dev);
+    src[1] = reinterpret_cast<const int64_t*>(given_dev + 1);
+  } else {
+    if (!x->m.tr_valid) src[0] = trace_src(x->m, sc);
+    src[1] = trace_src(c->m, sc + 1);
+  }
   spamm::UnionPrep prep;
   if (fused && fused_union && fused_union->ukeys) {  // built by X^2's finalisation
     prep.npos = x->m.G * x->m.G;
@@ -825,22 +849,29 @@ void sp2_finish(const spamm_mat* x, const spamm_mat* c, double n_occ, bool want_
     src[2] = sc + 2;
   }
   src[3] = spamm::pending_kept(c->m);  // lazy prune of X^2 rides along
-  src[4] = reinterpret_cast<const int64_t*>(idem_dev);  // fused ||X^2 - X||_F
+  src[4] = reinterpret_cast<const int64_t*>(given_dev ? given_dev + 2 : idem_dev);
   const bool has_kept = src[3] != nullptr;
   int64_t h[5];
   spamm::gather_sync(h, src, 5, s);
   spamm::htrace("fin_synced");
-  const bool idem_done = want_idem && idem_dev;
+  const bool idem_done = want_idem && (idem_dev || given_dev);
   if (idem_done) memcpy(idem, &h[4], sizeof(double));
   spamm::dfree(sc, s);
   if (has_kept) spamm::settle(const_cast<spamm_mat*>(c)->m, h[3], s);
-  if (!x->m.tr_valid) {
-    memcpy(&x->m.tr, &h[0], sizeof(double));
-    x->m.tr_valid = true;
+  double tx, tsq;
+  if (given_dev) {  // whole-matrix traces: not cached on the shards
+    memcpy(&tx, &h[0], sizeof(double));
+    memcpy(&tsq, &h[1], sizeof(double));
+  } else {
+    if (!x->m.tr_valid) {
+      memcpy(&x->m.tr, &h[0], sizeof(double));
+      x->m.tr_valid = true;
+    }
+    memcpy(&c->m.tr, &h[1], sizeof(double));
+    c->m.tr_valid = true;
+    tx = x->m.tr;
+    tsq = c->m.tr;
   }
-  memcpy(&c->m.tr, &h[1], sizeof(double));
-  c->m.tr_valid = true;
-  const double tx = x->m.tr, tsq = c->m.tr;
   // sp2.py:97-99: ties go to SQUARE.
   const double tex = 2.0 * tx - tsq;
   const bool square = std::fabs(tsq - n_occ) <= std::fabs(tex - n_occ);
@@ -900,6 +931,98 @@ int spamm_sp2_step(const spamm_mat* x, double n_occ, double tau, int32_t kernel,
   sp2_finish(x, c, n_occ, want_idem != 0, s, &square, &tx, &tsq, idem, &e, fuse.out, &fuse);
   spamm::dfree(fuse.out, s);
   spamm::dfree(fuse.ukeys, s);
+  if (e) {
+    c->m.release();
+    delete c;
+    *x_next = e;
+  } else {
+    *x_next = c;
+  }
+  *branch = square ? 0 : 1;
+  *t_x = tx;
+  *t_sq = tsq;
+  SPAMM_API_END
+}
+
+int spamm_shard_sp2_step(const spamm_mat* ext, const spamm_mat* x, double n_occ, double tau,
+                         int32_t kernel, int64_t lo, int64_t hi, int32_t* work,
+                         int32_t want_idem, spamm_allreduce_fn allreduce, void* ctx,
+                         void* stream, spamm_mat** x_next, int32_t* branch, double* t_x,
+                         double* t_sq, double* idem, spamm_stats* stats) {
+  if (int rc = check_conformable(ext, x)) return rc;
+  if (!x_next || !branch || !t_x || !t_sq || (want_idem && !idem))
+    return fail(SPAMM_EINVAL, "null argument");
+  if (!(tau >= 0.0) || tau == __builtin_inf())
+    return fail(SPAMM_EINVAL, "tau must be finite and >= 0, got " + std::to_string(tau));
+  if (kernel < 0 || kernel > 4) return fail(SPAMM_EINVAL, "unknown leaf kernel");
+  if (kernel == SPAMM_LEAF_OZAKI && !spamm::ozaki_supported(x->m.nb))
+    return fail(SPAMM_EINVAL, "INT8-sliced leaf kernel needs block size 32 or 64");
+  if (hi >= 0 && (lo < 0 || hi < lo || hi > x->m.G * x->m.G))
+    return fail(SPAMM_EINVAL, "shard range outside [0, G*G]");
+  if (allreduce && x->m.nb < 2) return fail(SPAMM_EINVAL, "sharded SP2 needs block size >= 2");
+  SPAMM_API_BEGIN
+  cudaStream_t s = S(stream);
+  const int64_t G = x->m.G;
+  auto* c = new spamm_mat();
+  spamm::IdemFuse fuse;
+  double* vec = nullptr;  // [diag X | diag X^2 | leaf ||X^2 - X||^2] (+ 3 scalars)
+  if (allreduce) vec = spamm::dmalloc<double>(2 * G + G * G + 3, s);
+  if (want_idem && spamm::idem_fusable(x->m)) {
+    fuse.x = &x->m;
+    fuse.out = spamm::dmalloc<double>(2, s);
+    fuse.ucount = reinterpret_cast<int64_t*>(fuse.out + 1);
+    fuse.ukeys = spamm::dmalloc<int64_t>(G * G, s);
+    if (vec) fuse.dleaf = vec + 2 * G;
+  }
+  try {
+    multiply_impl(ext, ext, tau, kernel, false, s, c->m, stats, hi >= 0 ? lo : 0, hi, work,
+                  true, fuse);
+  } catch (...) {
+    c->m.release();
+    delete c;
+    throw;
+  }
+  const double* given = nullptr;
+  if (vec) {
+    // this rank's parts, one all-reduce, then the whole matrices' scalars
+    spamm::diag_traces(x->m, vec, s);
+    spamm::diag_traces(c->m, vec + G, s);
+    if (want_idem && !fuse.dleaf) {  // unfused residual: materialise the shard's D
+      spamm::Mat d;
+      spamm::add_scaled(1.0, c->m, -1.0, x->m, d, s);
+      SPAMM_CK(cudaMemcpyAsync(vec + 2 * G, d.norms2 + spamm::tier_offset(d.depth),
+                               G * G * sizeof(double), cudaMemcpyDeviceToDevice, s));
+      d.release();
+    } else if (!want_idem) {
+      SPAMM_CK(cudaMemsetAsync(vec + 2 * G, 0, G * G * sizeof(double), s));
+    }
+    const int arc = allreduce(ctx, vec, 2 * G + G * G, stream);
+    if (arc != 0) throw std::runtime_error("sharded SP2: all-reduce callback failed");
+    double* out = vec + 2 * G + G * G;
+    k_shard_traces<<<1, 64, 0, s>>>(vec, G, out);
+    SPAMM_LAUNCH_CK();
+    if (want_idem) {  // the D pyramid's root, in the tier order of any other matrix
+      spamm::Mat d;
+      d.depth = x->m.depth;
+      d.G = G;
+      const int64_t ps = spamm::pyramid_size(d.depth);
+      d.norms = spamm::dmalloc<double>(ps, s);
+      d.norms2 = spamm::dmalloc<double>(ps, s);
+      spamm::set_leaf_pyramid(d, vec + 2 * G, s);
+      SPAMM_CK(cudaMemcpyAsync(out + 2, d.norms, sizeof(double), cudaMemcpyDeviceToDevice, s));
+      spamm::dfree(d.norms, s);
+      spamm::dfree(d.norms2, s);
+    }
+    given = out;
+  }
+  spamm_mat* e = nullptr;
+  bool square = true;
+  double tx = 0, tsq = 0;
+  sp2_finish(x, c, n_occ, want_idem != 0, s, &square, &tx, &tsq, idem, &e, fuse.out, &fuse,
+             nullptr, given);
+  spamm::dfree(fuse.out, s);
+  spamm::dfree(fuse.ukeys, s);
+  spamm::dfree(vec, s);
   if (e) {
     c->m.release();
     delete c;

@@ -403,9 +403,14 @@ __global__ void __launch_bounds__(CULL_THREADS)
                  int64_t* __restrict__ keys, int64_t* __restrict__ c_out,
                  int64_t* __restrict__ c_mirror, int32_t* __restrict__ order, int64_t Mn,
                  int64_t Vn, unsigned long long* __restrict__ aux, TieBand tb,
-                 unsigned long long* __restrict__ near, unsigned long long* __restrict__ margin) {
+                 unsigned long long* __restrict__ near, unsigned long long* __restrict__ margin,
+                 int64_t lo, int64_t hi, int32_t* __restrict__ work) {
   pdl_wait();
   const int64_t G = int64_t(1) << depth;
+  // Shard ownership (hi >= 0): the C positions whose Morton index lies in
+  // [lo, hi) -- on the symmetric path the upper positions in range plus their
+  // mirrors (a rank computes an upper block and writes its transpose).
+  auto in_range = [&](int64_t q) { return hi < 0 || (q >= lo && q < hi); };
   const int lane = threadIdx.x & 31;
   const unsigned lt_mask = (1u << lane) - 1u;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -416,7 +421,12 @@ __global__ void __launch_bounds__(CULL_THREADS)
     uint32_t ui, uj;
     morton_decode((uint64_t)m, ui, uj);
     const int64_t i = ui, j = uj;
-    const bool emitted = !sym || i <= j;
+    const bool owned = sym && i > j ? in_range((int64_t)morton_encode(uj, ui)) : in_range(m);
+    const bool emitted = owned && (!sym || i <= j);
+    if (!owned) {
+      if (!WRITE && lane == 0) cnt[m] = 0;
+      continue;
+    }
     int64_t toff = 0;
     if (WRITE) {
       const int64_t v = off[m], d = off[m + 1] - v;
@@ -468,6 +478,7 @@ __global__ void __launch_bounds__(CULL_THREADS)
     if (!WRITE && lane == 0) {
       cnt[m] = (emitted ? c + (c > 0 ? int64_t(1) << DT_NODE : 0) : 0) +
                (c > 0 ? int64_t(1) << DT_FULL : 0);
+      if (work && emitted && c) work[m] = (int32_t)c;  // persistence load balancing input
       full += c;
       if (c && emitted) atomicAdd(hist + (G - c), 1);
     }
@@ -510,7 +521,9 @@ __global__ void k_shard_cuts(const int64_t* __restrict__ off, int64_t npos, int 
 }
 
 bool dense_cull(const Mat& a, const Mat& b, double tau, bool want_tasks, CullResult& r,
-                cudaStream_t s, bool sym) {
+                cudaStream_t s, bool sym, int64_t lo = 0, int64_t hi = -1,
+                int32_t* work = nullptr) {
+  const bool ranged = hi >= 0;
   const int depth = a.depth;
   const int64_t G = int64_t(1) << depth, npos = G * G;
   // aux[0]: full leaf survivors, [1]: mirror mismatch, [2]: packed scan
@@ -532,7 +545,7 @@ bool dense_cull(const Mat& a, const Mat& b, double tau, bool want_tasks, CullRes
   int64_t* off = cnt + npos;
   SPAMM_CK(cudaMemsetAsync(zbuf, 0, aux_bytes + (G + 2) * sizeof(int), s));
   auto* u64 = reinterpret_cast<unsigned long long*>(aux);
-  if (depth > 0) {
+  if (depth > 0 && !ranged) {  // (a shard reports leaf-tier counts only)
     const int64_t tri = ((int64_t(1) << (3 * depth)) - 1) / 7;
     launch_pdl(k_dense_tiers, grid_for(tri, 256, 148LL * 8), 256, 0, s,
         a.norms, b.norms, tau, depth, u64 + 4, tb, u64 + NEAR, u64 + MARGIN);
@@ -541,7 +554,7 @@ bool dense_cull(const Mat& a, const Mat& b, double tau, bool want_tasks, CullRes
   launch_pdl(k_dense_leaf<false>, grid_for(npos * 32, CULL_THREADS, 148LL * 64), CULL_THREADS, 0, s,
       depth, a.norms, b.norms, tau, sym ? 1 : 0, cnt, nullptr, sched, nullptr, nullptr, nullptr,
       nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, 0, 0, u64,
-      tb, u64 + NEAR + depth, u64 + MARGIN);
+      tb, u64 + NEAR + depth, u64 + MARGIN, lo, hi, work);
   SPAMM_LAUNCH_CK();
   scan_exclusive_i64(cnt, npos, off, s);
   if (want_tasks) hist_scan_exclusive(sched, (int)G + 1, s);
@@ -578,7 +591,7 @@ bool dense_cull(const Mat& a, const Mat& b, double tau, bool want_tasks, CullRes
   for (int t = 0; t < depth; ++t) r.visited[t] = h[4 + t];
   r.visited[depth] = h[0];
   for (int t = 0; t <= depth; ++t)
-    r.culled[t] = (t == 0 ? 1 : 8 * r.visited[t - 1]) - r.visited[t];
+    r.culled[t] = ranged ? 0 : (t == 0 ? 1 : 8 * r.visited[t - 1]) - r.visited[t];
   if (!want_tasks || V == 0) {
     dfree(cnt, s);
     dfree(zbuf, s);
@@ -610,7 +623,7 @@ bool dense_cull(const Mat& a, const Mat& b, double tau, bool want_tasks, CullRes
   launch_pdl(k_dense_leaf<true>, grid_for(npos * 32, CULL_THREADS, 148LL * 64), CULL_THREADS, 0, s,
       depth, a.norms, b.norms, tau, sym ? 1 : 0, nullptr, off, sched, r.ci, r.cj, r.seg, r.k,
       a.slot, b.slot, r.a_idx, r.b_idx, r.keys, r.c_out, r.c_mirror, r.order, M, V, nullptr, tb,
-      nullptr, nullptr);
+      nullptr, nullptr, lo, hi, nullptr);
   SPAMM_LAUNCH_CK();
   dfree(cnt, s);
   r.n_c = M;
@@ -680,8 +693,8 @@ bool cull(const Mat& a, const Mat& b, double tau, bool want_tasks, CullResult& r
   r.sym = sym;
   r.near.assign(depth + 1, 0);
   r.margin = INFINITY;
-  if (g_dense_enabled && depth <= DENSE_MAX_DEPTH && lo <= 0 && hi < 0 && !work)
-    return dense_cull(a, b, tau, want_tasks, r, s, sym);
+  if (g_dense_enabled && depth <= DENSE_MAX_DEPTH)
+    return dense_cull(a, b, tau, want_tasks, r, s, sym, lo, hi, work);
 
   int32_t* ci = dmalloc<int32_t>(1, s);
   int32_t* cj = dmalloc<int32_t>(1, s);

@@ -87,6 +87,8 @@ struct IdemFuse {
   // capacity G*G) and its size, produced by the same launch
   int64_t* ukeys = nullptr;
   int64_t* ucount = nullptr;
+  // optional: the leaf tier (G * G, row-major) of ||X^2 - X||^2 (multi-GPU)
+  double* dleaf = nullptr;
 };
 bool idem_fusable(const Mat& x);
 void finalize(Mat& m, cudaStream_t s, IdemFuse idem, bool defer);

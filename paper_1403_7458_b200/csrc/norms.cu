@@ -412,7 +412,8 @@ __global__ void __launch_bounds__(FS_THREADS)
                      double* __restrict__ tr_out, double* host_top, int top_t,
                      const double* __restrict__ dn2, const double* __restrict__ xleaf2,
                      double* __restrict__ idem_out, const int32_t* __restrict__ xslot = nullptr,
-                     int64_t* __restrict__ ukeys = nullptr, int64_t* __restrict__ ucount = nullptr) {
+                     int64_t* __restrict__ ukeys = nullptr, int64_t* __restrict__ ucount = nullptr,
+                     double* __restrict__ dleaf = nullptr) {
   pdl_wait();
   extern __shared__ __align__(16) double p2[];  // squared pyramid, tiers 0..depth
   __shared__ int32_t dslot[128];
@@ -467,7 +468,9 @@ __global__ void __launch_bounds__(FS_THREADS)
 #pragma unroll 4
     for (int j = 0; j < FS_PER; ++j) {
       const int64_t p = (int64_t)j * FS_THREADS + tid;
-      if (p < npos) p2[leaf_off + p] = xleaf2[p];  // X-only blocks: (-x)^2 == x^2
+      // X-only blocks: (-x)^2 == x^2 -- only blocks this matrix stores (a
+      // multi-GPU shard carries the whole matrix's pyramid)
+      if (p < npos) p2[leaf_off + p] = (!xslot || xslot[p] >= 0) ? xleaf2[p] : 0.0;
     }
     __syncthreads();
 #pragma unroll 4
@@ -476,6 +479,13 @@ __global__ void __launch_bounds__(FS_THREADS)
       if (b < nblocks) p2[leaf_off + keys[b]] = dn2[b];
     }
     __syncthreads();
+    if (dleaf) {  // the leaf tier of ||X^2 - X||^2 (multi-GPU: all-reduced by the caller)
+#pragma unroll 4
+      for (int j = 0; j < FS_PER; ++j) {
+        const int64_t p = (int64_t)j * FS_THREADS + tid;
+        if (p < npos) dleaf[p] = p2[leaf_off + p];
+      }
+    }
     fs_tiers(p2, nullptr, nullptr, depth);
     if (tid == 0) *idem_out = __dsqrt_rn(p2[0]);
   } else {
@@ -769,7 +779,7 @@ void build_pyramid(const int64_t* keys, const double* blk_norms2, int64_t m, int
                           (int32_t*)nullptr, norms, norms2, (const double*)nullptr, 0,
                           (double*)nullptr, (double*)nullptr, 0, (const double*)nullptr,
                           (const double*)nullptr, (double*)nullptr, (const int32_t*)nullptr,
-                          (int64_t*)nullptr, (int64_t*)nullptr);
+                          (int64_t*)nullptr, (int64_t*)nullptr, (double*)nullptr);
     return;
   }
   const int64_t G = int64_t(1) << depth;
@@ -903,7 +913,7 @@ void finalize_impl(Mat& m, cudaStream_t s, double* pre_n2, uint8_t* pre_nz, bool
         (const double*)dn2,
         idem.x ? (const double*)(idem.x->norms2 + tier_offset(m.depth)) : (const double*)nullptr,
         idem.out, idem.x ? (const int32_t*)idem.x->slot : (const int32_t*)nullptr, idem.ukeys,
-        idem.ucount);
+        idem.ucount, idem.dleaf);
     if (m.host_top) SPAMM_CK(cudaEventRecord(m.top_ev, s));
     dfree(dn2, s);
     dfree(n2, s);  // (a locally computed n1 shares n2's allocation)

@@ -339,47 +339,50 @@ class DistributedSP2:
         import torch
         eng, comm = self.engine, self.comm
         want_idem = criterion == "fro"
+        multi = self.world > 1
         res = DistResult(x=x)
-        leaf, ex = self._globalize(x, sym)
+        # one rank: the shard is the whole matrix (its own pyramid and K4z
+        # scales are the global ones) and no collective runs
+        leaf, ex = self._globalize(x, sym) if multi else (None, None)
         tr_pending = False
         for it in range(max_iter):
             t0 = time.perf_counter()
             res.cuts_history.append(list(cuts))
             res.mode_history.append(mode)
             res.owned_blocks.append(eng.count(x))
-            lo, hi = cuts[self.rank], cuts[self.rank + 1]
-            # one symmetric-path decision for the whole grid (a mirror ulp tie
-            # anywhere sends every rank down the full path, as on one GPU)
+            lo, hi = (cuts[self.rank], cuts[self.rank + 1]) if multi else (0, -1)
             sym_eff = sym
-            if sym:
-                ok = eng.census_symmetric_ok(x, tau, lo, hi)
-                sym_eff = bool(comm.all_min(torch.tensor([1 if ok else 0],
-                                                         dtype=torch.int64)).item())
-            mode_c = UPPER if sym_eff else POS
-            req, got = self._halo(x, g, cuts, mode, tau, lo, hi, sym_eff)
-            res.halo_blocks.append(int(req.numel()))
-            ext = eng.extend(x, req, got, leaf, sym_eff, ex)
-            c, work, leaf_r, exec_r = eng.multiply_range(ext, tau, lo, hi, sym_eff)
+            ext = x
+            if multi:
+                # one symmetric-path decision for the whole grid (a mirror ulp
+                # tie anywhere sends every rank down the full path, as on one GPU)
+                if sym:
+                    ok = eng.census_symmetric_ok(x, tau, lo, hi)
+                    sym_eff = bool(comm.all_min(torch.tensor([1 if ok else 0],
+                                                             dtype=torch.int64)).item())
+                req, got = self._halo(x, g, cuts, mode, tau, lo, hi, sym_eff)
+                res.halo_blocks.append(int(req.numel()))
+                ext = eng.extend(x, req, got, leaf, sym_eff, ex)
+                mode_c = UPPER if sym_eff else POS
+                if mode != mode_c:                  # symmetry lost: re-home X by position
+                    x, _ = self.redistribute(x, g, cuts, mode_c)
+                    mode = mode_c
+            else:
+                res.halo_blocks.append(0)
+            # the rank's C segment, the whole-matrix scalars (one all-reduce
+            # inside the step), the branch and the update on the shard
+            (x_next, square, t_x, t_sq, idem, work, leaf_r,
+             exec_r) = eng.sp2_step(ext, x, n_occ, tau, lo, hi, want_idem, sym_eff,
+                                    comm if multi else None)
             del ext
             res.local_executed.append(int(exec_r))
-            if mode != mode_c:                      # symmetry lost: re-home X by position
-                x, _ = self.redistribute(x, g, cuts, mode_c)
-                mode = mode_c
-            # traces (per diagonal block) + residual leaf tier + counts: one all-reduce
-            parts = [eng.diag_traces(x), eng.diag_traces(c)]
-            if want_idem:
-                parts.append(eng.residual_leaf_norms2(c, x))
-            vec = comm.all_sum(torch.cat([p.to(torch.float64) for p in parts]))
-            vec = eng.to_numpy(vec)
-            t_x, t_sq = seq_sum(vec[:g]), seq_sum(vec[g:2 * g])
-            idem = float(np.sqrt(pyramid_root2(vec[2 * g:]))) if want_idem else None
-            cnt = comm.all_sum(torch.tensor([int(leaf_r)], dtype=torch.int64))
-            res.leaf_products.append(int(cnt.item()))
+            cnt = int(comm.all_sum(torch.tensor([int(leaf_r)], dtype=torch.int64)).item()) \
+                if multi else int(leaf_r)
+            res.leaf_products.append(cnt)
             if it == 0 or tr_pending:           # tr of X0, then of every accepted X
                 res.trace_history.append(t_x)
                 tr_pending = False
             t_ex = 2.0 * t_x - t_sq
-            square = abs(t_sq - n_occ) <= abs(t_ex - n_occ)            # sp2.py:97-99
             res.branch_margins.append(abs(t_ex - n_occ) - abs(t_sq - n_occ))
             if want_idem:
                 res.idempotency_history.append(idem)
@@ -390,24 +393,28 @@ class DistributedSP2:
                 res.converged = True
                 res.seconds_per_iteration.append(time.perf_counter() - t0)
                 break
-            x = c if square else eng.expand(x, c)
+            x = x_next
             sym = sym_eff
             res.iteration += 1
             res.branch_history.append("SQUARE" if square else "EXPAND")
             tr_pending = True
-            # persistence load balancing: next cut from this iteration's counts
-            if balance == "persistence" and self.world > 1:
-                w = comm.all_sum(work.to(torch.int64))
-                new_cuts = partition_work(eng.to_numpy(w), self.world)
-                if new_cuts != cuts:
-                    x, moved = self.redistribute(x, g, new_cuts, mode)
-                    res.moved_blocks.append(moved)
-                    cuts = new_cuts
-            leaf, ex = self._globalize(x, sym)
+            if multi:
+                # persistence load balancing: next cut from this iteration's counts
+                if balance == "persistence":
+                    w = comm.all_sum(work.to(torch.int64))
+                    new_cuts = partition_work(eng.to_numpy(w), self.world)
+                    if new_cuts != cuts:
+                        x, moved = self.redistribute(x, g, new_cuts, mode)
+                        res.moved_blocks.append(moved)
+                        cuts = new_cuts
+                leaf, ex = self._globalize(x, sym)
             res.seconds_per_iteration.append(time.perf_counter() - t0)
         if tr_pending:
-            vec = eng.to_numpy(comm.all_sum(eng.diag_traces(x).to(torch.float64)))
-            res.trace_history.append(seq_sum(vec[:g]))
+            if multi:
+                vec = eng.to_numpy(comm.all_sum(eng.diag_traces(x).to(torch.float64)))
+                res.trace_history.append(seq_sum(vec[:g]))
+            else:
+                res.trace_history.append(eng.trace(x))
         res.x, res.cuts, res.mode, res.symmetric, res.leaf = x, cuts, mode, sym, leaf
         return res
 
@@ -623,6 +630,54 @@ class DeviceShardEngine:
         return c, work, int(st.leaf_products), int(st.executed_products)
 
     # -- SP2 pieces -------------------------------------------------------------
+    def sp2_step(self, ext, x, n_occ, tau, lo, hi, want_idem, sym, comm):
+        """spamm_shard_sp2_step: the rank's C segment of X^2 from its operand
+        ``ext``, the scalars of the whole matrices (``comm`` all-reduces one
+        vector from inside the step; None on one rank), the branch and the
+        fused update on the shard."""
+        import ctypes
+
+        import torch
+
+        from . import _native as nat
+        from .kernel import _leaf_kernel, _check_tau
+        from .quadtree import QuadTreeMatrix
+        g = x.n_blocks
+        work = torch.zeros(g * g, dtype=torch.int32, device="cuda") if hi >= 0 else None
+        st = nat.Stats()
+        out = ctypes.c_void_p()
+        br = ctypes.c_int32()
+        t_x, t_sq, idem = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
+        stream = nat.current_stream()
+        cb = None
+        if comm is not None:
+            def _allreduce(_ctx, ptr, n, _stream):
+                try:
+                    t = torch.as_tensor(_DevArray(ptr, n, "<f8"), device="cuda")
+                    t.copy_(comm.all_sum(t.clone()))
+                    return 0
+                except Exception:  # noqa: BLE001 - reported to the library as a failure
+                    import traceback
+                    traceback.print_exc()
+                    return 1
+            cb = nat.ALLREDUCE_FN(_allreduce)
+        self._set_sym(sym)
+        try:
+            nat.check(nat.load().spamm_shard_sp2_step(
+                ext._h, x._h, float(n_occ), _check_tau(tau), _leaf_kernel(self.kernel),
+                int(lo), int(hi), work.data_ptr() if work is not None else None, int(want_idem),
+                cb, None, stream, ctypes.byref(out), ctypes.byref(br), ctypes.byref(t_x),
+                ctypes.byref(t_sq), ctypes.byref(idem), ctypes.byref(st)))
+        finally:
+            self._set_sym(True)
+        return (QuadTreeMatrix(out, stream), br.value == 0, float(t_x.value), float(t_sq.value),
+                float(idem.value) if want_idem else None, work, int(st.leaf_products),
+                int(st.executed_products))
+
+    def trace(self, m):
+        from .quadtree import trace
+        return trace(m)
+
     def diag_traces(self, m):
         import torch
 
@@ -631,10 +686,11 @@ class DeviceShardEngine:
         nat.check(nat.load().spamm_mat_diag_traces(m._h, out.data_ptr(), nat.current_stream()))
         return out
 
-    def residual_leaf_norms2(self, c, x):
-        from .quadtree import add_scaled
-        return add_scaled(1.0, c, -1.0, x).leaf_norms2_device()
 
-    def expand(self, x, c):
-        from .quadtree import add_scaled
-        return add_scaled(2.0, x, -1.0, c)
+class _DevArray:
+    """A raw device buffer seen by torch without a copy (__cuda_array_interface__)."""
+
+    def __init__(self, ptr: int, n: int, typestr: str):
+        self.__cuda_array_interface__ = {"shape": (int(n),), "typestr": typestr,
+                                         "data": (int(ptr), False), "version": 3,
+                                         "strides": None}

@@ -180,6 +180,25 @@ class OracleDistEngine:
         return out, torch.from_numpy(work), full, len(ti)
 
     # SP2 pieces
+    def sp2_step(self, ext, x, n_occ, tau, lo, hi, want_idem, sym, comm):
+        g = x.m.n_blocks
+        c, work, full, executed = self.multiply_range(ext, tau, lo, hi if hi >= 0 else g * g, sym)
+        parts = [self.diag_traces(x), self.diag_traces(c)]
+        if want_idem:
+            parts.append(self.residual_leaf_norms2(c, x))
+        vec = torch.cat(parts)
+        if comm is not None:
+            vec = comm.all_sum(vec)
+        vec = vec.numpy()
+        t_x, t_sq = seq_sum(vec[:g]), seq_sum(vec[g:2 * g])
+        idem = float(np.sqrt(pyramid_root2(vec[2 * g:]))) if want_idem else None
+        square = abs(t_sq - n_occ) <= abs((2.0 * t_x - t_sq) - n_occ)
+        nxt = c if square else self.expand(x, c)
+        return nxt, square, t_x, t_sq, idem, work, full, executed
+
+    def trace(self, x):
+        return O.trace(x.m)
+
     def diag_traces(self, x):
         m = x.m
         g = m.n_blocks
