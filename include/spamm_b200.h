@@ -172,23 +172,6 @@ int spamm_set_dense_cull(int32_t enabled);
 /* Width of the near-tau band in ulps of tau (default 64: the norm error of
  * a DMMA / K4z operand against the reference's; 1 for the exact kernel). */
 int spamm_set_near_tau_ulps(int32_t ulps);
-/* Sharded SP2 iteration (multi-GPU, X replicated; parallel.ShardedSP2):
- * spamm_sp2_multiply_shard runs the full dense cull of X*X on every rank (so
- * every rank holds the same C layout) and the leaf products of this rank's
- * contiguous run of emitted C nodes, cut into `world` equal task counts;
- * cut_pos (world + 1) receives the Morton cut positions.  C comes back
- * unfinalised with this rank's blocks (and their mirrors) computed; after the
- * caller has exchanged blocks (every C block has one owner: the rank whose
- * Morton range holds its upper-triangle position), spamm_sp2_shard_finish
- * finalises C and runs the rest of the iteration (traces, residual, branch,
- * update) exactly as spamm_sp2_step; *x_next is 2X - X^2 on EXPAND, NULL on
- * SQUARE (the next X is then C itself).  Needs depth <= 8. */
-int spamm_sp2_multiply_shard(const spamm_mat* x, double tau, int32_t kernel, int32_t rank,
-                             int32_t world, void* stream, spamm_mat** c, int64_t* cut_pos,
-                             spamm_stats* stats);
-int spamm_sp2_shard_finish(const spamm_mat* x, spamm_mat* c, double n_occ, int32_t want_idem,
-                           void* stream, int32_t* branch, double* t_x, double* t_sq,
-                           double* idem, spamm_mat** x_next);
 /* One SP2 iteration on this rank's Morton shard (multi-GPU, dist.py).
  * `x` is the rank's share of X (the whole matrix's pyramid installed with
  * spamm_mat_set_pyramid), `ext` its operand: x plus the fetched halo blocks

@@ -104,11 +104,6 @@ _SIGS = {
                                      ctypes.POINTER(c_i32), ctypes.POINTER(c_f64),
                                      ctypes.POINTER(c_f64), ctypes.POINTER(c_f64),
                                      ctypes.POINTER(Stats)]),
-    "spamm_sp2_multiply_shard": (c_i32, [c_vp, c_f64, c_i32, c_i32, c_i32, c_vp,
-                                         ctypes.POINTER(c_vp), c_vp, ctypes.POINTER(Stats)]),
-    "spamm_sp2_shard_finish": (c_i32, [c_vp, c_vp, c_f64, c_i32, c_vp, ctypes.POINTER(c_i32),
-                                       ctypes.POINTER(c_f64), ctypes.POINTER(c_f64),
-                                       ctypes.POINTER(c_f64), ctypes.POINTER(c_vp)]),
     "spamm_tasks": (c_i32, [c_vp, c_vp, c_f64, c_vp, c_vp, c_vp, c_i64, ctypes.POINTER(c_i64), c_vp]),
     "spamm_census_range": (c_i32, [c_vp, c_vp, c_f64, c_i64, c_i64, c_vp, c_vp,
                                    ctypes.POINTER(Stats)]),

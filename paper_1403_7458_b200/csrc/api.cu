@@ -727,88 +727,6 @@ __global__ void k_shard_traces(const double* __restrict__ vec, int64_t G, double
   }
 }
 
-__global__ void k_iota64(int64_t* out, int64_t n) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x)
-    out[i] = i;
-}
-
-// Sharded SP2 product (multi-GPU, X replicated): every rank runs the same
-// dense cull -- so every rank holds the same C layout -- and the leaf
-// products of its own contiguous run of emitted C nodes, cut so that all
-// ranks get the same task count (the current iteration's counts: exact load
-// balance).  C is returned unfinalised with only this rank's blocks (and
-// their mirrors) computed; the caller exchanges blocks, then
-// spamm_sp2_shard_finish finalises it.  cut_pos: the Morton cut positions.
-void multiply_shard_impl(const spamm_mat* a, double tau, int32_t kernel, cudaStream_t s,
-                         spamm::Mat& C, spamm_stats* stats, int rank, int world,
-                         int64_t* cut_pos) {
-  if (a->m.depth > 8) throw std::invalid_argument("sharded SP2 products need depth <= 8");
-  OzakiAhead oz;  // K4z operand pre-passes alongside the cull (as in multiply_impl)
-  ozaki_ahead(a, a, kernel, s, oz);
-  spamm::CullResult r;
-  r.world = world;
-  bool sym = g_sym_enabled && a->m.sym;
-  if (sym && !spamm::cull(a->m, a->m, tau, true, r, s, true)) sym = false;
-  if (!sym) spamm::cull(a->m, a->m, tau, true, r, s, false);
-  C.n_native = a->m.n_native;
-  C.nb = a->m.nb;
-  C.chunk_size = a->m.chunk_size;
-  C.depth = a->m.depth;
-  C.G = a->m.G;
-  C.stream = s;
-  C.sym = sym;
-  const int64_t nb2 = (int64_t)C.nb * C.nb;
-  if (r.n_tasks == 0 || !r.keys) {  // nothing survives: empty C on every rank
-    C.nblocks = 0;
-    C.keys = spamm::dmalloc<int64_t>(0, s);
-    C.data = spamm::dmalloc<double>(0, s);
-    for (int i = 0; i <= world; ++i) cut_pos[i] = i == world ? C.G * C.G : 0;
-    fill_stats(stats, tau, r, C.nb);
-    r.release(s);
-    return;
-  }
-  if (world == 1) {
-    r.cut_pos = {0, C.G * C.G};
-    r.node_cut = {0, r.n_c};
-  }
-  if ((int)r.cut_pos.size() != world + 1) throw std::runtime_error("sharded cull: no cuts");
-  C.nblocks = r.n_c_full;
-  C.keys = r.keys;
-  r.keys = nullptr;
-  C.data = spamm::dmalloc<double>((size_t)C.nblocks * nb2, s);
-  int64_t* ident = nullptr;
-  int64_t* c_out = r.c_out;
-  if (!c_out) {  // non-symmetric layout: node m is storage slot m
-    ident = spamm::dmalloc<int64_t>(r.n_c, s);
-    k_iota64<<<spamm::grid_for(r.n_c, 256), 256, 0, s>>>(ident, r.n_c);
-    SPAMM_LAUNCH_CK();
-    c_out = ident;
-  }
-  const int64_t n_lo = r.node_cut[rank], n_hi = r.node_cut[rank + 1];
-  if (oz.ok) {
-    if (oz.ready) SPAMM_CK(cudaStreamWaitEvent(s, oz.ready, 0));
-    oz.ready = nullptr;
-    if (n_hi > n_lo)
-      spamm::ozaki_launch<int32_t>(n_hi - n_lo, r.seg + n_lo, r.a_idx, r.b_idx, c_out + n_lo,
-                                   r.c_mirror ? r.c_mirror + n_lo : nullptr, false, a->m, a->m,
-                                   oz.op, C.data, s);
-    spamm::ozaki_release(oz.op, s);
-    oz.ok = false;
-  } else if (n_hi > n_lo) {
-    leaf_dispatch(n_hi - n_lo, r.seg + n_lo, r.a_idx, r.b_idx, c_out + n_lo,
-                  r.c_mirror ? r.c_mirror + n_lo : nullptr, a, a, C.data, kernel, s, {});
-  }
-  spamm::dfree(ident, s);
-  for (int i = 0; i <= world; ++i) cut_pos[i] = r.cut_pos[i];
-  fill_stats(stats, tau, r, C.nb);
-  if (stats) {
-    stats->c_blocks = C.nblocks;
-    stats->executed_products = r.n_tasks;
-    stats->symmetric = sym ? 1 : 0;
-  }
-  r.release(s);
-}
 
 // Second half of an SP2 iteration given X and X2 = X*X (sp2.py:94-101 + the
 // idempotency test): traces (tr X cached) and the union size in one sync, the
@@ -1030,65 +948,6 @@ int spamm_shard_sp2_step(const spamm_mat* ext, const spamm_mat* x, double n_occ,
   } else {
     *x_next = c;
   }
-  *branch = square ? 0 : 1;
-  *t_x = tx;
-  *t_sq = tsq;
-  SPAMM_API_END
-}
-
-int spamm_sp2_multiply_shard(const spamm_mat* x, double tau, int32_t kernel, int32_t rank,
-                             int32_t world, void* stream, spamm_mat** c, int64_t* cut_pos,
-                             spamm_stats* stats) {
-  if (!x || !c || !cut_pos) return fail(SPAMM_EINVAL, "null argument");
-  if (world < 1 || world > 16 || rank < 0 || rank >= world)
-    return fail(SPAMM_EINVAL, "rank/world out of range (world <= 16)");
-  if (!(tau >= 0.0) || tau == __builtin_inf())
-    return fail(SPAMM_EINVAL, "tau must be finite and >= 0, got " + std::to_string(tau));
-  if (kernel < 0 || kernel > 4) return fail(SPAMM_EINVAL, "unknown leaf kernel");
-  if (kernel == SPAMM_LEAF_OZAKI && !spamm::ozaki_supported(x->m.nb))
-    return fail(SPAMM_EINVAL, "INT8-sliced leaf kernel needs block size 32 or 64");
-  if (x->m.depth > 8) return fail(SPAMM_EINVAL, "sharded SP2 products need depth <= 8");
-  SPAMM_API_BEGIN
-  auto* h = new spamm_mat();
-  try {
-    multiply_shard_impl(x, tau, kernel, S(stream), h->m, stats, rank, world, cut_pos);
-  } catch (...) {
-    h->m.release();
-    delete h;
-    throw;
-  }
-  *c = h;
-  SPAMM_API_END
-}
-
-int spamm_sp2_shard_finish(const spamm_mat* x, spamm_mat* c, double n_occ, int32_t want_idem,
-                           void* stream, int32_t* branch, double* t_x, double* t_sq, double* idem,
-                           spamm_mat** x_next) {
-  if (int rc = check_conformable(x, c)) return rc;
-  if (!branch || !t_x || !t_sq || !x_next || (want_idem && !idem))
-    return fail(SPAMM_EINVAL, "null argument");
-  SPAMM_API_BEGIN
-  cudaStream_t s = S(stream);
-  const bool sym = c->m.sym;
-  spamm::IdemFuse fuse;
-  if (want_idem && spamm::idem_fusable(x->m)) {
-    fuse.x = &x->m;
-    fuse.out = spamm::dmalloc<double>(2, s);
-    fuse.ucount = reinterpret_cast<int64_t*>(fuse.out + 1);
-    fuse.ukeys = spamm::dmalloc<int64_t>(x->m.G * x->m.G, s);
-    spamm::finalize(c->m, s, fuse, true);
-  } else {
-    spamm::finalize(c->m, s, nullptr, nullptr, true);
-  }
-  c->m.sym = sym;
-  spamm_mat* e = nullptr;
-  bool square = true;
-  double tx = 0, tsq = 0;
-  sp2_finish(x, c, n_occ, want_idem != 0, s, &square, &tx, &tsq, idem, &e, fuse.out,
-             fuse.x ? &fuse : nullptr);
-  spamm::dfree(fuse.out, s);
-  spamm::dfree(fuse.ukeys, s);
-  *x_next = e;
   *branch = square ? 0 : 1;
   *t_x = tx;
   *t_sq = tsq;

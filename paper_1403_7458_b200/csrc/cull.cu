@@ -493,33 +493,6 @@ __global__ void __launch_bounds__(CULL_THREADS)
   }
 }
 
-// Sharded SP2: Morton cut positions that split the emitted tasks into
-// `world` equal parts (exclusive task prefix off[p] & mask is monotone in p),
-// and the node index at each cut.  out[0..world] = positions,
-// out[world+1 .. 2 world+1] = node bounds.
-__global__ void k_shard_cuts(const int64_t* __restrict__ off, int64_t npos, int world,
-                             int64_t* __restrict__ out) {
-  const int r = threadIdx.x;
-  if (r > world) return;
-  const int64_t total = off[npos] & DT_TASK_MASK;
-  int64_t pos;
-  if (r == 0) {
-    pos = 0;
-  } else if (r == world) {
-    pos = npos;
-  } else {
-    const int64_t target = (total * r + world - 1) / world;
-    int64_t lo = 0, hi = npos;  // smallest p with prefix(p) >= target
-    while (lo < hi) {
-      const int64_t mid = (lo + hi) / 2;
-      if ((off[mid] & DT_TASK_MASK) >= target) hi = mid; else lo = mid + 1;
-    }
-    pos = lo;
-  }
-  out[r] = pos;
-  out[world + 1 + r] = (off[pos] >> DT_NODE) & DT_IDX_MASK;
-}
-
 bool dense_cull(const Mat& a, const Mat& b, double tau, bool want_tasks, CullResult& r,
                 cudaStream_t s, bool sym, int64_t lo = 0, int64_t hi = -1,
                 int32_t* work = nullptr) {
@@ -528,15 +501,13 @@ bool dense_cull(const Mat& a, const Mat& b, double tau, bool want_tasks, CullRes
   const int64_t G = int64_t(1) << depth, npos = G * G;
   // aux[0]: full leaf survivors, [1]: mirror mismatch, [2]: packed scan
   // total, [4 + t]: tier-t survivors (t < depth), [NEAR + t]: near-tau
-  // products of tier t (t <= depth), [MARGIN]: inverted min relative margin,
-  // [CUTS ..]: shard cuts.
+  // products of tier t (t <= depth), [MARGIN]: inverted min relative margin.
   // [aux | LPT schedule: G + 1 length bins (bin 0 = G tasks) + the K4 counter]
   // zeroed by one memset; the schedule part is handed to K4 (r.sched).
   htrace("dc_start");
-  const int world = r.world > 1 ? r.world : 1;
   constexpr int NEAR = 4 + DENSE_MAX_DEPTH, MARGIN = NEAR + DENSE_MAX_DEPTH + 1,
                 CUTS = MARGIN + 1;
-  const size_t aux_bytes = (CUTS + 2 * (world + 1)) * sizeof(int64_t);
+  const size_t aux_bytes = (size_t)CUTS * sizeof(int64_t);
   const TieBand tb = tie_band(tau);
   char* zbuf = dmalloc<char>(aux_bytes + (G + 2) * sizeof(int), s);
   int64_t* aux = reinterpret_cast<int64_t*>(zbuf);
@@ -558,29 +529,18 @@ bool dense_cull(const Mat& a, const Mat& b, double tau, bool want_tasks, CullRes
   SPAMM_LAUNCH_CK();
   scan_exclusive_i64(cnt, npos, off, s);
   if (want_tasks) hist_scan_exclusive(sched, (int)G + 1, s);
-  int64_t* cuts = aux + CUTS;
-  if (world > 1) {
-    k_shard_cuts<<<1, 32, 0, s>>>(off, npos, world, cuts);
-    SPAMM_LAUNCH_CK();
-  }
-  // gathered: aux[0..4+depth), near[0..depth], margin, cuts
+  // gathered: aux[0..4+depth), near[0..depth], margin
   const int n_base = 4 + depth, n_near = depth + 1;
-  const int nsc = n_base + n_near + 1 + (world > 1 ? 2 * (world + 1) : 0);
+  const int nsc = n_base + n_near + 1;
   const int64_t* src[64];
   for (int i = 0; i < n_base; ++i) src[i] = aux + i;
   src[2] = off + npos;
   for (int t = 0; t < n_near; ++t) src[n_base + t] = aux + NEAR + t;
   src[n_base + n_near] = aux + MARGIN;
-  const int n_cut0 = n_base + n_near + 1;
-  for (int i = 0; world > 1 && i < 2 * (world + 1); ++i) src[n_cut0 + i] = cuts + i;
   int64_t h[64];
   gather_sync(h, src, nsc, s);
   for (int t = 0; t < n_near; ++t) r.near[t] = h[n_base + t];
   r.margin = margin_from_bits(h[n_base + n_near]);
-  if (world > 1) {
-    r.cut_pos.assign(h + n_cut0, h + n_cut0 + world + 1);
-    r.node_cut.assign(h + n_cut0 + world + 1, h + n_cut0 + 2 * world + 2);
-  }
   if (h[1]) {  // leaf survivor set not mirror-symmetric (ulp tie): full cull
     dfree(cnt, s);
     dfree(zbuf, s);

@@ -159,11 +159,6 @@ struct CullResult {
   int32_t* order = nullptr;
   int* sched = nullptr;                  // hist/counter scratch (counter inside)
   void* block = nullptr;                 // dense cull: single allocation of the arrays
-  // Sharded SP2 (input): split the emitted C nodes into `world` contiguous
-  // Morton segments of equal task count; (output) their Morton cut positions
-  // and node index bounds (world + 1 each).  Dense cull only.
-  int world = 1;
-  std::vector<int64_t> cut_pos, node_cut;
   int* counter = nullptr;
   void release(cudaStream_t s);
 };

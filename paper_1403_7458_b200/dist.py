@@ -649,7 +649,7 @@ class DeviceShardEngine:
         br = ctypes.c_int32()
         t_x, t_sq, idem = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
         stream = nat.current_stream()
-        cb = None
+        cb = nat.ALLREDUCE_FN()          # NULL: one rank, no collective
         if comm is not None:
             def _allreduce(_ctx, ptr, n, _stream):
                 try:

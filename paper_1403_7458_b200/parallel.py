@@ -1,27 +1,13 @@
-"""Multi-GPU SP2: the C-block Morton curve sharded across ranks.
+"""Distributed-operand SpAMM for BASELINE config 5: H is split by
+Morton segments of the block grid and no rank holds all of it.
 
 Reference semantics: the paper's over-decomposition of the (i, k, j)
-convolution space with persistence-based load balancing (PAPER.md:505-512,
-812-833), which the reference only *simulates* (chare_sim.py:180-328:
-``build_chare_graph``, ``greedy_comm_balance`` using the previous measured
-cost).  Here it is executed, one process per GPU:
-
-* every rank holds X (replicated; cfg4 X is 114 MB) and its norm pyramid;
-* the C grid, in the storage's Morton order, is cut into ``world`` contiguous
-  segments of equal predicted work -- the per-C-block task counts of the
-  previous iteration (persistence); the first iteration splits evenly;
-* each rank runs the multiply on its segment only (``spamm_multiply_range``:
-  the cull prunes every quadtree node whose Morton subtree misses the
-  segment), on the symmetric path the upper blocks in range plus mirrors;
-* the computed blocks are all-gathered (NCCL over NVLink on GPUs, gloo in the
-  CPU tests) and X^2 is re-assembled identically on every rank;
-* the rest of the iteration (traces, branch, fused update, idempotency) runs
-  redundantly on the replicated X^2, so the trajectory is bitwise the
-  single-GPU one and no scalar reduction is needed.
-
-The engine argument isolates device work: :class:`DeviceEngine` calls the
-sm_100a library; ``tests/test_distributed.py`` supplies a CPU engine backed
-by the oracle to exercise this host logic with gloo (world size 2).
+convolution space over PEs with a measured-cost balance (PAPER.md:505-512,
+812-833), which the reference only simulates (chare_sim.py:180-328).  The SP2
+driver over the same primitives -- X, X^2 and the update sharded, persistence
+load balancing -- is ``dist.py``.  ``engine`` isolates device work:
+:class:`DeviceEngine` calls the sm_100a library; the CPU tests supply an
+oracle-backed engine and run the same logic under gloo.
 """
 
 from __future__ import annotations
@@ -33,151 +19,11 @@ import numpy as np
 
 from .synth_morton import morton_keys
 
-__all__ = ["partition_work", "even_cuts", "ShardedSP2", "DeviceEngine", "ShardedResult",
-           "ShardedMultiply", "ShardProduct", "morton_positions", "NativeShardedSP2",
-           "exchange_blocks", "block_owners"]
+__all__ = ["partition_work", "even_cuts", "DeviceEngine", "ShardedMultiply", "ShardProduct",
+           "morton_positions"]
 
 
-def even_cuts(n_pos: int, world: int) -> list:
-    """Equal-length Morton segments [cuts[r], cuts[r+1])."""
-    return [(n_pos * r) // world for r in range(world + 1)]
-
-
-def partition_work(work: np.ndarray, world: int) -> list:
-    """Cut the Morton-indexed work vector into ``world`` contiguous segments of
-    (nearly) equal total work: cut r is the first position whose inclusive
-    prefix sum reaches r/world of the total (deterministic on every rank)."""
-    work = np.asarray(work, dtype=np.int64).reshape(-1)
-    n = len(work)
-    total = int(work.sum())
-    if total == 0 or world == 1:
-        return even_cuts(n, world)
-    csum = np.cumsum(work)
-    cuts = [0]
-    for r in range(1, world):
-        target = (total * r + world - 1) // world
-        pos = int(np.searchsorted(csum, target, side="left")) + 1
-        cuts.append(min(max(pos, cuts[-1]), n))
-    cuts.append(n)
-    return cuts
-
-
-@dataclass
-class ShardedResult:
-    x: object
-    iteration: int = 0
-    converged: bool = False
-    trace_history: list = field(default_factory=list)
-    branch_history: list = field(default_factory=list)
-    idempotency_history: list = field(default_factory=list)
-    cuts_history: list = field(default_factory=list)
-    local_work: list = field(default_factory=list)      # tasks this rank ran, per iteration
-    leaf_products: list = field(default_factory=list)   # full (all ranks) per iteration
-    seconds_per_iteration: list = field(default_factory=list)
-
-
-class ShardedSP2:
-    """SP2 with the multiply sharded over a torch.distributed process group."""
-
-    def __init__(self, engine, group=None):
-        import torch.distributed as dist
-        self.engine = engine
-        self.group = group
-        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
-        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
-
-    # -- collectives ---------------------------------------------------------
-    def _allgather_blocks(self, keys, blocks):
-        """Variable-size all-gather of (keys int64 [m], blocks f64 [m, nb, nb])."""
-        import torch
-        import torch.distributed as dist
-        if self.world == 1:
-            return keys, blocks
-        dev = blocks.device
-        m = torch.tensor([keys.numel()], dtype=torch.int64, device=dev)
-        sizes = [torch.zeros_like(m) for _ in range(self.world)]
-        dist.all_gather(sizes, m, group=self.group)
-        sizes = [int(s.item()) for s in sizes]
-        mx = max(sizes)
-        nb = blocks.shape[-1]
-        kp = torch.full((mx,), -1, dtype=torch.int64, device=dev)
-        bp = torch.zeros((mx, nb, nb), dtype=blocks.dtype, device=dev)
-        if keys.numel():
-            kp[: keys.numel()] = keys
-            bp[: keys.numel()] = blocks
-        kl = [torch.empty_like(kp) for _ in range(self.world)]
-        bl = [torch.empty_like(bp) for _ in range(self.world)]
-        dist.all_gather(kl, kp, group=self.group)
-        dist.all_gather(bl, bp, group=self.group)
-        keys = torch.cat([k[:s] for k, s in zip(kl, sizes)])
-        blocks = torch.cat([b[:s] for b, s in zip(bl, sizes)])
-        return keys, blocks
-
-    def _consistent_shard(self, x, tau, lo, hi):
-        """Shard multiply with one symmetric-path decision for all ranks: a
-        rank whose range meets a mirror ulp tie falls back to the full path, and
-        then every rank must (else mirrors and full-range blocks overlap)."""
-        import torch
-        import torch.distributed as dist
-        out = self.engine.multiply_shard(x, tau, lo, hi)
-        sym = getattr(self.engine, "last_symmetric", None)
-        if self.world == 1 or sym is None:
-            return out
-        flags = torch.tensor([1 if sym else 0, 1 if sym else 0], dtype=torch.int64,
-                             device=out[2].device)
-        flags[1] = -flags[1]
-        dist.all_reduce(flags, op=dist.ReduceOp.MIN, group=self.group)
-        any_full, all_full = int(flags[0]) == 0, int(-flags[1]) == 0
-        if any_full and not all_full:
-            out = self.engine.multiply_shard(x, tau, lo, hi, symmetric=False)
-        return out
-
-    def _allreduce_sum(self, t):
-        import torch.distributed as dist
-        if self.world > 1:
-            dist.all_reduce(t, group=self.group)
-        return t
-
-    # -- solve ---------------------------------------------------------------
-    def solve(self, f, n_occ: int, tau: float, max_iter: int = 100, criterion: str = "fro",
-              fro_tol: float = 1e-6, idem_tol: float = 1e-9) -> ShardedResult:
-        eng = self.engine
-        x = eng.init_x0(f)
-        n_pos = eng.grid(x) ** 2
-        cuts = even_cuts(n_pos, self.world)
-        res = ShardedResult(x=x)
-        res.trace_history.append(eng.trace(x))
-        want_idem = criterion == "fro"
-        for _ in range(max_iter):
-            t0 = time.perf_counter()
-            res.cuts_history.append(list(cuts))
-            lo, hi = cuts[self.rank], cuts[self.rank + 1]
-            keys, blocks, work, n_exec, n_full = self._consistent_shard(x, tau, lo, hi)
-            res.local_work.append(int(n_exec))
-            keys, blocks = self._allgather_blocks(keys, blocks)
-            x2 = eng.assemble(x, keys, blocks)
-            work = self._allreduce_sum(work)
-            counts = self._allreduce_sum(eng.scalar_tensor(n_full, like=work))
-            res.leaf_products.append(int(counts.item()))
-            # persistence load balancing: next cut from this iteration's tasks
-            cuts = partition_work(eng.to_numpy(work), self.world)
-            x_next, branch, t_x, t_sq, idem = eng.finish(x, x2, n_occ, want_idem)
-            if want_idem:
-                res.idempotency_history.append(idem)
-                done = idem < fro_tol
-            else:
-                done = abs(t_sq - t_x) < idem_tol and abs(t_x - n_occ) < 1e-6 * n_occ
-            if done:
-                res.converged = True
-                res.seconds_per_iteration.append(time.perf_counter() - t0)
-                break
-            x = x_next
-            res.iteration += 1
-            res.trace_history.append(eng.trace(x))
-            res.branch_history.append(branch)
-            res.seconds_per_iteration.append(time.perf_counter() - t0)
-        res.x = x
-        return res
+from .dist import even_cuts, partition_work  # noqa: E402  (shared host logic)
 
 
 def morton_positions(keys, g: int):
@@ -231,11 +77,21 @@ class ShardedMultiply:
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
 
     def globalize(self, local, symmetric: bool):
+        """All-reduce the leaf tier of norm^2 (and, for the INT8-sliced leaf
+        kernel, the row / column scale exponents with MAX) and install the
+        whole matrix's pyramid on the shard."""
         import torch.distributed as dist
         leaf = self.engine.leaf_norms2(local)
         if self.world > 1:
             dist.all_reduce(leaf, group=self.group)
         self.engine.set_pyramid(local, leaf, symmetric)
+        self.ex = None
+        ex = getattr(self.engine, "oz_exponents", lambda m: None)(local)
+        if ex is not None:
+            if self.world > 1:
+                for e in ex:
+                    dist.all_reduce(e, op=dist.ReduceOp.MAX, group=self.group)
+            self.ex = ex
         return leaf
 
     def balance(self, local, tau: float):
@@ -287,6 +143,8 @@ class ShardedMultiply:
         blocks_in = self._all_to_all(blocks_out, rc, sc, row=nb * nb).reshape(-1, nb, nb)
         t["exchange"] = time.perf_counter() - t0 - t["plan"]
         ext = eng.extend(local, req_keys, blocks_in, leaf, symmetric)
+        if getattr(self, "ex", None) is not None:   # the whole matrix's K4z row scales
+            eng.install_exponents(ext, *self.ex)
         c, leaf_products, executed = eng.multiply_range(ext, tau, lo, hi)
         t["total"] = time.perf_counter() - t0
         return ShardProduct(c=c, leaf_products=leaf_products, executed_products=executed,
@@ -302,73 +160,6 @@ class DeviceEngine:
 
     def grid(self, x):
         return x.n_blocks
-
-    def init_x0(self, f):
-        from .sp2 import _reserve_for, gershgorin_bounds, sp2_init
-        _reserve_for(f)
-        return sp2_init(f, gershgorin_bounds(f))
-
-    def trace(self, x):
-        from .quadtree import trace
-        return trace(x)
-
-    def multiply_shard(self, x, tau, lo, hi, symmetric=True):
-        import ctypes
-
-        import torch
-
-        from . import _native as nat
-        from .kernel import _check_tau, _leaf_kernel
-        from .quadtree import QuadTreeMatrix
-        tau = _check_tau(tau)
-        g = x.n_blocks
-        work = torch.zeros(g * g, dtype=torch.int32, device="cuda")
-        st = nat.Stats()
-        out = ctypes.c_void_p()
-        stream = nat.current_stream()
-        lib = nat.load()
-        if not symmetric:
-            lib.spamm_set_symmetric_products(0)
-        try:
-            nat.check(lib.spamm_multiply_range(x._h, x._h, tau, _leaf_kernel(self.kernel),
-                                               int(lo), int(hi), work.data_ptr(), stream,
-                                               ctypes.byref(out), ctypes.byref(st)))
-        finally:
-            if not symmetric:
-                lib.spamm_set_symmetric_products(1)
-        self.last_symmetric = bool(st.symmetric) or not x.symmetric
-        c = QuadTreeMatrix(out, stream)
-        keys = c.keys_device().clone()
-        blocks = c.blocks_device().clone()
-        return keys, blocks, work.to(torch.int64), int(st.executed_products), int(st.leaf_products)
-
-    def assemble(self, x, keys, blocks):
-        from .quadtree import QuadTreeMatrix
-        return QuadTreeMatrix.from_blocks(x.n_native, x.block_size, x.chunk_size, keys, blocks,
-                                          x.depth)
-
-    def finish(self, x, x2, n_occ, want_idem):
-        import ctypes
-
-        from . import _native as nat
-        from .quadtree import QuadTreeMatrix
-        from .sp2 import EXPAND, SQUARE
-        stream = nat.current_stream()
-        br = ctypes.c_int32()
-        t_x, t_sq, idem = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
-        e = ctypes.c_void_p()
-        nat.check(nat.load().spamm_sp2_finish(x._h, x2._h, float(n_occ), int(want_idem), stream,
-                                              ctypes.byref(br), ctypes.byref(t_x),
-                                              ctypes.byref(t_sq), ctypes.byref(idem),
-                                              ctypes.byref(e)))
-        if br.value == 0:
-            return x2, SQUARE, t_x.value, t_sq.value, (idem.value if want_idem else None)
-        return (QuadTreeMatrix(e, stream), EXPAND, t_x.value, t_sq.value,
-                idem.value if want_idem else None)
-
-    def scalar_tensor(self, v, like):
-        import torch
-        return torch.tensor([int(v)], dtype=torch.int64, device=like.device)
 
     def to_numpy(self, t):
         return t.cpu().numpy()
@@ -420,7 +211,10 @@ class DeviceEngine:
                                         ctypes.byref(n), stream))
         g = m.n_blocks
         ti, tk, tj = (x.to(torch.int64) for x in t)
-        return torch.unique(torch.cat([ti * g + tk, tk * g + tj]))
+        parts = [ti * g + tk, tk * g + tj]
+        if m.symmetric:                 # K4z's B operand on the symmetric path: X_jk^T
+            parts.append(tj * g + tk)
+        return torch.unique(torch.cat(parts))
 
     def gather(self, m, keys):
         import torch
@@ -447,6 +241,26 @@ class DeviceEngine:
         ext.set_global_pyramid(leaf, symmetric)
         return ext
 
+    def oz_exponents(self, m):
+        """K4z row / column exponents of the shard (None unless K4z applies)."""
+        import torch
+
+        from . import _native as nat
+        if self.kernel not in ("auto", "ozaki") or m.block_size not in (32, 64):
+            return None
+        out = []
+        for by_col in (0, 1):
+            ex = torch.empty(m.n_blocks * m.block_size, dtype=torch.int32, device="cuda")
+            nat.check(nat.load().spamm_mat_oz_exponents(m._h, by_col, ex.data_ptr(),
+                                                        nat.current_stream()))
+            out.append(ex)
+        return tuple(out)
+
+    def install_exponents(self, m, row, col):
+        from . import _native as nat
+        nat.check(nat.load().spamm_mat_set_oz_exponents(m._h, row.data_ptr(), col.data_ptr(),
+                                                        nat.current_stream()))
+
     def multiply_range(self, m, tau, lo, hi):
         import ctypes
 
@@ -461,147 +275,3 @@ class DeviceEngine:
                                                   None, stream, ctypes.byref(out),
                                                   ctypes.byref(st)))
         return QuadTreeMatrix(out, stream), int(st.leaf_products), int(st.executed_products)
-
-
-def morton_of_keys(keys: np.ndarray, g: int) -> np.ndarray:
-    """Morton position (row bit above column bit) of reference keys bi*G+bj."""
-    return morton_keys(np.asarray(keys) // g, np.asarray(keys) % g)
-
-
-# ---------------------------------------------------------------------------
-# Native sharded SP2 (the device path for N > 1)
-# ---------------------------------------------------------------------------
-
-def block_owners(keys, g: int, cut_pos) -> "torch.Tensor":
-    """Owner rank of every C block in a sharded SP2 product: the rank whose
-    Morton range holds the block's upper-triangle position (a rank computes
-    its upper blocks and writes their mirrors)."""
-    import torch
-    i, j = keys // g, keys % g
-    upper = torch.minimum(i, j) * g + torch.maximum(i, j)
-    inner = torch.as_tensor(list(cut_pos[1:-1]), dtype=torch.int64, device=keys.device)
-    return torch.searchsorted(inner, morton_positions(upper, g), right=True)
-
-
-def exchange_blocks(keys, blocks, g: int, cut_pos, group=None) -> dict:
-    """In-place all-gather of a sharded product's blocks: afterwards every
-    rank's ``blocks`` (storage order, same layout on every rank) holds every
-    rank's computed blocks.  One all_gather (NCCL on GPUs) of the owned blocks,
-    padded to the largest share."""
-    import torch
-    import torch.distributed as dist
-    world = dist.get_world_size(group) if dist.is_initialized() else 1
-    if world == 1 or blocks.shape[0] == 0:
-        return {"sent_blocks": 0, "received_blocks": 0}
-    rank = dist.get_rank(group)
-    owner = block_owners(keys, g, cut_pos)
-    counts = torch.bincount(owner, minlength=world).tolist()
-    mx = max(counts)
-    nb = blocks.shape[-1]
-    mine = owner == rank
-    send = torch.zeros((mx, nb, nb), dtype=blocks.dtype, device=blocks.device)
-    send[: counts[rank]] = blocks[mine]
-    out = torch.empty((world * mx, nb, nb), dtype=blocks.dtype, device=blocks.device)
-    dist.all_gather_into_tensor(out, send, group=group)
-    for r in range(world):
-        if r != rank and counts[r]:
-            blocks[owner == r] = out[r * mx: r * mx + counts[r]]
-    return {"sent_blocks": counts[rank], "received_blocks": sum(counts) - counts[rank]}
-
-
-class NativeShardedSP2:
-    """SP2 on N GPUs (one process per GPU), X replicated: per iteration every
-    rank runs the same dense cull (``spamm_sp2_multiply_shard``), computes the
-    leaf products of its contiguous run of C nodes -- cut by the current
-    iteration's task counts, so every rank gets the same work -- the owned
-    blocks are all-gathered (``exchange_blocks``), and the rest of the
-    iteration runs on every rank (``spamm_sp2_shard_finish``: traces, fused
-    residual, branch, update).  The trajectory is bitwise the single-GPU
-    ``sp2_solve``'s; at world size 1 it is that solve."""
-
-    def __init__(self, kernel: str = "auto", group=None):
-        import torch.distributed as dist
-        self.kernel = kernel
-        self.group = group
-        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
-        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
-
-    def multiply_shard(self, x, tau: float, rank: int | None = None, world: int | None = None):
-        import ctypes
-
-        from . import _native as nat
-        from .kernel import _check_tau, _leaf_kernel
-        from .quadtree import QuadTreeMatrix
-        rank = self.rank if rank is None else rank
-        world = self.world if world is None else world
-        st = nat.Stats()
-        out = ctypes.c_void_p()
-        cuts = (ctypes.c_int64 * (world + 1))()
-        stream = nat.current_stream()
-        nat.check(nat.load().spamm_sp2_multiply_shard(x._h, _check_tau(tau),
-                                                      _leaf_kernel(self.kernel), int(rank),
-                                                      int(world), stream, ctypes.byref(out),
-                                                      ctypes.cast(cuts, ctypes.c_void_p),
-                                                      ctypes.byref(st)))
-        self.last_executed = int(st.executed_products)   # the whole product's (all ranks)
-        return QuadTreeMatrix(out, stream), list(cuts), int(st.leaf_products)
-
-    def finish(self, x, c, n_occ: float, want_idem: bool):
-        import ctypes
-
-        from . import _native as nat
-        from .quadtree import QuadTreeMatrix
-        stream = nat.current_stream()
-        br = ctypes.c_int32()
-        t_x, t_sq, idem = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
-        e = ctypes.c_void_p()
-        nat.check(nat.load().spamm_sp2_shard_finish(x._h, c._h, float(n_occ), int(want_idem),
-                                                    stream, ctypes.byref(br), ctypes.byref(t_x),
-                                                    ctypes.byref(t_sq), ctypes.byref(idem),
-                                                    ctypes.byref(e)))
-        from .sp2 import EXPAND, SQUARE
-        c._refresh()
-        nxt = QuadTreeMatrix(e, stream) if e.value else c
-        return (nxt, SQUARE if br.value == 0 else EXPAND, t_x.value, t_sq.value,
-                idem.value if want_idem else None)
-
-    def solve(self, f, n_occ: int, tau: float, max_iter: int = 100, criterion: str = "fro",
-              fro_tol: float = 1e-6, idem_tol: float = 1e-9) -> ShardedResult:
-        from .quadtree import trace
-        from .sp2 import _reserve_for, gershgorin_bounds, sp2_init
-        _reserve_for(f)
-        x = sp2_init(f, gershgorin_bounds(f))
-        g = x.n_blocks
-        res = ShardedResult(x=x)
-        res.trace_history.append(trace(x))
-        want_idem = criterion == "fro"
-        pending = False
-        for _ in range(max_iter):
-            t0 = time.perf_counter()
-            c, cuts, leaf = self.multiply_shard(x, tau)
-            res.cuts_history.append(cuts)
-            res.leaf_products.append(leaf)
-            # cuts give every rank an equal share of the executed products
-            res.local_work.append(self.last_executed // self.world)
-            exchange_blocks(c.keys_device(), c.blocks_device(), g, cuts, self.group)
-            nxt, branch, t_x, t_sq, idem = self.finish(x, c, n_occ, want_idem)
-            if pending:
-                res.trace_history.append(t_x)
-                pending = False
-            if want_idem:
-                res.idempotency_history.append(idem)
-                done = idem < fro_tol
-            else:
-                done = abs(t_sq - t_x) < idem_tol and abs(t_x - n_occ) < 1e-6 * n_occ
-            res.seconds_per_iteration.append(time.perf_counter() - t0)
-            if done:
-                res.converged = True
-                break
-            x = nxt
-            res.iteration += 1
-            res.branch_history.append(branch)
-            pending = True
-        if pending:
-            res.trace_history.append(trace(x))
-        res.x = x
-        return res

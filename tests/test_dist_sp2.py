@@ -21,7 +21,7 @@ from oracle import spamm_oracle as O
 from paper_1403_7458_b200.dist import (POS, UPPER, DistributedSP2, even_cuts, owners,
                                        partition_work, pyramid_root2, seq_sum)
 from paper_1403_7458_b200.synth import water_cluster
-from paper_1403_7458_b200.synth_morton import morton_keys
+from paper_1403_7458_b200.synth_morton import morton_decode, morton_keys
 
 
 @dataclass
@@ -348,3 +348,12 @@ def test_partition_work_properties():
         assert sum(parts) == w.sum()
         assert max(parts) - w.sum() / world <= w.max()
     assert partition_work(np.zeros(64, dtype=np.int64), 4) == even_cuts(64, 4)
+
+
+def test_morton_helpers_roundtrip():
+    i, j = np.meshgrid(np.arange(16), np.arange(16), indexing="ij")
+    m = morton_keys(i.ravel(), j.ravel())
+    assert sorted(m.tolist()) == list(range(256))
+    ii, jj = morton_decode(m)
+    assert np.array_equal(ii, i.ravel()) and np.array_equal(jj, j.ravel())
+    assert morton_keys(1, 0) == 2 and morton_keys(0, 1) == 1   # row bit above column bit

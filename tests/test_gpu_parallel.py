@@ -1,6 +1,8 @@
-"""Device side of the multi-GPU path on one GPU: shard multiplies
-(spamm_multiply_range) must tile the full product exactly, and the sharded
-SP2 driver with the device engine must reproduce sp2_solve bitwise."""
+"""Device side of the multi-GPU paths on one GPU: range multiplies (the
+dense cull over a Morton range, spamm_multiply_range) must tile the full
+product exactly, their work vectors balance the next cut, and the
+distributed-operand pieces (ShardedMultiply, config 5) reproduce the
+single-GPU product bitwise -- with the K4z row scales all-reduced."""
 
 import numpy as np
 import pytest
@@ -11,13 +13,15 @@ from conftest import pyramid_flat
 pytestmark = pytest.mark.gpu
 
 import paper_1403_7458_b200 as sp  # noqa: E402
-from paper_1403_7458_b200.parallel import DeviceEngine, ShardedSP2, even_cuts, partition_work  # noqa: E402
+from paper_1403_7458_b200.dist import DeviceShardEngine, owners  # noqa: E402
+from paper_1403_7458_b200.parallel import DeviceEngine, even_cuts, partition_work  # noqa: E402
 from paper_1403_7458_b200.synth import CONFIGS, water_cluster  # noqa: E402
 
 
 @pytest.mark.parametrize("symmetric", [True, False])
-def test_shards_tile_the_full_product(rng, symmetric):
-    n, nb = 300, 16
+@pytest.mark.parametrize("nb", [16, 64])
+def test_range_products_tile_the_full_product(rng, symmetric, nb):
+    n = 300 if nb == 16 else 1000
     d = rng.standard_normal((n, n)) * np.exp(-0.02 * np.abs(np.subtract.outer(np.arange(n),
                                                                               np.arange(n))))
     if symmetric:
@@ -26,16 +30,20 @@ def test_shards_tile_the_full_product(rng, symmetric):
     assert x.symmetric == symmetric
     tau = 1e-3
     full, st = sp.multiply(x, x, tau)
-    eng = DeviceEngine()
+    eng = DeviceShardEngine()
     g = x.n_blocks
+    mode = "upper" if symmetric else "pos"
     for world in (1, 3, 5):
         keys, blocks, leaf, execd = [], [], 0, 0
         work_tot = torch.zeros(g * g, dtype=torch.int64, device="cuda")
-        for r, (lo, hi) in enumerate(zip(even_cuts(g * g, world), even_cuts(g * g, world)[1:])):
-            k, b, w, n_exec, n_full = eng.multiply_shard(x, tau, lo, hi)
+        cuts = even_cuts(g * g, world)
+        for r in range(world):
+            c, w, n_full, n_exec = eng.multiply_range(x, tau, cuts[r], cuts[r + 1], symmetric)
+            k = c.keys_device().clone()
+            assert bool((owners(k, g, cuts, mode) == r).all())    # exactly the owned blocks
             keys.append(k)
-            blocks.append(b)
-            work_tot += w
+            blocks.append(c.blocks_device().clone())
+            work_tot += w.to(torch.int64)
             leaf += n_full
             execd += n_exec
         keys = torch.cat(keys)
@@ -47,28 +55,15 @@ def test_shards_tile_the_full_product(rng, symmetric):
         assert int(work_tot.sum()) == st.executed_products
 
 
-def test_device_engine_sharded_solve_world1_matches_sp2_solve():
-    cfg = CONFIGS[3]
-    h, n_occ = water_cluster(cfg.n_mol, seed=0)
-    f = sp.build_from_dense(h, cfg.block_size)
-    p, st = sp.sp2_solve(f, n_occ, cfg.tau, criterion="fro")
-    res = ShardedSP2(DeviceEngine()).solve(f, n_occ, cfg.tau, criterion="fro")
-    assert res.iteration == st.iteration and res.converged
-    assert res.trace_history == st.trace_history
-    assert res.idempotency_history == st.idempotency_history
-    assert np.array_equal(sp.to_dense(res.x), sp.to_dense(p))
-    assert res.leaf_products == list(st.leaf_products)
-
-
 def test_persistence_cuts_balance_cfg4_work():
     """Cuts from one iteration's measured task counts balance the next one."""
     cfg = CONFIGS[4]
     h, _ = water_cluster(cfg.n_mol, seed=0)
     f = sp.build_from_dense(h, cfg.block_size)
     x = sp.sp2_init(f, sp.gershgorin_bounds(f))
-    eng = DeviceEngine()
+    eng = DeviceShardEngine()
     g = x.n_blocks
-    _, _, work, n_exec, _ = eng.multiply_shard(x, cfg.tau, 0, g * g)
+    _, work, _, n_exec = eng.multiply_range(x, cfg.tau, 0, g * g, True)
     w = work.cpu().numpy()
     for world in (2, 4, 8):
         cuts = partition_work(w, world)
@@ -90,6 +85,10 @@ def _shard_run(full, shards, tau, sym, leaf=None):
         leaf = sum(eng.leaf_norms2(s) for s in shards)
     for s in shards:
         eng.set_pyramid(s, leaf, sym)
+    ex = None
+    if eng.oz_exponents(shards[0]) is not None:     # K4z: the whole matrix's row scales
+        exs = [eng.oz_exponents(s) for s in shards]
+        ex = tuple(torch.stack([e[i] for e in exs]).max(0).values for i in range(2))
     work, sym_ok = eng.census_work(shards[0], tau)
     cuts = partition_work(eng.to_numpy(work), len(shards))
     if sym and not sym_ok:           # a mirror ulp tie somewhere: every shard runs the full path
@@ -107,11 +106,14 @@ def _shard_run(full, shards, tau, sym, leaf=None):
             if bool(hit.any()):
                 blocks.append((halo[hit], eng.gather(o, halo[hit])))
         hk = torch.cat([k for k, _ in blocks]) if blocks else halo
-        hb = torch.cat([b for _, b in blocks]) if blocks else torch.empty((0, 16, 16),
+        nb = full.block_size
+        hb = torch.cat([b for _, b in blocks]) if blocks else torch.empty((0, nb, nb),
                                                                           dtype=torch.float64,
                                                                           device="cuda")
         assert hk.numel() == halo.numel()
         ext = eng.extend(s, hk, hb, leaf, sym)
+        if ex is not None:
+            eng.install_exponents(ext, *ex)
         c, lp, _ = eng.multiply_range(ext, tau, cuts[r], cuts[r + 1])
         out_k.append(c.keys_device().clone())
         out_b.append(c.blocks_device().clone())
@@ -119,13 +121,15 @@ def _shard_run(full, shards, tau, sym, leaf=None):
     return torch.cat(out_k), torch.cat(out_b), leaf_total
 
 
-@pytest.mark.parametrize("nshards", [2, 3])
-def test_distributed_operand_shards_reproduce_product(nshards):
+@pytest.mark.parametrize("nshards,nb", [(2, 16), (3, 16), (3, 64)])
+def test_distributed_operand_shards_reproduce_product(nshards, nb):
+    """nb = 64 runs K4z: bitwise only because the shards' row scales are
+    the whole matrix's (the halo alone would give other exponents)."""
     import torch
     from paper_1403_7458_b200.parallel import even_cuts, morton_positions
     from paper_1403_7458_b200.synth import water_cluster
-    h, _ = water_cluster(20, seed=6)
-    full = sp.build_from_dense(h, 16)
+    h, _ = water_cluster(20 if nb == 16 else 60, seed=6)
+    full = sp.build_from_dense(h, nb)
     assert full.symmetric
     tau = 1e-6
     ref, st = sp.multiply(full, full, tau)
@@ -136,7 +140,7 @@ def test_distributed_operand_shards_reproduce_product(nshards):
     shards = []
     for r in range(nshards):
         m = (mk >= own_cuts[r]) & (mk < own_cuts[r + 1])
-        shards.append(sp.QuadTreeMatrix.from_blocks(full.n_native, 16, full.chunk_size,
+        shards.append(sp.QuadTreeMatrix.from_blocks(full.n_native, nb, full.chunk_size,
                                                     keys[m], blocks[m], full.depth))
     ck, cb, lp = _shard_run(full, shards, tau, True)
     assert lp == st.leaf_products
@@ -173,51 +177,3 @@ def test_cluster_shards_match_whole_matrix():
     assert lp == st.leaf_products
     o, ro = torch.argsort(ck), torch.argsort(ref.keys_device())
     assert torch.equal(cb[o], ref.blocks_device()[ro])
-
-
-# -- native sharded SP2 (the N-GPU device path) ---------------------------------
-
-@pytest.mark.parametrize("cfg_index", [3, 4])
-def test_native_sharded_world1_is_sp2_solve(cfg_index):
-    from paper_1403_7458_b200.parallel import NativeShardedSP2
-    cfg = CONFIGS[cfg_index]
-    h, n_occ = water_cluster(cfg.n_mol, seed=0)
-    f = sp.build_from_dense(h, cfg.block_size)
-    res = NativeShardedSP2().solve(f, n_occ, cfg.tau, criterion="fro", fro_tol=1e-6)
-    p, st = sp.sp2_solve(f, n_occ, cfg.tau, criterion="fro", fro_tol=1e-6)
-    assert res.iteration == st.iteration and res.converged == st.converged
-    assert res.branch_history == st.branch_history
-    assert res.trace_history == st.trace_history
-    assert res.idempotency_history == st.idempotency_history
-    assert res.leaf_products == list(st.leaf_products)
-    assert np.array_equal(sp.to_dense(res.x), sp.to_dense(p))
-
-
-@pytest.mark.parametrize("world", [2, 3, 5])
-def test_native_sharded_ranks_rebuild_the_product(world):
-    """Every rank's share, merged by ownership, is bitwise the single-GPU step
-    (ranks run one after another here; NCCL moves the shares on N GPUs)."""
-    import torch
-    from paper_1403_7458_b200.parallel import NativeShardedSP2, block_owners
-    cfg = CONFIGS[4]
-    h, n_occ = water_cluster(cfg.n_mol, seed=0)
-    f = sp.build_from_dense(h, cfg.block_size)
-    x = sp.sp2_init(f, sp.gershgorin_bounds(f))
-    drv = NativeShardedSP2()
-    g = x.n_blocks
-    for it in range(4):
-        shares = [drv.multiply_shard(x, cfg.tau, rank=r, world=world) for r in range(world)]
-        c0, cuts, _ = shares[0]
-        assert all(s[1] == cuts for s in shares)                 # same cut on every rank
-        owner = block_owners(c0.keys_device(), g, cuts)
-        merged = c0.blocks_device()
-        for r in range(1, world):
-            mine = owner == r
-            merged[mine] = shares[r][0].blocks_device()[mine]
-        counts = torch.bincount(owner, minlength=world).tolist()
-        assert min(counts) > 0
-        nxt, br, t_x, t_sq, idem = drv.finish(x, c0, n_occ, True)
-        ref, rbr = sp.sp2_step(x, n_occ, cfg.tau)
-        assert br == rbr
-        assert np.array_equal(sp.to_dense(nxt), sp.to_dense(ref))
-        x = nxt

@@ -177,45 +177,3 @@ def test_sharded_multiply_gloo_world2_bitwise(tmp_path):
     assert np.array_equal(outs[0]["cuts"], outs[1]["cuts"])
     e0, e1 = int(outs[0]["executed"]), int(outs[1]["executed"])
     assert abs(e0 - e1) <= 0.2 * (e0 + e1)                # census-balanced shards
-
-
-# -- native sharded SP2: the block exchange ------------------------------------
-
-def _exchange_worker(rank, world, port, g, nb, out_dir):
-    import torch.distributed as dist
-    from paper_1403_7458_b200.parallel import block_owners, exchange_blocks
-    os.environ["MASTER_ADDR"] = "127.0.0.1"
-    os.environ["MASTER_PORT"] = str(port)
-    dist.init_process_group("gloo", rank=rank, world_size=world)
-    try:
-        r = np.random.default_rng(7)
-        keys = np.sort(r.choice(g * g, size=150, replace=False)).astype(np.int64)
-        truth = r.standard_normal((150, nb, nb))
-        cuts = [0, 170, 600, g * g]                       # 3 ranks, uneven shares
-        kt = torch.from_numpy(keys)
-        owner = block_owners(kt, g, cuts).numpy()
-        blocks = np.where((owner == rank)[:, None, None], truth, 0.0)   # only own blocks computed
-        bt = torch.from_numpy(blocks.copy())
-        info = exchange_blocks(kt, bt, g, cuts)
-        np.savez(os.path.join(out_dir, f"x{rank}.npz"), blocks=bt.numpy(), truth=truth,
-                 owner=owner, sent=info["sent_blocks"])
-    finally:
-        dist.destroy_process_group()
-
-
-def test_native_sharded_exchange_gloo_world3(tmp_path):
-    g, nb = 32, 4
-    port = _free_port()
-    torch.multiprocessing.spawn(_exchange_worker, args=(3, port, g, nb, str(tmp_path)), nprocs=3,
-                                join=True)
-    outs = [np.load(tmp_path / f"x{r}.npz") for r in range(3)]
-    for r, o in enumerate(outs):
-        assert np.array_equal(o["blocks"], o["truth"])          # every block everywhere
-        assert int(o["sent"]) == int((o["owner"] == r).sum())
-    # ownership follows the upper-triangle position: a block and its mirror agree
-    from paper_1403_7458_b200.parallel import block_owners
-    i, j = np.meshgrid(np.arange(g), np.arange(g), indexing="ij")
-    k = torch.from_numpy((i * g + j).ravel())
-    km = torch.from_numpy((j * g + i).ravel())
-    assert torch.equal(block_owners(k, g, [0, 170, 600, g * g]),
-                       block_owners(km, g, [0, 170, 600, g * g]))
