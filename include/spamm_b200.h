@@ -144,6 +144,9 @@ int spamm_mat_set_oz_exponents(spamm_mat* m, const int32_t* ex_row, const int32_
 int spamm_mat_identity(int64_t n, int32_t block_size, int64_t chunk_size, void* stream,
                        spamm_mat** out);
 int spamm_mat_info_get(const spamm_mat* m, spamm_mat_info* info);
+/* Geometry and symmetry only, without settling a lazily pruned product (no
+ * host sync): `stored` is -1 and data / keys / slot are NULL. */
+int spamm_mat_info_peek(const spamm_mat* m, spamm_mat_info* info);
 int spamm_mat_free(spamm_mat* m);
 /* to_dense (quadtree.py:245-252): dense n_native x n_native, leading dim ld. */
 int spamm_mat_to_dense(const spamm_mat* m, double* dense, int64_t ld, void* stream);

@@ -88,6 +88,7 @@ _SIGS = {
     "spamm_mat_set_oz_exponents": (c_i32, [c_vp, c_vp, c_vp, c_vp]),
     "spamm_mat_identity": (c_i32, [c_i64, c_i32, c_i64, c_vp, ctypes.POINTER(c_vp)]),
     "spamm_mat_info_get": (c_i32, [c_vp, ctypes.POINTER(MatInfo)]),
+    "spamm_mat_info_peek": (c_i32, [c_vp, ctypes.POINTER(MatInfo)]),
     "spamm_mat_free": (c_i32, [c_vp]),
     "spamm_mat_to_dense": (c_i32, [c_vp, c_vp, c_i64, c_vp]),
     "spamm_multiply": (c_i32, [c_vp, c_vp, c_f64, c_i32, c_i32, c_vp, ctypes.POINTER(c_vp),

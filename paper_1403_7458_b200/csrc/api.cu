@@ -422,6 +422,23 @@ int spamm_mat_identity(int64_t n, int32_t block_size, int64_t chunk_size, void* 
   SPAMM_API_END
 }
 
+int spamm_mat_info_peek(const spamm_mat* h, spamm_mat_info* info) {
+  if (!h || !info) return fail(SPAMM_EINVAL, "null argument");
+  info->n_native = h->m.n_native;
+  info->block_size = h->m.nb;
+  info->depth = h->m.depth;
+  info->chunk_size = h->m.chunk_size;
+  info->n_blocks = h->m.G;
+  info->stored = -1;  // unknown until settled (lazy prune)
+  info->data = nullptr;
+  info->keys = nullptr;
+  info->slot = nullptr;
+  info->norms = h->m.norms;
+  info->norms2 = h->m.norms2;
+  info->symmetric = h->m.sym ? 1 : 0;
+  return SPAMM_OK;
+}
+
 int spamm_mat_info_get(const spamm_mat* h, spamm_mat_info* info) {
   if (!h || !info) return fail(SPAMM_EINVAL, "null argument");
   if (h->m.pend_nz) {  // never expose a lazily pruned matrix
@@ -512,25 +529,27 @@ bool auto_ozaki_for(int nb) {
 // K4 dispatch: the INT8-sliced kernel takes the operand matrices (row / column
 // exponents from their keys), the others the block arrays.  AUTO picks it for
 // Nb = 64 (faster than DMMA and closer to the exact product), DMMA otherwise.
-void leaf_dispatch(int64_t n, const int64_t* seg, const int32_t* ai, const int32_t* bi,
+// Returns true when K4z ran (then ex_out, if given, holds C's row exponents).
+bool leaf_dispatch(int64_t n, const int64_t* seg, const int32_t* ai, const int32_t* bi,
                    const int64_t* c_out, const int64_t* c_mirror, const spamm_mat* a,
                    const spamm_mat* b, double* C, int32_t kernel, cudaStream_t s,
-                   spamm::LptSchedule lpt) {
+                   spamm::LptSchedule lpt, int* ex_out = nullptr) {
   const bool auto_ozaki = auto_ozaki_enabled();
   const bool sym_b = a == b && a->m.sym;
   if (kernel == spamm::LEAF_OZAKI) {
     spamm::leaf_products_ozaki<int32_t>(n, seg, ai, bi, c_out, c_mirror, false, a->m, b->m,
-                                        sym_b, C, s, lpt);
-    return;
+                                        sym_b, C, s, lpt, false, ex_out);
+    return true;
   }
   // AUTO also needs room for the digit slices (the operands' size again): a
   // matrix that nearly fills HBM (config 5 on one GPU) stays on DMMA.
   if (kernel == spamm::LEAF_AUTO && auto_ozaki && auto_ozaki_for(a->m.nb) &&
       spamm::leaf_products_ozaki<int32_t>(n, seg, ai, bi, c_out, c_mirror, false, a->m, b->m,
-                                          sym_b, C, s, lpt, /*try_only=*/true))
-    return;
+                                          sym_b, C, s, lpt, /*try_only=*/true, ex_out))
+    return true;
   spamm::leaf_products<int32_t>(n, seg, ai, bi, c_out, c_mirror, false, a->m.data, a->m.nblocks,
                                   b->m.data, b->m.nblocks, C, a->m.nb, kernel, s, lpt);
+  return false;
 }
 
 // K4z's operand pre-passes (row exponents, digit slices) depend only on the
@@ -665,6 +684,19 @@ void multiply_impl(const spamm_mat* a, const spamm_mat* b, double tau, int32_t k
     }
   }
   C.data = spamm::dmalloc<double>((size_t)C.nblocks * nb2, s);
+  // A symmetric product on K4z also yields its own K4z row exponents (the
+  // epilogue's row / mirror-column maxima), so a multiply on C -- the next
+  // SP2 iteration after SQUARE -- skips the exponent pass.
+  int* ex_out = nullptr;
+  const bool k4z_possible = kernel == spamm::LEAF_OZAKI ||
+                            (kernel == spamm::LEAF_AUTO && auto_ozaki_enabled() &&
+                             auto_ozaki_for(a->m.nb));
+  if (sym && r.n_c > 0 && k4z_possible && spamm::ozaki_supported(C.nb) &&
+      !getenv("SPAMM_OZ_NO_EXOUT")) {
+    ex_out = spamm::dmalloc<int>(C.G * C.nb, s);
+    SPAMM_CK(cudaMemsetAsync(ex_out, 0x80, C.G * C.nb * sizeof(int), s));
+  }
+  bool ex_done = false;
   if (g_side) g_side->window(s);  // PCIe chunk alongside K4
   tm.mark(1);  // leaf window = the K4 launch only (allocation stays outside)
   if (oz.ok) {  // K4z on the operands prepared alongside the cull
@@ -675,7 +707,8 @@ void multiply_impl(const spamm_mat* a, const spamm_mat* b, double tau, int32_t k
       lpt.order = r.order;
       lpt.counter = r.counter;
       spamm::ozaki_launch<int32_t>(r.n_c, r.seg, r.a_idx, r.b_idx, c_out, c_mirror, false,
-                                   a->m, b->m, oz.op, C.data, s, lpt);
+                                   a->m, b->m, oz.op, C.data, s, lpt, ex_out);
+      ex_done = ex_out != nullptr;
     }
     spamm::ozaki_release(oz.op, s);
     oz.ok = false;
@@ -683,7 +716,13 @@ void multiply_impl(const spamm_mat* a, const spamm_mat* b, double tau, int32_t k
     spamm::LptSchedule lpt;
     lpt.order = r.order;
     lpt.counter = r.counter;
-    leaf_dispatch(r.n_c, r.seg, r.a_idx, r.b_idx, c_out, c_mirror, a, b, C.data, kernel, s, lpt);
+    ex_done = leaf_dispatch(r.n_c, r.seg, r.a_idx, r.b_idx, c_out, c_mirror, a, b, C.data,
+                            kernel, s, lpt, ex_out) && ex_out != nullptr;
+  }
+  if (ex_done) {
+    C.oz_ex_row = ex_out;
+  } else {
+    spamm::dfree(ex_out, s);
   }
   tm.mark(2);
   spamm::htrace("mul_k4");

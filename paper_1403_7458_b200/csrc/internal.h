@@ -236,14 +236,18 @@ void oz32_operand_passes(const Mat& M, bool trans, int* ex, int8_t* out, cudaStr
 template <class Idx>
 void oz32_launch(int64_t n_seg, const int64_t* seg, const Idx* a_idx, const Idx* b_idx,
                  const int64_t* c_out, const int64_t* c_mirror, bool accumulate, const Mat& A,
-                 const Mat& B, const OzakiOperands& op, double* C, cudaStream_t s, int* counter);
+                 const Mat& B, const OzakiOperands& op, double* C, cudaStream_t s, int* counter,
+                 int* ex_out = nullptr);
 bool ozaki_prepare(const Mat& A, const Mat& B, bool sym_b, cudaStream_t s, OzakiOperands& op,
                    bool try_only);
 template <class Idx>
+// ex_out (optional, G * nb ints preset to the 0x80 pattern): receives the K4z
+// row exponents of the product C (symmetric products: rows and, through the
+// mirrors, columns), so a following multiply on C skips its exponent pass.
 void ozaki_launch(int64_t n_seg, const int64_t* seg, const Idx* a_idx, const Idx* b_idx,
                   const int64_t* c_out, const int64_t* c_mirror, bool accumulate, const Mat& A,
                   const Mat& B, const OzakiOperands& op, double* C, cudaStream_t s,
-                  LptSchedule lpt = {});
+                  LptSchedule lpt = {}, int* ex_out = nullptr);
 void ozaki_release(OzakiOperands& op, cudaStream_t s);
 // Free this thread's kept slice buffer on the current device (if idle).
 void ozaki_cache_trim();
@@ -256,7 +260,7 @@ template <class Idx>
 bool leaf_products_ozaki(int64_t n_seg, const int64_t* seg, const Idx* a_idx, const Idx* b_idx,
                          const int64_t* c_out, const int64_t* c_mirror, bool accumulate,
                          const Mat& A, const Mat& B, bool sym_b, double* C, cudaStream_t s,
-                         LptSchedule lpt = {}, bool try_only = false);
+                         LptSchedule lpt = {}, bool try_only = false, int* ex_out = nullptr);
 template <class Idx>
 void leaf_products_tma(int64_t n_seg, const int64_t* seg, const Idx* a_idx, const Idx* b_idx,
                        const int64_t* c_out, const int64_t* c_mirror, bool accumulate,

@@ -208,7 +208,8 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
                  const int64_t* __restrict__ c_out, const int64_t* __restrict__ c_mirror,
                  int accumulate, double* __restrict__ C, const int32_t* __restrict__ order,
                  int* __restrict__ next_block, int hint, long long* __restrict__ prof,
-                 const double* __restrict__ Ad, const double* __restrict__ Bd) {
+                 const double* __restrict__ Ad, const double* __restrict__ Bd,
+                 int* __restrict__ ex_out) {
   pdl_wait();
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
@@ -418,6 +419,12 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
       double* Cb = C + (c_out ? c_out[m] : m) * (int64_t)(OZ_NB * OZ_NB);
       const int64_t mi = c_mirror ? c_mirror[m] : -1;
       double* Cm = mi >= 0 ? C + mi * (int64_t)(OZ_NB * OZ_NB) : nullptr;
+      // ex_out (symmetric X^2): the K4z row exponents of the product itself,
+      // so the next multiply skips its exponent pass -- this thread's row max
+      // over its columns, and per column the max over the warp's 32 rows
+      // (the rows of the mirror block)
+      const bool want_ex = ex_out != nullptr && seg_end;
+      double rmax = 0.0;
 #pragma unroll 1
       for (int cl = 0; cl < 4; ++cl) {
         const int cc = grp * 4 + cl;
@@ -507,6 +514,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
             }
             rp[c] = v;
             if (Cm) Cm[(col0 + c) * OZ_NB + r] = v;
+            res[c] = v;
           }
         } else {
           if (cont) {
@@ -530,8 +538,18 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
               for (int c = 0; c < 4; ++c) Cm[(col0 + c) * OZ_NB + r] = res[c];
           }
         }
+        if (want_ex) {
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const double v = oz_absf(res[c]);
+            rmax = fmax(rmax, v);
+            const unsigned mx = __reduce_max_sync(0xffffffffu, oz_ex_code(v));
+            if (lane == 0 && mx && Cm) atomicMax(ex_out + bj * OZ_NB + col0 + c, oz_ex_decode(mx));
+          }
+        }
         asm volatile("bar.sync %0, 128;\n" ::"r"(1 + grp) : "memory");
       }
+      if (want_ex && rmax > 0.0) atomicMax(ex_out + bi * OZ_NB + r, oz_exp_of(rmax));
       if (prof && threadIdx.x == 0) {
         e_all += clock64() - te0;
         ++n_blk;
@@ -779,7 +797,7 @@ template <class Idx>
 void ozaki_launch(int64_t n_seg, const int64_t* seg, const Idx* a_idx, const Idx* b_idx,
                   const int64_t* c_out, const int64_t* c_mirror, bool accumulate, const Mat& A,
                   const Mat& B, const OzakiOperands& op, double* C, cudaStream_t s,
-                  LptSchedule lpt) {
+                  LptSchedule lpt, int* ex_out) {
   if (n_seg <= 0) return;
   const int32_t* order = lpt.order;
   int* counter = lpt.counter;
@@ -802,7 +820,7 @@ void ozaki_launch(int64_t n_seg, const int64_t* seg, const Idx* a_idx, const Idx
   }
   if (op.nb == 32) {
     oz32_launch<Idx>(n_seg, seg, a_idx, b_idx, c_out, c_mirror, accumulate, A, B, op, C, s,
-                     counter);
+                     counter, ex_out);
     dfree(scratch, s);
     return;
   }
@@ -828,7 +846,7 @@ void ozaki_launch(int64_t n_seg, const int64_t* seg, const Idx* a_idx, const Idx
              (const int32_t*)op.b_tr, (const int64_t*)A.keys, (const int64_t*)B.keys, op.G,
              (const int8_t*)op.as, (const int8_t*)op.bs, (const int*)op.ex_a, (const int*)op.ex_b,
              c_out, c_mirror, accumulate ? 1 : 0, C, order, counter, hint, prof,
-             (const double*)A.data, (const double*)B.data);
+             (const double*)A.data, (const double*)B.data, ex_out);
   SPAMM_LAUNCH_CK();
   oz_dbg("k4z", s);
   if (prof) {  // SPAMM_K4Z_PROF=1: per-launch cycle breakdown (diagnostics; syncs)
@@ -851,25 +869,27 @@ template <class Idx>
 bool leaf_products_ozaki(int64_t n_seg, const int64_t* seg, const Idx* a_idx, const Idx* b_idx,
                          const int64_t* c_out, const int64_t* c_mirror, bool accumulate,
                          const Mat& A, const Mat& B, bool sym_b, double* C, cudaStream_t s,
-                         LptSchedule lpt, bool try_only) {
+                         LptSchedule lpt, bool try_only, int* ex_out) {
   if (n_seg <= 0) return true;
   OzakiOperands op;
   if (!ozaki_prepare(A, B, sym_b, s, op, try_only)) return false;
-  ozaki_launch<Idx>(n_seg, seg, a_idx, b_idx, c_out, c_mirror, accumulate, A, B, op, C, s, lpt);
+  ozaki_launch<Idx>(n_seg, seg, a_idx, b_idx, c_out, c_mirror, accumulate, A, B, op, C, s, lpt,
+                    ex_out);
   ozaki_release(op, s);
   return true;
 }
 
 template void ozaki_launch<int32_t>(int64_t, const int64_t*, const int32_t*, const int32_t*,
                                     const int64_t*, const int64_t*, bool, const Mat&, const Mat&,
-                                    const OzakiOperands&, double*, cudaStream_t, LptSchedule);
+                                    const OzakiOperands&, double*, cudaStream_t, LptSchedule,
+                                    int*);
 template bool leaf_products_ozaki<int32_t>(int64_t, const int64_t*, const int32_t*,
                                            const int32_t*, const int64_t*, const int64_t*, bool,
                                            const Mat&, const Mat&, bool, double*, cudaStream_t,
-                                           LptSchedule, bool);
+                                           LptSchedule, bool, int*);
 template bool leaf_products_ozaki<int64_t>(int64_t, const int64_t*, const int64_t*,
                                            const int64_t*, const int64_t*, const int64_t*, bool,
                                            const Mat&, const Mat&, bool, double*, cudaStream_t,
-                                           LptSchedule, bool);
+                                           LptSchedule, bool, int*);
 
 }  // namespace spamm

@@ -157,7 +157,7 @@ __global__ void __launch_bounds__(Z_THREADS, NBUF == 2 ? 1 : 2)
                    const int64_t* __restrict__ c_out, const int64_t* __restrict__ c_mirror,
                    int accumulate, double* __restrict__ C, const int32_t* __restrict__ order,
                    int* __restrict__ next_block, const double* __restrict__ Ad,
-                   const double* __restrict__ Bd) {
+                   const double* __restrict__ Bd, int* __restrict__ ex_out) {
   pdl_wait();
   constexpr int Z_STAGE = ZCfg<NBUF, Z_TPS, Z_STAGES>::STAGE;
   constexpr uint32_t TCOLS = 256u * NBUF;
@@ -346,6 +346,9 @@ __global__ void __launch_bounds__(Z_THREADS, NBUF == 2 ? 1 : 2)
       const int64_t mi = c_mirror ? c_mirror[m] : -1;
       double* Cm = mi >= 0 ? C + mi * (int64_t)(Z_NB * Z_NB) : nullptr;
       const uint32_t tb = lane_base + 256u * b;
+      // ex_out: the product's own row exponents (see leaf_ozaki.cu)
+      const bool want_ex = ex_out != nullptr && seg_end;
+      double rmax = 0.0;
 #pragma unroll 1
       for (int cc = 0; cc < 4; ++cc) {
         int V[2][4][8];  // [tile][j][c8] of TMEM lane (w, r)
@@ -417,6 +420,7 @@ __global__ void __launch_bounds__(Z_THREADS, NBUF == 2 ? 1 : 2)
             }
             rp[h] = v;
             if (Cm) Cm[(col0 + h) * Z_NB + r] = v;
+            res[h] = v;
           }
         } else {
           if (cont) {
@@ -430,8 +434,18 @@ __global__ void __launch_bounds__(Z_THREADS, NBUF == 2 ? 1 : 2)
             Cm[(col0 + 1) * Z_NB + r] = res[1];
           }
         }
+        if (want_ex) {  // lane = row: a column's max over the warp is the block's
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const double v = oz_absf(res[h]);
+            rmax = fmax(rmax, v);
+            const unsigned mx = __reduce_max_sync(0xffffffffu, oz_ex_code(v));
+            if (lane == 0 && mx && Cm) atomicMax(ex_out + bj * Z_NB + col0 + h, oz_ex_decode(mx));
+          }
+        }
         asm volatile("bar.sync 1, 128;\n" ::: "memory");
       }
+      if (want_ex && rmax > 0.0) atomicMax(ex_out + bi * Z_NB + r, oz_exp_of(rmax));
     }
   }
   tc_before();
@@ -473,7 +487,7 @@ template <class Idx, int NBUF, int TPS, int STAGES>
 void oz32_launch_cfg(int64_t n_seg, const int64_t* seg, const Idx* a_idx, const Idx* b_idx,
                      const int64_t* c_out, const int64_t* c_mirror, bool accumulate, const Mat& A,
                      const Mat& B, const OzakiOperands& op, double* C, cudaStream_t s,
-                     int* counter) {
+                     int* counter, int* ex_out) {
   using Cfg = ZCfg<NBUF, TPS, STAGES>;
   auto kern = k_leaf_ozaki32<Idx, NBUF, TPS, STAGES>;
   static std::once_flag once;
@@ -487,7 +501,8 @@ void oz32_launch_cfg(int64_t n_seg, const int64_t* seg, const Idx* a_idx, const 
                (const int32_t*)op.b_tr, (const int64_t*)A.keys, (const int64_t*)B.keys, op.G,
                (const int8_t*)op.as, (const int8_t*)op.bs, (const int*)op.ex_a,
                (const int*)op.ex_b, c_out, c_mirror, accumulate ? 1 : 0, C,
-               (const int32_t*)nullptr, counter, (const double*)A.data, (const double*)B.data);
+               (const int32_t*)nullptr, counter, (const double*)A.data, (const double*)B.data,
+               ex_out);
   SPAMM_LAUNCH_CK();
 }
 
@@ -495,7 +510,7 @@ template <class Idx>
 void oz32_launch(int64_t n_seg, const int64_t* seg, const Idx* a_idx, const Idx* b_idx,
                  const int64_t* c_out, const int64_t* c_mirror, bool accumulate, const Mat& A,
                  const Mat& B, const OzakiOperands& op, double* C, cudaStream_t s,
-                 int* counter) {
+                 int* counter, int* ex_out) {
   // Two CTAs per SM (256 TMEM columns each, 2 stages of 2 tasks): the kernel
   // is latency-bound, and a second CTA hides it better than double-buffered
   // accumulators in one (cfg3 K4z 8.0 vs 10.9 ms per solve; 1 task x 4 stages:
@@ -506,17 +521,17 @@ void oz32_launch(int64_t n_seg, const int64_t* seg, const Idx* a_idx, const Idx*
   }();
   if (shape == 1)
     oz32_launch_cfg<Idx, 2, 4, 3>(n_seg, seg, a_idx, b_idx, c_out, c_mirror, accumulate, A, B,
-                                  op, C, s, counter);
+                                  op, C, s, counter, ex_out);
   else
     oz32_launch_cfg<Idx, 1, 2, 2>(n_seg, seg, a_idx, b_idx, c_out, c_mirror, accumulate, A, B,
-                                  op, C, s, counter);
+                                  op, C, s, counter, ex_out);
 }
 
 template void oz32_launch<int32_t>(int64_t, const int64_t*, const int32_t*, const int32_t*,
                                    const int64_t*, const int64_t*, bool, const Mat&, const Mat&,
-                                   const OzakiOperands&, double*, cudaStream_t, int*);
+                                   const OzakiOperands&, double*, cudaStream_t, int*, int*);
 template void oz32_launch<int64_t>(int64_t, const int64_t*, const int64_t*, const int64_t*,
                                    const int64_t*, const int64_t*, bool, const Mat&, const Mat&,
-                                   const OzakiOperands&, double*, cudaStream_t, int*);
+                                   const OzakiOperands&, double*, cudaStream_t, int*, int*);
 
 }  // namespace spamm

@@ -45,6 +45,17 @@ __device__ __forceinline__ int oz_frexp(double mx) {
   const double f = frexp(mx, &e);
   return f >= 0.994140625 ? e + 1 : e;
 }
+// An exponent as an unsigned code whose order is the exponents' (0: none,
+// 0xFFFF: OZ_EXP_BAD) -- for warp max-reductions (__reduce_max_sync).
+__device__ __forceinline__ int oz_exp_of(double mx);
+__device__ __forceinline__ unsigned oz_ex_code(double v) {
+  if (!(v > 0.0)) return 0u;
+  const int e = oz_exp_of(v);
+  return e == OZ_EXP_BAD ? 0xFFFFu : (unsigned)(e + 0x8000);
+}
+__device__ __forceinline__ int oz_ex_decode(unsigned c) {
+  return c == 0xFFFFu ? OZ_EXP_BAD : (int)c - 0x8000;
+}
 // The row / column exponent of a reduced max oz_absf (mx > 0).
 __device__ __forceinline__ int oz_exp_of(double mx) {
   return isinf(mx) ? OZ_EXP_BAD : oz_frexp(mx);

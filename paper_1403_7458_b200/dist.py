@@ -349,7 +349,8 @@ class DistributedSP2:
             t0 = time.perf_counter()
             res.cuts_history.append(list(cuts))
             res.mode_history.append(mode)
-            res.owned_blocks.append(eng.count(x))
+            if multi:       # (reading the count settles a lazily pruned shard: a sync)
+                res.owned_blocks.append(eng.count(x))
             lo, hi = (cuts[self.rank], cuts[self.rank + 1]) if multi else (0, -1)
             sym_eff = sym
             ext = x

@@ -82,9 +82,13 @@ class QuadTreeMatrix:
     def __init__(self, handle: ctypes.c_void_p, stream: int):
         self._h = handle
         self._stream = stream
+        # geometry only: the storage view (count, pointers) is read on first
+        # use, which settles a lazily pruned product (one host sync) -- a
+        # matrix passed straight on to the next multiply never pays for it
         info = nat.MatInfo()
-        nat.check(nat.load().spamm_mat_info_get(handle, ctypes.byref(info)))
-        self._info = info
+        nat.check(nat.load().spamm_mat_info_peek(handle, ctypes.byref(info)))
+        self._peek = info
+        self._full = None
         self.n_native = int(info.n_native)
         self.block_size = int(info.block_size)
         self.chunk_size = int(info.chunk_size)
@@ -112,19 +116,28 @@ class QuadTreeMatrix:
         return 1 << self._depth
 
     @property
+    def _info(self):
+        if self._full is None:
+            info = nat.MatInfo()
+            nat.check(nat.load().spamm_mat_info_get(self._h, ctypes.byref(info)))
+            self._full = info
+        return self._full
+
+    @property
     def stored_leaf_count(self) -> int:
         return int(self._info.stored)
 
     @property
     def symmetric(self) -> bool:
         """Exactly symmetric (X == X^T bitwise); X*X then runs the symmetric path."""
-        return bool(self._info.symmetric)
+        return bool((self._full or self._peek).symmetric)
 
     def _refresh(self) -> None:
         """Re-read the handle after the library finalised it in place."""
         info = nat.MatInfo()
         nat.check(nat.load().spamm_mat_info_get(self._h, ctypes.byref(info)))
-        self._info = info
+        self._full = info
+        self._peek = info
         self._host = None
         self._root = None
 
@@ -144,11 +157,7 @@ class QuadTreeMatrix:
         stream = nat.current_stream()
         nat.check(nat.load().spamm_mat_set_pyramid(self._h, leaf.data_ptr(), int(bool(symmetric)),
                                                    stream))
-        info = nat.MatInfo()
-        nat.check(nat.load().spamm_mat_info_get(self._h, ctypes.byref(info)))
-        self._info = info
-        self._host = None
-        self._root = None
+        self._refresh()
 
     def norm(self) -> float:
         """Frobenius norm (root of the pyramid)."""
