@@ -120,6 +120,14 @@ int spamm_mat_cluster_range(const double* pos, const int64_t* orig, const double
                             int64_t n, int32_t block_size, int64_t chunk_size, double amp,
                             double decay, uint64_t seed, int64_t lo, int64_t hi, void* stream,
                             spamm_mat** out);
+/* Gershgorin bounds (sp2.py:68-76) over rows [row0, row1) of the config-5
+ * generator, evaluated on the fly (no matrix): eps_min = min(d - r), eps_max
+ * = max(d + r) with r = pairwise_sum(|row|) - |d| in numpy's order -- so the
+ * min / max over every rank's row range is bitwise gershgorin() of the whole
+ * matrix (multi-GPU config 5, where no rank holds the whole matrix). */
+int spamm_cluster_gershgorin(const double* pos, const int64_t* orig, const double* diag, int64_t n,
+                             double amp, double decay, uint64_t seed, int64_t row0, int64_t row1,
+                             void* stream, double* eps_min, double* eps_max);
 /* Leaf tier of the norm^2 pyramid (device double[G*G], row-major bi*G+bj,
  * 0 where no block) -- the per-shard contribution to the global pyramid. */
 int spamm_mat_leaf_norms2(const spamm_mat* m, double* out, void* stream);

@@ -83,6 +83,9 @@ _SIGS = {
                                         ctypes.c_uint64, c_i64, c_i64, c_vp,
                                         ctypes.POINTER(c_vp)]),
     "spamm_mat_leaf_norms2": (c_i32, [c_vp, c_vp, c_vp]),
+    "spamm_cluster_gershgorin": (c_i32, [c_vp, c_vp, c_vp, c_i64, c_f64, c_f64, ctypes.c_uint64,
+                                         c_i64, c_i64, c_vp, ctypes.POINTER(c_f64),
+                                         ctypes.POINTER(c_f64)]),
     "spamm_mat_set_pyramid": (c_i32, [c_vp, c_vp, c_i32, c_vp]),
     "spamm_mat_oz_exponents": (c_i32, [c_vp, c_i32, c_vp, c_vp]),
     "spamm_mat_set_oz_exponents": (c_i32, [c_vp, c_vp, c_vp, c_vp]),

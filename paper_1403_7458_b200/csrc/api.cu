@@ -356,6 +356,17 @@ int spamm_mat_cluster_range(const double* pos, const int64_t* orig, const double
   SPAMM_API_END
 }
 
+int spamm_cluster_gershgorin(const double* pos, const int64_t* orig, const double* diag, int64_t n,
+                             double amp, double decay, uint64_t seed, int64_t row0, int64_t row1,
+                             void* stream, double* eps_min, double* eps_max) {
+  if (!pos || !orig || !diag || !eps_min || !eps_max) return fail(SPAMM_EINVAL, "null argument");
+  if (n < 1 || row0 < 0 || row1 < row0 || row1 > n) return fail(SPAMM_EINVAL, "row range outside [0, n]");
+  SPAMM_API_BEGIN
+  spamm::cluster_gershgorin(pos, orig, diag, n, amp, decay, seed, row0, row1, eps_min, eps_max,
+                            S(stream));
+  SPAMM_API_END
+}
+
 int spamm_mat_leaf_norms2(const spamm_mat* m, double* out, void* stream) {
   if (!m || !out) return fail(SPAMM_EINVAL, "null argument");
   SPAMM_API_BEGIN
@@ -684,15 +695,20 @@ void multiply_impl(const spamm_mat* a, const spamm_mat* b, double tau, int32_t k
     }
   }
   C.data = spamm::dmalloc<double>((size_t)C.nblocks * nb2, s);
-  // A symmetric product on K4z also yields its own K4z row exponents (the
-  // epilogue's row / mirror-column maxima), so a multiply on C -- the next
-  // SP2 iteration after SQUARE -- skips the exponent pass.
+  // SPAMM_OZ_EXOUT=1: a symmetric product on K4z also yields its own K4z row
+  // exponents (the epilogue's row / mirror-column maxima), so a multiply on C
+  // -- the next SP2 iteration after SQUARE -- skips its exponent pass.
+  // Measured neutral on cfg4 (the pass saved, ~0.45 ms per solve, is paid
+  // back by a slower epilogue: K4z 0.63 vs 0.65 of the INT8 peak), so off.
   int* ex_out = nullptr;
   const bool k4z_possible = kernel == spamm::LEAF_OZAKI ||
                             (kernel == spamm::LEAF_AUTO && auto_ozaki_enabled() &&
                              auto_ozaki_for(a->m.nb));
-  if (sym && r.n_c > 0 && k4z_possible && spamm::ozaki_supported(C.nb) &&
-      !getenv("SPAMM_OZ_NO_EXOUT")) {
+  static const bool exout = [] {
+    const char* v = getenv("SPAMM_OZ_EXOUT");
+    return v && strcmp(v, "1") == 0;
+  }();
+  if (exout && sym && r.n_c > 0 && k4z_possible && spamm::ozaki_supported(C.nb)) {
     ex_out = spamm::dmalloc<int>(C.G * C.nb, s);
     SPAMM_CK(cudaMemsetAsync(ex_out, 0x80, C.G * C.nb * sizeof(int), s));
   }

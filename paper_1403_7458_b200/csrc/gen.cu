@@ -7,6 +7,10 @@
 // (SplitMix64 counter hash, Cody-Waite/Horner exp, sqrt, division), so every
 // block is bitwise equal to the host reference (tests/test_gpu_gen.py), and
 // writes the blocks straight into the Morton-ordered storage.
+#include <cmath>
+#include <cstring>
+#include <vector>
+
 #include "internal.h"
 
 namespace spamm {
@@ -41,6 +45,85 @@ __device__ __forceinline__ double det_exp(double x) {
     p = __dadd_rn(__dmul_rn(p, r), __ddiv_rn(1.0, fact));
   }
   return ldexp(p, (int)k);
+}
+
+// H_ab of the counter-based cluster (the expression of k_cluster_blocks, in
+// the same operation order), straight from the site arrays.
+__device__ __forceinline__ double cluster_elem(const double* __restrict__ pos,
+                                               const int64_t* __restrict__ orig,
+                                               const double* __restrict__ diag, int64_t n,
+                                               double amp, double decay, uint64_t seed, int64_t a,
+                                               int64_t b) {
+  if (a == b) return diag[a];
+  double r2 = 0.0;
+#pragma unroll
+  for (int ax = 0; ax < 3; ++ax) {
+    const double dd = __dadd_rn(pos[3 * a + ax], -pos[3 * b + ax]);
+    r2 = __dadd_rn(r2, __dmul_rn(dd, dd));
+  }
+  const double x = __ddiv_rn(-__dsqrt_rn(r2), decay);
+  const double s = sym_uniform((uint64_t)orig[a], (uint64_t)orig[b], (uint64_t)n, seed);
+  return __dmul_rn(__dmul_rn(amp, det_exp(x)), s);
+}
+
+// Gershgorin discs of rows [row0, row1) of the cluster H without building it
+// (multi-GPU config 5: each rank takes a row range): numpy's pairwise sum of
+// |H_row| (the same leaf / fold schedule as ops.cu k_gersh_rows_warp, so the
+// bounds are bitwise those of gershgorin() on the stored matrix), one warp
+// per row, lanes on the <= 128-element leaves, lane 0 folds them in order.
+__global__ void __launch_bounds__(256)
+    k_gersh_cluster(const double* __restrict__ pos, const int64_t* __restrict__ orig,
+                    const double* __restrict__ diag, int64_t n, double amp, double decay,
+                    uint64_t seed, int64_t row0, int64_t row1, const int64_t* __restrict__ leaf_lo,
+                    const int32_t* __restrict__ leaf_len, int n_leaves,
+                    const int32_t* __restrict__ ops, int n_ops, double* __restrict__ lo,
+                    double* __restrict__ hi) {
+  extern __shared__ double leafv[];  // [8 warps][n_leaves]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* lv = leafv + (int64_t)warp * n_leaves;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = row0 + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5); i < row1;
+       i += nw) {
+    auto at = [&](int64_t c) { return fabs(cluster_elem(pos, orig, diag, n, amp, decay, seed, i, c)); };
+    for (int k = lane; k < n_leaves; k += 32) {
+      const int64_t l0 = leaf_lo[k];
+      const int ln = leaf_len[k];
+      double res;
+      if (ln < 8) {
+        res = 0.0;
+        for (int q = 0; q < ln; ++q) res = __dadd_rn(res, at(l0 + q));
+      } else {
+        double r[8];
+        for (int j = 0; j < 8; ++j) r[j] = at(l0 + j);
+        int q = 8;
+        for (; q < ln - (ln % 8); q += 8)
+          for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], at(l0 + q + j));
+        res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                        __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+        for (; q < ln; ++q) res = __dadd_rn(res, at(l0 + q));
+      }
+      lv[k] = res;
+    }
+    __syncwarp();
+    if (lane == 0) {
+      double st[48];
+      int sp = 0;
+      for (int o = 0; o < n_ops; ++o) {
+        const int op = ops[o];
+        if (op >= 0) {
+          st[sp++] = lv[op];
+        } else {
+          const double r = st[--sp];
+          st[sp - 1] = __dadd_rn(st[sp - 1], r);
+        }
+      }
+      const double d = diag[i];
+      const double radius = __dadd_rn(st[0], -fabs(d));
+      lo[i - row0] = __dadd_rn(d, -radius);
+      hi[i - row0] = __dadd_rn(d, radius);
+    }
+    __syncwarp();
+  }
 }
 
 __global__ void k_native_flags(int depth, int64_t nbn, int64_t lo, int64_t hi,
@@ -117,6 +200,46 @@ __global__ void __launch_bounds__(256)
 }
 
 }  // namespace
+
+void cluster_gershgorin(const double* pos, const int64_t* orig, const double* diag, int64_t n,
+                        double amp, double decay, uint64_t seed, int64_t row0, int64_t row1,
+                        double* eps_min, double* eps_max, cudaStream_t s) {
+  std::vector<int64_t> leaf_lo;
+  std::vector<int32_t> leaf_len, ops;
+  pairwise_schedule(n, leaf_lo, leaf_len, ops);
+  const int nl = (int)leaf_lo.size(), no = (int)ops.size();
+  const size_t smem = 8 * (size_t)nl * sizeof(double);
+  if (smem > 200 * 1024) throw CudaError("cluster Gershgorin: row too long for the leaf buffer");
+  const int64_t rows = row1 - row0;
+  if (rows <= 0) {
+    *eps_min = INFINITY;
+    *eps_max = -INFINITY;
+    return;
+  }
+  double* buf = dmalloc<double>(2 * rows + 2, s);
+  int64_t* d_lo = dmalloc<int64_t>(nl, s);
+  int32_t* d_len = dmalloc<int32_t>(nl, s);
+  int32_t* d_ops = dmalloc<int32_t>(no, s);
+  SPAMM_CK(cudaMemcpyAsync(d_lo, leaf_lo.data(), nl * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+  SPAMM_CK(cudaMemcpyAsync(d_len, leaf_len.data(), nl * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+  SPAMM_CK(cudaMemcpyAsync(d_ops, ops.data(), no * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+  if (smem > 48 * 1024)
+    SPAMM_CK(cudaFuncSetAttribute(k_gersh_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)smem));
+  k_gersh_cluster<<<grid_for(rows * 32, 256, 148LL * 16), 256, smem, s>>>(
+      pos, orig, diag, n, amp, decay, seed, row0, row1, d_lo, d_len, nl, d_ops, no, buf,
+      buf + rows);
+  SPAMM_LAUNCH_CK();
+  minmax_launch(buf, buf + rows, rows, buf + 2 * rows, s);
+  int64_t bits[2];
+  d2h_sync(bits, reinterpret_cast<const int64_t*>(buf + 2 * rows), 2, s);
+  memcpy(eps_min, &bits[0], 8);
+  memcpy(eps_max, &bits[1], 8);
+  dfree(buf, s);
+  dfree(d_lo, s);
+  dfree(d_len, s);
+  dfree(d_ops, s);
+}
 
 void cluster_build(const double* pos, const int64_t* orig, const double* diag, double amp,
                    double decay, uint64_t seed, Mat& m, cudaStream_t s, int64_t lo,

@@ -279,6 +279,15 @@ void trace_launch(const Mat& m, double* dev_out, cudaStream_t s);  // no host sy
 // if absent -- trace() adds these in block order (multi-GPU: all-reduced).
 void diag_traces(const Mat& m, double* out, cudaStream_t s);
 void gershgorin(const Mat& f, double* eps_min, double* eps_max, double* asym, cudaStream_t s);
+// numpy pairwise_sum tree for a length-n row, flattened into <= 128-element
+// leaves (lo, len) and a post-order fold list (k >= 0: push leaf k, -1: add).
+void pairwise_schedule(int64_t n, std::vector<int64_t>& leaf_lo, std::vector<int32_t>& leaf_len,
+                       std::vector<int32_t>& ops);
+void minmax_launch(const double* lo, const double* hi, int64_t n, double* out, cudaStream_t s);
+// Gershgorin bounds of rows [row0, row1) of the config-5 generator (gen.cu).
+void cluster_gershgorin(const double* pos, const int64_t* orig, const double* diag, int64_t n,
+                        double amp, double decay, uint64_t seed, int64_t row0, int64_t row1,
+                        double* eps_min, double* eps_max, cudaStream_t s);
 // Counter-based cluster Hamiltonian (config 5) built on the device (gen.cu).
 // Build the pyramid of m from a full leaf tier of norm^2 (G*G, row-major
 // bi*G+bj): the same tier sums as finalize, so a Morton shard given the

@@ -424,7 +424,11 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
       // over its columns, and per column the max over the warp's 32 rows
       // (the rows of the mirror block)
       const bool want_ex = ex_out != nullptr && seg_end;
-      double rmax = 0.0;
+      unsigned rcode = 0u;        // row max (code, oz_ex_code)
+      // per chunk cl: the 4 column codes, two per word (named registers: the
+      // chunk loop is not unrolled, an indexed array would live in local memory)
+      unsigned ca0 = 0, cb0 = 0, ca1 = 0, cb1 = 0, ca2 = 0, cb2 = 0, ca3 = 0, cb3 = 0;
+
 #pragma unroll 1
       for (int cl = 0; cl < 4; ++cl) {
         const int cc = grp * 4 + cl;
@@ -538,18 +542,36 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
               for (int c = 0; c < 4; ++c) Cm[(col0 + c) * OZ_NB + r] = res[c];
           }
         }
-        if (want_ex) {
+        if (want_ex) {  // codes only here; the reductions run after TMEM is released
+          unsigned k4[4];
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
-            const double v = oz_absf(res[c]);
-            rmax = fmax(rmax, v);
-            const unsigned mx = __reduce_max_sync(0xffffffffu, oz_ex_code(v));
-            if (lane == 0 && mx && Cm) atomicMax(ex_out + bj * OZ_NB + col0 + c, oz_ex_decode(mx));
+            k4[c] = oz_ex_code(res[c]);
+            rcode = max(rcode, k4[c]);
           }
+          const unsigned wa = k4[0] | (k4[1] << 16), wb = k4[2] | (k4[3] << 16);
+          if (cl == 0) { ca0 = wa; cb0 = wb; }
+          else if (cl == 1) { ca1 = wa; cb1 = wb; }
+          else if (cl == 2) { ca2 = wa; cb2 = wb; }
+          else { ca3 = wa; cb3 = wb; }
         }
         asm volatile("bar.sync %0, 128;\n" ::"r"(1 + grp) : "memory");
       }
-      if (want_ex && rmax > 0.0) atomicMax(ex_out + bi * OZ_NB + r, oz_exp_of(rmax));
+      if (want_ex) {
+        if (Cm) {  // mirror rows: a column's max over this warp's 32 rows
+          const unsigned cw[8] = {ca0, cb0, ca1, cb1, ca2, cb2, ca3, cb3};
+#pragma unroll
+          for (int cl = 0; cl < 4; ++cl)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              const unsigned k = (cw[2 * cl + (c >> 1)] >> (16 * (c & 1))) & 0xFFFFu;
+              const unsigned mx = __reduce_max_sync(0xffffffffu, k);
+              if (lane == 0 && mx)
+                atomicMax(ex_out + bj * OZ_NB + (grp * 4 + cl) * 8 + own0 + c, oz_ex_decode(mx));
+            }
+        }
+        if (rcode) atomicMax(ex_out + bi * OZ_NB + r, oz_ex_decode(rcode));
+      }
       if (prof && threadIdx.x == 0) {
         e_all += clock64() - te0;
         ++n_blk;

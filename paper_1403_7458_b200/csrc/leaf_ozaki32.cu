@@ -348,7 +348,8 @@ __global__ void __launch_bounds__(Z_THREADS, NBUF == 2 ? 1 : 2)
       const uint32_t tb = lane_base + 256u * b;
       // ex_out: the product's own row exponents (see leaf_ozaki.cu)
       const bool want_ex = ex_out != nullptr && seg_end;
-      double rmax = 0.0;
+      unsigned rcode = 0u;
+      unsigned cc0 = 0, cc1 = 0, cc2 = 0, cc3 = 0;  // per chunk: 2 column codes (registers)
 #pragma unroll 1
       for (int cc = 0; cc < 4; ++cc) {
         int V[2][4][8];  // [tile][j][c8] of TMEM lane (w, r)
@@ -434,18 +435,30 @@ __global__ void __launch_bounds__(Z_THREADS, NBUF == 2 ? 1 : 2)
             Cm[(col0 + 1) * Z_NB + r] = res[1];
           }
         }
-        if (want_ex) {  // lane = row: a column's max over the warp is the block's
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const double v = oz_absf(res[h]);
-            rmax = fmax(rmax, v);
-            const unsigned mx = __reduce_max_sync(0xffffffffu, oz_ex_code(v));
-            if (lane == 0 && mx && Cm) atomicMax(ex_out + bj * Z_NB + col0 + h, oz_ex_decode(mx));
-          }
+        if (want_ex) {
+          const unsigned k0 = oz_ex_code(res[0]), k1 = oz_ex_code(res[1]);
+          rcode = max(rcode, max(k0, k1));
+          const unsigned wk = k0 | (k1 << 16);
+          if (cc == 0) cc0 = wk;
+          else if (cc == 1) cc1 = wk;
+          else if (cc == 2) cc2 = wk;
+          else cc3 = wk;
         }
         asm volatile("bar.sync 1, 128;\n" ::: "memory");
       }
-      if (want_ex && rmax > 0.0) atomicMax(ex_out + bi * Z_NB + r, oz_exp_of(rmax));
+      if (want_ex) {
+        if (Cm) {  // lane = row: a column's max over the warp is the block's
+          const unsigned cw[4] = {cc0, cc1, cc2, cc3};
+#pragma unroll
+          for (int cc = 0; cc < 4; ++cc)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const unsigned mx = __reduce_max_sync(0xffffffffu, (cw[cc] >> (16 * h)) & 0xFFFFu);
+              if (lane == 0 && mx) atomicMax(ex_out + bj * Z_NB + cc * 8 + 2 * w + h, oz_ex_decode(mx));
+            }
+        }
+        if (rcode) atomicMax(ex_out + bi * Z_NB + r, oz_ex_decode(rcode));
+      }
     }
   }
   tc_before();

@@ -505,22 +505,8 @@ double trace(const Mat& m, cudaStream_t s) {
   return v;
 }
 
-void gershgorin(const Mat& f, double* eps_min, double* eps_max, double* asym, cudaStream_t s) {
-  const int64_t n = f.n_native;
-  double* buf = dmalloc<double>(2 * n + 3, s);
-  double* lo = buf;
-  double* hi = buf + n;
-  double* res = buf + 2 * n;
-  SPAMM_CK(cudaMemsetAsync(res + 2, 0, sizeof(double), s));
-  if (f.nblocks > 0) {
-    k_asym<<<grid_for(f.nblocks, 1, 148LL * 16), 256, 0, s>>>(
-        f.data, f.keys, f.slot, f.nblocks, f.nb, f.G, n,
-        reinterpret_cast<unsigned long long*>(res + 2));
-    SPAMM_LAUNCH_CK();
-  }
-  // numpy pairwise_sum tree for a row of length n, flattened (same for all rows)
-  std::vector<int64_t> leaf_lo;
-  std::vector<int32_t> leaf_len, ops;
+void pairwise_schedule(int64_t n, std::vector<int64_t>& leaf_lo, std::vector<int32_t>& leaf_len,
+                       std::vector<int32_t>& ops) {
   struct Sched {
     std::vector<int64_t>& lo;
     std::vector<int32_t>& len;
@@ -540,6 +526,30 @@ void gershgorin(const Mat& f, double* eps_min, double* eps_max, double* asym, cu
     }
   } sched{leaf_lo, leaf_len, ops};
   sched.build(0, n);
+}
+
+void minmax_launch(const double* lo, const double* hi, int64_t n, double* out, cudaStream_t s) {
+  k_minmax<<<1, 1024, 0, s>>>(lo, hi, n, out);
+  SPAMM_LAUNCH_CK();
+}
+
+void gershgorin(const Mat& f, double* eps_min, double* eps_max, double* asym, cudaStream_t s) {
+  const int64_t n = f.n_native;
+  double* buf = dmalloc<double>(2 * n + 3, s);
+  double* lo = buf;
+  double* hi = buf + n;
+  double* res = buf + 2 * n;
+  SPAMM_CK(cudaMemsetAsync(res + 2, 0, sizeof(double), s));
+  if (f.nblocks > 0) {
+    k_asym<<<grid_for(f.nblocks, 1, 148LL * 16), 256, 0, s>>>(
+        f.data, f.keys, f.slot, f.nblocks, f.nb, f.G, n,
+        reinterpret_cast<unsigned long long*>(res + 2));
+    SPAMM_LAUNCH_CK();
+  }
+  // numpy pairwise_sum tree for a row of length n, flattened (same for all rows)
+  std::vector<int64_t> leaf_lo;
+  std::vector<int32_t> leaf_len, ops;
+  pairwise_schedule(n, leaf_lo, leaf_len, ops);
   const int nl = (int)leaf_lo.size(), no = (int)ops.size();
   const size_t smem = 8 * (size_t)nl * sizeof(double);
   if (smem <= 200 * 1024) {

@@ -45,13 +45,25 @@ __device__ __forceinline__ int oz_frexp(double mx) {
   const double f = frexp(mx, &e);
   return f >= 0.994140625 ? e + 1 : e;
 }
-// An exponent as an unsigned code whose order is the exponents' (0: none,
-// 0xFFFF: OZ_EXP_BAD) -- for warp max-reductions (__reduce_max_sync).
-__device__ __forceinline__ int oz_exp_of(double mx);
-__device__ __forceinline__ unsigned oz_ex_code(double v) {
-  if (!(v > 0.0)) return 0u;
-  const int e = oz_exp_of(v);
-  return e == OZ_EXP_BAD ? 0xFFFFu : (unsigned)(e + 0x8000);
+// The scale exponent of |x| as an unsigned code in the exponents' order (0:
+// x == 0, 0xFFFF: Inf / NaN = OZ_EXP_BAD, else oz_frexp(|x|) + 0x8000), from
+// the bit pattern with integer operations only (cheap enough for the K4z
+// epilogue): frexp's exponent is the biased exponent - 1022 (subnormals: the
+// bit length of the mantissa - 1074), bumped when the 8 mantissa bits after
+// the leading one are >= 0xFD, i.e. frac >= 0.994140625 as in oz_frexp.
+__device__ __forceinline__ unsigned oz_ex_code(double x) {
+  const uint64_t b = (uint64_t)__double_as_longlong(x) & 0x7FFFFFFFFFFFFFFFull;
+  if (b == 0) return 0u;
+  const unsigned E = (unsigned)(b >> 52);
+  if (E == 0x7FFu) return 0xFFFFu;
+  int e;
+  if (E) {
+    e = (int)E - 1022 + (((b >> 44) & 0xFF) >= 0xFD ? 1 : 0);
+  } else {
+    const int lz = __clzll((long long)b);
+    e = (64 - lz) - 1074 + (((b << (lz + 1)) >> 56) >= 0xFD ? 1 : 0);
+  }
+  return (unsigned)(e + 0x8000);
 }
 __device__ __forceinline__ int oz_ex_decode(unsigned c) {
   return c == 0xFFFFu ? OZ_EXP_BAD : (int)c - 0x8000;

@@ -326,6 +326,44 @@ class DistributedSP2:
         return self._loop(x, g, cuts, mode, sym, n_occ, tau, max_iter, criterion, fro_tol,
                           idem_tol, balance)
 
+    def solve_cluster(self, cs, block_size: int, tau: float, max_iter: int = 100,
+                      criterion: str = "fro", fro_tol: float = 1e-6, idem_tol: float = 1e-9,
+                      balance: str = "persistence"):
+        """Config 5: SP2 of the counter-based cluster H (synth.cluster_sites)
+        with no rank ever holding H or X.  Each rank generates its Morton share
+        of H in HBM, the Gershgorin bounds come from a row range per rank
+        evaluated on the fly (min / max over ranks: bitwise the single-GPU
+        bounds), X0 = (eps_max I - H) / (eps_max - eps_min) is formed on the
+        shard, and the first cut comes from a census of X0 * X0 on the
+        all-reduced pyramid."""
+        import torch
+        eng, comm = self.engine, self.comm
+        n = len(cs.orig)
+        g = 1
+        while g * block_size < n:
+            g *= 2
+        cuts0 = even_cuts(g * g, self.world)
+        f = eng.cluster_shard(cs, block_size, cuts0[self.rank], cuts0[self.rank + 1])
+        rows = even_cuts(n, self.world)
+        lo, hi = eng.cluster_gershgorin(cs, rows[self.rank], rows[self.rank + 1])
+        lo = float(comm.all_min(torch.tensor([lo], dtype=torch.float64)).item())
+        hi = float(comm.all_max(torch.tensor([hi], dtype=torch.float64)).item())
+        if not hi > lo:
+            raise ValueError("degenerate spectral bounds: eps_max equals eps_min")
+        x = eng.shard_init(f, lo, hi, owners(eng.keys(eng.identity_like(f)), g, cuts0, POS)
+                           == self.rank)
+        del f
+        # census-balanced first cut on the whole matrix's pyramid, then re-home
+        # X0 to its symmetric ownership
+        leaf = comm.all_sum(eng.leaf_norms2(x))
+        eng.install_pyramid(x, leaf, True)
+        work = eng.census_work(x, tau, True)
+        work = comm.all_max(work)       # identical on every rank (a safety net)
+        cuts = partition_work(eng.to_numpy(work), self.world) if balance != "even" else cuts0
+        x, _ = self.redistribute(x, g, cuts, UPPER)
+        return self._loop(x, g, cuts, UPPER, True, cs.n_occ, tau, max_iter, criterion,
+                          fro_tol, idem_tol, balance)
+
     def solve_sharded(self, x, g: int, cuts, mode: str, sym: bool, n_occ, tau: float,
                       max_iter: int = 100, criterion: str = "fro", fro_tol: float = 1e-6,
                       idem_tol: float = 1e-9, balance: str = "persistence"):
@@ -498,6 +536,39 @@ class DeviceShardEngine:
 
     def symmetric(self, m):
         return bool(m.symmetric)
+
+    # -- config 5: sharded start ---------------------------------------------------
+    def cluster_shard(self, cs, block_size, lo, hi):
+        from .synth import device_cluster
+        return device_cluster(cs, block_size, shard=(lo, hi))
+
+    def cluster_gershgorin(self, cs, row0, row1):
+        import ctypes
+
+        import torch
+
+        from . import _native as nat
+        pos = torch.from_numpy(np.ascontiguousarray(cs.pos, dtype=np.float64)).cuda()
+        orig = torch.from_numpy(np.ascontiguousarray(cs.orig, dtype=np.int64)).cuda()
+        diag = torch.from_numpy(np.ascontiguousarray(cs.diag, dtype=np.float64)).cuda()
+        lo, hi = ctypes.c_double(), ctypes.c_double()
+        nat.check(nat.load().spamm_cluster_gershgorin(
+            pos.data_ptr(), orig.data_ptr(), diag.data_ptr(), len(cs.orig), float(cs.amp),
+            float(cs.decay), int(cs.seed), int(row0), int(row1), nat.current_stream(),
+            ctypes.byref(lo), ctypes.byref(hi)))
+        return float(lo.value), float(hi.value)
+
+    def identity_like(self, m):
+        from .quadtree import identity
+        return identity(m.n_native, m.block_size, m.chunk_size)
+
+    def shard_init(self, f, lo, hi, eye_mask):
+        """X0's share: (eps_max I - F) / (eps_max - eps_min) (sp2.py:79-89) on
+        the shard (the identity's owned diagonal blocks, add_scaled)."""
+        from .quadtree import add_scaled
+        spread = hi - lo
+        eye = self.select(self.identity_like(f), eye_mask)
+        return add_scaled(hi / spread, eye, -1.0 / spread, f)
 
     # -- global structure --------------------------------------------------------
     def leaf_norms2(self, m):

@@ -105,3 +105,74 @@ def test_distributed_ranks_on_one_gpu_bitwise_sp2_solve(tmp_path, world, cfg_ind
     # persistence LB: from the second iteration on, the shares are balanced
     # by the previous iteration's counts (X^2 fills in slowly between iterations)
     assert ((ex.max(axis=0) - ex.min(axis=0))[1:] <= 0.1 * ex.mean(axis=0)[1:]).all()
+
+
+# -- config 5 path: H generated per rank, Gershgorin per row range ---------------
+
+def _cluster_ref(n_mol, nb, tau):
+    from paper_1403_7458_b200.synth import cluster_sites, device_cluster
+    cs = cluster_sites(n_mol, seed=2)
+    h = device_cluster(cs, nb)
+    p, st = sp.sp2_solve(h, cs.n_occ, tau, criterion="fro", fro_tol=1e-6)
+    return cs, sp.to_dense(p), st
+
+
+def test_cluster_gershgorin_row_ranges_bitwise():
+    from paper_1403_7458_b200.synth import cluster_sites, device_cluster
+    cs = cluster_sites(120, seed=2)
+    h = device_cluster(cs, 32)
+    b = sp.gershgorin_bounds(h)
+    eng = DeviceShardEngine()
+    n = len(cs.orig)
+    for parts in (1, 3, 7):
+        cuts = [n * r // parts for r in range(parts + 1)]
+        got = [eng.cluster_gershgorin(cs, cuts[r], cuts[r + 1]) for r in range(parts)]
+        assert min(g[0] for g in got) == b.eps_min
+        assert max(g[1] for g in got) == b.eps_max
+
+
+def test_cluster_world1_is_sp2_solve():
+    from paper_1403_7458_b200.synth import cluster_sites
+    cs, ref, st = _cluster_ref(120, 32, 1e-7)
+    res = DistributedSP2(DeviceShardEngine()).solve_cluster(cs, 32, 1e-7)
+    assert res.iteration == st.iteration and res.converged
+    assert res.trace_history == st.trace_history
+    assert res.idempotency_history == st.idempotency_history
+    assert np.array_equal(sp.to_dense(res.x), ref)
+    del cluster_sites
+
+
+def _cluster_worker(rank, world, port, n_mol, nb, tau, out_dir):
+    import torch.distributed as dist
+    from paper_1403_7458_b200.synth import cluster_sites
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        cs = cluster_sites(n_mol, seed=2)
+        drv = DistributedSP2(DeviceShardEngine())
+        res = drv.solve_cluster(cs, nb, tau)
+        p = drv.gather(res)
+        out = dict(iters=res.iteration, traces=np.array(res.trace_history),
+                   idem=np.array(res.idempotency_history), owned=np.array(res.owned_blocks),
+                   halo=np.array(res.halo_blocks))
+        if rank == 0:
+            out["p"] = sp.to_dense(p)
+        np.savez(os.path.join(out_dir, f"c{rank}.npz"), **out)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_cluster_ranks_on_one_gpu_bitwise_sp2_solve(tmp_path, world):
+    cs, ref, st = _cluster_ref(120, 32, 1e-7)
+    torch.multiprocessing.spawn(_cluster_worker, args=(world, _free_port(), 120, 32, 1e-7,
+                                                       str(tmp_path)), nprocs=world, join=True)
+    outs = [np.load(tmp_path / f"c{r}.npz") for r in range(world)]
+    for o in outs:
+        assert int(o["iters"]) == st.iteration
+        assert list(o["traces"]) == st.trace_history
+        assert list(o["idem"]) == st.idempotency_history
+        assert o["halo"].sum() > 0
+    assert np.array_equal(outs[0]["p"], ref)

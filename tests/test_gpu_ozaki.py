@@ -164,3 +164,29 @@ def test_auto_falls_back_to_dmma_without_slice_memory():
     out = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True,
                          text=True, timeout=300)
     assert out.returncode == 0 and "fallback ok" in out.stdout, out.stderr[-2000:]
+
+
+def test_product_exponents_from_the_epilogue_are_the_exponent_pass(tmp_path):
+    """SPAMM_OZ_EXOUT=1 (the K4z epilogue writes X^2's own row exponents and
+    the next multiply skips its exponent pass): bitwise the default SP2, for
+    Nb = 64 (K4z) and Nb = 32 (K4z32)."""
+    import os
+    import subprocess
+    import sys
+    code = ("import sys, numpy as np; sys.path.insert(0, %r)\n"
+            "import paper_1403_7458_b200 as sp\n"
+            "from paper_1403_7458_b200.synth import CONFIGS, water_cluster\n"
+            "for ci in (3, 4):\n"
+            "    cfg = CONFIGS[ci]; h, n = water_cluster(cfg.n_mol, seed=0)\n"
+            "    p, st = sp.sp2_solve(sp.build_from_dense(h, cfg.block_size), n, cfg.tau,"
+            " criterion='fro')\n"
+            "    np.save(sys.argv[1] + f'_{ci}.npy', sp.to_dense(p))\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = {}
+    for flag in ("0", "1"):
+        env = dict(os.environ, SPAMM_OZ_EXOUT=flag)
+        base = str(tmp_path / f"p{flag}")
+        subprocess.run([sys.executable, "-c", code % root, base], env=env, check=True)
+        outs[flag] = [np.load(f"{base}_{ci}.npy") for ci in (3, 4)]
+    for a, b in zip(outs["0"], outs["1"]):
+        assert np.array_equal(a, b)
