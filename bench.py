@@ -204,11 +204,18 @@ def run_ours(args):
     nb3x2 = 2 * cfg.block_size ** 3
     sharded = ws > 1 or args.sharded
 
+    ties = {}
+
     def solve(ff, timed):
         """One SP2 solve -> (P, reference-equivalent flops of the whole job, flops this rank
         executed, K4 ms on this rank, multiplies, iterations)."""
         if not sharded:
             p, st = sp.sp2_solve(ff, n_occ, cfg.tau, timed=timed, **crit)
+            # the parity contract's documented ties (kernel.py:108, sp2.py:97-99)
+            ties.update(near_tau_products=int(sum(st.near_tau_history)),
+                        min_relative_tau_margin=float(min(st.tau_margin_history)),
+                        min_abs_branch_margin=float(min(abs(b) for b in st.branch_margins[:-1])),
+                        near_tau_ulps=64)
             return p, st.flops, st.executed_flops, st.ms_leaf, len(st.leaf_products), st.iteration
         from paper_1403_7458_b200.dist import DeviceShardEngine, DistributedSP2
         drv = DistributedSP2(DeviceShardEngine())
@@ -372,6 +379,10 @@ def run_ours(args):
                                 "accumulation, FP64 assembly; inputs/outputs FP64"
                                 if k4 == "ozaki" else "FP64 tensor cores (DMMA)"),
             "roofline": roofline,
+            "ties": dict(ties, note=("tested products within near_tau_ulps ulp(tau) of tau over "
+                                     "the solve, the smallest |p - tau| / tau of a tested "
+                                     "product (inf: none within tau 2^-20), the smallest "
+                                     "|t_ex - n_occ| - |t_sq - n_occ| of an accepted step")),
             "e2e": {"value": e2e_flops_all / (e2e_max * 1e-3) / 1e9, "unit": UNIT,
                     "h2d_bytes_per_step": int(h.nbytes), "d2h_bytes_per_step": int(h.nbytes),
                     "api": "pipeline.sp2_solve_many over the steps' pinned host H (H2D, "
@@ -647,6 +658,82 @@ def run_sweep_sharded(args):
     dist.destroy_process_group()
 
 
+def run_cluster_sp2(args):
+    """Config 5 SP2 on N GPUs (torchrun): the counter-based cluster H is
+    generated per rank (Morton shard), the Gershgorin bounds come from a row
+    range per rank, and X, X^2 and the update stay sharded for the whole solve
+    (dist.DistributedSP2.solve_cluster).  One step = one complete SP2 solve at
+    --tau (criterion ||X^2 - X||_F < 1e-6); CUDA events, max over ranks.  The
+    full-size problem needs X, X^2 and 2X - X^2 (3 x 84 GB) across the ranks:
+    N >= 3 B200, or --molecules for a smaller cluster."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1403_7458_b200 import _native as nat
+    from paper_1403_7458_b200.dist import DeviceShardEngine, DistributedSP2
+    from paper_1403_7458_b200.synth import CONFIGS, cluster_sites
+
+    ws, rank, local_rank = dist_env()
+    torch.cuda.set_device(local_rank)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    lib = nat.load()
+    cfg = CONFIGS[5]
+    n_mol = args.molecules or cfg.n_mol
+    cs = cluster_sites(n_mol, seed=0)
+    tau = args.tau or 1e-8
+    nb3x2 = 2 * cfg.block_size ** 3
+    stream = torch.cuda.current_stream()
+
+    def one():
+        if ws > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        res = DistributedSP2(DeviceShardEngine()).solve_cluster(cs, cfg.block_size, tau)
+        e1.record(stream)
+        e1.synchronize()
+        t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
+        if ws > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t[0]), res
+
+    for _ in range(max(1, args.warmup - 2)):
+        one()
+    l0 = lib.spamm_launch_count()
+    total_ms, flops, res = 0.0, 0, None
+    with ClockSampler(local_rank) as clocks:
+        for _ in range(args.steps):
+            ms, res = one()
+            total_ms += ms
+            flops += sum(res.leaf_products) * nb3x2
+    launches = lib.spamm_launch_count() - l0
+    if rank == 0:
+        n = len(cs.orig)
+        out = {
+            "metric": METRIC, "value": flops / (total_ms * 1e-3) / 1e9, "unit": UNIT,
+            "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"cfg5-water{n_mol}-N{n}-Nb{cfg.block_size}-sp2",
+                       "tau": tau, "n_occ": cs.n_occ, "criterion": "||X^2-X||_F<1e-6",
+                       "step": "one full SP2 solve, H generated per rank",
+                       "parallelism": f"X, X^2 Morton-sharded x{ws} (dist.py)",
+                       "l2": "operands far larger than L2"},
+            "sp2_iterations": res.iteration, "sp2_ms_per_iter":
+                total_ms / args.steps / max(len(res.leaf_products), 1),
+            "halo_blocks_per_multiply_rank0": float(np.mean(res.halo_blocks)),
+            "e2e": {"value": flops / (total_ms * 1e-3) / 1e9, "unit": UNIT,
+                    "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
+                    "note": "H is generated in HBM per rank; P stays sharded"},
+            "gpu_launches": int(launches), "clocks": clocks.summary(),
+        }
+        print(json.dumps(out), flush=True)
+    if dist.is_initialized():
+        dist.destroy_process_group()
+
+
 def run_reference(args):
     """The reference's algorithm (oracle port, all host threads) on the same
     step as our arm: one complete SP2 solve of the workload per step."""
@@ -692,11 +779,17 @@ def main():
                          "sharded SP2; config 5: distributed operand)")
     ap.add_argument("--molecules", type=int, default=None,
                     help="config 5: override the molecule count (smoke tests)")
+    ap.add_argument("--sp2", action="store_true",
+                    help="config 5: SP2 solves with X distributed (dist.py) instead of the "
+                         "H*H tau sweep")
+    ap.add_argument("--tau", type=float, default=None, help="config 5 --sp2: tau (1e-8)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":
         run_reference(args)
+    elif args.config == 5 and args.sp2:
+        run_cluster_sp2(args)
     elif args.config == 5:
         if dist_env()[0] > 1 or args.sharded:
             run_sweep_sharded(args)
