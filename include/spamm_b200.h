@@ -203,6 +203,28 @@ int spamm_shard_sp2_step(const spamm_mat* ext, const spamm_mat* x, double n_occ,
                          int32_t want_idem, spamm_allreduce_fn allreduce, void* ctx,
                          void* stream, spamm_mat** x_next, int32_t* branch, double* t_x,
                          double* t_sq, double* idem, spamm_stats* stats);
+/* Halo plan of a rank's C segment [lo, hi) (multi-GPU, dist.py): culls x
+ * (a shard carrying the whole matrix's pyramid) and writes into out_keys
+ * (device int64, capacity G*G) the operand block keys its tasks read
+ * (A_ik, B_kj, and X_jk on the symmetric path) that another rank owns --
+ * ownership by the Morton position of (i,j), or with `upper` of (min,max),
+ * under cuts[world + 1] (host) -- grouped by owner; counts[world + 1] (host)
+ * gets the per-owner counts and the total.  *sym_ok: the symmetric path held
+ * on the range (sym_try; a mirror ulp tie turns it off).  *n_tasks: the
+ * range's executed leaf products. */
+int spamm_shard_plan(const spamm_mat* x, double tau, int64_t lo, int64_t hi, int32_t sym_try,
+                     int32_t rank, int32_t world, const int64_t* cuts, int32_t upper,
+                     int64_t* out_keys, int64_t* counts, int32_t* sym_ok, int64_t* n_tasks,
+                     void* stream);
+/* Copy the stored blocks with the given keys (device int64[n]) into out
+ * (device double[n * Nb * Nb]) -- what a rank sends to the ranks that asked. */
+int spamm_mat_gather_blocks(const spamm_mat* x, const int64_t* keys, int64_t n, double* out,
+                            void* stream);
+/* The rank's operand: x's blocks plus n received blocks (device keys / data,
+ * any order), in Morton storage order, with x's pyramid, symmetry flag and
+ * installed K4z exponents. */
+int spamm_shard_extend(const spamm_mat* x, const int64_t* keys, const double* blocks, int64_t n,
+                       void* stream, spamm_mat** out);
 /* Pre-grow the library's stream-ordered memory pool by `bytes` (kept mapped),
  * so steady-state allocations never wait on a new device mapping. */
 int spamm_reserve_pool(int64_t bytes, void* stream);

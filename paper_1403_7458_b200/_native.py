@@ -103,6 +103,10 @@ _SIGS = {
     "spamm_multiply_range": (c_i32, [c_vp, c_vp, c_f64, c_i32, c_i64, c_i64, c_vp, c_vp,
                                      ctypes.POINTER(c_vp), ctypes.POINTER(Stats)]),
     "spamm_reserve_pool": (c_i32, [c_i64, c_vp]),
+    "spamm_shard_plan": (c_i32, [c_vp, c_f64, c_i64, c_i64, c_i32, c_i32, c_i32, c_vp, c_i32,
+                                 c_vp, c_vp, ctypes.POINTER(c_i32), ctypes.POINTER(c_i64), c_vp]),
+    "spamm_mat_gather_blocks": (c_i32, [c_vp, c_vp, c_i64, c_vp, c_vp]),
+    "spamm_shard_extend": (c_i32, [c_vp, c_vp, c_vp, c_i64, c_vp, ctypes.POINTER(c_vp)]),
     "spamm_shard_sp2_step": (c_i32, [c_vp, c_vp, c_f64, c_f64, c_i32, c_i64, c_i64, c_vp, c_i32,
                                      ALLREDUCE_FN, c_vp, c_vp, ctypes.POINTER(c_vp),
                                      ctypes.POINTER(c_i32), ctypes.POINTER(c_f64),

@@ -1062,6 +1062,53 @@ int spamm_multiply_range(const spamm_mat* a, const spamm_mat* b, double tau, int
   SPAMM_API_END
 }
 
+int spamm_shard_plan(const spamm_mat* x, double tau, int64_t lo, int64_t hi, int32_t sym_try,
+                     int32_t rank, int32_t world, const int64_t* cuts, int32_t upper,
+                     int64_t* out_keys, int64_t* counts, int32_t* sym_ok, int64_t* n_tasks,
+                     void* stream) {
+  if (!x || !cuts || !out_keys || !counts || !sym_ok || !n_tasks)
+    return fail(SPAMM_EINVAL, "null argument");
+  if (world < 1 || world > 16 || rank < 0 || rank >= world)
+    return fail(SPAMM_EINVAL, "rank/world out of range (world <= 16)");
+  if (!(tau >= 0.0) || tau == __builtin_inf())
+    return fail(SPAMM_EINVAL, "tau must be finite and >= 0, got " + std::to_string(tau));
+  if (lo < 0 || hi < lo || hi > x->m.G * x->m.G)
+    return fail(SPAMM_EINVAL, "shard range outside [0, G*G]");
+  SPAMM_API_BEGIN
+  bool ok = false;
+  spamm::settle_sync(const_cast<spamm_mat*>(x)->m, S(stream));
+  spamm::shard_plan(x->m, tau, lo, hi, sym_try != 0 && g_sym_enabled && x->m.sym, rank, world,
+                    cuts, upper != 0, out_keys, counts, &ok, n_tasks, S(stream));
+  *sym_ok = ok ? 1 : 0;
+  SPAMM_API_END
+}
+
+int spamm_mat_gather_blocks(const spamm_mat* x, const int64_t* keys, int64_t n, double* out,
+                            void* stream) {
+  if (!x || (n > 0 && (!keys || !out))) return fail(SPAMM_EINVAL, "null argument");
+  SPAMM_API_BEGIN
+  spamm::settle_sync(const_cast<spamm_mat*>(x)->m, S(stream));
+  spamm::gather_blocks(x->m, keys, n, out, S(stream));
+  SPAMM_API_END
+}
+
+int spamm_shard_extend(const spamm_mat* x, const int64_t* keys, const double* blocks, int64_t n,
+                       void* stream, spamm_mat** out) {
+  if (!x || !out || (n > 0 && (!keys || !blocks))) return fail(SPAMM_EINVAL, "null argument");
+  SPAMM_API_BEGIN
+  spamm::settle_sync(const_cast<spamm_mat*>(x)->m, S(stream));
+  auto* h = new spamm_mat();
+  try {
+    spamm::shard_extend(x->m, keys, blocks, n, h->m, S(stream));
+  } catch (...) {
+    h->m.release();
+    delete h;
+    throw;
+  }
+  *out = h;
+  SPAMM_API_END
+}
+
 int spamm_reserve_pool(int64_t bytes, void* stream) {
   if (bytes < 0) return fail(SPAMM_EINVAL, "negative size");
   SPAMM_API_BEGIN

@@ -120,6 +120,26 @@ void sp2_update_finish(const Mat& x, const Mat& x2, UnionPrep& prep, int64_t U, 
 bool sp2_fused_supported(int nb);
 
 void scatter_slots(const int64_t* keys, int64_t m, int32_t* slot, cudaStream_t s);
+// (Re)write the pinned host mirror of m's top tiers from its device pyramid.
+void attach_host_top(Mat& m, cudaStream_t s);
+// A thread-local pinned staging buffer of >= bytes (small host->device copies).
+void* pinned_scratch(size_t bytes);
+
+// ---- multi-GPU shard plumbing (shard.cu) ----
+// Halo plan of the C segment [lo, hi): cull x (the whole matrix's pyramid
+// installed), list the operand blocks the tasks read that another rank owns
+// (ownership: Morton position of (i,j) or, upper, of (min,max) under `cuts`),
+// grouped by owner into out_keys (capacity G*G); counts_host[world + 1] gets
+// the per-owner counts and the total.  *sym_ok: the symmetric path held on
+// the range (sym_try).  One host sync besides the cull's.
+void shard_plan(const Mat& x, double tau, int64_t lo, int64_t hi, bool sym_try, int rank,
+                int world, const int64_t* cuts_host, bool upper, int64_t* out_keys,
+                int64_t* counts_host, bool* sym_ok, int64_t* n_tasks, cudaStream_t s);
+void gather_blocks(const Mat& x, const int64_t* keys, int64_t n, double* out, cudaStream_t s);
+// e = x's blocks + n received (keys, blocks) in Morton order, with x's pyramid,
+// symmetry flag and installed K4z exponents (the rank's operand).
+void shard_extend(const Mat& x, const int64_t* keys, const double* blocks, int64_t n, Mat& e,
+                  cudaStream_t s);
 // Leaf norm^2 (einsum recipe) and nonzero flags for m blocks of nb x nb.
 // norms1 (optional, Nb 32 / 64 only): sqrt of each leaf norm^2
 void leaf_norms2(const double* data, int64_t m, int nb, double* norms2, uint8_t* nonzero,

@@ -988,6 +988,29 @@ void finalize_impl(Mat& m, cudaStream_t s, double* pre_n2, uint8_t* pre_nz, bool
   }
 }
 
+void attach_host_top(Mat& m, cudaStream_t s) {
+  if (m.depth < 2) return;
+  if (!m.host_top) {
+    m.top_t = std::min(m.depth - 1, HOST_TOP_TIERS);
+    top_acquire(&m.host_top, &m.top_ev);
+  } else {
+    event_wait(m.top_ev);
+  }
+  copy_to_pinned(m.host_top, m.norms, tier_offset(m.top_t + 1), s);
+  SPAMM_CK(cudaEventRecord(m.top_ev, s));
+}
+
+void* pinned_scratch(size_t bytes) {
+  thread_local void* buf = nullptr;
+  thread_local size_t cap = 0;
+  if (bytes > cap) {
+    if (buf) cudaFreeHost(buf);
+    cap = std::max(bytes, (size_t)4096);
+    SPAMM_CK(cudaMallocHost(&buf, cap));
+  }
+  return buf;
+}
+
 const int64_t* pending_kept(const Mat& m) {
   if (m.pend_kept) return m.pend_kept;
   return m.pend_off ? m.pend_off + m.nblocks : nullptr;

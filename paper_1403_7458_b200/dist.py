@@ -277,34 +277,39 @@ class DistributedSP2:
         return out, int(go.sum())
 
     def _globalize(self, x, sym: bool):
-        """All-reduce the leaf tier (and the K4z row scales) and install them."""
+        """All-reduce the leaf tier (and the K4z row scales) and install them
+        on the shard (its operand copies them)."""
         eng = self.engine
         leaf = self.comm.all_sum(eng.leaf_norms2(x))
         eng.install_pyramid(x, leaf, sym)
         ex = eng.oz_exponents(x)
         if ex is not None:
             ex = tuple(self.comm.all_max(e) if e is not None else None for e in ex)
+            eng.install_exponents(x, ex)
         return leaf, ex
 
-    def _halo(self, x, g, cuts, mode, tau, lo, hi, sym):
-        """Fetch the operand blocks this rank's tasks read from their owners."""
+    def _plan(self, x, g, cuts, mode, tau, lo, hi, sym):
+        """The symmetric-path decision for the whole grid (a mirror ulp tie on
+        any rank sends every rank down the full path, as on one GPU) and the
+        operand keys this rank must fetch, grouped by owner (one native cull)."""
         import torch
-        eng = self.engine
-        ti, tk, tj = eng.tasks(x, tau, lo, hi, sym)
-        parts = [ti * g + tk, tk * g + tj]
+        eng, comm = self.engine, self.comm
+        ok, req, counts = eng.plan(x, tau, lo, hi, sym, self.rank, self.world, cuts, mode)
+        sym_eff = sym
         if sym:
-            parts.append(tj * g + tk)      # K4z's B operand on the symmetric path: X_jk^T
-        need = torch.unique(torch.cat(parts)) if len(ti) else parts[0]
-        own = owners(need, g, cuts, mode)
-        remote = own != self.rank
-        req, req_owner = need[remote], own[remote]
-        order = torch.argsort(req_owner, stable=True)
-        req, req_owner = req[order], req_owner[order]
-        counts = torch.bincount(req_owner, minlength=self.world).tolist()
+            sym_eff = bool(comm.all_min(torch.tensor([1 if ok else 0], dtype=torch.int64)).item())
+            if ok and not sym_eff:
+                _, req, counts = eng.plan(x, tau, lo, hi, False, self.rank, self.world, cuts,
+                                          mode)
+        return sym_eff, req, counts
+
+    def _halo(self, x, req, counts):
+        """Fetch the planned operand blocks from their owners (all-to-all of
+        the keys, then of the blocks)."""
         wanted, rc = self.comm.all_to_all_rows(req, counts)     # keys others need from me
-        blocks = eng.gather(x, wanted)
+        blocks = self.engine.gather(x, wanted)
         got, _ = self.comm.all_to_all_rows(blocks, rc)
-        return req, got
+        return got
 
     # -- solve ---------------------------------------------------------------
     def solve(self, f, n_occ, tau: float, max_iter: int = 100, criterion: str = "fro",
@@ -395,11 +400,8 @@ class DistributedSP2:
             if multi:
                 # one symmetric-path decision for the whole grid (a mirror ulp
                 # tie anywhere sends every rank down the full path, as on one GPU)
-                if sym:
-                    ok = eng.census_symmetric_ok(x, tau, lo, hi)
-                    sym_eff = bool(comm.all_min(torch.tensor([1 if ok else 0],
-                                                             dtype=torch.int64)).item())
-                req, got = self._halo(x, g, cuts, mode, tau, lo, hi, sym_eff)
+                sym_eff, req, counts = self._plan(x, g, cuts, mode, tau, lo, hi, sym)
+                got = self._halo(x, req, counts)
                 res.halo_blocks.append(int(req.numel()))
                 ext = eng.extend(x, req, got, leaf, sym_eff, ex)
                 mode_c = UPPER if sym_eff else POS
@@ -512,17 +514,46 @@ class DeviceShardEngine:
         return self._from_blocks(like, keys, blocks)
 
     def gather(self, m, keys):
+        """The stored blocks with the given keys (spamm_mat_gather_blocks)."""
         import torch
+
+        from . import _native as nat
         nb = m.block_size
-        if keys.numel() == 0:
-            return torch.empty((0, nb, nb), dtype=torch.float64, device="cuda")
-        own = self.keys(m)
-        order = torch.argsort(own)
-        pos = torch.searchsorted(own[order], keys.to(own.device))
-        pos = order[pos.clamp(max=own.numel() - 1)]
-        if not bool((own[pos] == keys.to(own.device)).all()):
-            raise RuntimeError("DistributedSP2: a requested block is not owned by this rank")
-        return self.blocks(m)[pos].contiguous()
+        keys = keys.to(device="cuda", dtype=torch.int64).contiguous()
+        out = torch.empty((keys.numel(), nb, nb), dtype=torch.float64, device="cuda")
+        if keys.numel():
+            nat.check(nat.load().spamm_mat_gather_blocks(m._h, keys.data_ptr(), keys.numel(),
+                                                         out.data_ptr(), nat.current_stream()))
+        return out
+
+    def plan(self, m, tau, lo, hi, sym, rank, world, cuts, mode):
+        """spamm_shard_plan: (symmetric path held on the range, the remote
+        operand keys grouped by owner, per-owner counts)."""
+        import ctypes
+
+        import torch
+
+        from . import _native as nat
+        g = m.n_blocks
+        keys = torch.empty(g * g, dtype=torch.int64, device="cuda")
+        cuts_h = (ctypes.c_int64 * (world + 1))(*[int(c) for c in cuts])
+        counts = (ctypes.c_int64 * (world + 1))()
+        ok = ctypes.c_int32()
+        n_tasks = ctypes.c_int64()
+        nat.check(nat.load().spamm_shard_plan(
+            m._h, float(tau), int(lo), int(hi), int(bool(sym)), int(rank), int(world),
+            ctypes.cast(cuts_h, ctypes.c_void_p), int(mode == UPPER), keys.data_ptr(),
+            ctypes.cast(counts, ctypes.c_void_p), ctypes.byref(ok), ctypes.byref(n_tasks),
+            nat.current_stream()))
+        per = [int(counts[r]) for r in range(world)]
+        return bool(ok.value), keys[: int(counts[world])], per
+
+    def install_exponents(self, m, ex):
+        from . import _native as nat
+        row, col = ex
+        nat.check(nat.load().spamm_mat_set_oz_exponents(
+            m._h, row.data_ptr(), col.data_ptr() if col is not None else None,
+            nat.current_stream()))
 
     # -- replicated start ------------------------------------------------------
     def gershgorin(self, f):
@@ -619,18 +650,6 @@ class DeviceShardEngine:
             self._set_sym(True)
         return work.to(torch.int64)
 
-    def census_symmetric_ok(self, m, tau, lo, hi):
-        """Whether the symmetric cull holds on [lo, hi) (no mirror ulp tie)."""
-        import ctypes
-
-        from . import _native as nat
-        if hi <= lo:
-            return True
-        st = nat.Stats()
-        nat.check(nat.load().spamm_census_range(m._h, m._h, float(tau), int(lo), int(hi), None,
-                                                nat.current_stream(), ctypes.byref(st)))
-        return bool(st.symmetric)
-
     def tasks(self, m, tau, lo, hi, sym):
         import ctypes
 
@@ -658,24 +677,24 @@ class DeviceShardEngine:
         return tuple(x.to(torch.int64) for x in t)
 
     def extend(self, m, keys, blocks, leaf, sym, ex):
-        """The rank's operand: its own blocks plus the fetched ones, with the
-        whole matrix's pyramid, symmetry flag and K4z row scales (with
-        nothing fetched -- one rank -- the shard itself)."""
+        """The rank's operand: its own blocks plus the fetched ones
+        (spamm_shard_extend: Morton order, the shard's installed pyramid,
+        symmetry flag and K4z scales -- the whole matrix's)."""
+        import ctypes
+
+        import torch
+
         from . import _native as nat
-        if keys.numel():
-            ext = self.rebuild(m, self.keys(m), self.blocks(m), keys,
-                               blocks.reshape(-1, m.block_size, m.block_size))
-            ext.set_global_pyramid(leaf, sym)
-        else:
-            ext = m
-            if bool(m.symmetric) != bool(sym):
-                ext.set_global_pyramid(leaf, sym)
-        if ex is not None and self._ozaki(m):
-            row, col = ex
-            nat.check(nat.load().spamm_mat_set_oz_exponents(
-                ext._h, row.data_ptr(), col.data_ptr() if col is not None else None,
-                nat.current_stream()))
-        return ext
+        from .quadtree import QuadTreeMatrix
+        if keys.numel() == 0:
+            return m
+        keys = keys.to(device="cuda", dtype=torch.int64).contiguous()
+        blocks = blocks.to(device="cuda", dtype=torch.float64).contiguous()
+        out = ctypes.c_void_p()
+        stream = nat.current_stream()
+        nat.check(nat.load().spamm_shard_extend(m._h, keys.data_ptr(), blocks.data_ptr(),
+                                                keys.numel(), stream, ctypes.byref(out)))
+        return QuadTreeMatrix(out, stream)
 
     def multiply_range(self, m, tau, lo, hi, sym):
         import ctypes

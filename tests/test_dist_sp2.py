@@ -146,6 +146,19 @@ class OracleDistEngine:
         a, k, b = ti[lw], tk[lw], tj[lw]
         return all(((bb * g + kk) * g + aa) in fwd for aa, kk, bb in zip(a, k, b))
 
+    def plan(self, x, tau, lo, hi, sym, rank, world, cuts, mode):
+        ok = self.census_symmetric_ok(x, tau, lo, hi) if sym else False
+        g = x.m.n_blocks
+        ti, tk, tj = self._tasks(x, tau, lo, hi, sym and ok)
+        parts = [ti * g + tk, tk * g + tj] + ([tj * g + tk] if sym and ok else [])
+        need = torch.from_numpy(np.unique(np.concatenate(parts)).astype(np.int64))
+        own = owners(need, g, cuts, mode)
+        remote = own != rank
+        req, req_owner = need[remote], own[remote]
+        order = torch.argsort(req_owner, stable=True)
+        counts = torch.bincount(req_owner, minlength=world).tolist()
+        return ok, req[order], counts
+
     def tasks(self, x, tau, lo, hi, sym):
         return tuple(torch.from_numpy(v) for v in self._tasks(x, tau, lo, hi, sym))
 
