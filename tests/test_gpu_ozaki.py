@@ -190,3 +190,57 @@ def test_product_exponents_from_the_epilogue_are_the_exponent_pass(tmp_path):
         outs[flag] = [np.load(f"{base}_{ci}.npy") for ci in (3, 4)]
     for a, b in zip(outs["0"], outs["1"]):
         assert np.array_equal(a, b)
+
+
+def _exact_product(a, b):
+    """C = A B exactly (Python integers on the doubles' mantissa grid), then
+    the exact values as (numerator, exponent) -> float via Fraction."""
+    from fractions import Fraction
+    n = a.shape[0]
+    fa = [[Fraction(float(v)) for v in row] for row in a]
+    fb = [[Fraction(float(v)) for v in row] for row in b]
+    out = np.zeros((n, n))
+    err_ref = np.zeros((n, n), dtype=object)
+    for i in range(n):
+        for j in range(n):
+            s = sum(fa[i][k] * fb[k][j] for k in range(n))
+            err_ref[i, j] = s
+            out[i, j] = float(s)
+    return out, err_ref
+
+
+@pytest.mark.parametrize("nb", [32, 64])
+def test_elementwise_accuracy_envelope(nb):
+    """K4z scales each global row of A (column of B) by one power of two, so
+    its error bound is absolute against the row / column maxima -- a
+    fixed-point format of 63 bits per row: |c - c_exact| <= K 2^-62
+    2^(E_r + E_c) per element (E: the scale exponents, max|A_r| < 2^E_r), where
+    FP64's bound is relative to sum |a_rk b_kc|.  An element 2^-k below the
+    product of its row and column maxima therefore keeps ~63 - k bits (FP64:
+    ~53).  Rows here span 60 binades; the bound must hold for every element,
+    and the matrix-level error stays below FP64's."""
+    rng = np.random.default_rng(3)
+    n = nb
+    a = rng.uniform(-1, 1, (n, n)) * np.exp2(-rng.integers(0, 60, (n, n)))
+    b = rng.uniform(-1, 1, (n, n)) * np.exp2(-rng.integers(0, 60, (n, n)))
+    ref, exact = _exact_product(a, b)
+    got = sp.to_dense(sp.multiply(sp.build_from_dense(a, nb), sp.build_from_dense(b, nb), 0.0,
+                                  kernel="ozaki")[0])
+    fp64 = sp.to_dense(sp.multiply(sp.build_from_dense(a, nb), sp.build_from_dense(b, nb), 0.0,
+                                   kernel="exact")[0])
+    er = np.ceil(np.log2(np.abs(a).max(axis=1))) + 1       # >= the kernel's row scale exponents
+    ec = np.ceil(np.log2(np.abs(b).max(axis=0))) + 1
+    scale = np.exp2(er[:, None] + ec[None, :])
+    # digit truncation of both operands (K terms) + the rounding of the result
+    bound = n * np.exp2(-62.0) * scale + np.exp2(-52.0) * np.abs(ref)
+    from fractions import Fraction
+    err = np.array([[abs(float(Fraction(float(got[i, j])) - exact[i, j])) for j in range(n)]
+                    for i in range(n)])
+    assert (err <= bound).all(), float((err / bound).max())
+    # matrix level: K4z is closer to the exact product than the FP64 loop
+    assert np.linalg.norm(got - ref) <= np.linalg.norm(fp64 - ref)
+    # elements within 2^8 of their row x column scale keep FP64-level relative
+    # accuracy; smaller ones lose relative bits as the envelope says
+    rel = err / np.maximum(np.abs(ref), 1e-300)
+    big = np.abs(ref) >= np.exp2(-8) * scale
+    assert big.any() and rel[big].max() < 1e-14
