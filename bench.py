@@ -150,10 +150,33 @@ class ClockSampler:
                 "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
+def init_dist(local: int) -> None:
+    """One process per GPU over NCCL.  SPAMM_DIST_BACKEND=gloo runs the same
+    multi-rank path with host-memory collectives (a smoke test of the
+    torchrun launch on a box with fewer GPUs than ranks; not a measurement)."""
+    import torch
+    import torch.distributed as dist
+    backend = os.environ.get("SPAMM_DIST_BACKEND", "nccl")
+    if backend == "nccl":
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        dist.init_process_group(backend)
+
+
+def coll_device() -> str:
+    """Device for the bench's own scalar collectives (gloo: host)."""
+    import torch.distributed as dist
+    return "cpu" if dist.get_backend() == "gloo" else "cuda"
+
+
 def dist_env():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if os.environ.get("SPAMM_DIST_BACKEND", "nccl") != "nccl":
+        import torch    # (the gloo smoke test may put several ranks on one GPU)
+        if torch.cuda.is_available():
+            local %= torch.cuda.device_count()
     return ws, rank, local
 
 
@@ -192,7 +215,7 @@ def run_ours(args):
     ws, rank, local = dist_env()
     torch.cuda.set_device(local)
     if ws > 1 or (args.sharded and "RANK" in os.environ):
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        init_dist(local)
     lib = nat.load()
     cfg, h, n_occ = workload(args.config)
     crit = dict(criterion="fro", fro_tol=1e-6)
@@ -298,10 +321,10 @@ def run_ours(args):
     tmax = dev_ms
     e2e_max = e2e_ms
     if ws > 1:
-        t = torch.tensor([dev_ms, e2e_ms], dtype=torch.float64, device="cuda")
+        t = torch.tensor([dev_ms, e2e_ms], dtype=torch.float64, device=coll_device())
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         tmax, e2e_max = float(t[0]), float(t[1])
-        xf = torch.tensor([exec_flops], dtype=torch.float64, device="cuda")
+        xf = torch.tensor([exec_flops], dtype=torch.float64, device=coll_device())
         dist.all_reduce(xf, op=dist.ReduceOp.SUM)
         exec_all = float(xf[0])
     else:
@@ -571,7 +594,7 @@ def run_sweep_sharded(args):
 
     ws, rank, local_rank = dist_env()
     torch.cuda.set_device(local_rank)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    init_dist(local_rank)
     lib = nat.load()
     cfg = CONFIGS[5]
     n_mol = args.molecules or cfg.n_mol
@@ -600,7 +623,7 @@ def run_sweep_sharded(args):
         e1.record(stream)
         e1.synchronize()
         t = torch.tensor([e0.elapsed_time(e1), prod.leaf_products, prod.executed_products,
-                          prod.halo_blocks], dtype=torch.float64, device="cuda")
+                          prod.halo_blocks], dtype=torch.float64, device=coll_device())
         mx, sm_ = t.clone(), t.clone()
         dist.all_reduce(mx, op=dist.ReduceOp.MAX)
         dist.all_reduce(sm_)
@@ -676,7 +699,7 @@ def run_cluster_sp2(args):
     ws, rank, local_rank = dist_env()
     torch.cuda.set_device(local_rank)
     if ws > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        init_dist(local_rank)
     lib = nat.load()
     cfg = CONFIGS[5]
     n_mol = args.molecules or cfg.n_mol
@@ -694,7 +717,8 @@ def run_cluster_sp2(args):
         res = DistributedSP2(DeviceShardEngine()).solve_cluster(cs, cfg.block_size, tau)
         e1.record(stream)
         e1.synchronize()
-        t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
+        t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64,
+                         device=coll_device() if ws > 1 else "cuda")
         if ws > 1:
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t[0]), res
