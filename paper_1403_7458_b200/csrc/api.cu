@@ -589,11 +589,24 @@ size_t device_total_bytes() {
   return total;
 }
 cudaStream_t ozaki_side_stream() {  // one per (host thread, device)
+  // The pre-passes are the longer of the two concurrent chains before K4z
+  // (exponents + split ~70 us vs the cull ~55 us at cfg4), so the side
+  // stream gets the highest priority: its CTAs are scheduled first and the
+  // latency-bound cull kernels fill the remaining slots
+  // (SPAMM_OZ_SIDE_PRIO=0: default priority).
+  static const bool prio = [] {
+    const char* v = getenv("SPAMM_OZ_SIDE_PRIO");
+    return !(v && strcmp(v, "0") == 0);
+  }();
   thread_local cudaStream_t side[64] = {};
   int dev = 0;
   SPAMM_CK(cudaGetDevice(&dev));
   cudaStream_t& t = side[dev & 63];
-  if (!t) SPAMM_CK(cudaStreamCreateWithFlags(&t, cudaStreamNonBlocking));
+  if (!t) {
+    int lo = 0, hi = 0;
+    SPAMM_CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    SPAMM_CK(cudaStreamCreateWithPriority(&t, cudaStreamNonBlocking, prio ? hi : lo));
+  }
   return t;
 }
 void ozaki_ahead(const spamm_mat* a, const spamm_mat* b, int32_t kernel, cudaStream_t s,
