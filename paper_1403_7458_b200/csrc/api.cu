@@ -217,10 +217,11 @@ struct SideQueue {
 };
 thread_local SideQueue* g_side = nullptr;
 
+struct OzakiAhead;
 void multiply_impl(const spamm_mat* a, const spamm_mat* b, double tau, int32_t kernel, bool timed,
                    cudaStream_t s, spamm::Mat& C, spamm_stats* stats, int64_t lo = 0,
                    int64_t hi = -1, int32_t* work = nullptr, bool defer_prune = false,
-                   spamm::IdemFuse idem = {});
+                   spamm::IdemFuse idem = {}, OzakiAhead* pre = nullptr);
 
 }  // namespace
 
@@ -652,11 +653,20 @@ void ozaki_ahead(const spamm_mat* a, const spamm_mat* b, int32_t kernel, cudaStr
 
 void multiply_impl(const spamm_mat* a, const spamm_mat* b, double tau, int32_t kernel, bool timed,
                    cudaStream_t s, spamm::Mat& C, spamm_stats* stats, int64_t lo, int64_t hi,
-                   int32_t* work, bool defer_prune, spamm::IdemFuse idem) {
+                   int32_t* work, bool defer_prune, spamm::IdemFuse idem, OzakiAhead* pre) {
   EventTimer tm(timed, s);
   tm.mark(0);
   OzakiAhead oz;
-  ozaki_ahead(a, b, kernel, s, oz);
+  if (pre && pre->ok) {  // operand pre-passes already launched (SP2 speculation)
+    oz.op = pre->op;
+    oz.ready = pre->ready;
+    oz.s = s;
+    oz.ok = true;
+    pre->ok = false;
+    pre->ready = nullptr;
+  } else {
+    ozaki_ahead(a, b, kernel, s, oz);
+  }
   spamm::CullResult r;
   // Symmetric SpAMM: X*X with X == X^T bitwise -> compute C_ij for i <= j only
   // and store C_ji = C_ij^T (bitwise what the full product yields).
@@ -1416,6 +1426,23 @@ int spamm_sp2_solve_ex(const spamm_mat* f, double n_occ, double tau, int32_t max
     ~Graveyard() { flush(); }
   } dead;
   auto t_iter = std::chrono::steady_clock::now();
+  // SPAMM_OZ_SPEC=1: after each X^2 the K4z operand pre-passes of X^2 start on
+  // the side stream before the branch is known (SQUARE makes X^2 the next X);
+  // on EXPAND, or when X^2's lazy prune compacts its storage, they are dropped.
+  static const bool spec_on = [] {
+    const char* v = getenv("SPAMM_OZ_SPEC");
+    return v && strcmp(v, "1") == 0;
+  }();
+  OzakiAhead spec;
+  const spamm_mat* spec_for = nullptr;
+  auto drop_spec = [&]() {
+    if (!spec.ok) return;
+    // on the pre-passes' own stream: ordered after them, and s never waits
+    spamm::ozaki_release(spec.op, spec.ready ? ozaki_side_stream() : s);
+    spec.ok = false;
+    spec.ready = nullptr;
+    spec_for = nullptr;
+  };
   for (int it = 0; it < max_iter; ++it) {
     auto* c = new spamm_mat();
     spamm_stats st;
@@ -1427,8 +1454,15 @@ int spamm_sp2_solve_ex(const spamm_mat* f, double n_occ, double tau, int32_t max
       fuse.ukeys = spamm::dmalloc<int64_t>(x->m.G * x->m.G, s);
     }
     spamm::htrace("it_mul");
-    multiply_impl(x, x, tau, kernel, timed != 0, s, c->m, &st, 0, -1, nullptr, true, fuse);
+    multiply_impl(x, x, tau, kernel, timed != 0, s, c->m, &st, 0, -1, nullptr, true, fuse,
+                  spec.ok && spec_for == x ? &spec : nullptr);
+    drop_spec();  // (unused speculation)
     spamm::htrace("it_mul_done");
+    if (spec_on) {
+      ozaki_ahead(c, c, kernel, s, spec);
+      spec_for = spec.ok ? c : nullptr;
+    }
+    const int64_t c_blocks_before = c->m.nblocks;
     dead.flush();
     spamm::htrace("it_flushed");
     bool square = true;
@@ -1437,6 +1471,7 @@ int spamm_sp2_solve_ex(const spamm_mat* f, double n_occ, double tau, int32_t max
     double bmargin = 0.0;
     sp2_finish(x, c, n_occ, want_idem, s, &square, &tx, &tsq, &idem, &e, fuse.out, &fuse,
                &bmargin);
+    if (spec.ok && (!square || c->m.nblocks != c_blocks_before)) drop_spec();
     spamm::dfree(fuse.ukeys, s);  // (null once the update took it)
     const int k = rep->n_multiplies++;
     rep->leaf_products[k] = st.leaf_products;
@@ -1466,6 +1501,7 @@ int spamm_sp2_solve_ex(const spamm_mat* f, double n_occ, double tau, int32_t max
       done = std::fabs(tsq - tx) < idem_tol && std::fabs(tx - n_occ) < 1e-6 * n_occ;
     }
     if (done) {  // sp2.py:133-136: converged on X^2, the old X is returned
+      drop_spec();
       rep->converged = 1;
       if (e) {
         e->m.release();
@@ -1486,6 +1522,7 @@ int spamm_sp2_solve_ex(const spamm_mat* f, double n_occ, double tau, int32_t max
     rep->iterations += 1;
     pending_trace = true;
   }
+  drop_spec();
   if (pending_trace) rep->trace_history[n_tr++] = spamm::trace(x->m, s);
   g_side = nullptr;
   sideq.drain(s);
