@@ -63,13 +63,46 @@ int check_conformable(const spamm_mat* a, const spamm_mat* b) {
   return SPAMM_OK;
 }
 
+// Timing events of one multiply (timed = 1).  Events come from a per-thread
+// pool.  Inside the SP2 loop the readout is deferred (g_defer_timing): the
+// elapsed times are read after the iteration's own host sync, when the
+// events have completed -- a timed solve then has no extra sync per multiply.
+thread_local std::vector<cudaEvent_t> g_event_pool;
+thread_local bool g_defer_timing = false;
+struct PendingTiming {
+  cudaEvent_t e[4];
+  spamm_stats* st;
+};
+thread_local std::vector<PendingTiming> g_pending_timing;
+cudaEvent_t pooled_event() {
+  if (g_event_pool.empty()) {
+    cudaEvent_t e;
+    SPAMM_CK(cudaEventCreate(&e));
+    return e;
+  }
+  cudaEvent_t e = g_event_pool.back();
+  g_event_pool.pop_back();
+  return e;
+}
+void resolve_timings() {  // events complete: no wait
+  for (auto& p : g_pending_timing) {
+    float v[3] = {0.f, 0.f, 0.f};
+    for (int i = 0; i < 3; ++i) SPAMM_CK(cudaEventElapsedTime(&v[i], p.e[i], p.e[i + 1]));
+    p.st->ms_cull = v[0];
+    p.st->ms_leaf = v[1];
+    p.st->ms_finalize = v[2];
+    for (auto x : p.e) g_event_pool.push_back(x);
+  }
+  g_pending_timing.clear();
+}
 struct EventTimer {
   cudaEvent_t e[4] = {nullptr, nullptr, nullptr, nullptr};
   bool on;
   cudaStream_t s;
+  spamm_stats* defer_to = nullptr;
   EventTimer(bool on_, cudaStream_t s_) : on(on_), s(s_) {
     if (on)
-      for (auto& x : e) SPAMM_CK(cudaEventCreate(&x));
+      for (auto& x : e) x = pooled_event();
   }
   void mark(int i) {
     if (on) SPAMM_CK(cudaEventRecord(e[i], s));
@@ -82,8 +115,12 @@ struct EventTimer {
     return v;
   }
   ~EventTimer() {
-    if (on)
-      for (auto& x : e) cudaEventDestroy(x);
+    if (!on) return;
+    if (defer_to) {
+      g_pending_timing.push_back({{e[0], e[1], e[2], e[3]}, defer_to});
+    } else {
+      for (auto& x : e) g_event_pool.push_back(x);
+    }
   }
 };
 
@@ -781,9 +818,13 @@ void multiply_impl(const spamm_mat* a, const spamm_mat* b, double tau, int32_t k
     stats->c_blocks = C.nblocks;
     stats->executed_products = r.n_tasks;
     stats->symmetric = sym ? 1 : 0;
-    stats->ms_cull = tm.ms(0, 1);
-    stats->ms_leaf = tm.ms(1, 2);
-    stats->ms_finalize = tm.ms(2, 3);
+    if (timed && g_defer_timing) {
+      tm.defer_to = stats;  // read after the SP2 iteration's host sync
+    } else {
+      stats->ms_cull = tm.ms(0, 1);
+      stats->ms_leaf = tm.ms(1, 2);
+      stats->ms_finalize = tm.ms(2, 3);
+    }
   }
   r.release(s);
 }
@@ -1435,6 +1476,13 @@ int spamm_sp2_solve_ex(const spamm_mat* f, double n_occ, double tau, int32_t max
   }();
   OzakiAhead spec;
   const spamm_mat* spec_for = nullptr;
+  struct DeferScope {  // timed multiplies read their events after the branch sync
+    DeferScope() { g_defer_timing = true; }
+    ~DeferScope() {
+      g_defer_timing = false;
+      g_pending_timing.clear();
+    }
+  } defer_scope;
   auto drop_spec = [&]() {
     if (!spec.ok) return;
     // on the pre-passes' own stream: ordered after them, and s never waits
@@ -1473,6 +1521,7 @@ int spamm_sp2_solve_ex(const spamm_mat* f, double n_occ, double tau, int32_t max
                &bmargin);
     if (spec.ok && (!square || c->m.nblocks != c_blocks_before)) drop_spec();
     spamm::dfree(fuse.ukeys, s);  // (null once the update took it)
+    resolve_timings();  // (after sp2_finish's host sync: the events are complete)
     const int k = rep->n_multiplies++;
     rep->leaf_products[k] = st.leaf_products;
     rep->executed_products[k] = st.executed_products;
