@@ -322,6 +322,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
   } else if (warp == OZ_MMA) {
     // ---------------- MMA issuer: one thread ----------------
     if (lane == 0) {
+      const bool wide = !(hint & 4);  // SPAMM_K4Z_HINT bit 2: the 10 x N = 128 MMA form
       int stage = 0;
       uint32_t phase = 0, tphase = 0;
       int64_t cur2 = 0;
@@ -357,6 +358,25 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
           tc_after();
         }
         const uint32_t sa = base + stage * OZ_STAGE, sb = sa + OZ_BLOCK_BYTES;
+        if (wide) {
+          // the same 10 slice-pair blocks as 4 MMAs of N = 256 (four B slices:
+          // two adjacent tiles) + 2 of N = 128 per k-step: 20 % less shared-
+          // memory operand traffic (the A pair is read once for two B pairs).
+          // The first two open tiles 0-1 and 2-3; the rest accumulate.
+#pragma unroll
+          for (int ks = 0; ks < 2; ++ks) {
+#pragma unroll
+            for (int mi = 0; mi < 6; ++mi) {
+              const int p = mi == 0 ? 0 : mi == 1 ? 0 : mi == 2 ? 2 : mi == 3 ? 4 : mi == 4 ? 2 : 6;
+              const int q = mi == 1 ? 4 : mi == 4 ? 4 : 0;
+              const bool n256 = mi < 4;
+              const bool opens = mi < 2;
+              oz_mma(tbase + 128u * ((p + q) / 2), oz_desc(sa + p * OZ_SLICE_BYTES + ks * 256),
+                     oz_desc(sb + q * OZ_SLICE_BYTES + ks * 256),
+                     (first && opens && ks == 0) ? 0u : 1u, n256 ? OZ_IDESC_N256 : OZ_IDESC);
+            }
+          }
+        } else {
 #pragma unroll
         for (int ci = 0; ci < 10; ++ci) {
           const int p = oz_p(ci), q = oz_q(ci), t = (p + q) / 2;
@@ -366,6 +386,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
             oz_mma(tbase + 128u * t, oz_desc(sa + p * OZ_SLICE_BYTES + ks * 256),
                    oz_desc(sb + q * OZ_SLICE_BYTES + ks * 256),
                    (first && opens && ks == 0) ? 0u : 1u);
+        }
         }
         oz_commit(empty(stage));  // stage free once these MMAs have read it
         ++n_tasks;

@@ -163,11 +163,15 @@ __device__ __forceinline__ uint64_t oz_desc(uint32_t addr, uint32_t sbo = 512) {
 // Instruction descriptor: D s32, A/B signed int8, both K-major, N = 128, M = 128.
 constexpr uint32_t OZ_IDESC =
     (2u << 4) | (1u << 7) | (1u << 10) | ((128u >> 3) << 17) | ((128u >> 4) << 24);
-__device__ __forceinline__ void oz_mma(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t acc) {
+// N = 256 (four B slices): the accumulator spans two adjacent 128-column tiles.
+constexpr uint32_t OZ_IDESC_N256 =
+    (2u << 4) | (1u << 7) | (1u << 10) | ((256u >> 3) << 17) | ((128u >> 4) << 24);
+__device__ __forceinline__ void oz_mma(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t acc,
+                                       uint32_t idesc = OZ_IDESC) {
   asm volatile(
       "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
       " tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
-      "l"(a), "l"(b), "r"(OZ_IDESC), "r"(acc)
+      "l"(a), "l"(b), "r"(idesc), "r"(acc)
       : "memory");
 }
 __device__ __forceinline__ void oz_commit(uint32_t bar) {
