@@ -147,6 +147,9 @@ __global__ void __launch_bounds__(256) k_oz32_split(const double* __restrict__ d
   }
 }
 
+__constant__ int c_z_narrow = 0;  // 1: three N = 128 MMAs per product (SPAMM_K4Z_HINT bit 2)
+__device__ __forceinline__ bool z_wide_mma() { return c_z_narrow == 0; }
+
 template <class Idx, int NBUF, int Z_TPS, int Z_STAGES>
 __global__ void __launch_bounds__(Z_THREADS, NBUF == 2 ? 1 : 2)
     k_leaf_ozaki32(int64_t n_seg, const int64_t* __restrict__ seg, const Idx* __restrict__ a_idx,
@@ -277,6 +280,8 @@ __global__ void __launch_bounds__(Z_THREADS, NBUF == 2 ? 1 : 2)
   } else if (warp == 5) {
     // ---------------- MMA issuer: one thread, 3 MMAs per task ----------------
     if (lane == 0) {
+      static_assert(Z_NB == 32, "");
+      const bool wide = z_wide_mma();
       int stage = 0, nchunk = 0;
       uint32_t phase = 0, tph[2] = {0u, 0u};
       int64_t cur2 = 0;
@@ -304,8 +309,12 @@ __global__ void __launch_bounds__(Z_THREADS, NBUF == 2 ? 1 : 2)
         for (int q = 0; q < n_in; ++q) {
           const uint32_t sa = base + stage * Z_STAGE + q * Z_TASK, sb = sa + Z_BLOCK_BYTES;
           const uint32_t init = (first && q == 0) ? 0u : 1u;
-          oz_mma(d0, oz_desc(sa, Z_SBO), oz_desc(sb, Z_SBO), init);
-          oz_mma(d0 + 128u, oz_desc(sa, Z_SBO), oz_desc(sb + 4 * Z_SLICE_BYTES, Z_SBO), init);
+          if (wide) {  // anchors (0,0) and (0,4) as one N = 256 MMA over tiles 0-1
+            oz_mma(d0, oz_desc(sa, Z_SBO), oz_desc(sb, Z_SBO), init, OZ_IDESC_N256);
+          } else {
+            oz_mma(d0, oz_desc(sa, Z_SBO), oz_desc(sb, Z_SBO), init);
+            oz_mma(d0 + 128u, oz_desc(sa, Z_SBO), oz_desc(sb + 4 * Z_SLICE_BYTES, Z_SBO), init);
+          }
           oz_mma(d0 + 128u, oz_desc(sa + 4 * Z_SLICE_BYTES, Z_SBO), oz_desc(sb, Z_SBO), 1u);
         }
         oz_commit(empty(stage));
@@ -507,6 +516,9 @@ void oz32_launch_cfg(int64_t n_seg, const int64_t* seg, const Idx* a_idx, const 
   std::call_once(once, [&] {
     SPAMM_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)Cfg::SMEM));
+    const char* v = getenv("SPAMM_K4Z_HINT");
+    const int narrow = (v && (atoi(v) & 4)) ? 1 : 0;
+    SPAMM_CK(cudaMemcpyToSymbol(c_z_narrow, &narrow, sizeof(int)));
   });
   int64_t grid = (int64_t)multiprocessors() * Cfg::CTAS;
   if (grid > n_seg) grid = n_seg;
