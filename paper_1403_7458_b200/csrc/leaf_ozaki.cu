@@ -21,10 +21,12 @@
 //    order);
 //  * all digit pairs p + q <= 7 (and four of p + q = 8) are formed: A slices
 //    stacked two per MMA along M (rows 0-63 = s_p, 64-127 = s_p+1), B slices
-//    two per MMA along N, 10 slice-pair blocks x 2 k-steps = 20 MMAs of
-//    128x128x32 per task into 4 TMEM tiles of 128 columns (tile t holds the
-//    pairs of digit sums 2t, 2t+1, 2t+1, 2t+2 in its four quadrants) -- all
-//    512 TMEM columns;
+//    two per 128 columns along N: 10 slice-pair blocks per k-step into 4 TMEM
+//    tiles of 128 columns (tile t holds the pairs of digit sums 2t, 2t+1,
+//    2t+1, 2t+2 in its four quadrants) -- all 512 TMEM columns.  The blocks
+//    sharing an A pair and two consecutive B pairs are one MMA of N = 256 over
+//    two adjacent tiles: per k-step 4 MMAs of 128x256x32 + 2 of 128x128x32
+//    (12 per task, 20 % less shared-memory operand traffic than 20 of N = 128);
 //  * the epilogue adds the quadrants of equal digit sum d in int32 (exact),
 //    so S_d[r][c] = S_d[c][r] bitwise for a symmetric operand, and rounds once
 //    per d: C = 2^(Er+Ec-14) sum_d S_d 2^-8d (Horner with fused multiply-add).
@@ -38,8 +40,8 @@
 // bitwise symmetric), not bitwise the DMMA kernel's.
 //
 // Operand traffic per task is the FP64 kernel's (8 slices x 4 KB = 32 KB per
-// block), compute per task is 20 tcgen05 MMAs of 128x128x32 = 1,333 tensor
-// cycles versus ~4,100 cycles of DMMA at 64x64x64.
+// block), compute per task is the work of 20 tcgen05 MMAs of 128x128x32 =
+// 1,333 tensor cycles versus ~4,100 cycles of DMMA at 64x64x64.
 #include <climits>
 #include <cstdlib>
 #include <cstring>
