@@ -111,11 +111,13 @@ __global__ void __launch_bounds__(256) k_oz_exponents(const double* __restrict__
       }
       __syncthreads();
     } else {
-      // thread t: 16 consecutive elements of row t / 4 (8 independent 16-byte loads)
-      const double2* q = reinterpret_cast<const double2*>(b + (t >> 2) * OZ_NB + (t & 3) * 16);
+      // thread t: 16 elements of row t / 4, pairs t % 4, t % 4 + 4, ... (8
+      // independent 16-byte loads; a quad reads 64 contiguous bytes per load,
+      // so every sector a warp fetches is used whole)
+      const double2* q = reinterpret_cast<const double2*>(b + (t >> 2) * OZ_NB) + (t & 3);
       double2 v[8];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) v[i] = q[i];
+      for (int i = 0; i < 8; ++i) v[i] = q[4 * i];
       double mx = 0.0;
 #pragma unroll
       for (int i = 0; i < 8; ++i) mx = fmax(mx, fmax(oz_absf(v[i].x), oz_absf(v[i].y)));
@@ -136,7 +138,11 @@ __global__ void __launch_bounds__(256) k_oz_split(const double* __restrict__ dat
                                                   const int* __restrict__ ex,
                                                   int8_t* __restrict__ out) {
   pdl_wait();
-  __shared__ double tile[OZ_NB * (OZ_NB + 1)];
+  // Staged through shared memory in both roles (coalesced global loads):
+  // trans: element (r, c) at r * 65 + c, read down column n;  !trans: at
+  // r * 68 + c + c / 16, so a half-warp's reads (4 rows x 4 column groups)
+  // fall in 16 distinct 8-byte banks.
+  __shared__ double tile[OZ_NB * 68];
   const int t = threadIdx.x, n = t >> 2, kc = t & 3;
   for (int64_t s = blockIdx.x; s < nblocks; s += gridDim.x) {
     const double* b = data + s * (OZ_NB * OZ_NB);
@@ -146,16 +152,21 @@ __global__ void __launch_bounds__(256) k_oz_split(const double* __restrict__ dat
       __syncthreads();
 #pragma unroll
       for (int i = 0; i < 16; ++i) y[i] = tile[(kc * 16 + i) * (OZ_NB + 1) + n];
-      __syncthreads();
     } else {
-      const double2* q = reinterpret_cast<const double2*>(b + n * OZ_NB + kc * 16);
+      const double2* q = reinterpret_cast<const double2*>(b);
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
+      for (int j = 0; j < 8; ++j) {
+        const int i = t + 256 * j, c = (2 * i) & 63;
         const double2 v = q[i];
-        y[2 * i] = v.x;
-        y[2 * i + 1] = v.y;
+        double* d = tile + (i >> 5) * 68 + c + (c >> 4);
+        d[0] = v.x;
+        d[1] = v.y;
       }
+      __syncthreads();
+#pragma unroll
+      for (int i = 0; i < 16; ++i) y[i] = tile[n * 68 + kc * 17 + i];
     }
+    __syncthreads();
     const int64_t key = keys[s];
     const int e = oz_exp(ex[(trans ? key % G : key / G) * OZ_NB + n]);
     uint32_t hi[16], lo[16];
@@ -177,6 +188,15 @@ __global__ void __launch_bounds__(256) k_oz_split(const double* __restrict__ dat
                      oz_gather4(h[12], h[13], h[14], h[15], byte));
     }
   }
+}
+
+// One full wave of `fn` (resident CTAs per SM x SMs): grids of the streaming
+// pre-passes, which loop over the blocks, never leave a partial second wave.
+template <typename F>
+int resident_wave(F* fn, int threads) {
+  int per_sm = 0;
+  SPAMM_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, 0));
+  return (per_sm > 0 ? per_sm : 1) * multiprocessors();
 }
 
 // tr[s] = storage slot of the transposed block of s (symmetric operands).
@@ -770,9 +790,11 @@ bool ozaki_prepare(const Mat& A, const Mat& B, bool sym_b, cudaStream_t s, Ozaki
     }
     return true;
   }
-  const int gx = grid_for(A.nblocks, 1, (int64_t)multiprocessors() * 8);
+  static const int wave_ex = resident_wave(k_oz_exponents, 256);
+  static const int wave_split = resident_wave(k_oz_split, 256);
+  const int gx = grid_for(A.nblocks, 1, wave_split);
   if (!ex_a_given) {
-    launch_plain(k_oz_exponents, gx, 256, 0, s, A.data, A.keys, A.nblocks, G, 0, op.ex_a);
+    launch_plain(k_oz_exponents, grid_for(A.nblocks, 1, wave_ex), 256, 0, s, A.data, A.keys, A.nblocks, G, 0, op.ex_a);
     SPAMM_LAUNCH_CK();
     oz_dbg("exponents A", s);
     launch_pdl(k_oz_split, gx, 256, 0, s, A.data, A.keys, A.nblocks, G, 0, (const int*)op.ex_a,
@@ -791,14 +813,14 @@ bool ozaki_prepare(const Mat& A, const Mat& B, bool sym_b, cudaStream_t s, Ozaki
                A.nblocks, G, (const int32_t*)A.slot, op.b_tr);
     SPAMM_LAUNCH_CK();
   } else {
-    const int gy = grid_for(B.nblocks, 1, (int64_t)multiprocessors() * 8);
+    const int gy = grid_for(B.nblocks, 1, wave_split);
     if (ex_b_given) {
       op.ex_b_ext = true;
       op.ex_b = B.oz_ex_col;
     } else {
       op.ex_b = dmalloc<int>(G * OZ_NB, s);
       SPAMM_CK(cudaMemsetAsync(op.ex_b, 0x80, G * OZ_NB * sizeof(int), s));
-      launch_pdl(k_oz_exponents, gy, 256, 0, s, B.data, B.keys, B.nblocks, G, 1, op.ex_b);
+      launch_pdl(k_oz_exponents, grid_for(B.nblocks, 1, wave_ex), 256, 0, s, B.data, B.keys, B.nblocks, G, 1, op.ex_b);
       SPAMM_LAUNCH_CK();
     }
     launch_pdl(k_oz_split, gy, 256, 0, s, B.data, B.keys, B.nblocks, G, 1, (const int*)op.ex_b,
@@ -832,8 +854,8 @@ void ozaki_exponents(const Mat& M, bool by_col, int* ex, cudaStream_t s) {
     oz32_exponents(M, by_col, ex, s);
     return;
   }
-  const int gx = grid_for(M.nblocks, 1, (int64_t)multiprocessors() * 8);
-  launch_plain(k_oz_exponents, gx, 256, 0, s, (const double*)M.data, (const int64_t*)M.keys,
+  static const int wave_ex = resident_wave(k_oz_exponents, 256);
+  launch_plain(k_oz_exponents, grid_for(M.nblocks, 1, wave_ex), 256, 0, s, (const double*)M.data, (const int64_t*)M.keys,
                M.nblocks, M.G, by_col ? 1 : 0, ex);
   SPAMM_LAUNCH_CK();
 }

@@ -83,10 +83,11 @@ __global__ void __launch_bounds__(256) k_oz32_exponents(const double* __restrict
 #pragma unroll
         for (int i = 0; i < 16; ++i) mx = fmax(mx, oz_absf(b[(half * 16 + i) * Z_NB + line]));
       } else {
-        const double2* q = reinterpret_cast<const double2*>(b + line * Z_NB + half * 16);
+        // pairs half, half + 2, ...: a lane pair reads one whole sector per load
+        const double2* q = reinterpret_cast<const double2*>(b + line * Z_NB) + half;
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-          const double2 v = q[i];
+          const double2 v = q[2 * i];
           mx = fmax(mx, fmax(oz_absf(v.x), oz_absf(v.y)));
         }
       }
@@ -116,12 +117,27 @@ __global__ void __launch_bounds__(256) k_oz32_split(const double* __restrict__ d
 #pragma unroll
       for (int i = 0; i < 16; ++i) y[i] = b[(kc * 16 + i) * Z_NB + n];
     } else {
-      const double2* q = reinterpret_cast<const double2*>(b + n * Z_NB + kc * 16);
+      // coalesced: lane pair (kc = 0, 1) loads pairs kc + 2i (one sector per
+      // load), then swaps the halves the other lane needs -- lane kc ends
+      // with pairs 8 kc .. 8 kc + 7 (k = 16 kc .. 16 kc + 15)
+      const double2* q = reinterpret_cast<const double2*>(b + n * Z_NB) + kc;
+      double2 v[8];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const double2 v = q[i];
-        y[2 * i] = v.x;
-        y[2 * i + 1] = v.y;
+      for (int i = 0; i < 8; ++i) v[i] = q[2 * i];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        // lane 0 keeps v[i] (pair 2i) and receives lane 1's v[i] (pair 2i + 1);
+        // lane 1 keeps v[i + 4] (pair 2i + 9) and receives lane 0's v[i + 4] (pair 2i + 8)
+        const double2 send = kc ? v[i] : v[i + 4];
+        const double2 keep = kc ? v[i + 4] : v[i];
+        double2 got;
+        got.x = __shfl_xor_sync(0xffffffffu, send.x, 1);
+        got.y = __shfl_xor_sync(0xffffffffu, send.y, 1);
+        const double2 lo = kc ? got : keep, hi = kc ? keep : got;
+        y[4 * i] = lo.x;
+        y[4 * i + 1] = lo.y;
+        y[4 * i + 2] = hi.x;
+        y[4 * i + 3] = hi.y;
       }
     }
     const int64_t key = keys[s];
