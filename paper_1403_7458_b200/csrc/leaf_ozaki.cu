@@ -42,6 +42,7 @@
 // Operand traffic per task is the FP64 kernel's (8 slices x 4 KB = 32 KB per
 // block), compute per task is the work of 20 tcgen05 MMAs of 128x128x32 =
 // 1,333 tensor cycles versus ~4,100 cycles of DMMA at 64x64x64.
+#include <algorithm>
 #include <climits>
 #include <cstdlib>
 #include <cstring>
@@ -136,7 +137,9 @@ __global__ void __launch_bounds__(256) k_oz_split(const double* __restrict__ dat
                                                   const int64_t* __restrict__ keys,
                                                   int64_t nblocks, int64_t G, int trans,
                                                   const int* __restrict__ ex,
-                                                  int8_t* __restrict__ out) {
+                                                  int8_t* __restrict__ out,
+                                                  const int32_t* __restrict__ slot,
+                                                  int32_t* __restrict__ tr) {
   pdl_wait();
   // Staged through shared memory in both roles (coalesced global loads):
   // trans: element (r, c) at r * 65 + c, read down column n;  !trans: at
@@ -168,6 +171,8 @@ __global__ void __launch_bounds__(256) k_oz_split(const double* __restrict__ dat
     }
     __syncthreads();
     const int64_t key = keys[s];
+    // (symmetric operands) storage slot of the transposed block
+    if (tr && t == 0) tr[s] = slot[(key % G) * G + key / G];
     const int e = oz_exp(ex[(trans ? key % G : key / G) * OZ_NB + n]);
     uint32_t hi[16], lo[16];
 #pragma unroll
@@ -362,7 +367,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
           mbar_arrive(tfull);
           oz_commit(tfull);
           if (prof) {
-            long long* o = prof + blockIdx.x * 8;
+            long long* o = prof + blockIdx.x * 16;
             o[0] = clock64() - t_start;
             o[1] = w_full;
             o[2] = w_tempty;
@@ -435,6 +440,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
     const uint32_t lane_base = tbase + ((uint32_t)((warp & 3) * 32) << 16);
     uint32_t ephase = 0;
     long long e_wait = 0, e_hold = 0, e_all = 0, n_blk = 0;
+    long long e_ph[4] = {0, 0, 0, 0};  // chunk phases: TMEM read, exchange, convert+store, barrier
     for (;;) {
       long long te0 = prof ? clock64() : 0;
       mbar_wait(tfull, ephase);
@@ -445,10 +451,11 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
       const int64_t md = ring[0];
       if (md < 0) {
         if (prof && threadIdx.x == 0) {
-          prof[blockIdx.x * 8 + 4] = e_wait;
-          prof[blockIdx.x * 8 + 5] = e_hold;
-          prof[blockIdx.x * 8 + 6] = e_all;
-          prof[blockIdx.x * 8 + 7] = n_blk;
+          prof[blockIdx.x * 16 + 4] = e_wait;
+          prof[blockIdx.x * 16 + 5] = e_hold;
+          prof[blockIdx.x * 16 + 6] = e_all;
+          prof[blockIdx.x * 16 + 7] = n_blk;
+          for (int i = 0; i < 4; ++i) prof[blockIdx.x * 16 + 8 + i] = e_ph[i];
         }
         break;
       }
@@ -475,6 +482,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
 #pragma unroll 1
       for (int cl = 0; cl < 4; ++cl) {
         const int cc = grp * 4 + cl;
+        long long tp = (prof && threadIdx.x == 0) ? clock64() : 0;
         int L[4][8], R[4][8];
 #pragma unroll
         for (int t = 0; t < 4; ++t) {
@@ -487,6 +495,11 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
         for (int t = 1; t < 4; ++t) {
           tmem_keep8(L[t]);
           tmem_keep8(R[t]);
+        }
+        if (prof && threadIdx.x == 0) {
+          const long long t1 = clock64();
+          e_ph[0] += t1 - tp;
+          tp = t1;
         }
         if (cl == 3) {  // this warp's TMEM reads are complete: hand TMEM back
           tc_before();
@@ -506,6 +519,11 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
         const int col0 = cc * 8 + own0;
         const int4 ec4 = *reinterpret_cast<const int4*>(ex_b + bj * OZ_NB + col0);
         asm volatile("bar.sync %0, 128;\n" ::"r"(1 + grp) : "memory");
+        if (prof && threadIdx.x == 0) {
+          const long long t1 = clock64();
+          e_ph[1] += t1 - tp;
+          tp = t1;
+        }
         int oL[4][4], oR[4][4];
 #pragma unroll
         for (int t = 0; t < 4; ++t) {
@@ -535,9 +553,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
           const int S[9] = {tl[0],         tr[0] + bl[0], tl[1] + br[0],
                             tr[1] + bl[1], tl[2] + br[1], tr[2] + bl[2],
                             tl[3] + br[2], tr[3] + bl[3], br[3]};
-          double v = (double)S[8];
-#pragma unroll
-          for (int d = 7; d >= 0; --d) v = __fma_rn(v, 0x1p-8, (double)S[d]);
+          const double v = oz_horner(S);
           const int k = er + (bad[c] ? 0 : oz_exp(ecs[c]));  // C = v 2^k
           res[c] = (k >= -1022 && k <= 1023)
                        ? __dmul_rn(v, __longlong_as_double((long long)(k + 1023) << 52))
@@ -564,22 +580,22 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
             res[c] = v;
           }
         } else {
+          double* rp = reinterpret_cast<double*>(row);
           if (cont) {
-            const double2 p0 = row[0], p1 = row[1];
-            res[0] = __dadd_rn(p0.x, res[0]);
-            res[1] = __dadd_rn(p0.y, res[1]);
-            res[2] = __dadd_rn(p1.x, res[2]);
-            res[3] = __dadd_rn(p1.y, res[3]);
+            double p0, p1, p2, p3;
+            oz_ld4(rp, p0, p1, p2, p3);
+            res[0] = __dadd_rn(p0, res[0]);
+            res[1] = __dadd_rn(p1, res[1]);
+            res[2] = __dadd_rn(p2, res[2]);
+            res[3] = __dadd_rn(p3, res[3]);
           }
           if (hint & 2) {  // products streamed past L2 (evict_first)
-            __stcs(row, make_double2(res[0], res[1]));
-            __stcs(row + 1, make_double2(res[2], res[3]));
+            oz_st4_cs(rp, res[0], res[1], res[2], res[3]);
             if (Cm)
 #pragma unroll
               for (int c = 0; c < 4; ++c) __stcs(Cm + (col0 + c) * OZ_NB + r, res[c]);
           } else {
-            row[0] = make_double2(res[0], res[1]);
-            row[1] = make_double2(res[2], res[3]);
+            oz_st4(rp, res[0], res[1], res[2], res[3]);
             if (Cm)
 #pragma unroll
               for (int c = 0; c < 4; ++c) Cm[(col0 + c) * OZ_NB + r] = res[c];
@@ -598,7 +614,13 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
           else if (cl == 2) { ca2 = wa; cb2 = wb; }
           else { ca3 = wa; cb3 = wb; }
         }
+        if (prof && threadIdx.x == 0) {
+          const long long t1 = clock64();
+          e_ph[2] += t1 - tp;
+          tp = t1;
+        }
         asm volatile("bar.sync %0, 128;\n" ::"r"(1 + grp) : "memory");
+        if (prof && threadIdx.x == 0) e_ph[3] += clock64() - tp;
       }
       if (want_ex) {
         if (Cm) {  // mirror rows: a column's max over this warp's 32 rows
@@ -793,25 +815,25 @@ bool ozaki_prepare(const Mat& A, const Mat& B, bool sym_b, cudaStream_t s, Ozaki
   static const int wave_ex = resident_wave(k_oz_exponents, 256);
   static const int wave_split = resident_wave(k_oz_split, 256);
   const int gx = grid_for(A.nblocks, 1, wave_split);
+  // symmetric: the transposed-slot map comes out of A's split
+  if (sym_b && !op.tail_cached) op.b_tr = dmalloc<int32_t>(A.nblocks > 0 ? A.nblocks : 1, s);
+  int32_t* tr = sym_b ? op.b_tr : nullptr;
   if (!ex_a_given) {
-    launch_plain(k_oz_exponents, grid_for(A.nblocks, 1, wave_ex), 256, 0, s, A.data, A.keys, A.nblocks, G, 0, op.ex_a);
+    launch_plain(k_oz_exponents, grid_for(A.nblocks, 1, wave_ex), 256, 0, s, A.data, A.keys,
+                 A.nblocks, G, 0, op.ex_a);
     SPAMM_LAUNCH_CK();
     oz_dbg("exponents A", s);
     launch_pdl(k_oz_split, gx, 256, 0, s, A.data, A.keys, A.nblocks, G, 0, (const int*)op.ex_a,
-               op.as);
+               op.as, (const int32_t*)A.slot, tr);
   } else {  // (first launch after the cross-stream wait: plain)
     launch_plain(k_oz_split, gx, 256, 0, s, A.data, A.keys, A.nblocks, G, 0,
-                 (const int*)op.ex_a, op.as);
+                 (const int*)op.ex_a, op.as, (const int32_t*)A.slot, tr);
   }
   SPAMM_LAUNCH_CK();
   oz_dbg("split A", s);
   if (sym_b) {
     op.ex_b = op.ex_a;
     op.bs = op.as;
-    if (!op.tail_cached) op.b_tr = dmalloc<int32_t>(A.nblocks > 0 ? A.nblocks : 1, s);
-    launch_pdl(k_oz_trslot, grid_for(A.nblocks, 256), 256, 0, s, (const int64_t*)A.keys,
-               A.nblocks, G, (const int32_t*)A.slot, op.b_tr);
-    SPAMM_LAUNCH_CK();
   } else {
     const int gy = grid_for(B.nblocks, 1, wave_split);
     if (ex_b_given) {
@@ -824,7 +846,7 @@ bool ozaki_prepare(const Mat& A, const Mat& B, bool sym_b, cudaStream_t s, Ozaki
       SPAMM_LAUNCH_CK();
     }
     launch_pdl(k_oz_split, gy, 256, 0, s, B.data, B.keys, B.nblocks, G, 1, (const int*)op.ex_b,
-               op.bs);
+               op.bs, (const int32_t*)nullptr, (int32_t*)nullptr);
     SPAMM_LAUNCH_CK();
     oz_dbg("B passes", s);
   }
@@ -905,8 +927,8 @@ void ozaki_launch(int64_t n_seg, const int64_t* seg, const Idx* a_idx, const Idx
   int64_t grid = multiprocessors();
   if (grid > n_seg) grid = n_seg;
   if (want_prof) {
-    prof = dmalloc<long long>((size_t)grid * 8, s);
-    SPAMM_CK(cudaMemsetAsync(prof, 0, (size_t)grid * 64, s));
+    prof = dmalloc<long long>((size_t)grid * 16, s);
+    SPAMM_CK(cudaMemsetAsync(prof, 0, (size_t)grid * 128, s));
   }
   // (plain launch: K4z follows a wait on the pre-pass stream, see launch_plain)
   launch_plain(kern, (unsigned)grid, OZ_THREADS, OZ_SMEM, s, n_seg, seg, a_idx, b_idx,
@@ -917,16 +939,21 @@ void ozaki_launch(int64_t n_seg, const int64_t* seg, const Idx* a_idx, const Idx
   SPAMM_LAUNCH_CK();
   oz_dbg("k4z", s);
   if (prof) {  // SPAMM_K4Z_PROF=1: per-launch cycle breakdown (diagnostics; syncs)
-    std::vector<long long> h((size_t)grid * 8);
+    std::vector<long long> h((size_t)grid * 16);
     SPAMM_CK(cudaMemcpyAsync(h.data(), prof, h.size() * 8, cudaMemcpyDeviceToHost, s));
     SPAMM_CK(cudaStreamSynchronize(s));
-    double a[8] = {0};
-    for (int64_t b = 0; b < grid; ++b)
-      for (int i = 0; i < 8; ++i) a[i] += (double)h[b * 8 + i] / grid;
+    double a[12] = {0}, lo = 1e300, hi = 0;
+    for (int64_t b = 0; b < grid; ++b) {
+      for (int i = 0; i < 12; ++i) a[i] += (double)h[b * 16 + i] / grid;
+      lo = std::min(lo, (double)h[b * 16]);
+      hi = std::max(hi, (double)h[b * 16]);
+    }
     fprintf(stderr,
-            "[k4z] cycles %.0f: mma waits full %.0f tempty %.0f, tasks %.0f (%.0f cyc/task); "
-            "epi wait %.0f hold %.0f all %.0f blocks %.0f\n",
-            a[0], a[1], a[2], a[3], a[0] / (a[3] > 0 ? a[3] : 1), a[4], a[5], a[6], a[7]);
+            "[k4z] cycles %.0f (CTA min %.0f max %.0f): mma waits full %.0f tempty %.0f, "
+            "tasks %.0f (%.0f cyc/task); epi wait %.0f hold %.0f all %.0f blocks %.0f; "
+            "chunk phases tmem %.0f exchange %.0f convert+store %.0f barrier %.0f\n",
+            a[0], lo, hi, a[1], a[2], a[3], a[0] / (a[3] > 0 ? a[3] : 1), a[4], a[5], a[6], a[7],
+            a[8], a[9], a[10], a[11]);
     dfree(prof, s);
   }
   dfree(scratch, s);

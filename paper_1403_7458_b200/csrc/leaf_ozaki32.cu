@@ -417,9 +417,7 @@ __global__ void __launch_bounds__(Z_THREADS, NBUF == 2 ? 1 : 2)
 #pragma unroll
               for (int i = 0; i < 4; ++i)
                 S[4 * T + i + j] += xb[(((T * 4 + j) * 4 + i) * 8 + c8) * 32 + r];
-          double v = (double)S[10];
-#pragma unroll
-          for (int d = 9; d >= 0; --d) v = __fma_rn(v, 0x1p-8, (double)S[d]);
+          const double v = oz_horner(S);
           const int col = cc * 8 + c8;
           const int exc = ex_b[bj * Z_NB + col];
           bad[h] = row_bad || exc == OZ_EXP_BAD;

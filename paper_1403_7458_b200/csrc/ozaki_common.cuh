@@ -16,6 +16,42 @@ constexpr int OZ_EXP_NONE = (int)0x80808080;  // memset pattern: "no nonzero see
 constexpr int OZ_EXP_BAD = 0x7fffffff;
 
 __device__ __forceinline__ int oz_exp(int e) { return e == OZ_EXP_NONE ? 0 : e; }
+
+// sum_d S_d 2^-8d (d = 0 .. NL-1) in the Horner order of the design --
+// v = S_{NL-1}, then v = RN(v 2^-8 + S_d) for d = NL-2 .. 0 -- bitwise, with
+// fewer FP64 operations: for |S_d| < 2^31 the first two steps are exact
+// (<= 40 and 48 significant bits) and the third rounds the exact value
+// T 2^-24, T = S_{NL-1} + 2^8 S_{NL-2} + 2^16 S_{NL-3} + 2^24 S_{NL-4}
+// (|T| < 2^56, exact in int64), so those three steps are one int64
+// conversion; the fourth folds the 2^-24 into its (exact) scaling.
+template <int NL>
+__device__ __forceinline__ double oz_horner(const int (&S)[NL]) {
+  static_assert(NL >= 5, "oz_horner: at least 5 digit levels");
+  const long long T = (long long)S[NL - 1] + (long long)S[NL - 2] * 256LL +
+                      (long long)S[NL - 3] * 65536LL + (long long)S[NL - 4] * 16777216LL;
+  double v = __fma_rn(__ll2double_rn(T), 0x1p-32, (double)S[NL - 5]);
+#pragma unroll
+  for (int d = NL - 6; d >= 0; --d) v = __fma_rn(v, 0x1p-8, (double)S[d]);
+  return v;
+}
+
+// 32-byte global accesses (sm_100: LDG/STG.256): one whole sector per lane
+// for the four C elements an epilogue thread owns in a row.
+__device__ __forceinline__ void oz_ld4(const double* p, double& a, double& b, double& c,
+                                       double& d) {
+  asm volatile("ld.global.v4.f64 {%0, %1, %2, %3}, [%4];"
+               : "=d"(a), "=d"(b), "=d"(c), "=d"(d)
+               : "l"(p));
+}
+__device__ __forceinline__ void oz_st4(double* p, double a, double b, double c, double d) {
+  asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d)
+               : "memory");
+}
+__device__ __forceinline__ void oz_st4_cs(double* p, double a, double b, double c, double d) {
+  asm volatile("st.global.cs.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(a), "d"(b), "d"(c),
+               "d"(d)
+               : "memory");
+}
 // |x| for the exponent passes, +Inf for a non-finite x (fmax would drop NaN).
 __device__ __forceinline__ double oz_absf(double x) {
   return isfinite(x) ? fabs(x) : __longlong_as_double(0x7ff0000000000000LL);
