@@ -564,8 +564,9 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
           // a non-finite operand entry in this row or one of these columns:
           // those elements are computed once, at the segment's end, in FP64
           // in the reference's order (earlier chunks leave them untouched)
+          // (unrolled: a dynamically indexed res[] would live in local memory)
           double* rp = Cb + r * OZ_NB + col0;
-#pragma unroll 1
+#pragma unroll
           for (int c = 0; c < 4; ++c) {
             double v = res[c];
             if (bad[c]) {

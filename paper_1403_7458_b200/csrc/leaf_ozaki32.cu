@@ -431,8 +431,9 @@ __global__ void __launch_bounds__(Z_THREADS, NBUF == 2 ? 1 : 2)
         if (bad[0] || bad[1]) {
           // non-finite operand entries: those elements are computed once, at
           // the segment's end, in FP64 in the reference's order (leaf_ozaki.cu)
+          // (unrolled: a dynamically indexed res[] would live in local memory)
           double* rp = Cb + r * Z_NB + col0;
-#pragma unroll 1
+#pragma unroll
           for (int h = 0; h < 2; ++h) {
             double v = res[h];
             if (bad[h]) {
