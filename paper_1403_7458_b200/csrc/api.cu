@@ -648,7 +648,7 @@ cudaStream_t ozaki_side_stream() {  // one per (host thread, device)
   return t;
 }
 void ozaki_ahead(const spamm_mat* a, const spamm_mat* b, int32_t kernel, cudaStream_t s,
-                 OzakiAhead& oz) {
+                 OzakiAhead& oz, bool defer_tr = false) {
   // AUTO prepares ahead only when the slices are small next to HBM (they are
   // allocated before C, whose size the cull has not told yet); larger
   // operands take the post-cull path (leaf_dispatch), which tries the
@@ -666,7 +666,7 @@ void ozaki_ahead(const spamm_mat* a, const spamm_mat* b, int32_t kernel, cudaStr
   }();
   if (!use_side) {
     oz.ok = spamm::ozaki_prepare(a->m, b->m, a == b && a->m.sym, s, oz.op,
-                                 /*try_only=*/kernel == spamm::LEAF_AUTO);
+                                 /*try_only=*/kernel == spamm::LEAF_AUTO, defer_tr);
     return;  // (same stream: no event needed)
   }
   cudaStream_t side = ozaki_side_stream();
@@ -681,7 +681,7 @@ void ozaki_ahead(const spamm_mat* a, const spamm_mat* b, int32_t kernel, cudaStr
   SPAMM_CK(cudaEventRecord(ev[0], s));
   SPAMM_CK(cudaStreamWaitEvent(side, ev[0], 0));
   oz.ok = spamm::ozaki_prepare(a->m, b->m, a == b && a->m.sym, side, oz.op,
-                               /*try_only=*/kernel == spamm::LEAF_AUTO);
+                               /*try_only=*/kernel == spamm::LEAF_AUTO, defer_tr);
   if (oz.ok) {
     oz.ready = ev[1];
     SPAMM_CK(cudaEventRecord(oz.ready, side));
@@ -778,6 +778,7 @@ void multiply_impl(const spamm_mat* a, const spamm_mat* b, double tau, int32_t k
   if (oz.ok) {  // K4z on the operands prepared alongside the cull
     if (oz.ready) SPAMM_CK(cudaStreamWaitEvent(s, oz.ready, 0));
     oz.ready = nullptr;
+    spamm::ozaki_finish_tr(a->m, oz.op, s);  // (operands prepared before a's slot map)
     if (r.n_c > 0) {
       spamm::LptSchedule lpt;
       lpt.order = r.order;
@@ -854,7 +855,8 @@ void sp2_finish(const spamm_mat* x, const spamm_mat* c, double n_occ, bool want_
                 cudaStream_t s, bool* square_out, double* t_x, double* t_sq, double* idem,
                 spamm_mat** e_out, const double* idem_dev = nullptr,
                 spamm::IdemFuse* fused_union = nullptr, double* branch_margin = nullptr,
-                const double* given_dev = nullptr) {
+                const double* given_dev = nullptr, int32_t kernel = 0,
+                OzakiAhead* ahead = nullptr) {
   // given_dev (multi-GPU shard): device [tr X, tr X^2, ||X^2 - X||_F] of the
   // WHOLE matrices (all-reduced); x / c are then this rank's shards.
   const bool fused = spamm::sp2_fused_supported(x->m.nb);
@@ -919,8 +921,22 @@ void sp2_finish(const spamm_mat* x, const spamm_mat* c, double n_occ, bool want_
   if (fused) {
     // with the residual fused into K1 there is nothing left to sync on: E's
     // exact-zero blocks stay pending (settled when the handle is inspected)
+    // -- so E's K4z operand passes can start on the side stream as soon as
+    // the update is queued, ahead of E's finalisation and the next cull
+    struct Hook {
+      spamm_mat* e;
+      int32_t kernel;
+      cudaStream_t s;
+      OzakiAhead* ahead;
+      static void run(void* p) {
+        auto* h = static_cast<Hook*>(p);
+        ozaki_ahead(h->e, h->e, h->kernel, h->s, *h->ahead, /*defer_tr=*/true);
+      }
+    } hook{e, kernel, s, ahead};
+    const bool early = e && ahead && idem_done;
     spamm::sp2_update_finish(x->m, c->m, prep, h[2], want_idem && !idem_done, !square, idem,
-                             e ? e->m : dummy, s, /*settle_now=*/!idem_done);
+                             e ? e->m : dummy, s, /*settle_now=*/!idem_done,
+                             early ? &Hook::run : nullptr, &hook);
   } else {
     spamm::sp2_update(x->m, c->m, want_idem && !idem_done, !square, idem, e ? e->m : dummy, s);
   }
@@ -1476,6 +1492,10 @@ int spamm_sp2_solve_ex(const spamm_mat* f, double n_occ, double tau, int32_t max
   }();
   OzakiAhead spec;
   const spamm_mat* spec_for = nullptr;
+  // E = 2X - X^2 (EXPAND): its operand passes start right after the update
+  // kernel, inside sp2_finish (the next multiply takes them)
+  OzakiAhead ahead;
+  const spamm_mat* ahead_for = nullptr;
   struct DeferScope {  // timed multiplies read their events after the branch sync
     DeferScope() { g_defer_timing = true; }
     ~DeferScope() {
@@ -1484,12 +1504,15 @@ int spamm_sp2_solve_ex(const spamm_mat* f, double n_occ, double tau, int32_t max
     }
   } defer_scope;
   auto drop_spec = [&]() {
-    if (!spec.ok) return;
     // on the pre-passes' own stream: ordered after them, and s never waits
-    spamm::ozaki_release(spec.op, spec.ready ? ozaki_side_stream() : s);
+    if (spec.ok) spamm::ozaki_release(spec.op, spec.ready ? ozaki_side_stream() : s);
     spec.ok = false;
     spec.ready = nullptr;
     spec_for = nullptr;
+    if (ahead.ok) spamm::ozaki_release(ahead.op, ahead.ready ? ozaki_side_stream() : s);
+    ahead.ok = false;
+    ahead.ready = nullptr;
+    ahead_for = nullptr;
   };
   for (int it = 0; it < max_iter; ++it) {
     auto* c = new spamm_mat();
@@ -1503,7 +1526,9 @@ int spamm_sp2_solve_ex(const spamm_mat* f, double n_occ, double tau, int32_t max
     }
     spamm::htrace("it_mul");
     multiply_impl(x, x, tau, kernel, timed != 0, s, c->m, &st, 0, -1, nullptr, true, fuse,
-                  spec.ok && spec_for == x ? &spec : nullptr);
+                  spec.ok && spec_for == x     ? &spec
+                  : ahead.ok && ahead_for == x ? &ahead
+                                               : nullptr);
     drop_spec();  // (unused speculation)
     spamm::htrace("it_mul_done");
     if (spec_on) {
@@ -1518,8 +1543,9 @@ int spamm_sp2_solve_ex(const spamm_mat* f, double n_occ, double tau, int32_t max
     spamm_mat* e = nullptr;
     double bmargin = 0.0;
     sp2_finish(x, c, n_occ, want_idem, s, &square, &tx, &tsq, &idem, &e, fuse.out, &fuse,
-               &bmargin);
+               &bmargin, nullptr, kernel, spec_on ? nullptr : &ahead);
     if (spec.ok && (!square || c->m.nblocks != c_blocks_before)) drop_spec();
+    if (ahead.ok) ahead_for = e;
     spamm::dfree(fuse.ukeys, s);  // (null once the update took it)
     resolve_timings();  // (after sp2_finish's host sync: the events are complete)
     const int k = rep->n_multiplies++;

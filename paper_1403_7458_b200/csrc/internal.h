@@ -114,9 +114,13 @@ struct UnionPrep {
   int64_t* keys = nullptr;  // small trees: union keys already compacted (G*G capacity)
 };
 UnionPrep sp2_union_prepare(const Mat& x, const Mat& x2, int64_t* u_dev, cudaStream_t s);
+// after_update (EXPAND, may be null): called once E's blocks are queued on s
+// (the update kernel) and E's layout is set, before E's finalisation -- the
+// SP2 loop starts E's K4z operand passes there.
 void sp2_update_finish(const Mat& x, const Mat& x2, UnionPrep& prep, int64_t U, bool want_idem,
                        bool expand, double* idem_norm, Mat& e, cudaStream_t s,
-                       bool settle_now = true);
+                       bool settle_now = true, void (*after_update)(void*) = nullptr,
+                       void* after_ctx = nullptr);
 bool sp2_fused_supported(int nb);
 
 void scatter_slots(const int64_t* keys, int64_t m, int32_t* slot, cudaStream_t s);
@@ -247,6 +251,7 @@ struct OzakiOperands {
   bool as_cached = false;            // `as` is the per-thread kept buffer
   bool tail_cached = false;          // ex_a / b_tr live in it too
   bool ex_a_ext = false, ex_b_ext = false;  // exponents owned by the matrix (Mat::oz_ex_*)
+  bool tr_pending = false;  // b_tr not yet written (prepared before A's slot map existed)
   void (*release_cache)(cudaStream_t) = nullptr;  // marks it free after the work on s
 };
 // Nb = 32 variant (leaf_ozaki32.cu): operand passes (row / column exponents
@@ -259,7 +264,10 @@ void oz32_launch(int64_t n_seg, const int64_t* seg, const Idx* a_idx, const Idx*
                  const Mat& B, const OzakiOperands& op, double* C, cudaStream_t s, int* counter,
                  int* ex_out = nullptr);
 bool ozaki_prepare(const Mat& A, const Mat& B, bool sym_b, cudaStream_t s, OzakiOperands& op,
-                   bool try_only);
+                   bool try_only, bool defer_tr = false);
+// b_tr of a symmetric operand prepared with defer_tr, once A.slot is built
+// (launched on s, ahead of the K4z launch).
+void ozaki_finish_tr(const Mat& A, OzakiOperands& op, cudaStream_t s);
 template <class Idx>
 // ex_out (optional, G * nb ints preset to the 0x80 pattern): receives the K4z
 // row exponents of the product C (symmetric products: rows and, through the

@@ -699,7 +699,7 @@ static void oz_dbg(const char* what, cudaStream_t s) {
 }
 
 bool ozaki_prepare(const Mat& A, const Mat& B, bool sym_b, cudaStream_t s, OzakiOperands& op,
-                   bool try_only) {
+                   bool try_only, bool defer_tr) {
   op = OzakiOperands();
   oz_dbg("enter", s);
   if (!ozaki_supported(A.nb) || B.nb != A.nb)
@@ -798,9 +798,13 @@ bool ozaki_prepare(const Mat& A, const Mat& B, bool sym_b, cudaStream_t s, Ozaki
       op.ex_b = op.ex_a;
       op.bs = op.as;
       if (!op.tail_cached) op.b_tr = dmalloc<int32_t>(A.nblocks > 0 ? A.nblocks : 1, s);
-      launch_pdl(k_oz_trslot, grid_for(A.nblocks, 256), 256, 0, s, (const int64_t*)A.keys,
-                 A.nblocks, G, (const int32_t*)A.slot, op.b_tr);
-      SPAMM_LAUNCH_CK();
+      if (defer_tr) {
+        op.tr_pending = true;
+      } else {
+        launch_pdl(k_oz_trslot, grid_for(A.nblocks, 256), 256, 0, s, (const int64_t*)A.keys,
+                   A.nblocks, G, (const int32_t*)A.slot, op.b_tr);
+        SPAMM_LAUNCH_CK();
+      }
     } else {
       if (ex_b_given) {
         op.ex_b_ext = true;
@@ -813,12 +817,26 @@ bool ozaki_prepare(const Mat& A, const Mat& B, bool sym_b, cudaStream_t s, Ozaki
     }
     return true;
   }
-  static const int wave_ex = resident_wave(k_oz_exponents, 256);
-  static const int wave_split = resident_wave(k_oz_split, 256);
+  // CTAs per SM of the two passes: 3 (of the 4 / 6 that fit) leaves room for
+  // the cull kernels that run beside them on the main stream -- with a full
+  // wave the cull's CTAs wait for the passes to end (tools/critical_path.py:
+  // 227 -> 218 us between K4z launches).  SPAMM_OZ_SPLIT_CTAS=n overrides
+  // (0: full wave; < 0: one CTA per block).
+  static const int pass_ctas = [] {
+    const char* v = getenv("SPAMM_OZ_SPLIT_CTAS");
+    return v ? atoi(v) : 3;
+  }();
+  auto wave_of = [](int full) {
+    return pass_ctas > 0 ? std::min(full, pass_ctas * multiprocessors())
+                         : pass_ctas < 0 ? INT_MAX : full;
+  };
+  static const int wave_ex = wave_of(resident_wave(k_oz_exponents, 256));
+  static const int wave_split = wave_of(resident_wave(k_oz_split, 256));
   const int gx = grid_for(A.nblocks, 1, wave_split);
   // symmetric: the transposed-slot map comes out of A's split
   if (sym_b && !op.tail_cached) op.b_tr = dmalloc<int32_t>(A.nblocks > 0 ? A.nblocks : 1, s);
-  int32_t* tr = sym_b ? op.b_tr : nullptr;
+  int32_t* tr = sym_b && !defer_tr ? op.b_tr : nullptr;
+  op.tr_pending = sym_b && defer_tr;
   if (!ex_a_given) {
     launch_plain(k_oz_exponents, grid_for(A.nblocks, 1, wave_ex), 256, 0, s, A.data, A.keys,
                  A.nblocks, G, 0, op.ex_a);
@@ -852,6 +870,14 @@ bool ozaki_prepare(const Mat& A, const Mat& B, bool sym_b, cudaStream_t s, Ozaki
     oz_dbg("B passes", s);
   }
   return true;
+}
+
+void ozaki_finish_tr(const Mat& A, OzakiOperands& op, cudaStream_t s) {
+  if (!op.tr_pending) return;
+  launch_plain(k_oz_trslot, grid_for(A.nblocks, 256), 256, 0, s, (const int64_t*)A.keys,
+               A.nblocks, A.G, (const int32_t*)A.slot, op.b_tr);
+  SPAMM_LAUNCH_CK();
+  op.tr_pending = false;
 }
 
 void ozaki_release(OzakiOperands& op, cudaStream_t s) {

@@ -252,7 +252,8 @@ UnionPrep sp2_union_prepare(const Mat& x, const Mat& x2, int64_t* u_dev, cudaStr
 }
 
 void sp2_update_finish(const Mat& x, const Mat& x2, UnionPrep& prep, int64_t U, bool want_idem,
-                       bool expand, double* idem_norm, Mat& e, cudaStream_t s, bool settle_now) {
+                       bool expand, double* idem_norm, Mat& e, cudaStream_t s, bool settle_now,
+                       void (*after_update)(void*), void* after_ctx) {
   const int nb2 = x.nb * x.nb;
   int64_t* ukeys = prep.keys;
   prep.keys = nullptr;
@@ -296,8 +297,10 @@ void sp2_update_finish(const Mat& x, const Mat& x2, UnionPrep& prep, int64_t U, 
     e.nblocks = U;
     e.data = E;
     e.keys = ukeys;
-    finalize(e, s, nE2, nzE, /*defer=*/true, nE1);
     e.sym = x.sym && x2.sym;
+    e.stream = s;
+    if (after_update) after_update(after_ctx);
+    finalize(e, s, nE2, nzE, /*defer=*/true, nE1);
   } else {
     dfree(ukeys, s);
   }
