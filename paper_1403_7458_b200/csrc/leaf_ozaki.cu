@@ -595,6 +595,12 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
             if (Cm)
 #pragma unroll
               for (int c = 0; c < 4; ++c) __stcs(Cm + (col0 + c) * OZ_NB + r, res[c]);
+          } else if (hint & 8) {  // products kept in L2 for the norm pass that follows
+            const unsigned long long pol = oz_policy_evict_last();
+            oz_st4_hint(rp, res[0], res[1], res[2], res[3], pol);
+            if (Cm)
+#pragma unroll
+              for (int c = 0; c < 4; ++c) oz_st1_hint(Cm + (col0 + c) * OZ_NB + r, res[c], pol);
           } else {
             oz_st4(rp, res[0], res[1], res[2], res[3]);
             if (Cm)

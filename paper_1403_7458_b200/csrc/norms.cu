@@ -371,16 +371,19 @@ __global__ void k_tiers_small(double* __restrict__ norms2, double* __restrict__ 
 // map, leaf tier, upper tiers (same sums as k_tier_up / k_tiers_small), the
 // trace (same order as k_trace_blocks + k_trace, Nb >= 2), the pinned host
 // mirror of the top tiers and, for X^2 in SP2, the idempotency residual root
-// and the key union with X -- one launch of three independent CTAs instead of
-// ~12 small launches:
+// and the key union with X -- one launch of four independent CTAs instead of
+// ~12 small launches (the kernel is a chain of dependent memory round trips,
+// so the jobs run side by side and each CTA issues a phase's loads together):
 //   CTA 0: slot map, leaf tier and pyramid (squared pyramid in shared
 //          memory), kept count, host mirror;
 //   CTA 1: the D = X^2 - X pyramid (X's leaf norm^2 everywhere, overwritten
 //          by the fused D chains at X^2's blocks) -> root norm;
-//   CTA 2: trace (diagonal blocks found from the keys) and the key union
-//          (X^2's blocks flagged from its keys, X's from its slot map).
+//   CTA 2: trace (diagonal blocks found from the keys);
+//   CTA 3: the key union (X^2's blocks flagged from its keys, X's from its
+//          slot map).
 // Each thread owns FS_PER positions / blocks.  Any output may be null.
 constexpr int FS_THREADS = 1024;
+constexpr int FS_BATCH = 4;  // global loads issued together per thread
 
 __device__ __forceinline__ void fs_tiers(double* p2, double* norms, double* norms2, int depth) {
   const int tid = threadIdx.x;
@@ -422,9 +425,19 @@ __global__ void __launch_bounds__(FS_THREADS)
   const int tid = threadIdx.x;
   const int64_t leaf_off = tier_offset(depth);
 
+  // (each CTA issues all its global loads of a phase before using any of
+  // them: the kernel is latency-bound, one CTA per job)
   if (blockIdx.x == 0) {
     // ---- slot map, leaf tier, pyramid, kept count, host mirror ----
-#pragma unroll 4
+    __shared__ int kept_sh;
+    if (tid == 0) kept_sh = 0;
+    int cnt = 0;
+#pragma unroll
+    for (int j = 0; j < FS_PER; ++j) {
+      const int64_t b = (int64_t)j * FS_THREADS + tid;
+      cnt += b < nblocks && kept && nz ? (int)nz[b] : 0;
+    }
+#pragma unroll
     for (int j = 0; j < FS_PER; ++j) {
       const int64_t p = (int64_t)j * FS_THREADS + tid;
       if (p < npos) {
@@ -434,29 +447,35 @@ __global__ void __launch_bounds__(FS_THREADS)
         if (slot) slot[p] = -1;
       }
     }
+    __syncthreads();  // zero fill before the scatter; kept_sh initialised
     if (kept) {
-      int c = 0;
-#pragma unroll 4
-      for (int j = 0; j < FS_PER; ++j) {
-        const int64_t b = (int64_t)j * FS_THREADS + tid;
-        c += __syncthreads_count(b < nblocks && nz ? nz[b] : 0);
+      cnt = __reduce_add_sync(0xffffffffu, cnt);
+      if ((tid & 31) == 0 && cnt) atomicAdd(&kept_sh, cnt);
+    }
+#pragma unroll
+    for (int j0 = 0; j0 < FS_PER; j0 += FS_BATCH) {
+      int64_t kk[FS_BATCH];
+      double vv[FS_BATCH], ww[FS_BATCH];
+#pragma unroll
+      for (int u = 0; u < FS_BATCH; ++u) {
+        const int64_t b = (int64_t)(j0 + u) * FS_THREADS + tid;
+        const bool in = b < nblocks;
+        kk[u] = in ? keys[b] : -1;
+        vv[u] = in ? n2[b] : 0.0;
+        ww[u] = in && n1 ? n1[b] : 0.0;
       }
-      if (tid == 0) *kept = c;
+#pragma unroll
+      for (int u = 0; u < FS_BATCH; ++u) {
+        const int64_t k = kk[u];
+        if (k < 0) continue;
+        p2[leaf_off + k] = vv[u];
+        norms2[leaf_off + k] = vv[u];
+        norms[leaf_off + k] = n1 ? ww[u] : __dsqrt_rn(vv[u]);
+        if (slot) slot[k] = (int32_t)((int64_t)(j0 + u) * FS_THREADS + tid);
+      }
     }
     __syncthreads();
-    // scatter (the zero fill above is ordered before these writes by the barrier)
-#pragma unroll 4
-    for (int j = 0; j < FS_PER; ++j) {
-      const int64_t b = (int64_t)j * FS_THREADS + tid;
-      if (b >= nblocks) continue;
-      const int64_t k = keys[b];
-      const double v = n2[b];
-      p2[leaf_off + k] = v;
-      norms2[leaf_off + k] = v;
-      norms[leaf_off + k] = n1 ? n1[b] : __dsqrt_rn(v);
-      if (slot) slot[k] = (int32_t)b;
-    }
-    __syncthreads();
+    if (kept && tid == 0) *kept = kept_sh;
     fs_tiers(p2, norms, norms2, depth);
     if (host_top) {
       for (int64_t i = tid; i < tier_offset(top_t + 1); i += FS_THREADS)
@@ -465,18 +484,36 @@ __global__ void __launch_bounds__(FS_THREADS)
   } else if (blockIdx.x == 1) {
     // ---- D = add_scaled(1, X^2, -1, X): root norm ----
     if (!idem_out) return;
-#pragma unroll 4
-    for (int j = 0; j < FS_PER; ++j) {
-      const int64_t p = (int64_t)j * FS_THREADS + tid;
-      // X-only blocks: (-x)^2 == x^2 -- only blocks this matrix stores (a
-      // multi-GPU shard carries the whole matrix's pyramid)
-      if (p < npos) p2[leaf_off + p] = (!xslot || xslot[p] >= 0) ? xleaf2[p] : 0.0;
+#pragma unroll
+    for (int j0 = 0; j0 < FS_PER; j0 += FS_BATCH) {
+      double xv[FS_BATCH];
+#pragma unroll
+      for (int u = 0; u < FS_BATCH; ++u) {
+        const int64_t p = (int64_t)(j0 + u) * FS_THREADS + tid;
+        // X-only blocks: (-x)^2 == x^2 -- only blocks this matrix stores (a
+        // multi-GPU shard carries the whole matrix's pyramid)
+        xv[u] = p < npos && (!xslot || xslot[p] >= 0) ? xleaf2[p] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < FS_BATCH; ++u) {
+        const int64_t p = (int64_t)(j0 + u) * FS_THREADS + tid;
+        if (p < npos) p2[leaf_off + p] = xv[u];
+      }
     }
     __syncthreads();
-#pragma unroll 4
-    for (int j = 0; j < FS_PER; ++j) {
-      const int64_t b = (int64_t)j * FS_THREADS + tid;
-      if (b < nblocks) p2[leaf_off + keys[b]] = dn2[b];
+#pragma unroll
+    for (int j0 = 0; j0 < FS_PER; j0 += FS_BATCH) {
+      int64_t kk[FS_BATCH];
+      double dv[FS_BATCH];
+#pragma unroll
+      for (int u = 0; u < FS_BATCH; ++u) {
+        const int64_t b = (int64_t)(j0 + u) * FS_THREADS + tid;
+        kk[u] = b < nblocks ? keys[b] : -1;
+        dv[u] = b < nblocks ? dn2[b] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < FS_BATCH; ++u)
+        if (kk[u] >= 0) p2[leaf_off + kk[u]] = dv[u];
     }
     __syncthreads();
     if (dleaf) {  // the leaf tier of ||X^2 - X||^2 (multi-GPU: all-reduced by the caller)
@@ -488,76 +525,125 @@ __global__ void __launch_bounds__(FS_THREADS)
     }
     fs_tiers(p2, nullptr, nullptr, depth);
     if (tid == 0) *idem_out = __dsqrt_rn(p2[0]);
-  } else {
-    // ---- trace and key union ----
+  } else if (blockIdx.x == 2) {
+    // ---- trace: diagonal blocks found from the keys ----
+    if (!tr_out) return;
     if (tid < 128) dslot[tid] = -1;
-    uint8_t* cflag = reinterpret_cast<uint8_t*>(p2 + (tr_out ? G * nb : 0));  // after the staging
-    if (ukeys) {
-#pragma unroll 4
-      for (int j = 0; j < FS_PER; ++j) {
-        const int64_t p = (int64_t)j * FS_THREADS + tid;
-        if (p < npos) cflag[p] = 0;
+    __syncthreads();
+#pragma unroll
+    for (int j0 = 0; j0 < FS_PER; j0 += FS_BATCH) {
+      int64_t kk[FS_BATCH];
+#pragma unroll
+      for (int u = 0; u < FS_BATCH; ++u) {
+        const int64_t b = (int64_t)(j0 + u) * FS_THREADS + tid;
+        kk[u] = b < nblocks ? keys[b] : -1;
+      }
+#pragma unroll
+      for (int u = 0; u < FS_BATCH; ++u) {
+        const int64_t k = kk[u];
+        if (k >= 0 && (k >> depth) == (k & (G - 1)))
+          dslot[k & (G - 1)] = (int32_t)((int64_t)(j0 + u) * FS_THREADS + tid);
       }
     }
     __syncthreads();
+    // stage the diagonals of the G diagonal blocks, then one thread per
+    // block sums its diagonal in order, thread 0 the blocks in order
+    double* dg = p2;
+    const int64_t nb2 = (int64_t)nb * nb, nd = G * nb;
+    constexpr int DQ = 4;  // loads in flight per thread
+    for (int64_t q0 = tid; q0 < nd; q0 += (int64_t)DQ * FS_THREADS) {
+      double v[DQ];
+#pragma unroll
+      for (int u = 0; u < DQ; ++u) {
+        const int64_t q = q0 + (int64_t)u * FS_THREADS;
+        const int64_t b = q / nb, d = q % nb;
+        const int32_t sl = q < nd ? dslot[b] : -1;
+        v[u] = sl >= 0 ? data[(int64_t)sl * nb2 + d * nb + d] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < DQ; ++u) {
+        const int64_t q = q0 + (int64_t)u * FS_THREADS;
+        if (q < nd) dg[q] = v[u];
+      }
+    }
+    __syncthreads();
+    // (sequential sums; the operands are read 16 at a time ahead of the adds)
+    if (tid < G && dslot[tid] >= 0) {
+      const double* x = dg + (int64_t)tid * nb;
+      double acc = 0.0;
+      for (int d0 = 0; d0 < nb; d0 += 16) {
+        double v[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) v[u] = d0 + u < nb ? x[d0 + u] : 0.0;
+#pragma unroll
+        for (int u = 0; u < 16; ++u)
+          if (d0 + u < nb) acc = __dadd_rn(acc, v[u]);
+      }
+      part[tid] = acc;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      double tot = 0.0;
+      for (int64_t b0 = 0; b0 < G; b0 += 16) {
+        double v[16];
+        bool in[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+          in[u] = b0 + u < G && dslot[b0 + u] >= 0;
+          v[u] = in[u] ? part[b0 + u] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 16; ++u)
+          if (in[u]) tot = __dadd_rn(tot, v[u]);
+      }
+      *tr_out = tot;
+    }
+  } else {
+    // ---- key union of X and X^2 in Morton order ----
+    if (!ukeys) return;
+    uint8_t* cflag = reinterpret_cast<uint8_t*>(p2);
 #pragma unroll 4
     for (int j = 0; j < FS_PER; ++j) {
-      const int64_t b = (int64_t)j * FS_THREADS + tid;
-      if (b >= nblocks) continue;
-      const int64_t k = keys[b];
-      const uint32_t bi = (uint32_t)(k >> depth), bj = (uint32_t)(k & (G - 1));
-      if (bi == bj) dslot[bi] = (int32_t)b;
-      if (ukeys) cflag[morton_encode(bi, bj)] = 1;
+      const int64_t p = (int64_t)j * FS_THREADS + tid;
+      if (p < npos) cflag[p] = 0;
     }
     __syncthreads();
-    if (tr_out) {
-      // stage the diagonals of the G diagonal blocks, then one thread per
-      // block sums its diagonal in order, thread 0 the blocks in order
-      double* dg = p2;
-      const int64_t nb2 = (int64_t)nb * nb, nd = G * nb;
-      for (int64_t q = tid; q < nd; q += FS_THREADS) {
-        const int64_t b = q / nb, d = q % nb;
-        const int32_t sl = dslot[b];
-        dg[q] = sl >= 0 ? data[(int64_t)sl * nb2 + d * nb + d] : 0.0;
+#pragma unroll
+    for (int j0 = 0; j0 < FS_PER; j0 += FS_BATCH) {
+      int64_t kk[FS_BATCH];
+#pragma unroll
+      for (int u = 0; u < FS_BATCH; ++u) {
+        const int64_t b = (int64_t)(j0 + u) * FS_THREADS + tid;
+        kk[u] = b < nblocks ? keys[b] : -1;
       }
-      __syncthreads();
-      if (tid < G && dslot[tid] >= 0) {
-        const double* x = dg + (int64_t)tid * nb;
-        double acc = 0.0;
-        for (int d = 0; d < nb; ++d) acc = __dadd_rn(acc, x[d]);
-        part[tid] = acc;
-      }
-      __syncthreads();
-      if (tid == 0) {
-        double tot = 0.0;
-        for (int64_t b = 0; b < G; ++b)
-          if (dslot[b] >= 0) tot = __dadd_rn(tot, part[b]);
-        *tr_out = tot;
+#pragma unroll
+      for (int u = 0; u < FS_BATCH; ++u) {
+        const int64_t k = kk[u];
+        if (k >= 0) cflag[morton_encode((uint32_t)(k >> depth), (uint32_t)(k & (G - 1)))] = 1;
       }
     }
-    if (ukeys) {
-      // key union of X and X^2 in Morton order (FS_PER consecutive positions
-      // per thread: count, scan, write)
-      int fs = 0;
-#pragma unroll 4
-      for (int j = 0; j < FS_PER; ++j) {
-        const int64_t p = (int64_t)tid * FS_PER + j;
-        uint32_t bi, bj;
-        morton_decode((uint64_t)p, bi, bj);
-        fs += p < npos && (cflag[p] || xslot[(int64_t)bi * G + bj] >= 0) ? 1 : 0;
-      }
-      int64_t tot = 0;
-      int64_t o = cta_exclusive_scan(fs, &tot);
-#pragma unroll 4
-      for (int j = 0; j < FS_PER; ++j) {
-        const int64_t p = (int64_t)tid * FS_PER + j;
-        uint32_t bi, bj;
-        morton_decode((uint64_t)p, bi, bj);
-        const int64_t key = (int64_t)bi * G + bj;
-        if (p < npos && (cflag[p] || xslot[key] >= 0)) ukeys[o++] = key;
-      }
-      if (tid == 0) *ucount = tot;
+    __syncthreads();
+    // FS_PER consecutive positions per thread: count, scan, write
+    int fs = 0;
+    bool in_u[FS_PER];
+#pragma unroll
+    for (int j = 0; j < FS_PER; ++j) {
+      const int64_t p = (int64_t)tid * FS_PER + j;
+      uint32_t bi, bj;
+      morton_decode((uint64_t)p, bi, bj);
+      in_u[j] = p < npos && (xslot[(int64_t)bi * G + bj] >= 0 || cflag[p]);
+      fs += in_u[j] ? 1 : 0;
     }
+    int64_t tot = 0;
+    int64_t o = cta_exclusive_scan(fs, &tot);
+#pragma unroll
+    for (int j = 0; j < FS_PER; ++j) {
+      const int64_t p = (int64_t)tid * FS_PER + j;
+      uint32_t bi, bj;
+      morton_decode((uint64_t)p, bi, bj);
+      if (in_u[j]) ukeys[o++] = (int64_t)bi * G + bj;
+    }
+    if (tid == 0) *ucount = tot;
   }
 }
 
@@ -569,14 +655,14 @@ void launch_finalize_small(int depth, int nb, cudaStream_t s, Args... args) {
                                (size_t)(G * nb) * sizeof(double) + (size_t)(G * G) + 64);
   if (smem > 220 * 1024) throw CudaError("finalize: shared memory budget exceeded");
   if (depth <= 6 && smem <= 48 * 1024) {
-    launch_pdl(k_finalize_small<4>, 3, FS_THREADS, smem, s, args...);
+    launch_pdl(k_finalize_small<4>, 4, FS_THREADS, smem, s, args...);
   } else {
     static std::once_flag once;
     std::call_once(once, [] {
       SPAMM_CK(cudaFuncSetAttribute(k_finalize_small<16>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     });
-    launch_pdl(k_finalize_small<16>, 3, FS_THREADS, smem, s, args...);
+    launch_pdl(k_finalize_small<16>, 4, FS_THREADS, smem, s, args...);
   }
   SPAMM_LAUNCH_CK();
 }

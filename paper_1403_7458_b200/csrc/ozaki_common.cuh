@@ -47,6 +47,20 @@ __device__ __forceinline__ void oz_st4(double* p, double a, double b, double c, 
   asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d)
                : "memory");
 }
+__device__ __forceinline__ unsigned long long oz_policy_evict_last() {
+  unsigned long long pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void oz_st4_hint(double* p, double a, double b, double c, double d,
+                                            unsigned long long pol) {
+  asm volatile("st.global.L2::cache_hint.v4.f64 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p), "d"(a),
+               "d"(b), "d"(c), "d"(d), "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ void oz_st1_hint(double* p, double a, unsigned long long pol) {
+  asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(a), "l"(pol) : "memory");
+}
 __device__ __forceinline__ void oz_st4_cs(double* p, double a, double b, double c, double d) {
   asm volatile("st.global.cs.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(a), "d"(b), "d"(c),
                "d"(d)
