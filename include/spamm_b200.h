@@ -42,7 +42,8 @@ extern "C" {
  * scale per global row of A / column of B, digit pairs p + q <= 7 formed
  * exactly in int32); Nb = 32 or 64; relative error below FP64's (~5e-17 vs
  * ~5e-16 rel-Fro), deterministic, exactly symmetric, not bitwise DMMA.
- * Operands with non-finite entries are refused (AUTO falls back to DMMA).
+ * C elements in a row / column holding Inf or NaN are recomputed in FP64 in
+ * the reference's order (bitwise the reference's Inf / NaN pattern).
  * Accepted by the matrix entry points (spamm_multiply*, spamm_sp2_*), not by
  * spamm_gemm_batch (it needs the operands' row / column exponents). */
 #define SPAMM_LEAF_OZAKI 4

@@ -15,9 +15,10 @@ runs in ``libspamm_b200``:
 ``mode``/``workers``/``deterministic`` are accepted for drop-in compatibility;
 the GPU schedule is deterministic for every setting (one CTA owns one C block
 and reduces its k-ascending segment in registers).  Extra keyword
-``kernel``: "auto" (K4z for Nb in {32, 64} when the operands are finite and
-the digit slices fit, DMMA for Nb in {8, 16} and as the fallback), "ozaki"
-(force K4z; ``ValueError`` on non-finite operands), "dmma", or "exact"
+``kernel``: "auto" (K4z for Nb in {32, 64} when the digit slices fit, DMMA
+for Nb in {8, 16} and as the fallback), "ozaki" (force K4z; C elements in a
+row / column holding Inf or NaN are recomputed in FP64 in the reference's
+order), "dmma", or "exact"
 (CUDA-core, the reference's exact rounding order: bitwise-identical C).
 """
 
