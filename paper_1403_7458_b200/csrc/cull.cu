@@ -305,35 +305,34 @@ bool host_cull_top(const double* nA, const double* nB, int T0, int depth, double
 constexpr int DENSE_MAX_DEPTH = 8;
 bool g_dense_enabled = true;
 
+// The ancestor chain of a triple is evaluated without early exit: the 2 (t+1)
+// norm loads are independent (one L1 round trip instead of t + 1 dependent
+// ones), and the AND of the same IEEE predicates is the same decision.
 __device__ __forceinline__ bool keep_chain(const double* __restrict__ nA,
                                            const double* __restrict__ nB, double tau, int t,
                                            int64_t i, int64_t k, int64_t j) {
-  // tiers t, t-1, ..., 0 (most selective first)
+  bool ok = true;
   for (int u = t; u >= 0; --u) {
     const int sh = t - u;
     const int64_t W = int64_t(1) << u;
     const int64_t off = tier_offset(u);
-    if (!keep_pair(nA[off + (i >> sh) * W + (k >> sh)], nB[off + (k >> sh) * W + (j >> sh)], tau))
-      return false;
+    ok &= keep_pair(nA[off + (i >> sh) * W + (k >> sh)], nB[off + (k >> sh) * W + (j >> sh)], tau);
   }
-  return true;
+  return ok;
 }
 
-// Survivor counts of every tier t < depth (full enumeration, 8^t triples).
-// Counts are warp-reduced per tier before touching shared memory (a shared
-// 64-bit atomic per survivor serialised this kernel to ~15 us at cfg4).
 // every tier u < t of the triple's ancestor chain passes (the triple is tested)
 __device__ __forceinline__ bool ancestors_pass(const double* __restrict__ nA,
                                                const double* __restrict__ nB, double tau, int t,
                                                int64_t i, int64_t k, int64_t j) {
+  bool ok = true;
   for (int u = t - 1; u >= 0; --u) {
     const int sh = t - u;
     const int64_t W = int64_t(1) << u;
     const int64_t off = tier_offset(u);
-    if (!keep_pair(nA[off + (i >> sh) * W + (k >> sh)], nB[off + (k >> sh) * W + (j >> sh)], tau))
-      return false;
+    ok &= keep_pair(nA[off + (i >> sh) * W + (k >> sh)], nB[off + (k >> sh) * W + (j >> sh)], tau);
   }
-  return true;
+  return ok;
 }
 // tie probe of the tier-t triple (i, k, j) if it is tested (see tie_probe)
 __device__ __forceinline__ void chain_tie_probe(const double* __restrict__ nA,
@@ -347,149 +346,351 @@ __device__ __forceinline__ void chain_tie_probe(const double* __restrict__ nA,
   if (ancestors_pass(nA, nB, tb.tau, t, i, k, j)) tie_probe(p, tb, near, margin);
 }
 
-__global__ void __launch_bounds__(256)
-    k_dense_tiers(const double* __restrict__ nA, const double* __restrict__ nB, double tau,
-                  int depth, unsigned long long* __restrict__ counts, TieBand tb,
-                  unsigned long long* __restrict__ near, unsigned long long* __restrict__ margin) {
-  pdl_wait();
-  __shared__ unsigned int sc[DENSE_MAX_DEPTH];
-  if (threadIdx.x < DENSE_MAX_DEPTH) sc[threadIdx.x] = 0;
-  __syncthreads();
-  const int lane = threadIdx.x & 31;
-  const int64_t total = ((int64_t(1) << (3 * depth)) - 1) / 7;
-  // warp-uniform trip count so the per-tier reductions see full warps
-  for (int64_t q0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) & ~int64_t(31); q0 < total;
-       q0 += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t q = q0 + lane;
-    int t = -1;
-    if (q < total) {
-      t = 0;
-      while ((((int64_t(1) << (3 * (t + 1))) - 1) / 7) <= q) ++t;
-      const int64_t r = q - ((int64_t(1) << (3 * t)) - 1) / 7;
-      const int64_t i = r >> (2 * t), k = (r >> t) & ((int64_t(1) << t) - 1),
-                    j = r & ((int64_t(1) << t) - 1);
-      chain_tie_probe(nA, nB, tb, t, i, k, j, near + t, margin);
-      if (!keep_chain(nA, nB, tau, t, i, k, j)) t = -1;
-    }
-    for (int u = 0; u < depth; ++u) {
-      const unsigned v = __reduce_add_sync(0xffffffffu, t == u ? 1u : 0u);
-      if (lane == 0 && v) atomicAdd(sc + u, v);
-    }
-  }
-  __syncthreads();
-  if (threadIdx.x < depth && sc[threadIdx.x]) atomicAdd(counts + threadIdx.x, (unsigned long long)sc[threadIdx.x]);
-}
-
 // Leaf tier, one warp per C position m (Morton order).  Each m gets one
 // packed int64 so a single scan yields every offset the layout needs:
 //   bits  0..26  tasks of the node if it is emitted (symmetric: i <= j only)
 //   bits 27..44  1 if the node is emitted with >= 1 task  -> node index
 //   bits 45..62  1 if C block (i,j) exists at all         -> storage slot
-// (G <= 256: tasks <= 2^24, nodes <= 2^16.)  WRITE=false: counts, the LPT
-// length histogram and the symmetric mirror check.  WRITE=true: the task
-// lists, C keys, storage/mirror slots and the LPT order of the nodes.
+// (G <= 256: tasks <= 2^24, nodes <= 2^16.)
 constexpr int DT_NODE = 27, DT_FULL = 45;
 constexpr int64_t DT_TASK_MASK = (int64_t(1) << DT_NODE) - 1;
 constexpr int64_t DT_IDX_MASK = (int64_t(1) << (DT_FULL - DT_NODE)) - 1;
 
-template <bool WRITE>
-__global__ void __launch_bounds__(CULL_THREADS)
-    k_dense_leaf(int depth, const double* __restrict__ nA, const double* __restrict__ nB,
-                 double tau, int sym, int64_t* __restrict__ cnt, const int64_t* __restrict__ off,
-                 int* __restrict__ hist, int32_t* __restrict__ ci_o, int32_t* __restrict__ cj_o,
-                 int64_t* __restrict__ seg_o, int32_t* __restrict__ K_o,
-                 const int32_t* __restrict__ slotA, const int32_t* __restrict__ slotB,
-                 int32_t* __restrict__ aidx, int32_t* __restrict__ bidx,
-                 int64_t* __restrict__ keys, int64_t* __restrict__ c_out,
-                 int64_t* __restrict__ c_mirror, int32_t* __restrict__ order, int64_t Mn,
-                 int64_t Vn, unsigned long long* __restrict__ aux, TieBand tb,
-                 unsigned long long* __restrict__ near, unsigned long long* __restrict__ margin,
-                 int64_t lo, int64_t hi, int32_t* __restrict__ work) {
+// Block-wide (CULL_THREADS) exclusive scan of one int64 per thread; returns
+// the block total.
+__device__ __forceinline__ int64_t cull_block_scan(int64_t v, int64_t& excl, int64_t* wsum) {
+  constexpr int NW = CULL_THREADS / 32;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int64_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int64_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) wsum[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    const int64_t w = lane < NW ? wsum[lane] : 0;
+    int64_t z = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t y = __shfl_up_sync(0xffffffffu, z, o);
+      if (lane >= o) z += y;
+    }
+    if (lane < NW) wsum[lane] = z - w;
+    if (lane == NW - 1) wsum[NW] = z;
+  }
+  __syncthreads();
+  excl = wsum[warp] + x - v;
+  const int64_t total = wsum[NW];
+  __syncthreads();
+  return total;
+}
+
+// Count pass of the dense cull, one launch:
+//  * CTAs [n_tier, grid): the leaf tier, one warp per C position -- per node the
+//    packed count (cnt), the keep masks of its k-range (kmask, 32 k per word:
+//    the write pass compacts from them without re-testing), the LPT length
+//    histogram, the symmetric mirror check and the near-tau probes;
+//  * CTAs [0, n_tier): survivor counts and near-tau probes of every upper
+//    tier t < depth (full enumeration, 8^t triples; warp-reduced counts) --
+//    first in the grid, so they are in the first wave;
+//  * the last CTA to finish scans cnt into off (one pass over npos packed
+//    values), scans the histogram in place, and publishes the scalars the
+//    host needs to pinned memory (gather_sync's protocol) -- so the cull has
+//    one launch before its host sync instead of five.
+__global__ void __launch_bounds__(CULL_THREADS, 4)
+    k_dense_count(int depth, const double* __restrict__ nA, const double* __restrict__ nB,
+                  double tau, int sym, int64_t* __restrict__ cnt, uint32_t* __restrict__ kmask,
+                  int* __restrict__ hist, int want_tasks, unsigned long long* __restrict__ aux,
+                  TieBand tb, unsigned long long* __restrict__ near_tiers,
+                  unsigned long long* __restrict__ margin, int64_t lo, int64_t hi,
+                  int32_t* __restrict__ work, int n_tier, int tiers, unsigned* __restrict__ done,
+                  int64_t* __restrict__ off, ScalarSrc src, int n_src, int64_t* gvals,
+                  int64_t* gflag, int64_t seq) {
   pdl_wait();
-  const int64_t G = int64_t(1) << depth;
-  // Shard ownership (hi >= 0): the C positions whose Morton index lies in
-  // [lo, hi) -- on the symmetric path the upper positions in range plus their
-  // mirrors (a rank computes an upper block and writes its transpose).
-  auto in_range = [&](int64_t q) { return hi < 0 || (q >= lo && q < hi); };
+  __shared__ int64_t wsum[CULL_THREADS / 32 + 1];
+  __shared__ unsigned long long cta_full;
+  __shared__ unsigned int sc[DENSE_MAX_DEPTH];
+  __shared__ bool last;
+  const int64_t G = int64_t(1) << depth, npos = G * G;
+  const int KW = (int)((G + 31) >> 5);
+  const int lane = threadIdx.x & 31;
+  if ((int)blockIdx.x >= n_tier) {
+    const int n_leaf = (int)gridDim.x - n_tier;
+    auto in_range = [&](int64_t q) { return hi < 0 || (q >= lo && q < hi); };
+    unsigned long long* near = near_tiers + depth;
+    if (threadIdx.x == 0) cta_full = 0;
+    if (threadIdx.x == 0) sc[0] = 0;
+    __syncthreads();
+    unsigned long long full = 0;
+    // one C position m: counts, keep masks, histogram, mirror check, probes.
+    // keep(k) / keep_m(k): the leaf triple (i,k,j) / its mirror (j,k,i).
+    auto finish_pos = [&](int64_t m, bool emitted, int64_t c) {
+      if (lane == 0) {
+        cnt[m] = (emitted ? c + (c > 0 ? int64_t(1) << DT_NODE : 0) : 0) +
+                 (c > 0 ? int64_t(1) << DT_FULL : 0);
+        if (work && emitted && c) work[m] = (int32_t)c;  // persistence load balancing input
+        full += c;
+        if (want_tasks && c && emitted) atomicAdd(hist + (G - c), 1);
+      }
+    };
+    if (depth >= 2) {
+      // A CTA takes 8 consecutive Morton positions = the children of two
+      // tier-(depth-1) nodes.  The ancestor chains of all their leaf triples
+      // are those parents' chains over K = k/2: four warps evaluate them once
+      // (the two parents and, symmetric, their mirrors) into bit masks, and
+      // every leaf test is one product plus a mask bit -- the same predicates
+      // as keep_chain.  The parents' tested triples are exactly tier depth-1,
+      // so its survivor count and near-tau probes are taken here too.
+      __shared__ uint32_t pk[4][4];  // [own 0, own 1, mirror 0, mirror 1][K / 32], G/2 <= 128
+      const int warp = threadIdx.x >> 5;
+      const int64_t GH = G >> 1;
+      const int PW = (int)((GH + 31) >> 5);
+      const int64_t leaf_off = tier_offset(depth);
+      const int64_t ngroups = npos >> 3;
+      for (int64_t grp = blockIdx.x - n_tier; grp < ngroups; grp += n_leaf) {
+        if (warp < 4 && (warp < 2 || sym)) {
+          uint32_t I, J;
+          morton_decode((uint64_t)(grp * 2 + (warp & 1)), I, J);
+          if (warp >= 2) {
+            const uint32_t t_ = I;
+            I = J;
+            J = t_;
+          }
+          unsigned pc = 0;
+          for (int kw = 0; kw < PW; ++kw) {
+            const int64_t K = (int64_t)kw * 32 + lane;
+            const bool valid = K < GH;
+            const bool keep = valid && keep_chain(nA, nB, tau, depth - 1, I, K, J);
+            const unsigned bits = __ballot_sync(0xffffffffu, keep);
+            if (lane == 0) pk[warp][kw] = bits;
+            if (warp < 2 && tiers) {
+              if (valid)
+                chain_tie_probe(nA, nB, tb, depth - 1, I, K, J, near_tiers + depth - 1, margin);
+              pc += __popc(bits);
+            }
+          }
+          if (warp < 2 && tiers && lane == 0 && pc) atomicAdd(sc, pc);
+        }
+        __syncthreads();
+        {
+          const int64_t m = grp * 8 + warp;
+          uint32_t ui, uj;
+          morton_decode((uint64_t)m, ui, uj);
+          const int64_t i = ui, j = uj;
+          const bool owned = sym && i > j ? in_range((int64_t)morton_encode(uj, ui)) : in_range(m);
+          const bool emitted = owned && (!sym || i <= j);
+          if (!owned) {
+            if (lane == 0) cnt[m] = 0;
+          } else {
+            const uint32_t* pkm = pk[warp >> 2];
+            const uint32_t* pkx = pk[2 + (warp >> 2)];
+            const bool mirror = sym && i < j;
+            int64_t c = 0;
+            for (int64_t k0 = 0; k0 < G; k0 += 32) {
+              const int64_t k = k0 + lane;
+              const bool valid = k < G;
+              const bool par = valid && ((pkm[k >> 6] >> ((k >> 1) & 31)) & 1u);
+              const double pr =
+                  valid ? __dmul_rn(nA[leaf_off + i * G + k], nB[leaf_off + k * G + j]) : 0.0;
+              const bool keep = par && pr > tau;
+              const unsigned mask = __ballot_sync(0xffffffffu, keep);
+              if (valid && emitted && par && fabs(pr - tb.tau) <= tb.wide)
+                tie_probe(pr, tb, near, margin);
+              if (mirror) {
+                const bool parm = valid && ((pkx[k >> 6] >> ((k >> 1) & 31)) & 1u);
+                const double pm =
+                    valid ? __dmul_rn(nA[leaf_off + j * G + k], nB[leaf_off + k * G + i]) : 0.0;
+                const bool keep_m = parm && pm > tau;
+                if (valid && emitted && parm && fabs(pm - tb.tau) <= tb.wide)
+                  tie_probe(pm, tb, near, margin);
+                if (__any_sync(0xffffffffu, keep != keep_m) && lane == 0) atomicOr(aux + 1, 1ull);
+              }
+              if (want_tasks && emitted && lane == 0) kmask[m * KW + (k0 >> 5)] = mask;
+              c += __popc(mask);
+            }
+            finish_pos(m, emitted, c);
+          }
+        }
+        __syncthreads();  // pk is rewritten by the next group
+      }
+    } else {
+      const int64_t gw = ((int64_t)(blockIdx.x - n_tier) * blockDim.x + threadIdx.x) >> 5;
+      const int64_t nw = ((int64_t)n_leaf * blockDim.x) >> 5;
+      for (int64_t m = gw; m < npos; m += nw) {
+        uint32_t ui, uj;
+        morton_decode((uint64_t)m, ui, uj);
+        const int64_t i = ui, j = uj;
+        const bool owned = sym && i > j ? in_range((int64_t)morton_encode(uj, ui)) : in_range(m);
+        const bool emitted = owned && (!sym || i <= j);
+        if (!owned) {
+          if (lane == 0) cnt[m] = 0;
+          continue;
+        }
+        int64_t c = 0;
+        for (int64_t k0 = 0; k0 < G; k0 += 32) {
+          const int64_t k = k0 + lane;
+          const bool valid = k < G;
+          const bool keep = valid && keep_chain(nA, nB, tau, depth, i, k, j);
+          const unsigned mask = __ballot_sync(0xffffffffu, keep);
+          if (valid && emitted) {
+            chain_tie_probe(nA, nB, tb, depth, i, k, j, near, margin);
+            if (sym && i < j) chain_tie_probe(nA, nB, tb, depth, j, k, i, near, margin);
+          }
+          if (sym && i < j) {
+            const bool keep_m = valid && keep_chain(nA, nB, tau, depth, j, k, i);
+            if (__any_sync(0xffffffffu, keep != keep_m) && lane == 0) atomicOr(aux + 1, 1ull);
+          }
+          if (want_tasks && emitted && lane == 0) kmask[m * KW + (k0 >> 5)] = mask;
+          c += __popc(mask);
+        }
+        finish_pos(m, emitted, c);
+      }
+    }
+    // full (reference) leaf count: one global atomic per CTA
+    if (lane == 0 && full) atomicAdd(&cta_full, full);
+    __syncthreads();
+    if (threadIdx.x == 0 && cta_full) atomicAdd(aux, cta_full);
+    if (threadIdx.x == 0 && depth >= 2 && sc[0])
+      atomicAdd(aux + 4 + depth - 1, (unsigned long long)sc[0]);
+  } else {
+    if (threadIdx.x < DENSE_MAX_DEPTH) sc[threadIdx.x] = 0;
+    __syncthreads();
+    // tiers 0 .. depth-2 here (tier depth-1 is counted by the leaf CTAs)
+    const int64_t total = depth >= 2 ? ((int64_t(1) << (3 * (depth - 1))) - 1) / 7
+                                     : ((int64_t(1) << (3 * depth)) - 1) / 7;
+    const int64_t tb0 = (int64_t)blockIdx.x * blockDim.x;
+    const int64_t tstride = (int64_t)n_tier * blockDim.x;
+    // warp-uniform trip count so the per-tier reductions see full warps
+    for (int64_t q0 = (tb0 + threadIdx.x) & ~int64_t(31); q0 < total; q0 += tstride) {
+      const int64_t q = q0 + lane;
+      int t = -1;
+      if (q < total) {
+        t = 0;
+        while ((((int64_t(1) << (3 * (t + 1))) - 1) / 7) <= q) ++t;
+        const int64_t r = q - ((int64_t(1) << (3 * t)) - 1) / 7;
+        const int64_t i = r >> (2 * t), k = (r >> t) & ((int64_t(1) << t) - 1),
+                      j = r & ((int64_t(1) << t) - 1);
+        chain_tie_probe(nA, nB, tb, t, i, k, j, near_tiers + t, margin);
+        if (!keep_chain(nA, nB, tau, t, i, k, j)) t = -1;
+      }
+      for (int u = 0; u < depth; ++u) {
+        const unsigned v = __reduce_add_sync(0xffffffffu, t == u ? 1u : 0u);
+        if (lane == 0 && v) atomicAdd(sc + u, v);
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x < depth && sc[threadIdx.x])
+      atomicAdd(aux + 4 + threadIdx.x, (unsigned long long)sc[threadIdx.x]);
+  }
+  // ---- last CTA: scans and the host-visible scalars
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(done, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  constexpr int ITEMS = 16, TILE = CULL_THREADS * ITEMS;
+  int64_t carry = 0;
+  for (int64_t base = 0; base < npos; base += TILE) {
+    const int64_t b0 = base + (int64_t)threadIdx.x * ITEMS;
+    int64_t v[ITEMS];
+    int64_t sum = 0;
+#pragma unroll
+    for (int r = 0; r < ITEMS; ++r) {
+      v[r] = b0 + r < npos ? __ldcg(cnt + b0 + r) : 0;
+      sum += v[r];
+    }
+    int64_t excl;
+    const int64_t tot = cull_block_scan(sum, excl, wsum);
+    int64_t run = carry + excl;
+#pragma unroll
+    for (int r = 0; r < ITEMS; ++r) {
+      if (b0 + r < npos) off[b0 + r] = run;
+      run += v[r];
+    }
+    carry += tot;
+  }
+  if (threadIdx.x == 0) off[npos] = carry;
+  if (want_tasks) {  // LPT length histogram (G + 1 bins <= 257), in place
+    const int nbins = (int)G + 1;
+    const int per = (nbins + CULL_THREADS - 1) / CULL_THREADS;
+    const int h0 = threadIdx.x * per;
+    int64_t loc = 0;
+    for (int b = h0; b < h0 + per && b < nbins; ++b) loc += __ldcg(hist + b);
+    int64_t excl;
+    cull_block_scan(loc, excl, wsum);
+    for (int b = h0; b < h0 + per && b < nbins; ++b) {
+      const int x = __ldcg(hist + b);
+      hist[b] = (int)excl;
+      excl += x;
+    }
+  }
+  __threadfence();
+  __syncthreads();
+  if ((int)threadIdx.x < n_src) gvals[threadIdx.x] = src.p[threadIdx.x] ? __ldcg(src.p[threadIdx.x]) : 0;
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) *reinterpret_cast<volatile int64_t*>(gflag) = seq;
+}
+
+// Write pass: the task lists, C keys, storage / mirror slots and the LPT
+// order of the nodes, compacted from the count pass's keep masks (no norm is
+// read again).  One warp per C position.
+__global__ void __launch_bounds__(CULL_THREADS)
+    k_dense_write(int depth, int sym, const int64_t* __restrict__ off,
+                  const uint32_t* __restrict__ kmask, int* __restrict__ hist,
+                  int32_t* __restrict__ ci_o, int32_t* __restrict__ cj_o,
+                  int64_t* __restrict__ seg_o, int32_t* __restrict__ K_o,
+                  const int32_t* __restrict__ slotA, const int32_t* __restrict__ slotB,
+                  int32_t* __restrict__ aidx, int32_t* __restrict__ bidx,
+                  int64_t* __restrict__ keys, int64_t* __restrict__ c_out,
+                  int64_t* __restrict__ c_mirror, int32_t* __restrict__ order, int64_t Mn,
+                  int64_t Vn) {
+  pdl_wait();
+  const int64_t G = int64_t(1) << depth, npos = G * G;
+  const int KW = (int)((G + 31) >> 5);
   const int lane = threadIdx.x & 31;
   const unsigned lt_mask = (1u << lane) - 1u;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  if (WRITE && gw == 0 && lane == 0) seg_o[Mn] = Vn;
-  unsigned long long full = 0;
-  for (int64_t m = gw; m < G * G; m += nw) {
+  if (gw == 0 && lane == 0) seg_o[Mn] = Vn;
+  for (int64_t m = gw; m < npos; m += nw) {
+    const int64_t v = off[m], d = off[m + 1] - v;
+    if ((d >> DT_FULL) == 0) continue;  // no C block here (or not owned)
     uint32_t ui, uj;
     morton_decode((uint64_t)m, ui, uj);
     const int64_t i = ui, j = uj;
-    const bool owned = sym && i > j ? in_range((int64_t)morton_encode(uj, ui)) : in_range(m);
-    const bool emitted = owned && (!sym || i <= j);
-    if (!owned) {
-      if (!WRITE && lane == 0) cnt[m] = 0;
-      continue;
-    }
-    int64_t toff = 0;
-    if (WRITE) {
-      const int64_t v = off[m], d = off[m + 1] - v;
-      if ((d >> DT_FULL) == 0) continue;  // no C block here
-      const int64_t pfull = v >> DT_FULL;
-      const int64_t ntask = d & DT_TASK_MASK;
-      if (lane == 0) keys[pfull] = i * G + j;
-      if (!emitted) continue;  // mirror of an emitted node
-      const int64_t node = (v >> DT_NODE) & DT_IDX_MASK;
-      toff = v & DT_TASK_MASK;
-      if (lane == 0) {
-        ci_o[node] = (int32_t)i;
-        cj_o[node] = (int32_t)j;
-        seg_o[node] = toff;
-        if (c_out) {
-          c_out[node] = pfull;
-          c_mirror[node] =
-              i < j ? off[(int64_t)morton_encode((uint32_t)j, (uint32_t)i)] >> DT_FULL : -1;
-        }
-        order[atomicAdd(hist + (G - ntask), 1)] = (int32_t)node;
+    const int64_t pfull = v >> DT_FULL;
+    if (lane == 0) keys[pfull] = i * G + j;
+    if ((d & DT_TASK_MASK) == 0) continue;  // mirror of an emitted node
+    const int64_t ntask = d & DT_TASK_MASK;
+    const int64_t node = (v >> DT_NODE) & DT_IDX_MASK;
+    int64_t toff = v & DT_TASK_MASK;
+    if (lane == 0) {
+      ci_o[node] = (int32_t)i;
+      cj_o[node] = (int32_t)j;
+      seg_o[node] = toff;
+      if (c_out) {
+        c_out[node] = pfull;
+        c_mirror[node] =
+            i < j ? off[(int64_t)morton_encode((uint32_t)j, (uint32_t)i)] >> DT_FULL : -1;
       }
+      order[atomicAdd(hist + (G - ntask), 1)] = (int32_t)node;
     }
-    int64_t c = 0;
-    for (int64_t k0 = 0; k0 < G; k0 += 32) {
-      const int64_t k = k0 + lane;
-      const bool valid = k < G;
-      const bool keep = valid && keep_chain(nA, nB, tau, depth, i, k, j);
-      const unsigned mask = __ballot_sync(0xffffffffu, keep);
-      if (!WRITE && valid && emitted) {
-        chain_tie_probe(nA, nB, tb, depth, i, k, j, near, margin);
-        if (sym && i < j) chain_tie_probe(nA, nB, tb, depth, j, k, i, near, margin);
+    const uint32_t* mk = kmask + m * KW;
+    for (int w = 0; w < KW; ++w) {
+      const unsigned mask = mk[w];
+      if (mask >> lane & 1u) {
+        const int64_t k = (int64_t)w * 32 + lane;
+        const int64_t pos = toff + __popc(mask & lt_mask);
+        K_o[pos] = (int32_t)k;
+        aidx[pos] = slotA[i * G + k];
+        bidx[pos] = slotB[k * G + j];
       }
-      if (!WRITE && sym && i < j) {
-        const bool keep_m = valid && keep_chain(nA, nB, tau, depth, j, k, i);
-        if (__any_sync(0xffffffffu, keep != keep_m) && lane == 0) atomicOr(aux + 1, 1ull);
-      }
-      if (WRITE) {
-        if (keep) {
-          const int64_t pos = toff + __popc(mask & lt_mask);
-          K_o[pos] = (int32_t)k;
-          aidx[pos] = slotA[i * G + k];
-          bidx[pos] = slotB[k * G + j];
-        }
-        toff += __popc(mask);
-      } else {
-        c += __popc(mask);
-      }
+      toff += __popc(mask);
     }
-    if (!WRITE && lane == 0) {
-      cnt[m] = (emitted ? c + (c > 0 ? int64_t(1) << DT_NODE : 0) : 0) +
-               (c > 0 ? int64_t(1) << DT_FULL : 0);
-      if (work && emitted && c) work[m] = (int32_t)c;  // persistence load balancing input
-      full += c;
-      if (c && emitted) atomicAdd(hist + (G - c), 1);
-    }
-  }
-  if (!WRITE) {  // full (reference) leaf count: one global atomic per CTA
-    __shared__ unsigned long long cta_full;
-    if (threadIdx.x == 0) cta_full = 0;
-    __syncthreads();
-    if (lane == 0 && full) atomicAdd(&cta_full, full);
-    __syncthreads();
-    if (threadIdx.x == 0 && cta_full) atomicAdd(aux, cta_full);
   }
 }
 
@@ -499,11 +700,13 @@ bool dense_cull(const Mat& a, const Mat& b, double tau, bool want_tasks, CullRes
   const bool ranged = hi >= 0;
   const int depth = a.depth;
   const int64_t G = int64_t(1) << depth, npos = G * G;
+  const int64_t KW = (G + 31) >> 5;
   // aux[0]: full leaf survivors, [1]: mirror mismatch, [2]: packed scan
-  // total, [4 + t]: tier-t survivors (t < depth), [NEAR + t]: near-tau
-  // products of tier t (t <= depth), [MARGIN]: inverted min relative margin.
-  // [aux | LPT schedule: G + 1 length bins (bin 0 = G tasks) + the K4 counter]
-  // zeroed by one memset; the schedule part is handed to K4 (r.sched).
+  // total, [3]: count-pass CTAs done, [4 + t]: tier-t survivors (t < depth),
+  // [NEAR + t]: near-tau products of tier t (t <= depth), [MARGIN]: inverted
+  // min relative margin.  [aux | LPT schedule: G + 1 length bins (bin 0 = G
+  // tasks) + the K4 counter] zeroed by one memset; the schedule part is
+  // handed to K4 (r.sched).
   htrace("dc_start");
   constexpr int NEAR = 4 + DENSE_MAX_DEPTH, MARGIN = NEAR + DENSE_MAX_DEPTH + 1,
                 CUTS = MARGIN + 1;
@@ -512,37 +715,45 @@ bool dense_cull(const Mat& a, const Mat& b, double tau, bool want_tasks, CullRes
   char* zbuf = dmalloc<char>(aux_bytes + (G + 2) * sizeof(int), s);
   int64_t* aux = reinterpret_cast<int64_t*>(zbuf);
   int* sched = reinterpret_cast<int*>(zbuf + aux_bytes);
-  int64_t* cnt = dmalloc<int64_t>(2 * npos + 1, s);
+  // cnt | off (npos + 1) | keep masks (npos x KW words)
+  char* cbuf = dmalloc<char>((2 * npos + 1) * sizeof(int64_t) +
+                                 (want_tasks ? (size_t)npos * KW * sizeof(uint32_t) : 0), s);
+  int64_t* cnt = reinterpret_cast<int64_t*>(cbuf);
   int64_t* off = cnt + npos;
+  uint32_t* kmask = want_tasks ? reinterpret_cast<uint32_t*>(off + npos + 1) : nullptr;
   SPAMM_CK(cudaMemsetAsync(zbuf, 0, aux_bytes + (G + 2) * sizeof(int), s));
   auto* u64 = reinterpret_cast<unsigned long long*>(aux);
-  if (depth > 0 && !ranged) {  // (a shard reports leaf-tier counts only)
-    const int64_t tri = ((int64_t(1) << (3 * depth)) - 1) / 7;
-    launch_pdl(k_dense_tiers, grid_for(tri, 256, 148LL * 8), 256, 0, s,
-        a.norms, b.norms, tau, depth, u64 + 4, tb, u64 + NEAR, u64 + MARGIN);
-    SPAMM_LAUNCH_CK();
-  }
-  launch_pdl(k_dense_leaf<false>, grid_for(npos * 32, CULL_THREADS, 148LL * 64), CULL_THREADS, 0, s,
-      depth, a.norms, b.norms, tau, sym ? 1 : 0, cnt, nullptr, sched, nullptr, nullptr, nullptr,
-      nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, 0, 0, u64,
-      tb, u64 + NEAR + depth, u64 + MARGIN, lo, hi, work);
-  SPAMM_LAUNCH_CK();
-  scan_exclusive_i64(cnt, npos, off, s);
-  if (want_tasks) hist_scan_exclusive(sched, (int)G + 1, s);
-  // gathered: aux[0..4+depth), near[0..depth], margin
+  // gathered: aux[0..4+depth) (aux[2] := the scan total), near[0..depth], margin
   const int n_base = 4 + depth, n_near = depth + 1;
   const int nsc = n_base + n_near + 1;
-  const int64_t* src[64];
-  for (int i = 0; i < n_base; ++i) src[i] = aux + i;
-  src[2] = off + npos;
-  for (int t = 0; t < n_near; ++t) src[n_base + t] = aux + NEAR + t;
-  src[n_base + n_near] = aux + MARGIN;
+  ScalarSrc src{};
+  for (int i = 0; i < n_base; ++i) src.p[i] = aux + i;
+  src.p[2] = off + npos;
+  src.p[3] = nullptr;
+  for (int t = 0; t < n_near; ++t) src.p[n_base + t] = aux + NEAR + t;
+  src.p[n_base + n_near] = aux + MARGIN;
+  // leaf CTAs: one per 8 positions (parent-mask form, depth >= 2), capped so
+  // the whole grid stays one wave
+  const int n_leaf = depth >= 2 ? (int)std::min<int64_t>(npos / 8, 148LL * 3)
+                                : grid_for(npos * 32, CULL_THREADS, 148LL * 3);
+  const int64_t tri = depth > 0 && !ranged
+                          ? (depth >= 2 ? ((int64_t(1) << (3 * (depth - 1))) - 1) / 7
+                                        : ((int64_t(1) << (3 * depth)) - 1) / 7)
+                          : 0;
+  const int n_tier = tri > 0 ? grid_for(tri, CULL_THREADS, 148LL) : 0;
+  const PinnedGather pg = pinned_gather_begin();
+  launch_pdl(k_dense_count, n_leaf + n_tier, CULL_THREADS, 0, s, depth, a.norms, b.norms, tau,
+             sym ? 1 : 0, cnt, kmask, sched, want_tasks ? 1 : 0, u64, tb, u64 + NEAR,
+             u64 + MARGIN, lo, hi, work, n_tier, ranged ? 0 : 1,
+             reinterpret_cast<unsigned*>(aux + 3), off, src,
+             nsc, pg.vals, pg.flag, pg.seq);
+  SPAMM_LAUNCH_CK();
   int64_t h[64];
-  gather_sync(h, src, nsc, s);
+  pinned_gather_wait(h, nsc, pg, s);
   for (int t = 0; t < n_near; ++t) r.near[t] = h[n_base + t];
   r.margin = margin_from_bits(h[n_base + n_near]);
   if (h[1]) {  // leaf survivor set not mirror-symmetric (ulp tie): full cull
-    dfree(cnt, s);
+    dfree(cbuf, s);
     dfree(zbuf, s);
     return false;
   }
@@ -553,7 +764,7 @@ bool dense_cull(const Mat& a, const Mat& b, double tau, bool want_tasks, CullRes
   for (int t = 0; t <= depth; ++t)
     r.culled[t] = ranged ? 0 : (t == 0 ? 1 : 8 * r.visited[t - 1]) - r.visited[t];
   if (!want_tasks || V == 0) {
-    dfree(cnt, s);
+    dfree(cbuf, s);
     dfree(zbuf, s);
     if (!want_tasks) r.n_tasks = r.visited[depth];
     return true;
@@ -580,12 +791,11 @@ bool dense_cull(const Mat& a, const Mat& b, double tau, bool want_tasks, CullRes
   r.order = r.b_idx + V;
   r.sched = reinterpret_cast<int*>(zbuf);  // frees the aux + schedule buffer
   r.counter = sched + G + 1;
-  launch_pdl(k_dense_leaf<true>, grid_for(npos * 32, CULL_THREADS, 148LL * 64), CULL_THREADS, 0, s,
-      depth, a.norms, b.norms, tau, sym ? 1 : 0, nullptr, off, sched, r.ci, r.cj, r.seg, r.k,
-      a.slot, b.slot, r.a_idx, r.b_idx, r.keys, r.c_out, r.c_mirror, r.order, M, V, nullptr, tb,
-      nullptr, nullptr, lo, hi, nullptr);
+  launch_pdl(k_dense_write, grid_for(npos * 32, CULL_THREADS, 148LL * 64), CULL_THREADS, 0, s,
+             depth, sym ? 1 : 0, off, kmask, sched, r.ci, r.cj, r.seg, r.k, a.slot, b.slot,
+             r.a_idx, r.b_idx, r.keys, r.c_out, r.c_mirror, r.order, M, V);
   SPAMM_LAUNCH_CK();
-  dfree(cnt, s);
+  dfree(cbuf, s);
   r.n_c = M;
   r.n_c_full = F;
   r.n_tasks = V;

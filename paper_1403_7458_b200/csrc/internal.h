@@ -23,6 +23,20 @@ void d2h_sync(int64_t* host, const int64_t* dev, int n, cudaStream_t s);
 // One launch copies n (<= 64) device scalars (null source -> 0) straight into
 // pinned host memory, then waits: replaces memset + D2D copies + D2H per sync.
 void gather_sync(int64_t* host, const int64_t* const* src, int n, cudaStream_t s);
+// The device side of gather_sync for kernels that publish their own scalars:
+// a kernel writes vals[0..n) (pinned, device-visible), fences at system scope
+// and stores seq to *flag; the host spins on the flag.
+constexpr int GATHER_MAX = 64;
+struct ScalarSrc {
+  const int64_t* p[GATHER_MAX];
+};
+struct PinnedGather {
+  int64_t* vals = nullptr;
+  int64_t* flag = nullptr;
+  int64_t seq = 0;
+};
+PinnedGather pinned_gather_begin();
+void pinned_gather_wait(int64_t* host, int n, const PinnedGather& g, cudaStream_t s);
 void copy_to_pinned(double* host, const double* dev, int64_t n, cudaStream_t s);
 void stream_wait(cudaStream_t s);   // spin-polls unless SPAMM_WAIT=block
 // Host-side timeline marks (SPAMM_HTRACE=1): label -> steady clock; htrace_dump

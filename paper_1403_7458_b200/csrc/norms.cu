@@ -132,10 +132,6 @@ void htrace_dump() {
   g_hmarks.clear();
 }
 
-constexpr int GATHER_MAX = 64;
-struct ScalarSrc {
-  const int64_t* p[GATHER_MAX];
-};
 // Writes the scalars, then (after a system-scope fence) the sequence number
 // the host spins on: the host sees completion as soon as the PCIe writes land,
 // without a driver round trip per poll.
@@ -154,23 +150,24 @@ int64_t* pinned_scalars() {
   return pinned;
 }
 
-void gather_sync(int64_t* host, const int64_t* const* src, int n, cudaStream_t s) {
-  if (n > GATHER_MAX) throw CudaError("gather_sync: too many scalars");
-  ScalarSrc ss{};
-  for (int i = 0; i < n; ++i) ss.p[i] = src[i];
-  int64_t* pinned = pinned_scalars() + 32;  // values [32, 96), sequence flag [96]
-  volatile int64_t* flag = pinned_scalars() + 32 + GATHER_MAX;
+PinnedGather pinned_gather_begin() {
   static thread_local int64_t seq = 0;
-  ++seq;
-  launch_pdl(k_gather_scalars, 1, 64, 0, s, ss, n, pinned, const_cast<int64_t*>(flag), seq);
-  SPAMM_LAUNCH_CK();
+  PinnedGather g;
+  g.vals = pinned_scalars() + 32;  // values [32, 96), sequence flag [96]
+  g.flag = pinned_scalars() + 32 + GATHER_MAX;
+  g.seq = ++seq;
+  return g;
+}
+
+void pinned_gather_wait(int64_t* host, int n, const PinnedGather& g, cudaStream_t s) {
   htrace("gs_wait");
+  const volatile int64_t* flag = g.flag;
   if (wait_blocking()) {
     stream_wait(s);
   } else {
     // spin on the flag; every 4096 polls ask the driver (surfaces a failed
     // kernel, and ends the wait if the stream completed)
-    for (unsigned spins = 1; *flag != seq; ++spins) {
+    for (unsigned spins = 1; *flag != g.seq; ++spins) {
       if ((spins & 4095u) == 0) {
         const cudaError_t e = cudaStreamQuery(s);
         if (e == cudaSuccess) break;
@@ -179,7 +176,17 @@ void gather_sync(int64_t* host, const int64_t* const* src, int n, cudaStream_t s
     }
   }
   htrace("gs_done");
-  for (int i = 0; i < n; ++i) host[i] = pinned[i];
+  for (int i = 0; i < n; ++i) host[i] = g.vals[i];
+}
+
+void gather_sync(int64_t* host, const int64_t* const* src, int n, cudaStream_t s) {
+  if (n > GATHER_MAX) throw CudaError("gather_sync: too many scalars");
+  ScalarSrc ss{};
+  for (int i = 0; i < n; ++i) ss.p[i] = src[i];
+  const PinnedGather g = pinned_gather_begin();
+  launch_pdl(k_gather_scalars, 1, 64, 0, s, ss, n, g.vals, g.flag, g.seq);
+  SPAMM_LAUNCH_CK();
+  pinned_gather_wait(host, n, g, s);
 }
 
 __global__ void k_copy_f64(double* __restrict__ dst, const double* __restrict__ src, int64_t n) {
