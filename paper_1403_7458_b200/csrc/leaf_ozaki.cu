@@ -28,8 +28,11 @@
 //    two adjacent tiles: per k-step 4 MMAs of 128x256x32 + 2 of 128x128x32
 //    (12 per task, 20 % less shared-memory operand traffic than 20 of N = 128);
 //  * the epilogue adds the quadrants of equal digit sum d in int32 (exact),
-//    so S_d[r][c] = S_d[c][r] bitwise for a symmetric operand, and rounds once
-//    per d: C = 2^(Er+Ec-14) sum_d S_d 2^-8d (Horner with fused multiply-add).
+//    so S_d[r][c] = S_d[c][r] bitwise for a symmetric operand, folds them
+//    into two exact int64 (Th = sum_{d<=4} S_d 2^(8(4-d)), Tl = the rest)
+//    while TMEM is held, hands TMEM back, and only then rounds Th + Tl 2^-32
+//    (oz_round2) and scales: C = 2^(Er+Ec-46) (Th + Tl 2^-32) -- the FP64
+//    work and the stores overlap the next C block's MMAs.
 //
 // Error: the dropped pairs (p + q >= 8) weigh <= 2^-64 K max|A_r| max|B_c|
 // per element, below the FP64 rounding of the sum: measured 5-6e-17 relative
@@ -225,7 +228,9 @@ __host__ __device__ constexpr int oz_q(int ci) {
        : ci == 6 ? 6 : ci == 7 ? 4 : ci == 8 ? 2 : 0;
 }
 
-template <class Idx>
+// PROF (SPAMM_K4Z_PROF): per-CTA cycle counters; a separate instantiation so
+// the counters cost the product kernel no registers.
+template <class Idx, bool PROF>
 __global__ void __launch_bounds__(OZ_THREADS, 1)
     k_leaf_ozaki(int64_t n_seg, const int64_t* __restrict__ seg, const Idx* __restrict__ a_idx,
                  const Idx* __restrict__ b_idx, const int32_t* __restrict__ b_tr,
@@ -354,11 +359,11 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
       uint32_t phase = 0, tphase = 0;
       int64_t cur2 = 0;
       long long w_full = 0, w_tempty = 0, n_tasks = 0;
-      const long long t_start = prof ? clock64() : 0;
+      const long long t_start = PROF ? clock64() : 0;
       for (;;) {
-        long long t0 = prof ? clock64() : 0;
+        long long t0 = PROF ? clock64() : 0;
         mbar_wait(full(stage), phase);
-        if (prof) w_full += clock64() - t0;
+        if (PROF) w_full += clock64() - t0;
         tc_after();
         const int64_t md = meta[stage];
         if (md < 0) {
@@ -366,7 +371,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
           ring[0] = -1;
           mbar_arrive(tfull);
           oz_commit(tfull);
-          if (prof) {
+          if (PROF) {
             long long* o = prof + blockIdx.x * 16;
             o[0] = clock64() - t_start;
             o[1] = w_full;
@@ -378,9 +383,9 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
         const bool first = md & 1;
         if (first) {
           cur2 = meta2[stage];
-          t0 = prof ? clock64() : 0;
+          t0 = PROF ? clock64() : 0;
           mbar_wait(tempty, tphase ^ 1u);  // TMEM drained by the epilogue
-          if (prof) w_tempty += clock64() - t0;
+          if (PROF) w_tempty += clock64() - t0;
           tphase ^= 1u;
           tc_after();
         }
@@ -442,15 +447,15 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
     long long e_wait = 0, e_hold = 0, e_all = 0, n_blk = 0;
     long long e_ph[4] = {0, 0, 0, 0};  // chunk phases: TMEM read, exchange, convert+store, barrier
     for (;;) {
-      long long te0 = prof ? clock64() : 0;
+      long long te0 = PROF ? clock64() : 0;
       mbar_wait(tfull, ephase);
-      if (prof && threadIdx.x == 0) e_wait += clock64() - te0;
-      te0 = prof ? clock64() : 0;
+      if (PROF && threadIdx.x == 0) e_wait += clock64() - te0;
+      te0 = PROF ? clock64() : 0;
       ephase ^= 1u;
       tc_after();
       const int64_t md = ring[0];
       if (md < 0) {
-        if (prof && threadIdx.x == 0) {
+        if (PROF && threadIdx.x == 0) {
           prof[blockIdx.x * 16 + 4] = e_wait;
           prof[blockIdx.x * 16 + 5] = e_hold;
           prof[blockIdx.x * 16 + 6] = e_all;
@@ -474,15 +479,21 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
       // over its columns, and per column the max over the warp's 32 rows
       // (the rows of the mirror block)
       const bool want_ex = ex_out != nullptr && seg_end;
-      unsigned rcode = 0u;        // row max (code, oz_ex_code)
-      // per chunk cl: the 4 column codes, two per word (named registers: the
-      // chunk loop is not unrolled, an indexed array would live in local memory)
-      unsigned ca0 = 0, cb0 = 0, ca1 = 0, cb1 = 0, ca2 = 0, cb2 = 0, ca3 = 0, cb3 = 0;
-
-#pragma unroll 1
+      unsigned rcode = 0u;  // row max (code, oz_ex_code)
+      // Phase 1 (TMEM held): per 8-column chunk cl, read the four tiles, hand
+      // the partner lane its 4 columns, and fold this thread's 4 columns into
+      // the exact integers Th = sum_{d<=4} S_d 2^(8(4-d)) and
+      // Tl = sum_{d=5..8} S_d 2^(8(8-d)) (|S_d| < 2^30: |Th| < 2^62.1, both
+      // exact in int64; S_d = S_d^T for a symmetric operand, so Th / Tl are
+      // too).  TMEM is handed back as soon as the last chunk's loads land.
+      // Phase 2 (TMEM released, beside the next C block's MMAs): round
+      // Th + Tl 2^-32 once, scale by 2^(Er + Ec - 46), accumulate, store.
+      long long Th[4][4], Tl[4][4];
+      int4* xg4 = reinterpret_cast<int4*>(xg);
+      long long tp = (PROF && threadIdx.x == 0) ? clock64() : 0;
+#pragma unroll
       for (int cl = 0; cl < 4; ++cl) {
         const int cc = grp * 4 + cl;
-        long long tp = (prof && threadIdx.x == 0) ? clock64() : 0;
         int L[4][8], R[4][8];
 #pragma unroll
         for (int t = 0; t < 4; ++t) {
@@ -496,7 +507,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
           tmem_keep8(L[t]);
           tmem_keep8(R[t]);
         }
-        if (prof && threadIdx.x == 0) {
+        if (PROF && threadIdx.x == 0) {
           const long long t1 = clock64();
           e_ph[0] += t1 - tp;
           tp = t1;
@@ -505,10 +516,9 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
           tc_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(tempty);
-          if (prof && threadIdx.x == 0) e_hold += clock64() - te0;
+          if (PROF && threadIdx.x == 0) e_hold += clock64() - te0;
         }
         // hand the partner the 4 columns it owns: one 16-byte store per (tile, half)
-        int4* xg4 = reinterpret_cast<int4*>(xg);
 #pragma unroll
         for (int t = 0; t < 4; ++t) {
           xg4[(t * 2) * OZ_GROUP + e] = top ? make_int4(L[t][4], L[t][5], L[t][6], L[t][7])
@@ -516,22 +526,53 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
           xg4[(t * 2 + 1) * OZ_GROUP + e] = top ? make_int4(R[t][4], R[t][5], R[t][6], R[t][7])
                                                 : make_int4(R[t][0], R[t][1], R[t][2], R[t][3]);
         }
-        const int col0 = cc * 8 + own0;
-        const int4 ec4 = *reinterpret_cast<const int4*>(ex_b + bj * OZ_NB + col0);
         asm volatile("bar.sync %0, 128;\n" ::"r"(1 + grp) : "memory");
-        if (prof && threadIdx.x == 0) {
+        if (PROF && threadIdx.x == 0) {
           const long long t1 = clock64();
           e_ph[1] += t1 - tp;
           tp = t1;
         }
-        int oL[4][4], oR[4][4];
 #pragma unroll
         for (int t = 0; t < 4; ++t) {
           const int4 a = xg4[(t * 2) * OZ_GROUP + partner];
           const int4 b = xg4[(t * 2 + 1) * OZ_GROUP + partner];
-          oL[t][0] = a.x; oL[t][1] = a.y; oL[t][2] = a.z; oL[t][3] = a.w;
-          oR[t][0] = b.x; oR[t][1] = b.y; oR[t][2] = b.z; oR[t][3] = b.w;
+          const int oa[4] = {a.x, a.y, a.z, a.w};
+          const int ob[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            // quadrants (top / bottom A slice x left / right B slice) of tile t
+            const int ml = top ? L[t][c] : L[t][4 + c];  // static register indices
+            const int mr = top ? R[t][c] : R[t][4 + c];
+            const int tl = top ? ml : oa[c], tr = top ? mr : ob[c];
+            const int bl = top ? oa[c] : ml, br = top ? ob[c] : mr;
+            // S_{2t} += tl, S_{2t+1} += tr + bl, S_{2t+2} += br
+            if (t == 0) {
+              Th[cl][c] = (long long)tl * 4294967296LL + (long long)(tr + bl) * 16777216LL;
+              Tl[cl][c] = (long long)br * 65536LL;  // S_2 (Th), placed below
+            } else if (t == 1) {
+              Th[cl][c] += ((long long)Tl[cl][c] + (long long)tl * 65536LL) +
+                           (long long)(tr + bl) * 256LL;
+              Tl[cl][c] = br;  // S_4 part (Th)
+            } else if (t == 2) {
+              Th[cl][c] += (long long)Tl[cl][c] + (long long)tl;
+              Tl[cl][c] = (long long)(tr + bl) * 16777216LL + (long long)br * 65536LL;
+            } else {
+              Tl[cl][c] += (long long)tl * 65536LL + (long long)(tr + bl) * 256LL + (long long)br;
+            }
+          }
         }
+        if (PROF && threadIdx.x == 0) {
+          const long long t1 = clock64();
+          e_ph[2] += t1 - tp;
+          tp = t1;
+        }
+        asm volatile("bar.sync %0, 128;\n" ::"r"(1 + grp) : "memory");
+      }
+      // ---- phase 2: TMEM is free; round, scale, accumulate, store ----
+#pragma unroll
+      for (int cl = 0; cl < 4; ++cl) {
+        const int col0 = (grp * 4 + cl) * 8 + own0;
+        const int4 ec4 = *reinterpret_cast<const int4*>(ex_b + bj * OZ_NB + col0);
         const int ecs[4] = {ec4.x, ec4.y, ec4.z, ec4.w};
         bool bad[4];
 #pragma unroll
@@ -539,22 +580,8 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
         double res[4];
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
-          int tl[4], tr[4], bl[4], br[4];
-#pragma unroll
-          for (int t = 0; t < 4; ++t) {
-            const int ml = top ? L[t][c] : L[t][4 + c];  // static register indices
-            const int mr = top ? R[t][c] : R[t][4 + c];
-            tl[t] = top ? ml : oL[t][c];
-            tr[t] = top ? mr : oR[t][c];
-            bl[t] = top ? oL[t][c] : ml;
-            br[t] = top ? oR[t][c] : mr;
-          }
-          // S_d: the exact digit-sum-d part (|quadrant| < 2^30: int32 sums exact)
-          const int S[9] = {tl[0],         tr[0] + bl[0], tl[1] + br[0],
-                            tr[1] + bl[1], tl[2] + br[1], tr[2] + bl[2],
-                            tl[3] + br[2], tr[3] + bl[3], br[3]};
-          const double v = oz_horner(S);
-          const int k = er + (bad[c] ? 0 : oz_exp(ecs[c]));  // C = v 2^k
+          const double v = oz_round2(Th[cl][c], Tl[cl][c]);
+          const int k = er - 32 + (bad[c] ? 0 : oz_exp(ecs[c]));  // C = v 2^k
           res[c] = (k >= -1022 && k <= 1023)
                        ? __dmul_rn(v, __longlong_as_double((long long)(k + 1023) << 52))
                        : ldexp(v, k);
@@ -564,7 +591,6 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
           // a non-finite operand entry in this row or one of these columns:
           // those elements are computed once, at the segment's end, in FP64
           // in the reference's order (earlier chunks leave them untouched)
-          // (unrolled: a dynamically indexed res[] would live in local memory)
           double* rp = Cb + r * OZ_NB + col0;
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
@@ -608,43 +634,26 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
               for (int c = 0; c < 4; ++c) Cm[(col0 + c) * OZ_NB + r] = res[c];
           }
         }
-        if (want_ex) {  // codes only here; the reductions run after TMEM is released
+        if (want_ex) {
           unsigned k4[4];
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
             k4[c] = oz_ex_code(res[c]);
             rcode = max(rcode, k4[c]);
           }
-          const unsigned wa = k4[0] | (k4[1] << 16), wb = k4[2] | (k4[3] << 16);
-          if (cl == 0) { ca0 = wa; cb0 = wb; }
-          else if (cl == 1) { ca1 = wa; cb1 = wb; }
-          else if (cl == 2) { ca2 = wa; cb2 = wb; }
-          else { ca3 = wa; cb3 = wb; }
-        }
-        if (prof && threadIdx.x == 0) {
-          const long long t1 = clock64();
-          e_ph[2] += t1 - tp;
-          tp = t1;
-        }
-        asm volatile("bar.sync %0, 128;\n" ::"r"(1 + grp) : "memory");
-        if (prof && threadIdx.x == 0) e_ph[3] += clock64() - tp;
-      }
-      if (want_ex) {
-        if (Cm) {  // mirror rows: a column's max over this warp's 32 rows
-          const unsigned cw[8] = {ca0, cb0, ca1, cb1, ca2, cb2, ca3, cb3};
-#pragma unroll
-          for (int cl = 0; cl < 4; ++cl)
+          if (Cm) {  // mirror rows: a column's max over this warp's 32 rows
 #pragma unroll
             for (int c = 0; c < 4; ++c) {
-              const unsigned k = (cw[2 * cl + (c >> 1)] >> (16 * (c & 1))) & 0xFFFFu;
-              const unsigned mx = __reduce_max_sync(0xffffffffu, k);
+              const unsigned mx = __reduce_max_sync(0xffffffffu, k4[c]);
               if (lane == 0 && mx)
-                atomicMax(ex_out + bj * OZ_NB + (grp * 4 + cl) * 8 + own0 + c, oz_ex_decode(mx));
+                atomicMax(ex_out + bj * OZ_NB + col0 + c, oz_ex_decode(mx));
             }
+          }
         }
-        if (rcode) atomicMax(ex_out + bi * OZ_NB + r, oz_ex_decode(rcode));
       }
-      if (prof && threadIdx.x == 0) {
+      if (want_ex && rcode) atomicMax(ex_out + bi * OZ_NB + r, oz_ex_decode(rcode));
+      if (PROF && threadIdx.x == 0) e_ph[3] += clock64() - tp;
+      if (PROF && threadIdx.x == 0) {
         e_all += clock64() - te0;
         ++n_blk;
       }
@@ -952,10 +961,13 @@ void ozaki_launch(int64_t n_seg, const int64_t* seg, const Idx* a_idx, const Idx
   }();
   static const bool want_prof = getenv("SPAMM_K4Z_PROF") != nullptr;
   long long* prof = nullptr;
-  auto kern = k_leaf_ozaki<Idx>;
+  auto kern = want_prof ? k_leaf_ozaki<Idx, true> : k_leaf_ozaki<Idx, false>;
   static std::once_flag once;
   std::call_once(once, [&] {
-    SPAMM_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)OZ_SMEM));
+    SPAMM_CK(cudaFuncSetAttribute(k_leaf_ozaki<Idx, true>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)OZ_SMEM));
+    SPAMM_CK(cudaFuncSetAttribute(k_leaf_ozaki<Idx, false>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)OZ_SMEM));
   });
   int64_t grid = multiprocessors();
   if (grid > n_seg) grid = n_seg;

@@ -35,6 +35,18 @@ __device__ __forceinline__ double oz_horner(const int (&S)[NL]) {
   return v;
 }
 
+// th + tl 2^-32 rounded to double (|th| < 2^62.1, |tl| < 2^54.1; the value of
+// sum_d S_d 2^-8d scaled by 2^32): hi = RN(th) and its exact remainder
+// th - hi (|.| <= 2^9, an integer), the remainder plus the low part in one
+// FMA, then one final add -- within a few units of 2^-60 of the exactly
+// rounded value, deterministic in (th, tl).
+__device__ __forceinline__ double oz_round2(long long th, long long tl) {
+  const double hi = __ll2double_rn(th);
+  const long long rem = th - __double2ll_rz(hi);  // exact: hi is an integer < 2^63
+  const double lo = __fma_rn(__ll2double_rn(tl), 0x1p-32, (double)rem);
+  return __dadd_rn(hi, lo);
+}
+
 // 32-byte global accesses (sm_100: LDG/STG.256): one whole sector per lane
 // for the four C elements an epilogue thread owns in a row.
 __device__ __forceinline__ void oz_ld4(const double* p, double& a, double& b, double& c,
