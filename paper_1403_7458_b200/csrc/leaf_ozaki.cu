@@ -293,58 +293,93 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
       t1 = seg[m + 1];
       return true;
     };
+    // Batches of 32 tasks (one index per lane).  The next batch's indices are
+    // loaded while the current batch's copies are issued (its dependent
+    // lookups -- transposed slot, the (i, j) of a chunk start -- one task
+    // later), and the block after the current one is claimed during its
+    // first batch: no chain of L2 round trips between two batches' copies.
+    auto first_lookups = [&](int64_t c0_, int64_t t0_, int64_t t1_, int64_t& ra_, int64_t& rb_,
+                             int64_t& kab_) {
+      const int64_t t = c0_ + lane;
+      kab_ = 0;
+      if (t < t1_) {
+        const int64_t rbo = rb_;
+        if ((t - t0_) % OZ_CHUNK == 0)
+          kab_ = ((a_keys[ra_] / G) << 32) | (b_keys[rbo] % G);
+        if (b_tr) rb_ = b_tr[rbo];
+      }
+    };
     int64_t m = 0, t0 = 0, t1 = 0;
     bool have = claim(m, t0, t1);
-    while (have) {
-      int64_t mn = 0, t0n = 0, t1n = 0;
-      const bool next = claim(mn, t0n, t1n);
-      for (int64_t c0 = t0; c0 < t1; c0 += 32) {
-        const int64_t t = c0 + lane;
-        int64_t ra_l = 0, rb_l = 0;
-        if (t < t1) {
-          ra_l = (int64_t)a_idx[t];
-          rb_l = (int64_t)b_idx[t];
-          if (b_tr) rb_l = b_tr[rb_l];
-        }
-        const int cnt = t1 - c0 < 32 ? (int)(t1 - c0) : 32;
-        for (int q = 0; q < cnt; ++q) {
-          const int64_t ra = __shfl_sync(0xffffffffu, ra_l, q);
-          const int64_t rb = __shfl_sync(0xffffffffu, rb_l, q);
-          mbar_wait(empty(stage), phase ^ 1u);
-          if (lane == 0) {
-            const int64_t tq = c0 + q, r = tq - t0;
-            const bool first = r % OZ_CHUNK == 0;
-            const bool last = tq + 1 == t1 || (r + 1) % OZ_CHUNK == 0;
-            const bool cont = r >= OZ_CHUNK || accumulate;
-            // bit 3: the chunk ends the C block's segment
-            meta[stage] = (m << 4) | (first ? 1 : 0) | (last ? 2 : 0) | (cont ? 4 : 0) |
-                          (tq + 1 == t1 ? 8 : 0);
-            if (first)
-              meta2[stage] = ((a_keys[a_idx[tq]] / G) << 32) | (b_keys[b_idx[tq]] % G);
-            mbar_expect_tx(full(stage), OZ_STAGE);
-            const uint32_t sa = base + stage * OZ_STAGE;
-            if (hint & 1) {  // operand slices evict_last (re-read by many C blocks)
-              const uint64_t pol = pol_evict_last();
-              bulk_g2s_pol(sa, As + ra * OZ_BLOCK_BYTES, OZ_BLOCK_BYTES, full(stage), pol);
-              bulk_g2s_pol(sa + OZ_BLOCK_BYTES, Bs + rb * OZ_BLOCK_BYTES, OZ_BLOCK_BYTES,
-                           full(stage), pol);
-            } else {
-              bulk_g2s(sa, As + ra * OZ_BLOCK_BYTES, OZ_BLOCK_BYTES, full(stage));
-              bulk_g2s(sa + OZ_BLOCK_BYTES, Bs + rb * OZ_BLOCK_BYTES, OZ_BLOCK_BYTES,
-                       full(stage));
-            }
-          }
-          __syncwarp();
-          if (++stage == OZ_STAGES) {
-            stage = 0;
-            phase ^= 1u;
-          }
-        }
+    int64_t c0 = t0, ra_l = 0, rb_l = 0, kab_l = 0;
+    if (have) {
+      if (c0 + lane < t1) {
+        ra_l = (int64_t)a_idx[c0 + lane];
+        rb_l = (int64_t)b_idx[c0 + lane];
       }
-      have = next;
-      m = mn;
-      t0 = t0n;
-      t1 = t1n;
+      first_lookups(c0, t0, t1, ra_l, rb_l, kab_l);
+    }
+    int64_t mn = 0, t0n = 0, t1n = 0;  // the block claimed ahead
+    bool hn = false, claimed = false;
+    while (have) {
+      const int cnt = t1 - c0 < 32 ? (int)(t1 - c0) : 32;
+      int64_t nm = 0, nt0 = 0, nt1 = 0, nc0 = 0, nra = 0, nrb = 0, nkab = 0;
+      bool hnext = false;
+      for (int q = 0; q < cnt; ++q) {
+        const int64_t ra = __shfl_sync(0xffffffffu, ra_l, q);
+        const int64_t rb = __shfl_sync(0xffffffffu, rb_l, q);
+        const int64_t kab = __shfl_sync(0xffffffffu, kab_l, q);
+        mbar_wait(empty(stage), phase ^ 1u);
+        if (lane == 0) {
+          const int64_t tq = c0 + q, r = tq - t0;
+          const bool first = r % OZ_CHUNK == 0;
+          const bool last = tq + 1 == t1 || (r + 1) % OZ_CHUNK == 0;
+          const bool cont = r >= OZ_CHUNK || accumulate;
+          // bit 3: the chunk ends the C block's segment
+          meta[stage] = (m << 4) | (first ? 1 : 0) | (last ? 2 : 0) | (cont ? 4 : 0) |
+                        (tq + 1 == t1 ? 8 : 0);
+          if (first) meta2[stage] = kab;
+          mbar_expect_tx(full(stage), OZ_STAGE);
+          const uint32_t sa = base + stage * OZ_STAGE;
+          if (hint & 1) {  // operand slices evict_last (re-read by many C blocks)
+            const uint64_t pol = pol_evict_last();
+            bulk_g2s_pol(sa, As + ra * OZ_BLOCK_BYTES, OZ_BLOCK_BYTES, full(stage), pol);
+            bulk_g2s_pol(sa + OZ_BLOCK_BYTES, Bs + rb * OZ_BLOCK_BYTES, OZ_BLOCK_BYTES,
+                         full(stage), pol);
+          } else {
+            bulk_g2s(sa, As + ra * OZ_BLOCK_BYTES, OZ_BLOCK_BYTES, full(stage));
+            bulk_g2s(sa + OZ_BLOCK_BYTES, Bs + rb * OZ_BLOCK_BYTES, OZ_BLOCK_BYTES,
+                     full(stage));
+          }
+        }
+        __syncwarp();
+        if (++stage == OZ_STAGES) {
+          stage = 0;
+          phase ^= 1u;
+        }
+        if (q == 0) {  // after this batch's first copy: claim ahead, load the next batch
+          if (!claimed) {
+            hn = claim(mn, t0n, t1n);
+            claimed = true;
+          }
+          if (c0 + 32 < t1) {
+            nm = m, nt0 = t0, nt1 = t1, nc0 = c0 + 32;
+            hnext = true;
+          } else {
+            nm = mn, nt0 = t0n, nt1 = t1n, nc0 = t0n;
+            hnext = hn;
+          }
+          if (hnext && nc0 + lane < nt1) {
+            nra = (int64_t)a_idx[nc0 + lane];
+            nrb = (int64_t)b_idx[nc0 + lane];
+          }
+        }
+        if (hnext && (q == 1 || cnt == 1)) first_lookups(nc0, nt0, nt1, nra, nrb, nkab);
+      }
+      if (!hnext) break;
+      if (nc0 == nt0) claimed = false;  // a new block: claim the one after it
+      m = nm, t0 = nt0, t1 = nt1, c0 = nc0;
+      ra_l = nra, rb_l = nrb, kab_l = nkab;
     }
     mbar_wait(empty(stage), phase ^ 1u);
     if (lane == 0) {
