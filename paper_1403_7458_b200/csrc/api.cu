@@ -557,6 +557,13 @@ namespace {
 
 // AUTO's choice of K4z for block size nb (SPAMM_AUTO_LEAF=dmma: never).
 bool auto_ozaki_for(int nb);
+bool oz_ex_from_producers() {  // SPAMM_OZ_EXPROD=0: exponent passes as before
+  static const bool on = [] {
+    const char* v = getenv("SPAMM_OZ_EXPROD");
+    return !(v && strcmp(v, "0") == 0);
+  }();
+  return on;
+}
 bool auto_ozaki_enabled() {  // SPAMM_AUTO_LEAF=dmma: AUTO keeps the DMMA kernel
   static const bool on = [] {
     const char* v = getenv("SPAMM_AUTO_LEAF");
@@ -772,6 +779,16 @@ void multiply_impl(const spamm_mat* a, const spamm_mat* b, double tau, int32_t k
     ex_out = spamm::dmalloc<int>(C.G * C.nb, s);
     SPAMM_CK(cudaMemsetAsync(ex_out, 0x80, C.G * C.nb * sizeof(int), s));
   }
+  // SP2 (idem fused): C's K4z exponents taken by the K1 pass over C (column
+  // maxima = row maxima of the bitwise symmetric C), so the next multiply on
+  // C -- after SQUARE -- skips its exponent pass.  SPAMM_OZ_EXPROD=0: off.
+  int* ex_k1 = nullptr;
+  if (!ex_out && oz_ex_from_producers() && idem.x && sym && k4z_possible &&
+      spamm::ozaki_supported(C.nb) && spamm::idem_fusable(C)) {
+    ex_k1 = spamm::dmalloc<int>(C.G * C.nb, s);
+    SPAMM_CK(cudaMemsetAsync(ex_k1, 0x80, C.G * C.nb * sizeof(int), s));
+    idem.ex_col = ex_k1;
+  }
   bool ex_done = false;
   if (g_side) g_side->window(s);  // PCIe chunk alongside K4
   tm.mark(1);  // leaf window = the K4 launch only (allocation stays outside)
@@ -811,6 +828,7 @@ void multiply_impl(const spamm_mat* a, const spamm_mat* b, double tau, int32_t k
     spamm::finalize(C, s, idem, defer_prune);
   else
     spamm::finalize(C, s, nullptr, nullptr, defer_prune);
+  if (ex_k1) C.oz_ex_row = ex_k1;
   C.sym = sym;
   spamm::htrace("mul_final");
   tm.mark(3);
@@ -934,9 +952,14 @@ void sp2_finish(const spamm_mat* x, const spamm_mat* c, double n_occ, bool want_
       }
     } hook{e, kernel, s, ahead};
     const bool early = e && ahead && idem_done;
+    const bool k4z_next = kernel == spamm::LEAF_OZAKI ||
+                          (kernel == spamm::LEAF_AUTO && auto_ozaki_enabled() &&
+                           auto_ozaki_for(x->m.nb));
     spamm::sp2_update_finish(x->m, c->m, prep, h[2], want_idem && !idem_done, !square, idem,
                              e ? e->m : dummy, s, /*settle_now=*/!idem_done,
-                             early ? &Hook::run : nullptr, &hook);
+                             early ? &Hook::run : nullptr, &hook,
+                             k4z_next && oz_ex_from_producers() &&
+                                 spamm::ozaki_supported(x->m.nb));
   } else {
     spamm::sp2_update(x->m, c->m, want_idem && !idem_done, !square, idem, e ? e->m : dummy, s);
   }

@@ -103,6 +103,9 @@ struct IdemFuse {
   int64_t* ucount = nullptr;
   // optional: the leaf tier (G * G, row-major) of ||X^2 - X||^2 (multi-GPU)
   double* dleaf = nullptr;
+  // optional: C's K4z column exponents (G * nb, preset to OZ_EXP_NONE), taken
+  // by the same pass -- the row exponents of a bitwise symmetric C
+  int* ex_col = nullptr;
 };
 bool idem_fusable(const Mat& x);
 void finalize(Mat& m, cudaStream_t s, IdemFuse idem, bool defer);
@@ -134,7 +137,7 @@ UnionPrep sp2_union_prepare(const Mat& x, const Mat& x2, int64_t* u_dev, cudaStr
 void sp2_update_finish(const Mat& x, const Mat& x2, UnionPrep& prep, int64_t U, bool want_idem,
                        bool expand, double* idem_norm, Mat& e, cudaStream_t s,
                        bool settle_now = true, void (*after_update)(void*) = nullptr,
-                       void* after_ctx = nullptr);
+                       void* after_ctx = nullptr, bool want_oz_ex = false);
 bool sp2_fused_supported(int nb);
 
 void scatter_slots(const int64_t* keys, int64_t m, int32_t* slot, cudaStream_t s);

@@ -22,6 +22,7 @@
 #include <vector>
 
 #include "internal.h"
+#include "ozaki_common.cuh"
 
 namespace spamm {
 
@@ -771,9 +772,10 @@ __global__ void __launch_bounds__(32 * WARPS)
                      int64_t m, const double* __restrict__ xdata,
                      const int32_t* __restrict__ xslot, double* __restrict__ out,
                      uint8_t* __restrict__ nz, double* __restrict__ dout,
-                     double* __restrict__ out1) {
+                     double* __restrict__ out1, int* __restrict__ ex_col, int64_t G) {
   pdl_wait();
   constexpr int NCH = NB2 / 256, BPW = 2;
+  constexpr int NB = NB2 == 4096 ? 64 : 32;
   __shared__ __align__(16) double rows_all[WARPS][BPW * 4 * CHAIN_ROW];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double* rows = rows_all[warp];
@@ -798,6 +800,9 @@ __global__ void __launch_bounds__(32 * WARPS)
     }
     double acc = 0.0;
     unsigned anyq = 0;
+    double cm[BPW][2];  // K4z column maxima (ex_col)
+#pragma unroll
+    for (int q = 0; q < BPW; ++q) cm[q][0] = cm[q][1] = 0.0;
     for (int ch = 0; ch < NCH; ++ch) {
       __syncwarp();
 #pragma unroll
@@ -805,6 +810,10 @@ __global__ void __launch_bounds__(32 * WARPS)
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
           double* rq = rows + q * 4 * CHAIN_ROW + chain_pos(k, lane);
+          if (ex_col) {
+            cm[q][0] = fmax(cm[q][0], ozk::oz_absf(r[q][k].x));
+            cm[q][1] = fmax(cm[q][1], ozk::oz_absf(r[q][k].y));
+          }
           const double d0 = __dsub_rn(r[q][k].x, y[q][k].x);
           const double d1 = __dsub_rn(r[q][k].y, y[q][k].y);
           rq[0] = __dmul_rn(r[q][k].x, r[q][k].x);
@@ -839,6 +848,8 @@ __global__ void __launch_bounds__(32 * WARPS)
         nz[b0 + q] = any ? 1 : 0;
         dout[b0 + q] = __dadd_rn(e0, e1);
       }
+      if (ex_col && b0 + q < m)
+        ozk::oz_col_exponents<NB>(cm[q][0], cm[q][1], keys[b0 + q] % G, ex_col, lane);
     }
   }
 }
@@ -978,10 +989,12 @@ void finalize_impl(Mat& m, cudaStream_t s, double* pre_n2, uint8_t* pre_nz, bool
         const int grid = grid_for((m.nblocks + 1) / 2 * 32, 32 * WARPS, 1LL << 20);
         if (nb2 == 4096)
           launch_pdl(k_leaf_norms2_cd<4096, WARPS>, grid, 32 * WARPS, 0, s,
-              m.data, m.keys, m.nblocks, idem.x->data, idem.x->slot, n2, nz, dn2, n1);
+              m.data, m.keys, m.nblocks, idem.x->data, idem.x->slot, n2, nz, dn2, n1,
+              idem.ex_col, int64_t(1) << m.depth);
         else
           launch_pdl(k_leaf_norms2_cd<1024, WARPS>, grid, 32 * WARPS, 0, s,
-              m.data, m.keys, m.nblocks, idem.x->data, idem.x->slot, n2, nz, dn2, n1);
+              m.data, m.keys, m.nblocks, idem.x->data, idem.x->slot, n2, nz, dn2, n1,
+              idem.ex_col, int64_t(1) << m.depth);
         SPAMM_LAUNCH_CK();
       } else {
         leaf_norms2(m.data, m.nblocks, m.nb, n2, nz, s, n1);

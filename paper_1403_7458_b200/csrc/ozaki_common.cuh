@@ -264,5 +264,23 @@ __device__ __forceinline__ void tmem_keep8(int (&v)[8]) {
 }
 
 
+// K4z column exponents produced by a kernel that already streams a block
+// warp-wide with lane l holding columns (2l, 2l + 1) mod Nb of every row it
+// reads (K1, the SP2 update): m0 / m1 = the lane's max oz_absf over those
+// columns; atomicMax into ex[bj * Nb + col] as k_oz_exponents(by_col = 1)
+// would.  For a bitwise symmetric matrix these are its row exponents too.
+template <int NB>
+__device__ __forceinline__ void oz_col_exponents(double m0, double m1, int64_t bj, int* ex,
+                                                 int lane) {
+  if (NB == 32) {  // lanes l and l ^ 16 hold the same column pair
+    m0 = fmax(m0, __shfl_xor_sync(0xffffffffu, m0, 16));
+    m1 = fmax(m1, __shfl_xor_sync(0xffffffffu, m1, 16));
+    if (lane >= 16) return;
+  }
+  const int c = (2 * lane) % NB;
+  if (m0 > 0.0) atomicMax(ex + bj * NB + c, oz_exp_of(m0));
+  if (m1 > 0.0) atomicMax(ex + bj * NB + c + 1, oz_exp_of(m1));
+}
+
 }  // namespace ozk
 }  // namespace spamm

@@ -13,6 +13,7 @@
 // is reduced to its root with the same tier order as any other matrix.
 // HBM roofline: reads 2 S Nb^2 8 B, writes S Nb^2 8 B (EXPAND).
 #include "internal.h"
+#include "ozaki_common.cuh"
 
 namespace spamm {
 
@@ -85,9 +86,11 @@ __global__ void __launch_bounds__(32 * WARPS)
                        const int32_t* __restrict__ sx, const double* __restrict__ X2,
                        const int32_t* __restrict__ sx2, double* __restrict__ E,
                        double* __restrict__ nD2, double* __restrict__ nE2,
-                       uint8_t* __restrict__ nzE, double* __restrict__ nE1) {
+                       uint8_t* __restrict__ nzE, double* __restrict__ nE1,
+                       int* __restrict__ ex_col, int64_t G) {
   pdl_wait();
   constexpr int NCH = NB2 / 256;
+  constexpr int NB = NB2 == 4096 ? 64 : 32;
   __shared__ __align__(16) double rows_all[WARPS][BPW * 4 * CHAIN_ROW];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double* rows = rows_all[warp];
@@ -116,6 +119,9 @@ __global__ void __launch_bounds__(32 * WARPS)
     }
     double acc = 0.0;
     unsigned anyq = 0;
+    double cm[BPW][2];  // E's K4z column maxima (ex_col)
+#pragma unroll
+    for (int q = 0; q < BPW; ++q) cm[q][0] = cm[q][1] = 0.0;
     for (int c = 0; c < NCH; ++c) {
       __syncwarp();
 #pragma unroll
@@ -147,6 +153,10 @@ __global__ void __launch_bounds__(32 * WARPS)
             rq[3 * CHAIN_ROW] = __dmul_rn(e1, e1);
             if (pe[q]) pe[q][c * 128 + k * 32 + lane] = make_double2(e0, e1);
             if ((e0 != 0.0) | (e1 != 0.0)) anyq |= 1u << q;
+            if (ex_col) {
+              cm[q][0] = fmax(cm[q][0], ozk::oz_absf(e0));
+              cm[q][1] = fmax(cm[q][1], ozk::oz_absf(e1));
+            }
           }
         }
       __syncwarp();
@@ -179,6 +189,8 @@ __global__ void __launch_bounds__(32 * WARPS)
           nzE[u0 + q] = any ? 1 : 0;
         }
       }
+      if (EXPAND && ex_col && u0 + q < U)
+        ozk::oz_col_exponents<NB>(cm[q][0], cm[q][1], ukeys[u0 + q] % G, ex_col, lane);
     }
   }
 }
@@ -186,18 +198,18 @@ __global__ void __launch_bounds__(32 * WARPS)
 template <int NB2>
 void launch_update(bool idem, bool expand, const int64_t* ukeys, int64_t U, const Mat& x,
                    const Mat& x2, double* E, double* nD2, double* nE2, uint8_t* nzE,
-                   cudaStream_t s, double* nE1) {
+                   cudaStream_t s, double* nE1, int* ex_col) {
   constexpr int BPW = 2, WARPS = 4;
   const int grid = grid_for((U + BPW - 1) / BPW * 32, 32 * WARPS, 1LL << 20);
   if (idem && expand)
     launch_pdl(k_sp2_update_multi<NB2, true, true, BPW, WARPS>, grid, 32 * WARPS, 0, s,
-        ukeys, U, x.data, x.slot, x2.data, x2.slot, E, nD2, nE2, nzE, nE1);
+        ukeys, U, x.data, x.slot, x2.data, x2.slot, E, nD2, nE2, nzE, nE1, ex_col, x.G);
   else if (idem)
     launch_pdl(k_sp2_update_multi<NB2, true, false, BPW, WARPS>, grid, 32 * WARPS, 0, s,
-        ukeys, U, x.data, x.slot, x2.data, x2.slot, E, nD2, nE2, nzE, nE1);
+        ukeys, U, x.data, x.slot, x2.data, x2.slot, E, nD2, nE2, nzE, nE1, ex_col, x.G);
   else
     launch_pdl(k_sp2_update_multi<NB2, false, true, BPW, WARPS>, grid, 32 * WARPS, 0, s,
-        ukeys, U, x.data, x.slot, x2.data, x2.slot, E, nD2, nE2, nzE, nE1);
+        ukeys, U, x.data, x.slot, x2.data, x2.slot, E, nD2, nE2, nzE, nE1, ex_col, x.G);
   SPAMM_LAUNCH_CK();
 }
 
@@ -253,7 +265,7 @@ UnionPrep sp2_union_prepare(const Mat& x, const Mat& x2, int64_t* u_dev, cudaStr
 
 void sp2_update_finish(const Mat& x, const Mat& x2, UnionPrep& prep, int64_t U, bool want_idem,
                        bool expand, double* idem_norm, Mat& e, cudaStream_t s, bool settle_now,
-                       void (*after_update)(void*), void* after_ctx) {
+                       void (*after_update)(void*), void* after_ctx, bool want_oz_ex) {
   const int nb2 = x.nb * x.nb;
   int64_t* ukeys = prep.keys;
   prep.keys = nullptr;
@@ -275,11 +287,18 @@ void sp2_update_finish(const Mat& x, const Mat& x2, UnionPrep& prep, int64_t U, 
   double* nE1 = expand ? dmalloc<double>(U, s) : nullptr;
   uint8_t* nzE = expand ? dmalloc<uint8_t>(U, s) : nullptr;
   double* E = expand ? dmalloc<double>((size_t)U * nb2, s) : nullptr;
+  // E's K4z row exponents (= its column exponents: E is bitwise symmetric
+  // when X and X^2 are), so E's first multiply skips its exponent pass
+  int* ex = nullptr;
+  if (expand && want_oz_ex && x.sym && x2.sym) {
+    ex = dmalloc<int>(x.G * x.nb, s);
+    SPAMM_CK(cudaMemsetAsync(ex, 0x80, x.G * x.nb * sizeof(int), s));
+  }
   if (U > 0) {
     if (nb2 == 4096)
-      launch_update<4096>(want_idem, expand, ukeys, U, x, x2, E, nD2, nE2, nzE, s, nE1);
+      launch_update<4096>(want_idem, expand, ukeys, U, x, x2, E, nD2, nE2, nzE, s, nE1, ex);
     else
-      launch_update<1024>(want_idem, expand, ukeys, U, x, x2, E, nD2, nE2, nzE, s, nE1);
+      launch_update<1024>(want_idem, expand, ukeys, U, x, x2, E, nD2, nE2, nzE, s, nE1, ex);
   }
   double* pn = nullptr;
   if (want_idem) {
@@ -299,6 +318,7 @@ void sp2_update_finish(const Mat& x, const Mat& x2, UnionPrep& prep, int64_t U, 
     e.keys = ukeys;
     e.sym = x.sym && x2.sym;
     e.stream = s;
+    e.oz_ex_row = ex;
     if (after_update) after_update(after_ctx);
     finalize(e, s, nE2, nzE, /*defer=*/true, nE1);
   } else {

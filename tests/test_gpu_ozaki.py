@@ -166,10 +166,16 @@ def test_auto_falls_back_to_dmma_without_slice_memory():
     assert out.returncode == 0 and "fallback ok" in out.stdout, out.stderr[-2000:]
 
 
-def test_product_exponents_from_the_epilogue_are_the_exponent_pass(tmp_path):
-    """SPAMM_OZ_EXOUT=1 (the K4z epilogue writes X^2's own row exponents and
-    the next multiply skips its exponent pass): bitwise the default SP2, for
-    Nb = 64 (K4z) and Nb = 32 (K4z32)."""
+@pytest.mark.parametrize("env_on,env_off", [
+    ({"SPAMM_OZ_EXOUT": "1", "SPAMM_OZ_EXPROD": "0"}, {"SPAMM_OZ_EXPROD": "0"}),
+    ({}, {"SPAMM_OZ_EXPROD": "0"}),
+])
+def test_product_exponents_from_the_epilogue_are_the_exponent_pass(tmp_path, env_on, env_off):
+    """The next multiply's K4z row exponents taken from the kernel that
+    produced the matrix -- the K4z epilogue (SPAMM_OZ_EXOUT=1), or, by default,
+    the column maxima of the K1 pass over X^2 and of the SP2 update over
+    2X - X^2 (SPAMM_OZ_EXPROD) -- instead of a separate exponent pass: bitwise
+    the SP2 with the pass, for Nb = 64 (K4z) and Nb = 32 (K4z32)."""
     import os
     import subprocess
     import sys
@@ -183,8 +189,8 @@ def test_product_exponents_from_the_epilogue_are_the_exponent_pass(tmp_path):
             "    np.save(sys.argv[1] + f'_{ci}.npy', sp.to_dense(p))\n")
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     outs = {}
-    for flag in ("0", "1"):
-        env = dict(os.environ, SPAMM_OZ_EXOUT=flag)
+    for flag, extra in (("0", env_off), ("1", env_on)):
+        env = dict(os.environ, **extra)
         base = str(tmp_path / f"p{flag}")
         subprocess.run([sys.executable, "-c", code % root, base], env=env, check=True)
         outs[flag] = [np.load(f"{base}_{ci}.npy") for ci in (3, 4)]

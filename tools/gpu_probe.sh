@@ -1,4 +1,2 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo EXIT $? >> gpurun_out/pytest_gpu.log
-timeout 600 python tools/env_ab.py 4 3 'SPAMM_LIB_PATH=ab/libspamm_head.so' '' > gpurun_out/ab.log 2>&1
-timeout 300 python tools/critical_path.py 4 > gpurun_out/critical_path.log 2>&1
+timeout 1200 python tools/env_ab.py 4 3 '' 'SPAMM_OZ_SIDE_PRIO=0' 'SPAMM_OZ_SPLIT_CTAS=2' 'SPAMM_OZ_SPLIT_CTAS=1' 'SPAMM_OZ_SIDE_PRIO=0 SPAMM_OZ_SPLIT_CTAS=2' 'SPAMM_OZ_SPLIT_CTAS=0' > gpurun_out/ab.log 2>&1
