@@ -654,8 +654,21 @@ cudaStream_t ozaki_side_stream() {  // one per (host thread, device)
   }
   return t;
 }
+// two reusable events per (host thread, device): [0] orders the pre-passes
+// after the operand's producer on the caller's stream, [1] marks them done
+cudaEvent_t* ozaki_events() {
+  thread_local cudaEvent_t evs[64][2] = {};
+  int dev = 0;
+  SPAMM_CK(cudaGetDevice(&dev));
+  cudaEvent_t* ev = evs[dev & 63];
+  for (int i = 0; i < 2; ++i)
+    if (!ev[i]) SPAMM_CK(cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming));
+  return ev;
+}
+// dep_recorded: ozaki_events()[0] was already recorded on s at the point the
+// pre-passes must follow (the caller queued more work on s since).
 void ozaki_ahead(const spamm_mat* a, const spamm_mat* b, int32_t kernel, cudaStream_t s,
-                 OzakiAhead& oz, bool defer_tr = false) {
+                 OzakiAhead& oz, bool defer_tr = false, bool dep_recorded = false) {
   // AUTO prepares ahead only when the slices are small next to HBM (they are
   // allocated before C, whose size the cull has not told yet); larger
   // operands take the post-cull path (leaf_dispatch), which tries the
@@ -677,15 +690,10 @@ void ozaki_ahead(const spamm_mat* a, const spamm_mat* b, int32_t kernel, cudaStr
     return;  // (same stream: no event needed)
   }
   cudaStream_t side = ozaki_side_stream();
-  // two reusable events per (host thread, device): each is waited on right
-  // after it is recorded, and a thread has one multiply in flight
-  thread_local cudaEvent_t evs[64][2] = {};
-  int dev = 0;
-  SPAMM_CK(cudaGetDevice(&dev));
-  cudaEvent_t* ev = evs[dev & 63];
-  for (int i = 0; i < 2; ++i)
-    if (!ev[i]) SPAMM_CK(cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming));
-  SPAMM_CK(cudaEventRecord(ev[0], s));
+  // (a thread has one multiply in flight: each event is waited on before it
+  // is recorded again)
+  cudaEvent_t* ev = ozaki_events();
+  if (!dep_recorded) SPAMM_CK(cudaEventRecord(ev[0], s));
   SPAMM_CK(cudaStreamWaitEvent(side, ev[0], 0));
   oz.ok = spamm::ozaki_prepare(a->m, b->m, a == b && a->m.sym, side, oz.op,
                                /*try_only=*/kernel == spamm::LEAF_AUTO, defer_tr);
@@ -708,16 +716,32 @@ void multiply_impl(const spamm_mat* a, const spamm_mat* b, double tau, int32_t k
     oz.ok = true;
     pre->ok = false;
     pre->ready = nullptr;
-  } else {
-    ozaki_ahead(a, b, kernel, s, oz);
   }
+  // The operand pre-passes (side stream) are queued right after the cull's
+  // count pass, so the cull's CTAs are resident before the passes fill the
+  // SMs (tier-walk culls: after the cull).
+  struct Ahead {
+    const spamm_mat *a, *b;
+    int32_t kernel;
+    cudaStream_t s;
+    OzakiAhead* oz;
+    bool done;
+    static void run(void* p) {
+      auto* h = static_cast<Ahead*>(p);
+      if (h->done) return;
+      h->done = true;
+      ozaki_ahead(h->a, h->b, h->kernel, h->s, *h->oz, false, /*dep_recorded=*/true);
+    }
+  } ahead{a, b, kernel, s, &oz, oz.ok};
+  if (!oz.ok) SPAMM_CK(cudaEventRecord(ozaki_events()[0], s));  // the operands are ready here
   spamm::CullResult r;
   // Symmetric SpAMM: X*X with X == X^T bitwise -> compute C_ij for i <= j only
   // and store C_ji = C_ij^T (bitwise what the full product yields).
   bool sym = g_sym_enabled && a == b && a->m.sym;
-  if (sym && !spamm::cull(a->m, b->m, tau, true, r, s, true, lo, hi, work))
+  if (sym && !spamm::cull(a->m, b->m, tau, true, r, s, true, lo, hi, work, &Ahead::run, &ahead))
     sym = false;  // ulp tie: full path
-  if (!sym) spamm::cull(a->m, b->m, tau, true, r, s, false, lo, hi, work);
+  if (!sym) spamm::cull(a->m, b->m, tau, true, r, s, false, lo, hi, work, &Ahead::run, &ahead);
+  Ahead::run(&ahead);
   spamm::htrace("mul_culled");
   C.n_native = a->m.n_native;
   C.nb = a->m.nb;

@@ -388,137 +388,179 @@ __device__ __forceinline__ int64_t cull_block_scan(int64_t v, int64_t& excl, int
 }
 
 // Count pass of the dense cull, one launch:
-//  * CTAs [n_tier, grid): the leaf tier, one warp per C position -- per node the
-//    packed count (cnt), the keep masks of its k-range (kmask, 32 k per word:
-//    the write pass compacts from them without re-testing), the LPT length
-//    histogram, the symmetric mirror check and the near-tau probes;
 //  * CTAs [0, n_tier): survivor counts and near-tau probes of every upper
-//    tier t < depth (full enumeration, 8^t triples; warp-reduced counts) --
-//    first in the grid, so they are in the first wave;
-//  * the last CTA to finish scans cnt into off (one pass over npos packed
-//    values), scans the histogram in place, and publishes the scalars the
-//    host needs to pinned memory (gather_sync's protocol) -- so the cull has
-//    one launch before its host sync instead of five.
-__global__ void __launch_bounds__(CULL_THREADS, 4)
+//    tier t < depth - 1 (full enumeration, 8^t triples; warp-reduced counts)
+//    -- first in the grid, so they are in the first wave;
+//  * CTAs [n_tier, grid): the leaf tier, DC_PPC = 32 consecutive Morton
+//    positions per CTA, one warp per tier-(depth-1) parent node and its four
+//    children.  The ancestor chains of the children's leaf triples are the
+//    parent's chains over K = k/2: the warp evaluates them once (and, on the
+//    symmetric path, its mirror's) into bit masks, so every leaf test is one
+//    product plus a mask bit -- the same predicates as keep_chain.  The
+//    parents' tested triples are exactly tier depth-1, so its survivor count
+//    and near-tau probes are taken there too.  Per position: the packed count
+//    (cnt), the keep masks of its k-range (kmask, 32 k per word: the write
+//    pass compacts from them without re-testing), the LPT length histogram,
+//    the symmetric mirror check and the near-tau probes; per CTA the
+//    exclusive prefix of its positions (lofs) and their total (ctasum);
+//  * the last CTA to finish scans the CTA totals (ctapre: off[q] =
+//    ctapre[q / DC_PPC] + lofs[q]), scans the histogram in place, and
+//    publishes the scalars the host needs to pinned memory (gather_sync's
+//    protocol) -- one launch before the cull's host sync.
+constexpr int DC_PPC = 32;  // positions per leaf CTA (8 warps x 4 children)
+__device__ __forceinline__ int64_t dc_off(const int64_t* __restrict__ ctapre,
+                                          const int64_t* __restrict__ lofs, int64_t q) {
+  return ctapre[q / DC_PPC] + lofs[q];
+}
+
+__global__ void __launch_bounds__(CULL_THREADS, 2)
     k_dense_count(int depth, const double* __restrict__ nA, const double* __restrict__ nB,
                   double tau, int sym, int64_t* __restrict__ cnt, uint32_t* __restrict__ kmask,
                   int* __restrict__ hist, int want_tasks, unsigned long long* __restrict__ aux,
                   TieBand tb, unsigned long long* __restrict__ near_tiers,
                   unsigned long long* __restrict__ margin, int64_t lo, int64_t hi,
                   int32_t* __restrict__ work, int n_tier, int tiers, unsigned* __restrict__ done,
-                  int64_t* __restrict__ off, ScalarSrc src, int n_src, int64_t* gvals,
-                  int64_t* gflag, int64_t seq) {
+                  int64_t* __restrict__ lofs, int64_t* __restrict__ ctasum,
+                  int64_t* __restrict__ ctapre, ScalarSrc src, int n_src, int64_t* gvals,
+                  int64_t* gflag, int64_t seq, unsigned long long* __restrict__ prof) {
+  // prof (SPAMM_CULL_PROF): %globaltimer per CTA [start, end] + last CTA phases
+  auto gtime = []() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+  };
+  if (prof && threadIdx.x == 0) prof[2 * blockIdx.x] = gtime();
   pdl_wait();
   __shared__ int64_t wsum[CULL_THREADS / 32 + 1];
+  __shared__ int64_t pcnt[DC_PPC];
   __shared__ unsigned long long cta_full;
   __shared__ unsigned int sc[DENSE_MAX_DEPTH];
   __shared__ bool last;
   const int64_t G = int64_t(1) << depth, npos = G * G;
   const int KW = (int)((G + 31) >> 5);
-  const int lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int n_leaf = (int)gridDim.x - n_tier;
   if ((int)blockIdx.x >= n_tier) {
-    const int n_leaf = (int)gridDim.x - n_tier;
+    const int64_t cta = blockIdx.x - n_tier;
     auto in_range = [&](int64_t q) { return hi < 0 || (q >= lo && q < hi); };
     unsigned long long* near = near_tiers + depth;
-    if (threadIdx.x == 0) cta_full = 0;
-    if (threadIdx.x == 0) sc[0] = 0;
+    if (threadIdx.x == 0) {
+      cta_full = 0;
+      sc[0] = 0;
+    }
+    if (threadIdx.x < DC_PPC) pcnt[threadIdx.x] = 0;
     __syncthreads();
     unsigned long long full = 0;
-    // one C position m: counts, keep masks, histogram, mirror check, probes.
-    // keep(k) / keep_m(k): the leaf triple (i,k,j) / its mirror (j,k,i).
+    // one C position m: counts, histogram, work; keep(k) / keep_m(k) are the
+    // leaf triple (i,k,j) / its mirror (j,k,i)
     auto finish_pos = [&](int64_t m, bool emitted, int64_t c) {
       if (lane == 0) {
-        cnt[m] = (emitted ? c + (c > 0 ? int64_t(1) << DT_NODE : 0) : 0) +
-                 (c > 0 ? int64_t(1) << DT_FULL : 0);
+        const int64_t v = (emitted ? c + (c > 0 ? int64_t(1) << DT_NODE : 0) : 0) +
+                          (c > 0 ? int64_t(1) << DT_FULL : 0);
+        cnt[m] = v;
+        pcnt[m - cta * DC_PPC] = v;
         if (work && emitted && c) work[m] = (int32_t)c;  // persistence load balancing input
         full += c;
         if (want_tasks && c && emitted) atomicAdd(hist + (G - c), 1);
       }
     };
     if (depth >= 2) {
-      // A CTA takes 8 consecutive Morton positions = the children of two
-      // tier-(depth-1) nodes.  The ancestor chains of all their leaf triples
-      // are those parents' chains over K = k/2: four warps evaluate them once
-      // (the two parents and, symmetric, their mirrors) into bit masks, and
-      // every leaf test is one product plus a mask bit -- the same predicates
-      // as keep_chain.  The parents' tested triples are exactly tier depth-1,
-      // so its survivor count and near-tau probes are taken here too.
-      __shared__ uint32_t pk[4][4];  // [own 0, own 1, mirror 0, mirror 1][K / 32], G/2 <= 128
-      const int warp = threadIdx.x >> 5;
-      const int64_t GH = G >> 1;
-      const int PW = (int)((GH + 31) >> 5);
-      const int64_t leaf_off = tier_offset(depth);
-      const int64_t ngroups = npos >> 3;
-      for (int64_t grp = blockIdx.x - n_tier; grp < ngroups; grp += n_leaf) {
-        if (warp < 4 && (warp < 2 || sym)) {
-          uint32_t I, J;
-          morton_decode((uint64_t)(grp * 2 + (warp & 1)), I, J);
-          if (warp >= 2) {
-            const uint32_t t_ = I;
-            I = J;
-            J = t_;
-          }
-          unsigned pc = 0;
-          for (int kw = 0; kw < PW; ++kw) {
-            const int64_t K = (int64_t)kw * 32 + lane;
-            const bool valid = K < GH;
-            const bool keep = valid && keep_chain(nA, nB, tau, depth - 1, I, K, J);
-            const unsigned bits = __ballot_sync(0xffffffffu, keep);
-            if (lane == 0) pk[warp][kw] = bits;
-            if (warp < 2 && tiers) {
-              if (valid)
-                chain_tie_probe(nA, nB, tb, depth - 1, I, K, J, near_tiers + depth - 1, margin);
-              pc += __popc(bits);
-            }
-          }
-          if (warp < 2 && tiers && lane == 0 && pc) atomicAdd(sc, pc);
-        }
-        __syncthreads();
-        {
-          const int64_t m = grp * 8 + warp;
-          uint32_t ui, uj;
-          morton_decode((uint64_t)m, ui, uj);
-          const int64_t i = ui, j = uj;
-          const bool owned = sym && i > j ? in_range((int64_t)morton_encode(uj, ui)) : in_range(m);
-          const bool emitted = owned && (!sym || i <= j);
-          if (!owned) {
-            if (lane == 0) cnt[m] = 0;
-          } else {
-            const uint32_t* pkm = pk[warp >> 2];
-            const uint32_t* pkx = pk[2 + (warp >> 2)];
-            const bool mirror = sym && i < j;
-            int64_t c = 0;
-            for (int64_t k0 = 0; k0 < G; k0 += 32) {
-              const int64_t k = k0 + lane;
-              const bool valid = k < G;
-              const bool par = valid && ((pkm[k >> 6] >> ((k >> 1) & 31)) & 1u);
-              const double pr =
-                  valid ? __dmul_rn(nA[leaf_off + i * G + k], nB[leaf_off + k * G + j]) : 0.0;
-              const bool keep = par && pr > tau;
-              const unsigned mask = __ballot_sync(0xffffffffu, keep);
-              if (valid && emitted && par && fabs(pr - tb.tau) <= tb.wide)
-                tie_probe(pr, tb, near, margin);
-              if (mirror) {
-                const bool parm = valid && ((pkx[k >> 6] >> ((k >> 1) & 31)) & 1u);
-                const double pm =
-                    valid ? __dmul_rn(nA[leaf_off + j * G + k], nB[leaf_off + k * G + i]) : 0.0;
-                const bool keep_m = parm && pm > tau;
-                if (valid && emitted && parm && fabs(pm - tb.tau) <= tb.wide)
-                  tie_probe(pm, tb, near, margin);
-                if (__any_sync(0xffffffffu, keep != keep_m) && lane == 0) atomicOr(aux + 1, 1ull);
-              }
-              if (want_tasks && emitted && lane == 0) kmask[m * KW + (k0 >> 5)] = mask;
-              c += __popc(mask);
-            }
-            finish_pos(m, emitted, c);
+      const int64_t P = cta * (DC_PPC / 4) + warp;  // this warp's tier-(depth-1) parent
+      if (P < npos / 4) {
+        const int64_t GH = G >> 1;
+        const int PW = (int)((GH + 31) >> 5);  // <= 4 (G <= 256)
+        const int64_t leaf_off = tier_offset(depth);
+        uint32_t I, J;
+        morton_decode((uint64_t)P, I, J);
+        uint32_t pk[4] = {0u, 0u, 0u, 0u}, px[4] = {0u, 0u, 0u, 0u};
+        unsigned pc = 0;
+#pragma unroll
+        for (int kw = 0; kw < 4; ++kw) {
+          if (kw >= PW) break;
+          const int64_t K = (int64_t)kw * 32 + lane;
+          const bool valid = K < GH;
+          const bool keep = valid && keep_chain(nA, nB, tau, depth - 1, I, K, J);
+          const bool keepx = sym && valid && keep_chain(nA, nB, tau, depth - 1, J, K, I);
+          pk[kw] = __ballot_sync(0xffffffffu, keep);
+          px[kw] = __ballot_sync(0xffffffffu, keepx);
+          if (tiers) {
+            if (valid)
+              chain_tie_probe(nA, nB, tb, depth - 1, I, K, J, near_tiers + depth - 1, margin);
+            pc += __popc(pk[kw]);
           }
         }
-        __syncthreads();  // pk is rewritten by the next group
+        if (tiers && lane == 0 && pc) atomicAdd(sc, pc);
+        // the four children (Morton order: ch = 2 (i & 1) + (j & 1)); leaf
+        // norms are loaded one 32-k chunk ahead (rows 2I, 2I+1 of nA, columns
+        // 2J, 2J+1 of nB, and the mirror's), all in flight together
+        bool owned[4], emitted[4];
+        int64_t c[4];
+#pragma unroll
+        for (int ch = 0; ch < 4; ++ch) {
+          const int64_t m = 4 * P + ch;
+          const int64_t i = 2 * (int64_t)I + (ch >> 1), j = 2 * (int64_t)J + (ch & 1);
+          owned[ch] = sym && i > j ? in_range((int64_t)morton_encode((uint32_t)j, (uint32_t)i))
+                                   : in_range(m);
+          emitted[ch] = owned[ch] && (!sym || i <= j);
+          c[ch] = 0;
+          if (!owned[ch] && lane == 0) cnt[m] = 0;
+        }
+        const int64_t i0 = 2 * (int64_t)I, j0 = 2 * (int64_t)J;
+        auto load = [&](int it, double (&v)[8]) {
+          const int64_t k = (int64_t)it * 32 + lane;
+          const bool valid = k < G;
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            v[u] = valid ? nA[leaf_off + (i0 + u) * G + k] : 0.0;      // A row 2I + u
+            v[2 + u] = valid ? nB[leaf_off + k * G + j0 + u] : 0.0;    // B column 2J + u
+            v[4 + u] = valid && sym ? nA[leaf_off + (j0 + u) * G + k] : 0.0;  // mirror A row
+            v[6 + u] = valid && sym ? nB[leaf_off + k * G + i0 + u] : 0.0;    // mirror B col
+          }
+        };
+        double cur[8], nxt[8];
+        load(0, cur);
+#pragma unroll
+        for (int it = 0; it < 8; ++it) {  // G <= 256: <= 8 chunks of 32 k
+          const int64_t k0 = (int64_t)it * 32;
+          if (k0 >= G) break;
+          if (k0 + 32 < G) load(it + 1, nxt);
+          const int64_t k = k0 + lane;
+          const bool valid = k < G;
+          const int w = it >> 1, sh = (int)(((k0 >> 1) + (lane >> 1)) & 31);
+          const bool par = valid && ((pk[w] >> sh) & 1u);
+          const bool parm = valid && ((px[w] >> sh) & 1u);
+#pragma unroll
+          for (int ch = 0; ch < 4; ++ch) {
+            if (!owned[ch]) continue;
+            const int ri = ch >> 1, cj = ch & 1;
+            const int64_t m = 4 * P + ch;
+            const bool mirror = sym && i0 + ri < j0 + cj;
+            const double pr = __dmul_rn(cur[ri], cur[2 + cj]);
+            const bool keep = par && pr > tau;
+            const unsigned mask = __ballot_sync(0xffffffffu, keep);
+            if (valid && emitted[ch] && par && fabs(pr - tb.tau) <= tb.wide)
+              tie_probe(pr, tb, near, margin);
+            if (mirror) {
+              const double pm = __dmul_rn(cur[4 + cj], cur[6 + ri]);
+              const bool keep_m = parm && pm > tau;
+              if (valid && emitted[ch] && parm && fabs(pm - tb.tau) <= tb.wide)
+                tie_probe(pm, tb, near, margin);
+              if (__any_sync(0xffffffffu, keep != keep_m) && lane == 0) atomicOr(aux + 1, 1ull);
+            }
+            if (want_tasks && emitted[ch] && lane == 0) kmask[m * KW + it] = mask;
+            c[ch] += __popc(mask);
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) cur[u] = nxt[u];
+        }
+#pragma unroll
+        for (int ch = 0; ch < 4; ++ch)
+          if (owned[ch]) finish_pos(4 * P + ch, emitted[ch], c[ch]);
       }
     } else {
-      const int64_t gw = ((int64_t)(blockIdx.x - n_tier) * blockDim.x + threadIdx.x) >> 5;
-      const int64_t nw = ((int64_t)n_leaf * blockDim.x) >> 5;
-      for (int64_t m = gw; m < npos; m += nw) {
+      // G <= 2: one CTA, one warp per position, full chains
+      const int64_t m = warp;
+      if (cta == 0 && m < npos) {
         uint32_t ui, uj;
         morton_decode((uint64_t)m, ui, uj);
         const int64_t i = ui, j = uj;
@@ -526,11 +568,8 @@ __global__ void __launch_bounds__(CULL_THREADS, 4)
         const bool emitted = owned && (!sym || i <= j);
         if (!owned) {
           if (lane == 0) cnt[m] = 0;
-          continue;
-        }
-        int64_t c = 0;
-        for (int64_t k0 = 0; k0 < G; k0 += 32) {
-          const int64_t k = k0 + lane;
+        } else {
+          const int64_t k = lane;
           const bool valid = k < G;
           const bool keep = valid && keep_chain(nA, nB, tau, depth, i, k, j);
           const unsigned mask = __ballot_sync(0xffffffffu, keep);
@@ -542,10 +581,9 @@ __global__ void __launch_bounds__(CULL_THREADS, 4)
             const bool keep_m = valid && keep_chain(nA, nB, tau, depth, j, k, i);
             if (__any_sync(0xffffffffu, keep != keep_m) && lane == 0) atomicOr(aux + 1, 1ull);
           }
-          if (want_tasks && emitted && lane == 0) kmask[m * KW + (k0 >> 5)] = mask;
-          c += __popc(mask);
+          if (want_tasks && emitted && lane == 0) kmask[m * KW] = mask;
+          finish_pos(m, emitted, __popc(mask));
         }
-        finish_pos(m, emitted, c);
       }
     }
     // full (reference) leaf count: one global atomic per CTA
@@ -554,6 +592,18 @@ __global__ void __launch_bounds__(CULL_THREADS, 4)
     if (threadIdx.x == 0 && cta_full) atomicAdd(aux, cta_full);
     if (threadIdx.x == 0 && depth >= 2 && sc[0])
       atomicAdd(aux + 4 + depth - 1, (unsigned long long)sc[0]);
+    if (warp == 0) {  // the CTA's positions: exclusive prefix and total
+      const int64_t v = pcnt[lane];
+      int64_t x = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int64_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      const int64_t q = cta * DC_PPC + lane;
+      if (q < npos) lofs[q] = x - v;
+      if (lane == 31) ctasum[cta] = x;
+    }
   } else {
     if (threadIdx.x < DENSE_MAX_DEPTH) sc[threadIdx.x] = 0;
     __syncthreads();
@@ -584,62 +634,97 @@ __global__ void __launch_bounds__(CULL_THREADS, 4)
     if (threadIdx.x < depth && sc[threadIdx.x])
       atomicAdd(aux + 4 + threadIdx.x, (unsigned long long)sc[threadIdx.x]);
   }
-  // ---- last CTA: scans and the host-visible scalars
+  // ---- last CTA: the CTA-total scan and the host-visible scalars
   __threadfence();
   __syncthreads();
+  if (prof && threadIdx.x == 0) prof[2 * blockIdx.x + 1] = gtime();
   if (threadIdx.x == 0) last = atomicAdd(done, 1u) == gridDim.x - 1;
   __syncthreads();
   if (!last) return;
   __threadfence();
-  constexpr int ITEMS = 16, TILE = CULL_THREADS * ITEMS;
-  int64_t carry = 0;
-  for (int64_t base = 0; base < npos; base += TILE) {
-    const int64_t b0 = base + (int64_t)threadIdx.x * ITEMS;
-    int64_t v[ITEMS];
-    int64_t sum = 0;
+  if (prof && threadIdx.x == 0) prof[2 * gridDim.x] = gtime();
+  // three independent jobs, one warp each, one barrier: warp 0 scans the CTA
+  // totals, warp 1 the LPT length histogram (in place), warp 2 gathers the
+  // other scalars; then one thread publishes
+  __shared__ int64_t total_sh;
+  if (warp == 0) {
+    int64_t carry = 0;
+    for (int64_t b0 = 0; b0 < n_leaf; b0 += 32 * 8) {
+      int64_t v[8];
+      int64_t sum = 0;
 #pragma unroll
-    for (int r = 0; r < ITEMS; ++r) {
-      v[r] = b0 + r < npos ? __ldcg(cnt + b0 + r) : 0;
-      sum += v[r];
-    }
-    int64_t excl;
-    const int64_t tot = cull_block_scan(sum, excl, wsum);
-    int64_t run = carry + excl;
+      for (int r = 0; r < 8; ++r) {
+        const int64_t b = b0 + lane * 8 + r;
+        v[r] = b < n_leaf ? __ldcg(ctasum + b) : 0;
+        sum += v[r];
+      }
+      int64_t x = sum;
 #pragma unroll
-    for (int r = 0; r < ITEMS; ++r) {
-      if (b0 + r < npos) off[b0 + r] = run;
-      run += v[r];
+      for (int o = 1; o < 32; o <<= 1) {
+        const int64_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      int64_t run = carry + x - sum;
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        const int64_t b = b0 + lane * 8 + r;
+        if (b < n_leaf) ctapre[b] = run;
+        run += v[r];
+      }
+      carry += __shfl_sync(0xffffffffu, x, 31);
     }
-    carry += tot;
-  }
-  if (threadIdx.x == 0) off[npos] = carry;
-  if (want_tasks) {  // LPT length histogram (G + 1 bins <= 257), in place
+    if (lane == 0) total_sh = carry;
+  } else if (warp == 1 && want_tasks) {  // G + 1 <= 257 bins
     const int nbins = (int)G + 1;
-    const int per = (nbins + CULL_THREADS - 1) / CULL_THREADS;
-    const int h0 = threadIdx.x * per;
-    int64_t loc = 0;
-    for (int b = h0; b < h0 + per && b < nbins; ++b) loc += __ldcg(hist + b);
-    int64_t excl;
-    cull_block_scan(loc, excl, wsum);
-    for (int b = h0; b < h0 + per && b < nbins; ++b) {
-      const int x = __ldcg(hist + b);
-      hist[b] = (int)excl;
-      excl += x;
+    int64_t carry = 0;
+    for (int b0 = 0; b0 < nbins; b0 += 32 * 9) {
+      int v[9];
+      int sum = 0;
+#pragma unroll
+      for (int r = 0; r < 9; ++r) {
+        const int b = b0 + lane * 9 + r;
+        v[r] = b < nbins ? __ldcg(hist + b) : 0;
+        sum += v[r];
+      }
+      int x = sum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      int64_t run = carry + x - sum;
+#pragma unroll
+      for (int r = 0; r < 9; ++r) {
+        const int b = b0 + lane * 9 + r;
+        if (b < nbins) hist[b] = (int)run;
+        run += v[r];
+      }
+      carry += __shfl_sync(0xffffffffu, x, 31);
     }
+  } else if (warp == 2) {
+    for (int i = lane; i < n_src; i += 32)
+      if (i != 2) gvals[i] = src.p[i] ? __ldcg(src.p[i]) : 0;
+    __threadfence_system();  // (pinned host memory: before the flag below)
   }
   __threadfence();
   __syncthreads();
-  if ((int)threadIdx.x < n_src) gvals[threadIdx.x] = src.p[threadIdx.x] ? __ldcg(src.p[threadIdx.x]) : 0;
-  __threadfence_system();
-  __syncthreads();
-  if (threadIdx.x == 0) *reinterpret_cast<volatile int64_t*>(gflag) = seq;
+  if (prof && threadIdx.x == 0) prof[2 * gridDim.x + 1] = gtime();
+  if (prof && threadIdx.x == 0) prof[2 * gridDim.x + 2] = gtime();
+  if (threadIdx.x == 0) {
+    aux[2] = total_sh;   // packed totals
+    gvals[2] = total_sh;
+    __threadfence_system();
+    *reinterpret_cast<volatile int64_t*>(gflag) = seq;
+  }
+  if (prof && threadIdx.x == 0) prof[2 * gridDim.x + 3] = gtime();
 }
 
 // Write pass: the task lists, C keys, storage / mirror slots and the LPT
 // order of the nodes, compacted from the count pass's keep masks (no norm is
 // read again).  One warp per C position.
 __global__ void __launch_bounds__(CULL_THREADS)
-    k_dense_write(int depth, int sym, const int64_t* __restrict__ off,
+    k_dense_write(int depth, int sym, const int64_t* __restrict__ cnt,
+                  const int64_t* __restrict__ lofs, const int64_t* __restrict__ ctapre,
                   const uint32_t* __restrict__ kmask, int* __restrict__ hist,
                   int32_t* __restrict__ ci_o, int32_t* __restrict__ cj_o,
                   int64_t* __restrict__ seg_o, int32_t* __restrict__ K_o,
@@ -657,8 +742,9 @@ __global__ void __launch_bounds__(CULL_THREADS)
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   if (gw == 0 && lane == 0) seg_o[Mn] = Vn;
   for (int64_t m = gw; m < npos; m += nw) {
-    const int64_t v = off[m], d = off[m + 1] - v;
+    const int64_t d = cnt[m];
     if ((d >> DT_FULL) == 0) continue;  // no C block here (or not owned)
+    const int64_t v = dc_off(ctapre, lofs, m);
     uint32_t ui, uj;
     morton_decode((uint64_t)m, ui, uj);
     const int64_t i = ui, j = uj;
@@ -675,7 +761,9 @@ __global__ void __launch_bounds__(CULL_THREADS)
       if (c_out) {
         c_out[node] = pfull;
         c_mirror[node] =
-            i < j ? off[(int64_t)morton_encode((uint32_t)j, (uint32_t)i)] >> DT_FULL : -1;
+            i < j ? dc_off(ctapre, lofs, (int64_t)morton_encode((uint32_t)j, (uint32_t)i)) >>
+                        DT_FULL
+                  : -1;
       }
       order[atomicAdd(hist + (G - ntask), 1)] = (int32_t)node;
     }
@@ -696,13 +784,14 @@ __global__ void __launch_bounds__(CULL_THREADS)
 
 bool dense_cull(const Mat& a, const Mat& b, double tau, bool want_tasks, CullResult& r,
                 cudaStream_t s, bool sym, int64_t lo = 0, int64_t hi = -1,
-                int32_t* work = nullptr) {
+                int32_t* work = nullptr, void (*after_launch)(void*) = nullptr,
+                void* after_ctx = nullptr) {
   const bool ranged = hi >= 0;
   const int depth = a.depth;
   const int64_t G = int64_t(1) << depth, npos = G * G;
   const int64_t KW = (G + 31) >> 5;
-  // aux[0]: full leaf survivors, [1]: mirror mismatch, [2]: packed scan
-  // total, [3]: count-pass CTAs done, [4 + t]: tier-t survivors (t < depth),
+  // aux[0]: full leaf survivors, [1]: mirror mismatch, [2]: packed totals,
+  // [3]: count-pass CTAs done, [4 + t]: tier-t survivors (t < depth),
   // [NEAR + t]: near-tau products of tier t (t <= depth), [MARGIN]: inverted
   // min relative margin.  [aux | LPT schedule: G + 1 length bins (bin 0 = G
   // tasks) + the K4 counter] zeroed by one memset; the schedule part is
@@ -715,41 +804,66 @@ bool dense_cull(const Mat& a, const Mat& b, double tau, bool want_tasks, CullRes
   char* zbuf = dmalloc<char>(aux_bytes + (G + 2) * sizeof(int), s);
   int64_t* aux = reinterpret_cast<int64_t*>(zbuf);
   int* sched = reinterpret_cast<int*>(zbuf + aux_bytes);
-  // cnt | off (npos + 1) | keep masks (npos x KW words)
-  char* cbuf = dmalloc<char>((2 * npos + 1) * sizeof(int64_t) +
+  const int n_leaf = (int)((npos + DC_PPC - 1) / DC_PPC);
+  // cnt | lofs (npos each) | ctasum | ctapre (n_leaf each) | keep masks (npos x KW words)
+  char* cbuf = dmalloc<char>((2 * npos + 2 * n_leaf) * sizeof(int64_t) +
                                  (want_tasks ? (size_t)npos * KW * sizeof(uint32_t) : 0), s);
   int64_t* cnt = reinterpret_cast<int64_t*>(cbuf);
-  int64_t* off = cnt + npos;
-  uint32_t* kmask = want_tasks ? reinterpret_cast<uint32_t*>(off + npos + 1) : nullptr;
+  int64_t* lofs = cnt + npos;
+  int64_t* ctasum = lofs + npos;
+  int64_t* ctapre = ctasum + n_leaf;
+  uint32_t* kmask = want_tasks ? reinterpret_cast<uint32_t*>(ctapre + n_leaf) : nullptr;
   SPAMM_CK(cudaMemsetAsync(zbuf, 0, aux_bytes + (G + 2) * sizeof(int), s));
   auto* u64 = reinterpret_cast<unsigned long long*>(aux);
-  // gathered: aux[0..4+depth) (aux[2] := the scan total), near[0..depth], margin
+  // gathered: aux[0..4+depth), near[0..depth], margin
   const int n_base = 4 + depth, n_near = depth + 1;
   const int nsc = n_base + n_near + 1;
   ScalarSrc src{};
   for (int i = 0; i < n_base; ++i) src.p[i] = aux + i;
-  src.p[2] = off + npos;
   src.p[3] = nullptr;
   for (int t = 0; t < n_near; ++t) src.p[n_base + t] = aux + NEAR + t;
   src.p[n_base + n_near] = aux + MARGIN;
-  // leaf CTAs: one per 8 positions (parent-mask form, depth >= 2), capped so
-  // the whole grid stays one wave
-  const int n_leaf = depth >= 2 ? (int)std::min<int64_t>(npos / 8, 148LL * 3)
-                                : grid_for(npos * 32, CULL_THREADS, 148LL * 3);
-  const int64_t tri = depth > 0 && !ranged
-                          ? (depth >= 2 ? ((int64_t(1) << (3 * (depth - 1))) - 1) / 7
-                                        : ((int64_t(1) << (3 * depth)) - 1) / 7)
-                          : 0;
+  const int64_t tri = depth >= 2 && !ranged ? ((int64_t(1) << (3 * (depth - 1))) - 1) / 7
+                      : depth == 1 && !ranged ? 1
+                                              : 0;
   const int n_tier = tri > 0 ? grid_for(tri, CULL_THREADS, 148LL) : 0;
   const PinnedGather pg = pinned_gather_begin();
-  launch_pdl(k_dense_count, n_leaf + n_tier, CULL_THREADS, 0, s, depth, a.norms, b.norms, tau,
+  static const bool cprof = getenv("SPAMM_CULL_PROF") != nullptr;
+  unsigned long long* prof = nullptr;
+  const int grid_c = n_leaf + n_tier;
+  if (cprof) prof = dmalloc<unsigned long long>(2 * grid_c + 4, s);
+  launch_pdl(k_dense_count, grid_c, CULL_THREADS, 0, s, depth, a.norms, b.norms, tau,
              sym ? 1 : 0, cnt, kmask, sched, want_tasks ? 1 : 0, u64, tb, u64 + NEAR,
              u64 + MARGIN, lo, hi, work, n_tier, ranged ? 0 : 1,
-             reinterpret_cast<unsigned*>(aux + 3), off, src,
-             nsc, pg.vals, pg.flag, pg.seq);
+             reinterpret_cast<unsigned*>(aux + 3), lofs, ctasum, ctapre, src, nsc, pg.vals,
+             pg.flag, pg.seq, prof);
   SPAMM_LAUNCH_CK();
+  if (after_launch) after_launch(after_ctx);
   int64_t h[64];
   pinned_gather_wait(h, nsc, pg, s);
+  if (prof) {  // diagnostics (syncs): CTA start spread, end spread, last-CTA phases
+    std::vector<unsigned long long> hp(2 * grid_c + 4);
+    SPAMM_CK(cudaMemcpyAsync(hp.data(), prof, hp.size() * 8, cudaMemcpyDeviceToHost, s));
+    SPAMM_CK(cudaStreamSynchronize(s));
+    unsigned long long s0 = ~0ull, s1 = 0, e0 = ~0ull, e1 = 0;
+    double tier_end = 0, leaf_end = 0;
+    for (int b = 0; b < grid_c; ++b) {
+      s0 = std::min(s0, hp[2 * b]);
+      s1 = std::max(s1, hp[2 * b]);
+      e0 = std::min(e0, hp[2 * b + 1]);
+      e1 = std::max(e1, hp[2 * b + 1]);
+    }
+    for (int b = 0; b < grid_c; ++b) {
+      const double d = (double)(hp[2 * b + 1] - s0) / 1e3;
+      if (b < n_tier) tier_end = std::max(tier_end, d); else leaf_end = std::max(leaf_end, d);
+    }
+    const unsigned long long* L = hp.data() + 2 * grid_c;
+    fprintf(stderr, "[cull] us from first CTA start: starts %.2f..%.2f ends %.2f..%.2f "
+            "(tiers %.2f leaf %.2f) last: begin %.2f scan %.2f hist %.2f published %.2f\n",
+            0.0, (s1 - s0) / 1e3, (e0 - s0) / 1e3, (e1 - s0) / 1e3, tier_end, leaf_end,
+            (L[0] - s0) / 1e3, (L[1] - s0) / 1e3, (L[2] - s0) / 1e3, (L[3] - s0) / 1e3);
+    dfree(prof, s);
+  }
   for (int t = 0; t < n_near; ++t) r.near[t] = h[n_base + t];
   r.margin = margin_from_bits(h[n_base + n_near]);
   if (h[1]) {  // leaf survivor set not mirror-symmetric (ulp tie): full cull
@@ -791,9 +905,9 @@ bool dense_cull(const Mat& a, const Mat& b, double tau, bool want_tasks, CullRes
   r.order = r.b_idx + V;
   r.sched = reinterpret_cast<int*>(zbuf);  // frees the aux + schedule buffer
   r.counter = sched + G + 1;
-  launch_pdl(k_dense_write, grid_for(npos * 32, CULL_THREADS, 148LL * 64), CULL_THREADS, 0, s,
-             depth, sym ? 1 : 0, off, kmask, sched, r.ci, r.cj, r.seg, r.k, a.slot, b.slot,
-             r.a_idx, r.b_idx, r.keys, r.c_out, r.c_mirror, r.order, M, V);
+  launch_pdl(k_dense_write, grid_for(npos * 32, CULL_THREADS, 148LL * 8), CULL_THREADS, 0, s,
+             depth, sym ? 1 : 0, cnt, lofs, ctapre, kmask, sched, r.ci, r.cj, r.seg, r.k,
+             a.slot, b.slot, r.a_idx, r.b_idx, r.keys, r.c_out, r.c_mirror, r.order, M, V);
   SPAMM_LAUNCH_CK();
   dfree(cbuf, s);
   r.n_c = M;
@@ -854,7 +968,8 @@ void CullResult::release(cudaStream_t s) {
 }
 
 bool cull(const Mat& a, const Mat& b, double tau, bool want_tasks, CullResult& r, cudaStream_t s,
-          bool sym, int64_t lo, int64_t hi, int32_t* work) {
+          bool sym, int64_t lo, int64_t hi, int32_t* work, void (*after_launch)(void*),
+          void* after_ctx) {
   // hi < 0: no shard filter (the whole C grid)
   const int depth = a.depth;
   r.visited.assign(depth + 1, 0);
@@ -864,7 +979,7 @@ bool cull(const Mat& a, const Mat& b, double tau, bool want_tasks, CullResult& r
   r.near.assign(depth + 1, 0);
   r.margin = INFINITY;
   if (g_dense_enabled && depth <= DENSE_MAX_DEPTH)
-    return dense_cull(a, b, tau, want_tasks, r, s, sym, lo, hi, work);
+    return dense_cull(a, b, tau, want_tasks, r, s, sym, lo, hi, work, after_launch, after_ctx);
 
   int32_t* ci = dmalloc<int32_t>(1, s);
   int32_t* cj = dmalloc<int32_t>(1, s);

@@ -214,8 +214,12 @@ struct CullResult {
 // block (persistence load balancing).
 void set_dense_cull(bool enabled);
 void set_near_tau_ulps(int k);
+// after_launch (dense cull only, may be null): called once the count pass is
+// queued, before the host waits on it (the SP2 loop queues the next operand's
+// K4z pre-passes there, behind the cull's CTAs).
 bool cull(const Mat& a, const Mat& b, double tau, bool want_tasks, CullResult& r, cudaStream_t s,
-          bool sym = false, int64_t lo = 0, int64_t hi = -1, int32_t* work = nullptr);
+          bool sym = false, int64_t lo = 0, int64_t hi = -1, int32_t* work = nullptr,
+          void (*after_launch)(void*) = nullptr, void* after_ctx = nullptr);
 
 // ---- leaf products ----
 // LEAF_DMMA_CPASYNC: the first-generation DMMA kernel (cp.async ring, one CTA
