@@ -255,10 +255,18 @@ struct SideQueue {
 thread_local SideQueue* g_side = nullptr;
 
 struct OzakiAhead;
+// Trace-first SP2 (sp2_solve_tf): the product is returned unfinalised (its
+// slot map from the cull), and one extra device scalar rides on the cull's
+// host sync.
+struct MulOpts {
+  bool defer_finalize = false;
+  const int64_t* extra_src = nullptr;
+  int64_t extra = 0;
+};
 void multiply_impl(const spamm_mat* a, const spamm_mat* b, double tau, int32_t kernel, bool timed,
                    cudaStream_t s, spamm::Mat& C, spamm_stats* stats, int64_t lo = 0,
                    int64_t hi = -1, int32_t* work = nullptr, bool defer_prune = false,
-                   spamm::IdemFuse idem = {}, OzakiAhead* pre = nullptr);
+                   spamm::IdemFuse idem = {}, OzakiAhead* pre = nullptr, MulOpts* mo = nullptr);
 
 }  // namespace
 
@@ -705,7 +713,8 @@ void ozaki_ahead(const spamm_mat* a, const spamm_mat* b, int32_t kernel, cudaStr
 
 void multiply_impl(const spamm_mat* a, const spamm_mat* b, double tau, int32_t kernel, bool timed,
                    cudaStream_t s, spamm::Mat& C, spamm_stats* stats, int64_t lo, int64_t hi,
-                   int32_t* work, bool defer_prune, spamm::IdemFuse idem, OzakiAhead* pre) {
+                   int32_t* work, bool defer_prune, spamm::IdemFuse idem, OzakiAhead* pre,
+                   MulOpts* mo) {
   EventTimer tm(timed, s);
   tm.mark(0);
   OzakiAhead oz;
@@ -738,9 +747,15 @@ void multiply_impl(const spamm_mat* a, const spamm_mat* b, double tau, int32_t k
   // Symmetric SpAMM: X*X with X == X^T bitwise -> compute C_ij for i <= j only
   // and store C_ji = C_ij^T (bitwise what the full product yields).
   bool sym = g_sym_enabled && a == b && a->m.sym;
-  if (sym && !spamm::cull(a->m, b->m, tau, true, r, s, true, lo, hi, work, &Ahead::run, &ahead))
+  const bool want_slot = mo && mo->defer_finalize;
+  const int64_t* extra_src = mo ? mo->extra_src : nullptr;
+  if (sym && !spamm::cull(a->m, b->m, tau, true, r, s, true, lo, hi, work, &Ahead::run, &ahead,
+                          want_slot, extra_src))
     sym = false;  // ulp tie: full path
-  if (!sym) spamm::cull(a->m, b->m, tau, true, r, s, false, lo, hi, work, &Ahead::run, &ahead);
+  if (!sym)
+    spamm::cull(a->m, b->m, tau, true, r, s, false, lo, hi, work, &Ahead::run, &ahead, want_slot,
+                extra_src);
+  if (mo) mo->extra = r.extra;
   Ahead::run(&ahead);
   spamm::htrace("mul_culled");
   C.n_native = a->m.n_native;
@@ -848,10 +863,18 @@ void multiply_impl(const spamm_mat* a, const spamm_mat* b, double tau, int32_t k
     spamm::dfree(c_out, s);
     spamm::dfree(c_mirror, s);
   }
-  if (idem.x)
+  if (mo && mo->defer_finalize) {
+    // (the caller finalises: the slot map from the cull stands in until then)
+    C.slot = r.c_slot;
+    r.c_slot = nullptr;
+    if (!C.slot) {  // (not a dense cull: no slot map to hand over)
+      throw spamm::CudaError("multiply: deferred finalisation needs the dense cull");
+    }
+  } else if (idem.x) {
     spamm::finalize(C, s, idem, defer_prune);
-  else
+  } else {
     spamm::finalize(C, s, nullptr, nullptr, defer_prune);
+  }
   if (ex_k1) C.oz_ex_row = ex_k1;
   C.sym = sym;
   spamm::htrace("mul_final");
@@ -1561,6 +1584,205 @@ int spamm_sp2_solve_ex(const spamm_mat* f, double n_occ, double tau, int32_t max
     ahead.ready = nullptr;
     ahead_for = nullptr;
   };
+  // Trace-first SP2 (round 2): the branch needs only tr(X^2), so it is taken
+  // right after the leaf products from the diagonal blocks, before any norm
+  // pass -- SQUARE then runs K1 on X^2 (norms, the residual ||X^2 - X||,
+  // the next K4z exponents), EXPAND runs the update alone (E, E's norms and
+  // the residual in one pass over X and X^2) and skips K1 on the discarded
+  // X^2.  The residual of step k is read at the next host sync (the cull of
+  // step k + 1); if it converged there, step k + 1's product is dropped and
+  // X_k is returned, exactly the reference loop's result (sp2.py:133-136).
+  // SPAMM_SP2_TF=0 keeps the loop below.
+  static const bool tf_on = [] {
+    const char* v = getenv("SPAMM_SP2_TF");
+    return !(v && strcmp(v, "0") == 0);
+  }();
+  const bool tf = tf_on && !spec_on && spamm::sp2_fused_supported(x->m.nb) &&
+                  spamm::idem_fusable(x->m) && spamm::dense_cull_applies(x->m.depth);
+  if (tf) {
+    // dev: [0] residual of the pending step, [1] tr X^2, [2] tr X, [3] union size
+    double* dev = spamm::dmalloc<double>(4, s);
+    struct DevFree {
+      double* p;
+      cudaStream_t s;
+      ~DevFree() { spamm::dfree(p, s); }
+    } dev_free{dev, s};
+    struct Pending {
+      bool has = false;
+      int k = 0;
+      bool square = true;
+      spamm_mat* prev_x = nullptr;  // X_k: the result if step k converged
+    } P;
+    const bool k4z_next = kernel == spamm::LEAF_OZAKI ||
+                          (kernel == spamm::LEAF_AUTO && auto_ozaki_enabled() &&
+                           auto_ozaki_for(x->m.nb));
+    const bool want_ex = k4z_next && oz_ex_from_producers() && spamm::ozaki_supported(x->m.nb);
+    auto accept_pending = [&]() {  // step P.k is not the last: X_{k+1} stands
+      rep->branch_history[rep->iterations] = P.square ? 0 : 1;
+      rep->iterations += 1;
+      pending_trace = true;
+      dead.v.push_back(P.prev_x);
+      P.has = false;
+      P.prev_x = nullptr;
+    };
+    auto converge_pending = [&]() {  // step P.k converged: X_k is the result
+      rep->converged = 1;
+      dead.v.push_back(x);
+      x = P.prev_x;
+      P.has = false;
+      P.prev_x = nullptr;
+    };
+    for (int it = 0; it < max_iter; ++it) {
+      auto* c = new spamm_mat();
+      spamm_stats st;
+      MulOpts mo;
+      mo.defer_finalize = true;
+      mo.extra_src = P.has ? reinterpret_cast<const int64_t*>(dev) : nullptr;
+      spamm::htrace("it_mul");
+      multiply_impl(x, x, tau, kernel, timed != 0, s, c->m, &st, 0, -1, nullptr, true,
+                    spamm::IdemFuse{}, ahead.ok && ahead_for == x ? &ahead : nullptr, &mo);
+      if (ahead.ok) drop_spec();  // (unused pre-passes)
+      spamm::htrace("it_mul_done");
+      if (P.has) {  // the residual of the previous step rode on this cull's sync
+        double r;
+        memcpy(&r, &mo.extra, sizeof(double));
+        rep->idem_history[P.k] = r;
+        if (r < fro_tol) {  // converged: this product is not part of the solve
+          c->m.release();
+          delete c;
+          converge_pending();
+          break;
+        }
+        accept_pending();
+      }
+      dead.flush();
+      // pre-branch: tr X^2 from its diagonal blocks, the key union of X and
+      // X^2 (the update's block set), tr X if not cached -- one host sync
+      if (!x->m.tr_valid && !x->m.tr_dev) {  // (not expected: X0 / X^2 / E carry theirs)
+        x->m.tr = spamm::trace(x->m, s);
+        x->m.tr_valid = true;
+      }
+      int64_t h[3];
+      spamm::UnionPrep prep = spamm::tf_prebranch(x->m, c->m, dev + 1,
+                                                  reinterpret_cast<int64_t*>(dev + 3), h, s);
+      spamm::htrace("fin_synced");
+      if (!x->m.tr_valid) {
+        memcpy(&x->m.tr, &h[1], sizeof(double));
+        x->m.tr_valid = true;
+      }
+      double tsq;
+      memcpy(&tsq, &h[0], sizeof(double));
+      c->m.tr = tsq;
+      c->m.tr_valid = true;
+      const double tx = x->m.tr;
+      const int64_t U = h[2];
+      // sp2.py:97-99: ties go to SQUARE.
+      const double tex = 2.0 * tx - tsq;
+      const bool square = std::fabs(tsq - n_occ) <= std::fabs(tex - n_occ);
+      const double bmargin = std::fabs(tex - n_occ) - std::fabs(tsq - n_occ);
+      resolve_timings();  // (after the host sync: the events are complete)
+      const int k = rep->n_multiplies++;
+      rep->leaf_products[k] = st.leaf_products;
+      rep->executed_products[k] = st.executed_products;
+      if (rep->ms_leaf) rep->ms_leaf[k] = st.ms_leaf;
+      if (rep->branch_margin) rep->branch_margin[k] = bmargin;
+      if (rep->near_tau) {
+        int64_t nt = 0;
+        for (int t = 0; t < st.n_tiers; ++t) nt += st.near_tau[t];
+        rep->near_tau[k] = nt;
+      }
+      if (rep->tau_margin) rep->tau_margin[k] = st.tau_margin;
+      if (rep->wall_seconds) {
+        const auto now = std::chrono::steady_clock::now();
+        rep->wall_seconds[k] = std::chrono::duration<double>(now - t_iter).count();
+        t_iter = now;
+      }
+      if (pending_trace) {  // tr of the last accepted X = this step's t_x
+        rep->trace_history[n_tr++] = tx;
+        pending_trace = false;
+      }
+      if (!want_idem &&
+          std::fabs(tsq - tx) < idem_tol && std::fabs(tx - n_occ) < 1e-6 * n_occ) {
+        rep->converged = 1;  // sp2.py:133-136: converged on X^2, the old X is returned
+        spamm::dfree(prep.keys, s);
+        spamm::dfree(prep.flags, s);
+        spamm::dfree(prep.off, s);
+        c->m.release();
+        delete c;
+        break;
+      }
+      spamm::htrace("fin_branch");
+      spamm_mat* next = nullptr;
+      if (square) {
+        spamm::dfree(prep.keys, s);
+        spamm::dfree(prep.flags, s);
+        spamm::dfree(prep.off, s);
+        spamm::IdemFuse f;
+        f.x = &x->m;
+        f.out = want_idem ? dev : nullptr;
+        int* ex = nullptr;
+        if (want_ex && want_idem && c->m.sym) {  // (taken by the fused K1 pass)
+          ex = spamm::dmalloc<int>(c->m.G * c->m.nb, s);
+          SPAMM_CK(cudaMemsetAsync(ex, 0x80, c->m.G * c->m.nb * sizeof(int), s));
+          f.ex_col = ex;
+        }
+        const double keep_tr = c->m.tr;
+        if (f.out)
+          spamm::finalize(c->m, s, f, /*defer=*/true);
+        else
+          spamm::finalize(c->m, s, nullptr, nullptr, /*defer=*/true);
+        c->m.tr = keep_tr;
+        c->m.tr_valid = true;
+        if (ex) c->m.oz_ex_row = ex;
+        next = c;
+      } else {
+        auto* e = new spamm_mat();
+        struct Hook {
+          spamm_mat* e;
+          int32_t kernel;
+          cudaStream_t s;
+          OzakiAhead* ahead;
+          static void run(void* p) {
+            auto* h = static_cast<Hook*>(p);
+            ozaki_ahead(h->e, h->e, h->kernel, h->s, *h->ahead, /*defer_tr=*/true);
+          }
+        } hook{e, kernel, s, &ahead};
+        double idem_unused = 0.0;
+        spamm::sp2_update_finish(x->m, c->m, prep, U, want_idem, /*expand=*/true, &idem_unused,
+                                 e->m, s, /*settle_now=*/false, &Hook::run, &hook, want_ex,
+                                 want_idem ? dev : nullptr);
+        e->m.stream = s;
+        e->m.sym = x->m.sym && c->m.sym;
+        if (ahead.ok) ahead_for = e;
+        dead.v.push_back(c);  // (X^2 is read by the update only: freed stream-ordered)
+        next = e;
+      }
+      spamm::htrace("fin_end");
+      if (want_idem) {
+        P.has = true;
+        P.k = k;
+        P.square = square;
+        P.prev_x = x;
+      } else {
+        rep->branch_history[rep->iterations] = square ? 0 : 1;
+        rep->iterations += 1;
+        pending_trace = true;
+        dead.v.push_back(x);
+      }
+      x = next;
+    }
+    if (P.has) {  // the last step's residual
+      int64_t bits = 0;
+      spamm::d2h_sync(&bits, reinterpret_cast<const int64_t*>(dev), 1, s);
+      double r;
+      memcpy(&r, &bits, sizeof(double));
+      rep->idem_history[P.k] = r;
+      if (r < fro_tol)
+        converge_pending();
+      else
+        accept_pending();
+    }
+  } else
   for (int it = 0; it < max_iter; ++it) {
     auto* c = new spamm_mat();
     spamm_stats st;

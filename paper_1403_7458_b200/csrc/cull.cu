@@ -732,7 +732,7 @@ __global__ void __launch_bounds__(CULL_THREADS)
                   int32_t* __restrict__ aidx, int32_t* __restrict__ bidx,
                   int64_t* __restrict__ keys, int64_t* __restrict__ c_out,
                   int64_t* __restrict__ c_mirror, int32_t* __restrict__ order, int64_t Mn,
-                  int64_t Vn) {
+                  int64_t Vn, int32_t* __restrict__ c_slot) {
   pdl_wait();
   const int64_t G = int64_t(1) << depth, npos = G * G;
   const int KW = (int)((G + 31) >> 5);
@@ -743,13 +743,19 @@ __global__ void __launch_bounds__(CULL_THREADS)
   if (gw == 0 && lane == 0) seg_o[Mn] = Vn;
   for (int64_t m = gw; m < npos; m += nw) {
     const int64_t d = cnt[m];
-    if ((d >> DT_FULL) == 0) continue;  // no C block here (or not owned)
-    const int64_t v = dc_off(ctapre, lofs, m);
     uint32_t ui, uj;
     morton_decode((uint64_t)m, ui, uj);
     const int64_t i = ui, j = uj;
+    if ((d >> DT_FULL) == 0) {  // no C block here (or not owned)
+      if (c_slot && lane == 0) c_slot[i * G + j] = -1;
+      continue;
+    }
+    const int64_t v = dc_off(ctapre, lofs, m);
     const int64_t pfull = v >> DT_FULL;
-    if (lane == 0) keys[pfull] = i * G + j;
+    if (lane == 0) {
+      keys[pfull] = i * G + j;
+      if (c_slot) c_slot[i * G + j] = (int32_t)pfull;
+    }
     if ((d & DT_TASK_MASK) == 0) continue;  // mirror of an emitted node
     const int64_t ntask = d & DT_TASK_MASK;
     const int64_t node = (v >> DT_NODE) & DT_IDX_MASK;
@@ -785,7 +791,8 @@ __global__ void __launch_bounds__(CULL_THREADS)
 bool dense_cull(const Mat& a, const Mat& b, double tau, bool want_tasks, CullResult& r,
                 cudaStream_t s, bool sym, int64_t lo = 0, int64_t hi = -1,
                 int32_t* work = nullptr, void (*after_launch)(void*) = nullptr,
-                void* after_ctx = nullptr) {
+                void* after_ctx = nullptr, bool want_slot = false,
+                const int64_t* extra_src = nullptr) {
   const bool ranged = hi >= 0;
   const int depth = a.depth;
   const int64_t G = int64_t(1) << depth, npos = G * G;
@@ -823,6 +830,8 @@ bool dense_cull(const Mat& a, const Mat& b, double tau, bool want_tasks, CullRes
   src.p[3] = nullptr;
   for (int t = 0; t < n_near; ++t) src.p[n_base + t] = aux + NEAR + t;
   src.p[n_base + n_near] = aux + MARGIN;
+  const int nsc_all = nsc + (extra_src ? 1 : 0);
+  if (extra_src) src.p[nsc] = extra_src;
   const int64_t tri = depth >= 2 && !ranged ? ((int64_t(1) << (3 * (depth - 1))) - 1) / 7
                       : depth == 1 && !ranged ? 1
                                               : 0;
@@ -835,12 +844,13 @@ bool dense_cull(const Mat& a, const Mat& b, double tau, bool want_tasks, CullRes
   launch_pdl(k_dense_count, grid_c, CULL_THREADS, 0, s, depth, a.norms, b.norms, tau,
              sym ? 1 : 0, cnt, kmask, sched, want_tasks ? 1 : 0, u64, tb, u64 + NEAR,
              u64 + MARGIN, lo, hi, work, n_tier, ranged ? 0 : 1,
-             reinterpret_cast<unsigned*>(aux + 3), lofs, ctasum, ctapre, src, nsc, pg.vals,
+             reinterpret_cast<unsigned*>(aux + 3), lofs, ctasum, ctapre, src, nsc_all, pg.vals,
              pg.flag, pg.seq, prof);
   SPAMM_LAUNCH_CK();
   if (after_launch) after_launch(after_ctx);
   int64_t h[64];
-  pinned_gather_wait(h, nsc, pg, s);
+  pinned_gather_wait(h, nsc_all, pg, s);
+  if (extra_src) r.extra = h[nsc];
   if (prof) {  // diagnostics (syncs): CTA start spread, end spread, last-CTA phases
     std::vector<unsigned long long> hp(2 * grid_c + 4);
     SPAMM_CK(cudaMemcpyAsync(hp.data(), prof, hp.size() * 8, cudaMemcpyDeviceToHost, s));
@@ -877,7 +887,9 @@ bool dense_cull(const Mat& a, const Mat& b, double tau, bool want_tasks, CullRes
   r.visited[depth] = h[0];
   for (int t = 0; t <= depth; ++t)
     r.culled[t] = ranged ? 0 : (t == 0 ? 1 : 8 * r.visited[t - 1]) - r.visited[t];
+  if (want_slot) r.c_slot = dmalloc<int32_t>(npos, s);
   if (!want_tasks || V == 0) {
+    if (r.c_slot) SPAMM_CK(cudaMemsetAsync(r.c_slot, 0xff, npos * sizeof(int32_t), s));
     dfree(cbuf, s);
     dfree(zbuf, s);
     if (!want_tasks) r.n_tasks = r.visited[depth];
@@ -907,7 +919,8 @@ bool dense_cull(const Mat& a, const Mat& b, double tau, bool want_tasks, CullRes
   r.counter = sched + G + 1;
   launch_pdl(k_dense_write, grid_for(npos * 32, CULL_THREADS, 148LL * 8), CULL_THREADS, 0, s,
              depth, sym ? 1 : 0, cnt, lofs, ctapre, kmask, sched, r.ci, r.cj, r.seg, r.k,
-             a.slot, b.slot, r.a_idx, r.b_idx, r.keys, r.c_out, r.c_mirror, r.order, M, V);
+             a.slot, b.slot, r.a_idx, r.b_idx, r.keys, r.c_out, r.c_mirror, r.order, M, V,
+             r.c_slot);
   SPAMM_LAUNCH_CK();
   dfree(cbuf, s);
   r.n_c = M;
@@ -933,6 +946,8 @@ void set_dense_cull(bool enabled) { g_dense_enabled = enabled; }
 void set_near_tau_ulps(int k) { g_near_ulps = k; }
 
 void CullResult::release(cudaStream_t s) {
+  dfree(c_slot, s);
+  c_slot = nullptr;
   if (block) {  // dense cull: every array but keys lives in one allocation
     dfree(block, s);
     dfree(sched, s);
@@ -967,9 +982,11 @@ void CullResult::release(cudaStream_t s) {
   n_c = n_tasks = 0;
 }
 
+bool dense_cull_applies(int depth) { return g_dense_enabled && depth <= DENSE_MAX_DEPTH; }
+
 bool cull(const Mat& a, const Mat& b, double tau, bool want_tasks, CullResult& r, cudaStream_t s,
           bool sym, int64_t lo, int64_t hi, int32_t* work, void (*after_launch)(void*),
-          void* after_ctx) {
+          void* after_ctx, bool want_slot, const int64_t* extra_src) {
   // hi < 0: no shard filter (the whole C grid)
   const int depth = a.depth;
   r.visited.assign(depth + 1, 0);
@@ -979,7 +996,8 @@ bool cull(const Mat& a, const Mat& b, double tau, bool want_tasks, CullResult& r
   r.near.assign(depth + 1, 0);
   r.margin = INFINITY;
   if (g_dense_enabled && depth <= DENSE_MAX_DEPTH)
-    return dense_cull(a, b, tau, want_tasks, r, s, sym, lo, hi, work, after_launch, after_ctx);
+    return dense_cull(a, b, tau, want_tasks, r, s, sym, lo, hi, work, after_launch, after_ctx,
+                      want_slot, extra_src);
 
   int32_t* ci = dmalloc<int32_t>(1, s);
   int32_t* cj = dmalloc<int32_t>(1, s);

@@ -131,13 +131,19 @@ struct UnionPrep {
   int64_t* keys = nullptr;  // small trees: union keys already compacted (G*G capacity)
 };
 UnionPrep sp2_union_prepare(const Mat& x, const Mat& x2, int64_t* u_dev, cudaStream_t s);
+// Trace-first SP2 (small trees): one launch + one host sync before the branch
+// rule -- host3 = {tr X^2 bits, tr X bits (from x.tr_dev; 0 if x.tr_valid),
+// union size}; returns the union keys (the update's block set).
+UnionPrep tf_prebranch(const Mat& x, const Mat& c, double* ctr_dev, int64_t* u_dev,
+                       int64_t* host3, cudaStream_t s);
 // after_update (EXPAND, may be null): called once E's blocks are queued on s
 // (the update kernel) and E's layout is set, before E's finalisation -- the
 // SP2 loop starts E's K4z operand passes there.
 void sp2_update_finish(const Mat& x, const Mat& x2, UnionPrep& prep, int64_t U, bool want_idem,
                        bool expand, double* idem_norm, Mat& e, cudaStream_t s,
                        bool settle_now = true, void (*after_update)(void*) = nullptr,
-                       void* after_ctx = nullptr, bool want_oz_ex = false);
+                       void* after_ctx = nullptr, bool want_oz_ex = false,
+                       double* idem_dev_out = nullptr);
 bool sp2_fused_supported(int nb);
 
 void scatter_slots(const int64_t* keys, int64_t m, int32_t* slot, cudaStream_t s);
@@ -201,6 +207,13 @@ struct CullResult {
   int* sched = nullptr;                  // hist/counter scratch (counter inside)
   void* block = nullptr;                 // dense cull: single allocation of the arrays
   int* counter = nullptr;
+  // dense cull, on request (want_slot): the C slot map (G*G int32, storage
+  // slot of each position's C block or -1) -- the product's slot map before
+  // its finalisation; ownership passes to the caller
+  int32_t* c_slot = nullptr;
+  // dense cull, on request (extra_src): one more device scalar read at the
+  // cull's host sync
+  int64_t extra = 0;
   void release(cudaStream_t s);
 };
 // Tiered culling (kernel.py:96-122).  want_tasks=false: census only
@@ -219,7 +232,9 @@ void set_near_tau_ulps(int k);
 // K4z pre-passes there, behind the cull's CTAs).
 bool cull(const Mat& a, const Mat& b, double tau, bool want_tasks, CullResult& r, cudaStream_t s,
           bool sym = false, int64_t lo = 0, int64_t hi = -1, int32_t* work = nullptr,
-          void (*after_launch)(void*) = nullptr, void* after_ctx = nullptr);
+          void (*after_launch)(void*) = nullptr, void* after_ctx = nullptr,
+          bool want_slot = false, const int64_t* extra_src = nullptr);
+bool dense_cull_applies(int depth);
 
 // ---- leaf products ----
 // LEAF_DMMA_CPASYNC: the first-generation DMMA kernel (cp.async ring, one CTA

@@ -1001,6 +1001,7 @@ void finalize_impl(Mat& m, cudaStream_t s, double* pre_n2, uint8_t* pre_nz, bool
       }
     }
     m.G = int64_t(1) << m.depth;
+    dfree(m.slot, s);  // (a provisional slot map from the cull, trace-first SP2)
     m.slot = dmalloc<int32_t>(m.G * m.G, s);
     const int64_t ps = pyramid_size(m.depth);
     m.norms = dmalloc<double>(ps, s);

@@ -75,6 +75,76 @@ __global__ void __launch_bounds__(1024)
   if (threadIdx.x == 0) *count = tot;
 }
 
+// Trace-first SP2 pre-branch pass (one CTA, one launch): tr X^2 from the
+// diagonal blocks of the unfinalised product (the cull's slot map) in the
+// trace()'s order (each block's diagonal summed in order, then the blocks in
+// order: k_trace_blocks + k_trace), the key union of X and X^2 with its size
+// (k_union_small), and tr X copied from its finalisation if not cached --
+// all published to pinned memory for the branch rule (gather_sync protocol).
+template <int PER>
+__global__ void __launch_bounds__(1024)
+    k_tf_prebranch(const int32_t* __restrict__ xslot, const int32_t* __restrict__ cslot,
+                   const double* __restrict__ cdata, int nb, int depth,
+                   int64_t* __restrict__ ukeys, const double* __restrict__ xtr_dev,
+                   double* __restrict__ ctr_out, int64_t* __restrict__ ucount_out,
+                   int64_t* gvals, int64_t* gflag, int64_t seq) {
+  pdl_wait();
+  __shared__ double partial[128];  // small trees: G <= 128
+  __shared__ unsigned char present[128];
+  const int64_t G = int64_t(1) << depth, npos = G * G;
+  const int64_t nb2 = (int64_t)nb * nb;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int64_t b = warp; b < G; b += 32) {
+    const int32_t sl = cslot[b * G + b];
+    if (lane == 0) present[b] = sl >= 0;
+    if (sl < 0) continue;
+    const double* x = cdata + (int64_t)sl * nb2;
+    double acc = 0.0;
+    for (int d0 = 0; d0 < nb; d0 += 32) {
+      const int d = d0 + lane;
+      const double v = d < nb ? x[(int64_t)d * nb + d] : 0.0;
+      const int cnt = min(32, nb - d0);
+      for (int i = 0; i < cnt; ++i) acc = __dadd_rn(acc, __shfl_sync(0xffffffffu, v, i));
+    }
+    if (lane == 0) partial[b] = acc;
+  }
+  // the key union (k_union_small)
+  int64_t key[PER];
+  int f[PER];
+#pragma unroll
+  for (int j = 0; j < PER; ++j) {
+    const int64_t p = (int64_t)threadIdx.x * PER + j;
+    uint32_t bi, bj;
+    morton_decode((uint64_t)p, bi, bj);
+    key[j] = (int64_t)bi * G + bj;
+  }
+  int fs = 0;
+#pragma unroll
+  for (int j = 0; j < PER; ++j) {
+    const bool ok = (int64_t)threadIdx.x * PER + j < npos;
+    const int32_t va = ok ? xslot[key[j]] : -1, vb = ok ? cslot[key[j]] : -1;
+    f[j] = (va >= 0) | (vb >= 0);
+    fs += f[j];
+  }
+  int64_t tot = 0;
+  int64_t o = cta_exclusive_scan(fs, &tot);  // (synchronises the CTA)
+#pragma unroll
+  for (int j = 0; j < PER; ++j)
+    if (f[j]) ukeys[o++] = key[j];
+  if (threadIdx.x == 0) {
+    double tr = 0.0;
+    for (int64_t b = 0; b < G; ++b)
+      if (present[b]) tr = __dadd_rn(tr, partial[b]);
+    *ctr_out = tr;
+    *ucount_out = tot;
+    gvals[0] = __double_as_longlong(tr);
+    gvals[1] = xtr_dev ? __double_as_longlong(*xtr_dev) : 0;
+    gvals[2] = tot;
+    __threadfence_system();
+    *reinterpret_cast<volatile int64_t*>(gflag) = seq;
+  }
+}
+
 // K6: BPW union blocks per warp; D = fl(fl(1*x2) + fl(-1*x)) (norm^2 only) and
 // E = fl(fl(2*x) + fl(-1*x2)) (written) with exactly the reference's rounding
 // (absent operand = no term); the D and E chains of all of them run on lanes
@@ -242,6 +312,26 @@ void sp2_update(const Mat& x, const Mat& x2, bool want_idem, bool expand, double
 
 bool sp2_fused_supported(int nb) { return nb == 32 || nb == 64; }
 
+UnionPrep tf_prebranch(const Mat& x, const Mat& c, double* ctr_dev, int64_t* u_dev,
+                       int64_t* host3, cudaStream_t s) {
+  UnionPrep p;
+  p.npos = x.G * x.G;
+  p.keys = dmalloc<int64_t>(p.npos, s);
+  const double* xtr = x.tr_valid ? nullptr : x.tr_dev;
+  const PinnedGather g = pinned_gather_begin();
+  if (x.depth <= 6)
+    launch_pdl(k_tf_prebranch<4>, 1, 1024, 0, s, (const int32_t*)x.slot, (const int32_t*)c.slot,
+               (const double*)c.data, x.nb, x.depth, p.keys, xtr, ctr_dev, u_dev, g.vals, g.flag,
+               g.seq);
+  else
+    launch_pdl(k_tf_prebranch<16>, 1, 1024, 0, s, (const int32_t*)x.slot,
+               (const int32_t*)c.slot, (const double*)c.data, x.nb, x.depth, p.keys, xtr,
+               ctr_dev, u_dev, g.vals, g.flag, g.seq);
+  SPAMM_LAUNCH_CK();
+  pinned_gather_wait(host3, 3, g, s);
+  return p;
+}
+
 UnionPrep sp2_union_prepare(const Mat& x, const Mat& x2, int64_t* u_dev, cudaStream_t s) {
   UnionPrep p;
   p.npos = x.G * x.G;
@@ -265,7 +355,8 @@ UnionPrep sp2_union_prepare(const Mat& x, const Mat& x2, int64_t* u_dev, cudaStr
 
 void sp2_update_finish(const Mat& x, const Mat& x2, UnionPrep& prep, int64_t U, bool want_idem,
                        bool expand, double* idem_norm, Mat& e, cudaStream_t s, bool settle_now,
-                       void (*after_update)(void*), void* after_ctx, bool want_oz_ex) {
+                       void (*after_update)(void*), void* after_ctx, bool want_oz_ex,
+                       double* idem_dev_out) {
   const int nb2 = x.nb * x.nb;
   int64_t* ukeys = prep.keys;
   prep.keys = nullptr;
@@ -323,6 +414,12 @@ void sp2_update_finish(const Mat& x, const Mat& x2, UnionPrep& prep, int64_t U, 
     finalize(e, s, nE2, nzE, /*defer=*/true, nE1);
   } else {
     dfree(ukeys, s);
+  }
+  // idem_dev_out (trace-first SP2): the residual stays on the device (read
+  // at a later sync), and so does E's kept count (settle_now = false)
+  if (want_idem && idem_dev_out) {
+    SPAMM_CK(cudaMemcpyAsync(idem_dev_out, pn, sizeof(double), cudaMemcpyDeviceToDevice, s));
+    want_idem = false;
   }
   // One host sync for the idempotency norm and E's kept-block count.
   const int64_t* kept_dev = expand && settle_now ? pending_kept(e) : nullptr;

@@ -164,3 +164,56 @@ def test_idempotency_and_energy_error():
     proj = v[:, :n_occ] @ v[:, :n_occ].T
     assert np.linalg.norm(sp.to_dense(p) - proj) < 1e-6
     assert of.n_native == h.shape[0]
+
+
+_TF_CODE = r"""
+import json, sys
+import numpy as np
+sys.path.insert(0, %r)
+import paper_1403_7458_b200 as sp
+from paper_1403_7458_b200.synth import CONFIGS, water_cluster
+out = {}
+for ci, crit, max_iter in ((3, "fro", 100), (4, "fro", 100), (4, "trace", 100), (4, "fro", 7),
+                           (4, "fro", 1), (3, "trace", 5)):
+    cfg = CONFIGS[ci]
+    h, n = water_cluster(cfg.n_mol, seed=0)
+    kw = dict(criterion=crit, max_iter=max_iter)
+    if crit == "trace":
+        kw["idem_tol"] = 1e-7
+    p, st = sp.sp2_solve(sp.build_from_dense(h, cfg.block_size), n, cfg.tau, **kw)
+    d = sp.to_dense(p)
+    key = f"{ci}-{crit}-{max_iter}"
+    np.save(sys.argv[1] + key + ".npy", d)
+    out[key] = dict(it=st.iteration, conv=st.converged, br=[str(b) for b in st.branch_history],
+                    tr=[float(v).hex() for v in st.trace_history],
+                    idem=[float(v).hex() for v in (st.idempotency_history or [])],
+                    leaf=[int(v) for v in st.leaf_products],
+                    bm=[float(v).hex() for v in st.branch_margins],
+                    near=[int(v) for v in st.near_tau_history])
+json.dump(out, open(sys.argv[1] + "meta.json", "w"))
+"""
+
+
+def test_trace_first_loop_bitwise_equals_previous_loop(tmp_path):
+    """The trace-first SP2 loop (branch from tr X^2 before any norm pass; the
+    residual read one host sync later, a converged step's next product
+    dropped) gives bitwise the same P, iteration count, branches, traces,
+    residuals and per-multiply survivor counts as the loop that finalises X^2
+    before the branch (SPAMM_SP2_TF=0) -- converged runs with both criteria
+    and runs cut by max_iter."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = {}
+    for flag in ("0", "1"):
+        base = str(tmp_path / f"tf{flag}_")
+        env = dict(os.environ, SPAMM_SP2_TF=flag)
+        subprocess.run([sys.executable, "-c", _TF_CODE % root, base], env=env, check=True,
+                       timeout=900)
+        res[flag] = (base, json.load(open(base + "meta.json")))
+    (b0, m0), (b1, m1) = res["0"], res["1"]
+    assert m0 == m1
+    for key in m0:
+        assert np.array_equal(np.load(b0 + key + ".npy"), np.load(b1 + key + ".npy")), key
