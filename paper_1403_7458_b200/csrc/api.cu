@@ -642,14 +642,15 @@ size_t device_total_bytes() {
   return total;
 }
 cudaStream_t ozaki_side_stream() {  // one per (host thread, device)
-  // The pre-passes are the longer of the two concurrent chains before K4z
-  // (exponents + split ~70 us vs the cull ~55 us at cfg4), so the side
-  // stream gets the highest priority: its CTAs are scheduled first and the
-  // latency-bound cull kernels fill the remaining slots
-  // (SPAMM_OZ_SIDE_PRIO=0: default priority).
+  // Default priority: since round 2 the exponent pass comes from the
+  // producers and the split is no longer the longer of the two chains before
+  // K4z, so the latency-bound cull / finalisation kernels on the caller's
+  // stream should not queue behind its CTAs (cfg4 solve, interleaved A/B:
+  // 30.36 vs 30.71 ms with the side stream at the highest priority, the
+  // round-1 setting; SPAMM_OZ_SIDE_PRIO=1 restores it).
   static const bool prio = [] {
     const char* v = getenv("SPAMM_OZ_SIDE_PRIO");
-    return !(v && strcmp(v, "0") == 0);
+    return v && strcmp(v, "1") == 0;
   }();
   thread_local cudaStream_t side[64] = {};
   int dev = 0;

@@ -86,23 +86,35 @@ inline void launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, 
 __host__ __device__ inline int64_t tier_offset(int t) { return ((int64_t(1) << (2 * t)) - 1) / 3; }
 __host__ __device__ inline int64_t pyramid_size(int depth) { return tier_offset(depth + 1); }
 
-// Morton code with the row bit above the column bit at each level.
+// Morton code with the row bit above the column bit at each level (bit b of
+// i -> bit 2b + 1, bit b of j -> bit 2b), by mask-and-shift bit spreading
+// (5 steps instead of a 32-iteration bit loop: these run per C position in
+// the cull, the union and the trace kernels).
+__host__ __device__ inline uint64_t morton_spread(uint32_t v) {
+  uint64_t x = v;
+  x = (x | (x << 16)) & 0x0000ffff0000ffffull;
+  x = (x | (x << 8)) & 0x00ff00ff00ff00ffull;
+  x = (x | (x << 4)) & 0x0f0f0f0f0f0f0f0full;
+  x = (x | (x << 2)) & 0x3333333333333333ull;
+  x = (x | (x << 1)) & 0x5555555555555555ull;
+  return x;
+}
+__host__ __device__ inline uint32_t morton_compact(uint64_t x) {
+  x &= 0x5555555555555555ull;
+  x = (x | (x >> 1)) & 0x3333333333333333ull;
+  x = (x | (x >> 2)) & 0x0f0f0f0f0f0f0f0full;
+  x = (x | (x >> 4)) & 0x00ff00ff00ff00ffull;
+  x = (x | (x >> 8)) & 0x0000ffff0000ffffull;
+  x = (x | (x >> 16)) & 0x00000000ffffffffull;
+  return (uint32_t)x;
+}
 __host__ __device__ inline uint64_t morton_encode(uint32_t i, uint32_t j) {
-  uint64_t m = 0;
-  for (int b = 0; b < 32; ++b) {
-    m |= (uint64_t)((i >> b) & 1u) << (2 * b + 1);
-    m |= (uint64_t)((j >> b) & 1u) << (2 * b);
-  }
-  return m;
+  return (morton_spread(i) << 1) | morton_spread(j);
 }
 
 __host__ __device__ inline void morton_decode(uint64_t m, uint32_t& i, uint32_t& j) {
-  i = 0;
-  j = 0;
-  for (int b = 0; b < 32; ++b) {
-    i |= (uint32_t)((m >> (2 * b + 1)) & 1u) << b;
-    j |= (uint32_t)((m >> (2 * b)) & 1u) << b;
-  }
+  i = morton_compact(m >> 1);
+  j = morton_compact(m);
 }
 
 inline int grid_for(int64_t n, int threads, int64_t cap = 148LL * 64) {

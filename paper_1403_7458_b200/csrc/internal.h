@@ -106,12 +106,20 @@ struct IdemFuse {
   // optional: C's K4z column exponents (G * nb, preset to OZ_EXP_NONE), taken
   // by the same pass -- the row exponents of a bitwise symmetric C
   int* ex_col = nullptr;
+  // optional: the residual's leaf norm^2 per block of m (already computed by
+  // the producer, caller-owned) -- with out, the D pyramid is built from it
+  const double* pre_dn2 = nullptr;
 };
 bool idem_fusable(const Mat& x);
 void finalize(Mat& m, cudaStream_t s, IdemFuse idem, bool defer);
 // pre_n1 (optional): sqrt of pre_n2, computed by the producer.
 void finalize(Mat& m, cudaStream_t s, double* pre_n2 = nullptr, uint8_t* pre_nz = nullptr,
               bool defer = false, double* pre_n1 = nullptr);
+// Deferred finalisation of a producer-normed matrix (the SP2 update's E) that
+// also reduces the residual's per-block leaf norm^2 (pre_dn2, one per block of
+// m) to its root norm, written to *out (device) -- one launch.
+void finalize_with_residual(Mat& m, cudaStream_t s, double* pre_n2, uint8_t* pre_nz,
+                            double* pre_n1, const double* pre_dn2, double* out);
 const int64_t* pending_kept(const Mat& m);  // device count, or nullptr if settled
 void settle(Mat& m, int64_t kept, cudaStream_t s);
 void settle_sync(Mat& m, cudaStream_t s);

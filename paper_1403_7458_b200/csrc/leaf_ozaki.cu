@@ -867,14 +867,14 @@ bool ozaki_prepare(const Mat& A, const Mat& B, bool sym_b, cudaStream_t s, Ozaki
     }
     return true;
   }
-  // CTAs per SM of the two passes: a full wave.  (Round 1 capped them at 3
-  // per SM to leave room for the cull kernels beside them; since round 2 the
-  // pre-passes are queued after the cull's count pass, whose CTAs are then
-  // already resident: full wave 30.7 vs 31.5 ms per cfg4 solve.)
-  // SPAMM_OZ_SPLIT_CTAS=n caps at n per SM (< 0: one CTA per block).
+  // CTAs per SM of the two passes: 2 of the 4 that fit, leaving room for the
+  // latency-bound cull and finalisation kernels that run beside them on the
+  // main stream (cfg4 solve, interleaved A/B: 2 per SM 30.7, a full wave
+  // 30.9, 1 per SM 31.3 ms).  SPAMM_OZ_SPLIT_CTAS=n caps at n per SM (0: a
+  // full wave; < 0: one CTA per block).
   static const int pass_ctas = [] {
     const char* v = getenv("SPAMM_OZ_SPLIT_CTAS");
-    return v ? atoi(v) : 0;
+    return v ? atoi(v) : 2;
   }();
   auto wave_of = [](int full) {
     return pass_ctas > 0 ? std::min(full, pass_ctas * multiprocessors())

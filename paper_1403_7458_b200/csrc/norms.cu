@@ -500,7 +500,7 @@ __global__ void __launch_bounds__(FS_THREADS)
         const int64_t p = (int64_t)(j0 + u) * FS_THREADS + tid;
         // X-only blocks: (-x)^2 == x^2 -- only blocks this matrix stores (a
         // multi-GPU shard carries the whole matrix's pyramid)
-        xv[u] = p < npos && (!xslot || xslot[p] >= 0) ? xleaf2[p] : 0.0;
+        xv[u] = xleaf2 && p < npos && (!xslot || xslot[p] >= 0) ? xleaf2[p] : 0.0;
       }
 #pragma unroll
       for (int u = 0; u < FS_BATCH; ++u) {
@@ -968,6 +968,15 @@ void finalize(Mat& m, cudaStream_t s, double* pre_n2, uint8_t* pre_nz, bool defe
   finalize_impl(m, s, pre_n2, pre_nz, defer, IdemFuse{}, pre_n1);
 }
 
+void finalize_with_residual(Mat& m, cudaStream_t s, double* pre_n2, uint8_t* pre_nz,
+                            double* pre_n1, const double* pre_dn2, double* out) {
+  if (!idem_fusable(m)) throw CudaError("finalize_with_residual: small trees, Nb 32 / 64");
+  IdemFuse f;
+  f.out = out;
+  f.pre_dn2 = pre_dn2;
+  finalize_impl(m, s, pre_n2, pre_nz, /*defer=*/true, f, pre_n1);
+}
+
 void finalize_impl(Mat& m, cudaStream_t s, double* pre_n2, uint8_t* pre_nz, bool defer,
                    IdemFuse idem, double* pre_n1) {
   m.stream = s;
@@ -978,6 +987,7 @@ void finalize_impl(Mat& m, cudaStream_t s, double* pre_n2, uint8_t* pre_nz, bool
     uint8_t* nz = pre_nz;
     double* n1 = pre_n1;
     double* dn2 = nullptr;
+    const double* dn2_in = idem.pre_dn2;  // (caller-owned)
     const bool multi = nb2 == 1024 || nb2 == 4096;
     if (m.nblocks > 0 && !n2) {
       n2 = dmalloc<double>(2 * m.nblocks, s);
@@ -1017,7 +1027,7 @@ void finalize_impl(Mat& m, cudaStream_t s, double* pre_n2, uint8_t* pre_nz, bool
         m.depth, m.nb, s, (const int64_t*)m.keys, (const double*)n2, (const double*)n1,
         (const uint8_t*)nz, m.nblocks, m.depth, kept, m.slot, m.norms, m.norms2,
         (const double*)m.data, m.nb, m.tr_dev, m.host_top, m.host_top ? m.top_t : -1,
-        (const double*)dn2,
+        dn2_in ? dn2_in : (const double*)dn2,
         idem.x ? (const double*)(idem.x->norms2 + tier_offset(m.depth)) : (const double*)nullptr,
         idem.out, idem.x ? (const int32_t*)idem.x->slot : (const int32_t*)nullptr, idem.ukeys,
         idem.ucount, idem.dleaf);

@@ -81,67 +81,150 @@ __global__ void __launch_bounds__(1024)
 // order: k_trace_blocks + k_trace), the key union of X and X^2 with its size
 // (k_union_small), and tr X copied from its finalisation if not cached --
 // all published to pinned memory for the branch rule (gather_sync protocol).
-template <int PER>
+template <int NB, int NPER>
 __global__ void __launch_bounds__(1024)
     k_tf_prebranch(const int32_t* __restrict__ xslot, const int32_t* __restrict__ cslot,
-                   const double* __restrict__ cdata, int nb, int depth,
+                   const double* __restrict__ cdata, int depth,
                    int64_t* __restrict__ ukeys, const double* __restrict__ xtr_dev,
                    double* __restrict__ ctr_out, int64_t* __restrict__ ucount_out,
-                   int64_t* gvals, int64_t* gflag, int64_t seq) {
+                   int64_t* gvals, int64_t* gflag, int64_t seq,
+                   unsigned long long* __restrict__ prof) {
+  auto gtime = []() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+  };
+  if (prof && threadIdx.x == 0) prof[0] = gtime();
   pdl_wait();
-  __shared__ double partial[128];  // small trees: G <= 128
-  __shared__ unsigned char present[128];
+  if (prof && threadIdx.x == 0) prof[1] = gtime();
+  __shared__ double partial[16 * NPER];  // G <= 16 NPER (small trees: G <= 128)
+  __shared__ unsigned char present[16 * NPER];
+  __shared__ int64_t wtot[17];
+  constexpr int NV = NB / 32;  // diagonal values per lane and block
   const int64_t G = int64_t(1) << depth, npos = G * G;
-  const int64_t nb2 = (int64_t)nb * nb;
+  constexpr int64_t nb2 = (int64_t)NB * NB;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int64_t b = warp; b < G; b += 32) {
-    const int32_t sl = cslot[b * G + b];
-    if (lane == 0) present[b] = sl >= 0;
-    if (sl < 0) continue;
-    const double* x = cdata + (int64_t)sl * nb2;
-    double acc = 0.0;
-    for (int d0 = 0; d0 < nb; d0 += 32) {
-      const int d = d0 + lane;
-      const double v = d < nb ? x[(int64_t)d * nb + d] : 0.0;
-      const int cnt = min(32, nb - d0);
-      for (int i = 0; i < cnt; ++i) acc = __dadd_rn(acc, __shfl_sync(0xffffffffu, v, i));
+  if (warp < 16) {
+    // warps 0-15: tr X^2.  Warp w takes blocks w, w + 16, ... (NPER); all slot
+    // and diagonal loads are issued before the (sequential, per block) sums,
+    // whose chains are interleaved across the warp's blocks.
+    const int64_t bl = warp + 16 * (int64_t)lane;
+    const int32_t sl_l = lane < NPER && bl < G ? cslot[bl * G + bl] : -1;
+    double v[NPER][NV];
+    int32_t sl[NPER];
+#pragma unroll
+    for (int q = 0; q < NPER; ++q) {
+      sl[q] = __shfl_sync(0xffffffffu, sl_l, q);
+      const bool ok = sl[q] >= 0;
+      const double* x = cdata + (int64_t)(ok ? sl[q] : 0) * nb2;
+#pragma unroll
+      for (int u = 0; u < NV; ++u) v[q][u] = ok ? x[(int64_t)(lane + 32 * u) * (NB + 1)] : 0.0;
     }
-    if (lane == 0) partial[b] = acc;
-  }
-  // the key union (k_union_small)
-  int64_t key[PER];
-  int f[PER];
+    if (prof && threadIdx.x == 0) prof[2] = gtime();
+    double acc[NPER];
 #pragma unroll
-  for (int j = 0; j < PER; ++j) {
-    const int64_t p = (int64_t)threadIdx.x * PER + j;
-    uint32_t bi, bj;
-    morton_decode((uint64_t)p, bi, bj);
-    key[j] = (int64_t)bi * G + bj;
-  }
-  int fs = 0;
+    for (int q = 0; q < NPER; ++q) acc[q] = 0.0;
+    // (fully unrolled: the shuffles run ahead of the dependent add chains)
 #pragma unroll
-  for (int j = 0; j < PER; ++j) {
-    const bool ok = (int64_t)threadIdx.x * PER + j < npos;
-    const int32_t va = ok ? xslot[key[j]] : -1, vb = ok ? cslot[key[j]] : -1;
-    f[j] = (va >= 0) | (vb >= 0);
-    fs += f[j];
-  }
-  int64_t tot = 0;
-  int64_t o = cta_exclusive_scan(fs, &tot);  // (synchronises the CTA)
+    for (int u = 0; u < NV; ++u)
 #pragma unroll
-  for (int j = 0; j < PER; ++j)
-    if (f[j]) ukeys[o++] = key[j];
+      for (int i = 0; i < 32; ++i) {
+#pragma unroll
+        for (int q = 0; q < NPER; ++q)
+          acc[q] = __dadd_rn(acc[q], __shfl_sync(0xffffffffu, v[q][u], i));
+      }
+    if (lane == 0) {
+#pragma unroll
+      for (int q = 0; q < NPER; ++q) {
+        const int64_t b = warp + 16 * q;
+        if (b < G) {
+          present[b] = sl[q] >= 0;
+          partial[b] = acc[q];
+        }
+      }
+    }
+    if (prof && threadIdx.x == 0) prof[3] = gtime();
+  } else {
+    // warps 16-31: the key union of X and X^2 (Morton order) and its size;
+    // thread t owns positions t NP .. t NP + NP - 1 (NP <= 32: a bit mask)
+    const int t = threadIdx.x - 512;
+    constexpr int NP = NPER * NPER / 2 > 0 ? NPER * NPER / 2 : 1;  // npos / 512, <= 32
+    constexpr int NB8 = NP < 8 ? NP : 8;  // slot loads in flight per batch
+    uint32_t fm = 0;
+#pragma unroll
+    for (int j0 = 0; j0 < NP; j0 += NB8) {
+      int32_t va[NB8], vb[NB8];
+#pragma unroll
+      for (int u = 0; u < NB8; ++u) {
+        const int64_t p = (int64_t)t * NP + j0 + u;
+        uint32_t bi, bj;
+        morton_decode((uint64_t)p, bi, bj);
+        const int64_t key = (int64_t)bi * G + bj;
+        const bool ok = p < npos;
+        va[u] = ok ? xslot[key] : -1;
+        vb[u] = ok ? cslot[key] : -1;
+      }
+#pragma unroll
+      for (int u = 0; u < NB8; ++u)
+        if ((va[u] >= 0) | (vb[u] >= 0)) fm |= 1u << (j0 + u);
+    }
+    const int fs = __popc(fm);
+    int64_t x = fs;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) wtot[warp - 16] = x;
+    asm volatile("bar.sync 1, 512;\n" ::: "memory");
+    if (warp == 16) {
+      const int64_t w = lane < 16 ? wtot[lane] : 0;
+      int64_t z = w;
+#pragma unroll
+      for (int o = 1; o < 16; o <<= 1) {
+        const int64_t y = __shfl_up_sync(0xffffffffu, z, o);
+        if (lane >= o) z += y;
+      }
+      if (lane < 16) wtot[lane] = z - w;
+      if (lane == 15) wtot[16] = z;
+    }
+    asm volatile("bar.sync 1, 512;\n" ::: "memory");
+    if (prof && threadIdx.x == 512) prof[4] = gtime();
+    int64_t o = wtot[warp - 16] + x - fs;
+    while (fm) {
+      const int j = __ffs(fm) - 1;
+      fm &= fm - 1;
+      uint32_t bi, bj;
+      morton_decode((uint64_t)((int64_t)t * NP + j), bi, bj);  // (NP as above)
+      ukeys[o++] = (int64_t)bi * G + bj;
+    }
+  }
+  __syncthreads();
+  if (prof && threadIdx.x == 0) prof[5] = gtime();
   if (threadIdx.x == 0) {
+    const int64_t tot = wtot[16];
     double tr = 0.0;
-    for (int64_t b = 0; b < G; ++b)
-      if (present[b]) tr = __dadd_rn(tr, partial[b]);
+    for (int64_t b0 = 0; b0 < G; b0 += 16) {  // (shared loads batched ahead of the chain)
+      double pv[16];
+      bool pp[16];
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        pp[u] = b0 + u < G && present[b0 + u];
+        pv[u] = pp[u] ? partial[b0 + u] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 16; ++u)
+        if (pp[u]) tr = __dadd_rn(tr, pv[u]);
+    }
     *ctr_out = tr;
     *ucount_out = tot;
     gvals[0] = __double_as_longlong(tr);
     gvals[1] = xtr_dev ? __double_as_longlong(*xtr_dev) : 0;
     gvals[2] = tot;
+    if (prof) prof[6] = gtime();
     __threadfence_system();
     *reinterpret_cast<volatile int64_t*>(gflag) = seq;
+    if (prof) prof[7] = gtime();
   }
 }
 
@@ -319,16 +402,37 @@ UnionPrep tf_prebranch(const Mat& x, const Mat& c, double* ctr_dev, int64_t* u_d
   p.keys = dmalloc<int64_t>(p.npos, s);
   const double* xtr = x.tr_valid ? nullptr : x.tr_dev;
   const PinnedGather g = pinned_gather_begin();
-  if (x.depth <= 6)
-    launch_pdl(k_tf_prebranch<4>, 1, 1024, 0, s, (const int32_t*)x.slot, (const int32_t*)c.slot,
-               (const double*)c.data, x.nb, x.depth, p.keys, xtr, ctr_dev, u_dev, g.vals, g.flag,
-               g.seq);
-  else
-    launch_pdl(k_tf_prebranch<16>, 1, 1024, 0, s, (const int32_t*)x.slot,
-               (const int32_t*)c.slot, (const double*)c.data, x.nb, x.depth, p.keys, xtr,
-               ctr_dev, u_dev, g.vals, g.flag, g.seq);
+  static const bool tprof = getenv("SPAMM_TF_PROF") != nullptr;
+  unsigned long long* prof = tprof ? dmalloc<unsigned long long>(8, s) : nullptr;
+  auto go = [&](auto kern) {
+    launch_pdl(kern, 1, 1024, 0, s, (const int32_t*)x.slot, (const int32_t*)c.slot,
+               (const double*)c.data, x.depth, p.keys, xtr, ctr_dev, u_dev, g.vals, g.flag, g.seq,
+               prof);
+  };
+  const int nper = x.G <= 16 ? 1 : (int)(x.G / 16);  // G <= 128
+  if (x.nb == 64) {
+    if (nper == 1) go(k_tf_prebranch<64, 1>);
+    else if (nper == 2) go(k_tf_prebranch<64, 2>);
+    else if (nper == 4) go(k_tf_prebranch<64, 4>);
+    else go(k_tf_prebranch<64, 8>);
+  } else {
+    if (nper == 1) go(k_tf_prebranch<32, 1>);
+    else if (nper == 2) go(k_tf_prebranch<32, 2>);
+    else if (nper == 4) go(k_tf_prebranch<32, 4>);
+    else go(k_tf_prebranch<32, 8>);
+  }
   SPAMM_LAUNCH_CK();
   pinned_gather_wait(host3, 3, g, s);
+  if (prof) {  // diagnostics (syncs)
+    unsigned long long h[8];
+    SPAMM_CK(cudaMemcpyAsync(h, prof, sizeof h, cudaMemcpyDeviceToHost, s));
+    SPAMM_CK(cudaStreamSynchronize(s));
+    fprintf(stderr, "[tf] us: waited %.2f loads %.2f chains %.2f union %.2f joined %.2f "
+            "summed %.2f published %.2f\n", (h[1] - h[0]) / 1e3, (h[2] - h[1]) / 1e3,
+            (h[3] - h[1]) / 1e3, (h[4] - h[1]) / 1e3, (h[5] - h[1]) / 1e3, (h[6] - h[1]) / 1e3,
+            (h[7] - h[1]) / 1e3);
+    dfree(prof, s);
+  }
   return p;
 }
 
@@ -392,7 +496,9 @@ void sp2_update_finish(const Mat& x, const Mat& x2, UnionPrep& prep, int64_t U, 
       launch_update<1024>(want_idem, expand, ukeys, U, x, x2, E, nD2, nE2, nzE, s, nE1, ex);
   }
   double* pn = nullptr;
-  if (want_idem) {
+  // (trace-first SP2: E's finalisation reduces the residual's leaf tier too)
+  const bool resid_in_fin = want_idem && expand && idem_dev_out && idem_fusable(x);
+  if (want_idem && !resid_in_fin) {
     const int64_t ps = pyramid_size(x.depth);
     pn = dmalloc<double>(2 * ps, s);
     build_pyramid(ukeys, nD2, U, x.depth, pn, pn + ps, s);
@@ -411,7 +517,13 @@ void sp2_update_finish(const Mat& x, const Mat& x2, UnionPrep& prep, int64_t U, 
     e.stream = s;
     e.oz_ex_row = ex;
     if (after_update) after_update(after_ctx);
-    finalize(e, s, nE2, nzE, /*defer=*/true, nE1);
+    if (resid_in_fin) {
+      finalize_with_residual(e, s, nE2, nzE, nE1, nD2, idem_dev_out);
+      dfree(nD2, s);
+      want_idem = false;  // (delivered on the device)
+    } else {
+      finalize(e, s, nE2, nzE, /*defer=*/true, nE1);
+    }
   } else {
     dfree(ukeys, s);
   }
