@@ -242,6 +242,12 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
                  int* __restrict__ next_block, int hint, long long* __restrict__ prof,
                  const double* __restrict__ Ad, const double* __restrict__ Bd,
                  int* __restrict__ ex_out) {
+  auto gtime = []() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return (long long)t;
+  };
+  if (PROF && threadIdx.x == 0) prof[blockIdx.x * 16 + 12] = gtime();
   pdl_wait();
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
@@ -412,6 +418,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
             o[1] = w_full;
             o[2] = w_tempty;
             o[3] = n_tasks;
+            o[13] = gtime();
           }
           break;
         }
@@ -496,6 +503,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
           prof[blockIdx.x * 16 + 6] = e_all;
           prof[blockIdx.x * 16 + 7] = n_blk;
           for (int i = 0; i < 4; ++i) prof[blockIdx.x * 16 + 8 + i] = e_ph[i];
+          prof[blockIdx.x * 16 + 14] = gtime();
         }
         break;
       }
@@ -1027,6 +1035,24 @@ void ozaki_launch(int64_t n_seg, const int64_t* seg, const Idx* a_idx, const Idx
       for (int i = 0; i < 12; ++i) a[i] += (double)h[b * 16 + i] / grid;
       lo = std::min(lo, (double)h[b * 16]);
       hi = std::max(hi, (double)h[b * 16]);
+    }
+    {  // globaltimer spans (us) from the first CTA's entry
+      long long e0 = LLONG_MAX, e1 = 0, m1 = 0, x1 = 0;
+      double mavg = 0;
+      for (int64_t b = 0; b < grid; ++b) {
+        e0 = std::min(e0, h[b * 16 + 12]);
+        e1 = std::max(e1, h[b * 16 + 12]);
+      }
+      for (int64_t b = 0; b < grid; ++b) {
+        m1 = std::max(m1, h[b * 16 + 13]);
+        x1 = std::max(x1, h[b * 16 + 14]);
+        mavg += (double)(h[b * 16 + 13] - e0) / grid;
+      }
+      fprintf(stderr,
+              "[k4z-span] us: entries 0..%.2f mma end avg %.2f max %.2f epilogue end max %.2f "
+              "(clock %.3f GHz)\n",
+              (e1 - e0) / 1e3, mavg / 1e3, (m1 - e0) / 1e3, (x1 - e0) / 1e3,
+              a[0] / (mavg > 0 ? mavg : 1));
     }
     fprintf(stderr,
             "[k4z] cycles %.0f (CTA min %.0f max %.0f): mma waits full %.0f tempty %.0f, "
