@@ -61,17 +61,29 @@ def fp64_peak():
 
 
 def i8_peak():
-    """Measured INT8 tcgen05 peak at K4z's MMA shape (tools/i8_peak.cu ->
-    profiles/i8_peak_r01.json, M = N = 128, K = 32); MEASURED_PEAKS.json has no
-    INT8 entry."""
-    path = os.path.join(ROOT, "profiles", "i8_peak_r01.json")
-    try:
-        with open(path) as f:
-            res = json.load(f)["results"]
-        best = max(r["tops"] for r in res if r.get("op") == "tcgen05_i8_m128n128k32")
-        return best, "measured tcgen05 kind::i8 M128 N128 peak, tools/i8_peak.cu (profiles/i8_peak_r01.json)"
-    except (OSError, KeyError, ValueError):
-        return 4500.0, "nominal B200 dense INT8 (fallback)"
+    """Measured INT8 tcgen05 peaks at K4z's MMA shape (tools/i8_peak.cu ->
+    profiles/i8_peak_r02.json, M = N = 128, K = 32); MEASURED_PEAKS.json has no
+    INT8 entry.  Returns (sustained, burst, source).  Burst: best of five short
+    launches with small-valued operands (no power limit met, 1,965 MHz).
+    Sustained: the same MMA stream back to back for 4 s with uniformly random
+    signed-byte operands -- the toggle rate of real digit slices -- which meets
+    the board's 1,000 W cap and settles at ~1.59 GHz; K4z is timed inside long
+    steps, so this is its roofline denominator (as bf16_tflops_sustained is
+    for the bf16 pipe in MEASURED_PEAKS.json)."""
+    for name in ("i8_peak_r02.json", "i8_peak_r01.json"):
+        path = os.path.join(ROOT, "profiles", name)
+        try:
+            with open(path) as f:
+                res = {r.get("op"): r["tops"] for r in json.load(f)["results"]}
+            burst = res["tcgen05_i8_m128n128k32"]
+            sus = res.get("tcgen05_i8_m128n128k32_random_sustained", burst)
+            kind = ("sustained, random signed-byte operands under the power cap"
+                    if "tcgen05_i8_m128n128k32_random_sustained" in res else "burst")
+            return sus, burst, (f"measured tcgen05 kind::i8 M128 N128 K32 peak ({kind}), "
+                                f"tools/i8_peak.cu (profiles/{name})")
+        except (OSError, KeyError, ValueError):
+            continue
+    return 4500.0, 4500.0, "nominal B200 dense INT8 (fallback)"
 
 
 # int8 ops K4z executes per leaf product: 20 tcgen05 MMAs of 128x128x32 at
@@ -345,7 +357,7 @@ def run_ours(args):
         k4 = leaf_kernel_in_use(cfg.block_size)
         if k4 == "ozaki":
             tasks = exec_flops / (2 * cfg.block_size ** 3)
-            ipeak, ipeak_src = i8_peak()
+            ipeak, ipeak_burst, ipeak_src = i8_peak()
             if leaf_ms > 0:
                 iach = tasks * k4z_ops_per_product(cfg.block_size) / (leaf_ms * 1e-3) / 1e12
                 inote = (f"executed leaf products x "
@@ -356,6 +368,7 @@ def run_ours(args):
                 inote = "int8 MMA ops of this rank / whole step time (lower bound)"
             roofline = {"bound": "tensor", "achieved": iach, "peak": ipeak, "unit": "TOPS",
                         "frac": iach / ipeak,
+                        "peak_burst": ipeak_burst, "frac_burst": iach / ipeak_burst,
                         "traffic": ncu_traffic("ozaki") if args.config == 4 else None,
                         "kernel": (f"k_leaf_ozaki{'' if cfg.block_size == 64 else '32'}<int> "
                                    "(K4z: FP64 leaf products as exact signed-8-bit digit "

@@ -3,6 +3,7 @@
 // The roofline denominator of the INT8-sliced leaf kernel K4z (MEASURED_PEAKS
 // has no INT8 entry).  Shapes: M = 128, N = 128 (K4z's) and 256, K = 32.
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o i8_peak i8_peak.cu
+#include <chrono>
 #include <cstdio>
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -15,14 +16,26 @@ __device__ __forceinline__ uint64_t desc(uint32_t addr) {  // K-major, no swizzl
          ((uint64_t)(256 >> 4) << 32) | (1ull << 46);
 }
 
+// Operand fill: small values (rnd = 0: few bits toggle) or uniformly random
+// signed bytes (rnd = 1: the toggle rate of real digit slices, which is what
+// decides whether a long run meets the board's power cap).
+__device__ __forceinline__ int8_t fill_byte(int i, int small, int rnd) {
+  if (!rnd) return (int8_t)small;
+  uint32_t h = (uint32_t)i * 2654435761u + blockIdx.x * 40503u;
+  h ^= h >> 15;
+  h *= 2246822519u;
+  h ^= h >> 13;
+  return (int8_t)(h & 0xff);
+}
+
 template <int N>
-__global__ void __launch_bounds__(128, 1) k_i8_peak(int iters, int* out) {
+__global__ void __launch_bounds__(128, 1) k_i8_peak(int iters, int* out, int rnd = 0) {
   __shared__ __align__(1024) int8_t a[128 * 32];
   __shared__ __align__(1024) int8_t b[256 * 32];
   __shared__ uint64_t bar;
   __shared__ uint32_t tslot;
-  for (int i = threadIdx.x; i < 128 * 32; i += 128) a[i] = (int8_t)(i & 7);
-  for (int i = threadIdx.x; i < 256 * 32; i += 128) b[i] = (int8_t)((i >> 3) & 7);
+  for (int i = threadIdx.x; i < 128 * 32; i += 128) a[i] = fill_byte(i, i & 7, rnd);
+  for (int i = threadIdx.x; i < 256 * 32; i += 128) b[i] = fill_byte(i + 4096, (i >> 3) & 7, rnd);
   const uint32_t bar_a = (uint32_t)__cvta_generic_to_shared(&bar);
   if (threadIdx.x == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(bar_a));
@@ -80,11 +93,11 @@ __device__ __forceinline__ uint64_t desc512(uint32_t addr) {
   return (uint64_t)((addr >> 4) & 0x3FFFu) | ((uint64_t)(128 >> 4) << 16) |
          ((uint64_t)(512 >> 4) << 32) | (1ull << 46);
 }
-__global__ void __launch_bounds__(128, 1) k_i8_k4z_pattern(int iters, int* out) {
+__global__ void __launch_bounds__(128, 1) k_i8_k4z_pattern(int iters, int* out, int rnd = 0) {
   extern __shared__ __align__(1024) int8_t sm[];
   __shared__ uint64_t bar;
   __shared__ uint32_t tslot;
-  for (int i = threadIdx.x; i < 65536; i += 128) sm[i] = (int8_t)((i * 7) & 15);
+  for (int i = threadIdx.x; i < 65536; i += 128) sm[i] = fill_byte(i, (i * 7) & 15, rnd);
   const uint32_t bar_a = (uint32_t)__cvta_generic_to_shared(&bar);
   if (threadIdx.x == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(bar_a));
@@ -187,6 +200,41 @@ int run(int sms, int clock_khz, int* out, bool last) {
   return 0;
 }
 
+// Sustained figure: the same kernels back to back for ~4 s (the power cap
+// settles within the first second), timed over the last ~2 s with events --
+// the roofline denominator for a kernel that runs inside a long step, as
+// MEASURED_PEAKS.json's bf16_tflops_sustained is for the bf16 pipe.
+template <class Launch>
+int run_sustained(const char* op, double ops_per_launch, Launch launch, bool last) {
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  const auto t0 = std::chrono::steady_clock::now();
+  auto secs = [&] {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  };
+  long n = 0, n_timed = 0;
+  bool timing = false;
+  while (secs() < 4.0) {
+    if (!timing && secs() >= 2.0) {
+      CK(cudaEventRecord(e0));
+      timing = true;
+    }
+    for (int i = 0; i < 8; ++i) launch();
+    n += 8;
+    if (timing) n_timed += 8;
+    if ((n & 63) == 0) CK(cudaStreamSynchronize(0));   // keep the queue short, the GPU never idle
+  }
+  CK(cudaEventRecord(e1));
+  CK(cudaEventSynchronize(e1));
+  CK(cudaGetLastError());
+  float ms;
+  CK(cudaEventElapsedTime(&ms, e0, e1));
+  printf("{\"op\": \"%s_sustained\", \"seconds\": %.2f, \"launches\": %ld, \"tops\": %.1f}%s\n",
+         op, ms * 1e-3, n_timed, ops_per_launch * n_timed / (ms * 1e-3) / 1e12, last ? "" : ",");
+  return 0;
+}
+
 int main() {
   int dev = 0, sms = 0, clk = 0;
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
@@ -196,7 +244,19 @@ int main() {
   printf("{\"sms\": %d, \"clock_khz\": %d, \"results\": [\n", sms, clk);
   if (run_pattern(sms, clk, out)) return 1;
   if (run<128>(sms, clk, out, false)) return 1;
-  if (run<256>(sms, clk, out, true)) return 1;
+  if (run<256>(sms, clk, out, false)) return 1;
+  if (run_sustained("tcgen05_i8_m128n128k32", 2.0 * 128 * 128 * 32 * 8.0 * 20000 * sms,
+                    [&] { k_i8_peak<128><<<sms, 128>>>(20000, out); }, false)) return 1;
+  if (run_sustained("tcgen05_i8_m128n256k32", 2.0 * 128 * 256 * 32 * 8.0 * 20000 * sms,
+                    [&] { k_i8_peak<256><<<sms, 128>>>(20000, out); }, false)) return 1;
+  if (run_sustained("k4z_task_pattern", 20.0 * 2 * 128 * 128 * 32 * 2000 * sms,
+                    [&] { k_i8_k4z_pattern<<<sms, 128, 65536 + 1024>>>(2000, out); }, false)) return 1;
+  if (run_sustained("tcgen05_i8_m128n128k32_random", 2.0 * 128 * 128 * 32 * 8.0 * 20000 * sms,
+                    [&] { k_i8_peak<128><<<sms, 128>>>(20000, out, 1); }, false)) return 1;
+  if (run_sustained("tcgen05_i8_m128n256k32_random", 2.0 * 128 * 256 * 32 * 8.0 * 20000 * sms,
+                    [&] { k_i8_peak<256><<<sms, 128>>>(20000, out, 1); }, false)) return 1;
+  if (run_sustained("k4z_task_pattern_random", 20.0 * 2 * 128 * 128 * 32 * 2000 * sms,
+                    [&] { k_i8_k4z_pattern<<<sms, 128, 65536 + 1024>>>(2000, out, 1); }, true)) return 1;
   printf("]}\n");
   return 0;
 }
