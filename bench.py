@@ -774,25 +774,40 @@ def run_cluster_sp2(args):
 def run_reference(args):
     """The reference's algorithm (oracle port, all host threads) on the same
     step as our arm: one complete SP2 solve of the workload per step."""
+    t_start = time.monotonic()
     ws, rank, _ = dist_env()
     if rank != 0:
         return
     cfg, h, n_occ = workload(args.config)
     threads = os.cpu_count() or 1
     oracle_warm(cfg, h, threads)   # warm-up: one multiply (a C kernel, nothing to JIT)
-    flops, secs, n_mult = 0, 0.0, 0
+    # Wall-clock guard: a complete solve takes ~40 s on 16 threads, 20 steps
+    # ~13 min.  On a slower or busier host the run stops after the last solve
+    # that fits SPAMM_REF_BUDGET_S (default 1,500 s from process start, under
+    # the driver's 1,800 s limit) and reports the steps it actually timed --
+    # a shorter line instead of a killed run with no line at all.
+    budget = float(os.environ.get("SPAMM_REF_BUDGET_S", "1500"))
+    flops, secs, n_mult, done = 0, 0.0, 0, 0
     for _ in range(args.steps):
         fl, dt, it, nm = oracle_solve(cfg, h, n_occ, threads)
         flops += fl
         secs += dt
         n_mult += nm
+        done += 1
         print(f"[reference] step {dt:.2f} s iterations {it}", file=sys.stderr, flush=True)
+        if done < args.steps and time.monotonic() - t_start + 1.25 * dt > budget:
+            print(f"[reference] wall-clock budget {budget:.0f} s: stopping after {done} of "
+                  f"{args.steps} steps", file=sys.stderr, flush=True)
+            break
     value = flops / secs / 1e9
-    sample = (f"one complete SP2 solve of {cfg.name} per step ({n_mult // args.steps} "
+    sample = (f"one complete SP2 solve of {cfg.name} per step ({n_mult // done} "
               f"multiplies), oracle port on {threads} host threads; warm-up: one multiply")
+    if done < args.steps:
+        sample += (f"; {done} of the {args.steps} requested steps timed "
+                   f"(wall-clock budget {budget:.0f} s)")
     out = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": secs * 1e3 / args.steps, "higher_is_better": True,
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": done,
+        "warmup": args.warmup, "ms_per_step": secs * 1e3 / done, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": config_dict(cfg, n_occ, args),
         "sp2_ms_per_iter": secs * 1e3 / max(n_mult, 1), "impl": "reference",
