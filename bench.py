@@ -104,13 +104,15 @@ def leaf_kernel_in_use(block_size: int) -> str:
 
 def ncu_traffic(kernel: str = "dmma"):
     """dram bytes per K4 launch from the committed ncu summary, if any."""
-    path = os.path.join(ROOT, "profiles",
-                        "ncu_leaf_ozaki_r01.json" if kernel == "ozaki" else "ncu_leaf_r01.json")
-    try:
-        with open(path) as f:
-            return json.load(f).get("dram_bytes_per_launch")
-    except (OSError, ValueError):
-        return None
+    names = ("k4z_dram_r02.json", "ncu_leaf_ozaki_r01.json") if kernel == "ozaki" \
+        else ("ncu_leaf_r01.json",)
+    for name in names:
+        try:
+            with open(os.path.join(ROOT, "profiles", name)) as f:
+                return json.load(f).get("dram_bytes_per_launch")
+        except (OSError, ValueError):
+            continue
+    return None
 
 
 class ClockSampler:

@@ -250,3 +250,28 @@ def test_elementwise_accuracy_envelope(nb):
     rel = err / np.maximum(np.abs(ref), 1e-300)
     big = np.abs(ref) >= np.exp2(-8) * scale
     assert big.any() and rel[big].max() < 1e-14
+
+
+@pytest.mark.parametrize("nb", [32, 64])
+@pytest.mark.parametrize("ea,eb", [(400, 400), (-490, -490), (500, -500), (-900, 900)])
+def test_power_of_two_scaling_commutes_exactly(nb, ea, eb):
+    """K4z's row / column scales are powers of two taken from the data, so
+    scaling A by 2^ea and B by 2^eb (no overflow; results compared where they
+    are normal numbers) must scale C by exactly 2^(ea + eb) -- bitwise -- and stay
+    within the north-star tolerance of the reference-order FP64 product at
+    magnitudes far from 1 (the epilogue's 2^k factor as one exact multiply, or
+    ldexp when k leaves the normal exponent range)."""
+    rng = np.random.default_rng(21)
+    n = 3 * nb + 5
+    a = rng.uniform(-1, 1, (n, n)) * np.exp(rng.uniform(-12, 0, (n, n)))
+    b = rng.uniform(-1, 1, (n, n)) * np.exp(rng.uniform(-12, 0, (n, n)))
+    c0 = sp.to_dense(sp.multiply(sp.build_from_dense(a, nb), sp.build_from_dense(b, nb), 0.0,
+                                 kernel="ozaki")[0])
+    sa, sb = np.ldexp(a, ea), np.ldexp(b, eb)
+    qa, qb = sp.build_from_dense(sa, nb), sp.build_from_dense(sb, nb)
+    c1 = sp.to_dense(sp.multiply(qa, qb, 0.0, kernel="ozaki")[0])
+    want = np.ldexp(c0, ea + eb)
+    normal = np.abs(want) >= np.ldexp(1.0, -1021)
+    assert normal.mean() > 0.99 and np.array_equal(c1[normal], want[normal])
+    ce = sp.to_dense(sp.multiply(qa, qb, 0.0, kernel="exact")[0])
+    assert np.isfinite(ce).all() and rel_fro(c1, ce) < REL_FRO_TOL
