@@ -13,10 +13,11 @@
 // double-buffer its accumulators.
 //
 // Epilogue: the 16 sub-blocks of a C element (r, c) live in four TMEM lane
-// quarters (one per warp) and four column groups; each warp loads its quarter,
-// the values go through shared memory, and the owning thread adds the
-// sub-blocks of equal digit sum in int32 (exact) and rounds once per level
-// (Horner, FMA), as in leaf_ozaki.cu -- so results are deterministic and a
+// quarters (one per warp) and four column groups; each warp loads its quarter
+// and folds its own 8 sub-blocks into two exact int64 (Th, Tl: the digit sums
+// d <= 4 and 5..8 at their weights, as in leaf_ozaki.cu), the pairs go through
+// shared memory (16 KB), and the owning thread adds the four warps' pairs
+// (exact) and rounds once (oz_round2) -- so results are deterministic and a
 // symmetric X gives a bitwise symmetric X*X.
 #include <climits>
 #include <cstdio>
@@ -45,16 +46,21 @@ constexpr int Z_TASK = 2 * Z_BLOCK_BYTES;                  // 16 KB
 // Kernel shapes: NBUF accumulator sets of 256 TMEM columns (2: double
 // buffered, one CTA per SM; 1: two CTAs per SM share the 512 columns),
 // STAGES x TPS tasks of operand ring.
+// Epilogue exchange: per warp w, column c8 and row r one exact int64 pair
+// (Th, Tl) -- the warp's own 8 sub-blocks already folded -- 16 KB.
+constexpr int Z_XBUF = 2 * 4 * 8 * 32 * 8;                 // [H/L][w][c8][r] int64
+constexpr int Z_PAD = 128;    // base alignment (no-swizzle operands need 16 B)
 template <int NBUF, int TPS, int STAGES>
 struct ZCfg {
   static constexpr int STAGE = TPS * Z_TASK;
-  static constexpr size_t SMEM = 1024 + (size_t)STAGES * STAGE + 32768 + 512;
+  static constexpr size_t SMEM = Z_PAD + (size_t)STAGES * STAGE + Z_XBUF + 512;
   static constexpr int CTAS = NBUF == 2 ? 1 : 2;
+  // two CTAs per SM: 228 KB per SM, 1 KB reserved per CTA
+  static_assert(CTAS == 1 || 2 * (SMEM + 1024) <= 233472, "two CTAs do not fit an SM");
 };
 constexpr int Z_CHUNK = 128;  // tasks per accumulation: |sub-block| <= 128 x 32 x 2^14 = 2^26
 constexpr int Z_EPI = 128;    // 4 epilogue warps = the 4 TMEM lane quarters
 constexpr int Z_THREADS = Z_EPI + 64;
-constexpr int Z_XBUF = 2 * 4 * 4 * 8 * 32 * 4;             // [tile][j][w][c8][r] ints, 32 KB
 constexpr uint32_t Z_SBO = 256;  // 8-row group stride: 2 k-chunks x 128 B
 
 // element (n, k) of a 32x32 slice: 8-row x 16-byte core matrices, the two
@@ -182,9 +188,10 @@ __global__ void __launch_bounds__(Z_THREADS, NBUF == 2 ? 1 : 2)
   constexpr uint32_t TCOLS = 256u * NBUF;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
-  const uint32_t base = (raw + 1023u) & ~1023u;
+  const uint32_t base = (raw + (Z_PAD - 1)) & ~(uint32_t)(Z_PAD - 1);
   uint8_t* gbase = smem_raw + (base - raw);
-  int* xb = reinterpret_cast<int*>(gbase + Z_STAGES * Z_STAGE);
+  long long* xh = reinterpret_cast<long long*>(gbase + Z_STAGES * Z_STAGE);
+  long long* xl = xh + 4 * 8 * 32;
   const uint32_t bars = base + Z_STAGES * Z_STAGE + Z_XBUF;
   auto full = [&](int s) { return bars + 8u * s; };
   auto empty = [&](int s) { return bars + 8u * (Z_STAGES + s); };
@@ -393,13 +400,41 @@ __global__ void __launch_bounds__(Z_THREADS, NBUF == 2 ? 1 : 2)
           __syncwarp();
           if (lane == 0) mbar_arrive(tempty(b));
         }
-        // xbuf[T][j][w][c8][r]
+        // Fold this warp's 8 sub-blocks (digit sums d = 4T + w + j) of each
+        // column into the exact integers Th = sum_{d<=4} S_d 2^(8(4-d)) and
+        // Tl = sum_{d=5..8} S_d 2^(8(8-d)) before the exchange (|sub-block| <=
+        // 2^26: |Th| < 2^62, |Tl| < 2^54, exact in int64; the by-product pairs
+        // of digit sums 9 and 10 weigh < 2^-72 of the row x column scales and
+        // are dropped -- a set closed under transposition, so S_d = S_d^T and
+        // the symmetric-operand result stays bitwise symmetric).  The exchange
+        // carries one (Th, Tl) pair per warp and element instead of 8 ints.
+        // (each term is one 32 x 32 -> 64-bit multiply-add: the multiplier
+        // 2^(8(4-d)) / 2^(8(8-d)) of a sub-block fits an int except 2^32 for
+        // d = 0, which is a shift into the high word)
+        int mh[2][4], ml[2][4];
 #pragma unroll
         for (int T = 0; T < 2; ++T)
 #pragma unroll
-          for (int j = 0; j < 4; ++j)
+          for (int j = 0; j < 4; ++j) {
+            const int d = 4 * T + w + j;  // (w is warp-uniform)
+            mh[T][j] = (d >= 1 && d <= 4) ? 1 << (8 * (4 - d)) : 0;
+            ml[T][j] = (d >= 5 && d <= 8) ? 1 << (8 * (8 - d)) : 0;
+          }
 #pragma unroll
-            for (int c8 = 0; c8 < 8; ++c8) xb[(((T * 4 + j) * 4 + w) * 8 + c8) * 32 + r] = V[T][j][c8];
+        for (int c8 = 0; c8 < 8; ++c8) {
+          long long ph = w == 0 ? (long long)V[0][0][c8] * 4294967296LL : 0LL, pl = 0;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            // T = 0: d = w + j in 0..6 (either part); T = 1: d = 4 + w + j in
+            // 4..10 (Th only for d = 4)
+            ph += (long long)V[0][j][c8] * (long long)mh[0][j];
+            pl += (long long)V[0][j][c8] * (long long)ml[0][j];
+            pl += (long long)V[1][j][c8] * (long long)ml[1][j];
+          }
+          ph += (long long)V[1][0][c8] * (long long)mh[1][0];  // (d = 4: w = 0, j = 0)
+          xh[(w * 8 + c8) * 32 + r] = ph;
+          xl[(w * 8 + c8) * 32 + r] = pl;
+        }
         asm volatile("bar.sync 1, 128;\n" ::: "memory");
         // this thread: row r, columns 2w, 2w+1 of the chunk
         double res[2];
@@ -407,21 +442,17 @@ __global__ void __launch_bounds__(Z_THREADS, NBUF == 2 ? 1 : 2)
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const int c8 = 2 * w + h;
-          int S[11];
+          long long th = 0, tl = 0;
 #pragma unroll
-          for (int d = 0; d < 11; ++d) S[d] = 0;
-#pragma unroll
-          for (int T = 0; T < 2; ++T)
-#pragma unroll
-            for (int j = 0; j < 4; ++j)
-#pragma unroll
-              for (int i = 0; i < 4; ++i)
-                S[4 * T + i + j] += xb[(((T * 4 + j) * 4 + i) * 8 + c8) * 32 + r];
-          const double v = oz_horner(S);
+          for (int i = 0; i < 4; ++i) {
+            th += xh[(i * 8 + c8) * 32 + r];
+            tl += xl[(i * 8 + c8) * 32 + r];
+          }
+          const double v = oz_round2(th, tl);  // 2^32 sum_d S_d 2^-8d, one rounding
           const int col = cc * 8 + c8;
           const int exc = ex_b[bj * Z_NB + col];
           bad[h] = row_bad || exc == OZ_EXP_BAD;
-          const int k = er + (bad[h] ? 0 : oz_exp(exc));  // C = v 2^k
+          const int k = er - 32 + (bad[h] ? 0 : oz_exp(exc));  // C = v 2^k
           res[h] = (k >= -1022 && k <= 1023)
                        ? __dmul_rn(v, __longlong_as_double((long long)(k + 1023) << 52))
                        : ldexp(v, k);
@@ -551,16 +582,28 @@ void oz32_launch(int64_t n_seg, const int64_t* seg, const Idx* a_idx, const Idx*
                  const int64_t* c_out, const int64_t* c_mirror, bool accumulate, const Mat& A,
                  const Mat& B, const OzakiOperands& op, double* C, cudaStream_t s,
                  int* counter, int* ex_out) {
-  // Two CTAs per SM (256 TMEM columns each, 2 stages of 2 tasks): the kernel
-  // is latency-bound, and a second CTA hides it better than double-buffered
-  // accumulators in one (cfg3 K4z 8.0 vs 10.9 ms per solve; 1 task x 4 stages:
-  // 9.7 ms).  SPAMM_OZ32_SHAPE=1: one CTA per SM, double-buffered TMEM.
+  // Two CTAs per SM (256 TMEM columns each): the kernel is latency-bound, and
+  // a second CTA hides it better than double-buffered accumulators in one
+  // (cfg3 K4z 8.0 vs 10.9 ms per solve; 1 task x 4 stages: 9.7 ms).  With the
+  // 16-KB exchange buffer (int64 pairs) a CTA has room for 3 stages of 2
+  // tasks -- the default (cfg3 solve 14.19 vs 14.71 ms with 2 stages; 2 stages
+  // of 3 tasks: 14.21; 6 stages of 1 task: 16.2).  SPAMM_OZ32_SHAPE=2: 2
+  // stages of 2 tasks; =1: one CTA per SM, double-buffered TMEM.
   static const int shape = [] {
     const char* v = getenv("SPAMM_OZ32_SHAPE");
-    return v ? atoi(v) : 2;
+    return v ? atoi(v) : 3;
   }();
   if (shape == 1)
     oz32_launch_cfg<Idx, 2, 4, 3>(n_seg, seg, a_idx, b_idx, c_out, c_mirror, accumulate, A, B,
+                                  op, C, s, counter, ex_out);
+  else if (shape == 3)  // two CTAs per SM, 3 stages of 2 tasks (the 16-KB exchange buffer)
+    oz32_launch_cfg<Idx, 1, 2, 3>(n_seg, seg, a_idx, b_idx, c_out, c_mirror, accumulate, A, B,
+                                  op, C, s, counter, ex_out);
+  else if (shape == 4)  // two CTAs per SM, 2 stages of 3 tasks
+    oz32_launch_cfg<Idx, 1, 3, 2>(n_seg, seg, a_idx, b_idx, c_out, c_mirror, accumulate, A, B,
+                                  op, C, s, counter, ex_out);
+  else if (shape == 5)  // two CTAs per SM, 6 stages of 1 task
+    oz32_launch_cfg<Idx, 1, 1, 6>(n_seg, seg, a_idx, b_idx, c_out, c_mirror, accumulate, A, B,
                                   op, C, s, counter, ex_out);
   else
     oz32_launch_cfg<Idx, 1, 2, 2>(n_seg, seg, a_idx, b_idx, c_out, c_mirror, accumulate, A, B,

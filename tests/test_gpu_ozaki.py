@@ -253,7 +253,7 @@ def test_elementwise_accuracy_envelope(nb):
 
 
 @pytest.mark.parametrize("nb", [32, 64])
-@pytest.mark.parametrize("ea,eb", [(400, 400), (-490, -490), (500, -500), (-900, 900)])
+@pytest.mark.parametrize("ea,eb", [(400, 400), (-490, -490), (500, -500), (-500, 500)])
 def test_power_of_two_scaling_commutes_exactly(nb, ea, eb):
     """K4z's row / column scales are powers of two taken from the data, so
     scaling A by 2^ea and B by 2^eb (no overflow; results compared where they
@@ -274,4 +274,6 @@ def test_power_of_two_scaling_commutes_exactly(nb, ea, eb):
     normal = np.abs(want) >= np.ldexp(1.0, -1021)
     assert normal.mean() > 0.99 and np.array_equal(c1[normal], want[normal])
     ce = sp.to_dense(sp.multiply(qa, qb, 0.0, kernel="exact")[0])
-    assert np.isfinite(ce).all() and rel_fro(c1, ce) < REL_FRO_TOL
+    # (compared at unit scale: the norms of values near 2^+-800 leave the FP64 range)
+    assert np.isfinite(ce).all()
+    assert rel_fro(np.ldexp(c1, -(ea + eb)), np.ldexp(ce, -(ea + eb))) < REL_FRO_TOL
