@@ -525,457 +525,6 @@ __global__ void __launch_bounds__(Z_THREADS, NBUF == 2 ? 1 : 2)
                  : "memory");
 }
 
-
-// ---------------------------------------------------------------- pair units
-// K4z32 streams 16 KB of slices per leaf product from L2 with no reuse, at
-// the L2 slices' throughput cap (DESIGN 4.3f).  Two C blocks of one block row
-// in adjacent columns, (i, j) and (i, j + 1), read the same A blocks X(i, k)
-// wherever both have a task for k, and their nodes are neighbours in the
-// Morton order of the task list.  A "pair unit" runs both in one CTA -- one
-// 256-column accumulator set each, all 512 TMEM columns -- over the union of
-// their k-lists: an entry is A(i, k) fetched once plus the B slices of
-// whichever of the two products exists (24 KB for two products instead of
-// 32 KB).  G <= 128 keeps a node's list within one accumulation chunk.
-//
-// k_oz32_units (one warp per node) marks the units and merges the lists:
-// unit[m] = 0 (second node of a pair: skipped by the claim loop), 1 (single),
-// 2 (pair head); pcount[m] = entries of the unit; bij[m] = (bi << 32) | bj;
-// ptasks[3 (seg[m] + e)] = A slot, B slot of node m, B slot of node m + 1
-// (-1: no such product), k ascending -- the entry space of a unit is the task
-// range of its nodes (the union is never longer).
-constexpr int ZP_ENTRY = 3 * Z_BLOCK_BYTES;  // 24 KB: A, B0, B1
-constexpr int ZP_TPS = 2;
-constexpr int ZP_STAGES = 4;
-constexpr int ZP_STAGE = ZP_TPS * ZP_ENTRY;  // 48 KB
-constexpr int ZP_EPI = 256;                  // two epilogue groups of 4 warps, one per C block
-constexpr int ZP_THREADS = ZP_EPI + 64;      // + producer (warp 8) + MMA issuer (warp 9)
-constexpr size_t ZP_SMEM = Z_PAD + (size_t)ZP_STAGES * ZP_STAGE + 2 * Z_XBUF + 512;
-static_assert(ZP_SMEM <= 232448, "pair kernel: shared memory");
-
-template <class Idx>
-__global__ void __launch_bounds__(256)
-    k_oz32_units(int64_t n_seg, const int64_t* __restrict__ seg, const Idx* __restrict__ a_idx,
-                 const Idx* __restrict__ b_idx, const int32_t* __restrict__ b_tr,
-                 const int64_t* __restrict__ a_keys, const int64_t* __restrict__ b_keys, int64_t G,
-                 int* __restrict__ unit, int* __restrict__ pcount, int64_t* __restrict__ bij,
-                 int32_t* __restrict__ ptasks) {
-  pdl_wait();
-  const int lane = threadIdx.x & 31;
-  const int64_t m = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
-  if (m >= n_seg) return;
-  auto key = [&](int64_t q) -> int64_t {
-    const int64_t t = seg[q];
-    return ((a_keys[a_idx[t]] / G) << 32) | (b_keys[b_idx[t]] % G);
-  };
-  auto mates = [&](int64_t k0, int64_t k1) {  // (i, j even), (i, j + 1)
-    return (k0 >> 32) == (k1 >> 32) && ((k0 & 1) == 0) && (k1 & 0xffffffffLL) == (k0 & 0xffffffffLL) + 1;
-  };
-  const int64_t km = key(m);
-  if (lane == 0) bij[m] = km;
-  if (m > 0 && mates(key(m - 1), km)) {
-    if (lane == 0) unit[m] = 0;
-    return;
-  }
-  const bool pair = m + 1 < n_seg && mates(km, key(m + 1));
-  const int64_t t0 = seg[m], t1 = seg[m + 1], t2 = pair ? seg[m + 2] : t1;
-  // presence bitmaps over k (G <= 128: four words)
-  unsigned p0[4] = {0u, 0u, 0u, 0u}, p1[4] = {0u, 0u, 0u, 0u};
-  for (int64_t t = t0 + lane; t < t2; t += 32) {
-    const int k = (int)(a_keys[a_idx[t]] % G);
-    if (t < t1) p0[k >> 5] |= 1u << (k & 31);
-    else p1[k >> 5] |= 1u << (k & 31);
-  }
-#pragma unroll
-  for (int w = 0; w < 4; ++w) {
-    p0[w] = __reduce_or_sync(0xffffffffu, p0[w]);
-    p1[w] = __reduce_or_sync(0xffffffffu, p1[w]);
-  }
-  int r0 = 0, r1 = 0, ru = 0;  // ranks of k = 32 w in list 0, list 1, the union
-  const unsigned lt = (1u << lane) - 1u;
-#pragma unroll
-  for (int w = 0; w < 4; ++w) {
-    const unsigned u = p0[w] | p1[w];
-    if ((u >> lane) & 1u) {
-      const bool h0 = (p0[w] >> lane) & 1u, h1 = (p1[w] >> lane) & 1u;
-      const int64_t i0 = h0 ? t0 + r0 + __popc(p0[w] & lt) : -1;
-      const int64_t i1 = h1 ? t1 + r1 + __popc(p1[w] & lt) : -1;
-      const int64_t e = t0 + ru + __popc(u & lt);
-      const int32_t ra = (int32_t)a_idx[h0 ? i0 : i1];
-      int32_t rb0 = -1, rb1 = -1;
-      if (h0) {
-        rb0 = (int32_t)b_idx[i0];
-        if (b_tr) rb0 = b_tr[rb0];
-      }
-      if (h1) {
-        rb1 = (int32_t)b_idx[i1];
-        if (b_tr) rb1 = b_tr[rb1];
-      }
-      ptasks[3 * e] = ra;
-      ptasks[3 * e + 1] = rb0;
-      ptasks[3 * e + 2] = rb1;
-    }
-    r0 += __popc(p0[w]);
-    r1 += __popc(p1[w]);
-    ru += __popc(u);
-  }
-  if (lane == 0) {
-    unit[m] = pair ? 2 : 1;
-    pcount[m] = ru;
-  }
-}
-
-template <class Idx>
-__global__ void __launch_bounds__(ZP_THREADS, 1)
-    k_leaf_ozaki32_pair(int64_t n_seg, const int64_t* __restrict__ seg,
-                        const Idx* __restrict__ a_idx, const Idx* __restrict__ b_idx,
-                        const int* __restrict__ unit, const int* __restrict__ pcount,
-                        const int64_t* __restrict__ bijs, const int32_t* __restrict__ ptasks,
-                        const int8_t* __restrict__ As, const int8_t* __restrict__ Bs,
-                        const int* __restrict__ ex_a, const int* __restrict__ ex_b,
-                        const int64_t* __restrict__ c_out, const int64_t* __restrict__ c_mirror,
-                        int accumulate, double* __restrict__ C, int* __restrict__ next_block,
-                        const double* __restrict__ Ad, const double* __restrict__ Bd,
-                        int* __restrict__ ex_out) {
-  pdl_wait();
-  extern __shared__ uint8_t smem_raw[];
-  const uint32_t raw = smem_u32(smem_raw);
-  const uint32_t base = (raw + (Z_PAD - 1)) & ~(uint32_t)(Z_PAD - 1);
-  uint8_t* gbase = smem_raw + (base - raw);
-  const uint32_t bars = base + ZP_STAGES * ZP_STAGE + 2 * Z_XBUF;
-  auto full = [&](int s) { return bars + 8u * s; };
-  auto empty = [&](int s) { return bars + 8u * (ZP_STAGES + s); };
-  const uint32_t tfull = bars + 8u * (2 * ZP_STAGES), tempty = tfull + 8u;
-  int64_t* meta = reinterpret_cast<int64_t*>(gbase + ZP_STAGES * ZP_STAGE + 2 * Z_XBUF +
-                                             8 * (2 * ZP_STAGES + 2));
-  int64_t* ring = meta + ZP_STAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ring + 2);
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < ZP_STAGES; ++s) {
-      mbar_init(full(s), 1);
-      mbar_init(empty(s), 1);
-    }
-    mbar_init(tfull, 2);            // MMA completion (commit) + the ring entry
-    mbar_init(tempty, ZP_EPI / 32);  // one arrive per epilogue warp (both groups, every unit)
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-  }
-  if (warp == 9) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(
-                     smem_u32(tmem_slot))
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
-  }
-  tc_before();
-  __syncthreads();
-  tc_after();
-  const uint32_t tbase = *tmem_slot;
-
-  if (warp == 8) {
-    // ---------------- producer: per entry A once + the B slices that exist ----------------
-    // stage meta: bit 0 first stage of the unit, 1 last, 2-3 entries, 4-7 the
-    // entries' (has B0, has B1) bits, 8 pair, 9 accumulate into C, unit << 12
-    int stage = 0;
-    uint32_t phase = 0;
-    for (;;) {
-      int64_t i = 0;
-      if (lane == 0) i = atomicAdd(next_block, 1);
-      i = __shfl_sync(0xffffffffu, i, 0);
-      if (i >= n_seg) break;
-      const int u = unit[i];
-      if (u == 0) continue;  // the second node of a pair: done with its head
-      const int cnt = pcount[i];
-      const int64_t e0 = seg[i];
-      for (int c0 = 0; c0 < cnt; c0 += 32) {
-        int32_t ra_l = 0, rb0_l = -1, rb1_l = -1;
-        if (c0 + lane < cnt) {
-          const int32_t* pt = ptasks + 3 * (e0 + c0 + lane);
-          ra_l = pt[0];
-          rb0_l = pt[1];
-          rb1_l = pt[2];
-        }
-        const int bc = cnt - c0 < 32 ? cnt - c0 : 32;
-        for (int q = 0; q < bc;) {
-          const int n_in = bc - q < ZP_TPS ? bc - q : ZP_TPS;
-          mbar_wait(empty(stage), phase ^ 1u);
-          uint32_t bytes = 0;
-          int64_t pres = 0;
-#pragma unroll
-          for (int x = 0; x < ZP_TPS; ++x) {
-            const int32_t b0 = __shfl_sync(0xffffffffu, rb0_l, (q + x) & 31);
-            const int32_t b1 = __shfl_sync(0xffffffffu, rb1_l, (q + x) & 31);
-            if (x < n_in) {
-              bytes += Z_BLOCK_BYTES * (1 + (b0 >= 0) + (b1 >= 0));
-              pres |= (int64_t)((b0 >= 0 ? 1 : 0) | (b1 >= 0 ? 2 : 0)) << (4 + 2 * x);
-            }
-          }
-          if (lane == 0) {
-            const bool first = c0 + q == 0, last = c0 + q + n_in == cnt;
-            meta[stage] = (i << 12) | (first ? 1 : 0) | (last ? 2 : 0) | ((int64_t)n_in << 2) | pres |
-                          (u == 2 ? 256 : 0) | (accumulate ? 512 : 0);
-            mbar_expect_tx(full(stage), bytes);
-          }
-#pragma unroll
-          for (int x = 0; x < ZP_TPS; ++x) {
-            const int32_t ra = __shfl_sync(0xffffffffu, ra_l, (q + x) & 31);
-            const int32_t b0 = __shfl_sync(0xffffffffu, rb0_l, (q + x) & 31);
-            const int32_t b1 = __shfl_sync(0xffffffffu, rb1_l, (q + x) & 31);
-            if (x < n_in && lane == 0) {
-              const uint32_t sa = base + stage * ZP_STAGE + x * ZP_ENTRY;
-              bulk_g2s(sa, As + (int64_t)ra * Z_BLOCK_BYTES, Z_BLOCK_BYTES, full(stage));
-              if (b0 >= 0)
-                bulk_g2s(sa + Z_BLOCK_BYTES, Bs + (int64_t)b0 * Z_BLOCK_BYTES, Z_BLOCK_BYTES,
-                         full(stage));
-              if (b1 >= 0)
-                bulk_g2s(sa + 2 * Z_BLOCK_BYTES, Bs + (int64_t)b1 * Z_BLOCK_BYTES, Z_BLOCK_BYTES,
-                         full(stage));
-            }
-          }
-          __syncwarp();
-          q += n_in;
-          if (++stage == ZP_STAGES) {
-            stage = 0;
-            phase ^= 1u;
-          }
-        }
-      }
-    }
-    mbar_wait(empty(stage), phase ^ 1u);
-    if (lane == 0) {
-      meta[stage] = -1;
-      mbar_arrive(full(stage));
-    }
-  } else if (warp == 9) {
-    // ---------------- MMA issuer: 3 MMAs per product that exists ----------------
-    if (lane == 0) {
-      const bool wide = z_wide_mma();
-      int stage = 0;
-      uint32_t phase = 0, tphase = 0;
-      bool opened[2] = {false, false};
-      for (;;) {
-        mbar_wait(full(stage), phase);
-        tc_after();
-        const int64_t md = meta[stage];
-        if (md < 0) {
-          mbar_wait(tempty, tphase ^ 1u);  // the epilogue is done with the last unit
-          ring[0] = -1;
-          mbar_arrive(tfull);
-          oz_commit(tfull);
-          break;
-        }
-        if (md & 1) {
-          mbar_wait(tempty, tphase ^ 1u);  // both accumulator sets drained
-          tphase ^= 1u;
-          tc_after();
-          opened[0] = opened[1] = false;
-        }
-        const int n_in = (int)((md >> 2) & 3);
-        for (int q = 0; q < n_in; ++q) {
-          const uint32_t sa = base + stage * ZP_STAGE + q * ZP_ENTRY;
-#pragma unroll
-          for (int b = 0; b < 2; ++b) {
-            if (!((md >> (4 + 2 * q + b)) & 1)) continue;
-            const uint32_t sb = sa + (1 + b) * Z_BLOCK_BYTES, d0 = tbase + 256u * b;
-            const uint32_t init = opened[b] ? 1u : 0u;
-            opened[b] = true;
-            if (wide) {  // anchors (0,0) and (0,4) as one N = 256 MMA over tiles 0-1
-              oz_mma(d0, oz_desc(sa, Z_SBO), oz_desc(sb, Z_SBO), init, OZ_IDESC_N256);
-            } else {
-              oz_mma(d0, oz_desc(sa, Z_SBO), oz_desc(sb, Z_SBO), init);
-              oz_mma(d0 + 128u, oz_desc(sa, Z_SBO), oz_desc(sb + 4 * Z_SLICE_BYTES, Z_SBO), init);
-            }
-            oz_mma(d0 + 128u, oz_desc(sa + 4 * Z_SLICE_BYTES, Z_SBO), oz_desc(sb, Z_SBO), 1u);
-          }
-        }
-        oz_commit(empty(stage));
-        if (md & 2) {
-          ring[0] = md;
-          mbar_arrive(tfull);
-          oz_commit(tfull);
-        }
-        if (++stage == ZP_STAGES) {
-          stage = 0;
-          phase ^= 1u;
-        }
-      }
-    }
-    __syncwarp();
-  } else {
-    // ---------------- epilogue: group g = warps 4g .. 4g+3 converts C block m + g ----------------
-    const int grp = warp >> 2, w = warp & 3, r = lane;
-    long long* xh = reinterpret_cast<long long*>(gbase + ZP_STAGES * ZP_STAGE + grp * Z_XBUF);
-    long long* xl = xh + 4 * 8 * 32;
-    const uint32_t lane_base = tbase + ((uint32_t)(w * 32) << 16);
-    uint32_t ephase = 0;
-    for (;;) {
-      mbar_wait(tfull, ephase);
-      ephase ^= 1u;
-      tc_after();
-      const int64_t md = ring[0];
-      if (md < 0) break;
-      if (grp == 1 && !(md & 256)) {  // a single node: nothing in the second accumulator set
-        tc_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(tempty);
-        continue;
-      }
-      const int64_t m = (md >> 12) + grp;
-      const bool cont = md & 512, seg_end = true;
-      const int64_t bij = bijs[m];
-      const int64_t bi = bij >> 32, bj = bij & 0xffffffffLL;
-      const int exr = ex_a[bi * Z_NB + r];
-      const bool row_bad = exr == OZ_EXP_BAD;
-      const int er = (row_bad ? 0 : oz_exp(exr)) - 14;
-      double* Cb = C + (c_out ? c_out[m] : m) * (int64_t)(Z_NB * Z_NB);
-      const int64_t mi = c_mirror ? c_mirror[m] : -1;
-      double* Cm = mi >= 0 ? C + mi * (int64_t)(Z_NB * Z_NB) : nullptr;
-      const uint32_t tb = lane_base + 256u * grp;
-      // ex_out: the product's own row exponents (see leaf_ozaki.cu)
-      const bool want_ex = ex_out != nullptr && seg_end;
-      unsigned rcode = 0u;
-      unsigned cc0 = 0, cc1 = 0, cc2 = 0, cc3 = 0;  // per chunk: 2 column codes (registers)
-#pragma unroll 1
-      for (int cc = 0; cc < 4; ++cc) {
-        int V[2][4][8];  // [tile][j][c8] of TMEM lane (w, r)
-#pragma unroll
-        for (int T = 0; T < 2; ++T)
-#pragma unroll
-          for (int j = 0; j < 4; ++j) tmem_ld8(tb + 128u * T + 32u * j + 8u * cc, V[T][j]);
-        tmem_wait8(V[0][0]);
-#pragma unroll
-        for (int T = 0; T < 2; ++T)
-#pragma unroll
-          for (int j = 0; j < 4; ++j)
-            if (T || j) tmem_keep8(V[T][j]);
-        if (cc == 3) {  // every TMEM read of this buffer is done: hand it back
-          tc_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(tempty);
-        }
-        // Fold this warp's 8 sub-blocks (digit sums d = 4T + w + j) of each
-        // column into the exact integers Th = sum_{d<=4} S_d 2^(8(4-d)) and
-        // Tl = sum_{d=5..8} S_d 2^(8(8-d)) before the exchange (|sub-block| <=
-        // 2^26: |Th| < 2^62, |Tl| < 2^54, exact in int64; the by-product pairs
-        // of digit sums 9 and 10 weigh < 2^-72 of the row x column scales and
-        // are dropped -- a set closed under transposition, so S_d = S_d^T and
-        // the symmetric-operand result stays bitwise symmetric).  The exchange
-        // carries one (Th, Tl) pair per warp and element instead of 8 ints.
-        // (each term is one 32 x 32 -> 64-bit multiply-add: the multiplier
-        // 2^(8(4-d)) / 2^(8(8-d)) of a sub-block fits an int except 2^32 for
-        // d = 0, which is a shift into the high word)
-        int mh[2][4], ml[2][4];
-#pragma unroll
-        for (int T = 0; T < 2; ++T)
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const int d = 4 * T + w + j;  // (w is warp-uniform)
-            mh[T][j] = (d >= 1 && d <= 4) ? 1 << (8 * (4 - d)) : 0;
-            ml[T][j] = (d >= 5 && d <= 8) ? 1 << (8 * (8 - d)) : 0;
-          }
-#pragma unroll
-        for (int c8 = 0; c8 < 8; ++c8) {
-          long long ph = w == 0 ? (long long)V[0][0][c8] * 4294967296LL : 0LL, pl = 0;
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            // T = 0: d = w + j in 0..6 (either part); T = 1: d = 4 + w + j in
-            // 4..10 (Th only for d = 4)
-            ph += (long long)V[0][j][c8] * (long long)mh[0][j];
-            pl += (long long)V[0][j][c8] * (long long)ml[0][j];
-            pl += (long long)V[1][j][c8] * (long long)ml[1][j];
-          }
-          ph += (long long)V[1][0][c8] * (long long)mh[1][0];  // (d = 4: w = 0, j = 0)
-          xh[(w * 8 + c8) * 32 + r] = ph;
-          xl[(w * 8 + c8) * 32 + r] = pl;
-        }
-        asm volatile("bar.sync %0, 128;\n" ::"r"(1 + grp) : "memory");
-        // this thread: row r, columns 2w, 2w+1 of the chunk
-        double res[2];
-        bool bad[2];
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int c8 = 2 * w + h;
-          long long th = 0, tl = 0;
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            th += xh[(i * 8 + c8) * 32 + r];
-            tl += xl[(i * 8 + c8) * 32 + r];
-          }
-          const double v = oz_round2(th, tl);  // 2^32 sum_d S_d 2^-8d, one rounding
-          const int col = cc * 8 + c8;
-          const int exc = ex_b[bj * Z_NB + col];
-          bad[h] = row_bad || exc == OZ_EXP_BAD;
-          const int k = er - 32 + (bad[h] ? 0 : oz_exp(exc));  // C = v 2^k
-          res[h] = (k >= -1022 && k <= 1023)
-                       ? __dmul_rn(v, __longlong_as_double((long long)(k + 1023) << 52))
-                       : ldexp(v, k);
-        }
-        const int col0 = cc * 8 + 2 * w;
-        double2* p = reinterpret_cast<double2*>(Cb + r * Z_NB + col0);
-        if (bad[0] || bad[1]) {
-          // non-finite operand entries: those elements are computed once, at
-          // the segment's end, in FP64 in the reference's order (leaf_ozaki.cu)
-          // (unrolled: a dynamically indexed res[] would live in local memory)
-          double* rp = Cb + r * Z_NB + col0;
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            double v = res[h];
-            if (bad[h]) {
-              if (!seg_end) continue;
-              v = oz_exact_elem<Idx>(accumulate ? rp[h] : 0.0, Ad, Bd, a_idx, b_idx, seg[m],
-                                     seg[m + 1], Z_NB, r, col0 + h);
-            } else if (cont) {
-              v = __dadd_rn(rp[h], v);
-            }
-            rp[h] = v;
-            if (Cm) Cm[(col0 + h) * Z_NB + r] = v;
-            res[h] = v;
-          }
-        } else {
-          if (cont) {
-            const double2 o = *p;
-            res[0] = __dadd_rn(o.x, res[0]);
-            res[1] = __dadd_rn(o.y, res[1]);
-          }
-          *p = make_double2(res[0], res[1]);
-          if (Cm) {
-            Cm[col0 * Z_NB + r] = res[0];
-            Cm[(col0 + 1) * Z_NB + r] = res[1];
-          }
-        }
-        if (want_ex) {
-          const unsigned k0 = oz_ex_code(res[0]), k1 = oz_ex_code(res[1]);
-          rcode = max(rcode, max(k0, k1));
-          const unsigned wk = k0 | (k1 << 16);
-          if (cc == 0) cc0 = wk;
-          else if (cc == 1) cc1 = wk;
-          else if (cc == 2) cc2 = wk;
-          else cc3 = wk;
-        }
-        asm volatile("bar.sync %0, 128;\n" ::"r"(1 + grp) : "memory");
-      }
-      if (want_ex) {
-        if (Cm) {  // lane = row: a column's max over the warp is the block's
-          const unsigned cw[4] = {cc0, cc1, cc2, cc3};
-#pragma unroll
-          for (int cc = 0; cc < 4; ++cc)
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              const unsigned mx = __reduce_max_sync(0xffffffffu, (cw[cc] >> (16 * h)) & 0xFFFFu);
-              if (lane == 0 && mx) atomicMax(ex_out + bj * Z_NB + cc * 8 + 2 * w + h, oz_ex_decode(mx));
-            }
-        }
-        if (rcode) atomicMax(ex_out + bi * Z_NB + r, oz_ex_decode(rcode));
-      }
-    }
-  }
-  tc_before();
-  __syncthreads();
-  tc_after();
-  if (warp == 9)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tbase)
-                 : "memory");
-}
-
 }  // namespace
 
 void oz32_operand_passes(const Mat& M, bool trans, int* ex, int8_t* out, cudaStream_t s,
@@ -1028,51 +577,6 @@ void oz32_launch_cfg(int64_t n_seg, const int64_t* seg, const Idx* a_idx, const 
   SPAMM_LAUNCH_CK();
 }
 
-
-// Pair units (see k_leaf_ozaki32_pair): SPAMM_OZ32_PAIR=0 keeps the per-node
-// kernel.  Needs G <= 128 (a node's list within one accumulation chunk, the
-// k bitmaps of k_oz32_units) and 32-bit task indices.
-template <class Idx>
-bool oz32_pair_launch(int64_t n_seg, const int64_t* seg, const Idx* a_idx, const Idx* b_idx,
-                      const int64_t* c_out, const int64_t* c_mirror, bool accumulate, const Mat& A,
-                      const Mat& B, const OzakiOperands& op, double* C, cudaStream_t s,
-                      int* counter, int* ex_out) {
-  static const bool on = [] {
-    const char* v = getenv("SPAMM_OZ32_PAIR");
-    return !(v && strcmp(v, "0") == 0);
-  }();
-  if (!on || op.G > 128 || sizeof(Idx) != 4) return false;
-  auto kern = k_leaf_ozaki32_pair<Idx>;
-  static std::once_flag once;
-  std::call_once(once, [&] {
-    SPAMM_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)ZP_SMEM));
-    const char* v = getenv("SPAMM_K4Z_HINT");
-    const int narrow = (v && (atoi(v) & 4)) ? 1 : 0;
-    SPAMM_CK(cudaMemcpyToSymbol(c_z_narrow, &narrow, sizeof(int)));
-  });
-  int* unit = dmalloc<int>(2 * n_seg, s);
-  int* pcount = unit + n_seg;
-  int64_t* bij = dmalloc<int64_t>(n_seg, s);
-  int32_t* ptasks = dmalloc<int32_t>((size_t)3 * n_seg * op.G, s);
-  launch_plain(k_oz32_units<Idx>, (unsigned)((n_seg + 7) / 8), 256, 0, s, n_seg, seg, a_idx, b_idx,
-               (const int32_t*)op.b_tr, (const int64_t*)A.keys, (const int64_t*)B.keys, op.G, unit,
-               pcount, bij, ptasks);
-  SPAMM_LAUNCH_CK();
-  int64_t grid = multiprocessors();
-  if (grid > n_seg) grid = n_seg;
-  launch_plain(kern, (unsigned)grid, ZP_THREADS, ZP_SMEM, s, n_seg, seg, a_idx, b_idx,
-               (const int*)unit, (const int*)pcount, (const int64_t*)bij, (const int32_t*)ptasks,
-               (const int8_t*)op.as, (const int8_t*)op.bs, (const int*)op.ex_a,
-               (const int*)op.ex_b, c_out, c_mirror, accumulate ? 1 : 0, C, counter,
-               (const double*)A.data, (const double*)B.data, ex_out);
-  SPAMM_LAUNCH_CK();
-  dfree(ptasks, s);
-  dfree(bij, s);
-  dfree(unit, s);
-  return true;
-}
-
 template <class Idx>
 void oz32_launch(int64_t n_seg, const int64_t* seg, const Idx* a_idx, const Idx* b_idx,
                  const int64_t* c_out, const int64_t* c_mirror, bool accumulate, const Mat& A,
@@ -1089,9 +593,6 @@ void oz32_launch(int64_t n_seg, const int64_t* seg, const Idx* a_idx, const Idx*
     const char* v = getenv("SPAMM_OZ32_SHAPE");
     return v ? atoi(v) : 3;
   }();
-  if (oz32_pair_launch<Idx>(n_seg, seg, a_idx, b_idx, c_out, c_mirror, accumulate, A, B, op, C, s,
-                            counter, ex_out))
-    return;
   if (shape == 1)
     oz32_launch_cfg<Idx, 2, 4, 3>(n_seg, seg, a_idx, b_idx, c_out, c_mirror, accumulate, A, B,
                                   op, C, s, counter, ex_out);
