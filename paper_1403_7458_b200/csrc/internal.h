@@ -305,8 +305,8 @@ void oz32_operand_passes(const Mat& M, bool trans, int* ex, int8_t* out, cudaStr
 template <class Idx>
 void oz32_launch(int64_t n_seg, const int64_t* seg, const Idx* a_idx, const Idx* b_idx,
                  const int64_t* c_out, const int64_t* c_mirror, bool accumulate, const Mat& A,
-                 const Mat& B, const OzakiOperands& op, double* C, cudaStream_t s, int* counter,
-                 int* ex_out = nullptr);
+                 const Mat& B, const OzakiOperands& op, double* C, cudaStream_t s,
+                 const int32_t* order, int* counter, int* ex_out = nullptr);
 bool ozaki_prepare(const Mat& A, const Mat& B, bool sym_b, cudaStream_t s, OzakiOperands& op,
                    bool try_only, bool defer_tr = false);
 // b_tr of a symmetric operand prepared with defer_tr, once A.slot is built

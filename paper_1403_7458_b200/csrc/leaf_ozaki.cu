@@ -976,14 +976,19 @@ void ozaki_launch(int64_t n_seg, const int64_t* seg, const Idx* a_idx, const Idx
   const int32_t* order = lpt.order;
   int* counter = lpt.counter;
   int* scratch = nullptr;
-  // C blocks are claimed in Morton order: neighbouring CTAs share operand rows
-  // and columns in L2 (measured 28.2 vs 28.9 ms of K4z per cfg4 solve against
-  // the longest-first order, whose tail advantage the short, uniform K4z
-  // blocks do not need).  SPAMM_K4_ORDER=lpt selects the LPT order.
-  static const bool morton = [] {
+  // Nb = 64: C blocks are claimed in Morton order: neighbouring CTAs share
+  // operand rows and columns in L2 (measured 28.2 vs 28.9 ms of K4z per cfg4
+  // solve against the longest-first order, whose tail advantage the short,
+  // uniform K4z blocks do not need).  Nb = 32: longest first -- a launch is
+  // ~9 C blocks per CTA, so the last wave of a Morton-ordered launch (the long
+  // diagonal blocks of the curve's end) leaves ~16 % of the launch to a tail,
+  // and the whole slice set (41 MB at cfg3) sits in L2 whatever the order.
+  // SPAMM_K4_ORDER=lpt / morton selects one order for both.
+  static const int order_mode = [] {
     const char* v = getenv("SPAMM_K4_ORDER");
-    return !(v && strcmp(v, "lpt") == 0);
+    return !v ? 0 : strcmp(v, "lpt") == 0 ? 1 : strcmp(v, "morton") == 0 ? 2 : 0;
   }();
+  const bool morton = order_mode == 2 || (order_mode == 0 && op.nb != 32);
   if (morton) {
     scratch = dmalloc<int>(1, s);
     SPAMM_CK(cudaMemsetAsync(scratch, 0, sizeof(int), s));
@@ -994,7 +999,7 @@ void ozaki_launch(int64_t n_seg, const int64_t* seg, const Idx* a_idx, const Idx
   }
   if (op.nb == 32) {
     oz32_launch<Idx>(n_seg, seg, a_idx, b_idx, c_out, c_mirror, accumulate, A, B, op, C, s,
-                     counter, ex_out);
+                     order, counter, ex_out);
     dfree(scratch, s);
     return;
   }

@@ -555,7 +555,7 @@ template <class Idx, int NBUF, int TPS, int STAGES>
 void oz32_launch_cfg(int64_t n_seg, const int64_t* seg, const Idx* a_idx, const Idx* b_idx,
                      const int64_t* c_out, const int64_t* c_mirror, bool accumulate, const Mat& A,
                      const Mat& B, const OzakiOperands& op, double* C, cudaStream_t s,
-                     int* counter, int* ex_out) {
+                     const int32_t* order, int* counter, int* ex_out) {
   using Cfg = ZCfg<NBUF, TPS, STAGES>;
   auto kern = k_leaf_ozaki32<Idx, NBUF, TPS, STAGES>;
   static std::once_flag once;
@@ -572,8 +572,7 @@ void oz32_launch_cfg(int64_t n_seg, const int64_t* seg, const Idx* a_idx, const 
                (const int32_t*)op.b_tr, (const int64_t*)A.keys, (const int64_t*)B.keys, op.G,
                (const int8_t*)op.as, (const int8_t*)op.bs, (const int*)op.ex_a,
                (const int*)op.ex_b, c_out, c_mirror, accumulate ? 1 : 0, C,
-               (const int32_t*)nullptr, counter, (const double*)A.data, (const double*)B.data,
-               ex_out);
+               order, counter, (const double*)A.data, (const double*)B.data, ex_out);
   SPAMM_LAUNCH_CK();
 }
 
@@ -581,7 +580,7 @@ template <class Idx>
 void oz32_launch(int64_t n_seg, const int64_t* seg, const Idx* a_idx, const Idx* b_idx,
                  const int64_t* c_out, const int64_t* c_mirror, bool accumulate, const Mat& A,
                  const Mat& B, const OzakiOperands& op, double* C, cudaStream_t s,
-                 int* counter, int* ex_out) {
+                 const int32_t* order, int* counter, int* ex_out) {
   // Two CTAs per SM (256 TMEM columns each): the kernel is latency-bound, and
   // a second CTA hides it better than double-buffered accumulators in one
   // (cfg3 K4z 8.0 vs 10.9 ms per solve; 1 task x 4 stages: 9.7 ms).  With the
@@ -595,26 +594,28 @@ void oz32_launch(int64_t n_seg, const int64_t* seg, const Idx* a_idx, const Idx*
   }();
   if (shape == 1)
     oz32_launch_cfg<Idx, 2, 4, 3>(n_seg, seg, a_idx, b_idx, c_out, c_mirror, accumulate, A, B,
-                                  op, C, s, counter, ex_out);
+                                  op, C, s, order, counter, ex_out);
   else if (shape == 3)  // two CTAs per SM, 3 stages of 2 tasks (the 16-KB exchange buffer)
     oz32_launch_cfg<Idx, 1, 2, 3>(n_seg, seg, a_idx, b_idx, c_out, c_mirror, accumulate, A, B,
-                                  op, C, s, counter, ex_out);
+                                  op, C, s, order, counter, ex_out);
   else if (shape == 4)  // two CTAs per SM, 2 stages of 3 tasks
     oz32_launch_cfg<Idx, 1, 3, 2>(n_seg, seg, a_idx, b_idx, c_out, c_mirror, accumulate, A, B,
-                                  op, C, s, counter, ex_out);
+                                  op, C, s, order, counter, ex_out);
   else if (shape == 5)  // two CTAs per SM, 6 stages of 1 task
     oz32_launch_cfg<Idx, 1, 1, 6>(n_seg, seg, a_idx, b_idx, c_out, c_mirror, accumulate, A, B,
-                                  op, C, s, counter, ex_out);
+                                  op, C, s, order, counter, ex_out);
   else
     oz32_launch_cfg<Idx, 1, 2, 2>(n_seg, seg, a_idx, b_idx, c_out, c_mirror, accumulate, A, B,
-                                  op, C, s, counter, ex_out);
+                                  op, C, s, order, counter, ex_out);
 }
 
 template void oz32_launch<int32_t>(int64_t, const int64_t*, const int32_t*, const int32_t*,
                                    const int64_t*, const int64_t*, bool, const Mat&, const Mat&,
-                                   const OzakiOperands&, double*, cudaStream_t, int*, int*);
+                                   const OzakiOperands&, double*, cudaStream_t, const int32_t*,
+                                   int*, int*);
 template void oz32_launch<int64_t>(int64_t, const int64_t*, const int64_t*, const int64_t*,
                                    const int64_t*, const int64_t*, bool, const Mat&, const Mat&,
-                                   const OzakiOperands&, double*, cudaStream_t, int*, int*);
+                                   const OzakiOperands&, double*, cudaStream_t, const int32_t*,
+                                   int*, int*);
 
 }  // namespace spamm
